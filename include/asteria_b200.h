@@ -1,0 +1,311 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * asteria_b200.h — C-ABI of the B200-native Asteria optimizer step.
+ *
+ * This is the drop-in boundary for the reference's optimizer path
+ * (reference: proj/include/asopt/precond.hpp, proj/include/asopt/asyncsched.hpp,
+ * proj/src/config.cpp). Every entry point is `extern "C"`, takes plain pointers
+ * and sizes, never throws, and returns an asg_status. The message of the last
+ * failure on the calling thread is available from asg_last_error().
+ *
+ * Which reference interface each entry point replaces is cited next to it
+ * (path:line relative to the reference's proj/ directory).
+ *
+ * Device memory convention: parameters (theta) and gradients are caller-owned
+ * fp32 device buffers, row-major with an explicit leading dimension. All
+ * optimizer state (factors, roots/bases, SOAP moments, shadow snapshots) is
+ * owned by an asg_blockset and lives in HBM.
+ *
+ * Streams are passed as `void*` (a cudaStream_t) so this header does not pull
+ * in the CUDA runtime headers. NULL means the blockset's own main stream.
+ */
+#ifndef ASTERIA_B200_H
+#define ASTERIA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASG_API_VERSION 1
+
+/* Status codes: 1:1 with the asopt::Error hierarchy (errors.hpp:10-47) that
+ * the optimizer path can raise, plus runtime failures of the GPU layer. */
+typedef enum asg_status {
+    ASG_OK = 0,
+    ASG_ERR_NON_FINITE = 1,          /* NonFiniteError            errors.hpp:16 */
+    ASG_ERR_NO_CONVERGENCE = 2,      /* NoConvergenceError        errors.hpp:17 */
+    ASG_ERR_NOT_PSD = 3,             /* NotPsdError               errors.hpp:18 */
+    ASG_ERR_LAYOUT_MISMATCH = 4,     /* LayoutMismatchError       errors.hpp:19 */
+    ASG_ERR_SHAPE_MISMATCH = 5,      /* ShapeMismatchError        errors.hpp:20 */
+    ASG_ERR_STALE_UNINITIALIZED = 6, /* StaleUninitializedError   errors.hpp:23 */
+    ASG_ERR_WORKER_POOL_DOWN = 7,    /* WorkerPoolDownError       errors.hpp:33 */
+    ASG_ERR_CONFIG_INVALID = 8,      /* ConfigInvalidError        errors.hpp:41 */
+    ASG_ERR_AUDIT = 9,               /* AuditError                errors.hpp:48 */
+    ASG_ERR_MISSING_KEY = 10,        /* MissingKeyError           errors.hpp:27 */
+    ASG_ERR_CUDA = 11,               /* CUDA runtime/driver failure            */
+    ASG_ERR_OUT_OF_MEMORY = 12,      /* device allocation failed               */
+    ASG_ERR_INVALID_ARGUMENT = 13,   /* bad handle / pointer / index           */
+    ASG_ERR_UNSUPPORTED = 14         /* no sm_100a device, or feature absent   */
+} asg_status;
+
+/* Method (precond.hpp:19) extended with KL-Shampoo, which the reference only
+ * names as a plug-in point. */
+typedef enum asg_method {
+    ASG_METHOD_ADAMW = 0,
+    ASG_METHOD_SHAMPOO = 1,
+    ASG_METHOD_SOAP = 2,
+    ASG_METHOD_KL_SHAMPOO = 3
+} asg_method;
+
+/* Accumulation (precond.hpp:20). */
+typedef enum asg_accumulation { ASG_ACCUM_SUM = 0, ASG_ACCUM_EMA = 1 } asg_accumulation;
+
+/* Arithmetic of the tensor-core GEMMs. 3xTF32 (hi/lo split, three tcgen05
+ * kind::tf32 products) is fp32-faithful and is the parity mode. */
+typedef enum asg_precision { ASG_PREC_3XTF32 = 0, ASG_PREC_TF32 = 1 } asg_precision;
+
+/* Tensor roles (tiers.hpp:35-44) plus the KL-Shampoo inverses and the
+ * installed eigenvalues. */
+typedef enum asg_role {
+    ASG_ROLE_FACTOR_L = 0,
+    ASG_ROLE_FACTOR_R = 1,
+    ASG_ROLE_INV_L = 2,     /* Shampoo: L^-1/4; KL-Shampoo: L^-1/2 */
+    ASG_ROLE_INV_R = 3,
+    ASG_ROLE_BASIS_L = 4,   /* SOAP eigenvectors (columns), row-major m x m */
+    ASG_ROLE_BASIS_R = 5,
+    ASG_ROLE_ROTATED_M = 6,
+    ASG_ROLE_ROTATED_V = 7,
+    ASG_ROLE_KL_INV_L = 8,  /* KL-Shampoo: L^-1 */
+    ASG_ROLE_KL_INV_R = 9,
+    ASG_ROLE_EIGVALS_L = 10, /* SOAP installed eigenvalues (ascending) */
+    ASG_ROLE_EIGVALS_R = 11
+} asg_role;
+
+/* OptimizerConfig (precond.hpp:27-44); JSON keys config.cpp:71-80. */
+typedef struct asg_optimizer_config {
+    int32_t method;        /* asg_method */
+    int32_t accumulation;  /* asg_accumulation */
+    double lr;
+    double beta1;
+    double beta2;
+    double eps;
+    double weight_decay;
+    int64_t precondition_frequency; /* pf */
+    double damping;                 /* relative: eps_eff = damping * tr/dim */
+    int64_t block_dim_limit;
+} asg_optimizer_config;
+
+/* Refresh-install policy of the shadow pipeline. */
+typedef enum asg_install_mode {
+    /* Reference semantics: a job dispatched at simulated time T with cost C is
+     * installable at T + C on the blockset's simulated clock
+     * (asyncsched.hpp:7-11, asyncsched.cpp:118-127,268-274). Deterministic. */
+    ASG_INSTALL_SIM_CLOCK = 0,
+    /* Free-running: a job is installable at StepEnd once its side-stream event
+     * has completed. Not bit-reproducible; the bounded-staleness barrier
+     * (asyncsched.cpp:191-221) still applies. */
+    ASG_INSTALL_EVENT = 1
+} asg_install_mode;
+
+/* SchedulerConfig (asyncsched.hpp:50-59); JSON keys config.cpp:81-86. */
+typedef struct asg_scheduler_config {
+    int64_t staleness_S;
+    int64_t pf;
+    int32_t pool_size;     /* accepted for schema compatibility; refresh runs on a side stream */
+    int32_t drain_budget;  /* accepted for schema compatibility (tier staging is out of scope) */
+    double inject_job_delay_steps;
+    double inject_job_delay_jitter_steps;
+    double step_compute_us;
+    double install_cost_us;
+    int32_t install_mode;  /* asg_install_mode */
+    int32_t reserved;
+} asg_scheduler_config;
+
+/* BlockSpec (precond.hpp:47-57). param_index identifies the parameter. */
+typedef struct asg_block_spec {
+    int64_t param_index;
+    int64_t row_begin, row_end;
+    int64_t col_begin, col_end;
+    int64_t block_dim_limit;
+} asg_block_spec;
+
+/* One caller-owned parameter: fp32 device buffers, row-major. */
+typedef struct asg_param_desc {
+    float* theta;
+    const float* grad;
+    int64_t rows, cols;
+    int64_t ld_theta, ld_grad;
+} asg_param_desc;
+
+/* FreshnessRecord (asyncsched.hpp:72-78); -1 encodes "no pending job". */
+typedef struct asg_freshness {
+    uint64_t installed_version;
+    int64_t dispatch_step_of_pending;
+    int64_t last_install_step;
+    int64_t installed_snapshot_step;
+} asg_freshness;
+
+/* PoolStats (asyncsched.hpp:61-70). */
+typedef struct asg_pool_stats {
+    uint64_t dispatched, completed, installed, coalesced, barrier_waits;
+    double wait_total_us;
+    int32_t pending, queue_depth;
+} asg_pool_stats;
+
+/* PrecondBlock bookkeeping (precond.hpp:63-75). */
+typedef struct asg_block_info {
+    asg_block_spec spec;
+    uint64_t version;
+    int64_t last_refresh_step;
+    int64_t moment_steps;
+    int32_t owner_rank;
+    int32_t use_adamw; /* 1-D / degenerate parameter: AdamW fallback (harness.cpp:352) */
+} asg_block_info;
+
+/* Schedule trace event kinds (subset of trace.hpp TraceEventKind). */
+typedef enum asg_event_kind {
+    ASG_EV_DISPATCH = 0,
+    ASG_EV_JOB_START = 1,
+    ASG_EV_JOB_DONE = 2,
+    ASG_EV_INSTALL = 3,
+    ASG_EV_BARRIER_WAIT_BEGIN = 4,
+    ASG_EV_BARRIER_WAIT_END = 5
+} asg_event_kind;
+
+typedef struct asg_event {
+    int64_t step;
+    int32_t kind;   /* asg_event_kind */
+    int32_t reserved;
+    int64_t block;  /* block index within the blockset */
+    uint64_t version;
+    double t_us;
+} asg_event;
+
+typedef struct asg_blockset asg_blockset;
+
+/* ---- library ----------------------------------------------------------- */
+const char* asg_last_error(void);
+int asg_api_version(void);
+/* 1 if a device with compute capability 10.0 is visible, else 0. */
+int asg_device_supported(int device);
+
+/* ---- configuration (precond.cpp:34-62, config.cpp:121-149) -------------- */
+int asg_optimizer_defaults(int32_t method, asg_optimizer_config* out);      /* OptimizerConfig::defaults_for precond.cpp:44-62 */
+int asg_optimizer_validate(const asg_optimizer_config* cfg);                /* OptimizerConfig::validate     precond.cpp:34-42 */
+int asg_scheduler_defaults(asg_scheduler_config* out);                      /* SchedulerConfig{}             asyncsched.hpp:50-59 */
+/* Parses the "optimizer" and "async" sections of a RunConfig JSON document;
+ * other sections are ignored, as read_if ignores unknown keys (config.cpp:12-15).
+ * Method defaults apply before field overrides (config.cpp:126-127);
+ * async.pf defaults to optimizer.precondition_frequency (config.cpp:140) and
+ * must equal it (config.cpp:42-43). Method strings: "AdamW", "Shampoo",
+ * "SOAP", "KL-Shampoo". An optional "gpu" section may set "precision"
+ * ("3xtf32"|"tf32") and "install_mode" ("sim_clock"|"event"). */
+int asg_config_from_json(const char* json, asg_optimizer_config* opt,
+                         asg_scheduler_config* sched, int32_t* precision);
+
+/* ---- blocking (precond.cpp:69-82) --------------------------------------- */
+/* Writes up to `capacity` specs; *count receives the total. */
+int asg_partition_param(int64_t param_index, int64_t rows, int64_t cols, int64_t limit,
+                        asg_block_spec* out, int64_t capacity, int64_t* count);
+
+/* ---- blockset lifecycle ------------------------------------------------- */
+/* Partitions every parameter with cfg->block_dim_limit, creates a
+ * PrecondBlock per block (PrecondBlock::create precond.cpp:84-110) with all
+ * state resident on `device`, and assigns each block one owner rank by LPT
+ * over (world, rank). 1-D parameters (rows==1 or cols==1) use AdamW
+ * (harness.cpp:352). `seed` keys the scheduler's jitter stream
+ * (asyncsched.cpp:248). */
+int asg_blockset_create(int device, const asg_optimizer_config* opt,
+                        const asg_scheduler_config* sched, const asg_param_desc* params,
+                        int64_t n_params, int32_t precision, int32_t rank, int32_t world,
+                        uint64_t seed, asg_blockset** out);
+int asg_blockset_destroy(asg_blockset* bs);
+/* Rebinds theta/grad device pointers (same shapes). */
+int asg_blockset_bind_params(asg_blockset* bs, const asg_param_desc* params, int64_t n_params);
+int asg_blockset_num_blocks(const asg_blockset* bs, int64_t* n);
+int asg_blockset_block_info(const asg_blockset* bs, int64_t idx, asg_block_info* out);
+/* Bytes of optimizer state resident in HBM. */
+int asg_blockset_state_bytes(const asg_blockset* bs, uint64_t* bytes);
+/* The blockset's main stream (cudaStream_t) for callers that want to order
+ * their own work with it. */
+int asg_blockset_stream(const asg_blockset* bs, void** stream);
+
+/* ---- the optimizer step (harness.cpp:439-475 per-block call order) ------ */
+/* Global gradient squared norm over every parameter (feeds clip_scale,
+ * harness.cpp:219-223,435) and a non-finite flag. Synchronizes the stream. */
+int asg_grad_sqnorm(asg_blockset* bs, void* stream, double* sqnorm, int32_t* nonfinite);
+/* accumulate_factors (precond.cpp:173-189) for every owned block on
+ * clip_scale * grad. KL-Shampoo uses the installed inverses. */
+int asg_accumulate(asg_blockset* bs, double clip_scale, void* stream);
+/* ShadowScheduler::maybe_dispatch (asyncsched.cpp:108-142) for every owned
+ * block: snapshot (snapshot_factors precond.cpp:112-117) and launch the
+ * refresh (compute_refresh precond.cpp:129-142) on the low-priority side
+ * stream. */
+int asg_maybe_dispatch(asg_blockset* bs, int64_t step, int64_t* n_dispatched);
+/* ShadowScheduler::staleness_barrier (asyncsched.cpp:191-221). */
+int asg_staleness_barrier(asg_blockset* bs, int64_t step, double* waited_us);
+/* Cold-start rule (harness.cpp:455-466) + precondition_{shampoo,soap}
+ * (precond.cpp:191-223) + apply_update (precond.cpp:244-251), fused, for
+ * every owned block; AdamW (precond.cpp:229-242) for 1-D parameters. */
+int asg_precondition_apply(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale,
+                           void* stream);
+/* on_hook(StepEnd) (asyncsched.cpp:268-286): installs ready refreshes. */
+int asg_step_end(asg_blockset* bs, int64_t step);
+/* accumulate -> maybe_dispatch -> staleness_barrier -> precondition/apply ->
+ * StepEnd, for one step. */
+int asg_step(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale, void* stream);
+/* Advances the simulated clock (SimClock::advance asyncsched.hpp:33-36). */
+int asg_clock_advance(asg_blockset* bs, double us);
+int asg_get_freshness(const asg_blockset* bs, int64_t idx, asg_freshness* out);
+int asg_get_stats(const asg_blockset* bs, asg_pool_stats* out);
+/* Copies up to `capacity` schedule events; *count receives the total. */
+int asg_get_events(const asg_blockset* bs, asg_event* out, int64_t capacity, int64_t* count);
+int asg_synchronize(asg_blockset* bs);
+
+/* ---- per-block entry points (parity tests; host fp64 in/out) ------------ */
+/* These mirror the per-block functions of precond.hpp for one block. */
+int asg_block_read(asg_blockset* bs, int64_t idx, int32_t role, double* out, int64_t count);
+int asg_block_write(asg_blockset* bs, int64_t idx, int32_t role, const double* in, int64_t count);
+int asg_block_set_counters(asg_blockset* bs, int64_t idx, uint64_t version,
+                           int64_t last_refresh_step, int64_t moment_steps);
+/* accumulate_factors(block, g, cfg) precond.cpp:173-189 */
+int asg_block_accumulate_f64(asg_blockset* bs, int64_t idx, const double* g, int64_t ld);
+/* refresh_inverse = install_refresh(compute_refresh(snapshot_factors(b)), step)
+ * precond.cpp:166-171, synchronous. */
+int asg_block_refresh_f64(asg_blockset* bs, int64_t idx, int64_t step);
+/* precondition_shampoo precond.cpp:191-198 (also KL-Shampoo's L^-1/2 G R^-1/2) */
+int asg_block_precondition_f64(asg_blockset* bs, int64_t idx, const double* g, int64_t ld,
+                               double* out);
+/* soap_scaled_step precond.cpp:208-223 (updates rotated moments) */
+int asg_block_soap_step_f64(asg_blockset* bs, int64_t idx, const double* g, int64_t ld,
+                            double* out);
+
+/* ---- multi-GPU: ownership sharding + parameter all-gather ---------------- */
+/* Elements of theta owned by `rank` (owner-major layout). */
+int asg_shard_elems(const asg_blockset* bs, int32_t rank, int64_t* elems);
+/* Packs this rank's owned block slices of theta into `sendbuf` (device). */
+int asg_pack_owned(asg_blockset* bs, float* sendbuf, void* stream);
+/* Scatters an all-gathered owner-major buffer (ranks concatenated, each
+ * padded to `stride_elems`) back into every parameter. */
+int asg_unpack_gathered(asg_blockset* bs, const float* recvbuf, int64_t stride_elems, void* stream);
+
+/* ---- diagnostics: the tensor-core GEMM on its own ----------------------- */
+/* C[b] = alpha * A[b] * B[b]^T + beta * C[b] for b < batch, fp32 device
+ * slabs: A is [batch][M][K], B is [batch][N][K], C is [batch][M][N]
+ * (row-major). M, N multiples of 128, K multiple of 32. Runs the same
+ * tcgen05 kernel the optimizer step uses. */
+int asg_gemm_tn(const float* A, const float* B, float* C, int64_t batch, int64_t M, int64_t N,
+                int64_t K, float alpha, float beta, int32_t precision, void* stream);
+/* Batched symmetric eigendecomposition (the refresh kernel): values
+ * ascending, vectors as columns, fp64 device buffers [batch][n][n]. */
+int asg_sym_eig_batched(const double* A, double* values, double* vectors, int64_t batch, int64_t n,
+                        void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* ASTERIA_B200_H */
