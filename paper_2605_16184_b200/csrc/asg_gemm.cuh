@@ -1,0 +1,372 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Batched "TN" tensor-core GEMM for sm_100a with fused optimizer epilogues.
+//
+//   acc[b] = A[b] * B[b]^T        A: [batch][M][K] fp32, B: [batch][N][K] fp32
+//
+// Both operands are K-major (row-major with K contiguous), staged by TMA into
+// 128B-swizzled shared memory, multiplied by tcgen05.mma kind::tf32 into an
+// fp32 accumulator in TMEM, and drained by four epilogue warps with
+// tcgen05.ld. Precision: NPASS=1 is plain TF32; NPASS=3 is 3xTF32, where every
+// operand is given as an exact (hi, lo) tf32 pair and the kernel accumulates
+// hi*hi + hi*lo + lo*hi — fp32-faithful products (relative error ~2^-21).
+//
+// Persistent: one CTA per SM loops over output tiles (128 x BN). Warp roles:
+//   warp 0: TMA producer      warp 1: MMA issuer + TMEM owner
+//   warps 2-5: epilogue (TMEM lane quadrant = warp % 4)
+// Pipelines: smem stages full/empty (TMA <-> MMA) and a double-buffered TMEM
+// accumulator tfull/tempty (MMA <-> epilogue), so tile t's epilogue overlaps
+// tile t+1's MMAs.
+//
+// Epilogues (the reference op each one fuses is cited):
+//   EPI_STORE    C = alpha*acc + beta*C                        (diagnostics)
+//   EPI_SYM_EMA  C = beta*C + alpha*acc on the lower triangle, mirrored to the
+//                upper (accumulate_factors precond.cpp:181-188 incl. the
+//                symmetrize of densela.hpp:152-156: C stays exactly symmetric)
+//   EPI_SPLIT    D = alpha*acc written as a (hi, lo) tf32 pair (next GEMM's A)
+//   EPI_SPLIT_T  same, transposed (next GEMM's B)
+//   EPI_ADAM     Adam in the rotated basis (soap_scaled_step precond.cpp:213-221):
+//                updates m, v in place, writes S = m^/(sqrt(v^)+eps) as (hi, lo)
+//   EPI_APPLY    theta -= lr*lr_scale*(alpha*acc + wd*theta) on the block's
+//                slice of the caller's parameter (apply_update precond.cpp:244-251)
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "asg_ptx.cuh"
+
+namespace asg {
+
+enum EpiKind { EPI_STORE = 0, EPI_SYM_EMA = 1, EPI_SPLIT = 2, EPI_SPLIT_T = 3, EPI_ADAM = 4, EPI_APPLY = 5 };
+
+struct ApplyEntry {
+    float* theta;   // first element of the block inside the parameter
+    int64_t ld;     // parameter leading dimension
+    int32_t rows;   // block extent (unpadded)
+    int32_t cols;
+};
+
+struct GemmParams {
+    int M, N, K, batch;   // padded per-batch problem
+    int tiles_n;          // N / BN
+    int tiles_per_batch;  // rectangular: (M/128)*(N/BN); symmetric: list length
+    int num_tiles;        // batch * tiles_per_batch
+    const int2* tile_list;  // symmetric schedules: (tile_m, tile_n) per batch-local tile
+    float alpha, beta;
+    float* C;             // EPI_STORE / EPI_SYM_EMA output
+    int64_t ldc, c_bstride;
+    float* Dhi;           // EPI_SPLIT / EPI_SPLIT_T / EPI_ADAM outputs
+    float* Dlo;
+    int64_t ldd, d_bstride;
+    float* mom_m;         // EPI_ADAM moments, [batch][M][N]
+    float* mom_v;
+    int64_t ldm, m_bstride;
+    float b1, b2, inv_bc1, inv_bc2, adam_eps;
+    const ApplyEntry* apply;  // EPI_APPLY: per batch entry
+    float lr_eff, wd;
+    int* flag;            // set to 1 on a non-finite update (EPI_APPLY)
+};
+
+template <int BN, int NPASS>
+struct GemmCfg {
+    static constexpr int BM = 128;
+    static constexpr int BK = 32;  // 32 fp32 = one 128-byte swizzle row
+    static constexpr bool kSplit = NPASS > 1;
+    static constexpr uint32_t kABytes = BM * BK * 4;
+    static constexpr uint32_t kBBytes = BN * BK * 4;
+    static constexpr uint32_t kStageBytes = (kABytes + kBBytes) * (kSplit ? 2 : 1);
+    static constexpr int kStagesRaw = (216 * 1024) / kStageBytes;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
+    static constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + 256;
+    static_assert(kStages >= 2, "need at least two pipeline stages");
+    static_assert(kTmemCols == 256 || kTmemCols == 512, "TMEM allocation must be a power of two");
+};
+
+__device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& b, int& tm, int& tn) {
+    b = t / p.tiles_per_batch;
+    const int l = t - b * p.tiles_per_batch;
+    if (p.tile_list) {
+        const int2 c = p.tile_list[l];
+        tm = c.x;
+        tn = c.y;
+    } else {
+        tm = l / p.tiles_n;
+        tn = l - tm * p.tiles_n;
+    }
+}
+
+// One thread owns one accumulator row (`row`) and 32 consecutive columns.
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int row, int col0,
+                                               const uint32_t (&r)[32]) {
+    if constexpr (EPI == EPI_STORE) {
+        float* c = p.C + int64_t(b) * p.c_bstride + int64_t(row) * p.ldc + col0;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            float4 v;
+            v.x = p.alpha * __uint_as_float(r[j + 0]);
+            v.y = p.alpha * __uint_as_float(r[j + 1]);
+            v.z = p.alpha * __uint_as_float(r[j + 2]);
+            v.w = p.alpha * __uint_as_float(r[j + 3]);
+            if (p.beta != 0.f) {
+                const float4 o = *reinterpret_cast<const float4*>(c + j);
+                v.x += p.beta * o.x;
+                v.y += p.beta * o.y;
+                v.z += p.beta * o.z;
+                v.w += p.beta * o.w;
+            }
+            *reinterpret_cast<float4*>(c + j) = v;
+        }
+    } else if constexpr (EPI == EPI_SYM_EMA) {
+        float* cb = p.C + int64_t(b) * p.c_bstride;
+        if (row < col0) return;  // whole chunk strictly above the diagonal
+        float* crow = cb + int64_t(row) * p.ldc + col0;
+        float vals[32];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            const float4 o = *reinterpret_cast<const float4*>(crow + j);
+            vals[j + 0] = p.beta * o.x + p.alpha * __uint_as_float(r[j + 0]);
+            vals[j + 1] = p.beta * o.y + p.alpha * __uint_as_float(r[j + 1]);
+            vals[j + 2] = p.beta * o.z + p.alpha * __uint_as_float(r[j + 2]);
+            vals[j + 3] = p.beta * o.w + p.alpha * __uint_as_float(r[j + 3]);
+        }
+        if (row >= col0 + 31) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(crow + j) = make_float4(vals[j], vals[j + 1], vals[j + 2], vals[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (row >= col0 + j) crow[j] = vals[j];
+        }
+        // Mirror: C[c][row] for c < row; consecutive lanes hit consecutive rows' column.
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (row > col0 + j) cb[int64_t(col0 + j) * p.ldc + row] = vals[j];
+    } else if constexpr (EPI == EPI_SPLIT) {
+        const int64_t off = int64_t(b) * p.d_bstride + int64_t(row) * p.ldd + col0;
+        float* dh = p.Dhi + off;
+        float* dl = p.Dlo + off;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            float4 h, l;
+            split_tf32(p.alpha * __uint_as_float(r[j + 0]), h.x, l.x);
+            split_tf32(p.alpha * __uint_as_float(r[j + 1]), h.y, l.y);
+            split_tf32(p.alpha * __uint_as_float(r[j + 2]), h.z, l.z);
+            split_tf32(p.alpha * __uint_as_float(r[j + 3]), h.w, l.w);
+            *reinterpret_cast<float4*>(dh + j) = h;
+            *reinterpret_cast<float4*>(dl + j) = l;
+        }
+    } else if constexpr (EPI == EPI_SPLIT_T) {
+        float* dh = p.Dhi + int64_t(b) * p.d_bstride + row;
+        float* dl = p.Dlo + int64_t(b) * p.d_bstride + row;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            float h, l;
+            split_tf32(p.alpha * __uint_as_float(r[j]), h, l);
+            dh[int64_t(col0 + j) * p.ldd] = h;
+            dl[int64_t(col0 + j) * p.ldd] = l;
+        }
+    } else if constexpr (EPI == EPI_ADAM) {
+        const int64_t moff = int64_t(b) * p.m_bstride + int64_t(row) * p.ldm + col0;
+        const int64_t doff = int64_t(b) * p.d_bstride + int64_t(row) * p.ldd + col0;
+        float* mm = p.mom_m + moff;
+        float* vv = p.mom_v + moff;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            float4 m4 = *reinterpret_cast<const float4*>(mm + j);
+            float4 v4 = *reinterpret_cast<const float4*>(vv + j);
+            float* mp = &m4.x;
+            float* vp = &v4.x;
+            float4 h, l;
+            float* hp = &h.x;
+            float* lp = &l.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float g = p.alpha * __uint_as_float(r[j + e]);
+                const float m = p.b1 * mp[e] + (1.f - p.b1) * g;
+                const float v = p.b2 * vp[e] + (1.f - p.b2) * (g * g);
+                mp[e] = m;
+                vp[e] = v;
+                const float s = (m * p.inv_bc1) / (sqrtf(v * p.inv_bc2) + p.adam_eps);
+                split_tf32(s, hp[e], lp[e]);
+            }
+            *reinterpret_cast<float4*>(mm + j) = m4;
+            *reinterpret_cast<float4*>(vv + j) = v4;
+            *reinterpret_cast<float4*>(p.Dhi + doff + j) = h;
+            *reinterpret_cast<float4*>(p.Dlo + doff + j) = l;
+        }
+    } else if constexpr (EPI == EPI_APPLY) {
+        const ApplyEntry e = p.apply[b];
+        if (row >= e.rows) return;
+        float* th = e.theta + int64_t(row) * e.ld;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int c = col0 + j;
+            if (c < e.cols) {
+                const float u = p.alpha * __uint_as_float(r[j]);
+                bad |= !isfinite(u);
+                const float t = th[c];
+                th[c] = t - p.lr_eff * (u + p.wd * t);
+            }
+        }
+        if (bad && p.flag) atomicOr(p.flag, 1);
+    }
+}
+
+template <int BN, int NPASS, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+                   const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
+                   const __grid_constant__ GemmParams p) {
+    using Cfg = GemmCfg<BN, NPASS>;
+    constexpr int BM = Cfg::BM, BK = Cfg::BK, STAGES = Cfg::kStages;
+    constexpr bool SPLIT = Cfg::kSplit;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * Cfg::kStageBytes);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+
+    auto a_hi = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes; };
+    auto a_lo = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes + Cfg::kABytes; };
+    auto b_hi = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes + (SPLIT ? 2 : 1) * Cfg::kABytes; };
+    auto b_lo = [&](int s) {
+        return smem + size_t(s) * Cfg::kStageBytes + 2 * Cfg::kABytes + Cfg::kBBytes;
+    };
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmAh);
+        tma_prefetch(&tmBh);
+        if (SPLIT) {
+            tma_prefetch(&tmAl);
+            tma_prefetch(&tmBl);
+        }
+    }
+    if (warp == 1) {
+        if (lane == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], 1);
+            }
+            for (int a = 0; a < 2; ++a) {
+                mbar_init(&tfull[a], 1);
+                mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+            }
+            fence_mbar_init();
+        }
+        __syncwarp();
+        tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int num_k = p.K / BK;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                int b, tm, tn;
+                decode_tile(p, t, b, tm, tn);
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+                    tma_load_3d(a_hi(stage), &tmAh, &full[stage], kb * BK, tm * BM, b);
+                    tma_load_3d(b_hi(stage), &tmBh, &full[stage], kb * BK, tn * BN, b);
+                    if (SPLIT) {
+                        tma_load_3d(a_lo(stage), &tmAl, &full[stage], kb * BK, tm * BM, b);
+                        tma_load_3d(b_lo(stage), &tmBl, &full[stage], kb * BK, tn * BN, b);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t ah = umma_desc_k_sw128(a_hi(stage));
+                    const uint64_t bh = umma_desc_k_sw128(b_hi(stage));
+                    const uint64_t al = SPLIT ? umma_desc_k_sw128(a_lo(stage)) : 0;
+                    const uint64_t bl = SPLIT ? umma_desc_k_sw128(b_lo(stage)) : 0;
+#pragma unroll
+                    for (int k = 0; k < BK / 8; ++k) {
+                        const uint64_t adv = uint64_t(k * 32) >> 4;  // 8 tf32 = 32 bytes along K
+                        mma_tf32(d, ah + adv, bh + adv, idesc, (kb | k) != 0 ? 1u : 0u);
+                        if (SPLIT) {
+                            mma_tf32(d, ah + adv, bl + adv, idesc, 1u);
+                            mma_tf32(d, al + adv, bh + adv, idesc, 1u);
+                        }
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            int b, tm, tn;
+            decode_tile(p, t, b, tm, tn);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = tm * BM + q * 32 + int(lane);
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32), r);
+                tmem_ld_wait();
+                epilogue_chunk<EPI>(p, b, row, tn * BN + c * 32, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    }
+}
+
+}  // namespace asg

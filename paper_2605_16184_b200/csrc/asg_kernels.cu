@@ -1,0 +1,696 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Device kernels of the optimizer step (all sm_100a) and their launchers.
+//
+//   GEMM          tcgen05 3xTF32/TF32 batched TN GEMM (asg_gemm.cuh), fused epilogues
+//   K1 prep       gradient gather + clip scale + tf32 (hi, lo) split + transpose
+//   K8 snapshot   factor slab -> fp64 shadow (snapshot_factors precond.cpp:112-117)
+//   K6 eigh       batched symmetric eigendecomposition, fp64 (sym_eig densela.hpp:182-264)
+//   K6 roots      (lam + eps)^p reconstruction (inv_root densela.hpp:267-282)
+//   K9 adamw      AdamW + apply for 1-D parameters (precond.cpp:229-251)
+//   K10 sqnorm    global gradient norm + non-finite flag (harness.cpp:219-223)
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <mutex>
+
+#include "../../include/asteria_b200.h"
+#include "asg_kernels.cuh"
+
+namespace asg {
+
+// ============================================================================
+// GEMM launcher
+// ============================================================================
+namespace {
+
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled encode_fn() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+// 3-D map over a [batch][rows][K] fp32 slab with a (32 x box_rows x 1) box,
+// 128-byte swizzle (matches the UMMA K-major SWIZZLE_128B descriptor).
+bool make_map(CUtensorMap* map, const float* base, int K, int rows, int batch, int box_rows) {
+    PFN_encodeTiled enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {cuuint64_t(K), cuuint64_t(rows), cuuint64_t(batch)};
+    cuuint64_t strides[2] = {cuuint64_t(K) * 4, cuuint64_t(K) * cuuint64_t(rows) * 4};
+    cuuint32_t box[3] = {32, cuuint32_t(box_rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, int NPASS, int EPI>
+cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
+                        const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
+    using Cfg = GemmCfg<BN, NPASS>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, NPASS, EPI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(Cfg::kSmemBytes));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+    if (grid <= 0) return cudaSuccess;
+    gemm_tn_kernel<BN, NPASS, EPI><<<grid, 192, Cfg::kSmemBytes, s>>>(ah, al, bh, bl, p);
+    return cudaGetLastError();
+}
+
+template <int BN, int NPASS>
+cudaError_t dispatch_epi(int epi, const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
+                         const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
+    switch (epi) {
+        case EPI_STORE: return launch_inst<BN, NPASS, EPI_STORE>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SYM_EMA: return launch_inst<BN, NPASS, EPI_SYM_EMA>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT: return launch_inst<BN, NPASS, EPI_SPLIT>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT_T: return launch_inst<BN, NPASS, EPI_SPLIT_T>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_ADAM: return launch_inst<BN, NPASS, EPI_ADAM>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_APPLY: return launch_inst<BN, NPASS, EPI_APPLY>(ah, al, bh, bl, p, num_sms, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int gemm_bn_for(int n) { return (n % 256 == 0) ? 256 : 128; }
+
+int gemm_sym_tile_list(int n, int bn, int2* out) {
+    int count = 0;
+    for (int tm = 0; tm < n / 128; ++tm)
+        for (int tn = 0; tn < n / bn; ++tn)
+            if ((tm + 1) * 128 - 1 >= tn * bn) {
+                if (out) out[count] = make_int2(tm, tn);
+                ++count;
+            }
+    return count;
+}
+
+cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStream_t stream) {
+    const int M = g.A.rows, N = g.B.rows, K = g.A.K;
+    if (M % 128 || N % 128 || K % 32 || g.B.K != K) return cudaErrorInvalidValue;
+    const int bn = gemm_bn_for(N);
+    const bool split = precision == ASG_PREC_3XTF32;
+    CUtensorMap ah, al, bh, bl;
+    if (!make_map(&ah, g.A.hi, K, M, g.batch, 128)) return cudaErrorInvalidValue;
+    if (!make_map(&bh, g.B.hi, K, N, g.batch, bn)) return cudaErrorInvalidValue;
+    if (split) {
+        if (!g.A.lo || !g.B.lo) return cudaErrorInvalidValue;
+        if (!make_map(&al, g.A.lo, K, M, g.batch, 128)) return cudaErrorInvalidValue;
+        if (!make_map(&bl, g.B.lo, K, N, g.batch, bn)) return cudaErrorInvalidValue;
+    } else {
+        al = ah;
+        bl = bh;
+    }
+    GemmParams p = g.p;
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.batch = g.batch;
+    p.tiles_n = N / bn;
+    if (g.sym_tiles) {
+        p.tile_list = g.sym_tiles;
+        p.tiles_per_batch = g.sym_tiles_count;
+    } else {
+        p.tile_list = nullptr;
+        p.tiles_per_batch = (M / 128) * (N / bn);
+    }
+    p.num_tiles = p.tiles_per_batch * g.batch;
+    if (bn == 256)
+        return split ? dispatch_epi<256, 3>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                     : dispatch_epi<256, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+    return split ? dispatch_epi<128, 3>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                 : dispatch_epi<128, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+}
+
+// ============================================================================
+// K1: gradient prep
+// ============================================================================
+__global__ void prep_grad_kernel(const BlockRef* __restrict__ blocks, int M, int N,
+                                 const float* __restrict__ scale_dev, float scale_val,
+                                 float* __restrict__ Gh, float* __restrict__ Gl,
+                                 float* __restrict__ GTh, float* __restrict__ GTl) {
+    __shared__ float th[32][33];
+    __shared__ float tl[32][33];
+    const int b = blockIdx.z;
+    const BlockRef blk = blocks[b];
+    const float s = scale_dev ? *scale_dev : scale_val;
+    const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    const int64_t slab = int64_t(M) * N;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int i = i0 + dy, j = j0 + threadIdx.x;
+        float x = 0.f;
+        if (i < blk.rows && j < blk.cols) x = s * blk.src[int64_t(i) * blk.ld + j];
+        float h, l;
+        if (Gl) {
+            split_tf32(x, h, l);
+        } else {
+            h = x;
+            l = 0.f;
+        }
+        Gh[b * slab + int64_t(i) * N + j] = h;
+        if (Gl) Gl[b * slab + int64_t(i) * N + j] = l;
+        th[dy][threadIdx.x] = h;
+        tl[dy][threadIdx.x] = l;
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int jj = j0 + dy, ii = i0 + threadIdx.x;  // GT[jj][ii] = G[ii][jj]
+        GTh[b * slab + int64_t(jj) * M + ii] = th[threadIdx.x][dy];
+        if (GTl) GTl[b * slab + int64_t(jj) * M + ii] = tl[threadIdx.x][dy];
+    }
+}
+
+void launch_prep_grad(const BlockRef* blocks_dev, int nb, int M, int N, const float* scale_dev,
+                      float scale_val, float* Gh, float* Gl, float* GTh, float* GTl, cudaStream_t s) {
+    dim3 grid(N / 32, M / 32, nb), block(32, 8);
+    prep_grad_kernel<<<grid, block, 0, s>>>(blocks_dev, M, N, scale_dev, scale_val, Gh, Gl, GTh, GTl);
+}
+
+__global__ void identity_split_kernel(float* hi, float* lo, int M, int m) {
+    const int64_t b = blockIdx.y;
+    const int64_t slab = int64_t(M) * M;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < slab; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / M), j = int(e % M);
+        hi[b * slab + e] = (i == j && i < m) ? 1.f : 0.f;
+        if (lo) lo[b * slab + e] = 0.f;
+    }
+}
+
+void launch_identity_split(float* hi, float* lo, int nb, int M, int m, cudaStream_t s) {
+    identity_split_kernel<<<dim3(256, nb), 256, 0, s>>>(hi, lo, M, m);
+}
+
+__global__ void identity_f32_kernel(float* a, int M, int m, float diag) {
+    const int64_t b = blockIdx.y;
+    const int64_t slab = int64_t(M) * M;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < slab; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / M), j = int(e % M);
+        a[b * slab + e] = (i == j && i < m) ? diag : 0.f;
+    }
+}
+
+void launch_identity_f32(float* a, int nb, int M, int m, float diag, cudaStream_t s) {
+    identity_f32_kernel<<<dim3(256, nb), 256, 0, s>>>(a, M, m, diag);
+}
+
+// ============================================================================
+// K10: global squared norm + non-finite flag; clip scale
+// ============================================================================
+__global__ void sqnorm_kernel(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                              double* acc, int* flag) {
+    double s = 0.0;
+    bool bad = false;
+    const int64_t n = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const float v = x[(e / cols) * ld + (e % cols)];
+        bad |= !isfinite(v);
+        s += double(v) * double(v);
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+    __shared__ double red[32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = s;
+    __syncthreads();
+    if (w == 0) {
+        s = (l < int(blockDim.x >> 5)) ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+        if (l == 0) atomicAdd(acc, s);
+    }
+    if (bad && flag) atomicOr(flag, 1);
+}
+
+void launch_sqnorm(const float* x, int64_t rows, int64_t cols, int64_t ld, double* acc, int* flag,
+                   cudaStream_t s) {
+    const int64_t n = rows * cols;
+    int grid = int((n + 1023) / 1024);
+    if (grid > 1184) grid = 1184;
+    if (grid < 1) grid = 1;
+    sqnorm_kernel<<<grid, 256, 0, s>>>(x, rows, cols, ld, acc, flag);
+}
+
+__global__ void clip_scale_kernel(const double* sq, double clip, float* out) {
+    const double norm = sqrt(*sq);
+    *out = (norm <= clip || norm == 0.0) ? 1.f : float(clip / norm);
+}
+
+void launch_clip_scale(const double* sqnorm, double clip_norm, float* scale_out, cudaStream_t s) {
+    clip_scale_kernel<<<1, 1, 0, s>>>(sqnorm, clip_norm, scale_out);
+}
+
+// ============================================================================
+// K9: AdamW + apply (1-D parameters)
+// ============================================================================
+__global__ void adamw_apply_kernel(float* __restrict__ theta, int64_t ld_t, const float* __restrict__ grad,
+                                   int64_t ld_g, int64_t rows, int64_t cols, float* __restrict__ m,
+                                   float* __restrict__ v, const float* scale_dev, float scale_val, float b1,
+                                   float b2, float inv_bc1, float inv_bc2, float eps, float lr_eff, float wd,
+                                   int* flag) {
+    const float s = scale_dev ? *scale_dev : scale_val;
+    const int64_t n = rows * cols;
+    bool bad = false;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / cols, c = e % cols;
+        const float g = s * grad[r * ld_g + c];
+        bad |= !isfinite(g);
+        const float mm = b1 * m[e] + (1.f - b1) * g;
+        const float vv = b2 * v[e] + (1.f - b2) * g * g;
+        m[e] = mm;
+        v[e] = vv;
+        const float u = (mm * inv_bc1) / (sqrtf(vv * inv_bc2) + eps);
+        float& t = theta[r * ld_t + c];
+        t = t - lr_eff * (u + wd * t);
+    }
+    if (bad && flag) atomicOr(flag, 1);
+}
+
+void launch_adamw_apply(float* theta, int64_t ld_t, const float* grad, int64_t ld_g, int64_t rows, int64_t cols,
+                        float* m, float* v, const float* scale_dev, float scale_val, float b1, float b2,
+                        float inv_bc1, float inv_bc2, float eps, float lr_eff, float wd, int* flag,
+                        cudaStream_t s) {
+    const int64_t n = rows * cols;
+    int grid = int((n + 255) / 256);
+    if (grid > 1184) grid = 1184;
+    if (grid < 1) grid = 1;
+    adamw_apply_kernel<<<grid, 256, 0, s>>>(theta, ld_t, grad, ld_g, rows, cols, m, v, scale_dev, scale_val, b1,
+                                            b2, inv_bc1, inv_bc2, eps, lr_eff, wd, flag);
+}
+
+// ============================================================================
+// K8: snapshot (fp32 factor slab -> fp64 shadow)
+// ============================================================================
+__global__ void snapshot_kernel(const float* __restrict__ src, int M, int m, double* __restrict__ dst) {
+    const int64_t b = blockIdx.y;
+    const int64_t n = int64_t(m) * m;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / m), j = int(e % m);
+        dst[b * n + e] = double(src[b * int64_t(M) * M + int64_t(i) * M + j]);
+    }
+}
+
+void launch_snapshot(const float* src, int nb, int M, int m, double* dst, cudaStream_t s) {
+    snapshot_kernel<<<dim3(128, nb), 256, 0, s>>>(src, M, m, dst);
+}
+
+// ============================================================================
+// K6: batched symmetric eigendecomposition (fp64)
+//
+// One CTA per matrix; parallel (round-robin tournament) two-sided Jacobi on
+// the matrix held in global memory (L2-resident for the dims this kernel is
+// used at). Same stopping rule as the reference's cyclic Jacobi: off-diagonal
+// Frobenius norm <= 1e-12 * ||A||_F within 30 sweeps (densela.hpp:192-249),
+// values ascending by a stable index-ordered rank (densela.hpp:251-262).
+// ============================================================================
+namespace {
+constexpr int kEigThreads = 512;
+constexpr int kMaxEigN = 4096;
+
+__device__ double block_reduce_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = (l < int(blockDim.x >> 5)) ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+        if (l == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ int tourney(int pos, int r, int P) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (P - 1); }
+}  // namespace
+
+__global__ void __launch_bounds__(kEigThreads) sym_eig_kernel(const double* __restrict__ Ain, double* values,
+                                                              double* vectors, double* work, int n, int* status) {
+    extern __shared__ double sh[];
+    double* cs = sh;                 // [P/2] cosines
+    double* sn = cs + kMaxEigN / 2;  // [P/2] sines
+    __shared__ double red[32];
+    const int64_t b = blockIdx.x;
+    const int64_t nn = int64_t(n) * n;
+    const double* A0 = Ain + b * nn;
+    double* A = work + b * nn;
+    double* V = vectors + b * nn;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    double fro = 0.0;
+    bool bad = false;
+    for (int64_t e = tid; e < nn; e += nt) {
+        const double x = A0[e];
+        bad |= !isfinite(x);
+        A[e] = x;
+        V[e] = (e / n == e % n) ? 1.0 : 0.0;
+        fro += x * x;
+    }
+    const int any_bad = __syncthreads_or(bad);
+    if (any_bad) {
+        if (tid == 0) atomicCAS(&status[b], ASG_OK, ASG_ERR_NON_FINITE);
+        return;
+    }
+    fro = sqrt(block_reduce_sum(fro, red));
+    const double tol = 1e-12 * fro;
+    const int P = n + (n & 1);  // players (a dummy when n is odd)
+    const int half = P / 2;
+
+    auto off_norm = [&]() {
+        double acc = 0.0;
+        for (int64_t e = tid; e < nn; e += nt) {
+            const int i = int(e / n), j = int(e % n);
+            if (j > i) acc += A[e] * A[e];
+        }
+        return sqrt(2.0 * block_reduce_sum(acc, red));
+    };
+
+    bool converged = (n <= 1) || off_norm() <= tol;
+    for (int sweep = 0; sweep < 30 && !converged; ++sweep) {
+        for (int r = 0; r < P - 1; ++r) {
+            // rotation parameters for every pair of this round
+            for (int k = tid; k < half; k += nt) {
+                int p = tourney(k, r, P), q = tourney(P - 1 - k, r, P);
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                double c = 1.0, s = 0.0;
+                if (q < n) {
+                    const double apq = A[int64_t(p) * n + q];
+                    if (apq != 0.0) {
+                        const double app = A[int64_t(p) * n + p], aqq = A[int64_t(q) * n + q];
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau))
+                                                      : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                    }
+                }
+                cs[k] = c;
+                sn[k] = s;
+            }
+            __syncthreads();
+            // rows: A <- J^T A
+            for (int64_t e = tid; e < int64_t(half) * n; e += nt) {
+                const int k = int(e / n), j = int(e % n);
+                const double s = sn[k];
+                if (s == 0.0) continue;
+                int p = tourney(k, r, P), q = tourney(P - 1 - k, r, P);
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                const double c = cs[k];
+                const double x = A[int64_t(p) * n + j], y = A[int64_t(q) * n + j];
+                A[int64_t(p) * n + j] = c * x - s * y;
+                A[int64_t(q) * n + j] = s * x + c * y;
+            }
+            __syncthreads();
+            // columns: A <- A J, V <- V J
+            for (int64_t e = tid; e < int64_t(half) * n; e += nt) {
+                const int k = int(e % half), i = int(e / half);
+                const double s = sn[k];
+                if (s == 0.0) continue;
+                int p = tourney(k, r, P), q = tourney(P - 1 - k, r, P);
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                const double c = cs[k];
+                double x = A[int64_t(i) * n + p], y = A[int64_t(i) * n + q];
+                double np = c * x - s * y, nq = s * x + c * y;
+                if (i == p) nq = 0.0;  // exact zero in the rotated plane
+                if (i == q) np = 0.0;
+                A[int64_t(i) * n + p] = np;
+                A[int64_t(i) * n + q] = nq;
+                x = V[int64_t(i) * n + p];
+                y = V[int64_t(i) * n + q];
+                V[int64_t(i) * n + p] = c * x - s * y;
+                V[int64_t(i) * n + q] = s * x + c * y;
+            }
+            __syncthreads();
+        }
+        converged = off_norm() <= tol;
+    }
+    if (!converged) {
+        if (tid == 0) atomicCAS(&status[b], ASG_OK, ASG_ERR_NO_CONVERGENCE);
+        return;
+    }
+    // ascending stable order by rank; diag -> shared, permuted vectors -> work
+    double* d = sh;  // reuse: n <= kMaxEigN doubles
+    __syncthreads();
+    for (int i = tid; i < n; i += nt) d[i] = A[int64_t(i) * n + i];
+    __syncthreads();
+    for (int i = tid; i < n; i += nt) {
+        const double di = d[i];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            const double dj = d[j];
+            rank += (dj < di) || (dj == di && j < i);
+        }
+        values[b * n + rank] = di;
+        for (int row = 0; row < n; ++row) A[int64_t(row) * n + rank] = V[int64_t(row) * n + i];
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < nn; e += nt) V[e] = A[e];
+}
+
+void launch_sym_eig(const double* A, double* values, double* vectors, double* work, int nb, int n, int* status,
+                    cudaStream_t s) {
+    static bool attr = false;
+    const size_t smem = sizeof(double) * kMaxEigN;
+    if (!attr) {
+        cudaFuncSetAttribute(sym_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    sym_eig_kernel<<<nb, kEigThreads, smem, s>>>(A, values, vectors, work, n, status);
+}
+
+// ============================================================================
+// K6: damping, column scaling (roots), conversions
+// ============================================================================
+__global__ void relative_damping_kernel(const double* A, int n, double damping, double* eps) {
+    __shared__ double red[32];
+    const int64_t b = blockIdx.x;
+    double tr = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) tr += A[b * int64_t(n) * n + int64_t(i) * n + i];
+    tr = block_reduce_sum(tr, red);
+    if (threadIdx.x == 0) eps[b] = n > 0 ? damping * tr / double(n) : 0.0;
+}
+
+void launch_relative_damping(const double* A, int nb, int n, double damping, double* eps, cudaStream_t s) {
+    relative_damping_kernel<<<nb, 256, 0, s>>>(A, n, damping, eps);
+}
+
+__global__ void scale_columns_kernel(const double* V, const double* values, const double* eps, double power,
+                                     int n, double* W, int* status) {
+    const int64_t b = blockIdx.y;
+    const int64_t nn = int64_t(n) * n;
+    const double e = eps ? eps[b] : 0.0;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < nn; idx += int64_t(gridDim.x) * blockDim.x) {
+        const int j = int(idx % n);
+        const double damped = values[b * n + j] + e;
+        if (damped <= 0.0) {
+            atomicCAS(&status[b], ASG_OK, ASG_ERR_NOT_PSD);
+            W[b * nn + idx] = 0.0;
+            continue;
+        }
+        W[b * nn + idx] = V[b * nn + idx] * pow(damped, power);
+    }
+}
+
+void launch_scale_columns(const double* V, const double* values, const double* eps, double power, int nb, int n,
+                          double* W, int* status, cudaStream_t s) {
+    scale_columns_kernel<<<dim3(128, nb), 256, 0, s>>>(V, values, eps, power, n, W, status);
+}
+
+// fp64 tiled batched GEMM on CUDA cores (64 x 64 tiles, 4 x 4 per thread).
+__global__ void dgemm_kernel(bool ta, bool tb, int m, int n, int k, double alpha, const double* __restrict__ A,
+                             int64_t lda, int64_t sa, const double* __restrict__ B, int64_t ldb, int64_t sb,
+                             double beta, double* __restrict__ C, int64_t ldc, int64_t sc) {
+    __shared__ double As[16][65];
+    __shared__ double Bs[16][65];
+    const int64_t bz = blockIdx.z;
+    A += bz * sa;
+    B += bz * sb;
+    C += bz * sc;
+    const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < k; k0 += 16) {
+        for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+            const int kk = e / 64, rr = e % 64;
+            const int gr = row0 + rr, gk = k0 + kk;
+            double a = 0.0;
+            if (gr < m && gk < k) a = ta ? A[int64_t(gk) * lda + gr] : A[int64_t(gr) * lda + gk];
+            As[kk][rr] = a;
+            const int gc = col0 + rr;
+            double bv = 0.0;
+            if (gc < n && gk < k) bv = tb ? B[int64_t(gc) * ldb + gk] : B[int64_t(gk) * ldb + gc];
+            Bs[kk][rr] = bv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            double a[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = row0 + ty * 4 + i, c = col0 + tx * 4 + j;
+            if (r < m && c < n) {
+                double v = alpha * acc[i][j];
+                if (beta != 0.0) v += beta * C[int64_t(r) * ldc + c];
+                C[int64_t(r) * ldc + c] = v;
+            }
+        }
+}
+
+void launch_dgemm(bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int64_t lda, int64_t sa,
+                  const double* B, int64_t ldb, int64_t sb, double beta, double* C, int64_t ldc, int64_t sc, int nb,
+                  cudaStream_t s) {
+    dim3 grid((n + 63) / 64, (m + 63) / 64, nb);
+    dgemm_kernel<<<grid, 256, 0, s>>>(ta, tb, m, n, k, alpha, A, lda, sa, B, ldb, sb, beta, C, ldc, sc);
+}
+
+__global__ void f64_to_split_kernel(const double* __restrict__ src, int n, int M, bool sym, float* hi, float* lo,
+                                    float* hi_t, float* lo_t) {
+    __shared__ float th[32][33];
+    __shared__ float tl[32][33];
+    const int64_t b = blockIdx.z;
+    const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    const int64_t slab = int64_t(M) * M, nn = int64_t(n) * n;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int i = i0 + dy, j = j0 + threadIdx.x;
+        double x = 0.0;
+        if (i < n && j < n) {
+            x = src[b * nn + int64_t(i) * n + j];
+            if (sym) x = 0.5 * (x + src[b * nn + int64_t(j) * n + i]);
+        }
+        const float xf = float(x);
+        float h = xf, l = 0.f;
+        if (lo) {
+            // hi/lo from the fp64 value: hi = tf32(x), lo = tf32(x - hi)
+            h = tf32_round(xf);
+            l = tf32_round(float(x - double(h)));
+        }
+        hi[b * slab + int64_t(i) * M + j] = h;
+        if (lo) lo[b * slab + int64_t(i) * M + j] = l;
+        th[dy][threadIdx.x] = h;
+        tl[dy][threadIdx.x] = l;
+    }
+    if (!hi_t) return;
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int jj = j0 + dy, ii = i0 + threadIdx.x;
+        hi_t[b * slab + int64_t(jj) * M + ii] = th[threadIdx.x][dy];
+        if (lo_t) lo_t[b * slab + int64_t(jj) * M + ii] = tl[threadIdx.x][dy];
+    }
+}
+
+void launch_f64_to_split(const double* src, int nb, int n, int M, bool symmetrize, float* hi, float* lo,
+                         float* hi_t, float* lo_t, cudaStream_t s) {
+    dim3 grid(M / 32, M / 32, nb), block(32, 8);
+    f64_to_split_kernel<<<grid, block, 0, s>>>(src, n, M, symmetrize, hi, lo, hi_t, lo_t);
+}
+
+__global__ void f64_to_f32_kernel(const double* src, int rows, int cols, float* dst, int R, int Cc) {
+    const int64_t b = blockIdx.y;
+    const int64_t tot = int64_t(R) * Cc;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / Cc), j = int(e % Cc);
+        dst[b * tot + e] = (i < rows && j < cols) ? float(src[b * int64_t(rows) * cols + int64_t(i) * cols + j]) : 0.f;
+    }
+}
+
+void launch_f64_to_f32(const double* src, int nb, int rows, int cols, float* dst, int R, int Cc, cudaStream_t s) {
+    f64_to_f32_kernel<<<dim3(128, nb), 256, 0, s>>>(src, rows, cols, dst, R, Cc);
+}
+
+__global__ void f32_to_f64_kernel(const float* src, int rows, int cols, int R, int Cc, double* dst) {
+    const int64_t b = blockIdx.y;
+    const int64_t tot = int64_t(rows) * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / cols), j = int(e % cols);
+        dst[b * tot + e] = double(src[b * int64_t(R) * Cc + int64_t(i) * Cc + j]);
+    }
+}
+
+void launch_f32_to_f64(const float* src, int nb, int rows, int cols, int R, int Cc, double* dst, cudaStream_t s) {
+    f32_to_f64_kernel<<<dim3(128, nb), 256, 0, s>>>(src, rows, cols, R, Cc, dst);
+}
+
+__global__ void square_f64_kernel(const double* a, double* out, int64_t n) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+        out[e] = a[e] * a[e];
+}
+
+void launch_square_f64(const double* a, double* out, int64_t n, cudaStream_t s) {
+    square_f64_kernel<<<256, 256, 0, s>>>(a, out, n);
+}
+
+// ============================================================================
+// Multi-GPU pack / unpack of block slices (owner-major all-gather layout)
+// ============================================================================
+__global__ void pack_kernel(const BlockRef* blocks, const int64_t* offsets, float* out) {
+    const BlockRef blk = blocks[blockIdx.y];
+    const int64_t n = int64_t(blk.rows) * blk.cols;
+    float* o = out + offsets[blockIdx.y];
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+        o[e] = blk.src[(e / blk.cols) * blk.ld + (e % blk.cols)];
+}
+
+__global__ void unpack_kernel(const BlockRef* blocks, const int64_t* offsets, const float* in) {
+    const BlockRef blk = blocks[blockIdx.y];
+    const int64_t n = int64_t(blk.rows) * blk.cols;
+    const float* i = in + offsets[blockIdx.y];
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+        blk.dst[(e / blk.cols) * blk.ld + (e % blk.cols)] = i[e];
+}
+
+void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out, cudaStream_t s) {
+    if (nb > 0) pack_kernel<<<dim3(64, nb), 256, 0, s>>>(blocks_dev, offsets_dev, out);
+}
+
+void launch_unpack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, const float* in,
+                          cudaStream_t s) {
+    if (nb > 0) unpack_kernel<<<dim3(64, nb), 256, 0, s>>>(blocks_dev, offsets_dev, in);
+}
+
+}  // namespace asg

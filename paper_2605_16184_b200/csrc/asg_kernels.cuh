@@ -1,0 +1,105 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host-callable launchers for every device kernel of the optimizer step.
+// Implemented in asg_kernels.cu; used by the runtime (asg_runtime.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "asg_gemm.cuh"
+
+namespace asg {
+
+// A slab operand for the TN GEMM: [batch][rows][K] fp32 pair (lo may be null
+// in TF32 mode).
+struct Operand {
+    const float* hi;
+    const float* lo;
+    int rows;
+    int K;
+};
+
+struct GemmLaunch {
+    Operand A, B;
+    int batch;
+    int epi;                 // EpiKind
+    GemmParams p;            // epilogue fields; shape/tile fields are filled by the launcher
+    const int2* sym_tiles;   // non-null: symmetric (lower-triangle) schedule
+    int sym_tiles_count;
+};
+
+// Picks the output tile width for an output with `n` columns (multiple of 128).
+int gemm_bn_for(int n);
+// Builds the lower-triangle tile list for an n x n symmetric output with
+// 128 x BN tiles. Returns the count; `out` may be null to query.
+int gemm_sym_tile_list(int n, int bn, int2* out);
+cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStream_t stream);
+
+// Block descriptors for the gather/scatter kernels.
+struct BlockRef {
+    const float* src;   // first element of the block in the caller's tensor
+    float* dst;         // (scatter targets)
+    int64_t ld;
+    int32_t rows, cols;
+};
+
+// G (caller layout, scaled by *scale or scale_val) -> padded slabs
+// Gh/Gl [b][M][N] and GTh/GTl [b][N][M] (tf32 hi/lo; lo null => TF32 mode).
+void launch_prep_grad(const BlockRef* blocks_dev, int nb, int M, int N, const float* scale_dev,
+                      float scale_val, float* Gh, float* Gl, float* GTh, float* GTl,
+                      cudaStream_t s);
+// Fills [nb][M][M] slabs with the padded identity (hi = I, lo = 0).
+void launch_identity_split(float* hi, float* lo, int nb, int M, int m, cudaStream_t s);
+// Fills [nb][M][M] fp32 with identity on the leading m x m (KL start) or zero.
+void launch_identity_f32(float* a, int nb, int M, int m, float diag, cudaStream_t s);
+// Sum of squares of a strided 2-D fp32 tensor into *acc (double), and
+// non-finite flag.
+void launch_sqnorm(const float* x, int64_t rows, int64_t cols, int64_t ld, double* acc, int* flag,
+                   cudaStream_t s);
+// clip scale from the accumulated squared norm (harness.cpp:219-223).
+void launch_clip_scale(const double* sqnorm, double clip_norm, float* scale_out, cudaStream_t s);
+// AdamW + apply for a 1-D/degenerate parameter (precond.cpp:229-251).
+void launch_adamw_apply(float* theta, int64_t ld_t, const float* grad, int64_t ld_g, int64_t rows,
+                        int64_t cols, float* m, float* v, const float* scale_dev, float scale_val,
+                        float b1, float b2, float inv_bc1, float inv_bc2, float eps, float lr_eff,
+                        float wd, int* flag, cudaStream_t s);
+
+// Refresh path (fp64).
+// Snapshot: [b][M][M] fp32 slab's leading m x m -> [b][m][m] fp64 (+ trace).
+void launch_snapshot(const float* src, int nb, int M, int m, double* dst, cudaStream_t s);
+// Batched symmetric eigendecomposition (values ascending, vectors as columns).
+// `work` must hold nb*n*n doubles. `status` receives per-matrix codes.
+void launch_sym_eig(const double* A, double* values, double* vectors, double* work, int nb, int n,
+                    int* status, cudaStream_t s);
+// eps[b] = damping * tr(A_b) / n  (relative_damping precond.cpp:121-125).
+void launch_relative_damping(const double* A, int nb, int n, double damping, double* eps,
+                             cudaStream_t s);
+// W[b][i][j] = V[b][i][j] * (values[b][j] + eps[b])^power; sets status[b] to
+// ASG_ERR_NOT_PSD if a damped eigenvalue is <= 0 (densela.hpp:274-278).
+void launch_scale_columns(const double* V, const double* values, const double* eps, double power,
+                          int nb, int n, double* W, int* status, cudaStream_t s);
+// C[b] = alpha * op(A[b]) * op(B[b]) + beta*C[b], fp64 (CUDA cores).
+void launch_dgemm(bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int64_t lda,
+                  int64_t sa, const double* B, int64_t ldb, int64_t sb, double beta, double* C,
+                  int64_t ldc, int64_t sc, int nb, cudaStream_t s);
+// fp64 [b][n][n] (optionally symmetrized) -> padded fp32 hi/lo slabs [b][M][M]
+// (and transposed copies if *_t non-null).
+void launch_f64_to_split(const double* src, int nb, int n, int M, bool symmetrize, float* hi,
+                         float* lo, float* hi_t, float* lo_t, cudaStream_t s);
+// fp64 [b][rows][cols] <-> padded fp32 [b][R][C] slab.
+void launch_f64_to_f32(const double* src, int nb, int rows, int cols, float* dst, int R, int Cc,
+                       cudaStream_t s);
+void launch_f32_to_f64(const float* src, int nb, int rows, int cols, int R, int Cc, double* dst,
+                       cudaStream_t s);
+
+void launch_square_f64(const double* a, double* out, int64_t n, cudaStream_t s);
+
+// Multi-GPU: pack owned block slices into a contiguous buffer and back.
+void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out,
+                        cudaStream_t s);
+void launch_unpack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb,
+                          const float* in, cudaStream_t s);
+
+}  // namespace asg

@@ -1,0 +1,1768 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host runtime of the B200 Asteria optimizer step, behind the C-ABI of
+// include/asteria_b200.h.
+//
+// A blockset holds the second-order state of every parameter block this rank
+// owns, grouped by block shape into contiguous HBM slabs ([block][rows][cols])
+// so that each GEMM of the step is ONE batched tcgen05 launch per shape group:
+//
+//   Shampoo     stats: L = b L + a G G^T, R = b R + a G^T G  (2 sym GEMMs)
+//               update: Y = P_L G ; theta -= lr (Y P_R + wd theta)  (2 GEMMs)
+//   SOAP        stats as Shampoo (EMA)
+//               T = Q_L^T G ; Adam(T Q_R) -> S ; W^T = (S Q_R^T)^T ;
+//               theta -= lr (Q_L W + wd theta)                     (4 GEMMs)
+//   KL-Shampoo  X = G R^-1 ; L = b L + a/n X G^T ; Z^T = G^T L^-1 ;
+//               R = b R + a/m G^T Z ; update as Shampoo with P = F^-1/2 (6 GEMMs)
+//
+// The refresh (snapshot -> fp64 eigh -> roots / bases) runs on a low-priority
+// side stream under the reference's bounded-staleness rules
+// (asyncsched.cpp:108-221,268-286), emulated exactly on a simulated clock
+// (ASG_INSTALL_SIM_CLOCK) or driven by stream events (ASG_INSTALL_EVENT).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/asteria_b200.h"
+#include "asg_json.hpp"
+#include "asg_kernels.cuh"
+
+namespace asg {
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+#define CK(x)                                                                                 \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess)                                                                \
+            throw Fail{e_ == cudaErrorMemoryAllocation ? ASG_ERR_OUT_OF_MEMORY : ASG_ERR_CUDA, \
+                       std::string(#x) + ": " + cudaGetErrorString(e_)};                      \
+    } while (0)
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return ASG_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return ASG_ERR_INVALID_ARGUMENT;
+    }
+}
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// configuration (precond.cpp:34-62, config.cpp:121-149)
+// ---------------------------------------------------------------------------
+asg_optimizer_config defaults_for(int method) {
+    asg_optimizer_config c{};
+    c.method = method;
+    c.lr = 1e-3;
+    c.beta1 = 0.9;
+    c.beta2 = 0.95;
+    c.eps = 1e-8;
+    c.weight_decay = 0.0;
+    c.precondition_frequency = 10;
+    c.accumulation = ASG_ACCUM_SUM;
+    c.damping = 1e-8;
+    c.block_dim_limit = 2048;
+    switch (method) {
+        case ASG_METHOD_ADAMW: c.beta2 = 0.999; break;
+        case ASG_METHOD_SHAMPOO: break;
+        case ASG_METHOD_SOAP:
+        case ASG_METHOD_KL_SHAMPOO: c.accumulation = ASG_ACCUM_EMA; break;
+        default: throw Fail{ASG_ERR_CONFIG_INVALID, "unknown optimizer method"};
+    }
+    return c;
+}
+
+void validate(const asg_optimizer_config& c) {
+    if (c.method < ASG_METHOD_ADAMW || c.method > ASG_METHOD_KL_SHAMPOO)
+        throw Fail{ASG_ERR_CONFIG_INVALID, "unknown optimizer method"};
+    if (c.accumulation != ASG_ACCUM_SUM && c.accumulation != ASG_ACCUM_EMA)
+        throw Fail{ASG_ERR_CONFIG_INVALID, "unknown accumulation mode"};
+    if (c.precondition_frequency < 1) throw Fail{ASG_ERR_CONFIG_INVALID, "precondition_frequency must be >= 1"};
+    if (c.beta1 < 0.0 || c.beta1 >= 1.0 || c.beta2 < 0.0 || c.beta2 >= 1.0)
+        throw Fail{ASG_ERR_CONFIG_INVALID, "betas must lie in [0, 1)"};
+    if (c.lr < 0.0 || c.eps <= 0.0 || c.damping < 0.0 || c.weight_decay < 0.0)
+        throw Fail{ASG_ERR_CONFIG_INVALID, "lr/eps/damping/weight_decay out of range"};
+    if (c.block_dim_limit < 1) throw Fail{ASG_ERR_CONFIG_INVALID, "block_dim_limit must be >= 1"};
+}
+
+asg_scheduler_config sched_defaults() {
+    asg_scheduler_config s{};
+    s.staleness_S = 5;
+    s.pf = 10;
+    s.pool_size = 0;
+    s.drain_budget = 4;
+    s.inject_job_delay_steps = 0.0;
+    s.inject_job_delay_jitter_steps = 0.0;
+    s.step_compute_us = 1000.0;
+    s.install_cost_us = 0.0;
+    s.install_mode = ASG_INSTALL_SIM_CLOCK;
+    return s;
+}
+
+int method_from_string(const std::string& s) {
+    if (s == "AdamW") return ASG_METHOD_ADAMW;
+    if (s == "Shampoo") return ASG_METHOD_SHAMPOO;
+    if (s == "SOAP") return ASG_METHOD_SOAP;
+    if (s == "KL-Shampoo") return ASG_METHOD_KL_SHAMPOO;
+    throw Fail{ASG_ERR_CONFIG_INVALID, "unknown optimizer method: " + s};
+}
+
+// ---------------------------------------------------------------------------
+// blockset state
+// ---------------------------------------------------------------------------
+struct Unit {
+    asg_block_spec spec{};
+    bool adamw = false;
+    int owner = 0;
+    int group = -1, slot = -1;
+    uint64_t version = 0;
+    int64_t last_refresh_step = -1;
+    int64_t moment_steps = 0;
+    // shadow scheduler
+    bool pending = false;
+    int64_t dispatch_step = 0;
+    double dispatch_sim = 0.0, completion_sim = 0.0;
+    bool launched = false;  // refresh enqueued on the side stream
+    cudaEvent_t done = nullptr;
+    bool has_fresh = false;
+    asg_freshness fresh{0, -1, -1, -1};
+    // AdamW state (1-D parameters)
+    float *am = nullptr, *av = nullptr;
+    int64_t adam_t = 0;
+    double cost = 0.0;
+};
+
+struct Group {
+    int m = 0, n = 0, M = 0, N = 0, nb = 0;
+    std::vector<int> units;
+    float *L = nullptr, *R = nullptr, *snapL = nullptr, *snapR = nullptr;
+    float *Gh = nullptr, *Gl = nullptr, *GTh = nullptr, *GTl = nullptr;
+    float *Th = nullptr, *Tl = nullptr, *Sh = nullptr, *Sl = nullptr;
+    // Shampoo: P = F^-1/4 ; KL: P = F^-1/2 and K = F^-1 (active + shadow)
+    float *PLh = nullptr, *PLl = nullptr, *PRh = nullptr, *PRl = nullptr;
+    float *sPLh = nullptr, *sPLl = nullptr, *sPRh = nullptr, *sPRl = nullptr;
+    float *KLh = nullptr, *KLl = nullptr, *KRh = nullptr, *KRl = nullptr;
+    float *sKLh = nullptr, *sKLl = nullptr, *sKRh = nullptr, *sKRl = nullptr;
+    // SOAP
+    float *QLh = nullptr, *QLl = nullptr, *QLTh = nullptr, *QLTl = nullptr;
+    float *QRh = nullptr, *QRl = nullptr, *QRTh = nullptr, *QRTl = nullptr;
+    float *mom_m = nullptr, *mom_v = nullptr;
+    double *QL64 = nullptr, *QR64 = nullptr, *valsL = nullptr, *valsR = nullptr;
+    double *sQL64 = nullptr, *sQR64 = nullptr, *svalsL = nullptr, *svalsR = nullptr;
+    BlockRef* d_refs = nullptr;
+    ApplyEntry* d_apply = nullptr;
+    int2 *tilesM = nullptr, *tilesN = nullptr;
+    int ntM = 0, ntN = 0;
+    int* d_status = nullptr;
+    int* h_status = nullptr;  // pinned
+};
+
+}  // namespace
+}  // namespace asg
+
+struct asg_blockset {
+    int device = 0;
+    int num_sms = 148;
+    asg_optimizer_config opt{};
+    asg_scheduler_config sc{};
+    int precision = ASG_PREC_3XTF32;
+    int rank = 0, world = 1;
+    std::vector<asg_param_desc> params;
+    std::vector<asg::Unit> units;
+    std::vector<asg::Group> groups;
+    std::vector<void*> allocs;
+    std::vector<void*> host_allocs;
+    cudaStream_t main = nullptr, side = nullptr;
+    bool own_main = false;
+    cudaEvent_t ev_snap = nullptr;
+    // scheduler
+    double now_us = 0.0;
+    std::mt19937_64 jitter;
+    asg_pool_stats stats{};
+    std::vector<asg_event> events;
+    // refresh workspace (fp64), sized for a chunk of blocks of dim <= ws_n
+    int ws_chunk = 0, ws_n = 0;
+    double *ws_snap = nullptr, *ws_vecs = nullptr, *ws_work = nullptr, *ws_W = nullptr, *ws_out = nullptr,
+           *ws_vals = nullptr, *ws_eps = nullptr;
+    // SOAP install workspace (one block)
+    double *iw_rotL = nullptr, *iw_rotR = nullptr, *iw_sq = nullptr, *iw_a = nullptr, *iw_b = nullptr;
+    // scalars
+    int* d_flag = nullptr;
+    double* d_sqnorm = nullptr;
+    float* d_scale = nullptr;
+    // parity staging
+    float* stage = nullptr;
+    size_t stage_elems = 0;
+    asg::BlockRef* d_ref1 = nullptr;
+    asg::ApplyEntry* d_apply1 = nullptr;
+    float* d_out1 = nullptr;
+    // multi-GPU pack layout
+    asg::BlockRef* d_pack_refs = nullptr;
+    int64_t* d_pack_offs = nullptr;
+    int n_pack = 0;
+    std::vector<int64_t> shard_elems;
+    asg::BlockRef* d_unpack_refs = nullptr;
+    int64_t* d_unpack_offs = nullptr;
+    int n_unpack = 0;
+    std::vector<int> unpack_rank;
+};
+
+namespace asg {
+namespace {
+
+template <class T>
+T* dalloc(asg_blockset* bs, size_t count) {
+    if (count == 0) return nullptr;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    bs->allocs.push_back(p);
+    return static_cast<T*>(p);
+}
+
+template <class T>
+T* halloc(asg_blockset* bs, size_t count) {
+    void* p = nullptr;
+    CK(cudaMallocHost(&p, std::max<size_t>(1, count) * sizeof(T)));
+    bs->host_allocs.push_back(p);
+    std::memset(p, 0, std::max<size_t>(1, count) * sizeof(T));
+    return static_cast<T*>(p);
+}
+
+// H2D upload ordered on `s` and complete on return (a pageable cudaMemcpy may
+// return before its DMA lands, and our streams do not sync with the legacy one).
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+bool is_precond(const asg_blockset* bs) { return bs->opt.method != ASG_METHOD_ADAMW; }
+bool is_soap(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_SOAP; }
+bool is_kl(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_KL_SHAMPOO; }
+bool split_mode(const asg_blockset* bs) { return bs->precision == ASG_PREC_3XTF32; }
+
+void emit(asg_blockset* bs, int64_t step, int kind, int64_t block, uint64_t version, double t) {
+    asg_event e{};
+    e.step = step;
+    e.kind = kind;
+    e.block = block;
+    e.version = version;
+    e.t_us = t;
+    bs->events.push_back(e);
+}
+
+size_t slabMM(const Group& g) { return size_t(g.M) * g.M; }
+size_t slabNN(const Group& g) { return size_t(g.N) * g.N; }
+size_t slabMN(const Group& g) { return size_t(g.M) * g.N; }
+
+// ---------------------------------------------------------------------------
+// construction
+// ---------------------------------------------------------------------------
+void build_units(asg_blockset* bs) {
+    for (int64_t p = 0; p < int64_t(bs->params.size()); ++p) {
+        const asg_param_desc& d = bs->params[size_t(p)];
+        if (d.rows < 1 || d.cols < 1) throw Fail{ASG_ERR_SHAPE_MISMATCH, "partition_param: empty parameter"};
+        const bool adamw = !is_precond(bs) || d.rows == 1 || d.cols == 1;  // harness.cpp:352
+        if (adamw) {
+            Unit u;
+            u.spec = {p, 0, d.rows, 0, d.cols, bs->opt.block_dim_limit};
+            u.adamw = true;
+            u.cost = 28.0 * double(d.rows * d.cols) / 400.0;  // bytes -> flop-equivalent at ~400 flop/B
+            bs->units.push_back(u);
+            continue;
+        }
+        const int64_t limit = bs->opt.block_dim_limit;
+        for (int64_t r = 0; r < d.rows; r += limit)  // partition_param precond.cpp:69-82
+            for (int64_t c = 0; c < d.cols; c += limit) {
+                Unit u;
+                u.spec = {p, r, std::min(d.rows, r + limit), c, std::min(d.cols, c + limit), limit};
+                const double m = double(u.spec.row_end - r), n = double(u.spec.col_end - c);
+                const double step_w = (is_soap(bs) ? 5.0 : is_kl(bs) ? 5.0 : 3.0) * m * n * (m + n);
+                const double refresh_w = 9.0 * (m * m * m + n * n * n);
+                u.cost = step_w + refresh_w / double(bs->opt.precondition_frequency);
+                bs->units.push_back(u);
+            }
+    }
+    // LPT ownership: heaviest first onto the least-loaded rank.
+    std::vector<int> order(bs->units.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return bs->units[size_t(a)].cost > bs->units[size_t(b)].cost; });
+    std::vector<double> load(size_t(bs->world), 0.0);
+    for (int i : order) {
+        int best = 0;
+        for (int r = 1; r < bs->world; ++r)
+            if (load[size_t(r)] < load[size_t(best)]) best = r;
+        bs->units[size_t(i)].owner = best;
+        load[size_t(best)] += bs->units[size_t(i)].cost;
+    }
+}
+
+void build_groups(asg_blockset* bs) {
+    std::map<std::pair<int, int>, int> by_shape;
+    for (size_t i = 0; i < bs->units.size(); ++i) {
+        Unit& u = bs->units[i];
+        if (u.adamw || u.owner != bs->rank) continue;
+        const int m = int(u.spec.row_end - u.spec.row_begin), n = int(u.spec.col_end - u.spec.col_begin);
+        auto key = std::make_pair(m, n);
+        auto it = by_shape.find(key);
+        if (it == by_shape.end()) {
+            Group g;
+            g.m = m;
+            g.n = n;
+            g.M = int(round_up(m, 128));
+            g.N = int(round_up(n, 128));
+            it = by_shape.emplace(key, int(bs->groups.size())).first;
+            bs->groups.push_back(g);
+        }
+        Group& g = bs->groups[size_t(it->second)];
+        u.group = it->second;
+        u.slot = int(g.units.size());
+        g.units.push_back(int(i));
+    }
+}
+
+void bind_group_tables(asg_blockset* bs, Group& g) {
+    std::vector<BlockRef> refs(size_t(g.nb));
+    std::vector<ApplyEntry> app(size_t(g.nb));
+    for (int s = 0; s < g.nb; ++s) {
+        const Unit& u = bs->units[size_t(g.units[size_t(s)])];
+        const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+        refs[size_t(s)].src = d.grad ? d.grad + u.spec.row_begin * d.ld_grad + u.spec.col_begin : nullptr;
+        refs[size_t(s)].dst = nullptr;
+        refs[size_t(s)].ld = d.ld_grad;
+        refs[size_t(s)].rows = g.m;
+        refs[size_t(s)].cols = g.n;
+        app[size_t(s)].theta = d.theta ? d.theta + u.spec.row_begin * d.ld_theta + u.spec.col_begin : nullptr;
+        app[size_t(s)].ld = d.ld_theta;
+        app[size_t(s)].rows = g.m;
+        app[size_t(s)].cols = g.n;
+    }
+    h2d(g.d_refs, refs.data(), refs.size() * sizeof(BlockRef), bs->main);
+    h2d(g.d_apply, app.data(), app.size() * sizeof(ApplyEntry), bs->main);
+}
+
+void alloc_group(asg_blockset* bs, Group& g) {
+    const bool sp = split_mode(bs);
+    g.nb = int(g.units.size());
+    const size_t nb = size_t(g.nb);
+    g.L = dalloc<float>(bs, nb * slabMM(g));
+    g.R = dalloc<float>(bs, nb * slabNN(g));
+    g.snapL = dalloc<float>(bs, nb * slabMM(g));
+    g.snapR = dalloc<float>(bs, nb * slabNN(g));
+    g.Gh = dalloc<float>(bs, nb * slabMN(g));
+    g.GTh = dalloc<float>(bs, nb * slabMN(g));
+    g.Th = dalloc<float>(bs, nb * slabMN(g));
+    g.Sh = dalloc<float>(bs, nb * slabMN(g));
+    if (sp) {
+        g.Gl = dalloc<float>(bs, nb * slabMN(g));
+        g.GTl = dalloc<float>(bs, nb * slabMN(g));
+        g.Tl = dalloc<float>(bs, nb * slabMN(g));
+        g.Sl = dalloc<float>(bs, nb * slabMN(g));
+    }
+    auto pair_mm = [&](float*& h, float*& l) {
+        h = dalloc<float>(bs, nb * slabMM(g));
+        if (sp) l = dalloc<float>(bs, nb * slabMM(g));
+    };
+    auto pair_nn = [&](float*& h, float*& l) {
+        h = dalloc<float>(bs, nb * slabNN(g));
+        if (sp) l = dalloc<float>(bs, nb * slabNN(g));
+    };
+    cudaStream_t s = bs->main;
+    if (is_soap(bs)) {
+        pair_mm(g.QLh, g.QLl);
+        pair_mm(g.QLTh, g.QLTl);
+        pair_nn(g.QRh, g.QRl);
+        pair_nn(g.QRTh, g.QRTl);
+        g.mom_m = dalloc<float>(bs, nb * slabMN(g));
+        g.mom_v = dalloc<float>(bs, nb * slabMN(g));
+        g.QL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
+        g.QR64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
+        g.sQL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
+        g.sQR64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
+        g.valsL = dalloc<double>(bs, nb * size_t(g.m));
+        g.valsR = dalloc<double>(bs, nb * size_t(g.n));
+        g.svalsL = dalloc<double>(bs, nb * size_t(g.m));
+        g.svalsR = dalloc<double>(bs, nb * size_t(g.n));
+        launch_identity_split(g.QLh, g.QLl, g.nb, g.M, g.m, s);
+        launch_identity_split(g.QLTh, g.QLTl, g.nb, g.M, g.m, s);
+        launch_identity_split(g.QRh, g.QRl, g.nb, g.N, g.n, s);
+        launch_identity_split(g.QRTh, g.QRTl, g.nb, g.N, g.n, s);
+        // fp64 identity bases, eigenvalues 1 (EigenPair::identity densela.hpp:119-121)
+        std::vector<double> eyeL(size_t(g.m) * g.m, 0.0), eyeR(size_t(g.n) * g.n, 0.0);
+        for (int i = 0; i < g.m; ++i) eyeL[size_t(i) * g.m + i] = 1.0;
+        for (int i = 0; i < g.n; ++i) eyeR[size_t(i) * g.n + i] = 1.0;
+        std::vector<double> onesL(size_t(g.m), 1.0), onesR(size_t(g.n), 1.0);
+        for (size_t b = 0; b < nb; ++b) {
+            h2d(g.QL64 + b * g.m * g.m, eyeL.data(), eyeL.size() * 8, bs->main);
+            h2d(g.QR64 + b * g.n * g.n, eyeR.data(), eyeR.size() * 8, bs->main);
+            h2d(g.valsL + b * g.m, onesL.data(), onesL.size() * 8, bs->main);
+            h2d(g.valsR + b * g.n, onesR.data(), onesR.size() * 8, bs->main);
+        }
+        CK(cudaMemsetAsync(g.mom_m, 0, nb * slabMN(g) * 4, s));
+        CK(cudaMemsetAsync(g.mom_v, 0, nb * slabMN(g) * 4, s));
+    } else {
+        pair_mm(g.PLh, g.PLl);
+        pair_nn(g.PRh, g.PRl);
+        pair_mm(g.sPLh, g.sPLl);
+        pair_nn(g.sPRh, g.sPRl);
+        launch_identity_split(g.PLh, g.PLl, g.nb, g.M, g.m, s);
+        launch_identity_split(g.PRh, g.PRl, g.nb, g.N, g.n, s);
+        if (is_kl(bs)) {
+            pair_mm(g.KLh, g.KLl);
+            pair_nn(g.KRh, g.KRl);
+            pair_mm(g.sKLh, g.sKLl);
+            pair_nn(g.sKRh, g.sKRl);
+            launch_identity_split(g.KLh, g.KLl, g.nb, g.M, g.m, s);
+            launch_identity_split(g.KRh, g.KRl, g.nb, g.N, g.n, s);
+        }
+    }
+    // statistics: zero (precond.cpp:89-90); KL-Shampoo starts from identity
+    launch_identity_f32(g.L, g.nb, g.M, g.m, is_kl(bs) ? 1.f : 0.f, s);
+    launch_identity_f32(g.R, g.nb, g.N, g.n, is_kl(bs) ? 1.f : 0.f, s);
+    CK(cudaMemsetAsync(g.Gh, 0, nb * slabMN(g) * 4, s));
+    CK(cudaMemsetAsync(g.GTh, 0, nb * slabMN(g) * 4, s));
+    if (sp) {
+        CK(cudaMemsetAsync(g.Gl, 0, nb * slabMN(g) * 4, s));
+        CK(cudaMemsetAsync(g.GTl, 0, nb * slabMN(g) * 4, s));
+    }
+    g.d_refs = dalloc<BlockRef>(bs, nb);
+    g.d_apply = dalloc<ApplyEntry>(bs, nb);
+    g.d_status = dalloc<int>(bs, nb);
+    g.h_status = halloc<int>(bs, nb);
+    CK(cudaMemsetAsync(g.d_status, 0, nb * sizeof(int), s));
+    const int bnM = gemm_bn_for(g.M), bnN = gemm_bn_for(g.N);
+    g.ntM = gemm_sym_tile_list(g.M, bnM, nullptr);
+    g.ntN = gemm_sym_tile_list(g.N, bnN, nullptr);
+    std::vector<int2> tl(size_t(std::max(g.ntM, g.ntN)));
+    g.tilesM = dalloc<int2>(bs, size_t(g.ntM));
+    gemm_sym_tile_list(g.M, bnM, tl.data());
+    h2d(g.tilesM, tl.data(), size_t(g.ntM) * sizeof(int2), bs->main);
+    g.tilesN = dalloc<int2>(bs, size_t(g.ntN));
+    gemm_sym_tile_list(g.N, bnN, tl.data());
+    h2d(g.tilesN, tl.data(), size_t(g.ntN) * sizeof(int2), bs->main);
+    bind_group_tables(bs, g);
+}
+
+void alloc_workspace(asg_blockset* bs) {
+    int nmax = 0;
+    size_t state_per_block = 0;
+    for (const Group& g : bs->groups) {
+        nmax = std::max({nmax, g.m, g.n});
+        state_per_block = std::max(state_per_block, size_t(g.m) * g.m + size_t(g.n) * g.n);
+    }
+    if (nmax == 0) return;
+    // Chunk the refresh so its fp64 workspace stays ~<= 4 GiB.
+    const size_t per = size_t(nmax) * nmax * 8 * 5;
+    int chunk = int(std::max<size_t>(1, (size_t(4) << 30) / per));
+    int maxnb = 0;
+    for (const Group& g : bs->groups) maxnb = std::max(maxnb, g.nb);
+    bs->ws_chunk = std::min(chunk, std::max(1, maxnb));
+    bs->ws_n = nmax;
+    const size_t nn = size_t(nmax) * nmax * size_t(bs->ws_chunk);
+    bs->ws_snap = dalloc<double>(bs, nn);
+    bs->ws_vecs = dalloc<double>(bs, nn);
+    bs->ws_work = dalloc<double>(bs, nn);
+    bs->ws_W = dalloc<double>(bs, nn);
+    bs->ws_out = dalloc<double>(bs, nn);
+    bs->ws_vals = dalloc<double>(bs, size_t(nmax) * bs->ws_chunk);
+    bs->ws_eps = dalloc<double>(bs, size_t(bs->ws_chunk));
+    if (is_soap(bs)) {
+        int maxmn = 0;
+        for (const Group& g : bs->groups) maxmn = std::max(maxmn, g.m * g.n);
+        bs->iw_rotL = dalloc<double>(bs, size_t(nmax) * nmax);
+        bs->iw_rotR = dalloc<double>(bs, size_t(nmax) * nmax);
+        bs->iw_sq = dalloc<double>(bs, size_t(nmax) * nmax);
+        bs->iw_a = dalloc<double>(bs, size_t(maxmn));
+        bs->iw_b = dalloc<double>(bs, size_t(maxmn));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// GEMM helpers
+// ---------------------------------------------------------------------------
+Operand op(const float* h, const float* l, int rows, int K) { return Operand{h, l, rows, K}; }
+
+void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const GemmParams& p,
+              const int2* sym_tiles, int nsym, cudaStream_t s) {
+    GemmLaunch g{};
+    g.A = A;
+    g.B = B;
+    g.batch = batch;
+    g.epi = epi;
+    g.p = p;
+    g.sym_tiles = sym_tiles;
+    g.sym_tiles_count = nsym;
+    CK(gemm_launch(g, bs->precision, bs->num_sms, s));
+}
+
+template <class T>
+T* at(T* base, size_t stride, int slot) {
+    return base ? base + stride * size_t(slot) : nullptr;
+}
+
+// Statistics for slots [s0, s0+cnt) of a group (G slabs already staged).
+void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
+    const asg_optimizer_config& o = bs->opt;
+    const bool ema = o.accumulation == ASG_ACCUM_EMA;
+    const size_t mn = slabMN(g), mm = slabMM(g), nn = slabNN(g);
+    GemmParams p{};
+    if (!is_kl(bs)) {
+        p.alpha = ema ? float(1.0 - o.beta2) : 1.f;
+        p.beta = ema ? float(o.beta2) : 1.f;
+        p.C = at(g.L, mm, s0);
+        p.ldc = g.M;
+        p.c_bstride = int64_t(mm);
+        run_gemm(bs, op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N), op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N),
+                 cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s);
+        p.C = at(g.R, nn, s0);
+        p.ldc = g.N;
+        p.c_bstride = int64_t(nn);
+        run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M),
+                 cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s);
+        return;
+    }
+    // KL-Shampoo: X = G R^-1 (T) ; L = b L + a/n X G^T
+    GemmParams px{};
+    px.alpha = 1.f;
+    px.Dhi = at(g.Th, mn, s0);
+    px.Dlo = at(g.Tl, mn, s0);
+    px.ldd = g.N;
+    px.d_bstride = int64_t(mn);
+    run_gemm(bs, op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N), op(at(g.KRh, nn, s0), at(g.KRl, nn, s0), g.N, g.N),
+             cnt, EPI_SPLIT, px, nullptr, 0, s);
+    const double a = ema ? (1.0 - o.beta2) : 1.0;
+    p.beta = ema ? float(o.beta2) : 1.f;
+    p.alpha = float(a / double(g.n));
+    p.C = at(g.L, mm, s0);
+    p.ldc = g.M;
+    p.c_bstride = int64_t(mm);
+    run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N),
+             cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s);
+    // Z^T = G^T L^-1 (S, [N][M]) ; R = b R + a/m G^T Z
+    px.Dhi = at(g.Sh, mn, s0);
+    px.Dlo = at(g.Sl, mn, s0);
+    px.ldd = g.M;
+    run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.KLh, mm, s0), at(g.KLl, mm, s0), g.M, g.M),
+             cnt, EPI_SPLIT, px, nullptr, 0, s);
+    p.alpha = float(a / double(g.m));
+    p.C = at(g.R, nn, s0);
+    p.ldc = g.N;
+    p.c_bstride = int64_t(nn);
+    run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.Sh, mn, s0), at(g.Sl, mn, s0), g.N, g.M),
+             cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s);
+}
+
+// Preconditioned update for slots [s0, s0+cnt). `final_epi` is EPI_APPLY (step)
+// or EPI_STORE into `store_out` ([cnt][M][N], parity entry points).
+void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, float lr_eff, const ApplyEntry* apply,
+                  float* store_out, cudaStream_t s) {
+    const asg_optimizer_config& o = bs->opt;
+    const size_t mn = slabMN(g), mm = slabMM(g), nn = slabNN(g);
+    GemmParams pf{};
+    pf.alpha = 1.f;
+    pf.beta = 0.f;
+    pf.apply = apply;
+    pf.lr_eff = lr_eff;
+    pf.wd = float(o.weight_decay);
+    pf.flag = bs->d_flag;
+    pf.C = store_out;
+    pf.ldc = g.N;
+    pf.c_bstride = int64_t(mn);
+    GemmParams ps{};
+    ps.alpha = 1.f;
+    ps.ldd = g.N;
+    ps.d_bstride = int64_t(mn);
+    if (!is_soap(bs)) {
+        // Y = P_L G -> T ; U = Y P_R
+        ps.Dhi = at(g.Th, mn, s0);
+        ps.Dlo = at(g.Tl, mn, s0);
+        run_gemm(bs, op(at(g.PLh, mm, s0), at(g.PLl, mm, s0), g.M, g.M), op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M),
+                 cnt, EPI_SPLIT, ps, nullptr, 0, s);
+        run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.PRh, nn, s0), at(g.PRl, nn, s0), g.N, g.N),
+                 cnt, final_epi, pf, nullptr, 0, s);
+        return;
+    }
+    // SOAP (soap_scaled_step precond.cpp:208-223)
+    const Unit& u0 = bs->units[size_t(g.units[size_t(s0)])];
+    const double t = double(u0.moment_steps);  // already incremented by the caller
+    GemmParams pa{};
+    pa.alpha = 1.f;
+    pa.Dhi = at(g.Sh, mn, s0);
+    pa.Dlo = at(g.Sl, mn, s0);
+    pa.ldd = g.N;
+    pa.d_bstride = int64_t(mn);
+    pa.mom_m = at(g.mom_m, mn, s0);
+    pa.mom_v = at(g.mom_v, mn, s0);
+    pa.ldm = g.N;
+    pa.m_bstride = int64_t(mn);
+    pa.b1 = float(o.beta1);
+    pa.b2 = float(o.beta2);
+    pa.inv_bc1 = float(1.0 / (1.0 - std::pow(o.beta1, t)));
+    pa.inv_bc2 = float(1.0 / (1.0 - std::pow(o.beta2, t)));
+    pa.adam_eps = float(o.eps);
+    // T = Q_L^T G
+    ps.Dhi = at(g.Th, mn, s0);
+    ps.Dlo = at(g.Tl, mn, s0);
+    run_gemm(bs, op(at(g.QLTh, mm, s0), at(g.QLTl, mm, s0), g.M, g.M), op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M),
+             cnt, EPI_SPLIT, ps, nullptr, 0, s);
+    // Adam(T Q_R) -> S
+    run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.QRTh, nn, s0), at(g.QRTl, nn, s0), g.N, g.N),
+             cnt, EPI_ADAM, pa, nullptr, 0, s);
+    // W^T = (S Q_R^T)^T -> T as [N][M]
+    GemmParams pt{};
+    pt.alpha = 1.f;
+    pt.Dhi = at(g.Th, mn, s0);
+    pt.Dlo = at(g.Tl, mn, s0);
+    pt.ldd = g.M;
+    pt.d_bstride = int64_t(mn);
+    run_gemm(bs, op(at(g.Sh, mn, s0), at(g.Sl, mn, s0), g.M, g.N), op(at(g.QRh, nn, s0), at(g.QRl, nn, s0), g.N, g.N),
+             cnt, EPI_SPLIT_T, pt, nullptr, 0, s);
+    // U = Q_L W
+    run_gemm(bs, op(at(g.QLh, mm, s0), at(g.QLl, mm, s0), g.M, g.M), op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.N, g.M),
+             cnt, final_epi, pf, nullptr, 0, s);
+}
+
+// ---------------------------------------------------------------------------
+// refresh (side stream) and install (main stream)
+// ---------------------------------------------------------------------------
+// One side of one chunk: factor slab slots [s0, s0+cnt) of dim d (padded D).
+void refresh_side(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaStream_t s) {
+    const int d = left ? g.m : g.n, D = left ? g.M : g.N;
+    const size_t DD = size_t(D) * D, dd = size_t(d) * d;
+    const float* snap = at(left ? g.snapL : g.snapR, DD, s0);
+    launch_snapshot(snap, cnt, D, d, bs->ws_snap, s);
+    launch_sym_eig(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, cnt, d, g.d_status + s0, s);
+    if (is_soap(bs)) {
+        CK(cudaMemcpyAsync(at(left ? g.sQL64 : g.sQR64, dd, s0), bs->ws_vecs, size_t(cnt) * dd * 8,
+                           cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(at(left ? g.svalsL : g.svalsR, size_t(d), s0), bs->ws_vals, size_t(cnt) * d * 8,
+                           cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    launch_relative_damping(bs->ws_snap, cnt, d, bs->opt.damping, bs->ws_eps, s);
+    struct Out {
+        double power;
+        float *hi, *lo;
+    };
+    std::vector<Out> outs;
+    if (is_kl(bs)) {
+        outs.push_back({-0.5, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
+        outs.push_back({-1.0, at(left ? g.sKLh : g.sKRh, DD, s0), at(left ? g.sKLl : g.sKRl, DD, s0)});
+    } else {
+        outs.push_back({-0.25, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
+    }
+    for (const Out& o : outs) {
+        launch_scale_columns(bs->ws_vecs, bs->ws_vals, bs->ws_eps, o.power, cnt, d, bs->ws_W, g.d_status + s0, s);
+        // V diag(w) V^T  (densela.hpp:280), symmetrized on conversion
+        launch_dgemm(false, true, d, d, d, 1.0, bs->ws_W, d, int64_t(dd), bs->ws_vecs, d, int64_t(dd), 0.0, bs->ws_out,
+                     d, int64_t(dd), cnt, s);
+        launch_f64_to_split(bs->ws_out, cnt, d, D, true, o.hi, o.lo, nullptr, nullptr, s);
+    }
+}
+
+// Launches the refresh for every unit marked dispatched-but-not-launched.
+void launch_refreshes(asg_blockset* bs) {
+    std::vector<std::vector<int>> per_group(bs->groups.size());
+    for (size_t i = 0; i < bs->units.size(); ++i) {
+        Unit& u = bs->units[i];
+        if (u.pending && !u.launched && u.group >= 0) per_group[size_t(u.group)].push_back(int(i));
+    }
+    bool any = false;
+    for (auto& v : per_group) any |= !v.empty();
+    if (!any) return;
+    // snapshot on the main stream (after this step's accumulation), then the
+    // side stream works from the snapshot (snapshot isolation, asyncsched.cpp:129-136)
+    for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
+        Group& g = bs->groups[gi];
+        for (int ui : per_group[gi]) {
+            const Unit& u = bs->units[size_t(ui)];
+            CK(cudaMemcpyAsync(at(g.snapL, slabMM(g), u.slot), at(g.L, slabMM(g), u.slot), slabMM(g) * 4,
+                               cudaMemcpyDeviceToDevice, bs->main));
+            CK(cudaMemcpyAsync(at(g.snapR, slabNN(g), u.slot), at(g.R, slabNN(g), u.slot), slabNN(g) * 4,
+                               cudaMemcpyDeviceToDevice, bs->main));
+        }
+    }
+    CK(cudaEventRecord(bs->ev_snap, bs->main));
+    CK(cudaStreamWaitEvent(bs->side, bs->ev_snap, 0));
+    for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
+        Group& g = bs->groups[gi];
+        std::vector<int> slots;
+        for (int ui : per_group[gi]) slots.push_back(bs->units[size_t(ui)].slot);
+        std::sort(slots.begin(), slots.end());
+        size_t i = 0;
+        while (i < slots.size()) {
+            // maximal contiguous run, split into workspace-sized chunks
+            size_t j = i + 1;
+            while (j < slots.size() && slots[j] == slots[j - 1] + 1 && int(j - i) < bs->ws_chunk) ++j;
+            const int s0 = slots[i], cnt = int(j - i);
+            CK(cudaMemsetAsync(g.d_status + s0, 0, size_t(cnt) * sizeof(int), bs->side));
+            refresh_side(bs, g, s0, cnt, true, bs->side);
+            refresh_side(bs, g, s0, cnt, false, bs->side);
+            CK(cudaMemcpyAsync(g.h_status + s0, g.d_status + s0, size_t(cnt) * sizeof(int), cudaMemcpyDeviceToHost,
+                               bs->side));
+            for (int k = 0; k < cnt; ++k) {
+                Unit& u = bs->units[size_t(g.units[size_t(s0 + k)])];
+                CK(cudaEventRecord(u.done, bs->side));
+                u.launched = true;
+            }
+            i = j;
+        }
+    }
+    CK(cudaGetLastError());
+}
+
+int status_to_code(int st) { return st; }
+
+// Device-side install of a finished refresh (install_refresh precond.cpp:144-164).
+void install_device(asg_blockset* bs, Unit& u) {
+    if (!u.launched) launch_refreshes(bs);
+    Group& g = bs->groups[size_t(u.group)];
+    CK(cudaEventSynchronize(u.done));
+    const int st = g.h_status[u.slot];
+    if (st != ASG_OK) {
+        const char* what = st == ASG_ERR_NOT_PSD       ? "refresh: damped eigenvalue <= 0"
+                           : st == ASG_ERR_NON_FINITE   ? "refresh: non-finite factor"
+                           : st == ASG_ERR_NO_CONVERGENCE ? "refresh: eigensolver sweep budget exhausted"
+                                                          : "refresh failed";
+        throw Fail{status_to_code(st), what};
+    }
+    CK(cudaStreamWaitEvent(bs->main, u.done, 0));
+    cudaStream_t s = bs->main;
+    const size_t mm = slabMM(g), nn = slabNN(g);
+    auto cp = [&](float* dst, const float* src, size_t n) {
+        if (dst && src) CK(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToDevice, s));
+    };
+    if (!is_soap(bs)) {
+        cp(at(g.PLh, mm, u.slot), at(g.sPLh, mm, u.slot), mm);
+        cp(at(g.PLl, mm, u.slot), at(g.sPLl, mm, u.slot), mm);
+        cp(at(g.PRh, nn, u.slot), at(g.sPRh, nn, u.slot), nn);
+        cp(at(g.PRl, nn, u.slot), at(g.sPRl, nn, u.slot), nn);
+        if (is_kl(bs)) {
+            cp(at(g.KLh, mm, u.slot), at(g.sKLh, mm, u.slot), mm);
+            cp(at(g.KLl, mm, u.slot), at(g.sKLl, mm, u.slot), mm);
+            cp(at(g.KRh, nn, u.slot), at(g.sKRh, nn, u.slot), nn);
+            cp(at(g.KRl, nn, u.slot), at(g.sKRl, nn, u.slot), nn);
+        }
+        return;
+    }
+    // SOAP: rot = Q_new^T Q_old per side; M <- rot_L M rot_R^T,
+    // V <- (rot_L o rot_L) V (rot_R o rot_R)^T; swap bases.
+    const int m = g.m, n = g.n;
+    const size_t dm = size_t(m) * m, dn = size_t(n) * n, mnd = size_t(m) * n, MN = slabMN(g);
+    double* qLn = at(g.sQL64, dm, u.slot);
+    double* qLo = at(g.QL64, dm, u.slot);
+    double* qRn = at(g.sQR64, dn, u.slot);
+    double* qRo = at(g.QR64, dn, u.slot);
+    launch_dgemm(true, false, m, m, m, 1.0, qLn, m, 0, qLo, m, 0, 0.0, bs->iw_rotL, m, 0, 1, s);
+    launch_dgemm(true, false, n, n, n, 1.0, qRn, n, 0, qRo, n, 0, 0.0, bs->iw_rotR, n, 0, 1, s);
+    for (int which = 0; which < 2; ++which) {
+        float* mom = at(which == 0 ? g.mom_m : g.mom_v, MN, u.slot);
+        const double* rl = bs->iw_rotL;
+        const double* rr = bs->iw_rotR;
+        if (which == 1) {
+            launch_square_f64(bs->iw_rotL, bs->iw_sq, int64_t(dm), s);
+            rl = bs->iw_sq;
+        }
+        launch_f32_to_f64(mom, 1, m, n, g.M, g.N, bs->iw_a, s);
+        launch_dgemm(false, false, m, n, m, 1.0, rl, m, 0, bs->iw_a, n, 0, 0.0, bs->iw_b, n, 0, 1, s);
+        if (which == 1) {
+            // rot_R o rot_R into iw_a's spare? reuse rotR in place after squaring
+            launch_square_f64(bs->iw_rotR, bs->iw_rotR, int64_t(dn), s);
+            rr = bs->iw_rotR;
+        }
+        launch_dgemm(false, true, m, n, n, 1.0, bs->iw_b, n, 0, rr, n, 0, 0.0, bs->iw_a, n, 0, 1, s);
+        launch_f64_to_f32(bs->iw_a, 1, m, n, mom, g.M, g.N, s);
+    }
+    (void)mnd;
+    CK(cudaMemcpyAsync(qLo, qLn, dm * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(qRo, qRn, dn * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(at(g.valsL, size_t(m), u.slot), at(g.svalsL, size_t(m), u.slot), size_t(m) * 8,
+                       cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(at(g.valsR, size_t(n), u.slot), at(g.svalsR, size_t(n), u.slot), size_t(n) * 8,
+                       cudaMemcpyDeviceToDevice, s));
+    launch_f64_to_split(qLo, 1, m, g.M, false, at(g.QLh, mm, u.slot), at(g.QLl, mm, u.slot), at(g.QLTh, mm, u.slot),
+                        at(g.QLTl, mm, u.slot), s);
+    launch_f64_to_split(qRo, 1, n, g.N, false, at(g.QRh, nn, u.slot), at(g.QRl, nn, u.slot), at(g.QRTh, nn, u.slot),
+                        at(g.QRTl, nn, u.slot), s);
+}
+
+// ShadowScheduler::install (asyncsched.cpp:144-189) bookkeeping + device install.
+void sched_install(asg_blockset* bs, int idx, int64_t step) {
+    Unit& u = bs->units[size_t(idx)];
+    bs->stats.completed += 1;
+    emit(bs, u.dispatch_step, ASG_EV_JOB_START, idx, u.version, u.dispatch_sim);
+    emit(bs, step, ASG_EV_JOB_DONE, idx, u.version, u.completion_sim);
+    install_device(bs, u);
+    u.version += 1;
+    u.last_refresh_step = step;
+    bs->now_us += bs->sc.install_cost_us;
+    u.fresh.installed_version = u.version;
+    u.fresh.last_install_step = step;
+    u.fresh.installed_snapshot_step = u.dispatch_step;
+    u.fresh.dispatch_step_of_pending = -1;
+    u.pending = false;
+    u.launched = false;
+    emit(bs, step, ASG_EV_INSTALL, idx, u.version, bs->now_us);
+    bs->stats.installed += 1;
+}
+
+// maybe_dispatch (asyncsched.cpp:108-142), host bookkeeping only.
+bool sched_dispatch(asg_blockset* bs, int idx, int64_t step) {
+    Unit& u = bs->units[size_t(idx)];
+    if (step % bs->sc.pf != 0) return false;
+    if (u.pending) {
+        bs->stats.coalesced += 1;
+        return false;
+    }
+    double cost = bs->sc.inject_job_delay_steps;
+    if (bs->sc.inject_job_delay_jitter_steps > 0.0) {
+        std::uniform_real_distribution<double> dist(0.0, bs->sc.inject_job_delay_jitter_steps);
+        cost += dist(bs->jitter);
+    }
+    u.pending = true;
+    u.launched = false;
+    u.dispatch_step = step;
+    u.dispatch_sim = bs->now_us;
+    u.completion_sim = bs->now_us + cost * bs->sc.step_compute_us;
+    emit(bs, step, ASG_EV_DISPATCH, idx, u.version, bs->now_us);
+    u.has_fresh = true;
+    u.fresh.dispatch_step_of_pending = step;
+    bs->stats.dispatched += 1;
+    return true;
+}
+
+// staleness_barrier (asyncsched.cpp:191-221).
+double sched_barrier(asg_blockset* bs, int idx, int64_t step) {
+    Unit& u = bs->units[size_t(idx)];
+    if (!u.pending) return 0.0;
+    const int64_t age = step - u.dispatch_step;
+    const bool stale_consumer =
+        u.version > 0 && step - u.fresh.installed_snapshot_step > (bs->sc.staleness_S + 1) * bs->sc.pf;
+    const bool wait = bs->sc.staleness_S == 0 || age > bs->sc.staleness_S || stale_consumer;
+    if (!wait) return 0.0;
+    double waited;
+    const double now = bs->now_us;
+    if (bs->sc.install_mode == ASG_INSTALL_EVENT) {
+        waited = 0.0;  // the main stream waits on the refresh event; the host does not block
+    } else {
+        waited = std::max(0.0, u.completion_sim - now);
+    }
+    emit(bs, step, ASG_EV_BARRIER_WAIT_BEGIN, idx, u.version, now);
+    bs->now_us += waited;
+    sched_install(bs, idx, step);
+    emit(bs, step, ASG_EV_BARRIER_WAIT_END, idx, u.version, bs->now_us);
+    bs->stats.barrier_waits += 1;
+    bs->stats.wait_total_us += waited;
+    return waited;
+}
+
+// on_hook(StepEnd) (asyncsched.cpp:268-286).
+void sched_step_end(asg_blockset* bs, int64_t step) {
+    launch_refreshes(bs);
+    std::vector<int> ready;
+    for (size_t i = 0; i < bs->units.size(); ++i) {
+        Unit& u = bs->units[i];
+        if (!u.pending) continue;
+        bool ok;
+        if (bs->sc.install_mode == ASG_INSTALL_EVENT)
+            ok = u.launched && cudaEventQuery(u.done) == cudaSuccess;
+        else
+            ok = u.completion_sim <= bs->now_us;
+        if (ok) ready.push_back(int(i));
+    }
+    for (int i : ready) sched_install(bs, i, step);
+}
+
+void check_owned_index(const asg_blockset* bs, int64_t idx) {
+    if (idx < 0 || idx >= int64_t(bs->units.size())) throw Fail{ASG_ERR_INVALID_ARGUMENT, "block index out of range"};
+}
+
+void stage_host_grad(asg_blockset* bs, const Unit& u, const double* g, int64_t ld) {
+    const int m = int(u.spec.row_end - u.spec.row_begin), n = int(u.spec.col_end - u.spec.col_begin);
+    std::vector<float> buf(size_t(m) * n);
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) {
+            const double x = g[size_t(i) * ld + j];
+            if (!std::isfinite(x)) throw Fail{ASG_ERR_NON_FINITE, "accumulate_factors: non-finite gradient"};
+            buf[size_t(i) * n + j] = float(x);
+        }
+    h2d(bs->stage, buf.data(), buf.size() * 4, bs->main);
+    BlockRef r{bs->stage, nullptr, n, m, n};
+    h2d(bs->d_ref1, &r, sizeof(r), bs->main);
+}
+
+Group& owned_group(asg_blockset* bs, const Unit& u) {
+    if (u.adamw || u.group < 0) throw Fail{ASG_ERR_INVALID_ARGUMENT, "block is not a preconditioned block owned by this rank"};
+    return bs->groups[size_t(u.group)];
+}
+
+void prep_single(asg_blockset* bs, Group& g, const Unit& u) {
+    const size_t mn = slabMN(g);
+    launch_prep_grad(bs->d_ref1, 1, g.M, g.N, nullptr, 1.f, at(g.Gh, mn, u.slot), at(g.Gl, mn, u.slot),
+                     at(g.GTh, mn, u.slot), at(g.GTl, mn, u.slot), bs->main);
+}
+
+void download_block(asg_blockset* bs, Group& g, double* out) {
+    std::vector<float> buf(slabMN(g));
+    CK(cudaStreamSynchronize(bs->main));
+    CK(cudaMemcpy(buf.data(), bs->d_out1, buf.size() * 4, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < g.m; ++i)
+        for (int j = 0; j < g.n; ++j) out[size_t(i) * g.n + j] = double(buf[size_t(i) * g.N + j]);
+}
+
+void check_flag(asg_blockset* bs) {
+    int f = 0;
+    CK(cudaMemcpy(&f, bs->d_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (f) {
+        CK(cudaMemset(bs->d_flag, 0, sizeof(int)));
+        throw Fail{ASG_ERR_NON_FINITE, "apply_update: non-finite update"};
+    }
+}
+
+}  // namespace
+}  // namespace asg
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+using namespace asg;
+
+extern "C" {
+
+const char* asg_last_error(void) { return g_err.c_str(); }
+int asg_api_version(void) { return ASG_API_VERSION; }
+
+int asg_device_supported(int device) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 0;
+    return prop.major == 10 && prop.minor == 0 ? 1 : 0;
+}
+
+int asg_optimizer_defaults(int32_t method, asg_optimizer_config* out) {
+    return guard([&] {
+        if (!out) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null output"};
+        *out = defaults_for(method);
+    });
+}
+
+int asg_optimizer_validate(const asg_optimizer_config* cfg) {
+    return guard([&] {
+        if (!cfg) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null config"};
+        validate(*cfg);
+    });
+}
+
+int asg_scheduler_defaults(asg_scheduler_config* out) {
+    return guard([&] { *out = sched_defaults(); });
+}
+
+int asg_config_from_json(const char* text, asg_optimizer_config* opt, asg_scheduler_config* sched, int32_t* precision) {
+    return guard([&] {
+        if (!text || !opt || !sched) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        json::Value j;
+        try {
+            j = json::Parser(text).parse();
+        } catch (const std::exception& e) {
+            throw Fail{ASG_ERR_CONFIG_INVALID, e.what()};
+        }
+        asg_optimizer_config o = defaults_for(ASG_METHOD_ADAMW);
+        asg_scheduler_config s = sched_defaults();
+        int32_t prec = ASG_PREC_3XTF32;
+        auto num = [&](const json::Value& v, const char* k, auto& out) {
+            if (!v.has(k)) return;
+            const json::Value& x = v.at(k);
+            if (x.kind != json::Value::Number) throw Fail{ASG_ERR_CONFIG_INVALID, std::string("not a number: ") + k};
+            out = static_cast<std::remove_reference_t<decltype(out)>>(x.num);
+        };
+        auto str = [&](const json::Value& v, const char* k) -> std::string {
+            const json::Value& x = v.at(k);
+            if (x.kind != json::Value::String) throw Fail{ASG_ERR_CONFIG_INVALID, std::string("not a string: ") + k};
+            return x.str;
+        };
+        if (j.has("optimizer")) {  // config.cpp:124-139
+            const json::Value& v = j.at("optimizer");
+            if (v.has("method")) o = defaults_for(method_from_string(str(v, "method")));
+            num(v, "lr", o.lr);
+            num(v, "beta1", o.beta1);
+            num(v, "beta2", o.beta2);
+            num(v, "eps", o.eps);
+            num(v, "weight_decay", o.weight_decay);
+            num(v, "precondition_frequency", o.precondition_frequency);
+            if (v.has("accumulation")) {
+                const std::string a = str(v, "accumulation");
+                if (a == "Sum") o.accumulation = ASG_ACCUM_SUM;
+                else if (a == "EMA") o.accumulation = ASG_ACCUM_EMA;
+                else throw Fail{ASG_ERR_CONFIG_INVALID, "unknown accumulation mode: " + a};
+            }
+            num(v, "damping", o.damping);
+            num(v, "block_dim_limit", o.block_dim_limit);
+        }
+        s.pf = o.precondition_frequency;  // config.cpp:140
+        if (j.has("async")) {             // config.cpp:141-149
+            const json::Value& a = j.at("async");
+            num(a, "staleness_S", s.staleness_S);
+            num(a, "pf", s.pf);
+            num(a, "pool_size", s.pool_size);
+            num(a, "inject_job_delay_steps", s.inject_job_delay_steps);
+            num(a, "inject_job_delay_jitter_steps", s.inject_job_delay_jitter_steps);
+            num(a, "drain_budget", s.drain_budget);
+        }
+        if (j.has("sim")) {  // config.cpp:193-202
+            num(j.at("sim"), "step_compute_us", s.step_compute_us);
+            num(j.at("sim"), "install_cost_us", s.install_cost_us);
+        } else {
+            s.install_cost_us = 10.0;  // SimCostConfig default (harness.hpp:51-54)
+        }
+        if (j.has("gpu")) {
+            const json::Value& g = j.at("gpu");
+            if (g.has("precision")) {
+                const std::string p = str(g, "precision");
+                if (p == "3xtf32") prec = ASG_PREC_3XTF32;
+                else if (p == "tf32") prec = ASG_PREC_TF32;
+                else throw Fail{ASG_ERR_CONFIG_INVALID, "unknown precision: " + p};
+            }
+            if (g.has("install_mode")) {
+                const std::string m = str(g, "install_mode");
+                if (m == "sim_clock") s.install_mode = ASG_INSTALL_SIM_CLOCK;
+                else if (m == "event") s.install_mode = ASG_INSTALL_EVENT;
+                else throw Fail{ASG_ERR_CONFIG_INVALID, "unknown install_mode: " + m};
+            }
+        }
+        validate(o);  // config.cpp:40-43
+        if (s.pf != o.precondition_frequency)
+            throw Fail{ASG_ERR_CONFIG_INVALID, "async.pf must equal optimizer.precondition_frequency"};
+        if (s.staleness_S < 0) throw Fail{ASG_ERR_CONFIG_INVALID, "staleness_S must be >= 0"};
+        *opt = o;
+        *sched = s;
+        if (precision) *precision = prec;
+    });
+}
+
+int asg_partition_param(int64_t param_index, int64_t rows, int64_t cols, int64_t limit, asg_block_spec* out,
+                        int64_t capacity, int64_t* count) {
+    return guard([&] {
+        if (limit < 1) throw Fail{ASG_ERR_CONFIG_INVALID, "partition_param: limit must be >= 1"};
+        if (rows < 1 || cols < 1) throw Fail{ASG_ERR_SHAPE_MISMATCH, "partition_param: empty parameter"};
+        int64_t k = 0;
+        for (int64_t r = 0; r < rows; r += limit)
+            for (int64_t c = 0; c < cols; c += limit) {
+                if (out && k < capacity)
+                    out[k] = asg_block_spec{param_index, r, std::min(rows, r + limit), c, std::min(cols, c + limit), limit};
+                ++k;
+            }
+        if (count) *count = k;
+    });
+}
+
+int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_scheduler_config* sched,
+                        const asg_param_desc* params, int64_t n_params, int32_t precision, int32_t rank, int32_t world,
+                        uint64_t seed, asg_blockset** out) {
+    asg_blockset* bs = nullptr;
+    int rc = guard([&] {
+        if (!opt || !sched || !out || (n_params > 0 && !params)) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        validate(*opt);
+        if (sched->staleness_S < 0) throw Fail{ASG_ERR_CONFIG_INVALID, "staleness_S must be >= 0"};
+        if (sched->pf < 1) throw Fail{ASG_ERR_CONFIG_INVALID, "pf must be >= 1"};
+        if (sched->pf != opt->precondition_frequency)
+            throw Fail{ASG_ERR_CONFIG_INVALID, "async.pf must equal optimizer.precondition_frequency"};
+        if (world < 1 || rank < 0 || rank >= world) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad rank/world"};
+        if (precision != ASG_PREC_3XTF32 && precision != ASG_PREC_TF32)
+            throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad precision"};
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+            throw Fail{ASG_ERR_UNSUPPORTED, "no CUDA device " + std::to_string(device)};
+        if (!asg_device_supported(device))
+            throw Fail{ASG_ERR_UNSUPPORTED, "device is not sm_100 (B200); this library has no other code path"};
+        CK(cudaSetDevice(device));
+        bs = new asg_blockset();
+        bs->device = device;
+        bs->opt = *opt;
+        bs->sc = *sched;
+        bs->precision = precision;
+        bs->rank = rank;
+        bs->world = world;
+        bs->jitter.seed(seed * 0x9e3779b97f4a7c15ull + 0x2545f4914f6cdd1dull);  // asyncsched.cpp:248
+        bs->params.assign(params, params + n_params);
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        bs->num_sms = prop.multiProcessorCount;
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&bs->main, cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&bs->side, cudaStreamNonBlocking, lo));
+        bs->own_main = true;
+        CK(cudaEventCreateWithFlags(&bs->ev_snap, cudaEventDisableTiming));
+        build_units(bs);
+        build_groups(bs);
+        for (Group& g : bs->groups) alloc_group(bs, g);
+        alloc_workspace(bs);
+        for (Unit& u : bs->units) {
+            CK(cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming));
+            if (u.adamw && u.owner == rank) {
+                const size_t n = size_t(u.spec.row_end - u.spec.row_begin) * size_t(u.spec.col_end - u.spec.col_begin);
+                u.am = dalloc<float>(bs, n);
+                u.av = dalloc<float>(bs, n);
+                CK(cudaMemsetAsync(u.am, 0, n * 4, bs->main));
+                CK(cudaMemsetAsync(u.av, 0, n * 4, bs->main));
+            }
+        }
+        bs->d_flag = dalloc<int>(bs, 1);
+        bs->d_sqnorm = dalloc<double>(bs, 1);
+        bs->d_scale = dalloc<float>(bs, 1);
+        CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), bs->main));
+        size_t stage = 0;
+        for (const Group& g : bs->groups) stage = std::max(stage, slabMN(g));
+        bs->stage_elems = stage;
+        bs->stage = dalloc<float>(bs, std::max<size_t>(stage, 1));
+        bs->d_out1 = dalloc<float>(bs, std::max<size_t>(stage, 1));
+        bs->d_ref1 = dalloc<BlockRef>(bs, 1);
+        bs->d_apply1 = dalloc<ApplyEntry>(bs, 1);
+        // owner-major all-gather layout
+        std::vector<BlockRef> pk, upk;
+        std::vector<int64_t> pko, upko;
+        bs->shard_elems.assign(size_t(world), 0);
+        for (int r = 0; r < world; ++r) {
+            for (size_t i = 0; i < bs->units.size(); ++i) {
+                const Unit& u = bs->units[i];
+                if (u.owner != r) continue;
+                const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+                BlockRef br{};
+                br.src = d.theta ? d.theta + u.spec.row_begin * d.ld_theta + u.spec.col_begin : nullptr;
+                br.dst = d.theta ? d.theta + u.spec.row_begin * d.ld_theta + u.spec.col_begin : nullptr;
+                br.ld = d.ld_theta;
+                br.rows = int32_t(u.spec.row_end - u.spec.row_begin);
+                br.cols = int32_t(u.spec.col_end - u.spec.col_begin);
+                if (r == rank) {
+                    pk.push_back(br);
+                    pko.push_back(bs->shard_elems[size_t(r)]);
+                }
+                upk.push_back(br);
+                upko.push_back(bs->shard_elems[size_t(r)]);
+                bs->unpack_rank.push_back(r);
+                bs->shard_elems[size_t(r)] += int64_t(br.rows) * br.cols;
+            }
+        }
+        bs->n_pack = int(pk.size());
+        bs->n_unpack = int(upk.size());
+        bs->d_pack_refs = dalloc<BlockRef>(bs, pk.size());
+        bs->d_pack_offs = dalloc<int64_t>(bs, pko.size());
+        bs->d_unpack_refs = dalloc<BlockRef>(bs, upk.size());
+        bs->d_unpack_offs = dalloc<int64_t>(bs, upko.size());
+        if (!pk.empty()) {
+            h2d(bs->d_pack_refs, pk.data(), pk.size() * sizeof(BlockRef), bs->main);
+            h2d(bs->d_pack_offs, pko.data(), pko.size() * 8, bs->main);
+        }
+        if (!upk.empty()) {
+            h2d(bs->d_unpack_refs, upk.data(), upk.size() * sizeof(BlockRef), bs->main);
+            h2d(bs->d_unpack_offs, upko.data(), upko.size() * 8, bs->main);
+        }
+        CK(cudaStreamSynchronize(bs->main));
+        CK(cudaGetLastError());
+        *out = bs;
+    });
+    if (rc != ASG_OK && bs) {
+        std::string keep = g_err;
+        asg_blockset_destroy(bs);
+        g_err = keep;
+    }
+    return rc;
+}
+
+int asg_blockset_destroy(asg_blockset* bs) {
+    if (!bs) return ASG_OK;
+    cudaSetDevice(bs->device);
+    if (bs->main) cudaStreamSynchronize(bs->main);
+    if (bs->side) cudaStreamSynchronize(bs->side);
+    for (auto& u : bs->units)
+        if (u.done) cudaEventDestroy(u.done);
+    if (bs->ev_snap) cudaEventDestroy(bs->ev_snap);
+    for (void* p : bs->allocs) cudaFree(p);
+    for (void* p : bs->host_allocs) cudaFreeHost(p);
+    if (bs->own_main && bs->main) cudaStreamDestroy(bs->main);
+    if (bs->side) cudaStreamDestroy(bs->side);
+    delete bs;
+    return ASG_OK;
+}
+
+int asg_blockset_bind_params(asg_blockset* bs, const asg_param_desc* params, int64_t n_params) {
+    return guard([&] {
+        if (!bs || !params || n_params != int64_t(bs->params.size())) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad params"};
+        for (int64_t i = 0; i < n_params; ++i)
+            if (params[i].rows != bs->params[size_t(i)].rows || params[i].cols != bs->params[size_t(i)].cols)
+                throw Fail{ASG_ERR_SHAPE_MISMATCH, "bind_params: shape changed"};
+        CK(cudaSetDevice(bs->device));
+        CK(cudaStreamSynchronize(bs->main));
+        bs->params.assign(params, params + n_params);
+        for (Group& g : bs->groups) bind_group_tables(bs, g);
+    });
+}
+
+int asg_blockset_num_blocks(const asg_blockset* bs, int64_t* n) {
+    return guard([&] {
+        if (!bs || !n) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        *n = int64_t(bs->units.size());
+    });
+}
+
+int asg_blockset_block_info(const asg_blockset* bs, int64_t idx, asg_block_info* out) {
+    return guard([&] {
+        if (!bs || !out) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        out->spec = u.spec;
+        out->version = u.version;
+        out->last_refresh_step = u.last_refresh_step;
+        out->moment_steps = u.moment_steps;
+        out->owner_rank = u.owner;
+        out->use_adamw = u.adamw ? 1 : 0;
+    });
+}
+
+int asg_blockset_state_bytes(const asg_blockset* bs, uint64_t* bytes) {
+    return guard([&] {
+        size_t total = 0;
+        for (void* p : bs->allocs) {
+            (void)p;
+        }
+        // recompute from group sizes (allocation sizes are not tracked per pointer)
+        for (const Group& g : bs->groups) {
+            const size_t nb = size_t(g.nb);
+            size_t f = nb * (2 * slabMM(g) + 2 * slabNN(g) + 4 * slabMN(g) * (split_mode(bs) ? 2 : 1));
+            if (is_soap(bs))
+                f += nb * ((slabMM(g) * 2 + slabNN(g) * 2) * (split_mode(bs) ? 2 : 1) + 2 * slabMN(g)) +
+                     nb * 2 * (size_t(g.m) * g.m + size_t(g.n) * g.n) * 2;
+            else
+                f += nb * (slabMM(g) + slabNN(g)) * 2 * (split_mode(bs) ? 2 : 1) * (is_kl(bs) ? 2 : 1);
+            total += f * 4;
+        }
+        *bytes = total;
+    });
+}
+
+int asg_blockset_stream(const asg_blockset* bs, void** stream) {
+    return guard([&] { *stream = bs->main; });
+}
+
+int asg_grad_sqnorm(asg_blockset* bs, void* stream, double* sqnorm, int32_t* nonfinite) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        CK(cudaMemsetAsync(bs->d_sqnorm, 0, sizeof(double), s));
+        CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), s));
+        for (const asg_param_desc& d : bs->params) launch_sqnorm(d.grad, d.rows, d.cols, d.ld_grad, bs->d_sqnorm, bs->d_flag, s);
+        double v = 0.0;
+        int f = 0;
+        CK(cudaMemcpyAsync(&v, bs->d_sqnorm, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&f, bs->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), s));
+        if (sqnorm) *sqnorm = v;
+        if (nonfinite) *nonfinite = f;
+    });
+}
+
+int asg_accumulate(asg_blockset* bs, double clip_scale, void* stream) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        if (s != bs->main) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CK(cudaEventRecord(e, s));
+            CK(cudaStreamWaitEvent(bs->main, e, 0));
+            CK(cudaEventDestroy(e));
+        }
+        for (Group& g : bs->groups) {
+            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, bs->main);
+            group_stats(bs, g, 0, g.nb, bs->main);
+        }
+        CK(cudaGetLastError());
+    });
+}
+
+int asg_maybe_dispatch(asg_blockset* bs, int64_t step, int64_t* n_dispatched) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        int64_t n = 0;
+        for (size_t i = 0; i < bs->units.size(); ++i) {
+            const Unit& u = bs->units[i];
+            if (u.adamw || u.owner != bs->rank) continue;
+            n += sched_dispatch(bs, int(i), step) ? 1 : 0;
+        }
+        launch_refreshes(bs);
+        if (n_dispatched) *n_dispatched = n;
+    });
+}
+
+int asg_staleness_barrier(asg_blockset* bs, int64_t step, double* waited_us) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        double w = 0.0;
+        for (size_t i = 0; i < bs->units.size(); ++i) {
+            const Unit& u = bs->units[i];
+            if (u.adamw || u.owner != bs->rank) continue;
+            w += sched_barrier(bs, int(i), step);
+        }
+        if (waited_us) *waited_us = w;
+    });
+}
+
+namespace {
+void precondition_apply_impl(asg_blockset* bs, double clip_scale, double lr_scale) {
+    const float lr_eff = float(bs->opt.lr * lr_scale);
+    for (Group& g : bs->groups) {
+        if (is_soap(bs)) {
+            int64_t ms = -1;
+            for (int ui : g.units) {
+                Unit& u = bs->units[size_t(ui)];
+                u.moment_steps += 1;
+                if (ms >= 0 && u.moment_steps != ms) throw Fail{ASG_ERR_AUDIT, "SOAP moment steps diverged within a group"};
+                ms = u.moment_steps;
+            }
+        }
+        group_update(bs, g, 0, g.nb, EPI_APPLY, lr_eff, g.d_apply, nullptr, bs->main);
+    }
+    for (Unit& u : bs->units) {
+        if (!u.adamw || u.owner != bs->rank) continue;
+        const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+        u.adam_t += 1;
+        const double t = double(u.adam_t);
+        launch_adamw_apply(d.theta, d.ld_theta, d.grad, d.ld_grad, d.rows, d.cols, u.am, u.av, nullptr, float(clip_scale),
+                           float(bs->opt.beta1), float(bs->opt.beta2), float(1.0 / (1.0 - std::pow(bs->opt.beta1, t))),
+                           float(1.0 / (1.0 - std::pow(bs->opt.beta2, t))), float(bs->opt.eps), lr_eff,
+                           float(bs->opt.weight_decay), bs->d_flag, bs->main);
+    }
+    CK(cudaGetLastError());
+}
+}  // namespace
+
+int asg_precondition_apply(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale, void* stream) {
+    (void)step;
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        precondition_apply_impl(bs, clip_scale, lr_scale);
+        if (stream && static_cast<cudaStream_t>(stream) != bs->main) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CK(cudaEventRecord(e, bs->main));
+            CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e, 0));
+            CK(cudaEventDestroy(e));
+        }
+    });
+}
+
+int asg_step_end(asg_blockset* bs, int64_t step) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        sched_step_end(bs, step);
+    });
+}
+
+int asg_step(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale, void* stream) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        if (s != bs->main) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CK(cudaEventRecord(e, s));
+            CK(cudaStreamWaitEvent(bs->main, e, 0));
+            CK(cudaEventDestroy(e));
+        }
+        // accumulate (all owned blocks, batched per shape group)
+        for (Group& g : bs->groups) {
+            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, bs->main);
+            group_stats(bs, g, 0, g.nb, bs->main);
+        }
+        // per-block dispatch -> barrier in the reference's order (harness.cpp:452-454);
+        // a barrier install launches any outstanding refresh first.
+        for (size_t i = 0; i < bs->units.size(); ++i) {
+            const Unit& u = bs->units[i];
+            if (u.adamw || u.owner != bs->rank) continue;
+            sched_dispatch(bs, int(i), step);
+            sched_barrier(bs, int(i), step);
+        }
+        launch_refreshes(bs);
+        precondition_apply_impl(bs, clip_scale, lr_scale);
+        sched_step_end(bs, step);
+        if (s != bs->main) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CK(cudaEventRecord(e, bs->main));
+            CK(cudaStreamWaitEvent(s, e, 0));
+            CK(cudaEventDestroy(e));
+        }
+    });
+}
+
+int asg_clock_advance(asg_blockset* bs, double us) {
+    return guard([&] { bs->now_us += us; });
+}
+
+int asg_get_freshness(const asg_blockset* bs, int64_t idx, asg_freshness* out) {
+    return guard([&] {
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        if (!u.has_fresh) throw Fail{ASG_ERR_MISSING_KEY, "asyncsched: no freshness record"};
+        *out = u.fresh;
+    });
+}
+
+int asg_get_stats(const asg_blockset* bs, asg_pool_stats* out) {
+    return guard([&] {
+        *out = bs->stats;
+        int pending = 0;
+        for (const Unit& u : bs->units) pending += u.pending ? 1 : 0;
+        out->pending = pending;
+        out->queue_depth = 0;
+    });
+}
+
+int asg_get_events(const asg_blockset* bs, asg_event* out, int64_t capacity, int64_t* count) {
+    return guard([&] {
+        const int64_t n = int64_t(bs->events.size());
+        for (int64_t i = 0; i < std::min(n, capacity); ++i) out[i] = bs->events[size_t(i)];
+        if (count) *count = n;
+    });
+}
+
+int asg_synchronize(asg_blockset* bs) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        CK(cudaStreamSynchronize(bs->main));
+        CK(cudaStreamSynchronize(bs->side));
+        check_flag(bs);
+    });
+}
+
+// ---- per-block parity entry points ------------------------------------------
+int asg_block_read(asg_blockset* bs, int64_t idx, int32_t role, double* out, int64_t count) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        Group& g = owned_group(bs, u);
+        CK(cudaStreamSynchronize(bs->main));
+        CK(cudaStreamSynchronize(bs->side));
+        const int m = g.m, n = g.n;
+        auto rd32 = [&](const float* base, size_t stride, int R, int Cc, int rows, int cols, const float* lo) {
+            if (count < int64_t(rows) * cols) throw Fail{ASG_ERR_SHAPE_MISMATCH, "output too small"};
+            if (!base) throw Fail{ASG_ERR_INVALID_ARGUMENT, "role not held by this method"};
+            std::vector<float> h(size_t(R) * Cc), l;
+            CK(cudaMemcpy(h.data(), base + stride * u.slot, h.size() * 4, cudaMemcpyDeviceToHost));
+            if (lo) {
+                l.resize(h.size());
+                CK(cudaMemcpy(l.data(), lo + stride * u.slot, l.size() * 4, cudaMemcpyDeviceToHost));
+            }
+            for (int i = 0; i < rows; ++i)
+                for (int j = 0; j < cols; ++j)
+                    out[size_t(i) * cols + j] = double(h[size_t(i) * Cc + j]) + (lo ? double(l[size_t(i) * Cc + j]) : 0.0);
+        };
+        auto rd64 = [&](const double* base, size_t stride, size_t cnt) {
+            if (count < int64_t(cnt)) throw Fail{ASG_ERR_SHAPE_MISMATCH, "output too small"};
+            if (!base) throw Fail{ASG_ERR_INVALID_ARGUMENT, "role not held by this method"};
+            CK(cudaMemcpy(out, base + stride * u.slot, cnt * 8, cudaMemcpyDeviceToHost));
+        };
+        switch (role) {
+            case ASG_ROLE_FACTOR_L: rd32(g.L, slabMM(g), g.M, g.M, m, m, nullptr); break;
+            case ASG_ROLE_FACTOR_R: rd32(g.R, slabNN(g), g.N, g.N, n, n, nullptr); break;
+            case ASG_ROLE_INV_L: rd32(g.PLh, slabMM(g), g.M, g.M, m, m, g.PLl); break;
+            case ASG_ROLE_INV_R: rd32(g.PRh, slabNN(g), g.N, g.N, n, n, g.PRl); break;
+            case ASG_ROLE_KL_INV_L: rd32(g.KLh, slabMM(g), g.M, g.M, m, m, g.KLl); break;
+            case ASG_ROLE_KL_INV_R: rd32(g.KRh, slabNN(g), g.N, g.N, n, n, g.KRl); break;
+            case ASG_ROLE_BASIS_L: rd64(g.QL64, size_t(m) * m, size_t(m) * m); break;
+            case ASG_ROLE_BASIS_R: rd64(g.QR64, size_t(n) * n, size_t(n) * n); break;
+            case ASG_ROLE_EIGVALS_L: rd64(g.valsL, size_t(m), size_t(m)); break;
+            case ASG_ROLE_EIGVALS_R: rd64(g.valsR, size_t(n), size_t(n)); break;
+            case ASG_ROLE_ROTATED_M: rd32(g.mom_m, slabMN(g), g.M, g.N, m, n, nullptr); break;
+            case ASG_ROLE_ROTATED_V: rd32(g.mom_v, slabMN(g), g.M, g.N, m, n, nullptr); break;
+            default: throw Fail{ASG_ERR_INVALID_ARGUMENT, "unknown role"};
+        }
+    });
+}
+
+int asg_block_write(asg_blockset* bs, int64_t idx, int32_t role, const double* in, int64_t count) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        Group& g = owned_group(bs, u);
+        CK(cudaStreamSynchronize(bs->main));
+        CK(cudaStreamSynchronize(bs->side));
+        const int m = g.m, n = g.n;
+        auto wr32 = [&](float* base, size_t stride, int R, int Cc, int rows, int cols, float* lo, float* hi_t, float* lo_t) {
+            if (count < int64_t(rows) * cols) throw Fail{ASG_ERR_SHAPE_MISMATCH, "input too small"};
+            if (!base) throw Fail{ASG_ERR_INVALID_ARGUMENT, "role not held by this method"};
+            std::vector<double> buf(size_t(rows) * cols);
+            std::memcpy(buf.data(), in, buf.size() * 8);
+            double* d = bs->ws_out ? bs->ws_out : nullptr;
+            if (!d || size_t(rows) * cols > size_t(bs->ws_n) * bs->ws_n) throw Fail{ASG_ERR_INVALID_ARGUMENT, "no staging space"};
+            h2d(d, buf.data(), buf.size() * 8, bs->main);
+            if (lo || hi_t) {
+                launch_f64_to_split(d, 1, rows, R, false, base + stride * u.slot, lo ? lo + stride * u.slot : nullptr,
+                                    hi_t ? hi_t + stride * u.slot : nullptr, lo_t ? lo_t + stride * u.slot : nullptr,
+                                    bs->main);
+                if (!lo && !hi_t) {
+                }
+            } else {
+                launch_f64_to_f32(d, 1, rows, cols, base + stride * u.slot, R, Cc, bs->main);
+            }
+            CK(cudaStreamSynchronize(bs->main));
+        };
+        auto wr64 = [&](double* base, size_t stride, size_t cnt) {
+            if (count < int64_t(cnt)) throw Fail{ASG_ERR_SHAPE_MISMATCH, "input too small"};
+            if (!base) throw Fail{ASG_ERR_INVALID_ARGUMENT, "role not held by this method"};
+            h2d(base + stride * u.slot, in, cnt * 8, bs->main);
+        };
+        const bool sp = split_mode(bs);
+        switch (role) {
+            case ASG_ROLE_FACTOR_L: wr32(g.L, slabMM(g), g.M, g.M, m, m, nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_FACTOR_R: wr32(g.R, slabNN(g), g.N, g.N, n, n, nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_INV_L: wr32(g.PLh, slabMM(g), g.M, g.M, m, m, sp ? g.PLl : nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_INV_R: wr32(g.PRh, slabNN(g), g.N, g.N, n, n, sp ? g.PRl : nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_KL_INV_L: wr32(g.KLh, slabMM(g), g.M, g.M, m, m, sp ? g.KLl : nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_KL_INV_R: wr32(g.KRh, slabNN(g), g.N, g.N, n, n, sp ? g.KRl : nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_BASIS_L:
+                wr64(g.QL64, size_t(m) * m, size_t(m) * m);
+                launch_f64_to_split(g.QL64 + size_t(m) * m * u.slot, 1, m, g.M, false, g.QLh + slabMM(g) * u.slot,
+                                    sp ? g.QLl + slabMM(g) * u.slot : nullptr, g.QLTh + slabMM(g) * u.slot,
+                                    sp ? g.QLTl + slabMM(g) * u.slot : nullptr, bs->main);
+                break;
+            case ASG_ROLE_BASIS_R:
+                wr64(g.QR64, size_t(n) * n, size_t(n) * n);
+                launch_f64_to_split(g.QR64 + size_t(n) * n * u.slot, 1, n, g.N, false, g.QRh + slabNN(g) * u.slot,
+                                    sp ? g.QRl + slabNN(g) * u.slot : nullptr, g.QRTh + slabNN(g) * u.slot,
+                                    sp ? g.QRTl + slabNN(g) * u.slot : nullptr, bs->main);
+                break;
+            case ASG_ROLE_EIGVALS_L: wr64(g.valsL, size_t(m), size_t(m)); break;
+            case ASG_ROLE_EIGVALS_R: wr64(g.valsR, size_t(n), size_t(n)); break;
+            case ASG_ROLE_ROTATED_M: wr32(g.mom_m, slabMN(g), g.M, g.N, m, n, nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_ROTATED_V: wr32(g.mom_v, slabMN(g), g.M, g.N, m, n, nullptr, nullptr, nullptr); break;
+            default: throw Fail{ASG_ERR_INVALID_ARGUMENT, "unknown role"};
+        }
+        CK(cudaStreamSynchronize(bs->main));
+    });
+}
+
+int asg_block_set_counters(asg_blockset* bs, int64_t idx, uint64_t version, int64_t last_refresh_step, int64_t moment_steps) {
+    return guard([&] {
+        check_owned_index(bs, idx);
+        Unit& u = bs->units[size_t(idx)];
+        u.version = version;
+        u.last_refresh_step = last_refresh_step;
+        u.moment_steps = moment_steps;
+    });
+}
+
+int asg_block_accumulate_f64(asg_blockset* bs, int64_t idx, const double* g, int64_t ld) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        Group& gr = owned_group(bs, u);
+        stage_host_grad(bs, u, g, ld);
+        prep_single(bs, gr, u);
+        group_stats(bs, gr, u.slot, 1, bs->main);
+        CK(cudaStreamSynchronize(bs->main));
+    });
+}
+
+int asg_block_refresh_f64(asg_blockset* bs, int64_t idx, int64_t step) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, idx);
+        Unit& u = bs->units[size_t(idx)];
+        owned_group(bs, u);
+        if (u.pending) throw Fail{ASG_ERR_INVALID_ARGUMENT, "block has a pending scheduled refresh"};
+        u.pending = true;
+        u.launched = false;
+        launch_refreshes(bs);
+        try {
+            install_device(bs, u);
+        } catch (...) {
+            u.pending = false;
+            u.launched = false;
+            throw;
+        }
+        u.pending = false;
+        u.launched = false;
+        u.version += 1;  // install_refresh precond.cpp:162-163
+        u.last_refresh_step = step;
+        CK(cudaStreamSynchronize(bs->main));
+    });
+}
+
+int asg_block_precondition_f64(asg_blockset* bs, int64_t idx, const double* g, int64_t ld, double* out) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        Group& gr = owned_group(bs, u);
+        if (is_soap(bs)) throw Fail{ASG_ERR_INVALID_ARGUMENT, "use asg_block_soap_step_f64 for SOAP"};
+        if (u.version == 0)  // precond.cpp:192-194
+            throw Fail{ASG_ERR_STALE_UNINITIALIZED, "precondition_shampoo: no inverse installed"};
+        stage_host_grad(bs, u, g, ld);
+        prep_single(bs, gr, u);
+        group_update(bs, gr, u.slot, 1, EPI_STORE, 0.f, nullptr, bs->d_out1, bs->main);
+        download_block(bs, gr, out);
+    });
+}
+
+int asg_block_soap_step_f64(asg_blockset* bs, int64_t idx, const double* g, int64_t ld, double* out) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, idx);
+        Unit& u = bs->units[size_t(idx)];
+        Group& gr = owned_group(bs, u);
+        if (!is_soap(bs)) throw Fail{ASG_ERR_INVALID_ARGUMENT, "not a SOAP blockset"};
+        stage_host_grad(bs, u, g, ld);
+        prep_single(bs, gr, u);
+        u.moment_steps += 1;  // precond.cpp:213
+        group_update(bs, gr, u.slot, 1, EPI_STORE, 0.f, nullptr, bs->d_out1, bs->main);
+        download_block(bs, gr, out);
+    });
+}
+
+// ---- multi-GPU --------------------------------------------------------------
+int asg_shard_elems(const asg_blockset* bs, int32_t rank, int64_t* elems) {
+    return guard([&] {
+        if (rank < 0 || rank >= bs->world) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad rank"};
+        *elems = bs->shard_elems[size_t(rank)];
+    });
+}
+
+int asg_pack_owned(asg_blockset* bs, float* sendbuf, void* stream) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        launch_pack_blocks(bs->d_pack_refs, bs->d_pack_offs, bs->n_pack, sendbuf, s);
+        CK(cudaGetLastError());
+    });
+}
+
+int asg_unpack_gathered(asg_blockset* bs, const float* recvbuf, int64_t stride_elems, void* stream) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        // offsets are within each rank's shard; ranks are `stride_elems` apart
+        std::vector<int64_t> offs(size_t(bs->n_unpack));
+        std::vector<int64_t> host_offs(size_t(bs->n_unpack));
+        if (bs->n_unpack > 0)
+            CK(cudaMemcpy(host_offs.data(), bs->d_unpack_offs, host_offs.size() * 8, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < bs->n_unpack; ++i)
+            offs[size_t(i)] = int64_t(bs->unpack_rank[size_t(i)]) * stride_elems + host_offs[size_t(i)];
+        int64_t* d_offs = nullptr;
+        if (bs->n_unpack > 0) {
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&d_offs), offs.size() * 8, s));
+            CK(cudaMemcpyAsync(d_offs, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, s));
+            launch_unpack_blocks(bs->d_unpack_refs, d_offs, bs->n_unpack, recvbuf, s);
+            CK(cudaFreeAsync(d_offs, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        CK(cudaGetLastError());
+    });
+}
+
+// ---- diagnostics ------------------------------------------------------------
+int asg_gemm_tn(const float* A, const float* B, float* C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
+                float beta, int32_t precision, void* stream) {
+    return guard([&] {
+        if (M % 128 || N % 128 || K % 32 || batch < 1) throw Fail{ASG_ERR_SHAPE_MISMATCH, "M,N % 128 and K % 32 required"};
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        if (!asg_device_supported(dev)) throw Fail{ASG_ERR_UNSUPPORTED, "device is not sm_100"};
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, dev));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const bool sp = precision == ASG_PREC_3XTF32;
+        // split operands into (hi, lo) slabs
+        float *Ah = nullptr, *Al = nullptr, *Bh = nullptr, *Bl = nullptr;
+        const size_t na = size_t(batch) * M * K, nbb = size_t(batch) * N * K;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&Ah), na * 4, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&Bh), nbb * 4, s));
+        if (sp) {
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&Al), na * 4, s));
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&Bl), nbb * 4, s));
+        }
+        // reuse prep (identity scale, no transpose needed: write the transposes into scratch)
+        float *scrA = nullptr, *scrB = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&scrA), na * 4 * (sp ? 2 : 1), s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&scrB), nbb * 4 * (sp ? 2 : 1), s));
+        std::vector<BlockRef> ra(static_cast<size_t>(batch)), rb(static_cast<size_t>(batch));
+        for (int64_t b = 0; b < batch; ++b) {
+            ra[size_t(b)] = BlockRef{A + b * M * K, nullptr, K, int32_t(M), int32_t(K)};
+            rb[size_t(b)] = BlockRef{B + b * N * K, nullptr, K, int32_t(N), int32_t(K)};
+        }
+        BlockRef *dra = nullptr, *drb = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&dra), ra.size() * sizeof(BlockRef), s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&drb), rb.size() * sizeof(BlockRef), s));
+        CK(cudaMemcpyAsync(dra, ra.data(), ra.size() * sizeof(BlockRef), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(drb, rb.data(), rb.size() * sizeof(BlockRef), cudaMemcpyHostToDevice, s));
+        launch_prep_grad(dra, int(batch), int(M), int(K), nullptr, 1.f, Ah, Al, scrA, sp ? scrA + na : nullptr, s);
+        launch_prep_grad(drb, int(batch), int(N), int(K), nullptr, 1.f, Bh, Bl, scrB, sp ? scrB + nbb : nullptr, s);
+        GemmLaunch g{};
+        g.A = Operand{Ah, Al, int(M), int(K)};
+        g.B = Operand{Bh, Bl, int(N), int(K)};
+        g.batch = int(batch);
+        g.epi = EPI_STORE;
+        g.p.alpha = alpha;
+        g.p.beta = beta;
+        g.p.C = C;
+        g.p.ldc = N;
+        g.p.c_bstride = M * N;
+        CK(gemm_launch(g, precision, prop.multiProcessorCount, s));
+        CK(cudaStreamSynchronize(s));
+        for (void* p : {static_cast<void*>(Ah), static_cast<void*>(Al), static_cast<void*>(Bh), static_cast<void*>(Bl),
+                        static_cast<void*>(scrA), static_cast<void*>(scrB), static_cast<void*>(dra), static_cast<void*>(drb)})
+            if (p) CK(cudaFreeAsync(p, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int asg_sym_eig_batched(const double* A, double* values, double* vectors, int64_t batch, int64_t n, void* stream) {
+    return guard([&] {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        double* work = nullptr;
+        int* status = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&work), size_t(batch) * n * n * 8, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&status), size_t(batch) * sizeof(int), s));
+        CK(cudaMemsetAsync(status, 0, size_t(batch) * sizeof(int), s));
+        launch_sym_eig(A, values, vectors, work, int(batch), int(n), status, s);
+        std::vector<int> st(static_cast<size_t>(batch));
+        CK(cudaMemcpyAsync(st.data(), status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaFreeAsync(work, s));
+        CK(cudaFreeAsync(status, s));
+        CK(cudaStreamSynchronize(s));
+        for (int v : st)
+            if (v != ASG_OK) throw Fail{v, "sym_eig_batched: a matrix failed"};
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Torch-facing front end: one optimizer step over a list of fp32 CUDA
+parameters, plus the owner-major parameter all-gather for block-sharded
+multi-GPU runs.
+
+PyTorch here is plumbing (device memory, streams, torch.distributed/NCCL);
+every FLOP of the step runs in libasteria_b200.so.
+"""
+import ctypes as C
+
+from . import abi
+from .runtime import check, lib
+
+
+class AsteriaOptimizer:
+    """Shampoo / SOAP / KL-Shampoo step (harness.cpp:439-475 call order) over
+    `params` with gradients `grads` (both lists of contiguous fp32 CUDA
+    tensors of matching shapes; 1-D tensors are treated as 1 x n rows and get
+    AdamW, harness.cpp:352)."""
+
+    def __init__(self, params, grads, opt_cfg, sched_cfg=None, precision=abi.PREC_3XTF32,
+                 rank=0, world=1, seed=1):
+        import torch
+        self.params, self.grads = list(params), list(grads)
+        self.device = self.params[0].device
+        for p, g in zip(self.params, self.grads):
+            if p.dtype != torch.float32 or g.dtype != torch.float32 or not p.is_cuda or not g.is_cuda:
+                raise abi.InvalidArgumentError("parameters and gradients must be fp32 CUDA tensors")
+            if not p.is_contiguous() or not g.is_contiguous() or p.shape != g.shape:
+                raise abi.ShapeMismatchError("parameters/gradients must be contiguous and shape-matched")
+        self.opt = opt_cfg.copy()
+        self.sched = (sched_cfg.copy() if sched_cfg is not None else abi.scheduler_defaults())
+        self.sched.pf = self.opt.precondition_frequency
+        self.rank, self.world = rank, world
+        descs = (abi.ParamDesc * len(self.params))()
+        for i, (p, g) in enumerate(zip(self.params, self.grads)):
+            rows, cols = (p.shape[0], p.numel() // p.shape[0]) if p.dim() >= 2 else (1, p.numel())
+            descs[i] = abi.ParamDesc(p.data_ptr(), g.data_ptr(), rows, cols, cols, cols)
+        self._descs = descs
+        h = C.c_void_p()
+        check(lib.asg_blockset_create(self.device.index or 0, C.byref(self.opt), C.byref(self.sched), descs,
+                                      len(self.params), precision, rank, world, seed, C.byref(h)))
+        self._h = h
+        s = C.c_void_p()
+        check(lib.asg_blockset_stream(h, C.byref(s)))
+        self.stream_handle = s.value
+        self._gather_buf = None
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.asg_blockset_destroy(self._h)
+            self._h = None
+
+    # ---- the step ----------------------------------------------------------
+    def grad_sqnorm(self):
+        v, f = C.c_double(), C.c_int32()
+        check(lib.asg_grad_sqnorm(self._h, None, C.byref(v), C.byref(f)))
+        if f.value:
+            raise abi.NonFiniteError("non-finite gradient")
+        return v.value
+
+    @staticmethod
+    def clip_scale_from_norm(norm, clip_norm=1.0):
+        """clip_scale (harness.cpp:219-223)."""
+        if norm <= clip_norm or norm == 0.0:
+            return 1.0
+        return clip_norm / norm
+
+    def step(self, step, clip_scale=1.0, lr_scale=1.0, stream=None):
+        """accumulate -> maybe_dispatch -> staleness_barrier -> precondition/apply
+        -> StepEnd for every owned block. `stream` (a torch.cuda.Stream or raw
+        handle) is ordered before and after the step."""
+        sh = getattr(stream, "cuda_stream", stream)
+        check(lib.asg_step(self._h, step, clip_scale, lr_scale, C.c_void_p(sh) if sh else None))
+
+    def synchronize(self):
+        check(lib.asg_synchronize(self._h))
+
+    def clock_advance(self, us):
+        check(lib.asg_clock_advance(self._h, us))
+
+    # ---- introspection -------------------------------------------------------
+    @property
+    def num_blocks(self):
+        n = C.c_int64()
+        check(lib.asg_blockset_num_blocks(self._h, C.byref(n)))
+        return n.value
+
+    def block_info(self, idx):
+        i = abi.BlockInfo()
+        check(lib.asg_blockset_block_info(self._h, idx, C.byref(i)))
+        return i
+
+    def stats(self):
+        s = abi.PoolStats()
+        check(lib.asg_get_stats(self._h, C.byref(s)))
+        return s
+
+    def freshness(self, idx):
+        f = abi.Freshness()
+        check(lib.asg_get_freshness(self._h, idx, C.byref(f)))
+        return f
+
+    def events(self):
+        n = C.c_int64()
+        check(lib.asg_get_events(self._h, None, 0, C.byref(n)))
+        buf = (abi.Event * max(1, n.value))()
+        check(lib.asg_get_events(self._h, buf, n.value, C.byref(n)))
+        return [buf[i] for i in range(n.value)]
+
+    def state_bytes(self):
+        b = C.c_uint64()
+        check(lib.asg_blockset_state_bytes(self._h, C.byref(b)))
+        return b.value
+
+    # ---- multi-GPU ------------------------------------------------------------
+    def shard_elems(self, rank):
+        e = C.c_int64()
+        check(lib.asg_shard_elems(self._h, rank, C.byref(e)))
+        return e.value
+
+    def allgather(self, group=None, stream=None):
+        """All-gathers every rank's owned (updated) block slices of theta over
+        NCCL and scatters them back into the parameters (owner-major layout)."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        stride = max(self.shard_elems(r) for r in range(self.world))
+        if self._gather_buf is None:
+            self._gather_send = torch.zeros(stride, dtype=torch.float32, device=self.device)
+            self._gather_buf = torch.zeros(stride * self.world, dtype=torch.float32, device=self.device)
+        sh = getattr(stream, "cuda_stream", stream)
+        check(lib.asg_pack_owned(self._h, C.c_void_p(self._gather_send.data_ptr()), C.c_void_p(sh) if sh else None))
+        if sh is None:
+            # order torch's current stream after the blockset's main stream
+            torch.cuda.current_stream().wait_stream(torch.cuda.ExternalStream(self.stream_handle)) \
+                if hasattr(torch.cuda, "ExternalStream") else torch.cuda.synchronize()
+        dist.all_gather_into_tensor(self._gather_buf, self._gather_send, group=group)
+        check(lib.asg_unpack_gathered(self._h, C.c_void_p(self._gather_buf.data_ptr()), stride,
+                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))

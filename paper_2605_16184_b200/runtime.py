@@ -1,0 +1,114 @@
+# SPDX-License-Identifier: Apache-2.0
+"""ctypes binding of the product library (include/asteria_b200.h).
+
+Importing this module loads ``csrc/build/libasteria_b200.so`` and fails
+loudly if it is missing: there is no CPU fallback anywhere in the product.
+"""
+import ctypes as C
+import os
+
+from . import abi
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "csrc", "build", "libasteria_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(or `make -C paper_2605_16184_b200/csrc`). There is no CPU fallback.")
+
+lib = C.CDLL(LIB_PATH)
+
+_vp = C.c_void_p
+_i32, _i64, _u64, _f32, _f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
+_P = C.POINTER
+
+_SIGS = {
+    "asg_last_error": (C.c_char_p, []),
+    "asg_api_version": (C.c_int, []),
+    "asg_device_supported": (C.c_int, [C.c_int]),
+    "asg_optimizer_defaults": (C.c_int, [_i32, _P(abi.OptimizerConfig)]),
+    "asg_optimizer_validate": (C.c_int, [_P(abi.OptimizerConfig)]),
+    "asg_scheduler_defaults": (C.c_int, [_P(abi.SchedulerConfig)]),
+    "asg_config_from_json": (C.c_int, [C.c_char_p, _P(abi.OptimizerConfig), _P(abi.SchedulerConfig), _P(_i32)]),
+    "asg_partition_param": (C.c_int, [_i64, _i64, _i64, _i64, _P(abi.BlockSpec), _i64, _P(_i64)]),
+    "asg_blockset_create": (C.c_int, [C.c_int, _P(abi.OptimizerConfig), _P(abi.SchedulerConfig),
+                                      _P(abi.ParamDesc), _i64, _i32, _i32, _i32, _u64, _P(_vp)]),
+    "asg_blockset_destroy": (C.c_int, [_vp]),
+    "asg_blockset_bind_params": (C.c_int, [_vp, _P(abi.ParamDesc), _i64]),
+    "asg_blockset_num_blocks": (C.c_int, [_vp, _P(_i64)]),
+    "asg_blockset_block_info": (C.c_int, [_vp, _i64, _P(abi.BlockInfo)]),
+    "asg_blockset_state_bytes": (C.c_int, [_vp, _P(_u64)]),
+    "asg_blockset_stream": (C.c_int, [_vp, _P(_vp)]),
+    "asg_grad_sqnorm": (C.c_int, [_vp, _vp, _P(_f64), _P(_i32)]),
+    "asg_accumulate": (C.c_int, [_vp, _f64, _vp]),
+    "asg_maybe_dispatch": (C.c_int, [_vp, _i64, _P(_i64)]),
+    "asg_staleness_barrier": (C.c_int, [_vp, _i64, _P(_f64)]),
+    "asg_precondition_apply": (C.c_int, [_vp, _i64, _f64, _f64, _vp]),
+    "asg_step_end": (C.c_int, [_vp, _i64]),
+    "asg_step": (C.c_int, [_vp, _i64, _f64, _f64, _vp]),
+    "asg_clock_advance": (C.c_int, [_vp, _f64]),
+    "asg_get_freshness": (C.c_int, [_vp, _i64, _P(abi.Freshness)]),
+    "asg_get_stats": (C.c_int, [_vp, _P(abi.PoolStats)]),
+    "asg_get_events": (C.c_int, [_vp, _P(abi.Event), _i64, _P(_i64)]),
+    "asg_synchronize": (C.c_int, [_vp]),
+    "asg_block_read": (C.c_int, [_vp, _i64, _i32, _P(_f64), _i64]),
+    "asg_block_write": (C.c_int, [_vp, _i64, _i32, _P(_f64), _i64]),
+    "asg_block_set_counters": (C.c_int, [_vp, _i64, _u64, _i64, _i64]),
+    "asg_block_accumulate_f64": (C.c_int, [_vp, _i64, _P(_f64), _i64]),
+    "asg_block_refresh_f64": (C.c_int, [_vp, _i64, _i64]),
+    "asg_block_precondition_f64": (C.c_int, [_vp, _i64, _P(_f64), _i64, _P(_f64)]),
+    "asg_block_soap_step_f64": (C.c_int, [_vp, _i64, _P(_f64), _i64, _P(_f64)]),
+    "asg_shard_elems": (C.c_int, [_vp, _i32, _P(_i64)]),
+    "asg_pack_owned": (C.c_int, [_vp, _vp, _vp]),
+    "asg_unpack_gathered": (C.c_int, [_vp, _vp, _i64, _vp]),
+    "asg_gemm_tn": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _f32, _i32, _vp]),
+    "asg_sym_eig_batched": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def check(rc):
+    if rc != abi.ASG_OK:
+        abi.raise_for(rc, lib.asg_last_error().decode(errors="replace"))
+
+
+def device_supported(device=0):
+    return bool(lib.asg_device_supported(device))
+
+
+def optimizer_defaults(method):
+    c = abi.OptimizerConfig()
+    check(lib.asg_optimizer_defaults(method, C.byref(c)))
+    return c
+
+
+def validate(cfg):
+    check(lib.asg_optimizer_validate(C.byref(cfg)))
+
+
+def scheduler_defaults():
+    s = abi.SchedulerConfig()
+    check(lib.asg_scheduler_defaults(C.byref(s)))
+    return s
+
+
+def config_from_json(text):
+    """(OptimizerConfig, SchedulerConfig, precision) from a RunConfig JSON string."""
+    o, s, p = abi.OptimizerConfig(), abi.SchedulerConfig(), _i32()
+    check(lib.asg_config_from_json(text.encode(), C.byref(o), C.byref(s), C.byref(p)))
+    return o, s, p.value
+
+
+def partition_param(rows, cols, limit, param_index=0):
+    n = _i64()
+    check(lib.asg_partition_param(param_index, rows, cols, limit, None, 0, C.byref(n)))
+    out = (abi.BlockSpec * max(1, n.value))()
+    check(lib.asg_partition_param(param_index, rows, cols, limit, out, n.value, C.byref(n)))
+    return [out[i] for i in range(n.value)]

