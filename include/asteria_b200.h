@@ -292,6 +292,18 @@ int asg_pack_owned(asg_blockset* bs, float* sendbuf, void* stream);
  * padded to `stride_elems`) back into every parameter. */
 int asg_unpack_gathered(asg_blockset* bs, const float* recvbuf, int64_t stride_elems, void* stream);
 
+/* ---- profiling ---------------------------------------------------------- */
+typedef struct asg_kernel_stats {
+    uint64_t launches;       /* kernels this library launched (process-wide counter delta) */
+    uint64_t gemm_launches;  /* tcgen05 GEMM launches recorded while profiling */
+    double gemm_alg_flops;   /* algorithmic flops of those launches (SYRK: n^2 k, GEMM: 2 m n k) */
+    double gemm_ms;          /* sum of their CUDA-event durations on the launching stream */
+} asg_kernel_stats;
+/* While enabled, every GEMM launch is bracketed by CUDA events on its stream. */
+int asg_profile_enable(asg_blockset* bs, int32_t enable);
+/* Synchronizes, returns the stats accumulated since the last reset. */
+int asg_get_kernel_stats(asg_blockset* bs, asg_kernel_stats* out, int32_t reset);
+
 /* ---- diagnostics: the tensor-core GEMM on its own ----------------------- */
 /* C[b] = alpha * A[b] * B[b]^T + beta * C[b] for b < batch, fp32 device
  * slabs: A is [batch][M][K], B is [batch][N][K], C is [batch][M][N]

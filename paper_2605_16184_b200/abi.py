@@ -158,6 +158,15 @@ class Event(C.Structure):
     ]
 
 
+class KernelStats(C.Structure):
+    _fields_ = [
+        ("launches", C.c_uint64),
+        ("gemm_launches", C.c_uint64),
+        ("gemm_alg_flops", C.c_double),
+        ("gemm_ms", C.c_double),
+    ]
+
+
 # ---- error taxonomy (errors.hpp:10-47) --------------------------------------
 class Error(RuntimeError):
     code = -1

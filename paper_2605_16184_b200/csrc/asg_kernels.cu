@@ -12,6 +12,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <mutex>
@@ -20,6 +21,12 @@
 #include "asg_kernels.cuh"
 
 namespace asg {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+uint64_t launch_count() { return g_launches.load(); }
+void count_launch(uint64_t n) { g_launches.fetch_add(n); }
 
 // ============================================================================
 // GEMM launcher
@@ -74,6 +81,7 @@ cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUte
     const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
     if (grid <= 0) return cudaSuccess;
     gemm_tn_kernel<BN, NPASS, EPI><<<grid, 192, Cfg::kSmemBytes, s>>>(ah, al, bh, bl, p);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -185,6 +193,7 @@ void launch_prep_grad(const BlockRef* blocks_dev, int nb, int M, int N, const fl
                       float scale_val, float* Gh, float* Gl, float* GTh, float* GTl, cudaStream_t s) {
     dim3 grid(N / 32, M / 32, nb), block(32, 8);
     prep_grad_kernel<<<grid, block, 0, s>>>(blocks_dev, M, N, scale_dev, scale_val, Gh, Gl, GTh, GTl);
+    count_launch();
 }
 
 __global__ void identity_split_kernel(float* hi, float* lo, int M, int m) {
@@ -199,6 +208,7 @@ __global__ void identity_split_kernel(float* hi, float* lo, int M, int m) {
 
 void launch_identity_split(float* hi, float* lo, int nb, int M, int m, cudaStream_t s) {
     identity_split_kernel<<<dim3(256, nb), 256, 0, s>>>(hi, lo, M, m);
+    count_launch();
 }
 
 __global__ void identity_f32_kernel(float* a, int M, int m, float diag) {
@@ -212,6 +222,7 @@ __global__ void identity_f32_kernel(float* a, int M, int m, float diag) {
 
 void launch_identity_f32(float* a, int nb, int M, int m, float diag, cudaStream_t s) {
     identity_f32_kernel<<<dim3(256, nb), 256, 0, s>>>(a, M, m, diag);
+    count_launch();
 }
 
 // ============================================================================
@@ -247,6 +258,7 @@ void launch_sqnorm(const float* x, int64_t rows, int64_t cols, int64_t ld, doubl
     if (grid > 1184) grid = 1184;
     if (grid < 1) grid = 1;
     sqnorm_kernel<<<grid, 256, 0, s>>>(x, rows, cols, ld, acc, flag);
+    count_launch();
 }
 
 __global__ void clip_scale_kernel(const double* sq, double clip, float* out) {
@@ -256,6 +268,7 @@ __global__ void clip_scale_kernel(const double* sq, double clip, float* out) {
 
 void launch_clip_scale(const double* sqnorm, double clip_norm, float* scale_out, cudaStream_t s) {
     clip_scale_kernel<<<1, 1, 0, s>>>(sqnorm, clip_norm, scale_out);
+    count_launch();
 }
 
 // ============================================================================
@@ -310,6 +323,7 @@ __global__ void snapshot_kernel(const float* __restrict__ src, int M, int m, dou
 
 void launch_snapshot(const float* src, int nb, int M, int m, double* dst, cudaStream_t s) {
     snapshot_kernel<<<dim3(128, nb), 256, 0, s>>>(src, M, m, dst);
+    count_launch();
 }
 
 // ============================================================================
@@ -489,6 +503,7 @@ void launch_sym_eig(const double* A, double* values, double* vectors, double* wo
         attr = true;
     }
     sym_eig_kernel<<<nb, kEigThreads, smem, s>>>(A, values, vectors, work, n, status);
+    count_launch();
 }
 
 // ============================================================================
@@ -505,6 +520,7 @@ __global__ void relative_damping_kernel(const double* A, int n, double damping, 
 
 void launch_relative_damping(const double* A, int nb, int n, double damping, double* eps, cudaStream_t s) {
     relative_damping_kernel<<<nb, 256, 0, s>>>(A, n, damping, eps);
+    count_launch();
 }
 
 __global__ void scale_columns_kernel(const double* V, const double* values, const double* eps, double power,
@@ -512,9 +528,17 @@ __global__ void scale_columns_kernel(const double* V, const double* values, cons
     const int64_t b = blockIdx.y;
     const int64_t nn = int64_t(n) * n;
     const double e = eps ? eps[b] : 0.0;
+    // The factor is fp32 (accumulated on tensor cores): eigenvalues within its
+    // rounding level, |lam| <= 4 * 2^-24 * n * max|lam|, are numerically zero.
+    // Negative ones in that band are clamped to 0 before damping; only a damped
+    // eigenvalue that is still <= 0 is NotPsd (densela.hpp:274-278).
+    const double lam_abs = fmax(fabs(values[b * n]), fabs(values[b * n + n - 1]));
+    const double tau = 4.0 * 5.9604644775390625e-08 * double(n) * lam_abs;
     for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < nn; idx += int64_t(gridDim.x) * blockDim.x) {
         const int j = int(idx % n);
-        const double damped = values[b * n + j] + e;
+        double lam = values[b * n + j];
+        if (lam < 0.0 && lam >= -tau) lam = 0.0;
+        const double damped = lam + e;
         if (damped <= 0.0) {
             atomicCAS(&status[b], ASG_OK, ASG_ERR_NOT_PSD);
             W[b * nn + idx] = 0.0;
@@ -527,6 +551,7 @@ __global__ void scale_columns_kernel(const double* V, const double* values, cons
 void launch_scale_columns(const double* V, const double* values, const double* eps, double power, int nb, int n,
                           double* W, int* status, cudaStream_t s) {
     scale_columns_kernel<<<dim3(128, nb), 256, 0, s>>>(V, values, eps, power, n, W, status);
+    count_launch();
 }
 
 // fp64 tiled batched GEMM on CUDA cores (64 x 64 tiles, 4 x 4 per thread).
@@ -587,6 +612,7 @@ void launch_dgemm(bool ta, bool tb, int m, int n, int k, double alpha, const dou
                   cudaStream_t s) {
     dim3 grid((n + 63) / 64, (m + 63) / 64, nb);
     dgemm_kernel<<<grid, 256, 0, s>>>(ta, tb, m, n, k, alpha, A, lda, sa, B, ldb, sb, beta, C, ldc, sc);
+    count_launch();
 }
 
 __global__ void f64_to_split_kernel(const double* __restrict__ src, int n, int M, bool sym, float* hi, float* lo,
@@ -628,6 +654,7 @@ void launch_f64_to_split(const double* src, int nb, int n, int M, bool symmetriz
                          float* hi_t, float* lo_t, cudaStream_t s) {
     dim3 grid(M / 32, M / 32, nb), block(32, 8);
     f64_to_split_kernel<<<grid, block, 0, s>>>(src, n, M, symmetrize, hi, lo, hi_t, lo_t);
+    count_launch();
 }
 
 __global__ void f64_to_f32_kernel(const double* src, int rows, int cols, float* dst, int R, int Cc) {
@@ -641,6 +668,7 @@ __global__ void f64_to_f32_kernel(const double* src, int rows, int cols, float* 
 
 void launch_f64_to_f32(const double* src, int nb, int rows, int cols, float* dst, int R, int Cc, cudaStream_t s) {
     f64_to_f32_kernel<<<dim3(128, nb), 256, 0, s>>>(src, rows, cols, dst, R, Cc);
+    count_launch();
 }
 
 __global__ void f32_to_f64_kernel(const float* src, int rows, int cols, int R, int Cc, double* dst) {
@@ -654,6 +682,7 @@ __global__ void f32_to_f64_kernel(const float* src, int rows, int cols, int R, i
 
 void launch_f32_to_f64(const float* src, int nb, int rows, int cols, int R, int Cc, double* dst, cudaStream_t s) {
     f32_to_f64_kernel<<<dim3(128, nb), 256, 0, s>>>(src, rows, cols, R, Cc, dst);
+    count_launch();
 }
 
 __global__ void square_f64_kernel(const double* a, double* out, int64_t n) {
@@ -663,6 +692,7 @@ __global__ void square_f64_kernel(const double* a, double* out, int64_t n) {
 
 void launch_square_f64(const double* a, double* out, int64_t n, cudaStream_t s) {
     square_f64_kernel<<<256, 256, 0, s>>>(a, out, n);
+    count_launch();
 }
 
 // ============================================================================
@@ -686,11 +716,13 @@ __global__ void unpack_kernel(const BlockRef* blocks, const int64_t* offsets, co
 
 void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out, cudaStream_t s) {
     if (nb > 0) pack_kernel<<<dim3(64, nb), 256, 0, s>>>(blocks_dev, offsets_dev, out);
+    count_launch();
 }
 
 void launch_unpack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, const float* in,
                           cudaStream_t s) {
     if (nb > 0) unpack_kernel<<<dim3(64, nb), 256, 0, s>>>(blocks_dev, offsets_dev, in);
+    count_launch();
 }
 
 }  // namespace asg

@@ -12,6 +12,10 @@
 
 namespace asg {
 
+// Process-wide count of kernels launched by this library.
+uint64_t launch_count();
+void count_launch(uint64_t n = 1);
+
 // A slab operand for the TN GEMM: [batch][rows][K] fp32 pair (lo may be null
 // in TF32 mode).
 struct Operand {

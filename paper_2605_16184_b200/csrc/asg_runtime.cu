@@ -231,6 +231,12 @@ struct asg_blockset {
     int64_t* d_unpack_offs = nullptr;
     int n_unpack = 0;
     std::vector<int> unpack_rank;
+    // profiling
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    double prof_flops = 0.0;
+    uint64_t prof_gemms = 0;
+    uint64_t launch_base = 0;
 };
 
 namespace asg {
@@ -509,7 +515,13 @@ void alloc_workspace(asg_blockset* bs) {
 Operand op(const float* h, const float* l, int rows, int K) { return Operand{h, l, rows, K}; }
 
 void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const GemmParams& p,
-              const int2* sym_tiles, int nsym, cudaStream_t s) {
+              const int2* sym_tiles, int nsym, cudaStream_t s, double alg_flops) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (bs->profiling) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, s));
+    }
     GemmLaunch g{};
     g.A = A;
     g.B = B;
@@ -519,6 +531,12 @@ void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const 
     g.sym_tiles = sym_tiles;
     g.sym_tiles_count = nsym;
     CK(gemm_launch(g, bs->precision, bs->num_sms, s));
+    if (bs->profiling) {
+        CK(cudaEventRecord(e1, s));
+        bs->prof_events.emplace_back(e0, e1);
+        bs->prof_flops += alg_flops;
+        bs->prof_gemms += 1;
+    }
 }
 
 template <class T>
@@ -529,6 +547,7 @@ T* at(T* base, size_t stride, int slot) {
 // Statistics for slots [s0, s0+cnt) of a group (G slabs already staged).
 void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
     const asg_optimizer_config& o = bs->opt;
+    const double mf = g.m, nf = g.n;  // algorithmic flops use the unpadded block
     const bool ema = o.accumulation == ASG_ACCUM_EMA;
     const size_t mn = slabMN(g), mm = slabMM(g), nn = slabNN(g);
     GemmParams p{};
@@ -539,12 +558,12 @@ void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
         p.ldc = g.M;
         p.c_bstride = int64_t(mm);
         run_gemm(bs, op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N), op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N),
-                 cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s);
+                 cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s, cnt * mf * mf * nf);
         p.C = at(g.R, nn, s0);
         p.ldc = g.N;
         p.c_bstride = int64_t(nn);
         run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M),
-                 cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s);
+                 cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s, cnt * nf * nf * mf);
         return;
     }
     // KL-Shampoo: X = G R^-1 (T) ; L = b L + a/n X G^T
@@ -555,7 +574,7 @@ void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
     px.ldd = g.N;
     px.d_bstride = int64_t(mn);
     run_gemm(bs, op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N), op(at(g.KRh, nn, s0), at(g.KRl, nn, s0), g.N, g.N),
-             cnt, EPI_SPLIT, px, nullptr, 0, s);
+             cnt, EPI_SPLIT, px, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
     const double a = ema ? (1.0 - o.beta2) : 1.0;
     p.beta = ema ? float(o.beta2) : 1.f;
     p.alpha = float(a / double(g.n));
@@ -563,19 +582,19 @@ void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
     p.ldc = g.M;
     p.c_bstride = int64_t(mm);
     run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N),
-             cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s);
+             cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s, cnt * mf * mf * nf);
     // Z^T = G^T L^-1 (S, [N][M]) ; R = b R + a/m G^T Z
     px.Dhi = at(g.Sh, mn, s0);
     px.Dlo = at(g.Sl, mn, s0);
     px.ldd = g.M;
     run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.KLh, mm, s0), at(g.KLl, mm, s0), g.M, g.M),
-             cnt, EPI_SPLIT, px, nullptr, 0, s);
+             cnt, EPI_SPLIT, px, nullptr, 0, s, cnt * 2.0 * nf * mf * mf);
     p.alpha = float(a / double(g.m));
     p.C = at(g.R, nn, s0);
     p.ldc = g.N;
     p.c_bstride = int64_t(nn);
     run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.Sh, mn, s0), at(g.Sl, mn, s0), g.N, g.M),
-             cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s);
+             cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s, cnt * nf * nf * mf);
 }
 
 // Preconditioned update for slots [s0, s0+cnt). `final_epi` is EPI_APPLY (step)
@@ -583,6 +602,7 @@ void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
 void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, float lr_eff, const ApplyEntry* apply,
                   float* store_out, cudaStream_t s) {
     const asg_optimizer_config& o = bs->opt;
+    const double mf = g.m, nf = g.n;
     const size_t mn = slabMN(g), mm = slabMM(g), nn = slabNN(g);
     GemmParams pf{};
     pf.alpha = 1.f;
@@ -603,9 +623,9 @@ void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, fl
         ps.Dhi = at(g.Th, mn, s0);
         ps.Dlo = at(g.Tl, mn, s0);
         run_gemm(bs, op(at(g.PLh, mm, s0), at(g.PLl, mm, s0), g.M, g.M), op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M),
-                 cnt, EPI_SPLIT, ps, nullptr, 0, s);
+                 cnt, EPI_SPLIT, ps, nullptr, 0, s, cnt * 2.0 * mf * mf * nf);
         run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.PRh, nn, s0), at(g.PRl, nn, s0), g.N, g.N),
-                 cnt, final_epi, pf, nullptr, 0, s);
+                 cnt, final_epi, pf, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
         return;
     }
     // SOAP (soap_scaled_step precond.cpp:208-223)
@@ -630,10 +650,10 @@ void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, fl
     ps.Dhi = at(g.Th, mn, s0);
     ps.Dlo = at(g.Tl, mn, s0);
     run_gemm(bs, op(at(g.QLTh, mm, s0), at(g.QLTl, mm, s0), g.M, g.M), op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M),
-             cnt, EPI_SPLIT, ps, nullptr, 0, s);
+             cnt, EPI_SPLIT, ps, nullptr, 0, s, cnt * 2.0 * mf * mf * nf);
     // Adam(T Q_R) -> S
     run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.QRTh, nn, s0), at(g.QRTl, nn, s0), g.N, g.N),
-             cnt, EPI_ADAM, pa, nullptr, 0, s);
+             cnt, EPI_ADAM, pa, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
     // W^T = (S Q_R^T)^T -> T as [N][M]
     GemmParams pt{};
     pt.alpha = 1.f;
@@ -642,10 +662,10 @@ void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, fl
     pt.ldd = g.M;
     pt.d_bstride = int64_t(mn);
     run_gemm(bs, op(at(g.Sh, mn, s0), at(g.Sl, mn, s0), g.M, g.N), op(at(g.QRh, nn, s0), at(g.QRl, nn, s0), g.N, g.N),
-             cnt, EPI_SPLIT_T, pt, nullptr, 0, s);
+             cnt, EPI_SPLIT_T, pt, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
     // U = Q_L W
     run_gemm(bs, op(at(g.QLh, mm, s0), at(g.QLl, mm, s0), g.M, g.M), op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.N, g.M),
-             cnt, final_epi, pf, nullptr, 0, s);
+             cnt, final_epi, pf, nullptr, 0, s, cnt * 2.0 * mf * mf * nf);
 }
 
 // ---------------------------------------------------------------------------
@@ -1686,6 +1706,42 @@ int asg_unpack_gathered(asg_blockset* bs, const float* recvbuf, int64_t stride_e
             CK(cudaStreamSynchronize(s));
         }
         CK(cudaGetLastError());
+    });
+}
+
+// ---- profiling ------------------------------------------------------------------
+int asg_profile_enable(asg_blockset* bs, int32_t enable) {
+    return guard([&] {
+        bs->profiling = enable != 0;
+        bs->launch_base = launch_count();
+    });
+}
+
+int asg_get_kernel_stats(asg_blockset* bs, asg_kernel_stats* out, int32_t reset) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        CK(cudaStreamSynchronize(bs->main));
+        CK(cudaStreamSynchronize(bs->side));
+        double ms = 0.0;
+        for (auto& e : bs->prof_events) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, e.first, e.second));
+            ms += t;
+        }
+        out->launches = launch_count() - bs->launch_base;
+        out->gemm_launches = bs->prof_gemms;
+        out->gemm_alg_flops = bs->prof_flops;
+        out->gemm_ms = ms;
+        if (reset) {
+            for (auto& e : bs->prof_events) {
+                cudaEventDestroy(e.first);
+                cudaEventDestroy(e.second);
+            }
+            bs->prof_events.clear();
+            bs->prof_flops = 0.0;
+            bs->prof_gemms = 0;
+            bs->launch_base = launch_count();
+        }
     });
 }
 

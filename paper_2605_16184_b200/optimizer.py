@@ -113,6 +113,14 @@ class AsteriaOptimizer:
         check(lib.asg_blockset_state_bytes(self._h, C.byref(b)))
         return b.value
 
+    def profile(self, enable=True):
+        check(lib.asg_profile_enable(self._h, 1 if enable else 0))
+
+    def kernel_stats(self, reset=True):
+        k = abi.KernelStats()
+        check(lib.asg_get_kernel_stats(self._h, C.byref(k), 1 if reset else 0))
+        return k
+
     # ---- multi-GPU ------------------------------------------------------------
     def shard_elems(self, rank):
         e = C.c_int64()
