@@ -1,0 +1,31 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Batched symmetric eigensolver of the refresh (see asg_eigh.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace asg {
+
+// At or below this dimension the direct parallel-Jacobi kernel (one CTA per
+// matrix) is used; above it the batched block-Jacobi solver.
+constexpr int kSmallEighN = 64;
+// Sweeps enqueued per solve (converged matrices skip work device-side; the
+// reference's budget is 30, densela.hpp:194). Non-convergence -> status.
+constexpr int kEighMaxLaunchedSweeps = 30;
+
+// fp64 workspace needed by launch_eigh for nb matrices of dimension n
+// (cold start; `_warm` when an initial basis is passed).
+size_t eigh_workspace_doubles(int nb, int n);
+size_t eigh_workspace_doubles_warm(int nb, int n);
+// A: [nb][n][n] fp64 symmetric (not modified). values: [nb][n] ascending.
+// vectors: [nb][n][n], eigenvectors as columns. status: per-matrix asg_status
+// (must be zero-initialised; only failures are written). Vinit (optional,
+// [nb][n][n] orthogonal): warm start from a previous eigenbasis — the solve
+// iterates on Vinit^T A Vinit, which is nearly diagonal when A changed little.
+void launch_eigh(const double* A, double* values, double* vectors, double* ws, int nb, int n, int* status,
+                 cudaStream_t s, const double* Vinit = nullptr);
+
+}  // namespace asg

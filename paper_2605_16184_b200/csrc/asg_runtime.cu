@@ -36,6 +36,7 @@
 #include <vector>
 
 #include "../../include/asteria_b200.h"
+#include "asg_eigh.cuh"
 #include "asg_json.hpp"
 #include "asg_kernels.cuh"
 
@@ -149,6 +150,8 @@ struct Unit {
     int64_t dispatch_step = 0;
     double dispatch_sim = 0.0, completion_sim = 0.0;
     bool launched = false;  // refresh enqueued on the side stream
+    bool needs_launch = false;  // dispatched, refresh not yet enqueued
+    bool warm_start = false;    // a previous eigenbasis exists (decided at dispatch)
     cudaEvent_t done = nullptr;
     bool has_fresh = false;
     asg_freshness fresh{0, -1, -1, -1};
@@ -175,6 +178,8 @@ struct Group {
     float *mom_m = nullptr, *mom_v = nullptr;
     double *QL64 = nullptr, *QR64 = nullptr, *valsL = nullptr, *valsR = nullptr;
     double *sQL64 = nullptr, *sQR64 = nullptr, *svalsL = nullptr, *svalsR = nullptr;
+    // Shampoo / KL-Shampoo: eigenvectors of the last refresh (warm start of the next)
+    double *EL64 = nullptr, *ER64 = nullptr;
     BlockRef* d_refs = nullptr;
     ApplyEntry* d_apply = nullptr;
     int2 *tilesM = nullptr, *tilesN = nullptr;
@@ -231,6 +236,9 @@ struct asg_blockset {
     int64_t* d_unpack_offs = nullptr;
     int n_unpack = 0;
     std::vector<int> unpack_rank;
+    // installs decided by the schedule bookkeeping, executed after the
+    // step's refreshes are launched as one batch
+    std::vector<int> deferred_installs;
     // profiling
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -439,6 +447,8 @@ void alloc_group(asg_blockset* bs, Group& g) {
         pair_nn(g.sPRh, g.sPRl);
         launch_identity_split(g.PLh, g.PLl, g.nb, g.M, g.m, s);
         launch_identity_split(g.PRh, g.PRl, g.nb, g.N, g.n, s);
+        g.EL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
+        g.ER64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
         if (is_kl(bs)) {
             pair_mm(g.KLh, g.KLl);
             pair_nn(g.KRh, g.KRl);
@@ -484,7 +494,7 @@ void alloc_workspace(asg_blockset* bs) {
     }
     if (nmax == 0) return;
     // Chunk the refresh so its fp64 workspace stays ~<= 4 GiB.
-    const size_t per = size_t(nmax) * nmax * 8 * 5;
+    const size_t per = size_t(nmax) * nmax * 8 * 7;
     int chunk = int(std::max<size_t>(1, (size_t(4) << 30) / per));
     int maxnb = 0;
     for (const Group& g : bs->groups) maxnb = std::max(maxnb, g.nb);
@@ -493,7 +503,16 @@ void alloc_workspace(asg_blockset* bs) {
     const size_t nn = size_t(nmax) * nmax * size_t(bs->ws_chunk);
     bs->ws_snap = dalloc<double>(bs, nn);
     bs->ws_vecs = dalloc<double>(bs, nn);
-    bs->ws_work = dalloc<double>(bs, nn);
+    size_t ew = nn;
+    for (const Group& g : bs->groups) {
+        ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.m));
+        ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.n));
+    }
+    for (const Group& g : bs->groups) {
+        ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.m));
+        ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.n));
+    }
+    bs->ws_work = dalloc<double>(bs, ew);
     bs->ws_W = dalloc<double>(bs, nn);
     bs->ws_out = dalloc<double>(bs, nn);
     bs->ws_vals = dalloc<double>(bs, size_t(nmax) * bs->ws_chunk);
@@ -677,7 +696,17 @@ void refresh_side(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaSt
     const size_t DD = size_t(D) * D, dd = size_t(d) * d;
     const float* snap = at(left ? g.snapL : g.snapR, DD, s0);
     launch_snapshot(snap, cnt, D, d, bs->ws_snap, s);
-    launch_sym_eig(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, cnt, d, g.d_status + s0, s);
+    // Warm start from the block's previous eigenbasis once every block of the
+    // chunk has one (the result does not depend on the start; only the sweep
+    // count does).
+    bool warm = true;
+    for (int k = 0; k < cnt; ++k) warm &= bs->units[size_t(g.units[size_t(s0 + k)])].warm_start;
+    const double* prev = nullptr;
+    if (warm) prev = is_soap(bs) ? at(left ? g.QL64 : g.QR64, dd, s0) : at(left ? g.EL64 : g.ER64, dd, s0);
+    launch_eigh(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, cnt, d, g.d_status + s0, s, prev);
+    if (!is_soap(bs))
+        CK(cudaMemcpyAsync(at(left ? g.EL64 : g.ER64, dd, s0), bs->ws_vecs, size_t(cnt) * dd * 8,
+                           cudaMemcpyDeviceToDevice, s));
     if (is_soap(bs)) {
         CK(cudaMemcpyAsync(at(left ? g.sQL64 : g.sQR64, dd, s0), bs->ws_vecs, size_t(cnt) * dd * 8,
                            cudaMemcpyDeviceToDevice, s));
@@ -711,7 +740,7 @@ void launch_refreshes(asg_blockset* bs) {
     std::vector<std::vector<int>> per_group(bs->groups.size());
     for (size_t i = 0; i < bs->units.size(); ++i) {
         Unit& u = bs->units[i];
-        if (u.pending && !u.launched && u.group >= 0) per_group[size_t(u.group)].push_back(int(i));
+        if (u.needs_launch && u.group >= 0) per_group[size_t(u.group)].push_back(int(i));
     }
     bool any = false;
     for (auto& v : per_group) any |= !v.empty();
@@ -750,6 +779,7 @@ void launch_refreshes(asg_blockset* bs) {
                 Unit& u = bs->units[size_t(g.units[size_t(s0 + k)])];
                 CK(cudaEventRecord(u.done, bs->side));
                 u.launched = true;
+                u.needs_launch = false;
             }
             i = j;
         }
@@ -761,7 +791,7 @@ int status_to_code(int st) { return st; }
 
 // Device-side install of a finished refresh (install_refresh precond.cpp:144-164).
 void install_device(asg_blockset* bs, Unit& u) {
-    if (!u.launched) launch_refreshes(bs);
+    if (u.needs_launch) launch_refreshes(bs);
     Group& g = bs->groups[size_t(u.group)];
     CK(cudaEventSynchronize(u.done));
     const int st = g.h_status[u.slot];
@@ -832,13 +862,15 @@ void install_device(asg_blockset* bs, Unit& u) {
                         at(g.QRTl, nn, u.slot), s);
 }
 
-// ShadowScheduler::install (asyncsched.cpp:144-189) bookkeeping + device install.
+// ShadowScheduler::install (asyncsched.cpp:144-189): bookkeeping now (so the
+// simulated clock and trace follow the reference's per-block order), device
+// work deferred to run_deferred_installs().
 void sched_install(asg_blockset* bs, int idx, int64_t step) {
     Unit& u = bs->units[size_t(idx)];
     bs->stats.completed += 1;
     emit(bs, u.dispatch_step, ASG_EV_JOB_START, idx, u.version, u.dispatch_sim);
     emit(bs, step, ASG_EV_JOB_DONE, idx, u.version, u.completion_sim);
-    install_device(bs, u);
+    bs->deferred_installs.push_back(idx);
     u.version += 1;
     u.last_refresh_step = step;
     bs->now_us += bs->sc.install_cost_us;
@@ -847,9 +879,21 @@ void sched_install(asg_blockset* bs, int idx, int64_t step) {
     u.fresh.installed_snapshot_step = u.dispatch_step;
     u.fresh.dispatch_step_of_pending = -1;
     u.pending = false;
-    u.launched = false;
     emit(bs, step, ASG_EV_INSTALL, idx, u.version, bs->now_us);
     bs->stats.installed += 1;
+}
+
+// Launches every outstanding refresh as one batch, then performs the deferred
+// device installs in decision order (main stream, before the update).
+void run_deferred_installs(asg_blockset* bs) {
+    launch_refreshes(bs);
+    std::vector<int> todo;
+    todo.swap(bs->deferred_installs);
+    for (int idx : todo) {
+        Unit& u = bs->units[size_t(idx)];
+        install_device(bs, u);
+        u.launched = false;
+    }
 }
 
 // maybe_dispatch (asyncsched.cpp:108-142), host bookkeeping only.
@@ -867,6 +911,8 @@ bool sched_dispatch(asg_blockset* bs, int idx, int64_t step) {
     }
     u.pending = true;
     u.launched = false;
+    u.needs_launch = true;
+    u.warm_start = u.version > 0;  // before this job's own install bookkeeping
     u.dispatch_step = step;
     u.dispatch_sim = bs->now_us;
     u.completion_sim = bs->now_us + cost * bs->sc.step_compute_us;
@@ -917,6 +963,7 @@ void sched_step_end(asg_blockset* bs, int64_t step) {
         if (ok) ready.push_back(int(i));
     }
     for (int i : ready) sched_install(bs, i, step);
+    run_deferred_installs(bs);
 }
 
 void check_owned_index(const asg_blockset* bs, int64_t idx) {
@@ -1349,6 +1396,7 @@ int asg_staleness_barrier(asg_blockset* bs, int64_t step, double* waited_us) {
             if (u.adamw || u.owner != bs->rank) continue;
             w += sched_barrier(bs, int(i), step);
         }
+        run_deferred_installs(bs);
         if (waited_us) *waited_us = w;
     });
 }
@@ -1428,7 +1476,7 @@ int asg_step(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale,
             sched_dispatch(bs, int(i), step);
             sched_barrier(bs, int(i), step);
         }
-        launch_refreshes(bs);
+        run_deferred_installs(bs);
         precondition_apply_impl(bs, clip_scale, lr_scale);
         sched_step_end(bs, step);
         if (s != bs->main) {
@@ -1622,12 +1670,15 @@ int asg_block_refresh_f64(asg_blockset* bs, int64_t idx, int64_t step) {
         if (u.pending) throw Fail{ASG_ERR_INVALID_ARGUMENT, "block has a pending scheduled refresh"};
         u.pending = true;
         u.launched = false;
+        u.needs_launch = true;
+        u.warm_start = u.version > 0;
         launch_refreshes(bs);
         try {
             install_device(bs, u);
         } catch (...) {
             u.pending = false;
             u.launched = false;
+            u.needs_launch = false;
             throw;
         }
         u.pending = false;
@@ -1806,10 +1857,11 @@ int asg_sym_eig_batched(const double* A, double* values, double* vectors, int64_
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         double* work = nullptr;
         int* status = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&work), size_t(batch) * n * n * 8, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&work),
+                           std::max(size_t(batch) * n * n, eigh_workspace_doubles(int(batch), int(n))) * 8, s));
         CK(cudaMallocAsync(reinterpret_cast<void**>(&status), size_t(batch) * sizeof(int), s));
         CK(cudaMemsetAsync(status, 0, size_t(batch) * sizeof(int), s));
-        launch_sym_eig(A, values, vectors, work, int(batch), int(n), status, s);
+        launch_eigh(A, values, vectors, work, int(batch), int(n), status, s);
         std::vector<int> st(static_cast<size_t>(batch));
         CK(cudaMemcpyAsync(st.data(), status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
