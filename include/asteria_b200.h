@@ -284,6 +284,13 @@ int asg_block_soap_step_f64(asg_blockset* bs, int64_t idx, const double* g, int6
                             double* out);
 
 /* ---- multi-GPU: ownership sharding + parameter all-gather ---------------- */
+/* Host-only ownership plan (no device needed): partitions every parameter with
+ * opt->block_dim_limit (precond.cpp:69-82) and assigns each unit (block, or a
+ * whole 1-D AdamW parameter) to one of `world` ranks by LPT on its per-step
+ * cost. Units are enumerated exactly as asg_blockset_create does; owner[i]
+ * receives the rank of unit i (capacity >= *count). */
+int asg_plan_owners(const asg_optimizer_config* opt, const int64_t* rows, const int64_t* cols,
+                    int64_t n_params, int32_t world, int32_t* owner, int64_t capacity, int64_t* count);
 /* Elements of theta owned by `rank` (owner-major layout). */
 int asg_shard_elems(const asg_blockset* bs, int32_t rank, int64_t* elems);
 /* Packs this rank's owned block slices of theta into `sendbuf` (device). */

@@ -1721,6 +1721,27 @@ int asg_block_soap_step_f64(asg_blockset* bs, int64_t idx, const double* g, int6
 }
 
 // ---- multi-GPU --------------------------------------------------------------
+int asg_plan_owners(const asg_optimizer_config* opt, const int64_t* rows, const int64_t* cols, int64_t n_params,
+                    int32_t world, int32_t* owner, int64_t capacity, int64_t* count) {
+    return guard([&] {
+        if (!opt || (n_params > 0 && (!rows || !cols)) || world < 1) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad argument"};
+        validate(*opt);
+        asg_blockset tmp;  // host-side planning only: no device state is created
+        tmp.opt = *opt;
+        tmp.world = world;
+        tmp.rank = 0;
+        for (int64_t p = 0; p < n_params; ++p) {
+            asg_param_desc d{};
+            d.rows = rows[p];
+            d.cols = cols[p];
+            tmp.params.push_back(d);
+        }
+        build_units(&tmp);
+        if (count) *count = int64_t(tmp.units.size());
+        for (size_t i = 0; i < tmp.units.size() && int64_t(i) < capacity; ++i) owner[i] = tmp.units[i].owner;
+    });
+}
+
 int asg_shard_elems(const asg_blockset* bs, int32_t rank, int64_t* elems) {
     return guard([&] {
         if (rank < 0 || rank >= bs->world) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad rank"};

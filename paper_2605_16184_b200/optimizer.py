@@ -69,7 +69,12 @@ class AsteriaOptimizer:
     def step(self, step, clip_scale=1.0, lr_scale=1.0, stream=None):
         """accumulate -> maybe_dispatch -> staleness_barrier -> precondition/apply
         -> StepEnd for every owned block. `stream` (a torch.cuda.Stream or raw
-        handle) is ordered before and after the step."""
+        handle; default: torch's current stream, like any torch op) is ordered
+        before and after the step, so gradient writes issued on it before the
+        call and parameter reads issued after it are race-free."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(self.device)
         sh = getattr(stream, "cuda_stream", stream)
         check(lib.asg_step(self._h, step, clip_scale, lr_scale, C.c_void_p(sh) if sh else None))
 
@@ -128,8 +133,10 @@ class AsteriaOptimizer:
         return e.value
 
     def allgather(self, group=None, stream=None):
-        """All-gathers every rank's owned (updated) block slices of theta over
-        NCCL and scatters them back into the parameters (owner-major layout)."""
+        """All-gathers every rank's owned (updated) block slices of theta and
+        scatters them back into the parameters (owner-major layout). NCCL
+        groups gather in HBM; gloo groups (CPU test harness) stage through host
+        memory."""
         import torch
         import torch.distributed as dist
         if self.world == 1:
@@ -138,12 +145,15 @@ class AsteriaOptimizer:
         if self._gather_buf is None:
             self._gather_send = torch.zeros(stride, dtype=torch.float32, device=self.device)
             self._gather_buf = torch.zeros(stride * self.world, dtype=torch.float32, device=self.device)
-        sh = getattr(stream, "cuda_stream", stream)
-        check(lib.asg_pack_owned(self._h, C.c_void_p(self._gather_send.data_ptr()), C.c_void_p(sh) if sh else None))
-        if sh is None:
-            # order torch's current stream after the blockset's main stream
-            torch.cuda.current_stream().wait_stream(torch.cuda.ExternalStream(self.stream_handle)) \
-                if hasattr(torch.cuda, "ExternalStream") else torch.cuda.synchronize()
-        dist.all_gather_into_tensor(self._gather_buf, self._gather_send, group=group)
+        main = C.c_void_p(self.stream_handle)
+        check(lib.asg_pack_owned(self._h, C.c_void_p(self._gather_send.data_ptr()), main))
+        torch.cuda.current_stream(self.device).wait_stream(torch.cuda.ExternalStream(self.stream_handle))
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(self._gather_buf, self._gather_send, group=group)
+        else:
+            send = self._gather_send.cpu()
+            recv = torch.empty(stride * self.world, dtype=torch.float32)
+            dist.all_gather_into_tensor(recv, send, group=group)
+            self._gather_buf.copy_(recv)
         check(lib.asg_unpack_gathered(self._h, C.c_void_p(self._gather_buf.data_ptr()), stride,
-                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+                                      C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))

@@ -59,6 +59,7 @@ _SIGS = {
     "asg_block_refresh_f64": (C.c_int, [_vp, _i64, _i64]),
     "asg_block_precondition_f64": (C.c_int, [_vp, _i64, _P(_f64), _i64, _P(_f64)]),
     "asg_block_soap_step_f64": (C.c_int, [_vp, _i64, _P(_f64), _i64, _P(_f64)]),
+    "asg_plan_owners": (C.c_int, [_P(abi.OptimizerConfig), _P(_i64), _P(_i64), _i64, _i32, _P(_i32), _i64, _P(_i64)]),
     "asg_shard_elems": (C.c_int, [_vp, _i32, _P(_i64)]),
     "asg_pack_owned": (C.c_int, [_vp, _vp, _vp]),
     "asg_unpack_gathered": (C.c_int, [_vp, _vp, _i64, _vp]),
@@ -113,4 +114,15 @@ def partition_param(rows, cols, limit, param_index=0):
     check(lib.asg_partition_param(param_index, rows, cols, limit, None, 0, C.byref(n)))
     out = (abi.BlockSpec * max(1, n.value))()
     check(lib.asg_partition_param(param_index, rows, cols, limit, out, n.value, C.byref(n)))
+    return [out[i] for i in range(n.value)]
+
+
+def plan_owners(opt, shapes, world):
+    """Owner rank of every unit (block or 1-D AdamW parameter), LPT over `world`."""
+    rows = (C.c_int64 * max(1, len(shapes)))(*[s[0] if len(s) > 1 else 1 for s in shapes])
+    cols = (C.c_int64 * max(1, len(shapes)))(*[s[-1] if len(s) > 1 else s[0] for s in shapes])
+    n = _i64()
+    check(lib.asg_plan_owners(C.byref(opt), rows, cols, len(shapes), world, None, 0, C.byref(n)))
+    out = (C.c_int32 * max(1, n.value))()
+    check(lib.asg_plan_owners(C.byref(opt), rows, cols, len(shapes), world, out, n.value, C.byref(n)))
     return [out[i] for i in range(n.value)]
