@@ -17,7 +17,9 @@
  * owned by an asg_blockset and lives in HBM.
  *
  * Streams are passed as `void*` (a cudaStream_t) so this header does not pull
- * in the CUDA runtime headers. NULL means the blockset's own main stream.
+ * in the CUDA runtime headers. NULL means the blockset's own main stream (a
+ * non-blocking stream); to order with the legacy default stream pass
+ * cudaStreamLegacy ((void*)0x1), e.g. for torch's default stream (handle 0).
  */
 #ifndef ASTERIA_B200_H
 #define ASTERIA_B200_H

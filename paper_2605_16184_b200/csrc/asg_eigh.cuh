@@ -25,7 +25,15 @@ size_t eigh_workspace_doubles_warm(int nb, int n);
 // (must be zero-initialised; only failures are written). Vinit (optional,
 // [nb][n][n] orthogonal): warm start from a previous eigenbasis — the solve
 // iterates on Vinit^T A Vinit, which is nearly diagonal when A changed little.
+// Stopping rule: relative = 0 is the reference's off(A) <= 1e-12 ||A||_F
+// (densela.hpp:192-203); relative = 1 rotates only elements with
+// |a_ij| > tol * sqrt(a_ii a_jj), skips pairs without one, and stops after a
+// sweep that rotated nothing (the fp32-level refresh).
+struct EighOpts {
+    int relative = 0;
+    double tol = 0.0;
+};
 void launch_eigh(const double* A, double* values, double* vectors, double* ws, int nb, int n, int* status,
-                 cudaStream_t s, const double* Vinit = nullptr);
+                 cudaStream_t s, const double* Vinit = nullptr, EighOpts opts = EighOpts{});
 
 }  // namespace asg

@@ -76,10 +76,12 @@ struct GemmCfg {
     static constexpr uint32_t kABytes = BM * BK * 4;
     static constexpr uint32_t kBBytes = BN * BK * 4;
     static constexpr uint32_t kStageBytes = (kABytes + kBBytes) * (kSplit ? 2 : 1);
-    static constexpr int kStagesRaw = (216 * 1024) / kStageBytes;
+    // per-epilogue-warp 32 x 33 fp32 transpose scratch (coalesced apply)
+    static constexpr uint32_t kScratchBytes = 4 * 32 * 33 * 4;
+    static constexpr int kStagesRaw = (198 * 1024) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
-    static constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + 256;
+    static constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + 256 + kScratchBytes;
     static_assert(kStages >= 2, "need at least two pipeline stages");
     static_assert(kTmemCols == 256 || kTmemCols == 512, "TMEM allocation must be a power of two");
 };
@@ -198,23 +200,36 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int r
             *reinterpret_cast<float4*>(p.Dhi + doff + j) = h;
             *reinterpret_cast<float4*>(p.Dlo + doff + j) = l;
         }
-    } else if constexpr (EPI == EPI_APPLY) {
-        const ApplyEntry e = p.apply[b];
-        if (row >= e.rows) return;
-        float* th = e.theta + int64_t(row) * e.ld;
-        bool bad = false;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const int c = col0 + j;
-            if (c < e.cols) {
-                const float u = p.alpha * __uint_as_float(r[j]);
-                bad |= !isfinite(u);
-                const float t = th[c];
-                th[c] = t - p.lr_eff * (u + p.wd * t);
-            }
-        }
-        if (bad && p.flag) atomicOr(p.flag, 1);
     }
+}
+
+// EPI_APPLY, warp-cooperative: the warp's 32 rows x 32 columns go through a
+// shared-memory transpose so that every read-modify-write of theta touches
+// 32 consecutive floats of one row (one 128-byte line per instruction)
+// instead of 32 rows (apply_update precond.cpp:244-251, NonFinite :248).
+__device__ __forceinline__ void apply_chunk(const GemmParams& p, int b, int row0, int col0, const uint32_t (&r)[32],
+                                            float (*scratch)[33]) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) scratch[lane][j] = p.alpha * __uint_as_float(r[j]);
+    __syncwarp();
+    const ApplyEntry e = p.apply[b];
+    const int c = col0 + int(lane);
+    bool bad = false;
+    if (c < e.cols) {
+        float* th = e.theta + c;
+        const int rows = min(32, e.rows - row0);
+#pragma unroll 4
+        for (int i = 0; i < rows; ++i) {
+            const float u = scratch[i][lane];
+            bad |= !isfinite(u);
+            float* pt = th + int64_t(row0 + i) * e.ld;
+            const float t = *pt;
+            *pt = t - p.lr_eff * (u + p.wd * t);
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag) atomicOr(p.flag, 1);
+    __syncwarp();
 }
 
 template <int BN, int NPASS, int EPI>
@@ -236,6 +251,8 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
+    float (*scratch)[33] = reinterpret_cast<float (*)[33]>(smem + size_t(STAGES) * Cfg::kStageBytes + 256 +
+                                                           size_t(warp & 3) * 32 * 33 * 4);
 
     auto a_hi = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes; };
     auto a_lo = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes + Cfg::kABytes; };
@@ -351,7 +368,10 @@ __global__ void __launch_bounds__(192, 1)
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32), r);
                 tmem_ld_wait();
-                epilogue_chunk<EPI>(p, b, row, tn * BN + c * 32, r);
+                if constexpr (EPI == EPI_APPLY)
+                    apply_chunk(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
+                else
+                    epilogue_chunk<EPI>(p, b, row, tn * BN + c * 32, r);
             }
             tc_fence_before();
             __syncwarp();

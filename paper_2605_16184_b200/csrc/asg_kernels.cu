@@ -696,6 +696,143 @@ void launch_square_f64(const double* a, double* out, int64_t n, cudaStream_t s) 
 }
 
 // ============================================================================
+// fp32-level refresh (tensor-core transforms): split / transpose / scale
+// ============================================================================
+__global__ void split_slab_kernel(const float* __restrict__ src, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t count) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x) {
+        float h, l;
+        split_tf32(src[e], h, l);
+        hi[e] = h;
+        lo[e] = l;
+    }
+}
+
+void launch_split_slab(const float* src, float* hi, float* lo, int64_t count, cudaStream_t s) {
+    split_slab_kernel<<<1184, 256, 0, s>>>(src, hi, lo, count);
+    count_launch();
+}
+
+// [b][M][M] fp32 slab (leading m x m) -> [b][m][m] fp64, symmetrized.
+__global__ void snapshot_sym_kernel(const float* __restrict__ src, int M, int m, double* __restrict__ dst) {
+    const int64_t b = blockIdx.y;
+    const int64_t n = int64_t(m) * m;
+    const float* sb = src + b * int64_t(M) * M;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / m), j = int(e % m);
+        dst[b * n + e] = 0.5 * (double(sb[int64_t(i) * M + j]) + double(sb[int64_t(j) * M + i]));
+    }
+}
+
+void launch_snapshot_sym(const float* src, int nb, int M, int m, double* dst, cudaStream_t s) {
+    snapshot_sym_kernel<<<dim3(128, nb), 256, 0, s>>>(src, M, m, dst);
+    count_launch();
+}
+
+// dst[b][c][r] = split(src_hi[b][r][c] + src_lo[b][r][c]); R, C multiples of 32.
+__global__ void transpose_split_kernel(const float* __restrict__ src_hi, const float* __restrict__ src_lo, int R, int C,
+                                       float* __restrict__ dst_hi, float* __restrict__ dst_lo, int square) {
+    __shared__ float t[32][33];
+    const int64_t b = blockIdx.z;
+    const int64_t slab = int64_t(R) * C;
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t off = b * slab + int64_t(r0 + dy) * C + c0 + threadIdx.x;
+        float x = src_hi[off] + (src_lo ? src_lo[off] : 0.f);
+        if (square) x = x * x;
+        t[dy][threadIdx.x] = x;
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t off = b * slab + int64_t(c0 + dy) * R + r0 + threadIdx.x;
+        float h, l;
+        split_tf32(t[threadIdx.x][dy], h, l);
+        dst_hi[off] = h;
+        if (dst_lo) dst_lo[off] = l;
+    }
+}
+
+void launch_transpose_split(const float* src_hi, const float* src_lo, int nb, int R, int C, float* dst_hi,
+                            float* dst_lo, bool square, cudaStream_t s) {
+    dim3 grid(C / 32, R / 32, nb), block(32, 8);
+    transpose_split_kernel<<<grid, block, 0, s>>>(src_hi, src_lo, R, C, dst_hi, dst_lo, square ? 1 : 0);
+    count_launch();
+}
+
+// Elementwise (hi + lo)^2, resplit (same layout).
+__global__ void square_split_kernel(const float* __restrict__ hi, const float* __restrict__ lo, float* __restrict__ oh,
+                                    float* __restrict__ ol, int64_t count) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x) {
+        const float x = hi[e] + (lo ? lo[e] : 0.f);
+        float h, l;
+        split_tf32(x * x, h, l);
+        oh[e] = h;
+        if (ol) ol[e] = l;
+    }
+}
+
+void launch_square_split(const float* hi, const float* lo, float* out_hi, float* out_lo, int64_t count,
+                         cudaStream_t s) {
+    square_split_kernel<<<1184, 256, 0, s>>>(hi, lo, out_hi, out_lo, count);
+    count_launch();
+}
+
+// W[b][i][j] = V[b][i][j] * (lam_j + eps_b)^power for j < n (0 beyond), as a
+// (hi, lo) split; V is a split [b][D][D] slab. Same clamp / NotPsd rule as
+// scale_columns_kernel (densela.hpp:274-278).
+__global__ void scale_columns_split_kernel(const float* __restrict__ Vh, const float* __restrict__ Vl,
+                                           const double* __restrict__ values, const double* __restrict__ eps,
+                                           double power, int n, int D, float* __restrict__ Wh, float* __restrict__ Wl,
+                                           int* __restrict__ status) {
+    const int64_t b = blockIdx.y;
+    const int64_t DD = int64_t(D) * D;
+    const double e = eps ? eps[b] : 0.0;
+    const double lam_abs = fmax(fabs(values[b * n]), fabs(values[b * n + n - 1]));
+    const double tau = 4.0 * 5.9604644775390625e-08 * double(n) * lam_abs;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < DD; idx += int64_t(gridDim.x) * blockDim.x) {
+        const int j = int(idx % D);
+        float out = 0.f;
+        if (j < n) {
+            double lam = values[b * n + j];
+            if (lam < 0.0 && lam >= -tau) lam = 0.0;
+            const double damped = lam + e;
+            if (damped <= 0.0) {
+                atomicCAS(&status[b], ASG_OK, ASG_ERR_NOT_PSD);
+            } else {
+                const double v = double(Vh[b * DD + idx]) + (Vl ? double(Vl[b * DD + idx]) : 0.0);
+                out = float(v * pow(damped, power));
+            }
+        }
+        float h, l;
+        split_tf32(out, h, l);
+        Wh[b * DD + idx] = h;
+        if (Wl) Wl[b * DD + idx] = l;
+    }
+}
+
+void launch_scale_columns_split(const float* Vh, const float* Vl, const double* values, const double* eps,
+                                double power, int nb, int n, int D, float* Wh, float* Wl, int* status,
+                                cudaStream_t s) {
+    scale_columns_split_kernel<<<dim3(256, nb), 256, 0, s>>>(Vh, Vl, values, eps, power, n, D, Wh, Wl, status);
+    count_launch();
+}
+
+// eps[b] = damping * tr(A_b) / n from an fp32 [b][M][M] slab.
+__global__ void relative_damping_f32_kernel(const float* A, int M, int n, double damping, double* eps) {
+    __shared__ double red[32];
+    const int64_t b = blockIdx.x;
+    double tr = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) tr += double(A[b * int64_t(M) * M + int64_t(i) * M + i]);
+    tr = block_reduce_sum(tr, red);
+    if (threadIdx.x == 0) eps[b] = n > 0 ? damping * tr / double(n) : 0.0;
+}
+
+void launch_relative_damping_f32(const float* A, int nb, int M, int n, double damping, double* eps, cudaStream_t s) {
+    relative_damping_f32_kernel<<<nb, 256, 0, s>>>(A, M, n, damping, eps);
+    count_launch();
+}
+
+// ============================================================================
 // Multi-GPU pack / unpack of block slices (owner-major all-gather layout)
 // ============================================================================
 __global__ void pack_kernel(const BlockRef* blocks, const int64_t* offsets, float* out) {

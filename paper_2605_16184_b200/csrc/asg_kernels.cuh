@@ -100,6 +100,25 @@ void launch_f32_to_f64(const float* src, int nb, int rows, int cols, int R, int 
 
 void launch_square_f64(const double* a, double* out, int64_t n, cudaStream_t s);
 
+// fp32-level refresh helpers (tensor-core transforms of the refresh).
+// Elementwise hi/lo tf32 split of an fp32 array.
+void launch_split_slab(const float* src, float* hi, float* lo, int64_t count, cudaStream_t s);
+// [b][M][M] fp32 slab (leading m x m) -> [b][m][m] fp64, symmetrized (A + A^T)/2.
+void launch_snapshot_sym(const float* src, int nb, int M, int m, double* dst, cudaStream_t s);
+// dst[b] = split(op(src[b])^T) for [b][R][C] -> [b][C][R]; op = identity or
+// elementwise square; src_lo may be null (plain fp32 source). R, C % 32 == 0.
+void launch_transpose_split(const float* src_hi, const float* src_lo, int nb, int R, int C, float* dst_hi,
+                            float* dst_lo, bool square, cudaStream_t s);
+// Elementwise (hi + lo)^2, resplit.
+void launch_square_split(const float* hi, const float* lo, float* out_hi, float* out_lo, int64_t count,
+                         cudaStream_t s);
+// W = V diag((lam + eps)^power) on split [b][D][D] slabs (columns >= n zeroed).
+void launch_scale_columns_split(const float* Vh, const float* Vl, const double* values, const double* eps,
+                                double power, int nb, int n, int D, float* Wh, float* Wl, int* status,
+                                cudaStream_t s);
+// eps[b] = damping * tr(A_b) / n from an fp32 slab [b][M][M].
+void launch_relative_damping_f32(const float* A, int nb, int M, int n, double damping, double* eps, cudaStream_t s);
+
 // Multi-GPU: pack owned block slices into a contiguous buffer and back.
 void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out,
                         cudaStream_t s);

@@ -12,6 +12,19 @@ from . import abi
 from .runtime import check, lib
 
 
+# cudaStreamLegacy: the legacy default stream. torch reports its default stream
+# as handle 0, which the C-ABI reads as "the blockset's own main stream" (a
+# non-blocking stream that does not order with the legacy one), so handle 0 is
+# passed as cudaStreamLegacy to keep torch's default-stream work ordered.
+_CUDA_STREAM_LEGACY = 1
+
+
+def stream_arg(stream):
+    """C-ABI stream argument for a torch.cuda.Stream (or raw handle)."""
+    sh = getattr(stream, "cuda_stream", stream)
+    return C.c_void_p(sh if sh else _CUDA_STREAM_LEGACY)
+
+
 class AsteriaOptimizer:
     """Shampoo / SOAP / KL-Shampoo step (harness.cpp:439-475 call order) over
     `params` with gradients `grads` (both lists of contiguous fp32 CUDA
@@ -52,9 +65,14 @@ class AsteriaOptimizer:
             self._h = None
 
     # ---- the step ----------------------------------------------------------
-    def grad_sqnorm(self):
+    def grad_sqnorm(self, stream=None):
+        """Global squared gradient norm (read on `stream`, default torch's
+        current stream, so gradient writes issued there are visible)."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
         v, f = C.c_double(), C.c_int32()
-        check(lib.asg_grad_sqnorm(self._h, None, C.byref(v), C.byref(f)))
+        check(lib.asg_grad_sqnorm(self._h, stream_arg(stream), C.byref(v), C.byref(f)))
         if f.value:
             raise abi.NonFiniteError("non-finite gradient")
         return v.value
@@ -75,8 +93,7 @@ class AsteriaOptimizer:
         if stream is None:
             import torch
             stream = torch.cuda.current_stream(self.device)
-        sh = getattr(stream, "cuda_stream", stream)
-        check(lib.asg_step(self._h, step, clip_scale, lr_scale, C.c_void_p(sh) if sh else None))
+        check(lib.asg_step(self._h, step, clip_scale, lr_scale, stream_arg(stream)))
 
     def synchronize(self):
         check(lib.asg_synchronize(self._h))
@@ -156,4 +173,4 @@ class AsteriaOptimizer:
             dist.all_gather_into_tensor(recv, send, group=group)
             self._gather_buf.copy_(recv)
         check(lib.asg_unpack_gathered(self._h, C.c_void_p(self._gather_buf.data_ptr()), stride,
-                                      C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+                                      stream_arg(torch.cuda.current_stream(self.device))))

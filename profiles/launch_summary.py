@@ -19,7 +19,7 @@ def load(path, skip=0):
         if len(r) <= vi:
             continue
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+        v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}[r[ui]]
         out.append((r[ki], v))  # (name, microseconds)
     return out[skip:]
 
