@@ -215,6 +215,9 @@ def main():
     ap.add_argument("--workload", default=os.environ.get("ASG_WORKLOAD", "C2"), choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--refresh", default="f32", choices=["f32", "f64"],
+                    help="refresh arithmetic: f32 = fp32-level tensor-core refresh (default), "
+                         "f64 = reference-tight fp64 eigensolve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -227,7 +230,7 @@ def main():
     step_flops, refresh_flops, flops = alg_flops(wl)
     cfg_out = {"workload": wl["name"], "method": wl["method"], "blocks": sum(len(blocks_of(s, wl["limit"])) for s in wl["shapes"]),
                "params": sum(math.prod(s) for s in wl["shapes"]), "block_dim_limit": wl["limit"],
-               "pf": wl["pf"], "staleness_S": wl["S"], "precision": args.precision,
+               "pf": wl["pf"], "staleness_S": wl["S"], "precision": args.precision, "refresh": args.refresh,
                "parallelism": f"block-sharded x{args.gpus}" if args.gpus > 1 else "single",
                "l2": "inputs > L2 (every step streams all state and gradients from HBM)",
                "alg_tflop_per_step": flops / 1e12}
@@ -265,6 +268,10 @@ def main():
     sched = runtime.scheduler_defaults()
     sched.pf, sched.staleness_S = wl["pf"], wl["S"]
     sched.install_mode = abi.INSTALL_EVENT if wl["S"] > 0 else abi.INSTALL_SIM_CLOCK
+    sched.refresh_mode = abi.REFRESH_F32 if args.refresh == "f32" else abi.REFRESH_F64
+    # The cold first refresh (dispatched at step 0, no previous basis) must be
+    # installed before timing: its barrier fires at step S+1, so warm up past it.
+    args.warmup = max(args.warmup, wl["S"] + 2)
     prec = abi.PREC_3XTF32 if args.precision == "3xtf32" else abi.PREC_TF32
 
     gen = torch.Generator(device=dev).manual_seed(1234)
@@ -329,9 +336,8 @@ def main():
         barrier()
         t0 = time.perf_counter()
         for _ in range(max(3, args.steps // 2)):
-            with torch.cuda.stream(stream):
-                for g, h in zip(grads, host):
-                    g.copy_(h, non_blocking=True)
+            for g, h in zip(grads, host):  # on torch's current stream; the step orders after it
+                g.copy_(h, non_blocking=True)
             one_step(step)
             step += 1
         barrier()

@@ -112,6 +112,19 @@ typedef enum asg_install_mode {
     ASG_INSTALL_EVENT = 1
 } asg_install_mode;
 
+/* Arithmetic of the refresh (compute_refresh precond.cpp:129-142).
+ *   F64: fp64 eigensolve of the fp32 factor snapshot to the reference's own
+ *        stopping rule off(A) <= 1e-12 ||A||_F (densela.hpp:192-203); roots
+ *        and SOAP re-projections in fp64. Reference-tight (parity mode).
+ *   F32: fp32-level refresh, the fast path. The snapshot is rotated into the
+ *        block's previous eigenbasis on the tensor cores (3xTF32:
+ *        B = Q^T A Q), a Jacobi eigensolve of B stops once every element obeys
+ *        |b_ij| <= 1e-6 * max(sqrt(b_ii b_jj), ||A||_F / sqrt(n)), and the new
+ *        basis Q J, the roots V f(lambda) V^T and the SOAP moment
+ *        re-projection J^T M J are 3xTF32 tensor-core GEMMs. Accuracy is that
+ *        of the fp32 factor it decomposes. */
+typedef enum asg_refresh_mode { ASG_REFRESH_F64 = 0, ASG_REFRESH_F32 = 1 } asg_refresh_mode;
+
 /* SchedulerConfig (asyncsched.hpp:50-59); JSON keys config.cpp:81-86. */
 typedef struct asg_scheduler_config {
     int64_t staleness_S;
@@ -123,7 +136,7 @@ typedef struct asg_scheduler_config {
     double step_compute_us;
     double install_cost_us;
     int32_t install_mode;  /* asg_install_mode */
-    int32_t reserved;
+    int32_t refresh_mode;  /* asg_refresh_mode (default F64) */
 } asg_scheduler_config;
 
 /* BlockSpec (precond.hpp:47-57). param_index identifies the parameter. */
@@ -204,7 +217,8 @@ int asg_scheduler_defaults(asg_scheduler_config* out);                      /* S
  * async.pf defaults to optimizer.precondition_frequency (config.cpp:140) and
  * must equal it (config.cpp:42-43). Method strings: "AdamW", "Shampoo",
  * "SOAP", "KL-Shampoo". An optional "gpu" section may set "precision"
- * ("3xtf32"|"tf32") and "install_mode" ("sim_clock"|"event"). */
+ * ("3xtf32"|"tf32"), "install_mode" ("sim_clock"|"event") and "refresh"
+ * ("f64"|"f32"). */
 int asg_config_from_json(const char* json, asg_optimizer_config* opt,
                          asg_scheduler_config* sched, int32_t* precision);
 

@@ -17,6 +17,8 @@ SUM, EMA = 0, 1
 PREC_3XTF32, PREC_TF32 = 0, 1
 # asg_install_mode
 INSTALL_SIM_CLOCK, INSTALL_EVENT = 0, 1
+# asg_refresh_mode
+REFRESH_F64, REFRESH_F32 = 0, 1
 # asg_role (tiers.hpp:35-44 + KL + eigenvalues)
 (FACTOR_L, FACTOR_R, INV_L, INV_R, BASIS_L, BASIS_R, ROTATED_M, ROTATED_V,
  KL_INV_L, KL_INV_R, EIGVALS_L, EIGVALS_R) = range(12)
@@ -60,7 +62,7 @@ class SchedulerConfig(C.Structure):
         ("step_compute_us", C.c_double),
         ("install_cost_us", C.c_double),
         ("install_mode", C.c_int32),
-        ("reserved", C.c_int32),
+        ("refresh_mode", C.c_int32),
     ]
 
     def copy(self):
@@ -76,6 +78,7 @@ def scheduler_defaults():
     s.inject_job_delay_steps, s.inject_job_delay_jitter_steps = 0.0, 0.0
     s.step_compute_us, s.install_cost_us = 1000.0, 0.0
     s.install_mode = INSTALL_SIM_CLOCK
+    s.refresh_mode = REFRESH_F64
     return s
 
 

@@ -140,7 +140,8 @@ __global__ void bj_init_kernel(const double* __restrict__ Ain, int n, int np, do
 __global__ void __launch_bounds__(256) bj_pair_eig_kernel(const double* __restrict__ A, int np, int m, int round,
                                                            double* __restrict__ J, const int* __restrict__ active,
                                                            const double* __restrict__ fro_all, int* __restrict__ pflag,
-                                                           int* __restrict__ rotations, int relative, double rtol) {
+                                                           int* __restrict__ rotations, int relative, double rtol,
+                                                           const int* __restrict__ n_true) {
     extern __shared__ double sm[];
     double* S = sm;               // [kP][kP + 1]
     double* Z = S + kP * (kP + 1);  // [kP][kP + 1]
@@ -165,6 +166,10 @@ __global__ void __launch_bounds__(256) bj_pair_eig_kernel(const double* __restri
         Z[i * (kP + 1) + j] = (i == j) ? 1.0 : 0.0;
     }
     __syncthreads();
+    // relative mode: element (i,j) counts iff |a_ij| > rtol * max(sqrt|a_ii a_jj|, ||A||_F / sqrt(n)):
+    // relative accuracy for the large eigenvalues, and an absolute floor at the
+    // fp32 noise level of the factor for the small ones.
+    const double floor_scale = fro_all[b] / sqrt(double(n_true[b]));
     if (relative) {
         // Skip the pair unless some off-diagonal element is relatively large.
         bool big = false;
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(256) bj_pair_eig_kernel(const double* __restri
             const int i = e / kP, j = e % kP;
             if (j > i) {
                 const double x = fabs(S[i * (kP + 1) + j]);
-                big |= x > rtol * sqrt(fabs(S[i * (kP + 1) + i] * S[j * (kP + 1) + j]));
+                big |= x > rtol * fmax(sqrt(fabs(S[i * (kP + 1) + i] * S[j * (kP + 1) + j])), floor_scale);
             }
         }
         if (!__syncthreads_or(big)) {
@@ -198,7 +203,8 @@ __global__ void __launch_bounds__(256) bj_pair_eig_kernel(const double* __restri
             for (int e = threadIdx.x; e < kP * kP; e += blockDim.x) {
                 const int i = e / kP, j = e % kP;
                 if (j > i)
-                    big |= fabs(S[i * (kP + 1) + j]) > itol * sqrt(fabs(S[i * (kP + 1) + i] * S[j * (kP + 1) + j]));
+                    big |= fabs(S[i * (kP + 1) + j]) >
+                           itol * fmax(sqrt(fabs(S[i * (kP + 1) + i] * S[j * (kP + 1) + j])), floor_scale);
             }
             if (!__syncthreads_or(big)) break;
         } else {
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(256) bj_pair_eig_kernel(const double* __restri
                 const double apq = S[a * (kP + 1) + c];
                 double cc = 1.0, ss = 0.0;
                 const double app = S[a * (kP + 1) + a], aqq = S[c * (kP + 1) + c];
-                if (apq != 0.0 && (!relative || fabs(apq) > itol * sqrt(fabs(app * aqq)))) {
+                if (apq != 0.0 && (!relative || fabs(apq) > itol * fmax(sqrt(fabs(app * aqq)), floor_scale))) {
                     const double tau = (aqq - app) / (2.0 * apq);
                     const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau)) : -1.0 / (-tau + sqrt(1.0 + tau * tau));
                     cc = 1.0 / sqrt(1.0 + t * t);
@@ -386,6 +392,11 @@ __global__ void bj_converge_kernel(const double* __restrict__ A, int np, int n, 
     }
 }
 
+__global__ void fill_int_kernel(int* a, int count, int v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) a[i] = v;
+}
+
 // Condition of the sweep loop: keep iterating while any matrix is active and
 // the sweep budget is not spent.
 __global__ void bj_loop_kernel(const int* __restrict__ active, int nb, int* __restrict__ sweep_count, int max_sweeps,
@@ -426,7 +437,7 @@ size_t eigh_workspace_doubles(int nb, int n) {
     const int m = np / kW;
     // A, V, pair rotations J, then per matrix: fro, active, sweeps, rotations
     // (4 doubles) and the per-pair flags (m/2 ints), plus the loop counter.
-    return size_t(nb) * (2 * size_t(np) * np + size_t(m / 2) * kP * kP + 4 + size_t(m / 2 + 1) / 2 + 1) + 1;
+    return size_t(nb) * (2 * size_t(np) * np + size_t(m / 2) * kP * kP + 4 + size_t(m / 2 + 1) / 2 + 2) + 1;
 }
 
 size_t eigh_workspace_doubles_warm(int nb, int n) { return eigh_workspace_doubles(nb, n) + 2 * size_t(nb) * n * n; }
@@ -449,6 +460,7 @@ void launch_eigh(const double* A, double* values, double* vectors, double* ws, i
     int* rotations = sweeps + nb;
     int* pflag = rotations + nb;
     int* loop_count = pflag + size_t(nb) * (m / 2);
+    int* ntrue = loop_count + 1;  // n per matrix (uniform here)
     static bool attr = false;
     const int smem = 2 * kP * (kP + 1) * int(sizeof(double));
     if (!attr) {
@@ -467,6 +479,7 @@ void launch_eigh(const double* A, double* values, double* vectors, double* ws, i
         cudaMemsetAsync(sweeps, 0, size_t(nb) * 3 * sizeof(int), st);  // sweeps, rotations, (pad)
         cudaMemsetAsync(rotations, 0, size_t(nb) * sizeof(int), st);
         cudaMemsetAsync(loop_count, 0, sizeof(int), st);
+        fill_int_kernel<<<(nb + 255) / 256, 256, 0, st>>>(ntrue, nb, n);
         if (Vinit) {
             const int64_t nn1 = int64_t(n) * n;
             launch_dgemm(false, false, n, n, n, 1.0, A, n, nn1, Vinit, n, nn1, 0.0, W1, n, nn1, nb, st);
@@ -477,7 +490,7 @@ void launch_eigh(const double* A, double* values, double* vectors, double* ws, i
     auto sweep = [&](cudaStream_t st) {
         for (int r = 0; r < m - 1; ++r) {
             bj_pair_eig_kernel<<<dim3(m / 2, nb), 256, smem, st>>>(Aw, np, m, r, J, active, fro, pflag, rotations,
-                                                                    rel, rtol);
+                                                                    rel, rtol, ntrue);
             // columns of A and V (fused), then rows of A
             bj_apply_kernel<false><<<dim3(np / kP, m / 2, 2 * nb), 256, smem, st>>>(Aw, Aw, np, m, r, J, active, nb, V,
                                                                                      pflag);

@@ -159,7 +159,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int r
             split_tf32(p.alpha * __uint_as_float(r[j + 2]), h.z, l.z);
             split_tf32(p.alpha * __uint_as_float(r[j + 3]), h.w, l.w);
             *reinterpret_cast<float4*>(dh + j) = h;
-            *reinterpret_cast<float4*>(dl + j) = l;
+            if (p.Dlo) *reinterpret_cast<float4*>(dl + j) = l;
         }
     } else if constexpr (EPI == EPI_SPLIT_T) {
         float* dh = p.Dhi + int64_t(b) * p.d_bstride + row;
@@ -169,7 +169,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int r
             float h, l;
             split_tf32(p.alpha * __uint_as_float(r[j]), h, l);
             dh[int64_t(col0 + j) * p.ldd] = h;
-            dl[int64_t(col0 + j) * p.ldd] = l;
+            if (p.Dlo) dl[int64_t(col0 + j) * p.ldd] = l;
         }
     } else if constexpr (EPI == EPI_ADAM) {
         const int64_t moff = int64_t(b) * p.m_bstride + int64_t(row) * p.ldm + col0;
@@ -198,7 +198,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int r
             *reinterpret_cast<float4*>(mm + j) = m4;
             *reinterpret_cast<float4*>(vv + j) = v4;
             *reinterpret_cast<float4*>(p.Dhi + doff + j) = h;
-            *reinterpret_cast<float4*>(p.Dlo + doff + j) = l;
+            if (p.Dlo) *reinterpret_cast<float4*>(p.Dlo + doff + j) = l;
         }
     }
 }

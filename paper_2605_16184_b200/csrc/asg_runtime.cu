@@ -123,6 +123,7 @@ asg_scheduler_config sched_defaults() {
     s.step_compute_us = 1000.0;
     s.install_cost_us = 0.0;
     s.install_mode = ASG_INSTALL_SIM_CLOCK;
+    s.refresh_mode = ASG_REFRESH_F64;
     return s;
 }
 
@@ -180,6 +181,11 @@ struct Group {
     double *sQL64 = nullptr, *sQR64 = nullptr, *svalsL = nullptr, *svalsR = nullptr;
     // Shampoo / KL-Shampoo: eigenvectors of the last refresh (warm start of the next)
     double *EL64 = nullptr, *ER64 = nullptr;
+    // F32 refresh: Shampoo / KL basis as split tf32 pairs, row-major and transposed
+    float *BLh = nullptr, *BLl = nullptr, *BLTh = nullptr, *BLTl = nullptr;
+    float *BRh = nullptr, *BRl = nullptr, *BRTh = nullptr, *BRTl = nullptr;
+    // F32 refresh, SOAP: shadow rotations J^T (new basis = Q_old J) per side
+    float *sJLTh = nullptr, *sJLTl = nullptr, *sJRTh = nullptr, *sJRTl = nullptr;
     BlockRef* d_refs = nullptr;
     ApplyEntry* d_apply = nullptr;
     int2 *tilesM = nullptr, *tilesN = nullptr;
@@ -215,6 +221,11 @@ struct asg_blockset {
     int ws_chunk = 0, ws_n = 0;
     double *ws_snap = nullptr, *ws_vecs = nullptr, *ws_work = nullptr, *ws_W = nullptr, *ws_out = nullptr,
            *ws_vals = nullptr, *ws_eps = nullptr;
+    // F32 refresh workspace (side stream): 8 split-tf32 slabs of ws_chunk x D x D
+    float* tw[8] = {};
+    size_t tw_slab = 0;  // floats per block slot (Dmax^2)
+    // F32 SOAP install workspace (main stream): 4 slabs of ws_chunk x D x D
+    float* iw32[4] = {};
     // SOAP install workspace (one block)
     double *iw_rotL = nullptr, *iw_rotR = nullptr, *iw_sq = nullptr, *iw_a = nullptr, *iw_b = nullptr;
     // scalars
@@ -280,6 +291,9 @@ bool is_precond(const asg_blockset* bs) { return bs->opt.method != ASG_METHOD_AD
 bool is_soap(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_SOAP; }
 bool is_kl(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_KL_SHAMPOO; }
 bool split_mode(const asg_blockset* bs) { return bs->precision == ASG_PREC_3XTF32; }
+bool f32_refresh(const asg_blockset* bs) { return bs->sc.refresh_mode == ASG_REFRESH_F32; }
+// Relative threshold of the F32 refresh's Jacobi (asg_eigh.cuh EighOpts).
+constexpr double kF32RefreshTol = 1e-6;
 
 void emit(asg_blockset* bs, int64_t step, int kind, int64_t block, uint64_t version, double t) {
     asg_event e{};
@@ -415,10 +429,15 @@ void alloc_group(asg_blockset* bs, Group& g) {
         pair_nn(g.QRTh, g.QRTl);
         g.mom_m = dalloc<float>(bs, nb * slabMN(g));
         g.mom_v = dalloc<float>(bs, nb * slabMN(g));
-        g.QL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
-        g.QR64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
-        g.sQL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
-        g.sQR64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
+        if (f32_refresh(bs)) {
+            pair_mm(g.sJLTh, g.sJLTl);
+            pair_nn(g.sJRTh, g.sJRTl);
+        } else {
+            g.QL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
+            g.QR64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
+            g.sQL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
+            g.sQR64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
+        }
         g.valsL = dalloc<double>(bs, nb * size_t(g.m));
         g.valsR = dalloc<double>(bs, nb * size_t(g.n));
         g.svalsL = dalloc<double>(bs, nb * size_t(g.m));
@@ -433,8 +452,8 @@ void alloc_group(asg_blockset* bs, Group& g) {
         for (int i = 0; i < g.n; ++i) eyeR[size_t(i) * g.n + i] = 1.0;
         std::vector<double> onesL(size_t(g.m), 1.0), onesR(size_t(g.n), 1.0);
         for (size_t b = 0; b < nb; ++b) {
-            h2d(g.QL64 + b * g.m * g.m, eyeL.data(), eyeL.size() * 8, bs->main);
-            h2d(g.QR64 + b * g.n * g.n, eyeR.data(), eyeR.size() * 8, bs->main);
+            if (g.QL64) h2d(g.QL64 + b * g.m * g.m, eyeL.data(), eyeL.size() * 8, bs->main);
+            if (g.QR64) h2d(g.QR64 + b * g.n * g.n, eyeR.data(), eyeR.size() * 8, bs->main);
             h2d(g.valsL + b * g.m, onesL.data(), onesL.size() * 8, bs->main);
             h2d(g.valsR + b * g.n, onesR.data(), onesR.size() * 8, bs->main);
         }
@@ -447,8 +466,19 @@ void alloc_group(asg_blockset* bs, Group& g) {
         pair_nn(g.sPRh, g.sPRl);
         launch_identity_split(g.PLh, g.PLl, g.nb, g.M, g.m, s);
         launch_identity_split(g.PRh, g.PRl, g.nb, g.N, g.n, s);
-        g.EL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
-        g.ER64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
+        if (f32_refresh(bs)) {  // basis of the last refresh, identity before the first
+            pair_mm(g.BLh, g.BLl);
+            pair_mm(g.BLTh, g.BLTl);
+            pair_nn(g.BRh, g.BRl);
+            pair_nn(g.BRTh, g.BRTl);
+            launch_identity_split(g.BLh, g.BLl, g.nb, g.M, g.m, s);
+            launch_identity_split(g.BLTh, g.BLTl, g.nb, g.M, g.m, s);
+            launch_identity_split(g.BRh, g.BRl, g.nb, g.N, g.n, s);
+            launch_identity_split(g.BRTh, g.BRTl, g.nb, g.N, g.n, s);
+        } else {
+            g.EL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
+            g.ER64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
+        }
         if (is_kl(bs)) {
             pair_mm(g.KLh, g.KLl);
             pair_nn(g.KRh, g.KRl);
@@ -517,6 +547,14 @@ void alloc_workspace(asg_blockset* bs) {
     bs->ws_out = dalloc<double>(bs, nn);
     bs->ws_vals = dalloc<double>(bs, size_t(nmax) * bs->ws_chunk);
     bs->ws_eps = dalloc<double>(bs, size_t(bs->ws_chunk));
+    if (f32_refresh(bs)) {
+        int Dmax = 0;
+        for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
+        bs->tw_slab = size_t(Dmax) * Dmax;
+        for (float*& t : bs->tw) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
+        if (is_soap(bs))
+            for (float*& t : bs->iw32) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
+    }
     if (is_soap(bs)) {
         int maxmn = 0;
         for (const Group& g : bs->groups) maxmn = std::max(maxmn, g.m * g.n);
@@ -735,6 +773,105 @@ void refresh_side(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaSt
     }
 }
 
+// F32 refresh of one side of one chunk (asg_refresh_mode F32). With Q the
+// block's previous eigenbasis (identity before the first refresh):
+//   B = Q^T A Q (two 3xTF32 GEMMs), J = eig(B) (fp64 block Jacobi, relative
+//   threshold), then Shampoo/KL: V = Q J becomes the new basis and the roots
+//   V f(lambda) V^T are GEMMs; SOAP: J^T is kept as the shadow rotation, the
+//   install forms Q J and re-projects the moments (install_soap_f32).
+void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaStream_t s) {
+    const int d = left ? g.m : g.n, D = left ? g.M : g.N;
+    const size_t DD = size_t(D) * D, cntDD = size_t(cnt) * DD;
+    const double dd3 = double(cnt) * d * double(d) * d;
+    float** t = bs->tw;
+    const float* snap = at(left ? g.snapL : g.snapR, DD, s0);
+    float *Qh, *Ql, *QTh, *QTl;
+    if (is_soap(bs)) {
+        Qh = at(left ? g.QLh : g.QRh, DD, s0);
+        Ql = at(left ? g.QLl : g.QRl, DD, s0);
+        QTh = at(left ? g.QLTh : g.QRTh, DD, s0);
+        QTl = at(left ? g.QLTl : g.QRTl, DD, s0);
+    } else {
+        Qh = at(left ? g.BLh : g.BRh, DD, s0);
+        Ql = at(left ? g.BLl : g.BRl, DD, s0);
+        QTh = at(left ? g.BLTh : g.BRTh, DD, s0);
+        QTl = at(left ? g.BLTl : g.BRTl, DD, s0);
+    }
+    const bool sp = split_mode(bs);
+    float* t1 = sp ? t[1] : nullptr;
+    float* t3 = sp ? t[3] : nullptr;
+    float* t5 = sp ? t[5] : nullptr;
+    float* t7 = sp ? t[7] : nullptr;
+    // A as a split operand
+    if (sp) launch_split_slab(snap, t[0], t[1], int64_t(cntDD), s);
+    else CK(cudaMemcpyAsync(t[0], snap, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+    // W^T = (A Q)^T
+    GemmParams p1{};
+    p1.alpha = 1.f;
+    p1.Dhi = t[2];
+    p1.Dlo = t3;
+    p1.ldd = D;
+    p1.d_bstride = int64_t(DD);
+    run_gemm(bs, op(t[0], t1, D, D), op(QTh, QTl, D, D), cnt, EPI_SPLIT_T, p1, nullptr, 0, s, 2.0 * dd3);
+    // B = Q^T W
+    GemmParams p2{};
+    p2.alpha = 1.f;
+    p2.beta = 0.f;
+    p2.C = t[4];
+    p2.ldc = D;
+    p2.c_bstride = int64_t(DD);
+    run_gemm(bs, op(QTh, QTl, D, D), op(t[2], t3, D, D), cnt, EPI_STORE, p2, nullptr, 0, s, 2.0 * dd3);
+    launch_snapshot_sym(t[4], cnt, D, d, bs->ws_snap, s);
+    EighOpts eo;
+    eo.relative = 1;
+    eo.tol = kF32RefreshTol;
+    launch_eigh(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, cnt, d, g.d_status + s0, s, nullptr, eo);
+    // J -> (t0, t1), J^T -> (t2, t3)
+    launch_f64_to_split(bs->ws_vecs, cnt, d, D, false, t[0], t1, t[2], t3, s);
+    if (is_soap(bs)) {
+        CK(cudaMemcpyAsync(at(left ? g.sJLTh : g.sJRTh, DD, s0), t[2], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        if (sp)
+            CK(cudaMemcpyAsync(at(left ? g.sJLTl : g.sJRTl, DD, s0), t[3], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(at(left ? g.svalsL : g.svalsR, size_t(d), s0), bs->ws_vals, size_t(cnt) * d * 8,
+                           cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    // V = Q J -> (t4, t5); it becomes the block's basis (row-major and transposed)
+    GemmParams p3{};
+    p3.alpha = 1.f;
+    p3.Dhi = t[4];
+    p3.Dlo = t5;
+    p3.ldd = D;
+    p3.d_bstride = int64_t(DD);
+    run_gemm(bs, op(Qh, Ql, D, D), op(t[2], t3, D, D), cnt, EPI_SPLIT, p3, nullptr, 0, s, 2.0 * dd3);
+    CK(cudaMemcpyAsync(Qh, t[4], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+    if (sp) CK(cudaMemcpyAsync(Ql, t[5], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+    launch_transpose_split(t[4], t5, cnt, D, D, QTh, sp ? QTl : nullptr, false, s);
+    // roots V diag((lambda + eps)^p) V^T  (inv_root densela.hpp:267-282, damping precond.cpp:121-125)
+    launch_relative_damping(bs->ws_snap, cnt, d, bs->opt.damping, bs->ws_eps, s);
+    struct Out {
+        double power;
+        float *hi, *lo;
+    };
+    std::vector<Out> outs;
+    if (is_kl(bs)) {
+        outs.push_back({-0.5, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
+        outs.push_back({-1.0, at(left ? g.sKLh : g.sKRh, DD, s0), at(left ? g.sKLl : g.sKRl, DD, s0)});
+    } else {
+        outs.push_back({-0.25, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
+    }
+    for (const Out& o : outs) {
+        launch_scale_columns_split(t[4], t5, bs->ws_vals, bs->ws_eps, o.power, cnt, d, D, t[6], t7, g.d_status + s0, s);
+        GemmParams pr{};
+        pr.alpha = 1.f;
+        pr.Dhi = o.hi;
+        pr.Dlo = o.lo;
+        pr.ldd = D;
+        pr.d_bstride = int64_t(DD);
+        run_gemm(bs, op(t[6], t7, D, D), op(t[4], t5, D, D), cnt, EPI_SPLIT, pr, nullptr, 0, s, 2.0 * dd3);
+    }
+}
+
 // Launches the refresh for every unit marked dispatched-but-not-launched.
 void launch_refreshes(asg_blockset* bs) {
     std::vector<std::vector<int>> per_group(bs->groups.size());
@@ -771,8 +908,13 @@ void launch_refreshes(asg_blockset* bs) {
             while (j < slots.size() && slots[j] == slots[j - 1] + 1 && int(j - i) < bs->ws_chunk) ++j;
             const int s0 = slots[i], cnt = int(j - i);
             CK(cudaMemsetAsync(g.d_status + s0, 0, size_t(cnt) * sizeof(int), bs->side));
-            refresh_side(bs, g, s0, cnt, true, bs->side);
-            refresh_side(bs, g, s0, cnt, false, bs->side);
+            if (f32_refresh(bs)) {
+                refresh_side_f32(bs, g, s0, cnt, true, bs->side);
+                refresh_side_f32(bs, g, s0, cnt, false, bs->side);
+            } else {
+                refresh_side(bs, g, s0, cnt, true, bs->side);
+                refresh_side(bs, g, s0, cnt, false, bs->side);
+            }
             CK(cudaMemcpyAsync(g.h_status + s0, g.d_status + s0, size_t(cnt) * sizeof(int), cudaMemcpyDeviceToHost,
                                bs->side));
             for (int k = 0; k < cnt; ++k) {
@@ -789,8 +931,8 @@ void launch_refreshes(asg_blockset* bs) {
 
 int status_to_code(int st) { return st; }
 
-// Device-side install of a finished refresh (install_refresh precond.cpp:144-164).
-void install_device(asg_blockset* bs, Unit& u) {
+// Waits for a unit's refresh (host: its status; main stream: its event).
+void install_wait(asg_blockset* bs, Unit& u) {
     if (u.needs_launch) launch_refreshes(bs);
     Group& g = bs->groups[size_t(u.group)];
     CK(cudaEventSynchronize(u.done));
@@ -803,6 +945,80 @@ void install_device(asg_blockset* bs, Unit& u) {
         throw Fail{status_to_code(st), what};
     }
     CK(cudaStreamWaitEvent(bs->main, u.done, 0));
+}
+
+// SOAP install of the F32 refresh for slots [s0, s0+cnt) of a group
+// (install_refresh precond.cpp:145-157 with rot = Q_new^T Q_old = J^T):
+//   Q <- Q J ;  M <- J_L^T M J_R ;  V <- (J_L o J_L)^T V (J_R o J_R) ;  values.
+void install_soap_f32(asg_blockset* bs, Group& g, int s0, int cnt) {
+    cudaStream_t s = bs->main;
+    const bool sp = split_mode(bs);
+    float** w = bs->iw32;
+    const size_t MN = slabMN(g);
+    for (int side = 0; side < 2; ++side) {
+        const bool left = side == 0;
+        const int d = left ? g.m : g.n, D = left ? g.M : g.N;
+        const size_t DD = size_t(D) * D, cntDD = size_t(cnt) * DD;
+        float* Qh = at(left ? g.QLh : g.QRh, DD, s0);
+        float* Ql = at(left ? g.QLl : g.QRl, DD, s0);
+        GemmParams p{};
+        p.alpha = 1.f;
+        p.Dhi = w[0];
+        p.Dlo = sp ? w[1] : nullptr;
+        p.ldd = D;
+        p.d_bstride = int64_t(DD);
+        run_gemm(bs, op(Qh, Ql, D, D), op(at(left ? g.sJLTh : g.sJRTh, DD, s0), at(left ? g.sJLTl : g.sJRTl, DD, s0), D, D),
+                 cnt, EPI_SPLIT, p, nullptr, 0, s, 2.0 * cnt * double(d) * d * d);
+        CK(cudaMemcpyAsync(Qh, w[0], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        if (sp) CK(cudaMemcpyAsync(Ql, w[1], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        launch_transpose_split(w[0], sp ? w[1] : nullptr, cnt, D, D, at(left ? g.QLTh : g.QRTh, DD, s0),
+                               at(left ? g.QLTl : g.QRTl, DD, s0), false, s);
+        CK(cudaMemcpyAsync(at(left ? g.valsL : g.valsR, size_t(d), s0), at(left ? g.svalsL : g.svalsR, size_t(d), s0),
+                           size_t(cnt) * d * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    const size_t mm = slabMM(g), nn = slabNN(g);
+    const double flops = 2.0 * cnt * double(g.m) * g.n * (g.m + g.n);
+    for (int which = 0; which < 2; ++which) {
+        float* mom = at(which == 0 ? g.mom_m : g.mom_v, MN, s0);
+        const float *lh = at(g.sJLTh, mm, s0), *ll = at(g.sJLTl, mm, s0);
+        const float *rh = at(g.sJRTh, nn, s0), *rl = at(g.sJRTl, nn, s0);
+        if (which == 1) {  // elementwise squares of the rotations
+            launch_square_split(lh, ll, w[0], sp ? w[1] : nullptr, int64_t(size_t(cnt) * mm), s);
+            launch_square_split(rh, rl, w[2], sp ? w[3] : nullptr, int64_t(size_t(cnt) * nn), s);
+            lh = w[0];
+            ll = sp ? w[1] : nullptr;
+            rh = w[2];
+            rl = sp ? w[3] : nullptr;
+        }
+        // M^T as the B operand (S slabs are free outside the update)
+        launch_transpose_split(mom, nullptr, cnt, g.M, g.N, at(g.Sh, MN, s0), at(g.Sl, MN, s0), false, s);
+        GemmParams pt{};
+        pt.alpha = 1.f;
+        pt.Dhi = at(g.Th, MN, s0);
+        pt.Dlo = at(g.Tl, MN, s0);
+        pt.ldd = g.N;
+        pt.d_bstride = int64_t(MN);
+        run_gemm(bs, op(lh, ll, g.M, g.M), op(at(g.Sh, MN, s0), at(g.Sl, MN, s0), g.N, g.M), cnt, EPI_SPLIT, pt, nullptr,
+                 0, s, 2.0 * cnt * double(g.m) * g.m * g.n);
+        GemmParams po{};
+        po.alpha = 1.f;
+        po.beta = 0.f;
+        po.C = mom;
+        po.ldc = g.N;
+        po.c_bstride = int64_t(MN);
+        run_gemm(bs, op(at(g.Th, MN, s0), at(g.Tl, MN, s0), g.M, g.N), op(rh, rl, g.N, g.N), cnt, EPI_STORE, po, nullptr,
+                 0, s, 2.0 * cnt * double(g.m) * g.n * g.n);
+    }
+    (void)flops;
+}
+
+// Device-side install of a finished refresh (install_refresh precond.cpp:144-164).
+void install_apply(asg_blockset* bs, Unit& u) {
+    Group& g = bs->groups[size_t(u.group)];
+    if (f32_refresh(bs) && is_soap(bs)) {
+        install_soap_f32(bs, g, u.slot, 1);
+        return;
+    }
     cudaStream_t s = bs->main;
     const size_t mm = slabMM(g), nn = slabNN(g);
     auto cp = [&](float* dst, const float* src, size_t n) {
@@ -889,11 +1105,30 @@ void run_deferred_installs(asg_blockset* bs) {
     launch_refreshes(bs);
     std::vector<int> todo;
     todo.swap(bs->deferred_installs);
-    for (int idx : todo) {
-        Unit& u = bs->units[size_t(idx)];
-        install_device(bs, u);
-        u.launched = false;
+    for (int idx : todo) install_wait(bs, bs->units[size_t(idx)]);
+    if (f32_refresh(bs) && is_soap(bs)) {
+        // batched: contiguous slot runs of one group, in workspace-sized chunks
+        std::vector<std::pair<int, int>> gs;
+        for (int idx : todo) gs.emplace_back(bs->units[size_t(idx)].group, bs->units[size_t(idx)].slot);
+        std::sort(gs.begin(), gs.end());
+        size_t i = 0;
+        while (i < gs.size()) {
+            size_t j = i + 1;
+            while (j < gs.size() && gs[j].first == gs[i].first && gs[j].second == gs[j - 1].second + 1 &&
+                   int(j - i) < bs->ws_chunk)
+                ++j;
+            install_soap_f32(bs, bs->groups[size_t(gs[i].first)], gs[i].second, int(j - i));
+            i = j;
+        }
+    } else {
+        for (int idx : todo) install_apply(bs, bs->units[size_t(idx)]);
     }
+    for (int idx : todo) bs->units[size_t(idx)].launched = false;
+}
+
+void install_device(asg_blockset* bs, Unit& u) {
+    install_wait(bs, u);
+    install_apply(bs, u);
 }
 
 // maybe_dispatch (asyncsched.cpp:108-142), host bookkeeping only.
@@ -1114,6 +1349,12 @@ int asg_config_from_json(const char* text, asg_optimizer_config* opt, asg_schedu
                 else if (p == "tf32") prec = ASG_PREC_TF32;
                 else throw Fail{ASG_ERR_CONFIG_INVALID, "unknown precision: " + p};
             }
+            if (g.has("refresh")) {
+                const std::string r = str(g, "refresh");
+                if (r == "f64") s.refresh_mode = ASG_REFRESH_F64;
+                else if (r == "f32") s.refresh_mode = ASG_REFRESH_F32;
+                else throw Fail{ASG_ERR_CONFIG_INVALID, "unknown refresh: " + r};
+            }
             if (g.has("install_mode")) {
                 const std::string m = str(g, "install_mode");
                 if (m == "sim_clock") s.install_mode = ASG_INSTALL_SIM_CLOCK;
@@ -1156,6 +1397,8 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         validate(*opt);
         if (sched->staleness_S < 0) throw Fail{ASG_ERR_CONFIG_INVALID, "staleness_S must be >= 0"};
         if (sched->pf < 1) throw Fail{ASG_ERR_CONFIG_INVALID, "pf must be >= 1"};
+        if (sched->refresh_mode != ASG_REFRESH_F64 && sched->refresh_mode != ASG_REFRESH_F32)
+            throw Fail{ASG_ERR_CONFIG_INVALID, "unknown refresh_mode"};
         if (sched->pf != opt->precondition_frequency)
             throw Fail{ASG_ERR_CONFIG_INVALID, "async.pf must equal optimizer.precondition_frequency"};
         if (world < 1 || rank < 0 || rank >= world) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad rank/world"};
@@ -1564,8 +1807,14 @@ int asg_block_read(asg_blockset* bs, int64_t idx, int32_t role, double* out, int
             case ASG_ROLE_INV_R: rd32(g.PRh, slabNN(g), g.N, g.N, n, n, g.PRl); break;
             case ASG_ROLE_KL_INV_L: rd32(g.KLh, slabMM(g), g.M, g.M, m, m, g.KLl); break;
             case ASG_ROLE_KL_INV_R: rd32(g.KRh, slabNN(g), g.N, g.N, n, n, g.KRl); break;
-            case ASG_ROLE_BASIS_L: rd64(g.QL64, size_t(m) * m, size_t(m) * m); break;
-            case ASG_ROLE_BASIS_R: rd64(g.QR64, size_t(n) * n, size_t(n) * n); break;
+            case ASG_ROLE_BASIS_L:
+                if (g.QL64) rd64(g.QL64, size_t(m) * m, size_t(m) * m);
+                else rd32(g.QLh, slabMM(g), g.M, g.M, m, m, g.QLl);  // F32 refresh: split basis
+                break;
+            case ASG_ROLE_BASIS_R:
+                if (g.QR64) rd64(g.QR64, size_t(n) * n, size_t(n) * n);
+                else rd32(g.QRh, slabNN(g), g.N, g.N, n, n, g.QRl);
+                break;
             case ASG_ROLE_EIGVALS_L: rd64(g.valsL, size_t(m), size_t(m)); break;
             case ASG_ROLE_EIGVALS_R: rd64(g.valsR, size_t(n), size_t(n)); break;
             case ASG_ROLE_ROTATED_M: rd32(g.mom_m, slabMN(g), g.M, g.N, m, n, nullptr); break;
@@ -1617,17 +1866,27 @@ int asg_block_write(asg_blockset* bs, int64_t idx, int32_t role, const double* i
             case ASG_ROLE_KL_INV_L: wr32(g.KLh, slabMM(g), g.M, g.M, m, m, sp ? g.KLl : nullptr, nullptr, nullptr); break;
             case ASG_ROLE_KL_INV_R: wr32(g.KRh, slabNN(g), g.N, g.N, n, n, sp ? g.KRl : nullptr, nullptr, nullptr); break;
             case ASG_ROLE_BASIS_L:
-                wr64(g.QL64, size_t(m) * m, size_t(m) * m);
-                launch_f64_to_split(g.QL64 + size_t(m) * m * u.slot, 1, m, g.M, false, g.QLh + slabMM(g) * u.slot,
-                                    sp ? g.QLl + slabMM(g) * u.slot : nullptr, g.QLTh + slabMM(g) * u.slot,
-                                    sp ? g.QLTl + slabMM(g) * u.slot : nullptr, bs->main);
+            case ASG_ROLE_BASIS_R: {
+                const bool left = role == ASG_ROLE_BASIS_L;
+                const int d = left ? m : n, D = left ? g.M : g.N;
+                double* q64 = left ? g.QL64 : g.QR64;
+                const double* src = nullptr;
+                if (q64) {  // F64 refresh keeps the fp64 basis
+                    wr64(q64, size_t(d) * d, size_t(d) * d);
+                    src = q64 + size_t(d) * d * u.slot;
+                } else {  // F32 refresh: split basis only; stage through the fp64 workspace
+                    if (count < int64_t(d) * d) throw Fail{ASG_ERR_SHAPE_MISMATCH, "input too small"};
+                    if (!g.QLh) throw Fail{ASG_ERR_INVALID_ARGUMENT, "role not held by this method"};
+                    h2d(bs->ws_out, in, size_t(d) * d * 8, bs->main);
+                    src = bs->ws_out;
+                }
+                const size_t DD = size_t(D) * D;
+                launch_f64_to_split(src, 1, d, D, false, (left ? g.QLh : g.QRh) + DD * u.slot,
+                                    sp ? (left ? g.QLl : g.QRl) + DD * u.slot : nullptr,
+                                    (left ? g.QLTh : g.QRTh) + DD * u.slot,
+                                    sp ? (left ? g.QLTl : g.QRTl) + DD * u.slot : nullptr, bs->main);
                 break;
-            case ASG_ROLE_BASIS_R:
-                wr64(g.QR64, size_t(n) * n, size_t(n) * n);
-                launch_f64_to_split(g.QR64 + size_t(n) * n * u.slot, 1, n, g.N, false, g.QRh + slabNN(g) * u.slot,
-                                    sp ? g.QRl + slabNN(g) * u.slot : nullptr, g.QRTh + slabNN(g) * u.slot,
-                                    sp ? g.QRTl + slabNN(g) * u.slot : nullptr, bs->main);
-                break;
+            }
             case ASG_ROLE_EIGVALS_L: wr64(g.valsL, size_t(m), size_t(m)); break;
             case ASG_ROLE_EIGVALS_R: wr64(g.valsR, size_t(n), size_t(n)); break;
             case ASG_ROLE_ROTATED_M: wr32(g.mom_m, slabMN(g), g.M, g.N, m, n, nullptr, nullptr, nullptr); break;

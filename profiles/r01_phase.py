@@ -64,6 +64,7 @@ def step(wls):
             opt.accumulation = abi.EMA
             sched = rt.scheduler_defaults()
             sched.pf, sched.staleness_S, sched.install_mode = pf, 0, abi.INSTALL_SIM_CLOCK
+            sched.refresh_mode = abi.REFRESH_F32 if os.environ.get("ASG_REFRESH", "f64") == "f32" else abi.REFRESH_F64
             o = AsteriaOptimizer(params, grads, opt, sched, precision=abi.PREC_3XTF32)
             st = torch.cuda.ExternalStream(o.stream_handle)
             o.step(0)  # first step (pf huge: the only dispatch)
@@ -77,7 +78,7 @@ def step(wls):
                 e1.record(st)
                 o.synchronize()
                 times.append((e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3))
-            print(json.dumps(dict(phase=label, workload=name, ms_device=[t[0] for t in times],
+            print(json.dumps(dict(phase=label, workload=name, refresh=os.environ.get("ASG_REFRESH", "f64"), ms_device=[t[0] for t in times],
                                   ms_wall=[t[1] for t in times])), flush=True)
             del o
             torch.cuda.empty_cache()

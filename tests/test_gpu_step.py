@@ -42,7 +42,8 @@ def O():
     return optimizer
 
 
-def run_pair(O, method, shapes, limit, pf, steps, seed=0, S=0, lr=1e-2, wd=0.0, clip=1.0, well=True, delay=0.0):
+def run_pair(O, method, shapes, limit, pf, steps, seed=0, S=0, lr=1e-2, wd=0.0, clip=1.0, well=True, delay=0.0,
+             refresh_mode=abi.REFRESH_F64, r_scale=1.0):
     """GPU step vs the oracle's per-block harness loop (harness.cpp:439-475) with
     the oracle's ShadowScheduler on the same simulated clock."""
     from paper_2605_16184_b200 import runtime
@@ -50,6 +51,7 @@ def run_pair(O, method, shapes, limit, pf, steps, seed=0, S=0, lr=1e-2, wd=0.0, 
     opt.lr, opt.weight_decay, opt.block_dim_limit, opt.precondition_frequency = lr, wd, limit, pf
     sched = runtime.scheduler_defaults()
     sched.pf, sched.staleness_S, sched.inject_job_delay_steps = pf, S, delay
+    sched.refresh_mode = refresh_mode
     rng = np.random.default_rng(seed)
     thetas0 = [0.1 * rng.standard_normal(s) for s in shapes]
     params = [torch.tensor(t, dtype=torch.float32, device="cuda") for t in thetas0]
@@ -109,7 +111,7 @@ def run_pair(O, method, shapes, limit, pf, steps, seed=0, S=0, lr=1e-2, wd=0.0, 
     for p, (kind, st, th), t0 in zip(params, ref, thetas0):
         got = p.double().cpu().numpy().reshape(th.shape)
         t0 = t0.reshape(th.shape)
-        r = 5e-4 if (method == abi.SOAP and kind == "blocks") else 2e-4
+        r = r_scale * (5e-4 if (method == abi.SOAP and kind == "blocks") else 2e-4)
         allowed = r * np.abs(th - t0).max() + steps * 2.0 ** -23 * np.abs(t0).max()
         errs.append(np.abs(got - th).max() / allowed)  # <= 1 passes
     return errs, o
