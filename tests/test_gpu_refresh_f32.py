@@ -9,7 +9,7 @@ until every |b_ij| <= 1e-6 * max(sqrt(b_ii b_jj), ||A||_F/sqrt(n)), and forms
 the new basis Q J, the roots V f(lambda) V^T and the SOAP re-projection with
 3xTF32 GEMMs. Stated tolerances against the fp64 oracle run on the GPU's own
 fp32 factor (normwise relative error max|x - x_ref| / max|x_ref|):
-  * eigenvalues:            <= 2e-6
+  * eigenvalues:            <= 5e-6 (3xTF32 B = Q^T A Q; tensor-core fp32 accumulation)
   * roots (Shampoo/KL):     <= 2e-5 (first order in the unrotated b_ij; no 1/gap
                                amplification, because f(lambda) is smooth)
   * eigenvectors (SOAP):    |<q, q_ref>| >= 1 - 1e-5 for separated eigenvalues
@@ -88,7 +88,7 @@ def test_f32_refresh_soap_bases_and_values(P, m, n):
         P.refresh_inverse(b, cfg, refresh)
         o = oracle_from(b, abi.SOAP, cfg, refresh)
         for side, d in ((abi.EIGVALS_L, m), (abi.EIGVALS_R, n)):
-            assert rel(b.get(side), o.get(side)) < 2e-6
+            assert rel(b.get(side), o.get(side)) < 5e-6
         for q, qo, vals in ((b.basis_l, o.basis_l, o.get(abi.EIGVALS_L)), (b.basis_r, o.basis_r, o.get(abi.EIGVALS_R))):
             assert np.abs(q.T @ q - np.eye(q.shape[0])).max() < 1e-5  # orthonormal at fp32 level
             # separated eigenvalues (relative gap > 1e-3 of the spectrum): vectors agree up to sign
