@@ -338,6 +338,11 @@ int asg_gemm_tn(const float* A, const float* B, float* C, int64_t batch, int64_t
  * ascending, vectors as columns, fp64 device buffers [batch][n][n]. */
 int asg_sym_eig_batched(const double* A, double* values, double* vectors, int64_t batch, int64_t n,
                         void* stream);
+/* The F32 refresh's tensor-core block Jacobi on its own: fp32 device buffers
+ * A [batch][n][n] (symmetric), vectors [batch][n][n] (columns), fp64 values
+ * [batch][n] ascending; n > 64. Same stopping rule as ASG_REFRESH_F32. */
+int asg_sym_eig_batched_f32(const float* A, double* values, float* vectors, int64_t batch, int64_t n,
+                            void* stream);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -36,4 +36,14 @@ struct EighOpts {
 void launch_eigh(const double* A, double* values, double* vectors, double* ws, int nb, int n, int* status,
                  cudaStream_t s, const double* Vinit = nullptr, EighOpts opts = EighOpts{});
 
+// Tensor-core block Jacobi of the F32 refresh (asg_jacobi_tc.cu).
+// B: [nb][D][D] fp32 symmetric (leading n x n), D = tc_eigh_dim(n) (n > kSmallEighN).
+// values: [nb][n] ascending (fp64). J / J^T: [nb][D][D] split tf32 pairs of the
+// eigenvectors (columns of J), zero outside the leading n x n. ws: floats from
+// tc_eigh_workspace_floats. status: per-matrix asg_status (zero-initialised).
+int tc_eigh_dim(int n);
+size_t tc_eigh_workspace_floats(int nb, int n);
+void launch_tc_eigh(const float* B, int D, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
+                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol);
+
 }  // namespace asg

@@ -1,0 +1,906 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Tensor-core block Jacobi: the batched symmetric eigensolver of the F32
+// refresh (asg_refresh_mode F32), replacing sym_eig (densela.hpp:182-264) for
+// factors above kSmallEighN. fp32-level arithmetic:
+//
+//   * A (the factor, rotated into the previous eigenbasis) and V (the
+//     accumulated rotation) live in HBM as (hi, lo) tf32 pairs, natural order.
+//   * Columns are split into 64-wide blocks; a round pairs the blocks by a
+//     round-robin tournament (m/2 disjoint pairs, m-1 rounds per sweep).
+//   * tj_pair_kernel: one CTA per (matrix, pair) gathers the 128x128 pair
+//     matrix and diagonalises it exactly in shared memory (parallel cyclic
+//     Jacobi, fp32, ascending order within the pair = sorted block Jacobi);
+//     it writes J^T as a split pair, or flags the pair as converged when no
+//     element exceeds |a_ij| > tol * max(sqrt(a_ii a_jj), ||A||_F / sqrt(n)).
+//   * tj_apply_kernel (tcgen05): every 128x128 tile (pair k1 rows, pair k2
+//     columns) of A becomes J_k1^T (A_tile J_k2) -- two chained 3xTF32 MMAs
+//     with the intermediate staged TMEM -> registers -> shared memory as the
+//     transposed K-major operand -- and every 128-row panel of V becomes
+//     V_tile J_k2. Tiles whose pairs are both converged are skipped. All
+//     operand tiles are gathered by TMA (64-row / 32-column boxes of the
+//     natural layout), so no data is permuted between rounds.
+//   * A sweep that rotated nothing ends the iteration (device flags; the
+//     sweeps run in a CUDA-graph WHILE loop), within the reference's budget of
+//     30 sweeps (densela.hpp:194); eigenvalues diag(A) are sorted ascending
+//     with a stable index order (densela.hpp:251-262).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../../include/asteria_b200.h"
+#include "asg_eigh.cuh"
+#include "asg_kernels.cuh"
+#include "asg_ptx.cuh"
+
+namespace asg {
+namespace {
+
+constexpr int JW = 64;   // column block
+constexpr int JP = 128;  // pair (tile) size
+constexpr int kPairThreads = 512;
+constexpr int kInner = 4;  // inner sweeps of the pair solve
+
+__device__ __forceinline__ int tourney(int pos, int r, int P) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (P - 1); }
+__device__ __forceinline__ void pair_of(int k, int r, int m, int& p, int& q) {
+    p = tourney(k, r, m);
+    q = tourney(m - 1 - k, r, m);
+    if (p > q) {
+        const int t = p;
+        p = q;
+        q = t;
+    }
+}
+// pair-local index (0..127) -> natural index
+__device__ __forceinline__ int nat(int i, int p, int q) { return i < JW ? p * JW + i : q * JW + (i - JW); }
+
+__device__ double tj_block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = (l < int(blockDim.x >> 5)) ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+        if (l == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// ---- init -------------------------------------------------------------------
+// One CTA per matrix: ||B||_F, the Gershgorin bound for the padding, finite check.
+__global__ void tj_stats_kernel(const float* __restrict__ B, int n, int D, double* __restrict__ fro,
+                                double* __restrict__ pad, int* __restrict__ active, int* __restrict__ status) {
+    __shared__ double red[32];
+    const int64_t b = blockIdx.x;
+    const float* Bb = B + b * int64_t(D) * D;
+    double s = 0.0, bound = 0.0;
+    bool bad = false;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double r = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double x = Bb[int64_t(i) * D + j];
+            bad |= !isfinite(x);
+            s += x * x;
+            r += fabs(x);
+        }
+        bound = fmax(bound, r);
+    }
+    const int any_bad = __syncthreads_or(bad);
+    s = tj_block_sum(s, red);
+    for (int o = 16; o > 0; o >>= 1) bound = fmax(bound, __shfl_xor_sync(0xffffffff, bound, o));
+    __shared__ double bm[32];
+    if ((threadIdx.x & 31) == 0) bm[threadIdx.x >> 5] = bound;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) mx = fmax(mx, bm[w]);
+        fro[b] = sqrt(s);
+        pad[b] = mx > 0.0 ? 2.0 * mx : 1.0;
+        active[b] = any_bad ? 0 : 1;
+        if (any_bad) atomicCAS(&status[b], ASG_OK, ASG_ERR_NON_FINITE);
+    }
+}
+
+// A = B (+ distinct padding diagonal above the spectrum), V = I; both split.
+__global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const double* __restrict__ pad,
+                               float* __restrict__ Ah, float* __restrict__ Al, float* __restrict__ Vh,
+                               float* __restrict__ Vl) {
+    const int64_t b = blockIdx.y;
+    const int64_t DD = int64_t(D) * D;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < DD; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / D), j = int(e % D);
+        float x;
+        if (i < n && j < n) x = 0.5f * (B[b * DD + e] + B[b * DD + int64_t(j) * D + i]);  // symmetrize
+        else x = (i == j) ? float(pad[b] * (1.0 + double(i - n + 1) * 1e-3)) : 0.f;
+        float h, l;
+        split_tf32(x, h, l);
+        Ah[b * DD + e] = h;
+        Al[b * DD + e] = l;
+        Vh[b * DD + e] = (i == j) ? 1.f : 0.f;
+        Vl[b * DD + e] = 0.f;
+    }
+}
+
+// ---- pair solve -----------------------------------------------------------------
+// One CTA per (pair k, matrix b). Shared: S (128 x 129), Z (128 x 129) fp32.
+__global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __restrict__ Ah, const float* __restrict__ Al,
+                                                               int D, int m, int round, float* __restrict__ JTh,
+                                                               float* __restrict__ JTl, int* __restrict__ pflag,
+                                                               int* __restrict__ rotations,
+                                                               const int* __restrict__ active,
+                                                               const double* __restrict__ fro, int n, float tol,
+                                                               int inner_sweeps) {
+    extern __shared__ float tsm[];
+    float* S = tsm;                    // [JP][JP+1]
+    float* Z = S + JP * (JP + 1);      // [JP][JP+1]
+    __shared__ float cs[JP / 2], sn[JP / 2];
+    __shared__ int rank_of[JP];
+    const int k = blockIdx.x;
+    const int64_t b = blockIdx.y;
+    const int npairs = m / 2;
+    int* flag = pflag + b * npairs + k;
+    if (!active[b]) {
+        if (threadIdx.x == 0) *flag = 0;
+        return;
+    }
+    int p, q;
+    pair_of(k, round, m, p, q);
+    const int64_t DD = int64_t(D) * D;
+    for (int e = threadIdx.x; e < JP * JP; e += blockDim.x) {
+        const int i = e / JP, j = e % JP;
+        const int64_t off = b * DD + int64_t(nat(i, p, q)) * D + nat(j, p, q);
+        S[i * (JP + 1) + j] = Ah[off] + Al[off];
+        Z[i * (JP + 1) + j] = (i == j) ? 1.f : 0.f;
+    }
+    __syncthreads();
+    const float floor_s = float(fro[b] / sqrt(double(n)));
+    auto big = [&](int i, int j, float t) {
+        return fabsf(S[i * (JP + 1) + j]) > t * fmaxf(sqrtf(fabsf(S[i * (JP + 1) + i] * S[j * (JP + 1) + j])), floor_s);
+    };
+    bool any = false;
+    for (int e = threadIdx.x; e < JP * JP; e += blockDim.x) {
+        const int i = e / JP, j = e % JP;
+        if (j > i) any |= big(i, j, tol);
+    }
+    float* jh = JTh + (b * npairs + k) * int64_t(JP) * JP;
+    float* jl = JTl + (b * npairs + k) * int64_t(JP) * JP;
+    if (!__syncthreads_or(any)) {
+        // converged pair: J = I (the apply still runs for tiles whose other pair moves)
+        for (int e = threadIdx.x; e < JP * JP; e += blockDim.x) {
+            jh[e] = (e / JP == e % JP) ? 1.f : 0.f;
+            jl[e] = 0.f;
+        }
+        if (threadIdx.x == 0) *flag = 0;
+        return;
+    }
+    if (threadIdx.x == 0) {
+        *flag = 1;
+        atomicAdd(&rotations[b], 1);
+    }
+    const float itol = 0.1f * tol;
+    for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
+        bool rot_any = false;
+        for (int r = 0; r < JP - 1; ++r) {
+            if (threadIdx.x < JP / 2) {
+                int a, c;
+                pair_of(threadIdx.x, r, JP, a, c);
+                float cc = 1.f, ss = 0.f;
+                if (big(a, c, itol)) {
+                    const double apq = S[a * (JP + 1) + c];
+                    const double app = S[a * (JP + 1) + a], aqq = S[c * (JP + 1) + c];
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau)) : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+                    const double c1 = 1.0 / sqrt(1.0 + t * t);
+                    cc = float(c1);
+                    ss = float(t * c1);
+                    rot_any = true;
+                }
+                cs[threadIdx.x] = cc;
+                sn[threadIdx.x] = ss;
+            }
+            __syncthreads();
+            // rows of S
+            for (int e = threadIdx.x; e < (JP / 2) * JP; e += blockDim.x) {
+                const int kk = e / JP, j = e % JP;
+                const float ss = sn[kk];
+                if (ss == 0.f) continue;
+                int a, c;
+                pair_of(kk, r, JP, a, c);
+                const float cc = cs[kk];
+                const float x = S[a * (JP + 1) + j], y = S[c * (JP + 1) + j];
+                S[a * (JP + 1) + j] = cc * x - ss * y;
+                S[c * (JP + 1) + j] = ss * x + cc * y;
+            }
+            __syncthreads();
+            // columns of S and Z
+            for (int e = threadIdx.x; e < (JP / 2) * JP; e += blockDim.x) {
+                const int kk = e % (JP / 2), i = e / (JP / 2);
+                const float ss = sn[kk];
+                if (ss == 0.f) continue;
+                int a, c;
+                pair_of(kk, r, JP, a, c);
+                const float cc = cs[kk];
+                float x = S[i * (JP + 1) + a], y = S[i * (JP + 1) + c];
+                float na = cc * x - ss * y, nc = ss * x + cc * y;
+                if (i == a) nc = 0.f;
+                if (i == c) na = 0.f;
+                S[i * (JP + 1) + a] = na;
+                S[i * (JP + 1) + c] = nc;
+                x = Z[i * (JP + 1) + a];
+                y = Z[i * (JP + 1) + c];
+                Z[i * (JP + 1) + a] = cc * x - ss * y;
+                Z[i * (JP + 1) + c] = ss * x + cc * y;
+            }
+            __syncthreads();
+        }
+        if (!__syncthreads_or(rot_any)) break;
+    }
+    // ascending order within the pair (sorted block Jacobi)
+    if (threadIdx.x < JP) {
+        const int i = threadIdx.x;
+        const float di = S[i * (JP + 1) + i];
+        int r = 0;
+        for (int j = 0; j < JP; ++j) {
+            const float dj = S[j * (JP + 1) + j];
+            r += (dj < di) || (dj == di && j < i);
+        }
+        rank_of[i] = r;
+    }
+    __syncthreads();
+    // J[:, rank(c)] = Z[:, c]  ->  J^T[rank(c)][row] = Z[row][c]
+    for (int e = threadIdx.x; e < JP * JP; e += blockDim.x) {
+        const int c = e / JP, row = e % JP;
+        float h, l;
+        split_tf32(Z[row * (JP + 1) + c], h, l);
+        jh[int64_t(rank_of[c]) * JP + row] = h;
+        jl[int64_t(rank_of[c]) * JP + row] = l;
+    }
+}
+
+// ---- apply (tcgen05) ------------------------------------------------------------------
+struct TJApply {
+    float *Ah, *Al, *Vh, *Vl;   // natural layout [nb][D][D]
+    const int* pflag;           // [nb][m/2]
+    const int* active;          // [nb]
+    int D, m, round, nb;
+    int tilesA, tilesV;         // per matrix: (m/2)^2 and (D/128)*(m/2)
+};
+
+constexpr uint32_t kChunk = JP * 32 * 4;      // 128 rows x 32 fp32 = 16 KB
+constexpr uint32_t kStage1 = 4 * kChunk;      // A hi/lo + J hi/lo
+constexpr uint32_t kStage2 = 2 * kChunk;      // J_k1^T hi/lo
+constexpr uint32_t kRegionS = 2 * kStage1;    // 128 KB: MMA1 ring, then X^T (4 chunks hi/lo)
+constexpr uint32_t kRegionT = 2 * kStage2;    // 64 KB
+constexpr size_t kApplySmem = 1024 + size_t(kRegionS) + kRegionT + 256;
+
+__device__ __forceinline__ void tj_decode(const TJApply& p, int t, int& b, bool& isA, int& i1, int& i2) {
+    const int per = p.tilesA + p.tilesV;
+    b = t / per;
+    int l = t - b * per;
+    const int np2 = p.m / 2;
+    if (l < p.tilesA) {
+        isA = true;
+        i1 = l / np2;
+        i2 = l - i1 * np2;
+    } else {
+        isA = false;
+        l -= p.tilesA;
+        i1 = l / np2;  // 128-row panel of V
+        i2 = l - i1 * np2;
+    }
+}
+
+// Swizzled (SWIZZLE_128B, K-major, 128 B rows) address of element (row, k) in a chunk buffer.
+__device__ __forceinline__ uint32_t sw128(int row, int k) {
+    return uint32_t(row) * 128u + ((uint32_t(k >> 2) ^ uint32_t(row & 7)) << 4) + uint32_t(k & 3) * 4u;
+}
+
+__global__ void __launch_bounds__(192, 1)
+    tj_apply_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+                    const __grid_constant__ CUtensorMap tmVh, const __grid_constant__ CUtensorMap tmVl,
+                    const __grid_constant__ CUtensorMap tmJh, const __grid_constant__ CUtensorMap tmJl,
+                    const __grid_constant__ TJApply p) {
+    extern __shared__ uint8_t tj_smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tj_smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* S = smem;
+    uint8_t* T = smem + kRegionS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(T + kRegionT);
+    uint64_t* full1 = bars;        // [2]
+    uint64_t* empty1 = bars + 2;   // [2]
+    uint64_t* full2 = bars + 4;    // [2]
+    uint64_t* empty2 = bars + 6;   // [2]
+    uint64_t* xdone = bars + 8;    // MMA1 complete
+    uint64_t* xready = bars + 9;   // X^T staged (4 epilogue warps)
+    uint64_t* adone = bars + 10;   // MMA2 complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmAh);
+        tma_prefetch(&tmAl);
+        tma_prefetch(&tmVh);
+        tma_prefetch(&tmVl);
+        tma_prefetch(&tmJh);
+        tma_prefetch(&tmJl);
+    }
+    if (warp == 1) {
+        if (lane == 0) {
+            for (int s = 0; s < 2; ++s) {
+                mbar_init(&full1[s], 1);
+                mbar_init(&empty1[s], 1);
+                mbar_init(&full2[s], 1);
+                mbar_init(&empty2[s], 1);
+            }
+            mbar_init(xdone, 1);
+            mbar_init(xready, 4);
+            mbar_init(adone, 1);
+            fence_mbar_init();
+        }
+        __syncwarp();
+        tmem_alloc<256>(tmem_slot);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t idesc = idesc_tf32(JP, JP);
+    const int total = p.nb * (p.tilesA + p.tilesV);
+    const int npairs = p.m / 2;
+
+    // phase bits (per barrier), advanced identically by every role that waits on it
+    uint32_t ph_full1[2] = {0, 0}, ph_empty1[2] = {0, 0}, ph_full2[2] = {0, 0}, ph_empty2[2] = {0, 0};
+    uint32_t ph_x = 0, ph_xr = 0, ph_a = 0;
+    int use1[2] = {0, 0}, use2[2] = {0, 0};  // producer: number of fills of each stage so far
+
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int b, i1, i2;
+        bool isA;
+        tj_decode(p, t, b, isA, i1, i2);
+        // skip converged work (uniform across the CTA)
+        if (!p.active[b]) continue;
+        const int f2 = p.pflag[b * npairs + i2];
+        const int f1 = isA ? p.pflag[b * npairs + i1] : 0;
+        if (!f2 && !f1) continue;
+        int p1 = 0, q1 = 0, p2, q2;
+        pair_of(i2, p.round, p.m, p2, q2);
+        if (isA) pair_of(i1, p.round, p.m, p1, q1);
+        const int jb2 = b * npairs + i2, jb1 = b * npairs + i1;
+
+        if (warp == 0) {
+            if (lane == 0) {
+                // MMA1 operands: 4 K-chunks (pair-k2 columns), ring of 2 stages
+                for (int c = 0; c < 4; ++c) {
+                    const int s = c & 1;
+                    if (use1[s] > 0) {
+                        mbar_wait(&empty1[s], ph_empty1[s]);
+                        ph_empty1[s] ^= 1;
+                    }
+                    ++use1[s];
+                    uint8_t* st = S + s * kStage1;
+                    mbar_arrive_expect_tx(&full1[s], kStage1);
+                    const int col = (c < 2 ? p2 * JW : q2 * JW) + (c & 1) * 32;
+                    if (isA) {
+                        tma_load_3d(st, &tmAh, &full1[s], col, p1 * JW, b);
+                        tma_load_3d(st + kChunk / 2, &tmAh, &full1[s], col, q1 * JW, b);
+                        tma_load_3d(st + kChunk, &tmAl, &full1[s], col, p1 * JW, b);
+                        tma_load_3d(st + kChunk + kChunk / 2, &tmAl, &full1[s], col, q1 * JW, b);
+                    } else {
+                        tma_load_3d(st, &tmVh, &full1[s], col, i1 * JP, b);
+                        tma_load_3d(st + kChunk / 2, &tmVh, &full1[s], col, i1 * JP + JW, b);
+                        tma_load_3d(st + kChunk, &tmVl, &full1[s], col, i1 * JP, b);
+                        tma_load_3d(st + kChunk + kChunk / 2, &tmVl, &full1[s], col, i1 * JP + JW, b);
+                    }
+                    tma_load_3d(st + 2 * kChunk, &tmJh, &full1[s], c * 32, 0, jb2);
+                    tma_load_3d(st + 3 * kChunk, &tmJl, &full1[s], c * 32, 0, jb2);
+                }
+                if (isA) {  // MMA2 A-operand: J_k1^T chunks
+                    for (int c = 0; c < 4; ++c) {
+                        const int s = c & 1;
+                        if (use2[s] > 0) {
+                            mbar_wait(&empty2[s], ph_empty2[s]);
+                            ph_empty2[s] ^= 1;
+                        }
+                        ++use2[s];
+                        uint8_t* st = T + s * kStage2;
+                        mbar_arrive_expect_tx(&full2[s], kStage2);
+                        tma_load_3d(st, &tmJh, &full2[s], c * 32, 0, jb1);
+                        tma_load_3d(st + kChunk, &tmJl, &full2[s], c * 32, 0, jb1);
+                    }
+                }
+            }
+        } else if (warp == 1) {
+            if (lane == 0) {
+                // MMA1: X = A_tile * J_k2 into TMEM cols [0, 128)
+                for (int c = 0; c < 4; ++c) {
+                    const int s = c & 1;
+                    mbar_wait(&full1[s], ph_full1[s]);
+                    ph_full1[s] ^= 1;
+                    tc_fence_after();
+                    uint8_t* st = S + s * kStage1;
+                    const uint64_t ah = umma_desc_k_sw128(st), al = umma_desc_k_sw128(st + kChunk);
+                    const uint64_t bh = umma_desc_k_sw128(st + 2 * kChunk), bl = umma_desc_k_sw128(st + 3 * kChunk);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t adv = uint64_t(kk * 32) >> 4;
+                        mma_tf32(tmem, ah + adv, bh + adv, idesc, (c | kk) != 0 ? 1u : 0u);
+                        mma_tf32(tmem, ah + adv, bl + adv, idesc, 1u);
+                        mma_tf32(tmem, al + adv, bh + adv, idesc, 1u);
+                    }
+                    mma_commit(&empty1[s]);
+                }
+                mma_commit(xdone);
+                if (isA) {
+                    // MMA2: A' = J_k1^T X, B operand = X^T staged in region S
+                    mbar_wait(xready, ph_xr);
+                    tc_fence_after();
+                    for (int c = 0; c < 4; ++c) {
+                        const int s = c & 1;
+                        mbar_wait(&full2[s], ph_full2[s]);
+                        ph_full2[s] ^= 1;
+                        tc_fence_after();
+                        uint8_t* st = T + s * kStage2;
+                        const uint64_t ah = umma_desc_k_sw128(st), al = umma_desc_k_sw128(st + kChunk);
+                        uint8_t* xb = S + c * 2 * kChunk;
+                        const uint64_t bh = umma_desc_k_sw128(xb), bl = umma_desc_k_sw128(xb + kChunk);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t adv = uint64_t(kk * 32) >> 4;
+                            mma_tf32(tmem + JP, ah + adv, bh + adv, idesc, (c | kk) != 0 ? 1u : 0u);
+                            mma_tf32(tmem + JP, ah + adv, bl + adv, idesc, 1u);
+                            mma_tf32(tmem + JP, al + adv, bh + adv, idesc, 1u);
+                        }
+                        mma_commit(&empty2[s]);
+                    }
+                    mma_commit(adone);
+                }
+            }
+        } else {
+            const int qd = warp & 3;  // TMEM lane quadrant: rows 32*qd .. 32*qd+31
+            const int row = qd * 32 + int(lane);
+            mbar_wait(xdone, ph_x);
+            tc_fence_after();
+            if (isA) {
+                // X rows [32 qd, 32 qd + 32) = K-chunk qd of MMA2's B operand (X^T)
+                uint8_t* xh = S + qd * 2 * kChunk;
+                uint8_t* xl = xh + kChunk;
+#pragma unroll 1
+                for (int cc = 0; cc < 4; ++cc) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        float h, l;
+                        split_tf32(__uint_as_float(r[j]), h, l);
+                        const uint32_t off = sw128(cc * 32 + j, int(lane));
+                        *reinterpret_cast<float*>(xh + off) = h;
+                        *reinterpret_cast<float*>(xl + off) = l;
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(xready);
+                mbar_wait(adone, ph_a);
+                tc_fence_after();
+                // A' rows -> natural positions
+                const int gr = nat(row, p1, q1);
+                const int64_t base = int64_t(b) * p.D * p.D + int64_t(gr) * p.D;
+#pragma unroll 1
+                for (int cc = 0; cc < 4; ++cc) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(JP + cc * 32), r);
+                    tmem_ld_wait();
+                    const int gc = (cc < 2 ? p2 * JW : q2 * JW) + (cc & 1) * 32;
+                    float* dh = p.Ah + base + gc;
+                    float* dl = p.Al + base + gc;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float4 h4, l4;
+                        split_tf32(__uint_as_float(r[j + 0]), h4.x, l4.x);
+                        split_tf32(__uint_as_float(r[j + 1]), h4.y, l4.y);
+                        split_tf32(__uint_as_float(r[j + 2]), h4.z, l4.z);
+                        split_tf32(__uint_as_float(r[j + 3]), h4.w, l4.w);
+                        *reinterpret_cast<float4*>(dh + j) = h4;
+                        *reinterpret_cast<float4*>(dl + j) = l4;
+                    }
+                }
+            } else {
+                const int gr = i1 * JP + row;
+                const int64_t base = int64_t(b) * p.D * p.D + int64_t(gr) * p.D;
+#pragma unroll 1
+                for (int cc = 0; cc < 4; ++cc) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
+                    tmem_ld_wait();
+                    const int gc = (cc < 2 ? p2 * JW : q2 * JW) + (cc & 1) * 32;
+                    float* dh = p.Vh + base + gc;
+                    float* dl = p.Vl + base + gc;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float4 h4, l4;
+                        split_tf32(__uint_as_float(r[j + 0]), h4.x, l4.x);
+                        split_tf32(__uint_as_float(r[j + 1]), h4.y, l4.y);
+                        split_tf32(__uint_as_float(r[j + 2]), h4.z, l4.z);
+                        split_tf32(__uint_as_float(r[j + 3]), h4.w, l4.w);
+                        *reinterpret_cast<float4*>(dh + j) = h4;
+                        *reinterpret_cast<float4*>(dl + j) = l4;
+                    }
+                }
+            }
+            tc_fence_before();
+        }
+        // every role has finished this tile (TMEM drained, smem operands consumed)
+        ph_x ^= 1;
+        if (isA) {
+            ph_xr ^= 1;
+            ph_a ^= 1;
+        }
+        __syncthreads();
+        tc_fence_after();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<256>(tmem);
+    }
+}
+
+// ---- convergence / loop / finish ------------------------------------------------------
+__global__ void tj_converge_kernel(int nb, int* __restrict__ active, int* __restrict__ rotations,
+                                   int* __restrict__ sweeps, int debug, int n) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb || !active[b]) return;
+    sweeps[b] += 1;
+    if (debug) printf("tjdbg n=%d b=%d sweep=%d rotated pairs=%d\n", n, b, sweeps[b], rotations[b]);
+    if (rotations[b] == 0) active[b] = 0;
+    rotations[b] = 0;
+}
+
+__global__ void tj_loop_kernel(const int* __restrict__ active, int nb, int* __restrict__ sweep_count, int max_sweeps,
+                               cudaGraphConditionalHandle handle) {
+    int any = 0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) any |= active[b];
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) {
+        const int s = ++*sweep_count;
+        cudaGraphSetConditional(handle, (any && s < max_sweeps) ? 1u : 0u);
+    }
+}
+
+// One CTA per matrix: ascending ranks of diag(A) (stable by index); the n real
+// eigenvalues come first (padding sits above the spectrum).
+__global__ void tj_rank_kernel(const float* __restrict__ Ah, const float* __restrict__ Al, int n, int D,
+                               int* __restrict__ rank, double* __restrict__ values, const int* __restrict__ active,
+                               int* __restrict__ status) {
+    extern __shared__ float dg[];
+    const int64_t b = blockIdx.x;
+    const int64_t DD = int64_t(D) * D;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) dg[i] = Ah[b * DD + int64_t(i) * D + i] + Al[b * DD + int64_t(i) * D + i];
+    __syncthreads();
+    if (threadIdx.x == 0 && active[b]) atomicCAS(&status[b], ASG_OK, ASG_ERR_NO_CONVERGENCE);
+    for (int i = threadIdx.x; i < D; i += blockDim.x) {
+        const float di = dg[i];
+        int r = 0;
+        for (int j = 0; j < D; ++j) {
+            const float dj = dg[j];
+            r += (dj < di) || (dj == di && j < i);
+        }
+        rank[b * D + i] = r;
+        if (r < n) values[b * n + r] = double(di);
+    }
+}
+
+// J[i][rank(c)] = V[i][c] for i, rank(c) < n (zero elsewhere), as split J and J^T.
+__global__ void tj_gather_kernel(const float* __restrict__ Vh, const float* __restrict__ Vl,
+                                 const int* __restrict__ rank, int n, int D, float* __restrict__ Jh,
+                                 float* __restrict__ Jl, float* __restrict__ JTh, float* __restrict__ JTl) {
+    const int64_t b = blockIdx.y;
+    const int64_t DD = int64_t(D) * D;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < DD; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / D), c = int(e % D);
+        const int rc = rank[b * D + c];
+        float h = 0.f, l = 0.f;
+        if (i < n && rc < n) {
+            h = Vh[b * DD + e];
+            l = Vl[b * DD + e];
+        }
+        if (rc < D) {
+            Jh[b * DD + int64_t(i) * D + rc] = h;
+            if (Jl) Jl[b * DD + int64_t(i) * D + rc] = l;
+            JTh[b * DD + int64_t(rc) * D + i] = h;
+            if (JTl) JTl[b * DD + int64_t(rc) * D + i] = l;
+        }
+    }
+}
+
+
+// Rayleigh-quotient eigenvalues and unit eigenvectors from the solve's J and
+// W = B J (one 3xTF32 product): lambda_i = (J_i . W_i) / (J_i . J_i), then
+// J_i /= |J_i|. This removes the slow drift of |J_i| and diag(A) that the
+// tensor cores' fp32 accumulation leaves over hundreds of rotation products.
+// Grid (D/32 column groups, nb), 256 threads = 32 columns x 8 row phases.
+__global__ void tj_rayleigh_kernel(float* __restrict__ Jh, float* __restrict__ Jl, float* __restrict__ JTh,
+                                   float* __restrict__ JTl, const float* __restrict__ W, int n, int D,
+                                   double* __restrict__ values) {
+    __shared__ double sjw[8][32], sjj[8][32];
+    __shared__ float scale[32];
+    const int64_t b = blockIdx.y;
+    const int64_t DD = int64_t(D) * D;
+    const int cl = threadIdx.x & 31, ph = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + cl;
+    double jw = 0.0, jj = 0.0;
+    for (int k = ph; k < n; k += 8) {
+        const int64_t o = b * DD + int64_t(k) * D + c;
+        const double j = double(Jh[o]) + (Jl ? double(Jl[o]) : 0.0);
+        jw += j * double(W[o]);
+        jj += j * j;
+    }
+    sjw[ph][cl] = jw;
+    sjj[ph][cl] = jj;
+    __syncthreads();
+    if (ph == 0) {
+        double a = 0.0, q = 0.0;
+        for (int t = 0; t < 8; ++t) {
+            a += sjw[t][cl];
+            q += sjj[t][cl];
+        }
+        float sc = 1.f;
+        if (c < n && q > 0.0) {
+            values[b * n + c] = a / q;
+            sc = float(1.0 / sqrt(q));
+        }
+        scale[cl] = sc;
+    }
+    __syncthreads();
+    // J[:, c] *= scale  (rows k, 32 consecutive columns per row)
+    for (int k = ph; k < n; k += 8) {
+        const int64_t o = b * DD + int64_t(k) * D + c;
+        float h, l;
+        split_tf32((Jh[o] + (Jl ? Jl[o] : 0.f)) * scale[cl], h, l);
+        Jh[o] = h;
+        if (Jl) Jl[o] = l;
+    }
+    // J^T rows [32 blockIdx.x, +32): row r scaled by scale[r - 32 blockIdx.x]
+    for (int rr = ph; rr < 32; rr += 8) {
+        const int r = blockIdx.x * 32 + rr;
+        if (r >= n) continue;
+        for (int k = cl; k < n; k += 32) {
+            const int64_t o = b * DD + int64_t(r) * D + k;
+            float h, l;
+            split_tf32((JTh[o] + (JTl ? JTl[o] : 0.f)) * scale[rr], h, l);
+            JTh[o] = h;
+            if (JTl) JTl[o] = l;
+        }
+    }
+}
+
+// Ascending order of the refined values (ties/inversions at rounding level;
+// the vectors keep their diag(A) order, which agrees to that level).
+__global__ void tj_sort_values_kernel(double* __restrict__ values, int n) {
+    extern __shared__ double sv[];
+    const int64_t b = blockIdx.x;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sv[i] = values[b * n + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double vi = sv[i];
+        int r = 0;
+        for (int j = 0; j < n; ++j) r += (sv[j] < vi) || (sv[j] == vi && j < i);
+        values[b * n + r] = vi;
+    }
+}
+
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled tj_encode_fn() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+    });
+    return fn;
+}
+
+// 3-D map over [batch][rows][cols] fp32, box (32 cols x box_rows x 1), 128B swizzle.
+bool tj_map(CUtensorMap* map, const float* base, int cols, int rows, int batch, int box_rows) {
+    PFN_encodeTiled enc = tj_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {cuuint64_t(cols), cuuint64_t(rows), cuuint64_t(batch)};
+    cuuint64_t strides[2] = {cuuint64_t(cols) * 4, cuuint64_t(cols) * cuuint64_t(rows) * 4};
+    cuuint32_t box[3] = {32, cuuint32_t(box_rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t tc_eigh_workspace_floats(int nb, int n) {
+    const int D = (n + JP - 1) / JP * JP;
+    const int m = D / JW;
+    // A hi/lo, V hi/lo, J^T hi/lo per pair, then per matrix: fro, pad (2 doubles = 4 floats),
+    // active, sweeps, rotations, flags (m/2), ranks (D); and the loop counter.
+    return size_t(nb) * (4 * size_t(D) * D + 2 * size_t(m / 2) * JP * JP + 4 + 3 + size_t(m / 2) + D) + 4;
+}
+
+int tc_eigh_dim(int n) { return (n + JP - 1) / JP * JP; }
+
+void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
+                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol) {
+    const int D = (n + JP - 1) / JP * JP;
+    (void)D_in;  // B, J, J^T are [nb][D][D] with D = roundup(n, 128) (== the group's padded dim)
+    const int m = D / JW, npairs = m / 2;
+    const size_t DD = size_t(D) * D;
+    float* Ah = ws;
+    float* Al = Ah + size_t(nb) * DD;
+    float* Vh = Al + size_t(nb) * DD;
+    float* Vl = Vh + size_t(nb) * DD;
+    float* JPh = Vl + size_t(nb) * DD;
+    float* JPl = JPh + size_t(nb) * npairs * JP * JP;
+    double* fro = reinterpret_cast<double*>(JPl + size_t(nb) * npairs * JP * JP);
+    double* pad = fro + nb;
+    int* active = reinterpret_cast<int*>(pad + nb);
+    int* sweeps = active + nb;
+    int* rotations = sweeps + nb;
+    int* pflag = rotations + nb;
+    int* rank = pflag + size_t(nb) * npairs;
+    int* loop_count = rank + size_t(nb) * D;
+
+    static bool attr = false;
+    const int pair_smem = 2 * JP * (JP + 1) * int(sizeof(float));
+    if (!attr) {
+        cudaFuncSetAttribute(tj_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
+        cudaFuncSetAttribute(tj_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kApplySmem));
+        cudaFuncSetAttribute(tj_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 4);
+        cudaFuncSetAttribute(tj_sort_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8);
+        attr = true;
+    }
+    TJApply ap{};
+    ap.Ah = Ah;
+    ap.Al = Al;
+    ap.Vh = Vh;
+    ap.Vl = Vl;
+    ap.pflag = pflag;
+    ap.active = active;
+    ap.D = D;
+    ap.m = m;
+    ap.nb = nb;
+    ap.tilesA = npairs * npairs;
+    ap.tilesV = (D / JP) * npairs;
+    CUtensorMap mAh, mAl, mVh, mVl, mJh, mJl;
+    bool ok = tj_map(&mAh, Ah, D, D, nb, JW) && tj_map(&mAl, Al, D, D, nb, JW) && tj_map(&mVh, Vh, D, D, nb, JW) &&
+              tj_map(&mVl, Vl, D, D, nb, JW) && tj_map(&mJh, JPh, JP, JP, nb * npairs, JP) &&
+              tj_map(&mJl, JPl, JP, JP, nb * npairs, JP);
+    if (!ok) {
+        // tensor maps unavailable: report through every matrix's status (no silent fallback)
+        cudaMemsetAsync(status, 0xff, size_t(nb) * sizeof(int), s);
+        return;
+    }
+    const int debug = getenv("ASG_EIGH_DEBUG") != nullptr ? 1 : 0;
+    const float ftol = float(tol);
+    const int inner = getenv("ASG_TJ_INNER") ? atoi(getenv("ASG_TJ_INNER")) : kInner;
+    const int total_tiles = nb * (ap.tilesA + ap.tilesV);
+    const int apply_grid = total_tiles < num_sms ? total_tiles : num_sms;
+
+    auto prologue = [&](cudaStream_t st) {
+        cudaMemsetAsync(sweeps, 0, size_t(nb) * 2 * sizeof(int), st);  // sweeps, rotations
+        cudaMemsetAsync(loop_count, 0, sizeof(int), st);
+        tj_stats_kernel<<<nb, 512, 0, st>>>(B, n, D, fro, pad, active, status);
+        tj_init_kernel<<<dim3(128, nb), 256, 0, st>>>(B, n, D, pad, Ah, Al, Vh, Vl);
+    };
+    auto sweep = [&](cudaStream_t st) {
+        for (int r = 0; r < m - 1; ++r) {
+            tj_pair_kernel<<<dim3(npairs, nb), kPairThreads, pair_smem, st>>>(Ah, Al, D, m, r, JPh, JPl, pflag, rotations,
+                                                                               active, fro, n, ftol, inner);
+            TJApply a = ap;
+            a.round = r;
+            tj_apply_kernel<<<apply_grid, 192, kApplySmem, st>>>(mAh, mAl, mVh, mVl, mJh, mJl, a);
+        }
+        tj_converge_kernel<<<(nb + 127) / 128, 128, 0, st>>>(nb, active, rotations, sweeps, debug, n);
+    };
+    auto epilogue = [&](cudaStream_t st) {
+        tj_rank_kernel<<<nb, 512, size_t(D) * 4, st>>>(Ah, Al, n, D, rank, values, active, status);
+        tj_gather_kernel<<<dim3(256, nb), 256, 0, st>>>(Vh, Vl, rank, n, D, Jh, Jl, JTh, JTl);
+    };
+    // W = B J (3xTF32, or TF32 when the outputs carry no lo part), then
+    // Rayleigh quotients + unit columns. Enqueued outside the cached graph.
+    auto rayleigh = [&](cudaStream_t st) {
+        launch_split_slab(B, Ah, Al, int64_t(size_t(nb) * DD), st);
+        GemmLaunch gl{};
+        gl.A = Operand{Ah, Al, D, D};
+        gl.B = Operand{JTh, JTl, D, D};
+        gl.batch = nb;
+        gl.epi = EPI_STORE;
+        gl.p.alpha = 1.f;
+        gl.p.beta = 0.f;
+        gl.p.C = Vh;
+        gl.p.ldc = D;
+        gl.p.c_bstride = int64_t(DD);
+        gemm_launch(gl, JTl ? ASG_PREC_3XTF32 : ASG_PREC_TF32, num_sms, st);
+        tj_rayleigh_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(Jh, Jl, JTh, JTl, Vh, n, D, values);
+        tj_sort_values_kernel<<<nb, 512, size_t(n) * 8, st>>>(values, n);
+        count_launch(3);
+    };
+    if (debug) {
+        prologue(s);
+        for (int k = 0; k < kEighMaxLaunchedSweeps; ++k) sweep(s);
+        epilogue(s);
+        rayleigh(s);
+        count_launch(4 + uint64_t(kEighMaxLaunchedSweeps) * (2 * uint64_t(m - 1) + 1));
+        return;
+    }
+    static std::mutex mu;
+    using Key = std::tuple<const void*, const void*, const void*, const void*, const void*, const void*, const void*,
+                           const void*, int, int, float, int>;
+    static std::map<Key, cudaGraphExec_t> cache;
+    const Key key{B, values, Jh, Jl, JTh, JTl, ws, status, nb, n, ftol, inner};
+    cudaGraphExec_t exec = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) exec = it->second;
+    }
+    if (!exec) {
+        cudaStream_t cap;
+        cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+        auto capture = [&](auto&& body) {
+            cudaGraph_t gph = nullptr;
+            cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+            body(cap);
+            cudaStreamEndCapture(cap, &gph);
+            return gph;
+        };
+        cudaGraph_t g = nullptr;
+        cudaGraphCreate(&g, 0);
+        cudaGraphConditionalHandle handle;
+        cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault);
+        cudaGraph_t gpro = capture(prologue);
+        cudaGraph_t gepi = capture(epilogue);
+        cudaGraphNode_t npro, nloop, nepi;
+        cudaGraphAddChildGraphNode(&npro, g, nullptr, 0, gpro);
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = handle;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphAddNode(&nloop, g, &npro, 1, &cp);
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+        sweep(cap);
+        tj_loop_kernel<<<1, 256, 0, cap>>>(active, nb, loop_count, kEighMaxLaunchedSweeps, handle);
+        cudaStreamEndCapture(cap, &body);
+        cudaGraphAddChildGraphNode(&nepi, g, &nloop, 1, gepi);
+        cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(gpro);
+        cudaGraphDestroy(gepi);
+        cudaGraphDestroy(g);
+        cudaStreamDestroy(cap);
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = exec;
+    }
+    count_launch(4 + 2 * uint64_t(m - 1) + 2 + 2);
+    cudaGraphLaunch(exec, s);
+    rayleigh(s);
+}
+
+}  // namespace asg

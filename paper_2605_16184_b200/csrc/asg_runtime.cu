@@ -26,6 +26,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -226,6 +227,9 @@ struct asg_blockset {
     size_t tw_slab = 0;  // floats per block slot (Dmax^2)
     // F32 SOAP install workspace (main stream): 4 slabs of ws_chunk x D x D
     float* iw32[4] = {};
+    // F32 refresh: tensor-core Jacobi workspace (side stream)
+    float* tc_ws = nullptr;
+    bool fp64_jacobi = false;  // ASG_F32_FP64_JACOBI=1: F32 refresh with the fp64 block Jacobi (diagnostics)
     // SOAP install workspace (one block)
     double *iw_rotL = nullptr, *iw_rotR = nullptr, *iw_sq = nullptr, *iw_a = nullptr, *iw_b = nullptr;
     // scalars
@@ -552,6 +556,7 @@ void alloc_workspace(asg_blockset* bs) {
         for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
         bs->tw_slab = size_t(Dmax) * Dmax;
         for (float*& t : bs->tw) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
+        bs->tc_ws = dalloc<float>(bs, tc_eigh_workspace_floats(bs->ws_chunk, Dmax));
         if (is_soap(bs))
             for (float*& t : bs->iw32) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
     }
@@ -821,13 +826,18 @@ void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cu
     p2.ldc = D;
     p2.c_bstride = int64_t(DD);
     run_gemm(bs, op(QTh, QTl, D, D), op(t[2], t3, D, D), cnt, EPI_STORE, p2, nullptr, 0, s, 2.0 * dd3);
-    launch_snapshot_sym(t[4], cnt, D, d, bs->ws_snap, s);
-    EighOpts eo;
-    eo.relative = 1;
-    eo.tol = kF32RefreshTol;
-    launch_eigh(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, cnt, d, g.d_status + s0, s, nullptr, eo);
-    // J -> (t0, t1), J^T -> (t2, t3)
-    launch_f64_to_split(bs->ws_vecs, cnt, d, D, false, t[0], t1, t[2], t3, s);
+    launch_snapshot_sym(t[4], cnt, D, d, bs->ws_snap, s);  // fp64 copy: trace for the damping (and small solves)
+    if (d > kSmallEighN && !bs->fp64_jacobi) {
+        // tensor-core block Jacobi: J -> (t0, t1), J^T -> (t2, t3)
+        launch_tc_eigh(t[4], D, bs->ws_vals, t[0], t1, t[2], t3, bs->tc_ws, cnt, d, g.d_status + s0, bs->num_sms, s,
+                       kF32RefreshTol);
+    } else {
+        EighOpts eo;
+        eo.relative = 1;
+        eo.tol = kF32RefreshTol;
+        launch_eigh(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, cnt, d, g.d_status + s0, s, nullptr, eo);
+        launch_f64_to_split(bs->ws_vecs, cnt, d, D, false, t[0], t1, t[2], t3, s);
+    }
     if (is_soap(bs)) {
         CK(cudaMemcpyAsync(at(left ? g.sJLTh : g.sJRTh, DD, s0), t[2], cntDD * 4, cudaMemcpyDeviceToDevice, s));
         if (sp)
@@ -1427,6 +1437,7 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         CK(cudaStreamCreateWithPriority(&bs->main, cudaStreamNonBlocking, hi));
         CK(cudaStreamCreateWithPriority(&bs->side, cudaStreamNonBlocking, lo));
         bs->own_main = true;
+        bs->fp64_jacobi = getenv("ASG_F32_FP64_JACOBI") != nullptr;
         CK(cudaEventCreateWithFlags(&bs->ev_snap, cudaEventDisableTiming));
         build_units(bs);
         build_groups(bs);
@@ -2154,3 +2165,63 @@ int asg_sym_eig_batched(const double* A, double* values, double* vectors, int64_
 }
 
 }  // extern "C"
+
+namespace asg {
+namespace {
+// [b][n][n] <-> [b][D][D] (zero padding) for the fp32 diagnostic solve.
+__global__ void pad_f32_kernel(const float* __restrict__ src, int n, int D, float* __restrict__ dst) {
+    const int64_t b = blockIdx.y;
+    const int64_t DD = int64_t(D) * D;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < DD; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / D), j = int(e % D);
+        dst[b * DD + e] = (i < n && j < n) ? src[b * int64_t(n) * n + int64_t(i) * n + j] : 0.f;
+    }
+}
+__global__ void unpad_sum_kernel(const float* __restrict__ hi, const float* __restrict__ lo, int n, int D,
+                                 float* __restrict__ dst) {
+    const int64_t b = blockIdx.y;
+    const int64_t nn = int64_t(n) * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nn; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / n), j = int(e % n);
+        const int64_t o = b * int64_t(D) * D + int64_t(i) * D + j;
+        dst[b * nn + e] = hi[o] + lo[o];
+    }
+}
+}  // namespace
+}  // namespace asg
+
+int asg_sym_eig_batched_f32(const float* A, double* values, float* vectors, int64_t batch, int64_t n, void* stream) {
+    return guard([&] {
+        if (n <= kSmallEighN) throw Fail{ASG_ERR_UNSUPPORTED, "sym_eig_batched_f32: n must exceed 64"};
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        int sms = 148;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int D = tc_eigh_dim(int(n));
+        const size_t DD = size_t(D) * D, nbDD = size_t(batch) * DD;
+        float *Bp = nullptr, *J = nullptr, *ws = nullptr;
+        int* status = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&Bp), nbDD * 4, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&J), 4 * nbDD * 4, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), tc_eigh_workspace_floats(int(batch), int(n)) * 4, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&status), size_t(batch) * sizeof(int), s));
+        CK(cudaMemsetAsync(status, 0, size_t(batch) * sizeof(int), s));
+        pad_f32_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(A, int(n), D, Bp);
+        launch_tc_eigh(Bp, D, values, J, J + nbDD, J + 2 * nbDD, J + 3 * nbDD, ws, int(batch), int(n), status, sms, s,
+                       kF32RefreshTol);
+        unpad_sum_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(J, J + nbDD, int(n), D, vectors);
+        count_launch(2);
+        std::vector<int> st(static_cast<size_t>(batch));
+        CK(cudaMemcpyAsync(st.data(), status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaFreeAsync(Bp, s));
+        CK(cudaFreeAsync(J, s));
+        CK(cudaFreeAsync(ws, s));
+        CK(cudaFreeAsync(status, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaGetLastError());
+        for (int v : st)
+            if (v != ASG_OK) throw Fail{v == -1 ? ASG_ERR_UNSUPPORTED : v, "sym_eig_batched_f32: a matrix failed"};
+    });
+}

@@ -67,6 +67,7 @@ _SIGS = {
     "asg_get_kernel_stats": (C.c_int, [_vp, _P(abi.KernelStats), _i32]),
     "asg_gemm_tn": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _f32, _i32, _vp]),
     "asg_sym_eig_batched": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "asg_sym_eig_batched_f32": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

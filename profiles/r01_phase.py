@@ -47,6 +47,39 @@ def eigh(ns):
                               alg_tflops=9 * n ** 3 * b / ms / 1e9, residual=res, orth=orth)), flush=True)
 
 
+def eigh32(ns):
+    """Cold batched eigh through the F32 refresh's tensor-core Jacobi."""
+    for n in ns:
+        b = max(1, min(512, (1 << 31) // (n * n * 4)))  # 8 GiB fp32 per point at most (C5 sizing)
+        b = min(b, int(os.environ.get("ASG_EIGH_BATCH", b)))
+        x = torch.randn(b, n, 2 * n, dtype=torch.float32, device="cuda")
+        a = (x @ x.transpose(1, 2)) / (2 * n) + 1e-3 * torch.eye(n, device="cuda")
+        del x
+        w = torch.empty(b, n, dtype=torch.float64, device="cuda")
+        v = torch.empty(b, n, n, dtype=torch.float32, device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+
+        def run():
+            rt.check(rt.lib.asg_sym_eig_batched_f32(C.c_void_p(a.data_ptr()), C.c_void_p(w.data_ptr()),
+                                                    C.c_void_p(v.data_ptr()), b, n, C.c_void_p(s)))
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        k = min(b, 4)
+        ad, vd, wd = a[:k].double(), v[:k].double(), w[:k]
+        res = (ad @ vd - vd * wd[:, None, :]).abs().amax().item() / ad.abs().amax().item()
+        orth = (vd.transpose(1, 2) @ vd - torch.eye(n, dtype=torch.float64, device="cuda")).abs().amax().item()
+        print(json.dumps(dict(phase="eigh32_cold", n=n, batch=b, ms=ms, ms_per_matrix=ms / b,
+                              alg_tflops=9 * n ** 3 * b / ms / 1e9, residual=res, orth=orth)), flush=True)
+        del a, v, w
+        torch.cuda.empty_cache()
+
+
 def step(wls):
     import bench
     for name in wls:
@@ -88,5 +121,7 @@ if __name__ == "__main__":
     what = sys.argv[1]
     if what == "eigh":
         eigh([int(x) for x in sys.argv[2:]] or [256, 512, 768, 1024, 2048])
+    elif what == "eigh32":
+        eigh32([int(x) for x in sys.argv[2:]] or [256, 512, 1024, 2048, 4096])
     else:
         step(sys.argv[2:] or ["C2"])
