@@ -46,7 +46,7 @@ namespace {
 constexpr int JW = 64;   // column block
 constexpr int JP = 128;  // pair (tile) size
 constexpr int kPairThreads = 512;
-constexpr int kInner = 4;  // inner sweeps of the pair solve
+constexpr int kInner = 1;  // inner sweeps of the pair solve (more outer sweeps are cheaper than inner ones)
 
 __device__ __forceinline__ int tourney(int pos, int r, int P) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (P - 1); }
 __device__ __forceinline__ void pair_of(int k, int r, int m, int& p, int& q) {
@@ -839,6 +839,34 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
         gemm_launch(gl, JTl ? ASG_PREC_3XTF32 : ASG_PREC_TF32, num_sms, st);
         tj_rayleigh_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(Jh, Jl, JTh, JTl, Vh, n, D, values);
         tj_sort_values_kernel<<<nb, 512, size_t(n) * 8, st>>>(values, n);
+        // one Newton-Schulz polar step on J (orthonormal to the fp32 floor):
+        // S = J^T J -> X = (3I - S)/2 -> J X; A/V slabs are free scratch here
+        GemmLaunch gs{};
+        gs.A = Operand{JTh, JTl, D, D};
+        gs.B = Operand{JTh, JTl, D, D};
+        gs.batch = nb;
+        gs.epi = EPI_STORE;
+        gs.p.alpha = 1.f;
+        gs.p.beta = 0.f;
+        gs.p.C = Vh;
+        gs.p.ldc = D;
+        gs.p.c_bstride = int64_t(DD);
+        gemm_launch(gs, JTl ? ASG_PREC_3XTF32 : ASG_PREC_TF32, num_sms, st);
+        launch_ns_x(Vh, nb, n, D, Vh, JTl ? Vl : nullptr, st);
+        GemmLaunch gx{};
+        gx.A = Operand{Jh, Jl, D, D};
+        gx.B = Operand{Vh, JTl ? Vl : nullptr, D, D};
+        gx.batch = nb;
+        gx.epi = EPI_SPLIT;
+        gx.p.alpha = 1.f;
+        gx.p.Dhi = Ah;
+        gx.p.Dlo = JTl ? Al : nullptr;
+        gx.p.ldd = D;
+        gx.p.d_bstride = int64_t(DD);
+        gemm_launch(gx, JTl ? ASG_PREC_3XTF32 : ASG_PREC_TF32, num_sms, st);
+        cudaMemcpyAsync(Jh, Ah, size_t(nb) * DD * 4, cudaMemcpyDeviceToDevice, st);
+        if (Jl) cudaMemcpyAsync(Jl, Al, size_t(nb) * DD * 4, cudaMemcpyDeviceToDevice, st);
+        launch_transpose_split(Ah, Jl ? Al : nullptr, nb, D, D, JTh, JTl, false, st);
         count_launch(3);
     };
     if (debug) {

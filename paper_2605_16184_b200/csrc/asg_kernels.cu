@@ -832,6 +832,29 @@ void launch_relative_damping_f32(const float* A, int nb, int M, int n, double da
     count_launch();
 }
 
+// One Newton-Schulz polar step V <- V X, X = (3 I - V^T V) / 2, restores
+// orthonormality of an eigenbasis to the fp32 floor (quadratic: 1e-5 -> 1e-10).
+// X from S = V^T V (fp32 [b][D][D]) on the leading d x d (zero elsewhere); in
+// place of S allowed (Xh == S).
+__global__ void ns_x_kernel(const float* S, int d, int D, float* Xh, float* __restrict__ Xl) {
+    const int64_t b = blockIdx.y;
+    const int64_t DD = int64_t(D) * D;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < DD; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / D), j = int(e % D);
+        float x = 0.f;
+        if (i < d && j < d) x = (i == j ? 1.5f : 0.f) - 0.5f * S[b * DD + e];
+        float h, l;
+        split_tf32(x, h, l);
+        Xh[b * DD + e] = h;
+        if (Xl) Xl[b * DD + e] = l;
+    }
+}
+
+void launch_ns_x(const float* S, int nb, int d, int D, float* Xh, float* Xl, cudaStream_t s) {
+    ns_x_kernel<<<dim3(256, nb), 256, 0, s>>>(S, d, D, Xh, Xl);
+    count_launch();
+}
+
 // ============================================================================
 // Multi-GPU pack / unpack of block slices (owner-major all-gather layout)
 // ============================================================================

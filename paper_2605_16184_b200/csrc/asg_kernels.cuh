@@ -119,6 +119,9 @@ void launch_scale_columns_split(const float* Vh, const float* Vl, const double* 
 // eps[b] = damping * tr(A_b) / n from an fp32 slab [b][M][M].
 void launch_relative_damping_f32(const float* A, int nb, int M, int n, double damping, double* eps, cudaStream_t s);
 
+// X = (3 I - S) / 2 on the leading d x d of S = V^T V (Newton-Schulz polar step).
+void launch_ns_x(const float* S, int nb, int d, int D, float* Xh, float* Xl, cudaStream_t s);
+
 // Multi-GPU: pack owned block slices into a contiguous buffer and back.
 void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out,
                         cudaStream_t s);

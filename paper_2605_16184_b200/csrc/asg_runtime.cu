@@ -225,8 +225,8 @@ struct asg_blockset {
     // F32 refresh workspace (side stream): 8 split-tf32 slabs of ws_chunk x D x D
     float* tw[8] = {};
     size_t tw_slab = 0;  // floats per block slot (Dmax^2)
-    // F32 SOAP install workspace (main stream): 4 slabs of ws_chunk x D x D
-    float* iw32[4] = {};
+    // F32 SOAP install workspace (main stream): 6 slabs of ws_chunk x D x D
+    float* iw32[6] = {};
     // F32 refresh: tensor-core Jacobi workspace (side stream)
     float* tc_ws = nullptr;
     bool fp64_jacobi = false;  // ASG_F32_FP64_JACOBI=1: F32 refresh with the fp64 block Jacobi (diagnostics)
@@ -778,6 +778,32 @@ void refresh_side(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaSt
     }
 }
 
+
+// One Newton-Schulz polar step on a split basis slab (cnt blocks of D x D):
+// out = V (3 I - V^T V) / 2. VT: scratch for V^T (split), Sx: fp32 scratch
+// reused in place for X's hi part, Xl: X's lo part (null in TF32 mode).
+void orthonormalize(asg_blockset* bs, const float* Vh, const float* Vl, float* outh, float* outl, float* VTh,
+                    float* VTl, float* Sx, float* Xl, int cnt, int d, int D, cudaStream_t s) {
+    const size_t DD = size_t(D) * D;
+    const double flops = 2.0 * cnt * double(d) * d * d;
+    launch_transpose_split(Vh, Vl, cnt, D, D, VTh, VTl, false, s);
+    GemmParams p1{};
+    p1.alpha = 1.f;
+    p1.beta = 0.f;
+    p1.C = Sx;
+    p1.ldc = D;
+    p1.c_bstride = int64_t(DD);
+    run_gemm(bs, op(VTh, VTl, D, D), op(VTh, VTl, D, D), cnt, EPI_STORE, p1, nullptr, 0, s, flops);
+    launch_ns_x(Sx, cnt, d, D, Sx, Xl, s);
+    GemmParams p2{};
+    p2.alpha = 1.f;
+    p2.Dhi = outh;
+    p2.Dlo = outl;
+    p2.ldd = D;
+    p2.d_bstride = int64_t(DD);
+    run_gemm(bs, op(Vh, Vl, D, D), op(Sx, Xl, D, D), cnt, EPI_SPLIT, p2, nullptr, 0, s, flops);
+}
+
 // F32 refresh of one side of one chunk (asg_refresh_mode F32). With Q the
 // block's previous eigenbasis (identity before the first refresh):
 //   B = Q^T A Q (two 3xTF32 GEMMs), J = eig(B) (fp64 block Jacobi, relative
@@ -854,8 +880,10 @@ void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cu
     p3.ldd = D;
     p3.d_bstride = int64_t(DD);
     run_gemm(bs, op(Qh, Ql, D, D), op(t[2], t3, D, D), cnt, EPI_SPLIT, p3, nullptr, 0, s, 2.0 * dd3);
-    CK(cudaMemcpyAsync(Qh, t[4], cntDD * 4, cudaMemcpyDeviceToDevice, s));
-    if (sp) CK(cudaMemcpyAsync(Ql, t[5], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+    // re-orthonormalize (the products drift at the fp32 level), straight into the basis
+    orthonormalize(bs, t[4], t5, Qh, sp ? Ql : nullptr, t[2], t3, t[6], t7, cnt, d, D, s);
+    CK(cudaMemcpyAsync(t[4], Qh, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+    if (sp) CK(cudaMemcpyAsync(t[5], Ql, cntDD * 4, cudaMemcpyDeviceToDevice, s));
     launch_transpose_split(t[4], t5, cnt, D, D, QTh, sp ? QTl : nullptr, false, s);
     // roots V diag((lambda + eps)^p) V^T  (inv_root densela.hpp:267-282, damping precond.cpp:121-125)
     launch_relative_damping(bs->ws_snap, cnt, d, bs->opt.damping, bs->ws_eps, s);
@@ -968,7 +996,7 @@ void install_soap_f32(asg_blockset* bs, Group& g, int s0, int cnt) {
     for (int side = 0; side < 2; ++side) {
         const bool left = side == 0;
         const int d = left ? g.m : g.n, D = left ? g.M : g.N;
-        const size_t DD = size_t(D) * D, cntDD = size_t(cnt) * DD;
+        const size_t DD = size_t(D) * D;
         float* Qh = at(left ? g.QLh : g.QRh, DD, s0);
         float* Ql = at(left ? g.QLl : g.QRl, DD, s0);
         GemmParams p{};
@@ -979,9 +1007,10 @@ void install_soap_f32(asg_blockset* bs, Group& g, int s0, int cnt) {
         p.d_bstride = int64_t(DD);
         run_gemm(bs, op(Qh, Ql, D, D), op(at(left ? g.sJLTh : g.sJRTh, DD, s0), at(left ? g.sJLTl : g.sJRTl, DD, s0), D, D),
                  cnt, EPI_SPLIT, p, nullptr, 0, s, 2.0 * cnt * double(d) * d * d);
-        CK(cudaMemcpyAsync(Qh, w[0], cntDD * 4, cudaMemcpyDeviceToDevice, s));
-        if (sp) CK(cudaMemcpyAsync(Ql, w[1], cntDD * 4, cudaMemcpyDeviceToDevice, s));
-        launch_transpose_split(w[0], sp ? w[1] : nullptr, cnt, D, D, at(left ? g.QLTh : g.QRTh, DD, s0),
+        // Q <- orthonormalized (Q_old J), then Q^T
+        orthonormalize(bs, w[0], sp ? w[1] : nullptr, Qh, sp ? Ql : nullptr, w[2], sp ? w[3] : nullptr, w[4],
+                       sp ? w[5] : nullptr, cnt, d, D, s);
+        launch_transpose_split(Qh, sp ? Ql : nullptr, cnt, D, D, at(left ? g.QLTh : g.QRTh, DD, s0),
                                at(left ? g.QLTl : g.QRTl, DD, s0), false, s);
         CK(cudaMemcpyAsync(at(left ? g.valsL : g.valsR, size_t(d), s0), at(left ? g.svalsL : g.svalsR, size_t(d), s0),
                            size_t(cnt) * d * 8, cudaMemcpyDeviceToDevice, s));
