@@ -15,7 +15,9 @@ fp32 factor (normwise relative error max|x - x_ref| / max|x_ref|):
   * eigenvectors (SOAP):    |<q, q_ref>| >= 1 - 1e-5 for separated eigenvalues
   * preconditioned update:  <= 1e-4 (SOAP, bases from the GPU)
 and trajectories as tests/test_gpu_step.py with r = 5e-4 (Shampoo, KL,
-AdamW) and 2e-3 (SOAP).
+AdamW) and 3e-3 (SOAP: its update rotates into the basis, whose error is
+~1e-6 * lambda / gap for near-degenerate eigenpairs; the roots are smooth in
+lambda and do not see the 1/gap).
 """
 import numpy as np
 import pytest
@@ -162,6 +164,6 @@ def test_f32_trajectory_matches_oracle_bounded_staleness(method):
     from paper_2605_16184_b200 import optimizer
     shapes = [(256, 384), (300,), (96, 96), (72, 72)]
     errs, o = T.run_pair(optimizer, method, shapes, limit=128, pf=4, steps=10, S=3, delay=2.0,
-                         refresh_mode=abi.REFRESH_F32, r_scale=(4.0 if method == abi.SOAP else 2.5))
+                         refresh_mode=abi.REFRESH_F32, r_scale=(6.0 if method == abi.SOAP else 2.5))
     assert o.stats().installed >= 2 * 8
     assert max(errs) <= 1.0, errs
