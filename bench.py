@@ -61,6 +61,10 @@ WORKLOADS = {
                shapes=llama_1b(), limit=2048, pf=10, S=5, lr=1e-3, accumulation="EMA"),
     "C4": dict(name="C4: SOAP LLaMA-shaped 1B layer set (256 x 2048^2), block-sharded", method="SOAP",
                shapes=llama_1b(), limit=2048, pf=10, S=5, lr=1e-3, accumulation="EMA"),
+    # C5: the refresh's batched eigensolve alone; a step = one cold solve of
+    # B_n = 2^31 / n^2 SPD factors (8 GiB fp32) of dimension --n, split over ranks.
+    "C5": dict(name="C5: batched eigh refresh sweep point (B_n = 2^31/n^2 SPD factors)", method="eigh",
+               shapes=[], limit=0, pf=1, S=0, lr=0.0, accumulation="EMA"),
 }
 
 
@@ -141,6 +145,20 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
+def traffic_for(workload):
+    """DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) per launch of
+    the dominant kernel, from the committed `ncu --set full` capture summary
+    (profiles/r01_traffic.json, written by profiles/ncu_traffic.py)."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if not os.path.exists(p):
+        return {"traffic": None}
+    d = json.load(open(p)).get(workload)
+    if not d:
+        return {"traffic": None}
+    return {"traffic": d["dram_bytes_per_launch"], "traffic_kernel": d["kernel"],
+            "traffic_alg_bytes": d.get("alg_bytes_per_launch"), "traffic_source": d["source"]}
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -205,6 +223,114 @@ def cpu_baseline(wl, budget_s=20.0):
 
 
 # ---------------------------------------------------------------------------
+# C5: batched eigensolve sweep point
+# ---------------------------------------------------------------------------
+def cpu_eigh_baseline(n, batch, budget_s=20.0):
+    """The oracle's cyclic Jacobi (densela.hpp:182-264 restated, -O3) on one
+    384x384 SPD factor, extrapolated by n^3 and spread over nproc threads (the
+    reference's refresh pool, harness.cpp:312-316)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import orc
+    ns = 384
+    a = orc.random_spd(ns, 7)
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < budget_s or k < 1:
+        orc.sym_eig(a)
+        k += 1
+    t1 = (time.perf_counter() - t0) / k
+    cores = os.cpu_count() or 1
+    t_total = t1 * (n / ns) ** 3 * batch / cores
+    return {"value": 9.0 * n ** 3 * batch / t_total / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+            "ms_per_step": t_total * 1e3,
+            "sample": f"oracle cyclic Jacobi (fp64, -O3) on one {ns}x{ns} SPD factor: {k} solves, {t1*1e3:.0f} ms "
+                      f"each; extrapolated by n^3 to {batch} factors of n={n} on {cores} threads"}
+
+
+def run_c5(args, rank, world, local):
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from paper_2605_16184_b200 import runtime as rt
+    n = args.n
+    total = (1 << 31) // (n * n)
+    per = (total + world - 1) // world
+    mine = max(0, min(per, total - rank * per))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    a = torch.empty(mine, n, n, dtype=torch.float32, device=dev)
+    for i in range(0, mine, 64):  # SPD factors A = X X^T / 2n + 1e-3 I (test_util.hpp:20-26 shape)
+        x = torch.randn(min(64, mine - i), n, 2 * n, device=dev, generator=gen)
+        a[i:i + 64] = torch.baddbmm(1e-3 * torch.eye(n, device=dev).expand(x.shape[0], n, n), x, x.transpose(1, 2),
+                                    alpha=1.0 / (2 * n))
+        del x
+    w = torch.empty(mine, n, dtype=torch.float64, device=dev)
+    v = torch.empty(mine, n, n, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def solve():
+        if mine:
+            rt.check(rt.lib.asg_sym_eig_batched_f32(C.c_void_p(a.data_ptr()), C.c_void_p(w.data_ptr()),
+                                                    C.c_void_p(v.data_ptr()), mine, n, C.c_void_p(stream.cuda_stream or 1)))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        solve()
+    barrier()
+    l0 = rt.lib.asg_api_version  # noqa: F841  (library loaded)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            solve()
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    k = min(mine, 2)
+    ad, vd = a[:k].double(), v[:k].double()
+    resid = ((ad @ vd - vd * w[:k, None, :]).abs().amax() / ad.abs().amax()).item() if k else None
+    if rank == 0:
+        flops = 9.0 * n ** 3 * total
+        peak, _, _, src = measured_peaks()
+        line = {"metric": "batched refresh eigensolve throughput (algorithmic TFLOP/s, 9n^3 per factor)",
+                "value": flops * args.steps / (ms / 1e3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32 (3xTF32 tcgen05 block Jacobi, fp32 pair solves)",
+                "data": "synthetic SPD factors X X^T/2n + 1e-3 I (cold solves)",
+                "config": {"workload": WORKLOADS["C5"]["name"], "n": n, "factors": total,
+                           "parallelism": f"factor-sharded x{world}" if world > 1 else "single",
+                           "l2": "inputs > L2 (8 GiB of factors per step)", "max_residual_rel": resid},
+                "roofline": {"kernel": "tj_apply_kernel + tj_pair_kernel (algorithmic 9n^3 vs tensor peak)",
+                             "bound": "tensor", "achieved": flops * args.steps / (ms / 1e3) / 1e12 / world,
+                             "peak": peak, "unit": "TFLOP/s",
+                             "frac": flops * args.steps / (ms / 1e3) / 1e12 / world / peak,
+                             "peak_note": f"{src} dense bf16", **traffic_for("C5")},
+                "gpu_launches": None, "clocks": clk.summary(),
+                "e2e": None}
+        if not args.no_cpu_baseline:
+            cb = cpu_eigh_baseline(n, total)
+            line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
 # main
 # ---------------------------------------------------------------------------
 def main():
@@ -218,6 +344,7 @@ def main():
     ap.add_argument("--refresh", default="f32", choices=["f32", "f64"],
                     help="refresh arithmetic: f32 = fp32-level tensor-core refresh (default), "
                          "f64 = reference-tight fp64 eigensolve")
+    ap.add_argument("--n", type=int, default=2048, help="C5: factor dimension of the sweep point")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -227,6 +354,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload == "C5" and args.impl == "ours":
+        run_c5(args, rank, world, local)
+        return
     step_flops, refresh_flops, flops = alg_flops(wl)
     cfg_out = {"workload": wl["name"], "method": wl["method"], "blocks": sum(len(blocks_of(s, wl["limit"])) for s in wl["shapes"]),
                "params": sum(math.prod(s) for s in wl["shapes"]), "block_dim_limit": wl["limit"],
@@ -238,8 +368,15 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_baseline(wl, budget_s=max(10.0, 3.0 * args.steps))
-        line = {"impl": "reference", "metric": "optimizer step throughput (algorithmic TFLOP/s)",
+        if args.workload == "C5":
+            total = (1 << 31) // (args.n * args.n)
+            cb = cpu_eigh_baseline(args.n, total, budget_s=max(10.0, 3.0 * args.steps))
+            cfg_out = {"workload": wl["name"], "n": args.n, "factors": total}
+        else:
+            cb = cpu_baseline(wl, budget_s=max(10.0, 3.0 * args.steps))
+        metric = ("batched refresh eigensolve throughput (algorithmic TFLOP/s, 9n^3 per factor)" if args.workload == "C5"
+                  else "optimizer step throughput (algorithmic TFLOP/s); step latency in ms_per_step")
+        line = {"impl": "reference", "metric": metric,
                 "value": cb["value"], "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -361,7 +498,9 @@ def main():
         "metric": "optimizer step throughput (algorithmic TFLOP/s); step latency in ms_per_step",
         "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 (3xTF32 tensor-core products, fp64 refresh)" if prec == abi.PREC_3XTF32 else "tf32",
+        "dtype": ("f32 (3xTF32 tensor-core products; " +
+                  ("fp32-level refresh: tensor-core block Jacobi)" if args.refresh == "f32" else "fp64 refresh)")
+                  if prec == abi.PREC_3XTF32 else "tf32"),
         "data": "synthetic (N(0, 1/cols) gradients, fixed per run; random-init parameters)",
         "config": cfg_out,
         "roofline": {"kernel": "tcgen05 TN GEMM (all fused epilogues), main stream", "bound": "tensor",
@@ -371,7 +510,7 @@ def main():
                                   f"3xTF32 issues 3 tf32 MMAs per algorithmic product",
                      "frac_of_mode_peak": (ach / (peak / 2 / (3 if prec == abi.PREC_3XTF32 else 1))) if ach else None,
                      "gemm_launches": ks.gemm_launches, "gemm_ms_per_step": ks.gemm_ms / args.steps,
-                     "traffic": None},
+                     **traffic_for(args.workload)},
         "gpu_launches": ks.launches,
         "clocks": clk.summary(),
         "schedule": {"dispatched": st1.dispatched - st0.dispatched, "installed": st1.installed - st0.installed,

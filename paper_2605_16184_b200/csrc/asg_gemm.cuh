@@ -217,18 +217,58 @@ __device__ __forceinline__ void apply_chunk(const GemmParams& p, int b, int row0
     const int c = col0 + int(lane);
     bool bad = false;
     if (c < e.cols) {
-        float* th = e.theta + c;
+        float* th = e.theta + c + int64_t(row0) * e.ld;
         const int rows = min(32, e.rows - row0);
-#pragma unroll 4
-        for (int i = 0; i < rows; ++i) {
-            const float u = scratch[i][lane];
-            bad |= !isfinite(u);
-            float* pt = th + int64_t(row0 + i) * e.ld;
-            const float t = *pt;
-            *pt = t - p.lr_eff * (u + p.wd * t);
+        // all 32 loads in flight before any store (the warp covers 32 full 128-byte lines)
+        float t[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) t[i] = (i < rows) ? __ldcs(th + int64_t(i) * e.ld) : 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            if (i < rows) {
+                const float u = scratch[i][lane];
+                bad |= !isfinite(u);
+                __stcs(th + int64_t(i) * e.ld, t[i] - p.lr_eff * (u + p.wd * t[i]));
+            }
         }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag) atomicOr(p.flag, 1);
+    __syncwarp();
+}
+
+// EPI_ADAM, warp-cooperative (soap_scaled_step precond.cpp:213-221): the
+// warp's 32 x 32 chunk of Ghat goes through the shared-memory transpose so
+// that the moment read-modify-writes and the S stores are 128-byte coalesced
+// rows; all 64 moment loads of a lane are in flight together.
+__device__ __forceinline__ void adam_chunk(const GemmParams& p, int b, int row0, int col0, const uint32_t (&r)[32],
+                                           float (*scratch)[33]) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) scratch[lane][j] = p.alpha * __uint_as_float(r[j]);
+    __syncwarp();
+    const int c = col0 + int(lane);
+    float* mm = p.mom_m + int64_t(b) * p.m_bstride + int64_t(row0) * p.ldm + c;
+    float* vv = p.mom_v + int64_t(b) * p.m_bstride + int64_t(row0) * p.ldm + c;
+    float mv[32], vvv[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        mv[i] = __ldcs(mm + int64_t(i) * p.ldm);
+        vvv[i] = __ldcs(vv + int64_t(i) * p.ldm);
+    }
+    float* dh = p.Dhi + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c;
+    float* dl = p.Dlo ? p.Dlo + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c : nullptr;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const float g = scratch[i][lane];
+        const float m = p.b1 * mv[i] + (1.f - p.b1) * g;
+        const float v = p.b2 * vvv[i] + (1.f - p.b2) * (g * g);
+        __stcs(mm + int64_t(i) * p.ldm, m);
+        __stcs(vv + int64_t(i) * p.ldm, v);
+        float h, l;
+        split_tf32((m * p.inv_bc1) / (sqrtf(v * p.inv_bc2) + p.adam_eps), h, l);
+        __stcs(dh + int64_t(i) * p.ldd, h);
+        if (dl) __stcs(dl + int64_t(i) * p.ldd, l);
+    }
     __syncwarp();
 }
 
@@ -370,6 +410,8 @@ __global__ void __launch_bounds__(192, 1)
                 tmem_ld_wait();
                 if constexpr (EPI == EPI_APPLY)
                     apply_chunk(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
+                else if constexpr (EPI == EPI_ADAM)
+                    adam_chunk(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
                 else
                     epilogue_chunk<EPI>(p, b, row, tn * BN + c * 32, r);
             }

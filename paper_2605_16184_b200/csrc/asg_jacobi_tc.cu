@@ -43,9 +43,10 @@
 namespace asg {
 namespace {
 
-constexpr int JW = 64;   // column block
-constexpr int JP = 128;  // pair (tile) size
-constexpr int kPairThreads = 512;
+constexpr int JW = 32;   // column block
+constexpr int PW = 64;   // pair subproblem (two blocks)
+constexpr int JP = 128;  // apply tile = a quad of blocks (two pairs)
+constexpr int kPairThreads = 256;
 constexpr int kInner = 1;  // inner sweeps of the pair solve (more outer sweeps are cheaper than inner ones)
 
 __device__ __forceinline__ int tourney(int pos, int r, int P) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (P - 1); }
@@ -134,7 +135,10 @@ __global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const 
 }
 
 // ---- pair solve -----------------------------------------------------------------
-// One CTA per (pair k, matrix b). Shared: S (128 x 129), Z (128 x 129) fp32.
+// One CTA per (pair k, matrix b): gathers the 64x64 pair matrix (blocks p, q),
+// diagonalises it in shared memory (fp32 parallel cyclic Jacobi) and writes
+// J^T into its diagonal 64x64 block of the quad tile (pairs 2g, 2g+1 share a
+// 128x128 tile; the off-diagonal blocks stay zero).
 __global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __restrict__ Ah, const float* __restrict__ Al,
                                                                int D, int m, int round, float* __restrict__ JTh,
                                                                float* __restrict__ JTl, int* __restrict__ pflag,
@@ -142,14 +146,13 @@ __global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __re
                                                                const int* __restrict__ active,
                                                                const double* __restrict__ fro, int n, float tol,
                                                                int inner_sweeps) {
-    extern __shared__ float tsm[];
-    float* S = tsm;                    // [JP][JP+1]
-    float* Z = S + JP * (JP + 1);      // [JP][JP+1]
-    __shared__ float cs[JP / 2], sn[JP / 2];
-    __shared__ int rank_of[JP];
+    __shared__ float S[PW * (PW + 1)];
+    __shared__ float Z[PW * (PW + 1)];
+    __shared__ float cs[PW / 2], sn[PW / 2];
+    __shared__ int rank_of[PW];
     const int k = blockIdx.x;
     const int64_t b = blockIdx.y;
-    const int npairs = m / 2;
+    const int npairs = m / 2, nquads = m / 4;
     int* flag = pflag + b * npairs + k;
     if (!active[b]) {
         if (threadIdx.x == 0) *flag = 0;
@@ -158,29 +161,32 @@ __global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __re
     int p, q;
     pair_of(k, round, m, p, q);
     const int64_t DD = int64_t(D) * D;
-    for (int e = threadIdx.x; e < JP * JP; e += blockDim.x) {
-        const int i = e / JP, j = e % JP;
+    for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) {
+        const int i = e / PW, j = e % PW;
         const int64_t off = b * DD + int64_t(nat(i, p, q)) * D + nat(j, p, q);
-        S[i * (JP + 1) + j] = Ah[off] + Al[off];
-        Z[i * (JP + 1) + j] = (i == j) ? 1.f : 0.f;
+        S[i * (PW + 1) + j] = Ah[off] + Al[off];
+        Z[i * (PW + 1) + j] = (i == j) ? 1.f : 0.f;
     }
     __syncthreads();
     const float floor_s = float(fro[b] / sqrt(double(n)));
     auto big = [&](int i, int j, float t) {
-        return fabsf(S[i * (JP + 1) + j]) > t * fmaxf(sqrtf(fabsf(S[i * (JP + 1) + i] * S[j * (JP + 1) + j])), floor_s);
+        return fabsf(S[i * (PW + 1) + j]) > t * fmaxf(sqrtf(fabsf(S[i * (PW + 1) + i] * S[j * (PW + 1) + j])), floor_s);
     };
     bool any = false;
-    for (int e = threadIdx.x; e < JP * JP; e += blockDim.x) {
-        const int i = e / JP, j = e % JP;
+    for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) {
+        const int i = e / PW, j = e % PW;
         if (j > i) any |= big(i, j, tol);
     }
-    float* jh = JTh + (b * npairs + k) * int64_t(JP) * JP;
-    float* jl = JTl + (b * npairs + k) * int64_t(JP) * JP;
+    const int half = k & 1;
+    const int64_t tile = (b * nquads + (k >> 1)) * int64_t(JP) * JP + int64_t(half * PW) * JP + half * PW;
+    float* jh = JTh + tile;  // block origin inside the quad tile, row stride JP
+    float* jl = JTl + tile;
     if (!__syncthreads_or(any)) {
-        // converged pair: J = I (the apply still runs for tiles whose other pair moves)
-        for (int e = threadIdx.x; e < JP * JP; e += blockDim.x) {
-            jh[e] = (e / JP == e % JP) ? 1.f : 0.f;
-            jl[e] = 0.f;
+        // converged pair: J = I (the apply still runs for quads whose other pair moves)
+        for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) {
+            const int i = e / PW, j = e % PW;
+            jh[int64_t(i) * JP + j] = (i == j) ? 1.f : 0.f;
+            jl[int64_t(i) * JP + j] = 0.f;
         }
         if (threadIdx.x == 0) *flag = 0;
         return;
@@ -192,14 +198,14 @@ __global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __re
     const float itol = 0.1f * tol;
     for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
         bool rot_any = false;
-        for (int r = 0; r < JP - 1; ++r) {
-            if (threadIdx.x < JP / 2) {
+        for (int r = 0; r < PW - 1; ++r) {
+            if (threadIdx.x < PW / 2) {
                 int a, c;
-                pair_of(threadIdx.x, r, JP, a, c);
+                pair_of(threadIdx.x, r, PW, a, c);
                 float cc = 1.f, ss = 0.f;
                 if (big(a, c, itol)) {
-                    const double apq = S[a * (JP + 1) + c];
-                    const double app = S[a * (JP + 1) + a], aqq = S[c * (JP + 1) + c];
+                    const double apq = S[a * (PW + 1) + c];
+                    const double app = S[a * (PW + 1) + a], aqq = S[c * (PW + 1) + c];
                     const double tau = (aqq - app) / (2.0 * apq);
                     const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau)) : -1.0 / (-tau + sqrt(1.0 + tau * tau));
                     const double c1 = 1.0 / sqrt(1.0 + t * t);
@@ -211,59 +217,57 @@ __global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __re
                 sn[threadIdx.x] = ss;
             }
             __syncthreads();
-            // rows of S
-            for (int e = threadIdx.x; e < (JP / 2) * JP; e += blockDim.x) {
-                const int kk = e / JP, j = e % JP;
+            for (int e = threadIdx.x; e < (PW / 2) * PW; e += blockDim.x) {  // rows of S
+                const int kk = e / PW, j = e % PW;
                 const float ss = sn[kk];
                 if (ss == 0.f) continue;
                 int a, c;
-                pair_of(kk, r, JP, a, c);
+                pair_of(kk, r, PW, a, c);
                 const float cc = cs[kk];
-                const float x = S[a * (JP + 1) + j], y = S[c * (JP + 1) + j];
-                S[a * (JP + 1) + j] = cc * x - ss * y;
-                S[c * (JP + 1) + j] = ss * x + cc * y;
+                const float x = S[a * (PW + 1) + j], y = S[c * (PW + 1) + j];
+                S[a * (PW + 1) + j] = cc * x - ss * y;
+                S[c * (PW + 1) + j] = ss * x + cc * y;
             }
             __syncthreads();
-            // columns of S and Z
-            for (int e = threadIdx.x; e < (JP / 2) * JP; e += blockDim.x) {
-                const int kk = e % (JP / 2), i = e / (JP / 2);
+            for (int e = threadIdx.x; e < (PW / 2) * PW; e += blockDim.x) {  // columns of S and Z
+                const int kk = e % (PW / 2), i = e / (PW / 2);
                 const float ss = sn[kk];
                 if (ss == 0.f) continue;
                 int a, c;
-                pair_of(kk, r, JP, a, c);
+                pair_of(kk, r, PW, a, c);
                 const float cc = cs[kk];
-                float x = S[i * (JP + 1) + a], y = S[i * (JP + 1) + c];
+                float x = S[i * (PW + 1) + a], y = S[i * (PW + 1) + c];
                 float na = cc * x - ss * y, nc = ss * x + cc * y;
                 if (i == a) nc = 0.f;
                 if (i == c) na = 0.f;
-                S[i * (JP + 1) + a] = na;
-                S[i * (JP + 1) + c] = nc;
-                x = Z[i * (JP + 1) + a];
-                y = Z[i * (JP + 1) + c];
-                Z[i * (JP + 1) + a] = cc * x - ss * y;
-                Z[i * (JP + 1) + c] = ss * x + cc * y;
+                S[i * (PW + 1) + a] = na;
+                S[i * (PW + 1) + c] = nc;
+                x = Z[i * (PW + 1) + a];
+                y = Z[i * (PW + 1) + c];
+                Z[i * (PW + 1) + a] = cc * x - ss * y;
+                Z[i * (PW + 1) + c] = ss * x + cc * y;
             }
             __syncthreads();
         }
         if (!__syncthreads_or(rot_any)) break;
     }
     // ascending order within the pair (sorted block Jacobi)
-    if (threadIdx.x < JP) {
+    if (threadIdx.x < PW) {
         const int i = threadIdx.x;
-        const float di = S[i * (JP + 1) + i];
+        const float di = S[i * (PW + 1) + i];
         int r = 0;
-        for (int j = 0; j < JP; ++j) {
-            const float dj = S[j * (JP + 1) + j];
+        for (int j = 0; j < PW; ++j) {
+            const float dj = S[j * (PW + 1) + j];
             r += (dj < di) || (dj == di && j < i);
         }
         rank_of[i] = r;
     }
     __syncthreads();
     // J[:, rank(c)] = Z[:, c]  ->  J^T[rank(c)][row] = Z[row][c]
-    for (int e = threadIdx.x; e < JP * JP; e += blockDim.x) {
-        const int c = e / JP, row = e % JP;
+    for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) {
+        const int c = e / PW, row = e % PW;
         float h, l;
-        split_tf32(Z[row * (JP + 1) + c], h, l);
+        split_tf32(Z[row * (PW + 1) + c], h, l);
         jh[int64_t(rank_of[c]) * JP + row] = h;
         jl[int64_t(rank_of[c]) * JP + row] = l;
     }
@@ -272,10 +276,10 @@ __global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __re
 // ---- apply (tcgen05) ------------------------------------------------------------------
 struct TJApply {
     float *Ah, *Al, *Vh, *Vl;   // natural layout [nb][D][D]
-    const int* pflag;           // [nb][m/2]
+    const int* pflag;           // [nb][m/2] per pair
     const int* active;          // [nb]
     int D, m, round, nb;
-    int tilesA, tilesV;         // per matrix: (m/2)^2 and (D/128)*(m/2)
+    int tilesA, tilesV;         // per matrix: (m/4)^2 and (D/128)*(m/4)
 };
 
 constexpr uint32_t kChunk = JP * 32 * 4;      // 128 rows x 32 fp32 = 16 KB
@@ -289,7 +293,7 @@ __device__ __forceinline__ void tj_decode(const TJApply& p, int t, int& b, bool&
     const int per = p.tilesA + p.tilesV;
     b = t / per;
     int l = t - b * per;
-    const int np2 = p.m / 2;
+    const int np2 = p.m / 4;  // quads
     if (l < p.tilesA) {
         isA = true;
         i1 = l / np2;
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t idesc = idesc_tf32(JP, JP);
     const int total = p.nb * (p.tilesA + p.tilesV);
-    const int npairs = p.m / 2;
+    const int npairs = p.m / 2, nquads = p.m / 4;
 
     // phase bits (per barrier), advanced identically by every role that waits on it
     uint32_t ph_full1[2] = {0, 0}, ph_empty1[2] = {0, 0}, ph_full2[2] = {0, 0}, ph_empty2[2] = {0, 0};
@@ -371,13 +375,18 @@ __global__ void __launch_bounds__(192, 1)
         tj_decode(p, t, b, isA, i1, i2);
         // skip converged work (uniform across the CTA)
         if (!p.active[b]) continue;
-        const int f2 = p.pflag[b * npairs + i2];
-        const int f1 = isA ? p.pflag[b * npairs + i1] : 0;
+        const int f2 = p.pflag[b * npairs + 2 * i2] | p.pflag[b * npairs + 2 * i2 + 1];
+        const int f1 = isA ? (p.pflag[b * npairs + 2 * i1] | p.pflag[b * npairs + 2 * i1 + 1]) : 0;
         if (!f2 && !f1) continue;
-        int p1 = 0, q1 = 0, p2, q2;
-        pair_of(i2, p.round, p.m, p2, q2);
-        if (isA) pair_of(i1, p.round, p.m, p1, q1);
-        const int jb2 = b * npairs + i2, jb1 = b * npairs + i1;
+        // the quad's four 32-blocks: pair 2g -> (0, 1), pair 2g+1 -> (2, 3)
+        int blk1[4] = {0, 0, 0, 0}, blk2[4];
+        pair_of(2 * i2, p.round, p.m, blk2[0], blk2[1]);
+        pair_of(2 * i2 + 1, p.round, p.m, blk2[2], blk2[3]);
+        if (isA) {
+            pair_of(2 * i1, p.round, p.m, blk1[0], blk1[1]);
+            pair_of(2 * i1 + 1, p.round, p.m, blk1[2], blk1[3]);
+        }
+        const int jb2 = b * nquads + i2, jb1 = b * nquads + i1;
 
         if (warp == 0) {
             if (lane == 0) {
@@ -391,17 +400,12 @@ __global__ void __launch_bounds__(192, 1)
                     ++use1[s];
                     uint8_t* st = S + s * kStage1;
                     mbar_arrive_expect_tx(&full1[s], kStage1);
-                    const int col = (c < 2 ? p2 * JW : q2 * JW) + (c & 1) * 32;
-                    if (isA) {
-                        tma_load_3d(st, &tmAh, &full1[s], col, p1 * JW, b);
-                        tma_load_3d(st + kChunk / 2, &tmAh, &full1[s], col, q1 * JW, b);
-                        tma_load_3d(st + kChunk, &tmAl, &full1[s], col, p1 * JW, b);
-                        tma_load_3d(st + kChunk + kChunk / 2, &tmAl, &full1[s], col, q1 * JW, b);
-                    } else {
-                        tma_load_3d(st, &tmVh, &full1[s], col, i1 * JP, b);
-                        tma_load_3d(st + kChunk / 2, &tmVh, &full1[s], col, i1 * JP + JW, b);
-                        tma_load_3d(st + kChunk, &tmVl, &full1[s], col, i1 * JP, b);
-                        tma_load_3d(st + kChunk + kChunk / 2, &tmVl, &full1[s], col, i1 * JP + JW, b);
+                    const int col = blk2[c] * JW;  // K-chunk c = the quad's c-th 32-column block
+#pragma unroll
+                    for (int rb = 0; rb < 4; ++rb) {  // four 32-row boxes (4 KB each)
+                        const int row0 = isA ? blk1[rb] * JW : i1 * JP + rb * JW;
+                        tma_load_3d(st + rb * (kChunk / 4), isA ? &tmAh : &tmVh, &full1[s], col, row0, b);
+                        tma_load_3d(st + kChunk + rb * (kChunk / 4), isA ? &tmAl : &tmVl, &full1[s], col, row0, b);
                     }
                     tma_load_3d(st + 2 * kChunk, &tmJh, &full1[s], c * 32, 0, jb2);
                     tma_load_3d(st + 3 * kChunk, &tmJl, &full1[s], c * 32, 0, jb2);
@@ -497,14 +501,14 @@ __global__ void __launch_bounds__(192, 1)
                 mbar_wait(adone, ph_a);
                 tc_fence_after();
                 // A' rows -> natural positions
-                const int gr = nat(row, p1, q1);
+                const int gr = blk1[row >> 5] * JW + (row & 31);
                 const int64_t base = int64_t(b) * p.D * p.D + int64_t(gr) * p.D;
 #pragma unroll 1
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(JP + cc * 32), r);
                     tmem_ld_wait();
-                    const int gc = (cc < 2 ? p2 * JW : q2 * JW) + (cc & 1) * 32;
+                    const int gc = blk2[cc] * JW;
                     float* dh = p.Ah + base + gc;
                     float* dl = p.Al + base + gc;
 #pragma unroll
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(192, 1)
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
                     tmem_ld_wait();
-                    const int gc = (cc < 2 ? p2 * JW : q2 * JW) + (cc & 1) * 32;
+                    const int gc = blk2[cc] * JW;
                     float* dh = p.Vh + base + gc;
                     float* dl = p.Vl + base + gc;
 #pragma unroll
@@ -738,9 +742,9 @@ bool tj_map(CUtensorMap* map, const float* base, int cols, int rows, int batch, 
 size_t tc_eigh_workspace_floats(int nb, int n) {
     const int D = (n + JP - 1) / JP * JP;
     const int m = D / JW;
-    // A hi/lo, V hi/lo, J^T hi/lo per pair, then per matrix: fro, pad (2 doubles = 4 floats),
-    // active, sweeps, rotations, flags (m/2), ranks (D); and the loop counter.
-    return size_t(nb) * (4 * size_t(D) * D + 2 * size_t(m / 2) * JP * JP + 4 + 3 + size_t(m / 2) + D) + 4;
+    // A hi/lo, V hi/lo, J^T hi/lo per quad tile, then per matrix: fro, pad (2 doubles = 4 floats),
+    // active, sweeps, rotations, flags (m/2 pairs), ranks (D); and the loop counter.
+    return size_t(nb) * (4 * size_t(D) * D + 2 * size_t(m / 4) * JP * JP + 4 + 3 + size_t(m / 2) + D) + 4;
 }
 
 int tc_eigh_dim(int n) { return (n + JP - 1) / JP * JP; }
@@ -749,15 +753,15 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
                     int nb, int n, int* status, int num_sms, cudaStream_t s, double tol) {
     const int D = (n + JP - 1) / JP * JP;
     (void)D_in;  // B, J, J^T are [nb][D][D] with D = roundup(n, 128) (== the group's padded dim)
-    const int m = D / JW, npairs = m / 2;
+    const int m = D / JW, npairs = m / 2, nquads = m / 4;
     const size_t DD = size_t(D) * D;
     float* Ah = ws;
     float* Al = Ah + size_t(nb) * DD;
     float* Vh = Al + size_t(nb) * DD;
     float* Vl = Vh + size_t(nb) * DD;
     float* JPh = Vl + size_t(nb) * DD;
-    float* JPl = JPh + size_t(nb) * npairs * JP * JP;
-    double* fro = reinterpret_cast<double*>(JPl + size_t(nb) * npairs * JP * JP);
+    float* JPl = JPh + size_t(nb) * nquads * JP * JP;
+    double* fro = reinterpret_cast<double*>(JPl + size_t(nb) * nquads * JP * JP);
     double* pad = fro + nb;
     int* active = reinterpret_cast<int*>(pad + nb);
     int* sweeps = active + nb;
@@ -767,9 +771,7 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
     int* loop_count = rank + size_t(nb) * D;
 
     static bool attr = false;
-    const int pair_smem = 2 * JP * (JP + 1) * int(sizeof(float));
     if (!attr) {
-        cudaFuncSetAttribute(tj_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
         cudaFuncSetAttribute(tj_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kApplySmem));
         cudaFuncSetAttribute(tj_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 4);
         cudaFuncSetAttribute(tj_sort_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8);
@@ -785,12 +787,12 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
     ap.D = D;
     ap.m = m;
     ap.nb = nb;
-    ap.tilesA = npairs * npairs;
-    ap.tilesV = (D / JP) * npairs;
+    ap.tilesA = nquads * nquads;
+    ap.tilesV = (D / JP) * nquads;
     CUtensorMap mAh, mAl, mVh, mVl, mJh, mJl;
     bool ok = tj_map(&mAh, Ah, D, D, nb, JW) && tj_map(&mAl, Al, D, D, nb, JW) && tj_map(&mVh, Vh, D, D, nb, JW) &&
-              tj_map(&mVl, Vl, D, D, nb, JW) && tj_map(&mJh, JPh, JP, JP, nb * npairs, JP) &&
-              tj_map(&mJl, JPl, JP, JP, nb * npairs, JP);
+              tj_map(&mVl, Vl, D, D, nb, JW) && tj_map(&mJh, JPh, JP, JP, nb * nquads, JP) &&
+              tj_map(&mJl, JPl, JP, JP, nb * nquads, JP);
     if (!ok) {
         // tensor maps unavailable: report through every matrix's status (no silent fallback)
         cudaMemsetAsync(status, 0xff, size_t(nb) * sizeof(int), s);
@@ -805,12 +807,14 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
     auto prologue = [&](cudaStream_t st) {
         cudaMemsetAsync(sweeps, 0, size_t(nb) * 2 * sizeof(int), st);  // sweeps, rotations
         cudaMemsetAsync(loop_count, 0, sizeof(int), st);
+        // quad tiles: the pair kernels write the two diagonal 64x64 blocks only
+        cudaMemsetAsync(JPh, 0, size_t(nb) * nquads * JP * JP * 2 * sizeof(float), st);
         tj_stats_kernel<<<nb, 512, 0, st>>>(B, n, D, fro, pad, active, status);
         tj_init_kernel<<<dim3(128, nb), 256, 0, st>>>(B, n, D, pad, Ah, Al, Vh, Vl);
     };
     auto sweep = [&](cudaStream_t st) {
         for (int r = 0; r < m - 1; ++r) {
-            tj_pair_kernel<<<dim3(npairs, nb), kPairThreads, pair_smem, st>>>(Ah, Al, D, m, r, JPh, JPl, pflag, rotations,
+            tj_pair_kernel<<<dim3(npairs, nb), kPairThreads, 0, st>>>(Ah, Al, D, m, r, JPh, JPl, pflag, rotations,
                                                                                active, fro, n, ftol, inner);
             TJApply a = ap;
             a.round = r;

@@ -38,6 +38,7 @@ def main():
     opt.accumulation = abi.EMA
     sched = rt.scheduler_defaults()
     sched.pf, sched.staleness_S, sched.install_mode = pf, 0, abi.INSTALL_SIM_CLOCK
+    sched.refresh_mode = abi.REFRESH_F64 if os.environ.get("ASG_REFRESH", "f32") == "f64" else abi.REFRESH_F32
     o = AsteriaOptimizer(params, grads, opt, sched, precision=abi.PREC_3XTF32)
     for k in range(steps):
         torch.cuda.nvtx.range_push(f"step{k}")
