@@ -285,7 +285,8 @@ def run_c5(args, rank, world, local):
     for _ in range(args.warmup):
         solve()
     barrier()
-    l0 = rt.lib.asg_api_version  # noqa: F841  (library loaded)
+    lc0, lc1 = C.c_uint64(), C.c_uint64()
+    rt.check(rt.lib.asg_launch_count(C.byref(lc0)))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -294,6 +295,7 @@ def run_c5(args, rank, world, local):
             solve()
         e1.record(stream)
         barrier()
+    rt.check(rt.lib.asg_launch_count(C.byref(lc1)))
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -319,7 +321,7 @@ def run_c5(args, rank, world, local):
                              "peak": peak, "unit": "TFLOP/s",
                              "frac": flops * args.steps / (ms / 1e3) / 1e12 / world / peak,
                              "peak_note": f"{src} dense bf16", **traffic_for("C5")},
-                "gpu_launches": None, "clocks": clk.summary(),
+                "gpu_launches": lc1.value - lc0.value, "clocks": clk.summary(),
                 "e2e": None}
         if not args.no_cpu_baseline:
             cb = cpu_eigh_baseline(n, total)

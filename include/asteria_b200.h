@@ -322,6 +322,10 @@ typedef struct asg_kernel_stats {
     double gemm_alg_flops;   /* algorithmic flops of those launches (SYRK: n^2 k, GEMM: 2 m n k) */
     double gemm_ms;          /* sum of their CUDA-event durations on the launching stream */
 } asg_kernel_stats;
+/* Process-wide count of kernel launches issued by this library (graph
+ * replays count the kernels of one pass through the graph; sweeps repeated by
+ * a device-driven WHILE loop are not counted again). */
+int asg_launch_count(uint64_t* count);
 /* While enabled, every GEMM launch is bracketed by CUDA events on its stream. */
 int asg_profile_enable(asg_blockset* bs, int32_t enable);
 /* Synchronizes, returns the stats accumulated since the last reset. */

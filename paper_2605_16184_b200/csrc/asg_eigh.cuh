@@ -43,7 +43,9 @@ void launch_eigh(const double* A, double* values, double* vectors, double* ws, i
 // tc_eigh_workspace_floats. status: per-matrix asg_status (zero-initialised).
 int tc_eigh_dim(int n);
 size_t tc_eigh_workspace_floats(int nb, int n);
+// orthonormalize: one Newton-Schulz step on J (callers that re-orthonormalize
+// the product Q J themselves pass false).
 void launch_tc_eigh(const float* B, int D, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
-                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol);
+                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize = true);
 
 }  // namespace asg

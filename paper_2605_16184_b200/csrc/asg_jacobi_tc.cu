@@ -43,10 +43,11 @@
 namespace asg {
 namespace {
 
-constexpr int JW = 32;   // column block
-constexpr int PW = 64;   // pair subproblem (two blocks)
-constexpr int JP = 128;  // apply tile = a quad of blocks (two pairs)
-constexpr int kPairThreads = 256;
+constexpr int JP = 128;  // apply tile: 128/PW pairs of two JW-wide blocks
+// Pair width PW = 2 JW: 64 (tiles of two pairs) below kWidePairN, 128 (one
+// pair per tile) from there on: small pairs make the shared-memory solves
+// cheap, wide pairs halve the rounds (and the tensor-core work) per sweep.
+constexpr int kWidePairN = 1536;
 constexpr int kInner = 1;  // inner sweeps of the pair solve (more outer sweeps are cheaper than inner ones)
 
 __device__ __forceinline__ int tourney(int pos, int r, int P) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (P - 1); }
@@ -59,7 +60,8 @@ __device__ __forceinline__ void pair_of(int k, int r, int m, int& p, int& q) {
         q = t;
     }
 }
-// pair-local index (0..127) -> natural index
+// pair-local index -> natural index
+template <int JW>
 __device__ __forceinline__ int nat(int i, int p, int q) { return i < JW ? p * JW + i : q * JW + (i - JW); }
 
 __device__ double tj_block_sum(double v, double* red) {
@@ -139,20 +141,23 @@ __global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const 
 // diagonalises it in shared memory (fp32 parallel cyclic Jacobi) and writes
 // J^T into its diagonal 64x64 block of the quad tile (pairs 2g, 2g+1 share a
 // 128x128 tile; the off-diagonal blocks stay zero).
-__global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __restrict__ Ah, const float* __restrict__ Al,
+template <int PW>
+__global__ void __launch_bounds__(PW * 4) tj_pair_kernel(const float* __restrict__ Ah, const float* __restrict__ Al,
                                                                int D, int m, int round, float* __restrict__ JTh,
                                                                float* __restrict__ JTl, int* __restrict__ pflag,
                                                                int* __restrict__ rotations,
                                                                const int* __restrict__ active,
                                                                const double* __restrict__ fro, int n, float tol,
                                                                int inner_sweeps) {
-    __shared__ float S[PW * (PW + 1)];
-    __shared__ float Z[PW * (PW + 1)];
+    constexpr int JW = PW / 2, G = JP / PW;  // G pairs share one 128x128 tile
+    extern __shared__ float tj_pair_smem[];
+    float* S = tj_pair_smem;            // [PW][PW+1]
+    float* Z = S + PW * (PW + 1);       // [PW][PW+1]
     __shared__ float cs[PW / 2], sn[PW / 2];
     __shared__ int rank_of[PW];
     const int k = blockIdx.x;
     const int64_t b = blockIdx.y;
-    const int npairs = m / 2, nquads = m / 4;
+    const int npairs = m / 2, ntiles = npairs / G;
     int* flag = pflag + b * npairs + k;
     if (!active[b]) {
         if (threadIdx.x == 0) *flag = 0;
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __re
     const int64_t DD = int64_t(D) * D;
     for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) {
         const int i = e / PW, j = e % PW;
-        const int64_t off = b * DD + int64_t(nat(i, p, q)) * D + nat(j, p, q);
+        const int64_t off = b * DD + int64_t(nat<JW>(i, p, q)) * D + nat<JW>(j, p, q);
         S[i * (PW + 1) + j] = Ah[off] + Al[off];
         Z[i * (PW + 1) + j] = (i == j) ? 1.f : 0.f;
     }
@@ -177,8 +182,8 @@ __global__ void __launch_bounds__(kPairThreads) tj_pair_kernel(const float* __re
         const int i = e / PW, j = e % PW;
         if (j > i) any |= big(i, j, tol);
     }
-    const int half = k & 1;
-    const int64_t tile = (b * nquads + (k >> 1)) * int64_t(JP) * JP + int64_t(half * PW) * JP + half * PW;
+    const int half = k % G;
+    const int64_t tile = (b * ntiles + k / G) * int64_t(JP) * JP + int64_t(half * PW) * JP + half * PW;
     float* jh = JTh + tile;  // block origin inside the quad tile, row stride JP
     float* jl = JTl + tile;
     if (!__syncthreads_or(any)) {
@@ -293,7 +298,7 @@ __device__ __forceinline__ void tj_decode(const TJApply& p, int t, int& b, bool&
     const int per = p.tilesA + p.tilesV;
     b = t / per;
     int l = t - b * per;
-    const int np2 = p.m / 4;  // quads
+    const int np2 = p.D / JP;  // 128x128 tiles per matrix row
     if (l < p.tilesA) {
         isA = true;
         i1 = l / np2;
@@ -311,6 +316,7 @@ __device__ __forceinline__ uint32_t sw128(int row, int k) {
     return uint32_t(row) * 128u + ((uint32_t(k >> 2) ^ uint32_t(row & 7)) << 4) + uint32_t(k & 3) * 4u;
 }
 
+template <int JW>
 __global__ void __launch_bounds__(192, 1)
     tj_apply_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                     const __grid_constant__ CUtensorMap tmVh, const __grid_constant__ CUtensorMap tmVl,
@@ -361,8 +367,9 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t idesc = idesc_tf32(JP, JP);
+    constexpr int G = JP / (2 * JW), NB = JP / JW;  // pairs and blocks per tile
     const int total = p.nb * (p.tilesA + p.tilesV);
-    const int npairs = p.m / 2, nquads = p.m / 4;
+    const int npairs = p.m / 2, ntiles = npairs / G;
 
     // phase bits (per barrier), advanced identically by every role that waits on it
     uint32_t ph_full1[2] = {0, 0}, ph_empty1[2] = {0, 0}, ph_full2[2] = {0, 0}, ph_empty2[2] = {0, 0};
@@ -375,18 +382,22 @@ __global__ void __launch_bounds__(192, 1)
         tj_decode(p, t, b, isA, i1, i2);
         // skip converged work (uniform across the CTA)
         if (!p.active[b]) continue;
-        const int f2 = p.pflag[b * npairs + 2 * i2] | p.pflag[b * npairs + 2 * i2 + 1];
-        const int f1 = isA ? (p.pflag[b * npairs + 2 * i1] | p.pflag[b * npairs + 2 * i1 + 1]) : 0;
-        if (!f2 && !f1) continue;
-        // the quad's four 32-blocks: pair 2g -> (0, 1), pair 2g+1 -> (2, 3)
-        int blk1[4] = {0, 0, 0, 0}, blk2[4];
-        pair_of(2 * i2, p.round, p.m, blk2[0], blk2[1]);
-        pair_of(2 * i2 + 1, p.round, p.m, blk2[2], blk2[3]);
-        if (isA) {
-            pair_of(2 * i1, p.round, p.m, blk1[0], blk1[1]);
-            pair_of(2 * i1 + 1, p.round, p.m, blk1[2], blk1[3]);
+        int f2 = 0, f1 = 0;
+#pragma unroll
+        for (int t2 = 0; t2 < G; ++t2) {
+            f2 |= p.pflag[b * npairs + G * i2 + t2];
+            if (isA) f1 |= p.pflag[b * npairs + G * i1 + t2];
         }
-        const int jb2 = b * nquads + i2, jb1 = b * nquads + i1;
+        if (!f2 && !f1) continue;
+        // the tile's JW-wide blocks: pair G*g + t -> blocks (2t, 2t+1)
+        int blk1[NB], blk2[NB];
+#pragma unroll
+        for (int t2 = 0; t2 < G; ++t2) {
+            pair_of(G * i2 + t2, p.round, p.m, blk2[2 * t2], blk2[2 * t2 + 1]);
+            if (isA) pair_of(G * i1 + t2, p.round, p.m, blk1[2 * t2], blk1[2 * t2 + 1]);
+            else blk1[2 * t2] = blk1[2 * t2 + 1] = 0;
+        }
+        const int jb2 = b * ntiles + i2, jb1 = b * ntiles + i1;
 
         if (warp == 0) {
             if (lane == 0) {
@@ -400,12 +411,12 @@ __global__ void __launch_bounds__(192, 1)
                     ++use1[s];
                     uint8_t* st = S + s * kStage1;
                     mbar_arrive_expect_tx(&full1[s], kStage1);
-                    const int col = blk2[c] * JW;  // K-chunk c = the quad's c-th 32-column block
+                    const int col = blk2[(c * 32) / JW] * JW + (c * 32) % JW;  // K-chunk c: 32 columns
 #pragma unroll
-                    for (int rb = 0; rb < 4; ++rb) {  // four 32-row boxes (4 KB each)
+                    for (int rb = 0; rb < NB; ++rb) {  // JW-row boxes
                         const int row0 = isA ? blk1[rb] * JW : i1 * JP + rb * JW;
-                        tma_load_3d(st + rb * (kChunk / 4), isA ? &tmAh : &tmVh, &full1[s], col, row0, b);
-                        tma_load_3d(st + kChunk + rb * (kChunk / 4), isA ? &tmAl : &tmVl, &full1[s], col, row0, b);
+                        tma_load_3d(st + rb * (kChunk / NB), isA ? &tmAh : &tmVh, &full1[s], col, row0, b);
+                        tma_load_3d(st + kChunk + rb * (kChunk / NB), isA ? &tmAl : &tmVl, &full1[s], col, row0, b);
                     }
                     tma_load_3d(st + 2 * kChunk, &tmJh, &full1[s], c * 32, 0, jb2);
                     tma_load_3d(st + 3 * kChunk, &tmJl, &full1[s], c * 32, 0, jb2);
@@ -501,14 +512,14 @@ __global__ void __launch_bounds__(192, 1)
                 mbar_wait(adone, ph_a);
                 tc_fence_after();
                 // A' rows -> natural positions
-                const int gr = blk1[row >> 5] * JW + (row & 31);
+                const int gr = blk1[row / JW] * JW + row % JW;
                 const int64_t base = int64_t(b) * p.D * p.D + int64_t(gr) * p.D;
 #pragma unroll 1
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(JP + cc * 32), r);
                     tmem_ld_wait();
-                    const int gc = blk2[cc] * JW;
+                    const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
                     float* dh = p.Ah + base + gc;
                     float* dl = p.Al + base + gc;
 #pragma unroll
@@ -530,7 +541,7 @@ __global__ void __launch_bounds__(192, 1)
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
                     tmem_ld_wait();
-                    const int gc = blk2[cc] * JW;
+                    const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
                     float* dh = p.Vh + base + gc;
                     float* dl = p.Vl + base + gc;
 #pragma unroll
@@ -741,27 +752,29 @@ bool tj_map(CUtensorMap* map, const float* base, int cols, int rows, int batch, 
 
 size_t tc_eigh_workspace_floats(int nb, int n) {
     const int D = (n + JP - 1) / JP * JP;
-    const int m = D / JW;
-    // A hi/lo, V hi/lo, J^T hi/lo per quad tile, then per matrix: fro, pad (2 doubles = 4 floats),
+    const int m = D / 32;  // the narrow variant has the most pairs
+    // A hi/lo, V hi/lo, J^T hi/lo per 128x128 tile, then per matrix: fro, pad (2 doubles = 4 floats),
     // active, sweeps, rotations, flags (m/2 pairs), ranks (D); and the loop counter.
-    return size_t(nb) * (4 * size_t(D) * D + 2 * size_t(m / 4) * JP * JP + 4 + 3 + size_t(m / 2) + D) + 4;
+    return size_t(nb) * (4 * size_t(D) * D + 2 * size_t(D / JP) * JP * JP + 4 + 3 + size_t(m / 2) + D) + 4;
 }
 
 int tc_eigh_dim(int n) { return (n + JP - 1) / JP * JP; }
 
 void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
-                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol) {
+                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize) {
     const int D = (n + JP - 1) / JP * JP;
     (void)D_in;  // B, J, J^T are [nb][D][D] with D = roundup(n, 128) (== the group's padded dim)
-    const int m = D / JW, npairs = m / 2, nquads = m / 4;
+    const bool wide = n >= kWidePairN;
+    const int JW = wide ? 64 : 32;
+    const int m = D / JW, npairs = m / 2, ntiles = D / JP;  // 128x128 J tiles per matrix
     const size_t DD = size_t(D) * D;
     float* Ah = ws;
     float* Al = Ah + size_t(nb) * DD;
     float* Vh = Al + size_t(nb) * DD;
     float* Vl = Vh + size_t(nb) * DD;
     float* JPh = Vl + size_t(nb) * DD;
-    float* JPl = JPh + size_t(nb) * nquads * JP * JP;
-    double* fro = reinterpret_cast<double*>(JPl + size_t(nb) * nquads * JP * JP);
+    float* JPl = JPh + size_t(nb) * ntiles * JP * JP;
+    double* fro = reinterpret_cast<double*>(JPl + size_t(nb) * ntiles * JP * JP);
     double* pad = fro + nb;
     int* active = reinterpret_cast<int*>(pad + nb);
     int* sweeps = active + nb;
@@ -772,7 +785,10 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
 
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tj_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kApplySmem));
+        cudaFuncSetAttribute(tj_apply_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kApplySmem));
+        cudaFuncSetAttribute(tj_apply_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kApplySmem));
+        cudaFuncSetAttribute(tj_pair_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 65 * 4);
+        cudaFuncSetAttribute(tj_pair_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 128 * 129 * 4);
         cudaFuncSetAttribute(tj_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 4);
         cudaFuncSetAttribute(tj_sort_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8);
         attr = true;
@@ -787,12 +803,12 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
     ap.D = D;
     ap.m = m;
     ap.nb = nb;
-    ap.tilesA = nquads * nquads;
-    ap.tilesV = (D / JP) * nquads;
+    ap.tilesA = ntiles * ntiles;
+    ap.tilesV = ntiles * ntiles;
     CUtensorMap mAh, mAl, mVh, mVl, mJh, mJl;
     bool ok = tj_map(&mAh, Ah, D, D, nb, JW) && tj_map(&mAl, Al, D, D, nb, JW) && tj_map(&mVh, Vh, D, D, nb, JW) &&
-              tj_map(&mVl, Vl, D, D, nb, JW) && tj_map(&mJh, JPh, JP, JP, nb * nquads, JP) &&
-              tj_map(&mJl, JPl, JP, JP, nb * nquads, JP);
+              tj_map(&mVl, Vl, D, D, nb, JW) && tj_map(&mJh, JPh, JP, JP, nb * ntiles, JP) &&
+              tj_map(&mJl, JPl, JP, JP, nb * ntiles, JP);
     if (!ok) {
         // tensor maps unavailable: report through every matrix's status (no silent fallback)
         cudaMemsetAsync(status, 0xff, size_t(nb) * sizeof(int), s);
@@ -807,18 +823,24 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
     auto prologue = [&](cudaStream_t st) {
         cudaMemsetAsync(sweeps, 0, size_t(nb) * 2 * sizeof(int), st);  // sweeps, rotations
         cudaMemsetAsync(loop_count, 0, sizeof(int), st);
-        // quad tiles: the pair kernels write the two diagonal 64x64 blocks only
-        cudaMemsetAsync(JPh, 0, size_t(nb) * nquads * JP * JP * 2 * sizeof(float), st);
+        // J tiles: the pair kernels write their diagonal PW x PW blocks only
+        cudaMemsetAsync(JPh, 0, size_t(nb) * ntiles * JP * JP * 2 * sizeof(float), st);
         tj_stats_kernel<<<nb, 512, 0, st>>>(B, n, D, fro, pad, active, status);
         tj_init_kernel<<<dim3(128, nb), 256, 0, st>>>(B, n, D, pad, Ah, Al, Vh, Vl);
     };
     auto sweep = [&](cudaStream_t st) {
         for (int r = 0; r < m - 1; ++r) {
-            tj_pair_kernel<<<dim3(npairs, nb), kPairThreads, 0, st>>>(Ah, Al, D, m, r, JPh, JPl, pflag, rotations,
-                                                                               active, fro, n, ftol, inner);
             TJApply a = ap;
             a.round = r;
-            tj_apply_kernel<<<apply_grid, 192, kApplySmem, st>>>(mAh, mAl, mVh, mVl, mJh, mJl, a);
+            if (wide) {
+                tj_pair_kernel<128><<<dim3(npairs, nb), 512, 2 * 128 * 129 * 4, st>>>(
+                    Ah, Al, D, m, r, JPh, JPl, pflag, rotations, active, fro, n, ftol, inner);
+                tj_apply_kernel<64><<<apply_grid, 192, kApplySmem, st>>>(mAh, mAl, mVh, mVl, mJh, mJl, a);
+            } else {
+                tj_pair_kernel<64><<<dim3(npairs, nb), 256, 2 * 64 * 65 * 4, st>>>(
+                    Ah, Al, D, m, r, JPh, JPl, pflag, rotations, active, fro, n, ftol, inner);
+                tj_apply_kernel<32><<<apply_grid, 192, kApplySmem, st>>>(mAh, mAl, mVh, mVl, mJh, mJl, a);
+            }
         }
         tj_converge_kernel<<<(nb + 127) / 128, 128, 0, st>>>(nb, active, rotations, sweeps, debug, n);
     };
@@ -843,6 +865,8 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
         gemm_launch(gl, JTl ? ASG_PREC_3XTF32 : ASG_PREC_TF32, num_sms, st);
         tj_rayleigh_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(Jh, Jl, JTh, JTl, Vh, n, D, values);
         tj_sort_values_kernel<<<nb, 512, size_t(n) * 8, st>>>(values, n);
+        count_launch(2);  // rayleigh + sort (split / GEMM count themselves)
+        if (!orthonormalize) return;
         // one Newton-Schulz polar step on J (orthonormal to the fp32 floor):
         // S = J^T J -> X = (3I - S)/2 -> J X; A/V slabs are free scratch here
         GemmLaunch gs{};
@@ -871,7 +895,6 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
         cudaMemcpyAsync(Jh, Ah, size_t(nb) * DD * 4, cudaMemcpyDeviceToDevice, st);
         if (Jl) cudaMemcpyAsync(Jl, Al, size_t(nb) * DD * 4, cudaMemcpyDeviceToDevice, st);
         launch_transpose_split(Ah, Jl ? Al : nullptr, nb, D, D, JTh, JTl, false, st);
-        count_launch(3);
     };
     if (debug) {
         prologue(s);

@@ -855,8 +855,9 @@ void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cu
     launch_snapshot_sym(t[4], cnt, D, d, bs->ws_snap, s);  // fp64 copy: trace for the damping (and small solves)
     if (d > kSmallEighN && !bs->fp64_jacobi) {
         // tensor-core block Jacobi: J -> (t0, t1), J^T -> (t2, t3)
+        // (Q J is re-orthonormalized below / at the SOAP install, so J itself is not)
         launch_tc_eigh(t[4], D, bs->ws_vals, t[0], t1, t[2], t3, bs->tc_ws, cnt, d, g.d_status + s0, bs->num_sms, s,
-                       kF32RefreshTol);
+                       kF32RefreshTol, false);
     } else {
         EighOpts eo;
         eo.relative = 1;
@@ -2081,6 +2082,13 @@ int asg_unpack_gathered(asg_blockset* bs, const float* recvbuf, int64_t stride_e
 }
 
 // ---- profiling ------------------------------------------------------------------
+int asg_launch_count(uint64_t* count) {
+    return guard([&] {
+        if (!count) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        *count = launch_count();
+    });
+}
+
 int asg_profile_enable(asg_blockset* bs, int32_t enable) {
     return guard([&] {
         bs->profiling = enable != 0;

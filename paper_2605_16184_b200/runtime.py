@@ -63,6 +63,7 @@ _SIGS = {
     "asg_shard_elems": (C.c_int, [_vp, _i32, _P(_i64)]),
     "asg_pack_owned": (C.c_int, [_vp, _vp, _vp]),
     "asg_unpack_gathered": (C.c_int, [_vp, _vp, _i64, _vp]),
+    "asg_launch_count": (C.c_int, [_P(_u64)]),
     "asg_profile_enable": (C.c_int, [_vp, _i32]),
     "asg_get_kernel_stats": (C.c_int, [_vp, _P(abi.KernelStats), _i32]),
     "asg_gemm_tn": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _f32, _i32, _vp]),
