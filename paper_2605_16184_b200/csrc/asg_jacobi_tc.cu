@@ -196,10 +196,7 @@ __global__ void __launch_bounds__(PW * 4) tj_pair_kernel(const float* __restrict
         if (threadIdx.x == 0) *flag = 0;
         return;
     }
-    if (threadIdx.x == 0) {
-        *flag = 1;
-        atomicAdd(&rotations[b], 1);
-    }
+    if (threadIdx.x == 0) *flag = 1;
     const float itol = 0.1f * tol;
     for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
         bool rot_any = false;
@@ -221,7 +218,8 @@ __global__ void __launch_bounds__(PW * 4) tj_pair_kernel(const float* __restrict
                 cs[threadIdx.x] = cc;
                 sn[threadIdx.x] = ss;
             }
-            __syncthreads();
+            // nearly diagonal pairs (warm refreshes) rotate in few rounds: skip the rest
+            if (!__syncthreads_or(threadIdx.x < PW / 2 && sn[threadIdx.x] != 0.f)) continue;
             for (int e = threadIdx.x; e < (PW / 2) * PW; e += blockDim.x) {  // rows of S
                 const int kk = e / PW, j = e % PW;
                 const float ss = sn[kk];
@@ -292,7 +290,8 @@ constexpr uint32_t kStage1 = 4 * kChunk;      // A hi/lo + J hi/lo
 constexpr uint32_t kStage2 = 2 * kChunk;      // J_k1^T hi/lo
 constexpr uint32_t kRegionS = 2 * kStage1;    // 128 KB: MMA1 ring, then X^T (4 chunks hi/lo)
 constexpr uint32_t kRegionT = 2 * kStage2;    // 64 KB
-constexpr size_t kApplySmem = 1024 + size_t(kRegionS) + kRegionT + 256;
+constexpr int kMaxFlags = 4096;  // nb * pairs per launch (asserted by the launcher)
+constexpr size_t kApplySmem = 1024 + size_t(kRegionS) + kRegionT + 128 + kMaxFlags * 4;
 
 __device__ __forceinline__ void tj_decode(const TJApply& p, int t, int& b, bool& isA, int& i1, int& i2) {
     const int per = p.tilesA + p.tilesV;
@@ -367,6 +366,12 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t idesc = idesc_tf32(JP, JP);
+    // per-pair flags and per-matrix activity, read once per launch (most tiles of
+    // a warm refresh are skipped; a global load per tile would serialise them)
+    int* sflag = reinterpret_cast<int*>(bars + 16);
+    const int nflags = p.nb * (p.m / 2);
+    for (int i = threadIdx.x; i < nflags; i += blockDim.x) sflag[i] = p.pflag[i] | (p.active[i / (p.m / 2)] << 1);
+    __syncthreads();
     constexpr int G = JP / (2 * JW), NB = JP / JW;  // pairs and blocks per tile
     const int total = p.nb * (p.tilesA + p.tilesV);
     const int npairs = p.m / 2, ntiles = npairs / G;
@@ -381,12 +386,12 @@ __global__ void __launch_bounds__(192, 1)
         bool isA;
         tj_decode(p, t, b, isA, i1, i2);
         // skip converged work (uniform across the CTA)
-        if (!p.active[b]) continue;
+        if (!(sflag[b * npairs] >> 1)) continue;  // matrix converged
         int f2 = 0, f1 = 0;
 #pragma unroll
         for (int t2 = 0; t2 < G; ++t2) {
-            f2 |= p.pflag[b * npairs + G * i2 + t2];
-            if (isA) f1 |= p.pflag[b * npairs + G * i1 + t2];
+            f2 |= sflag[b * npairs + G * i2 + t2] & 1;
+            if (isA) f1 |= sflag[b * npairs + G * i1 + t2] & 1;
         }
         if (!f2 && !f1) continue;
         // the tile's JW-wide blocks: pair G*g + t -> blocks (2t, 2t+1)
@@ -575,14 +580,40 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ---- convergence / loop / finish ------------------------------------------------------
-__global__ void tj_converge_kernel(int nb, int* __restrict__ active, int* __restrict__ rotations,
-                                   int* __restrict__ sweeps, int debug, int n) {
+// Convergence test over the whole matrix (the pair kernels' skip rule applied
+// to every off-diagonal element): big[b] = 1 if some element of matrix b still
+// exceeds the threshold. Grid (D/32 row groups, nb).
+__global__ void tj_check_kernel(const float* __restrict__ Ah, const float* __restrict__ Al, int D, int n,
+                                const double* __restrict__ fro, const int* __restrict__ active, int* __restrict__ big,
+                                float tol) {
+    const int64_t b = blockIdx.y;
+    if (!active[b]) return;
+    const int64_t DD = int64_t(D) * D;
+    const float floor_s = float(fro[b] / sqrt(double(n)));
+    bool any = false;
+    for (int r = blockIdx.x * 32 + (threadIdx.x >> 5); r < min(D, blockIdx.x * 32 + 32); r += blockDim.x >> 5) {
+        const float dr = fabsf(Ah[b * DD + int64_t(r) * D + r] + Al[b * DD + int64_t(r) * D + r]);
+        for (int c = threadIdx.x & 31; c < D; c += 32) {
+            if (c == r) continue;
+            const int64_t o = b * DD + int64_t(r) * D + c;
+            const float x = fabsf(Ah[o] + Al[o]);
+            if (x == 0.f) continue;
+            const float dc = fabsf(Ah[b * DD + int64_t(c) * D + c] + Al[b * DD + int64_t(c) * D + c]);
+            any |= x > tol * fmaxf(sqrtf(dr * dc), floor_s);
+        }
+    }
+    if (__syncthreads_or(any) && threadIdx.x == 0) big[b] = 1;
+}
+
+// After a sweep: a matrix stays active only while the check found a large element.
+__global__ void tj_settle_kernel(int nb, int* __restrict__ active, int* __restrict__ big, int* __restrict__ sweeps,
+                                 int debug, int n, int count_sweep) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nb || !active[b]) return;
-    sweeps[b] += 1;
-    if (debug) printf("tjdbg n=%d b=%d sweep=%d rotated pairs=%d\n", n, b, sweeps[b], rotations[b]);
-    if (rotations[b] == 0) active[b] = 0;
-    rotations[b] = 0;
+    if (count_sweep) sweeps[b] += 1;
+    if (debug) printf("tjdbg n=%d b=%d sweeps=%d still_large=%d\n", n, b, sweeps[b], big[b]);
+    if (!big[b]) active[b] = 0;
+    big[b] = 0;
 }
 
 __global__ void tj_loop_kernel(const int* __restrict__ active, int nb, int* __restrict__ sweep_count, int max_sweeps,
@@ -760,8 +791,9 @@ size_t tc_eigh_workspace_floats(int nb, int n) {
 
 int tc_eigh_dim(int n) { return (n + JP - 1) / JP * JP; }
 
-void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
-                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize) {
+namespace {
+void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
+                   int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize) {
     const int D = (n + JP - 1) / JP * JP;
     (void)D_in;  // B, J, J^T are [nb][D][D] with D = roundup(n, 128) (== the group's padded dim)
     const bool wide = n >= kWidePairN;
@@ -820,13 +852,19 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
     const int total_tiles = nb * (ap.tilesA + ap.tilesV);
     const int apply_grid = total_tiles < num_sms ? total_tiles : num_sms;
 
+    int* big = rotations;  // per-matrix "some element still above threshold" (tj_check_kernel)
+    auto check = [&](cudaStream_t st, int count_sweep) {
+        tj_check_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(Ah, Al, D, n, fro, active, big, ftol);
+        tj_settle_kernel<<<(nb + 127) / 128, 128, 0, st>>>(nb, active, big, sweeps, debug, n, count_sweep);
+    };
     auto prologue = [&](cudaStream_t st) {
-        cudaMemsetAsync(sweeps, 0, size_t(nb) * 2 * sizeof(int), st);  // sweeps, rotations
+        cudaMemsetAsync(sweeps, 0, size_t(nb) * 2 * sizeof(int), st);  // sweeps, rotations/big
         cudaMemsetAsync(loop_count, 0, sizeof(int), st);
         // J tiles: the pair kernels write their diagonal PW x PW blocks only
         cudaMemsetAsync(JPh, 0, size_t(nb) * ntiles * JP * JP * 2 * sizeof(float), st);
         tj_stats_kernel<<<nb, 512, 0, st>>>(B, n, D, fro, pad, active, status);
         tj_init_kernel<<<dim3(128, nb), 256, 0, st>>>(B, n, D, pad, Ah, Al, Vh, Vl);
+        check(st, 0);  // already diagonal to the threshold (warm refresh): no sweep at all
     };
     auto sweep = [&](cudaStream_t st) {
         for (int r = 0; r < m - 1; ++r) {
@@ -842,7 +880,7 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
                 tj_apply_kernel<32><<<apply_grid, 192, kApplySmem, st>>>(mAh, mAl, mVh, mVl, mJh, mJl, a);
             }
         }
-        tj_converge_kernel<<<(nb + 127) / 128, 128, 0, st>>>(nb, active, rotations, sweeps, debug, n);
+        check(st, 1);
     };
     auto epilogue = [&](cudaStream_t st) {
         tj_rank_kernel<<<nb, 512, size_t(D) * 4, st>>>(Ah, Al, n, D, rank, values, active, status);
@@ -928,17 +966,27 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
         cudaGraph_t g = nullptr;
         cudaGraphCreate(&g, 0);
         cudaGraphConditionalHandle handle;
-        cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault);
+        cudaGraphConditionalHandleCreate(&handle, g, 0, cudaGraphCondAssignDefault);
         cudaGraph_t gpro = capture(prologue);
         cudaGraph_t gepi = capture(epilogue);
-        cudaGraphNode_t npro, nloop, nepi;
+        cudaGraphNode_t npro, ndecide, nloop, nepi;
         cudaGraphAddChildGraphNode(&npro, g, nullptr, 0, gpro);
+        // enter the loop only if the prologue's check left a matrix active
+        int max_sweeps = kEighMaxLaunchedSweeps;
+        void* kargs[] = {&active, &nb, &loop_count, &max_sweeps, &handle};
+        cudaKernelNodeParams kp{};
+        kp.func = reinterpret_cast<void*>(tj_loop_kernel);
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(256);
+        kp.sharedMemBytes = 0;
+        kp.kernelParams = kargs;
+        cudaGraphAddKernelNode(&ndecide, g, &npro, 1, &kp);
         cudaGraphNodeParams cp{};
         cp.type = cudaGraphNodeTypeConditional;
         cp.conditional.handle = handle;
         cp.conditional.type = cudaGraphCondTypeWhile;
         cp.conditional.size = 1;
-        cudaGraphAddNode(&nloop, g, &npro, 1, &cp);
+        cudaGraphAddNode(&nloop, g, &ndecide, 1, &cp);
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
         sweep(cap);
@@ -956,6 +1004,22 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
     count_launch(4 + 2 * uint64_t(m - 1) + 2 + 2);
     cudaGraphLaunch(exec, s);
     rayleigh(s);
+}
+}  // namespace
+
+void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
+                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize) {
+    // the apply kernel keeps every pair flag of a launch in shared memory
+    const int D = (n + JP - 1) / JP * JP;
+    const int npairs = D / (n >= kWidePairN ? 64 : 32) / 2;
+    const int sub = kMaxFlags / npairs;
+    const size_t DD = size_t(D) * D;
+    for (int b0 = 0; b0 < nb; b0 += sub) {
+        const int cnt = nb - b0 < sub ? nb - b0 : sub;
+        tc_eigh_chunk(B + size_t(b0) * DD, D_in, values + size_t(b0) * n, Jh + size_t(b0) * DD,
+                      Jl ? Jl + size_t(b0) * DD : nullptr, JTh + size_t(b0) * DD, JTl ? JTl + size_t(b0) * DD : nullptr,
+                      ws, cnt, n, status + b0, num_sms, s, tol, orthonormalize);
+    }
 }
 
 }  // namespace asg

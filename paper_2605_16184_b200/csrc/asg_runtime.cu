@@ -297,7 +297,12 @@ bool is_kl(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_KL_SHAM
 bool split_mode(const asg_blockset* bs) { return bs->precision == ASG_PREC_3XTF32; }
 bool f32_refresh(const asg_blockset* bs) { return bs->sc.refresh_mode == ASG_REFRESH_F32; }
 // Relative threshold of the F32 refresh's Jacobi (asg_eigh.cuh EighOpts).
-constexpr double kF32RefreshTol = 1e-6;
+constexpr double kF32RefreshTolDefault = 1e-6;
+// ASG_F32_TOL overrides the threshold (diagnostics / tuning).
+double f32_refresh_tol() {
+    static const double t = getenv("ASG_F32_TOL") ? atof(getenv("ASG_F32_TOL")) : kF32RefreshTolDefault;
+    return t;
+}
 
 void emit(asg_blockset* bs, int64_t step, int kind, int64_t block, uint64_t version, double t) {
     asg_event e{};
@@ -810,7 +815,37 @@ void orthonormalize(asg_blockset* bs, const float* Vh, const float* Vl, float* o
 //   threshold), then Shampoo/KL: V = Q J becomes the new basis and the roots
 //   V f(lambda) V^T are GEMMs; SOAP: J^T is kept as the shadow rotation, the
 //   install forms Q J and re-projects the moments (install_soap_f32).
+// ASG_REFRESH_TIMING=1: per refresh chunk, host-synchronous phase timings on
+// the side stream (diagnostics only; breaks the overlap with the main stream).
+struct PhaseTimer {
+    bool on;
+    cudaStream_t s;
+    std::vector<std::pair<const char*, cudaEvent_t>> marks;
+    explicit PhaseTimer(cudaStream_t st) : on(getenv("ASG_REFRESH_TIMING") != nullptr), s(st) {}
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        marks.emplace_back(name, e);
+    }
+    void report(int d, int cnt) {
+        if (!on || marks.size() < 2) return;
+        cudaEventSynchronize(marks.back().second);
+        std::fprintf(stderr, "refresh d=%d cnt=%d:", d, cnt);
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+            std::fprintf(stderr, " %s %.3f", marks[i].first, ms);
+        }
+        std::fprintf(stderr, " ms\n");
+        for (auto& m : marks) cudaEventDestroy(m.second);
+    }
+};
+
 void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaStream_t s) {
+    PhaseTimer pt(s);
+    pt.mark("start");
     const int d = left ? g.m : g.n, D = left ? g.M : g.N;
     const size_t DD = size_t(D) * D, cntDD = size_t(cnt) * DD;
     const double dd3 = double(cnt) * d * double(d) * d;
@@ -852,20 +887,23 @@ void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cu
     p2.ldc = D;
     p2.c_bstride = int64_t(DD);
     run_gemm(bs, op(QTh, QTl, D, D), op(t[2], t3, D, D), cnt, EPI_STORE, p2, nullptr, 0, s, 2.0 * dd3);
+    pt.mark("transform");
     launch_snapshot_sym(t[4], cnt, D, d, bs->ws_snap, s);  // fp64 copy: trace for the damping (and small solves)
     if (d > kSmallEighN && !bs->fp64_jacobi) {
         // tensor-core block Jacobi: J -> (t0, t1), J^T -> (t2, t3)
         // (Q J is re-orthonormalized below / at the SOAP install, so J itself is not)
         launch_tc_eigh(t[4], D, bs->ws_vals, t[0], t1, t[2], t3, bs->tc_ws, cnt, d, g.d_status + s0, bs->num_sms, s,
-                       kF32RefreshTol, false);
+                       f32_refresh_tol(), false);
     } else {
         EighOpts eo;
         eo.relative = 1;
-        eo.tol = kF32RefreshTol;
+        eo.tol = f32_refresh_tol();
         launch_eigh(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, cnt, d, g.d_status + s0, s, nullptr, eo);
         launch_f64_to_split(bs->ws_vecs, cnt, d, D, false, t[0], t1, t[2], t3, s);
     }
+    pt.mark("eigh");
     if (is_soap(bs)) {
+        pt.report(d, cnt);
         CK(cudaMemcpyAsync(at(left ? g.sJLTh : g.sJRTh, DD, s0), t[2], cntDD * 4, cudaMemcpyDeviceToDevice, s));
         if (sp)
             CK(cudaMemcpyAsync(at(left ? g.sJLTl : g.sJRTl, DD, s0), t[3], cntDD * 4, cudaMemcpyDeviceToDevice, s));
@@ -909,6 +947,8 @@ void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cu
         pr.d_bstride = int64_t(DD);
         run_gemm(bs, op(t[6], t7, D, D), op(t[4], t5, D, D), cnt, EPI_SPLIT, pr, nullptr, 0, s, 2.0 * dd3);
     }
+    pt.mark("basis+roots");
+    pt.report(d, cnt);
 }
 
 // Launches the refresh for every unit marked dispatched-but-not-launched.
@@ -2246,7 +2286,7 @@ int asg_sym_eig_batched_f32(const float* A, double* values, float* vectors, int6
         CK(cudaMemsetAsync(status, 0, size_t(batch) * sizeof(int), s));
         pad_f32_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(A, int(n), D, Bp);
         launch_tc_eigh(Bp, D, values, J, J + nbDD, J + 2 * nbDD, J + 3 * nbDD, ws, int(batch), int(n), status, sms, s,
-                       kF32RefreshTol);
+                       f32_refresh_tol());
         unpad_sum_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(J, J + nbDD, int(n), D, vectors);
         count_launch(2);
         std::vector<int> st(static_cast<size_t>(batch));
