@@ -593,8 +593,9 @@ __global__ void tj_check_kernel(const float* __restrict__ Ah, const float* __res
     bool any = false;
     for (int r = blockIdx.x * 32 + (threadIdx.x >> 5); r < min(D, blockIdx.x * 32 + 32); r += blockDim.x >> 5) {
         const float dr = fabsf(Ah[b * DD + int64_t(r) * D + r] + Al[b * DD + int64_t(r) * D + r]);
-        for (int c = threadIdx.x & 31; c < D; c += 32) {
-            if (c == r) continue;
+        // upper triangle only: the pair kernels test a_ij with i < j too (the two
+        // triangles differ in their last bits after independent tile products)
+        for (int c = r + 1 + (threadIdx.x & 31); c < D; c += 32) {
             const int64_t o = b * DD + int64_t(r) * D + c;
             const float x = fabsf(Ah[o] + Al[o]);
             if (x == 0.f) continue;
