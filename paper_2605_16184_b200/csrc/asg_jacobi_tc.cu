@@ -586,20 +586,24 @@ __global__ void __launch_bounds__(192, 1)
 __global__ void tj_check_kernel(const float* __restrict__ Ah, const float* __restrict__ Al, int D, int n,
                                 const double* __restrict__ fro, const int* __restrict__ active, int* __restrict__ big,
                                 float tol) {
+    extern __shared__ float dgs[];  // |diag(A)| of matrix b
     const int64_t b = blockIdx.y;
     if (!active[b]) return;
     const int64_t DD = int64_t(D) * D;
+    for (int i = threadIdx.x; i < D; i += blockDim.x)
+        dgs[i] = fabsf(Ah[b * DD + int64_t(i) * D + i] + Al[b * DD + int64_t(i) * D + i]);
+    __syncthreads();
     const float floor_s = float(fro[b] / sqrt(double(n)));
     bool any = false;
     for (int r = blockIdx.x * 32 + (threadIdx.x >> 5); r < min(D, blockIdx.x * 32 + 32); r += blockDim.x >> 5) {
-        const float dr = fabsf(Ah[b * DD + int64_t(r) * D + r] + Al[b * DD + int64_t(r) * D + r]);
+        const float dr = dgs[r];
         // upper triangle only: the pair kernels test a_ij with i < j too (the two
         // triangles differ in their last bits after independent tile products)
         for (int c = r + 1 + (threadIdx.x & 31); c < D; c += 32) {
             const int64_t o = b * DD + int64_t(r) * D + c;
             const float x = fabsf(Ah[o] + Al[o]);
             if (x == 0.f) continue;
-            const float dc = fabsf(Ah[b * DD + int64_t(c) * D + c] + Al[b * DD + int64_t(c) * D + c]);
+            const float dc = dgs[c];
             any |= x > tol * fmaxf(sqrtf(dr * dc), floor_s);
         }
     }
@@ -855,7 +859,7 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
 
     int* big = rotations;  // per-matrix "some element still above threshold" (tj_check_kernel)
     auto check = [&](cudaStream_t st, int count_sweep) {
-        tj_check_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(Ah, Al, D, n, fro, active, big, ftol);
+        tj_check_kernel<<<dim3(D / 32, nb), 256, size_t(D) * 4, st>>>(Ah, Al, D, n, fro, active, big, ftol);
         tj_settle_kernel<<<(nb + 127) / 128, 128, 0, st>>>(nb, active, big, sweeps, debug, n, count_sweep);
     };
     auto prologue = [&](cudaStream_t st) {
