@@ -82,38 +82,42 @@ __device__ double tj_block_sum(double v, double* red) {
 }
 
 // ---- init -------------------------------------------------------------------
-// One CTA per matrix: ||B||_F, the Gershgorin bound for the padding, finite check.
-__global__ void tj_stats_kernel(const float* __restrict__ B, int n, int D, double* __restrict__ fro,
-                                double* __restrict__ pad, int* __restrict__ active, int* __restrict__ status) {
-    __shared__ double red[32];
-    const int64_t b = blockIdx.x;
+// ||B||_F^2, the Gershgorin bound (max absolute row sum) for the padding and
+// a non-finite flag, accumulated with atomics; grid (D/32 row groups, nb),
+// one warp per row, lanes along the row (coalesced).
+__global__ void tj_stats_kernel(const float* __restrict__ B, int n, int D, double* __restrict__ fro2,
+                                unsigned* __restrict__ bound_bits, int* __restrict__ bad) {
+    const int64_t b = blockIdx.y;
     const float* Bb = B + b * int64_t(D) * D;
-    double s = 0.0, bound = 0.0;
-    bool bad = false;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double r = 0.0;
-        for (int j = 0; j < n; ++j) {
-            const double x = Bb[int64_t(i) * D + j];
-            bad |= !isfinite(x);
-            s += x * x;
-            r += fabs(x);
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    bool nf = false;
+    for (int r = blockIdx.x * 32 + (threadIdx.x >> 5); r < min(n, blockIdx.x * 32 + 32); r += blockDim.x >> 5) {
+        float rs = 0.f;
+        for (int c = lane; c < n; c += 32) {
+            const float x = Bb[int64_t(r) * D + c];
+            nf |= !isfinite(x);
+            s += double(x) * x;
+            rs += fabsf(x);
         }
-        bound = fmax(bound, r);
+        for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffff, rs, o);
+        if (lane == 0) atomicMax(&bound_bits[b], __float_as_uint(rs));  // non-negative: bit order = value order
     }
-    const int any_bad = __syncthreads_or(bad);
-    s = tj_block_sum(s, red);
-    for (int o = 16; o > 0; o >>= 1) bound = fmax(bound, __shfl_xor_sync(0xffffffff, bound, o));
-    __shared__ double bm[32];
-    if ((threadIdx.x & 31) == 0) bm[threadIdx.x >> 5] = bound;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double mx = 0.0;
-        for (int w = 0; w < int(blockDim.x >> 5); ++w) mx = fmax(mx, bm[w]);
-        fro[b] = sqrt(s);
-        pad[b] = mx > 0.0 ? 2.0 * mx : 1.0;
-        active[b] = any_bad ? 0 : 1;
-        if (any_bad) atomicCAS(&status[b], ASG_OK, ASG_ERR_NON_FINITE);
-    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+    if (lane == 0 && s != 0.0) atomicAdd(&fro2[b], s);
+    if (__any_sync(0xffffffff, nf) && lane == 0) atomicOr(&bad[b], 1);
+}
+
+__global__ void tj_stats_finish_kernel(int nb, double* __restrict__ fro, double* __restrict__ pad,
+                                       const unsigned* __restrict__ bound_bits, const int* __restrict__ bad,
+                                       int* __restrict__ active, int* __restrict__ status) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    fro[b] = sqrt(fro[b]);  // accumulated as ||B||_F^2
+    const double mx = double(__uint_as_float(bound_bits[b]));
+    pad[b] = mx > 0.0 ? 2.0 * mx : 1.0;
+    active[b] = bad[b] ? 0 : 1;
+    if (bad[b]) atomicCAS(&status[b], ASG_OK, ASG_ERR_NON_FINITE);
 }
 
 // A = B (+ distinct padding diagonal above the spectrum), V = I; both split.
@@ -125,7 +129,7 @@ __global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const 
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < DD; e += int64_t(gridDim.x) * blockDim.x) {
         const int i = int(e / D), j = int(e % D);
         float x;
-        if (i < n && j < n) x = 0.5f * (B[b * DD + e] + B[b * DD + int64_t(j) * D + i]);  // symmetrize
+        if (i < n && j < n) x = B[b * DD + e];  // symmetric to fp32 rounding; the sweeps read the upper triangle
         else x = (i == j) ? float(pad[b] * (1.0 + double(i - n + 1) * 1e-3)) : 0.f;
         float h, l;
         split_tf32(x, h, l);
@@ -650,34 +654,30 @@ __global__ void tj_rank_kernel(const float* __restrict__ Ah, const float* __rest
             const float dj = dg[j];
             r += (dj < di) || (dj == di && j < i);
         }
-        rank[b * D + i] = r;
+        rank[b * D + r] = i;  // inverse permutation: output column r <- V column i
         if (r < n) values[b * n + r] = double(di);
     }
 }
 
-// J[i][rank(c)] = V[i][c] for i, rank(c) < n (zero elsewhere), as split J and J^T.
+// J[i][r] = V[i][src(r)] for i, r < n (zero elsewhere), split; src = the
+// inverse rank permutation (coalesced writes; J^T follows by a tiled transpose).
 __global__ void tj_gather_kernel(const float* __restrict__ Vh, const float* __restrict__ Vl,
-                                 const int* __restrict__ rank, int n, int D, float* __restrict__ Jh,
-                                 float* __restrict__ Jl, float* __restrict__ JTh, float* __restrict__ JTl) {
+                                 const int* __restrict__ src, int n, int D, float* __restrict__ Jh,
+                                 float* __restrict__ Jl) {
     const int64_t b = blockIdx.y;
     const int64_t DD = int64_t(D) * D;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < DD; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / D), c = int(e % D);
-        const int rc = rank[b * D + c];
+        const int i = int(e / D), r = int(e % D);
         float h = 0.f, l = 0.f;
-        if (i < n && rc < n) {
-            h = Vh[b * DD + e];
-            l = Vl[b * DD + e];
+        if (i < n && r < n) {
+            const int64_t o = b * DD + int64_t(i) * D + src[b * D + r];
+            h = Vh[o];
+            l = Vl[o];
         }
-        if (rc < D) {
-            Jh[b * DD + int64_t(i) * D + rc] = h;
-            if (Jl) Jl[b * DD + int64_t(i) * D + rc] = l;
-            JTh[b * DD + int64_t(rc) * D + i] = h;
-            if (JTl) JTl[b * DD + int64_t(rc) * D + i] = l;
-        }
+        Jh[b * DD + e] = h;
+        if (Jl) Jl[b * DD + e] = l;
     }
 }
-
 
 // Rayleigh-quotient eigenvalues and unit eigenvectors from the solve's J and
 // W = B J (one 3xTF32 product): lambda_i = (J_i . W_i) / (J_i . J_i), then
@@ -867,7 +867,12 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
         cudaMemsetAsync(loop_count, 0, sizeof(int), st);
         // J tiles: the pair kernels write their diagonal PW x PW blocks only
         cudaMemsetAsync(JPh, 0, size_t(nb) * ntiles * JP * JP * 2 * sizeof(float), st);
-        tj_stats_kernel<<<nb, 512, 0, st>>>(B, n, D, fro, pad, active, status);
+        unsigned* bound_bits = reinterpret_cast<unsigned*>(rank);  // rank[] is free until the epilogue
+        int* bad = rank + nb;
+        cudaMemsetAsync(fro, 0, size_t(nb) * sizeof(double), st);
+        cudaMemsetAsync(rank, 0, size_t(nb) * 2 * sizeof(int), st);
+        tj_stats_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(B, n, D, fro, bound_bits, bad);
+        tj_stats_finish_kernel<<<(nb + 127) / 128, 128, 0, st>>>(nb, fro, pad, bound_bits, bad, active, status);
         tj_init_kernel<<<dim3(128, nb), 256, 0, st>>>(B, n, D, pad, Ah, Al, Vh, Vl);
         check(st, 0);  // already diagonal to the threshold (warm refresh): no sweep at all
     };
@@ -889,7 +894,8 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
     };
     auto epilogue = [&](cudaStream_t st) {
         tj_rank_kernel<<<nb, 512, size_t(D) * 4, st>>>(Ah, Al, n, D, rank, values, active, status);
-        tj_gather_kernel<<<dim3(256, nb), 256, 0, st>>>(Vh, Vl, rank, n, D, Jh, Jl, JTh, JTl);
+        tj_gather_kernel<<<dim3(256, nb), 256, 0, st>>>(Vh, Vl, rank, n, D, Jh, Jl);
+        launch_transpose_split(Jh, Jl, nb, D, D, JTh, JTl, false, st);
     };
     // W = B J (3xTF32, or TF32 when the outputs carry no lo part), then
     // Rayleigh quotients + unit columns. Enqueued outside the cached graph.
