@@ -64,23 +64,6 @@ __device__ __forceinline__ void pair_of(int k, int r, int m, int& p, int& q) {
 template <int JW>
 __device__ __forceinline__ int nat(int i, int p, int q) { return i < JW ? p * JW + i : q * JW + (i - JW); }
 
-__device__ double tj_block_sum(double v, double* red) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    if (w == 0) {
-        v = (l < int(blockDim.x >> 5)) ? red[l] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
-        if (l == 0) red[0] = v;
-    }
-    __syncthreads();
-    const double r = red[0];
-    __syncthreads();
-    return r;
-}
-
 // ---- init -------------------------------------------------------------------
 // ||B||_F^2, the Gershgorin bound (max absolute row sum) for the padding and
 // a non-finite flag, accumulated with atomics; grid (D/32 row groups, nb),
@@ -120,23 +103,32 @@ __global__ void tj_stats_finish_kernel(int nb, double* __restrict__ fro, double*
     if (bad[b]) atomicCAS(&status[b], ASG_OK, ASG_ERR_NON_FINITE);
 }
 
-// A = B (+ distinct padding diagonal above the spectrum), V = I; both split.
+// A = (B + B^T)/2 (+ distinct padding diagonal above the spectrum), V = I;
+// both split. Tiled 32x32 through shared memory so both reads are coalesced.
 __global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const double* __restrict__ pad,
                                float* __restrict__ Ah, float* __restrict__ Al, float* __restrict__ Vh,
                                float* __restrict__ Vl) {
-    const int64_t b = blockIdx.y;
+    __shared__ float t1[32][33], t2[32][33];
+    const int64_t b = blockIdx.z;
     const int64_t DD = int64_t(D) * D;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < DD; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / D), j = int(e % D);
+    const int I = blockIdx.y * 32, J = blockIdx.x * 32;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        t1[dy][threadIdx.x] = B[b * DD + int64_t(I + dy) * D + J + threadIdx.x];
+        t2[dy][threadIdx.x] = B[b * DD + int64_t(J + dy) * D + I + threadIdx.x];
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int i = I + dy, j = J + threadIdx.x;
         float x;
-        if (i < n && j < n) x = B[b * DD + e];  // symmetric to fp32 rounding; the sweeps read the upper triangle
+        if (i < n && j < n) x = 0.5f * (t1[dy][threadIdx.x] + t2[threadIdx.x][dy]);
         else x = (i == j) ? float(pad[b] * (1.0 + double(i - n + 1) * 1e-3)) : 0.f;
         float h, l;
         split_tf32(x, h, l);
-        Ah[b * DD + e] = h;
-        Al[b * DD + e] = l;
-        Vh[b * DD + e] = (i == j) ? 1.f : 0.f;
-        Vl[b * DD + e] = 0.f;
+        const int64_t o = b * DD + int64_t(i) * D + j;
+        Ah[o] = h;
+        Al[o] = l;
+        Vh[o] = (i == j) ? 1.f : 0.f;
+        Vl[o] = 0.f;
     }
 }
 
@@ -873,7 +865,7 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
         cudaMemsetAsync(rank, 0, size_t(nb) * 2 * sizeof(int), st);
         tj_stats_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(B, n, D, fro, bound_bits, bad);
         tj_stats_finish_kernel<<<(nb + 127) / 128, 128, 0, st>>>(nb, fro, pad, bound_bits, bad, active, status);
-        tj_init_kernel<<<dim3(128, nb), 256, 0, st>>>(B, n, D, pad, Ah, Al, Vh, Vl);
+        tj_init_kernel<<<dim3(D / 32, D / 32, nb), dim3(32, 8), 0, st>>>(B, n, D, pad, Ah, Al, Vh, Vl);
         check(st, 0);  // already diagonal to the threshold (warm refresh): no sweep at all
     };
     auto sweep = [&](cudaStream_t st) {
