@@ -48,6 +48,7 @@ constexpr int JP = 128;  // apply tile: 128/PW pairs of two JW-wide blocks
 // pair per tile) from there on: small pairs make the shared-memory solves
 // cheap, wide pairs halve the rounds (and the tensor-core work) per sweep.
 constexpr int kWidePairN = 1536;
+constexpr int kFewBig = 8;  // pair solves with at most this many large elements rotate them one by one
 constexpr int kInner = 1;  // inner sweeps of the pair solve (more outer sweeps are cheaper than inner ones)
 
 __device__ __forceinline__ int tourney(int pos, int r, int P) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (P - 1); }
@@ -174,9 +175,13 @@ __global__ void __launch_bounds__(PW * 4) tj_pair_kernel(const float* __restrict
         return fabsf(S[i * (PW + 1) + j]) > t * fmaxf(sqrtf(fabsf(S[i * (PW + 1) + i] * S[j * (PW + 1) + j])), floor_s);
     };
     bool any = false;
+    int nbig = 0;
     for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) {
         const int i = e / PW, j = e % PW;
-        if (j > i) any |= big(i, j, tol);
+        if (j > i && big(i, j, tol)) {
+            any = true;
+            ++nbig;
+        }
     }
     const int half = k % G;
     const int64_t tile = (b * ntiles + k / G) * int64_t(JP) * JP + int64_t(half * PW) * JP + half * PW;
@@ -194,6 +199,96 @@ __global__ void __launch_bounds__(PW * 4) tj_pair_kernel(const float* __restrict
     }
     if (threadIdx.x == 0) *flag = 1;
     const float itol = 0.1f * tol;
+    // Few large elements (a warm refresh): classical Jacobi on the largest one
+    // at a time (a block-wide argmax, one rotation) instead of a full cyclic
+    // sweep of PW-1 synchronised rounds.
+    __shared__ int red_n[32];
+    __shared__ float red_v[32];
+    __shared__ int red_e[32];
+    {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        int cnt = nbig;
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffff, cnt, o);
+        if (lane == 0) red_n[wid] = cnt;
+        __syncthreads();
+        int total = 0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) total += red_n[w];
+        __syncthreads();
+        if (total <= kFewBig) {
+            for (int it = 0; it < 4 * kFewBig; ++it) {
+                float best = 0.f;
+                int be = -1;
+                for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) {
+                    const int i = e / PW, j = e % PW;
+                    if (j <= i) continue;
+                    const float thr = itol * fmaxf(sqrtf(fabsf(S[i * (PW + 1) + i] * S[j * (PW + 1) + j])), floor_s);
+                    const float ratio = fabsf(S[i * (PW + 1) + j]) / thr;
+                    if (ratio > 1.f && ratio > best) {
+                        best = ratio;
+                        be = e;
+                    }
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ob = __shfl_xor_sync(0xffffffff, best, o);
+                    const int oe = __shfl_xor_sync(0xffffffff, be, o);
+                    if (ob > best) {
+                        best = ob;
+                        be = oe;
+                    }
+                }
+                if (lane == 0) {
+                    red_v[wid] = best;
+                    red_e[wid] = be;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    float bb = 0.f;
+                    int ee = -1;
+                    for (int w = 0; w < int(blockDim.x >> 5); ++w)
+                        if (red_v[w] > bb) {
+                            bb = red_v[w];
+                            ee = red_e[w];
+                        }
+                    red_e[0] = ee;
+                    if (ee >= 0) {
+                        const int a = ee / PW, c = ee % PW;
+                        const double apq = S[a * (PW + 1) + c];
+                        const double app = S[a * (PW + 1) + a], aqq = S[c * (PW + 1) + c];
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau)) : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+                        const double c1 = 1.0 / sqrt(1.0 + t * t);
+                        cs[0] = float(c1);
+                        sn[0] = float(t * c1);
+                    }
+                }
+                __syncthreads();
+                const int ee = red_e[0];
+                if (ee < 0) break;
+                const int a = ee / PW, c = ee % PW;
+                const float cc = cs[0], ss = sn[0];
+                for (int j = threadIdx.x; j < PW; j += blockDim.x) {  // rows a, c of S
+                    const float x = S[a * (PW + 1) + j], y = S[c * (PW + 1) + j];
+                    S[a * (PW + 1) + j] = cc * x - ss * y;
+                    S[c * (PW + 1) + j] = ss * x + cc * y;
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < PW; i += blockDim.x) {  // columns a, c of S and Z
+                    float x = S[i * (PW + 1) + a], y = S[i * (PW + 1) + c];
+                    float na = cc * x - ss * y, nc = ss * x + cc * y;
+                    if (i == a) nc = 0.f;
+                    if (i == c) na = 0.f;
+                    S[i * (PW + 1) + a] = na;
+                    S[i * (PW + 1) + c] = nc;
+                    x = Z[i * (PW + 1) + a];
+                    y = Z[i * (PW + 1) + c];
+                    Z[i * (PW + 1) + a] = cc * x - ss * y;
+                    Z[i * (PW + 1) + c] = ss * x + cc * y;
+                }
+                __syncthreads();
+            }
+            inner_sweeps = 0;  // done: skip the cyclic sweep below
+        }
+    }
     for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
         bool rot_any = false;
         for (int r = 0; r < PW - 1; ++r) {
