@@ -61,6 +61,16 @@ __device__ __forceinline__ void pair_of(int k, int r, int m, int& p, int& q) {
         q = t;
     }
 }
+// Absolute floor of the rotation threshold, as a multiple of tol: the RMS
+// eigenvalue ||A||_F / sqrt(n), raised to the fp32 rounding level of a factor
+// accumulated over n-term sums (8 * 2^-24 * sqrt(n) of the RMS) so that pure
+// rounding noise is never chased.
+__device__ __forceinline__ float noise_floor(double fro, int n, float tol) {
+    const double rms = fro / sqrt(double(n));
+    const double lvl = 8.0 * 5.9604644775390625e-08 * sqrt(double(n));
+    return float(rms * fmax(1.0, lvl / double(tol)));
+}
+
 // pair-local index -> natural index
 template <int JW>
 __device__ __forceinline__ int nat(int i, int p, int q) { return i < JW ? p * JW + i : q * JW + (i - JW); }
@@ -170,7 +180,7 @@ __global__ void __launch_bounds__(PW * 4) tj_pair_kernel(const float* __restrict
         Z[i * (PW + 1) + j] = (i == j) ? 1.f : 0.f;
     }
     __syncthreads();
-    const float floor_s = float(fro[b] / sqrt(double(n)));
+    const float floor_s = noise_floor(fro[b], n, tol);
     auto big = [&](int i, int j, float t) {
         return fabsf(S[i * (PW + 1) + j]) > t * fmaxf(sqrtf(fabsf(S[i * (PW + 1) + i] * S[j * (PW + 1) + j])), floor_s);
     };
@@ -684,7 +694,7 @@ __global__ void tj_check_kernel(const float* __restrict__ Ah, const float* __res
     for (int i = threadIdx.x; i < D; i += blockDim.x)
         dgs[i] = fabsf(Ah[b * DD + int64_t(i) * D + i] + Al[b * DD + int64_t(i) * D + i]);
     __syncthreads();
-    const float floor_s = float(fro[b] / sqrt(double(n)));
+    const float floor_s = noise_floor(fro[b], n, tol);
     bool any = false;
     for (int r = blockIdx.x * 32 + (threadIdx.x >> 5); r < min(D, blockIdx.x * 32 + 32); r += blockDim.x >> 5) {
         const float dr = dgs[r];
