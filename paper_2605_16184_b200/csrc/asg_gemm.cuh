@@ -126,13 +126,18 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int r
         if (row < col0) return;  // whole chunk strictly above the diagonal
         float* crow = cb + int64_t(row) * p.ldc + col0;
         float vals[32];
+        if (p.beta != 0.f) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-            const float4 o = *reinterpret_cast<const float4*>(crow + j);
-            vals[j + 0] = p.beta * o.x + p.alpha * __uint_as_float(r[j + 0]);
-            vals[j + 1] = p.beta * o.y + p.alpha * __uint_as_float(r[j + 1]);
-            vals[j + 2] = p.beta * o.z + p.alpha * __uint_as_float(r[j + 2]);
-            vals[j + 3] = p.beta * o.w + p.alpha * __uint_as_float(r[j + 3]);
+            for (int j = 0; j < 32; j += 4) {
+                const float4 o = *reinterpret_cast<const float4*>(crow + j);
+                vals[j + 0] = p.beta * o.x + p.alpha * __uint_as_float(r[j + 0]);
+                vals[j + 1] = p.beta * o.y + p.alpha * __uint_as_float(r[j + 1]);
+                vals[j + 2] = p.beta * o.z + p.alpha * __uint_as_float(r[j + 2]);
+                vals[j + 3] = p.beta * o.w + p.alpha * __uint_as_float(r[j + 3]);
+            }
+        } else {  // C need not be initialised (scratch)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) vals[j] = p.alpha * __uint_as_float(r[j]);
         }
         if (row >= col0 + 31) {
 #pragma unroll

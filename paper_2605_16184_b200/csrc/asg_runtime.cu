@@ -784,11 +784,27 @@ void refresh_side(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaSt
 }
 
 
+// Newton-Schulz re-orthonormalization of Q J is needed after a cold solve (J
+// carries the tensor-core Jacobi's accumulated rounding) and periodically
+// after warm ones (each product adds ~1e-7 of drift): every kNsPeriod-th
+// refresh of a block.
+constexpr uint64_t kNsPeriod = 8;
+bool needs_ns(const asg_blockset* bs, const Group& g, int s0, int cnt, bool at_install) {
+    for (int k = 0; k < cnt; ++k) {
+        const Unit& u = bs->units[size_t(g.units[size_t(s0 + k)])];
+        // refresh: version before this job's install; install: version already bumped
+        const uint64_t v = at_install ? (u.version ? u.version - 1 : 0) : u.version;
+        if (!u.warm_start || v % kNsPeriod == 0) return true;
+    }
+    return false;
+}
+
 // One Newton-Schulz polar step on a split basis slab (cnt blocks of D x D):
 // out = V (3 I - V^T V) / 2. VT: scratch for V^T (split), Sx: fp32 scratch
 // reused in place for X's hi part, Xl: X's lo part (null in TF32 mode).
 void orthonormalize(asg_blockset* bs, const float* Vh, const float* Vl, float* outh, float* outl, float* VTh,
-                    float* VTl, float* Sx, float* Xl, int cnt, int d, int D, cudaStream_t s) {
+                    float* VTl, float* Sx, float* Xl, int cnt, int d, int D, const int2* sym_tiles, int nsym,
+                    cudaStream_t s) {
     const size_t DD = size_t(D) * D;
     const double flops = 2.0 * cnt * double(d) * d * d;
     launch_transpose_split(Vh, Vl, cnt, D, D, VTh, VTl, false, s);
@@ -798,7 +814,8 @@ void orthonormalize(asg_blockset* bs, const float* Vh, const float* Vl, float* o
     p1.C = Sx;
     p1.ldc = D;
     p1.c_bstride = int64_t(DD);
-    run_gemm(bs, op(VTh, VTl, D, D), op(VTh, VTl, D, D), cnt, EPI_STORE, p1, nullptr, 0, s, flops);
+    // V^T V is symmetric: lower-triangle tiles + mirror
+    run_gemm(bs, op(VTh, VTl, D, D), op(VTh, VTl, D, D), cnt, EPI_SYM_EMA, p1, sym_tiles, nsym, s, flops / 2);
     launch_ns_x(Sx, cnt, d, D, Sx, Xl, s);
     GemmParams p2{};
     p2.alpha = 1.f;
@@ -886,7 +903,9 @@ void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cu
     p2.C = t[4];
     p2.ldc = D;
     p2.c_bstride = int64_t(DD);
-    run_gemm(bs, op(QTh, QTl, D, D), op(t[2], t3, D, D), cnt, EPI_STORE, p2, nullptr, 0, s, 2.0 * dd3);
+    // B = Q^T A Q is symmetric: lower-triangle tiles + mirror (exactly symmetric output)
+    run_gemm(bs, op(QTh, QTl, D, D), op(t[2], t3, D, D), cnt, EPI_SYM_EMA, p2, left ? g.tilesM : g.tilesN,
+             left ? g.ntM : g.ntN, s, dd3);
     pt.mark("transform");
     launch_snapshot_sym(t[4], cnt, D, d, bs->ws_snap, s);  // fp64 copy: trace for the damping (and small solves)
     if (d > kSmallEighN && !bs->fp64_jacobi) {
@@ -920,9 +939,15 @@ void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cu
     p3.d_bstride = int64_t(DD);
     run_gemm(bs, op(Qh, Ql, D, D), op(t[2], t3, D, D), cnt, EPI_SPLIT, p3, nullptr, 0, s, 2.0 * dd3);
     // re-orthonormalize (the products drift at the fp32 level), straight into the basis
-    orthonormalize(bs, t[4], t5, Qh, sp ? Ql : nullptr, t[2], t3, t[6], t7, cnt, d, D, s);
-    CK(cudaMemcpyAsync(t[4], Qh, cntDD * 4, cudaMemcpyDeviceToDevice, s));
-    if (sp) CK(cudaMemcpyAsync(t[5], Ql, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+    if (needs_ns(bs, g, s0, cnt, false)) {
+        orthonormalize(bs, t[4], t5, Qh, sp ? Ql : nullptr, t[2], t3, t[6], t7, cnt, d, D,
+                       left ? g.tilesM : g.tilesN, left ? g.ntM : g.ntN, s);
+        CK(cudaMemcpyAsync(t[4], Qh, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        if (sp) CK(cudaMemcpyAsync(t[5], Ql, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+    } else {
+        CK(cudaMemcpyAsync(Qh, t[4], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        if (sp) CK(cudaMemcpyAsync(Ql, t[5], cntDD * 4, cudaMemcpyDeviceToDevice, s));
+    }
     launch_transpose_split(t[4], t5, cnt, D, D, QTh, sp ? QTl : nullptr, false, s);
     // roots V diag((lambda + eps)^p) V^T  (inv_root densela.hpp:267-282, damping precond.cpp:121-125)
     launch_relative_damping(bs->ws_snap, cnt, d, bs->opt.damping, bs->ws_eps, s);
@@ -1031,6 +1056,7 @@ void install_wait(asg_blockset* bs, Unit& u) {
 //   Q <- Q J ;  M <- J_L^T M J_R ;  V <- (J_L o J_L)^T V (J_R o J_R) ;  values.
 void install_soap_f32(asg_blockset* bs, Group& g, int s0, int cnt) {
     cudaStream_t s = bs->main;
+    const bool ns = needs_ns(bs, g, s0, cnt, true);
     const bool sp = split_mode(bs);
     float** w = bs->iw32;
     const size_t MN = slabMN(g);
@@ -1049,8 +1075,13 @@ void install_soap_f32(asg_blockset* bs, Group& g, int s0, int cnt) {
         run_gemm(bs, op(Qh, Ql, D, D), op(at(left ? g.sJLTh : g.sJRTh, DD, s0), at(left ? g.sJLTl : g.sJRTl, DD, s0), D, D),
                  cnt, EPI_SPLIT, p, nullptr, 0, s, 2.0 * cnt * double(d) * d * d);
         // Q <- orthonormalized (Q_old J), then Q^T
-        orthonormalize(bs, w[0], sp ? w[1] : nullptr, Qh, sp ? Ql : nullptr, w[2], sp ? w[3] : nullptr, w[4],
-                       sp ? w[5] : nullptr, cnt, d, D, s);
+        if (ns) {
+            orthonormalize(bs, w[0], sp ? w[1] : nullptr, Qh, sp ? Ql : nullptr, w[2], sp ? w[3] : nullptr, w[4],
+                           sp ? w[5] : nullptr, cnt, d, D, left ? g.tilesM : g.tilesN, left ? g.ntM : g.ntN, s);
+        } else {
+            CK(cudaMemcpyAsync(Qh, w[0], size_t(cnt) * DD * 4, cudaMemcpyDeviceToDevice, s));
+            if (sp) CK(cudaMemcpyAsync(Ql, w[1], size_t(cnt) * DD * 4, cudaMemcpyDeviceToDevice, s));
+        }
         launch_transpose_split(Qh, sp ? Ql : nullptr, cnt, D, D, at(left ? g.QLTh : g.QRTh, DD, s0),
                                at(left ? g.QLTl : g.QRTl, DD, s0), false, s);
         CK(cudaMemcpyAsync(at(left ? g.valsL : g.valsR, size_t(d), s0), at(left ? g.svalsL : g.svalsR, size_t(d), s0),
