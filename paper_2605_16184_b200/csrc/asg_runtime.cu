@@ -212,6 +212,11 @@ struct asg_blockset {
     std::vector<void*> host_allocs;
     cudaStream_t main = nullptr, side = nullptr;
     bool own_main = false;
+    // shape groups run their GEMM chains concurrently on these (small groups
+    // leave SMs idle; their persistent kernels overlap the big ones)
+    static constexpr int kGroupStreams = 4;
+    cudaStream_t gstream[kGroupStreams] = {};
+    cudaEvent_t gfork = nullptr, gjoin[kGroupStreams] = {};
     cudaEvent_t ev_snap = nullptr;
     // scheduler
     double now_us = 0.0;
@@ -609,6 +614,23 @@ void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const 
 template <class T>
 T* at(T* base, size_t stride, int slot) {
     return base ? base + stride * size_t(slot) : nullptr;
+}
+
+// Concurrent group chains: fork from the main stream, run group i on
+// stream_for(i), join back. With one group everything stays on main.
+int fork_groups(asg_blockset* bs) {
+    const int k = std::min<int>(asg_blockset::kGroupStreams, int(bs->groups.size()));
+    if (k <= 1) return 0;
+    CK(cudaEventRecord(bs->gfork, bs->main));
+    for (int i = 0; i < k; ++i) CK(cudaStreamWaitEvent(bs->gstream[i], bs->gfork, 0));
+    return k;
+}
+cudaStream_t stream_for(asg_blockset* bs, int k, int i) { return k ? bs->gstream[i % k] : bs->main; }
+void join_groups(asg_blockset* bs, int k) {
+    for (int i = 0; i < k; ++i) {
+        CK(cudaEventRecord(bs->gjoin[i], bs->gstream[i]));
+        CK(cudaStreamWaitEvent(bs->main, bs->gjoin[i], 0));
+    }
 }
 
 // Statistics for slots [s0, s0+cnt) of a group (G slabs already staged).
@@ -1538,6 +1560,11 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         CK(cudaStreamCreateWithPriority(&bs->main, cudaStreamNonBlocking, hi));
         CK(cudaStreamCreateWithPriority(&bs->side, cudaStreamNonBlocking, lo));
         bs->own_main = true;
+        for (int k = 0; k < asg_blockset::kGroupStreams; ++k) {
+            CK(cudaStreamCreateWithPriority(&bs->gstream[k], cudaStreamNonBlocking, hi));
+            CK(cudaEventCreateWithFlags(&bs->gjoin[k], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&bs->gfork, cudaEventDisableTiming));
         bs->fp64_jacobi = getenv("ASG_F32_FP64_JACOBI") != nullptr;
         CK(cudaEventCreateWithFlags(&bs->ev_snap, cudaEventDisableTiming));
         build_units(bs);
@@ -1621,6 +1648,14 @@ int asg_blockset_destroy(asg_blockset* bs) {
     cudaSetDevice(bs->device);
     if (bs->main) cudaStreamSynchronize(bs->main);
     if (bs->side) cudaStreamSynchronize(bs->side);
+    for (int k = 0; k < asg_blockset::kGroupStreams; ++k) {
+        if (bs->gstream[k]) {
+            cudaStreamSynchronize(bs->gstream[k]);
+            cudaStreamDestroy(bs->gstream[k]);
+        }
+        if (bs->gjoin[k]) cudaEventDestroy(bs->gjoin[k]);
+    }
+    if (bs->gfork) cudaEventDestroy(bs->gfork);
     for (auto& u : bs->units)
         if (u.done) cudaEventDestroy(u.done);
     if (bs->ev_snap) cudaEventDestroy(bs->ev_snap);
@@ -1720,10 +1755,14 @@ int asg_accumulate(asg_blockset* bs, double clip_scale, void* stream) {
             CK(cudaStreamWaitEvent(bs->main, e, 0));
             CK(cudaEventDestroy(e));
         }
-        for (Group& g : bs->groups) {
-            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, bs->main);
-            group_stats(bs, g, 0, g.nb, bs->main);
+        const int k = fork_groups(bs);
+        for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
+            Group& g = bs->groups[gi];
+            cudaStream_t gs = stream_for(bs, k, int(gi));
+            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs);
+            group_stats(bs, g, 0, g.nb, gs);
         }
+        join_groups(bs, k);
         CK(cudaGetLastError());
     });
 }
@@ -1759,7 +1798,9 @@ int asg_staleness_barrier(asg_blockset* bs, int64_t step, double* waited_us) {
 namespace {
 void precondition_apply_impl(asg_blockset* bs, double clip_scale, double lr_scale) {
     const float lr_eff = float(bs->opt.lr * lr_scale);
-    for (Group& g : bs->groups) {
+    const int k = fork_groups(bs);
+    for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
+        Group& g = bs->groups[gi];
         if (is_soap(bs)) {
             int64_t ms = -1;
             for (int ui : g.units) {
@@ -1769,8 +1810,9 @@ void precondition_apply_impl(asg_blockset* bs, double clip_scale, double lr_scal
                 ms = u.moment_steps;
             }
         }
-        group_update(bs, g, 0, g.nb, EPI_APPLY, lr_eff, g.d_apply, nullptr, bs->main);
+        group_update(bs, g, 0, g.nb, EPI_APPLY, lr_eff, g.d_apply, nullptr, stream_for(bs, k, int(gi)));
     }
+    cudaStream_t as = stream_for(bs, k, int(bs->groups.size()));  // AdamW on the least loaded group stream
     for (Unit& u : bs->units) {
         if (!u.adamw || u.owner != bs->rank) continue;
         const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
@@ -1779,8 +1821,9 @@ void precondition_apply_impl(asg_blockset* bs, double clip_scale, double lr_scal
         launch_adamw_apply(d.theta, d.ld_theta, d.grad, d.ld_grad, d.rows, d.cols, u.am, u.av, nullptr, float(clip_scale),
                            float(bs->opt.beta1), float(bs->opt.beta2), float(1.0 / (1.0 - std::pow(bs->opt.beta1, t))),
                            float(1.0 / (1.0 - std::pow(bs->opt.beta2, t))), float(bs->opt.eps), lr_eff,
-                           float(bs->opt.weight_decay), bs->d_flag, bs->main);
+                           float(bs->opt.weight_decay), bs->d_flag, as);
     }
+    join_groups(bs, k);
     CK(cudaGetLastError());
 }
 }  // namespace
@@ -1818,10 +1861,16 @@ int asg_step(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale,
             CK(cudaStreamWaitEvent(bs->main, e, 0));
             CK(cudaEventDestroy(e));
         }
-        // accumulate (all owned blocks, batched per shape group)
-        for (Group& g : bs->groups) {
-            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, bs->main);
-            group_stats(bs, g, 0, g.nb, bs->main);
+        // accumulate (all owned blocks, batched per shape group, groups concurrent)
+        {
+            const int k = fork_groups(bs);
+            for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
+                Group& g = bs->groups[gi];
+                cudaStream_t gs = stream_for(bs, k, int(gi));
+                launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs);
+                group_stats(bs, g, 0, g.nb, gs);
+            }
+            join_groups(bs, k);
         }
         // per-block dispatch -> barrier in the reference's order (harness.cpp:452-454);
         // a barrier install launches any outstanding refresh first.
