@@ -15,6 +15,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/asteria_b200.h"
@@ -101,7 +102,11 @@ cudaError_t dispatch_epi(int epi, const CUtensorMap& ah, const CUtensorMap& al, 
 
 }  // namespace
 
-int gemm_bn_for(int n) { return (n % 256 == 0) ? 256 : 128; }
+int gemm_bn_for(int n) {
+    static const int force = getenv("ASG_GEMM_BN") ? atoi(getenv("ASG_GEMM_BN")) : 0;  // tuning experiments
+    if (force == 128) return 128;
+    return (n % 256 == 0) ? 256 : 128;
+}
 
 int gemm_sym_tile_list(int n, int bn, int2* out) {
     int count = 0;
@@ -852,6 +857,20 @@ __global__ void ns_x_kernel(const float* S, int d, int D, float* Xh, float* __re
 
 void launch_ns_x(const float* S, int nb, int d, int D, float* Xh, float* Xl, cudaStream_t s) {
     ns_x_kernel<<<dim3(256, nb), 256, 0, s>>>(S, d, D, Xh, Xl);
+    count_launch();
+}
+
+// out[k] = first failure of (in[k], in[cnt + k]) (both sides of block k).
+__global__ void merge_status_kernel(const int* in, int cnt, int* out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    const int a = in[k], b = in[cnt + k];
+    if (a != ASG_OK) atomicCAS(&out[k], ASG_OK, a);
+    else if (b != ASG_OK) atomicCAS(&out[k], ASG_OK, b);
+}
+
+void launch_merge_status(const int* in, int cnt, int* out, cudaStream_t s) {
+    merge_status_kernel<<<(cnt + 127) / 128, 128, 0, s>>>(in, cnt, out);
     count_launch();
 }
 

@@ -122,6 +122,9 @@ void launch_relative_damping_f32(const float* A, int nb, int M, int n, double da
 // X = (3 I - S) / 2 on the leading d x d of S = V^T V (Newton-Schulz polar step).
 void launch_ns_x(const float* S, int nb, int d, int D, float* Xh, float* Xl, cudaStream_t s);
 
+// Per-block status from a both-sides eigensolve: out[k] <- first failure of in[k], in[cnt+k].
+void launch_merge_status(const int* in, int cnt, int* out, cudaStream_t s);
+
 // Multi-GPU: pack owned block slices into a contiguous buffer and back.
 void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out,
                         cudaStream_t s);

@@ -234,6 +234,7 @@ struct asg_blockset {
     float* iw32[6] = {};
     // F32 refresh: tensor-core Jacobi workspace (side stream)
     float* tc_ws = nullptr;
+    int* pair_status = nullptr;  // both-sides eigensolves: per-matrix status before the merge
     bool fp64_jacobi = false;  // ASG_F32_FP64_JACOBI=1: F32 refresh with the fp64 block Jacobi (diagnostics)
     // SOAP install workspace (one block)
     double *iw_rotL = nullptr, *iw_rotR = nullptr, *iw_sq = nullptr, *iw_a = nullptr, *iw_b = nullptr;
@@ -559,14 +560,16 @@ void alloc_workspace(asg_blockset* bs) {
     bs->ws_work = dalloc<double>(bs, ew);
     bs->ws_W = dalloc<double>(bs, nn);
     bs->ws_out = dalloc<double>(bs, nn);
-    bs->ws_vals = dalloc<double>(bs, size_t(nmax) * bs->ws_chunk);
-    bs->ws_eps = dalloc<double>(bs, size_t(bs->ws_chunk));
+    bs->ws_vals = dalloc<double>(bs, size_t(nmax) * bs->ws_chunk * 2);
+    bs->ws_eps = dalloc<double>(bs, size_t(bs->ws_chunk) * 2);
     if (f32_refresh(bs)) {
         int Dmax = 0;
         for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
         bs->tw_slab = size_t(Dmax) * Dmax;
-        for (float*& t : bs->tw) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
-        bs->tc_ws = dalloc<float>(bs, tc_eigh_workspace_floats(bs->ws_chunk, Dmax));
+        // two factor sides per chunk (square blocks share one eigensolve)
+        for (float*& t : bs->tw) t = dalloc<float>(bs, bs->tw_slab * size_t(2 * bs->ws_chunk));
+        bs->tc_ws = dalloc<float>(bs, tc_eigh_workspace_floats(2 * bs->ws_chunk, Dmax));
+        bs->pair_status = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
         if (is_soap(bs))
             for (float*& t : bs->iw32) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
     }
@@ -882,120 +885,152 @@ struct PhaseTimer {
     }
 };
 
-void refresh_side_f32(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaStream_t s) {
+// F32 refresh of one chunk of a group: both factor sides in one batched
+// eigensolve when they have the same dimension (square blocks), else one side.
+void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, bool first_left, cudaStream_t s) {
     PhaseTimer pt(s);
     pt.mark("start");
-    const int d = left ? g.m : g.n, D = left ? g.M : g.N;
+    const int d = first_left ? g.m : g.n, D = first_left ? g.M : g.N;
     const size_t DD = size_t(D) * D, cntDD = size_t(cnt) * DD;
     const double dd3 = double(cnt) * d * double(d) * d;
+    const int nb = nsides * cnt;  // matrices in the eigensolve
     float** t = bs->tw;
-    const float* snap = at(left ? g.snapL : g.snapR, DD, s0);
-    float *Qh, *Ql, *QTh, *QTl;
-    if (is_soap(bs)) {
-        Qh = at(left ? g.QLh : g.QRh, DD, s0);
-        Ql = at(left ? g.QLl : g.QRl, DD, s0);
-        QTh = at(left ? g.QLTh : g.QRTh, DD, s0);
-        QTl = at(left ? g.QLTl : g.QRTl, DD, s0);
-    } else {
-        Qh = at(left ? g.BLh : g.BRh, DD, s0);
-        Ql = at(left ? g.BLl : g.BRl, DD, s0);
-        QTh = at(left ? g.BLTh : g.BRTh, DD, s0);
-        QTl = at(left ? g.BLTl : g.BRTl, DD, s0);
-    }
     const bool sp = split_mode(bs);
+    auto off = [&](float* base, int j) { return base ? base + size_t(j) * cntDD : nullptr; };
+    struct Side {
+        bool left;
+        float *Qh, *Ql, *QTh, *QTl;
+        const int2* tiles;
+        int ntiles;
+    };
+    std::vector<Side> sides;
+    for (int j = 0; j < nsides; ++j) {
+        const bool left = nsides == 2 ? j == 0 : first_left;
+        Side sd{};
+        sd.left = left;
+        if (is_soap(bs)) {
+            sd.Qh = at(left ? g.QLh : g.QRh, DD, s0);
+            sd.Ql = at(left ? g.QLl : g.QRl, DD, s0);
+            sd.QTh = at(left ? g.QLTh : g.QRTh, DD, s0);
+            sd.QTl = at(left ? g.QLTl : g.QRTl, DD, s0);
+        } else {
+            sd.Qh = at(left ? g.BLh : g.BRh, DD, s0);
+            sd.Ql = at(left ? g.BLl : g.BRl, DD, s0);
+            sd.QTh = at(left ? g.BLTh : g.BRTh, DD, s0);
+            sd.QTl = at(left ? g.BLTl : g.BRTl, DD, s0);
+        }
+        sd.tiles = left ? g.tilesM : g.tilesN;
+        sd.ntiles = left ? g.ntM : g.ntN;
+        sides.push_back(sd);
+    }
+    // per side j: A_j split -> t0/t1[j], W_j^T = (A_j Q_j)^T -> t2/t3[j], B_j = Q_j^T W_j -> t4[j]
+    for (int j = 0; j < nsides; ++j) {
+        const Side& sd = sides[size_t(j)];
+        const float* snap = at(sd.left ? g.snapL : g.snapR, DD, s0);
+        if (sp) launch_split_slab(snap, off(t[0], j), off(t[1], j), int64_t(cntDD), s);
+        else CK(cudaMemcpyAsync(off(t[0], j), snap, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        GemmParams p1{};
+        p1.alpha = 1.f;
+        p1.Dhi = off(t[2], j);
+        p1.Dlo = sp ? off(t[3], j) : nullptr;
+        p1.ldd = D;
+        p1.d_bstride = int64_t(DD);
+        run_gemm(bs, op(off(t[0], j), sp ? off(t[1], j) : nullptr, D, D), op(sd.QTh, sd.QTl, D, D), cnt, EPI_SPLIT_T,
+                 p1, nullptr, 0, s, 2.0 * dd3);
+        GemmParams p2{};
+        p2.alpha = 1.f;
+        p2.beta = 0.f;
+        p2.C = off(t[4], j);
+        p2.ldc = D;
+        p2.c_bstride = int64_t(DD);
+        // B = Q^T A Q is symmetric: lower-triangle tiles + mirror (exactly symmetric output)
+        run_gemm(bs, op(sd.QTh, sd.QTl, D, D), op(off(t[2], j), sp ? off(t[3], j) : nullptr, D, D), cnt, EPI_SYM_EMA,
+                 p2, sd.tiles, sd.ntiles, s, dd3);
+    }
+    pt.mark("transform");
+    // relative damping eps = damping * tr(B) / d (tr B = tr A: orthogonal similarity)
+    launch_relative_damping_f32(t[4], nb, D, d, bs->opt.damping, bs->ws_eps, s);
+    int* st = nsides == 2 ? bs->pair_status : g.d_status + s0;
+    if (nsides == 2) CK(cudaMemsetAsync(st, 0, size_t(nb) * sizeof(int), s));
     float* t1 = sp ? t[1] : nullptr;
     float* t3 = sp ? t[3] : nullptr;
-    float* t5 = sp ? t[5] : nullptr;
-    float* t7 = sp ? t[7] : nullptr;
-    // A as a split operand
-    if (sp) launch_split_slab(snap, t[0], t[1], int64_t(cntDD), s);
-    else CK(cudaMemcpyAsync(t[0], snap, cntDD * 4, cudaMemcpyDeviceToDevice, s));
-    // W^T = (A Q)^T
-    GemmParams p1{};
-    p1.alpha = 1.f;
-    p1.Dhi = t[2];
-    p1.Dlo = t3;
-    p1.ldd = D;
-    p1.d_bstride = int64_t(DD);
-    run_gemm(bs, op(t[0], t1, D, D), op(QTh, QTl, D, D), cnt, EPI_SPLIT_T, p1, nullptr, 0, s, 2.0 * dd3);
-    // B = Q^T W
-    GemmParams p2{};
-    p2.alpha = 1.f;
-    p2.beta = 0.f;
-    p2.C = t[4];
-    p2.ldc = D;
-    p2.c_bstride = int64_t(DD);
-    // B = Q^T A Q is symmetric: lower-triangle tiles + mirror (exactly symmetric output)
-    run_gemm(bs, op(QTh, QTl, D, D), op(t[2], t3, D, D), cnt, EPI_SYM_EMA, p2, left ? g.tilesM : g.tilesN,
-             left ? g.ntM : g.ntN, s, dd3);
-    pt.mark("transform");
-    launch_snapshot_sym(t[4], cnt, D, d, bs->ws_snap, s);  // fp64 copy: trace for the damping (and small solves)
     if (d > kSmallEighN && !bs->fp64_jacobi) {
-        // tensor-core block Jacobi: J -> (t0, t1), J^T -> (t2, t3)
+        // tensor-core block Jacobi over all sides: J -> (t0, t1), J^T -> (t2, t3)
         // (Q J is re-orthonormalized below / at the SOAP install, so J itself is not)
-        launch_tc_eigh(t[4], D, bs->ws_vals, t[0], t1, t[2], t3, bs->tc_ws, cnt, d, g.d_status + s0, bs->num_sms, s,
+        launch_tc_eigh(t[4], D, bs->ws_vals, t[0], t1, t[2], t3, bs->tc_ws, nb, d, st, bs->num_sms, s,
                        f32_refresh_tol(), false);
     } else {
+        launch_snapshot_sym(t[4], nb, D, d, bs->ws_snap, s);
         EighOpts eo;
         eo.relative = 1;
         eo.tol = f32_refresh_tol();
-        launch_eigh(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, cnt, d, g.d_status + s0, s, nullptr, eo);
-        launch_f64_to_split(bs->ws_vecs, cnt, d, D, false, t[0], t1, t[2], t3, s);
+        launch_eigh(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, nb, d, st, s, nullptr, eo);
+        launch_f64_to_split(bs->ws_vecs, nb, d, D, false, t[0], t1, t[2], t3, s);
     }
+    if (nsides == 2) launch_merge_status(st, cnt, g.d_status + s0, s);
     pt.mark("eigh");
-    if (is_soap(bs)) {
-        pt.report(d, cnt);
-        CK(cudaMemcpyAsync(at(left ? g.sJLTh : g.sJRTh, DD, s0), t[2], cntDD * 4, cudaMemcpyDeviceToDevice, s));
-        if (sp)
-            CK(cudaMemcpyAsync(at(left ? g.sJLTl : g.sJRTl, DD, s0), t[3], cntDD * 4, cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(at(left ? g.svalsL : g.svalsR, size_t(d), s0), bs->ws_vals, size_t(cnt) * d * 8,
-                           cudaMemcpyDeviceToDevice, s));
-        return;
-    }
-    // V = Q J -> (t4, t5); it becomes the block's basis (row-major and transposed)
-    GemmParams p3{};
-    p3.alpha = 1.f;
-    p3.Dhi = t[4];
-    p3.Dlo = t5;
-    p3.ldd = D;
-    p3.d_bstride = int64_t(DD);
-    run_gemm(bs, op(Qh, Ql, D, D), op(t[2], t3, D, D), cnt, EPI_SPLIT, p3, nullptr, 0, s, 2.0 * dd3);
-    // re-orthonormalize (the products drift at the fp32 level), straight into the basis
-    if (needs_ns(bs, g, s0, cnt, false)) {
-        orthonormalize(bs, t[4], t5, Qh, sp ? Ql : nullptr, t[2], t3, t[6], t7, cnt, d, D,
-                       left ? g.tilesM : g.tilesN, left ? g.ntM : g.ntN, s);
-        CK(cudaMemcpyAsync(t[4], Qh, cntDD * 4, cudaMemcpyDeviceToDevice, s));
-        if (sp) CK(cudaMemcpyAsync(t[5], Ql, cntDD * 4, cudaMemcpyDeviceToDevice, s));
-    } else {
-        CK(cudaMemcpyAsync(Qh, t[4], cntDD * 4, cudaMemcpyDeviceToDevice, s));
-        if (sp) CK(cudaMemcpyAsync(Ql, t[5], cntDD * 4, cudaMemcpyDeviceToDevice, s));
-    }
-    launch_transpose_split(t[4], t5, cnt, D, D, QTh, sp ? QTl : nullptr, false, s);
-    // roots V diag((lambda + eps)^p) V^T  (inv_root densela.hpp:267-282, damping precond.cpp:121-125)
-    launch_relative_damping(bs->ws_snap, cnt, d, bs->opt.damping, bs->ws_eps, s);
-    struct Out {
-        double power;
-        float *hi, *lo;
-    };
-    std::vector<Out> outs;
-    if (is_kl(bs)) {
-        outs.push_back({-0.5, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
-        outs.push_back({-1.0, at(left ? g.sKLh : g.sKRh, DD, s0), at(left ? g.sKLl : g.sKRl, DD, s0)});
-    } else {
-        outs.push_back({-0.25, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
-    }
-    for (const Out& o : outs) {
-        launch_scale_columns_split(t[4], t5, bs->ws_vals, bs->ws_eps, o.power, cnt, d, D, t[6], t7, g.d_status + s0, s);
-        GemmParams pr{};
-        pr.alpha = 1.f;
-        pr.Dhi = o.hi;
-        pr.Dlo = o.lo;
-        pr.ldd = D;
-        pr.d_bstride = int64_t(DD);
-        run_gemm(bs, op(t[6], t7, D, D), op(t[4], t5, D, D), cnt, EPI_SPLIT, pr, nullptr, 0, s, 2.0 * dd3);
+    for (int j = 0; j < nsides; ++j) {
+        const Side& sd = sides[size_t(j)];
+        const bool left = sd.left;
+        const double* vals = bs->ws_vals + size_t(j) * cnt * d;
+        if (is_soap(bs)) {
+            CK(cudaMemcpyAsync(at(left ? g.sJLTh : g.sJRTh, DD, s0), off(t[2], j), cntDD * 4, cudaMemcpyDeviceToDevice, s));
+            if (sp)
+                CK(cudaMemcpyAsync(at(left ? g.sJLTl : g.sJRTl, DD, s0), off(t[3], j), cntDD * 4,
+                                   cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(at(left ? g.svalsL : g.svalsR, size_t(d), s0), vals, size_t(cnt) * d * 8,
+                               cudaMemcpyDeviceToDevice, s));
+            continue;
+        }
+        // V = Q J -> (t4, t5)[j] (B is no longer needed); it becomes the block's basis
+        float* V = off(t[4], j);
+        float* Vl = sp ? off(t[5], j) : nullptr;
+        GemmParams p3{};
+        p3.alpha = 1.f;
+        p3.Dhi = V;
+        p3.Dlo = Vl;
+        p3.ldd = D;
+        p3.d_bstride = int64_t(DD);
+        run_gemm(bs, op(sd.Qh, sd.Ql, D, D), op(off(t[2], j), sp ? off(t[3], j) : nullptr, D, D), cnt, EPI_SPLIT, p3,
+                 nullptr, 0, s, 2.0 * dd3);
+        // re-orthonormalize (the products drift at the fp32 level), straight into the basis
+        if (needs_ns(bs, g, s0, cnt, false)) {
+            orthonormalize(bs, V, Vl, sd.Qh, sp ? sd.Ql : nullptr, off(t[2], j), sp ? off(t[3], j) : nullptr,
+                           off(t[6], j), sp ? off(t[7], j) : nullptr, cnt, d, D, sd.tiles, sd.ntiles, s);
+            CK(cudaMemcpyAsync(V, sd.Qh, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+            if (sp) CK(cudaMemcpyAsync(Vl, sd.Ql, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        } else {
+            CK(cudaMemcpyAsync(sd.Qh, V, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+            if (sp) CK(cudaMemcpyAsync(sd.Ql, Vl, cntDD * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        launch_transpose_split(V, Vl, cnt, D, D, sd.QTh, sp ? sd.QTl : nullptr, false, s);
+        // roots V diag((lambda + eps)^p) V^T  (inv_root densela.hpp:267-282, damping precond.cpp:121-125)
+        struct Out {
+            double power;
+            float *hi, *lo;
+        };
+        std::vector<Out> outs;
+        if (is_kl(bs)) {
+            outs.push_back({-0.5, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
+            outs.push_back({-1.0, at(left ? g.sKLh : g.sKRh, DD, s0), at(left ? g.sKLl : g.sKRl, DD, s0)});
+        } else {
+            outs.push_back({-0.25, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
+        }
+        for (const Out& o : outs) {
+            launch_scale_columns_split(V, Vl, vals, bs->ws_eps + size_t(j) * cnt, o.power, cnt, d, D, off(t[6], j),
+                                       sp ? off(t[7], j) : nullptr, g.d_status + s0, s);
+            GemmParams pr{};
+            pr.alpha = 1.f;
+            pr.Dhi = o.hi;
+            pr.Dlo = o.lo;
+            pr.ldd = D;
+            pr.d_bstride = int64_t(DD);
+            run_gemm(bs, op(off(t[6], j), sp ? off(t[7], j) : nullptr, D, D), op(V, Vl, D, D), cnt, EPI_SPLIT, pr,
+                     nullptr, 0, s, 2.0 * dd3);
+        }
     }
     pt.mark("basis+roots");
-    pt.report(d, cnt);
+    pt.report(d, nb);
 }
 
 // Launches the refresh for every unit marked dispatched-but-not-launched.
@@ -1035,8 +1070,12 @@ void launch_refreshes(asg_blockset* bs) {
             const int s0 = slots[i], cnt = int(j - i);
             CK(cudaMemsetAsync(g.d_status + s0, 0, size_t(cnt) * sizeof(int), bs->side));
             if (f32_refresh(bs)) {
-                refresh_side_f32(bs, g, s0, cnt, true, bs->side);
-                refresh_side_f32(bs, g, s0, cnt, false, bs->side);
+                if (g.m == g.n && g.m > kSmallEighN && !bs->fp64_jacobi) {
+                    refresh_sides_f32(bs, g, s0, cnt, 2, true, bs->side);
+                } else {
+                    refresh_sides_f32(bs, g, s0, cnt, 1, true, bs->side);
+                    refresh_sides_f32(bs, g, s0, cnt, 1, false, bs->side);
+                }
             } else {
                 refresh_side(bs, g, s0, cnt, true, bs->side);
                 refresh_side(bs, g, s0, cnt, false, bs->side);
