@@ -241,6 +241,59 @@ __device__ __forceinline__ void apply_chunk(const GemmParams& p, int b, int row0
     __syncwarp();
 }
 
+// Coalesced STORE / SPLIT / SYM_EMA: the warp's 32 rows x 32 columns go
+// through the shared-memory transpose, so every global access of a lane
+// group is one 128-byte row segment (the row-per-thread mapping of
+// epilogue_chunk touches 32 rows per instruction).
+template <int EPI>
+__device__ __forceinline__ void rows_chunk(const GemmParams& p, int b, int row0, int col0, const uint32_t (&r)[32],
+                                           float (*scratch)[33]) {
+    const uint32_t lane = threadIdx.x & 31;
+    if constexpr (EPI == EPI_SYM_EMA) {
+        if (row0 + 31 < col0) return;  // whole chunk strictly above the diagonal (warp-uniform)
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) scratch[lane][j] = p.alpha * __uint_as_float(r[j]);
+    __syncwarp();
+    const int c = col0 + int(lane);
+    if constexpr (EPI == EPI_SPLIT) {
+        float* dh = p.Dhi + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c;
+        float* dl = p.Dlo ? p.Dlo + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c : nullptr;
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+            float h, l;
+            split_tf32(scratch[i][lane], h, l);
+            dh[int64_t(i) * p.ldd] = h;
+            if (dl) dl[int64_t(i) * p.ldd] = l;
+        }
+    } else {
+        float* cc = p.C + int64_t(b) * p.c_bstride + int64_t(row0) * p.ldc + c;
+        if (p.beta != 0.f) {
+            float o[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = cc[int64_t(i) * p.ldc];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) scratch[i][lane] += p.beta * o[i];
+        }
+        if constexpr (EPI == EPI_STORE) {
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i) cc[int64_t(i) * p.ldc] = scratch[i][lane];
+        } else {  // SYM_EMA: lower triangle here, mirror below
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i)
+                if (row0 + i >= c) cc[int64_t(i) * p.ldc] = scratch[i][lane];
+            __syncwarp();
+            // mirror C[col][row] = C[row][col] for col < row; lanes = consecutive rows (coalesced)
+            float* cb = p.C + int64_t(b) * p.c_bstride;
+            const int row = row0 + int(lane);
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j)
+                if (row > col0 + j) cb[int64_t(col0 + j) * p.ldc + row] = scratch[lane][j];
+        }
+    }
+    __syncwarp();
+}
+
 // EPI_ADAM, warp-cooperative (soap_scaled_step precond.cpp:213-221): the
 // warp's 32 x 32 chunk of Ghat goes through the shared-memory transpose so
 // that the moment read-modify-writes and the S stores are 128-byte coalesced
@@ -417,6 +470,8 @@ __global__ void __launch_bounds__(192, 1)
                     apply_chunk(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
                 else if constexpr (EPI == EPI_ADAM)
                     adam_chunk(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
+                else if constexpr (EPI == EPI_STORE || EPI == EPI_SPLIT || EPI == EPI_SYM_EMA)
+                    rows_chunk<EPI>(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
                 else
                     epilogue_chunk<EPI>(p, b, row, tn * BN + c * 32, r);
             }
