@@ -505,7 +505,7 @@ def main():
                   if prec == abi.PREC_3XTF32 else "tf32"),
         "data": "synthetic (N(0, 1/cols) gradients, fixed per run; random-init parameters)",
         "config": cfg_out,
-        "roofline": {"kernel": "tcgen05 TN GEMM (all fused epilogues), main stream", "bound": "tensor",
+        "roofline": {"kernel": "tcgen05 TN GEMMs of the step, fused epilogues (refresh GEMMs on the side stream excluded)", "bound": "tensor",
                      "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                      "frac": (ach / peak) if ach else None,
                      "peak_note": f"{peak_src} dense bf16 (MEASURED_PEAKS.json bf16_tflops); tf32 kind = bf16/2, "

@@ -592,7 +592,9 @@ Operand op(const float* h, const float* l, int rows, int K) { return Operand{h, 
 void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const GemmParams& p,
               const int2* sym_tiles, int nsym, cudaStream_t s, double alg_flops) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (bs->profiling) {
+    // profile the step's GEMMs (main and group streams); refresh GEMMs on the
+    // side stream overlap them and are not part of the step's roofline
+    if (bs->profiling && s != bs->side) {
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, s));
@@ -606,7 +608,7 @@ void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const 
     g.sym_tiles = sym_tiles;
     g.sym_tiles_count = nsym;
     CK(gemm_launch(g, bs->precision, bs->num_sms, s));
-    if (bs->profiling) {
+    if (e0) {
         CK(cudaEventRecord(e1, s));
         bs->prof_events.emplace_back(e0, e1);
         bs->prof_flops += alg_flops;
