@@ -324,30 +324,59 @@ __global__ void __launch_bounds__(PW * 4) tj_pair_kernel(const float* __restrict
             }
             // nearly diagonal pairs (warm refreshes) rotate in few rounds: skip the rest
             if (!__syncthreads_or(threadIdx.x < PW / 2 && sn[threadIdx.x] != 0.f)) continue;
-            // One pass: every 2x2 block (rows of pair ki, columns of pair kj) of S
-            // becomes R_ki^T S_block R_kj (half the shared-memory traffic of a row
-            // pass followed by a column pass), and Z's columns rotate.
-            for (int e = threadIdx.x; e < (PW / 2) * (PW / 2); e += blockDim.x) {
-                const int ki = e / (PW / 2), kj = e % (PW / 2);
-                const float si = sn[ki], sj = sn[kj];
-                if (si == 0.f && sj == 0.f) continue;
-                const float ci = cs[ki], cj = cs[kj];
-                const int ai = pa[ki], bi = pc[ki], aj = pa[kj], bj = pc[kj];
-                float s00 = S[ai * (PW + 1) + aj], s01 = S[ai * (PW + 1) + bj];
-                float s10 = S[bi * (PW + 1) + aj], s11 = S[bi * (PW + 1) + bj];
-                // rows: [r_a; r_b] <- [c r_a - s r_b; s r_a + c r_b]
-                float t00 = ci * s00 - si * s10, t01 = ci * s01 - si * s11;
-                float t10 = si * s00 + ci * s10, t11 = si * s01 + ci * s11;
-                // columns: [c_a, c_b] <- [c c_a - s c_b, s c_a + c c_b]
-                s00 = cj * t00 - sj * t01;
-                s01 = sj * t00 + cj * t01;
-                s10 = cj * t10 - sj * t11;
-                s11 = sj * t10 + cj * t11;
-                if (ki == kj && si != 0.f) s01 = s10 = 0.f;  // the annihilated pair
-                S[ai * (PW + 1) + aj] = s00;
-                S[ai * (PW + 1) + bj] = s01;
-                S[bi * (PW + 1) + aj] = s10;
-                S[bi * (PW + 1) + bj] = s11;
+            if constexpr (PW == 128) {
+                // wide pairs: row pass then column pass (conflict-free rows; the
+                // fused 2x2 pass scatters over banks at this width)
+                for (int e = threadIdx.x; e < (PW / 2) * PW; e += blockDim.x) {  // rows of S
+                    const int kk = e / PW, j = e % PW;
+                    const float ss = sn[kk];
+                    if (ss == 0.f) continue;
+                    const int a = pa[kk], c = pc[kk];
+                    const float cc = cs[kk];
+                    const float x = S[a * (PW + 1) + j], y = S[c * (PW + 1) + j];
+                    S[a * (PW + 1) + j] = cc * x - ss * y;
+                    S[c * (PW + 1) + j] = ss * x + cc * y;
+                }
+                __syncthreads();
+                for (int e = threadIdx.x; e < (PW / 2) * PW; e += blockDim.x) {  // columns of S
+                    const int kk = e % (PW / 2), i = e / (PW / 2);
+                    const float ss = sn[kk];
+                    if (ss == 0.f) continue;
+                    const int a = pa[kk], c = pc[kk];
+                    const float cc = cs[kk];
+                    const float x = S[i * (PW + 1) + a], y = S[i * (PW + 1) + c];
+                    float na = cc * x - ss * y, nc = ss * x + cc * y;
+                    if (i == a) nc = 0.f;
+                    if (i == c) na = 0.f;
+                    S[i * (PW + 1) + a] = na;
+                    S[i * (PW + 1) + c] = nc;
+                }
+            } else {
+                // One pass: every 2x2 block (rows of pair ki, columns of pair kj) of S
+                // becomes R_ki^T S_block R_kj (half the shared-memory traffic of a row
+                // pass followed by a column pass), and Z's columns rotate.
+                for (int e = threadIdx.x; e < (PW / 2) * (PW / 2); e += blockDim.x) {
+                    const int ki = e / (PW / 2), kj = e % (PW / 2);
+                    const float si = sn[ki], sj = sn[kj];
+                    if (si == 0.f && sj == 0.f) continue;
+                    const float ci = cs[ki], cj = cs[kj];
+                    const int ai = pa[ki], bi = pc[ki], aj = pa[kj], bj = pc[kj];
+                    float s00 = S[ai * (PW + 1) + aj], s01 = S[ai * (PW + 1) + bj];
+                    float s10 = S[bi * (PW + 1) + aj], s11 = S[bi * (PW + 1) + bj];
+                    // rows: [r_a; r_b] <- [c r_a - s r_b; s r_a + c r_b]
+                    float t00 = ci * s00 - si * s10, t01 = ci * s01 - si * s11;
+                    float t10 = si * s00 + ci * s10, t11 = si * s01 + ci * s11;
+                    // columns: [c_a, c_b] <- [c c_a - s c_b, s c_a + c c_b]
+                    s00 = cj * t00 - sj * t01;
+                    s01 = sj * t00 + cj * t01;
+                    s10 = cj * t10 - sj * t11;
+                    s11 = sj * t10 + cj * t11;
+                    if (ki == kj && si != 0.f) s01 = s10 = 0.f;  // the annihilated pair
+                    S[ai * (PW + 1) + aj] = s00;
+                    S[ai * (PW + 1) + bj] = s01;
+                    S[bi * (PW + 1) + aj] = s10;
+                    S[bi * (PW + 1) + bj] = s11;
+                }
             }
             for (int e = threadIdx.x; e < (PW / 2) * PW; e += blockDim.x) {  // columns of Z
                 const int kk = e % (PW / 2), i = e / (PW / 2);
