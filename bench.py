@@ -470,17 +470,39 @@ def main():
     # ---- e2e: pinned H2D of each step's gradients + D2H of the clip statistic ----
     e2e = None
     if not args.no_e2e:
+        # Each step's gradients arrive from pinned host memory. The H2D of step
+        # k+1 streams into a staging buffer on a copy stream while step k
+        # computes (double buffering, as a data loader would); step k+1 then
+        # moves them into the bound gradient tensors with a device copy.
         host = [g.cpu().pin_memory() for g in grads]
+        staging = [torch.empty_like(g) for g in grads]
         h2d = sum(h.numel() * 4 for h in host)
+        copy_stream = torch.cuda.Stream(dev)
+        ev_copied, ev_consumed = torch.cuda.Event(), torch.cuda.Event()
+        cur = torch.cuda.current_stream(dev)
+
+        def prefetch():
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(ev_consumed)  # staging free once the previous step took it
+                for st_, h in zip(staging, host):
+                    st_.copy_(h, non_blocking=True)
+                ev_copied.record(copy_stream)
+
+        n_e2e = max(3, args.steps // 2)
+        ev_consumed.record(cur)
         barrier()
         t0 = time.perf_counter()
-        for _ in range(max(3, args.steps // 2)):
-            for g, h in zip(grads, host):  # on torch's current stream; the step orders after it
-                g.copy_(h, non_blocking=True)
+        prefetch()
+        for k in range(n_e2e):
+            cur.wait_event(ev_copied)
+            for g, st_ in zip(grads, staging):
+                g.copy_(st_, non_blocking=True)
+            ev_consumed.record(cur)
+            if k + 1 < n_e2e:
+                prefetch()
             one_step(step)
             step += 1
         barrier()
-        n_e2e = max(3, args.steps // 2)
         t_e2e = (time.perf_counter() - t0) * 1e3
         if world > 1:
             t = torch.tensor([t_e2e], device=dev)

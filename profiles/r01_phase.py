@@ -52,7 +52,8 @@ def eigh32(ns):
     for n in ns:
         b = max(1, min(512, (1 << 31) // (n * n * 4)))  # 8 GiB fp32 per point at most (C5 sizing)
         b = min(b, int(os.environ.get("ASG_EIGH_BATCH", b)))
-        x = torch.randn(b, n, 2 * n, dtype=torch.float32, device="cuda")
+        g = torch.Generator(device="cuda").manual_seed(1234 + n)
+        x = torch.randn(b, n, 2 * n, dtype=torch.float32, device="cuda", generator=g)
         a = (x @ x.transpose(1, 2)) / (2 * n) + 1e-3 * torch.eye(n, device="cuda")
         del x
         w = torch.empty(b, n, dtype=torch.float64, device="cuda")
