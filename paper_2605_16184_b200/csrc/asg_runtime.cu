@@ -624,6 +624,11 @@ T* at(T* base, size_t stride, int slot) {
 // Concurrent group chains: fork from the main stream, run group i on
 // stream_for(i), join back. With one group everything stays on main.
 int fork_groups(asg_blockset* bs) {
+    // Off by default: measured no gain on C2 (the step's big groups already fill
+    // the GPU), and overlapping launches would blur the per-GEMM timing of
+    // the roofline. ASG_GROUP_STREAMS=1 enables it.
+    static const bool on = getenv("ASG_GROUP_STREAMS") != nullptr;
+    if (!on) return 0;
     const int k = std::min<int>(asg_blockset::kGroupStreams, int(bs->groups.size()));
     if (k <= 1) return 0;
     CK(cudaEventRecord(bs->gfork, bs->main));
