@@ -314,6 +314,39 @@ void launch_adamw_apply(float* theta, int64_t ld_t, const float* grad, int64_t l
                                             b2, inv_bc1, inv_bc2, eps, lr_eff, wd, flag);
 }
 
+// Multi-tensor AdamW + apply: every 1-D / degenerate parameter of the step in
+// one launch (blockIdx.y = parameter).
+__global__ void adamw_multi_kernel(const AdamEntry* __restrict__ entries, float scale_val, float b1, float b2,
+                                   float inv_bc1, float inv_bc2, float eps, float lr_eff, float wd, int* flag) {
+    const AdamEntry en = entries[blockIdx.y];
+    const int64_t n = en.rows * en.cols;
+    bool bad = false;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / en.cols, c = e % en.cols;
+        const float g = scale_val * en.grad[r * en.ld_g + c];
+        bad |= !isfinite(g);
+        const float mm = b1 * en.m[e] + (1.f - b1) * g;
+        const float vv = b2 * en.v[e] + (1.f - b2) * g * g;
+        en.m[e] = mm;
+        en.v[e] = vv;
+        const float u = (mm * inv_bc1) / (sqrtf(vv * inv_bc2) + eps);
+        float& t = en.theta[r * en.ld_t + c];
+        t = t - lr_eff * (u + wd * t);
+    }
+    if (bad && flag) atomicOr(flag, 1);
+}
+
+void launch_adamw_multi(const AdamEntry* entries, int count, int64_t max_elems, float scale_val, float b1, float b2,
+                        float inv_bc1, float inv_bc2, float eps, float lr_eff, float wd, int* flag, cudaStream_t s) {
+    if (count <= 0) return;
+    int gx = int((max_elems + 255) / 256);
+    if (gx > 64) gx = 64;
+    if (gx < 1) gx = 1;
+    adamw_multi_kernel<<<dim3(gx, count), 256, 0, s>>>(entries, scale_val, b1, b2, inv_bc1, inv_bc2, eps, lr_eff, wd,
+                                                       flag);
+    count_launch();
+}
+
 // ============================================================================
 // K8: snapshot (fp32 factor slab -> fp64 shadow)
 // ============================================================================

@@ -70,6 +70,17 @@ void launch_adamw_apply(float* theta, int64_t ld_t, const float* grad, int64_t l
                         float b1, float b2, float inv_bc1, float inv_bc2, float eps, float lr_eff,
                         float wd, int* flag, cudaStream_t s);
 
+// One 1-D / degenerate parameter of the multi-tensor AdamW launch.
+struct AdamEntry {
+    float* theta;
+    const float* grad;
+    float* m;
+    float* v;
+    int64_t ld_t, ld_g, rows, cols;
+};
+void launch_adamw_multi(const AdamEntry* entries, int count, int64_t max_elems, float scale_val, float b1, float b2,
+                        float inv_bc1, float inv_bc2, float eps, float lr_eff, float wd, int* flag, cudaStream_t s);
+
 // Refresh path (fp64).
 // Snapshot: [b][M][M] fp32 slab's leading m x m -> [b][m][m] fp64 (+ trace).
 void launch_snapshot(const float* src, int nb, int M, int m, double* dst, cudaStream_t s);

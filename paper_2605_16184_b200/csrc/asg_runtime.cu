@@ -248,6 +248,10 @@ struct asg_blockset {
     asg::BlockRef* d_ref1 = nullptr;
     asg::ApplyEntry* d_apply1 = nullptr;
     float* d_out1 = nullptr;
+    // multi-tensor AdamW table (owned 1-D / degenerate parameters)
+    asg::AdamEntry* d_adam = nullptr;
+    int n_adam = 0;
+    int64_t adam_max_elems = 0;
     // multi-GPU pack layout
     asg::BlockRef* d_pack_refs = nullptr;
     int64_t* d_pack_offs = nullptr;
@@ -619,6 +623,23 @@ void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const 
 template <class T>
 T* at(T* base, size_t stride, int slot) {
     return base ? base + stride * size_t(slot) : nullptr;
+}
+
+// (Re)builds the device table of the multi-tensor AdamW launch.
+void build_adam_table(asg_blockset* bs) {
+    std::vector<AdamEntry> t;
+    bs->adam_max_elems = 0;
+    for (const Unit& u : bs->units) {
+        if (!u.adamw || u.owner != bs->rank) continue;
+        const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+        AdamEntry e{d.theta, d.grad, u.am, u.av, d.ld_theta, d.ld_grad, d.rows, d.cols};
+        t.push_back(e);
+        bs->adam_max_elems = std::max(bs->adam_max_elems, d.rows * d.cols);
+    }
+    bs->n_adam = int(t.size());
+    if (t.empty()) return;
+    if (!bs->d_adam) bs->d_adam = dalloc<AdamEntry>(bs, t.size());
+    h2d(bs->d_adam, t.data(), t.size() * sizeof(AdamEntry), bs->main);
 }
 
 // Concurrent group chains: fork from the main stream, run group i on
@@ -1627,6 +1648,7 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
                 CK(cudaMemsetAsync(u.av, 0, n * 4, bs->main));
             }
         }
+        build_adam_table(bs);
         bs->d_flag = dalloc<int>(bs, 1);
         bs->d_sqnorm = dalloc<double>(bs, 1);
         bs->d_scale = dalloc<float>(bs, 1);
@@ -1723,6 +1745,7 @@ int asg_blockset_bind_params(asg_blockset* bs, const asg_param_desc* params, int
         CK(cudaStreamSynchronize(bs->main));
         bs->params.assign(params, params + n_params);
         for (Group& g : bs->groups) bind_group_tables(bs, g);
+        build_adam_table(bs);
     });
 }
 
@@ -1859,13 +1882,17 @@ void precondition_apply_impl(asg_blockset* bs, double clip_scale, double lr_scal
         group_update(bs, g, 0, g.nb, EPI_APPLY, lr_eff, g.d_apply, nullptr, stream_for(bs, k, int(gi)));
     }
     cudaStream_t as = stream_for(bs, k, int(bs->groups.size()));  // AdamW on the least loaded group stream
+    // AdamW for every owned 1-D / degenerate parameter in one launch (they step together)
+    int64_t t_adam = 0;
     for (Unit& u : bs->units) {
         if (!u.adamw || u.owner != bs->rank) continue;
-        const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
         u.adam_t += 1;
-        const double t = double(u.adam_t);
-        launch_adamw_apply(d.theta, d.ld_theta, d.grad, d.ld_grad, d.rows, d.cols, u.am, u.av, nullptr, float(clip_scale),
-                           float(bs->opt.beta1), float(bs->opt.beta2), float(1.0 / (1.0 - std::pow(bs->opt.beta1, t))),
+        t_adam = u.adam_t;
+    }
+    if (bs->n_adam > 0) {
+        const double t = double(t_adam);
+        launch_adamw_multi(bs->d_adam, bs->n_adam, bs->adam_max_elems, float(clip_scale), float(bs->opt.beta1),
+                           float(bs->opt.beta2), float(1.0 / (1.0 - std::pow(bs->opt.beta1, t))),
                            float(1.0 / (1.0 - std::pow(bs->opt.beta2, t))), float(bs->opt.eps), lr_eff,
                            float(bs->opt.weight_decay), bs->d_flag, as);
     }

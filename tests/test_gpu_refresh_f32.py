@@ -167,3 +167,27 @@ def test_f32_trajectory_matches_oracle_bounded_staleness(method):
                          refresh_mode=abi.REFRESH_F32, r_scale=(6.0 if method == abi.SOAP else 2.5))
     assert o.stats().installed >= 2 * 8
     assert max(errs) <= 1.0, errs
+
+
+@pytest.mark.parametrize("method", [abi.SHAMPOO, abi.SOAP, abi.KL_SHAMPOO])
+def test_tf32_mode_trajectory_runs_and_tracks_the_oracle(method):
+    """Single-pass TF32 products (ASG_PREC_TF32, no lo operands anywhere,
+    F32 refresh): the fast mode runs end to end and tracks the fp64 oracle to
+    TF32 accuracy. Stated tolerance: r = 2e-2 of the accumulated update (TF32
+    products carry ~1e-3 relative error per GEMM)."""
+    import test_gpu_step as T
+    from paper_2605_16184_b200 import optimizer
+
+    class TF32Optimizer(optimizer.AsteriaOptimizer):
+        def __init__(self, *a, **k):
+            k["precision"] = abi.PREC_TF32
+            super().__init__(*a, **k)
+
+    class Shim:
+        AsteriaOptimizer = TF32Optimizer
+
+    shapes = [(256, 384), (300,), (96, 96)]
+    errs, o = T.run_pair(Shim, method, shapes, limit=128, pf=4, steps=8, S=3, delay=2.0,
+                         refresh_mode=abi.REFRESH_F32, r_scale=(40.0 if method == abi.SOAP else 100.0))
+    assert o.stats().installed >= 2 * 7
+    assert max(errs) <= 1.0, errs
