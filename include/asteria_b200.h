@@ -307,6 +307,20 @@ int asg_block_soap_step_f64(asg_blockset* bs, int64_t idx, const double* g, int6
  * receives the rank of unit i (capacity >= *count). */
 int asg_plan_owners(const asg_optimizer_config* opt, const int64_t* rows, const int64_t* cols,
                     int64_t n_params, int32_t world, int32_t* owner, int64_t capacity, int64_t* count);
+/* Elements per rank segment of the owner-major exchange buffers (the largest
+ * shard); asg_unpack_gathered with this stride uses precomputed offsets. */
+int asg_gather_stride(const asg_blockset* bs, int64_t* stride);
+/* Data-parallel gradients -> owners ("next" row F1; harness.cpp:417-436): packs
+ * every unit's gradient slice owner-major (rank r's units at r * stride, zero
+ * padding) into `sendbuf` [world * stride] for a reduce-scatter (SUM) ... */
+int asg_pack_grads(asg_blockset* bs, float* sendbuf, void* stream);
+/* ... and writes this rank's reduced segment `recvbuf` [stride], times `scale`
+ * (1/world for the reference's average, simnet allreduce_avg), into its owned
+ * gradient slices. */
+int asg_unpack_reduced_grads(asg_blockset* bs, const float* recvbuf, float scale, void* stream);
+/* Squared norm over this rank's owned gradient slices (sum over ranks = the
+ * global clip norm, harness.cpp:219-223); synchronizes the stream. */
+int asg_grad_sqnorm_owned(asg_blockset* bs, void* stream, double* sqnorm, int32_t* nonfinite);
 /* Elements of theta owned by `rank` (owner-major layout). */
 int asg_shard_elems(const asg_blockset* bs, int32_t rank, int64_t* elems);
 /* Packs this rank's owned block slices of theta into `sendbuf` (device). */

@@ -931,6 +931,20 @@ void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, 
     count_launch();
 }
 
+__global__ void unpack_scaled_kernel(const BlockRef* blocks, const int64_t* offsets, const float* in, float scale) {
+    const BlockRef blk = blocks[blockIdx.y];
+    const int64_t n = int64_t(blk.rows) * blk.cols;
+    const float* i = in + offsets[blockIdx.y];
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+        blk.dst[(e / blk.cols) * blk.ld + (e % blk.cols)] = scale * i[e];
+}
+
+void launch_unpack_scaled(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, const float* in, float scale,
+                          cudaStream_t s) {
+    if (nb > 0) unpack_scaled_kernel<<<dim3(64, nb), 256, 0, s>>>(blocks_dev, offsets_dev, in, scale);
+    count_launch();
+}
+
 void launch_unpack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, const float* in,
                           cudaStream_t s) {
     if (nb > 0) unpack_kernel<<<dim3(64, nb), 256, 0, s>>>(blocks_dev, offsets_dev, in);

@@ -141,5 +141,8 @@ void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, 
                         cudaStream_t s);
 void launch_unpack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb,
                           const float* in, cudaStream_t s);
+// dst = scale * in (the reduced gradient segment -> the owned gradient slices)
+void launch_unpack_scaled(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, const float* in,
+                          float scale, cudaStream_t s);
 
 }  // namespace asg

@@ -261,6 +261,9 @@ struct asg_blockset {
     int64_t* d_unpack_offs = nullptr;
     int n_unpack = 0;
     std::vector<int> unpack_rank;
+    int64_t stride = 0;  // elements per rank segment of the owner-major buffers
+    asg::BlockRef *d_gpack_refs = nullptr, *d_gunpack_refs = nullptr;
+    int64_t *d_gpack_offs = nullptr, *d_gunpack_offs = nullptr;
     // installs decided by the schedule bookkeeping, executed after the
     // step's refreshes are launched as one batch
     std::vector<int> deferred_installs;
@@ -623,6 +626,68 @@ void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const 
 template <class T>
 T* at(T* base, size_t stride, int slot) {
     return base ? base + stride * size_t(slot) : nullptr;
+}
+
+// (Re)builds the owner-major layouts of the multi-GPU exchange:
+// rank r's owned units are contiguous at r * stride (stride = the largest shard):
+//   theta pack (owned) / theta unpack (all units, after the all-gather),
+//   gradient pack (all units, before a reduce-scatter) / gradient unpack (owned).
+void build_owner_layout(asg_blockset* bs) {
+    std::vector<BlockRef> pk, upk, gpk, gupk;
+    std::vector<int64_t> pko, upko, gpko, gupko;
+    std::vector<int64_t> inrank;
+    bs->shard_elems.assign(size_t(bs->world), 0);
+    bs->unpack_rank.clear();
+    for (int r = 0; r < bs->world; ++r)
+        for (size_t i = 0; i < bs->units.size(); ++i) {
+            const Unit& u = bs->units[i];
+            if (u.owner != r) continue;
+            const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+            const int32_t rows = int32_t(u.spec.row_end - u.spec.row_begin), cols = int32_t(u.spec.col_end - u.spec.col_begin);
+            BlockRef th{}, gr{};
+            th.src = th.dst = d.theta ? d.theta + u.spec.row_begin * d.ld_theta + u.spec.col_begin : nullptr;
+            th.ld = d.ld_theta;
+            th.rows = rows;
+            th.cols = cols;
+            gr.src = d.grad ? d.grad + u.spec.row_begin * d.ld_grad + u.spec.col_begin : nullptr;
+            gr.dst = const_cast<float*>(gr.src);
+            gr.ld = d.ld_grad;
+            gr.rows = rows;
+            gr.cols = cols;
+            const int64_t at_rank = bs->shard_elems[size_t(r)];
+            if (r == bs->rank) {
+                pk.push_back(th);
+                pko.push_back(at_rank);
+                gupk.push_back(gr);
+                gupko.push_back(at_rank);
+            }
+            upk.push_back(th);
+            gpk.push_back(gr);
+            inrank.push_back(at_rank);
+            bs->unpack_rank.push_back(r);
+            bs->shard_elems[size_t(r)] += int64_t(rows) * cols;
+        }
+    bs->stride = 0;
+    for (int64_t e : bs->shard_elems) bs->stride = std::max(bs->stride, e);
+    for (size_t i = 0; i < upk.size(); ++i) {
+        upko.push_back(int64_t(bs->unpack_rank[i]) * bs->stride + inrank[i]);
+        gpko.push_back(int64_t(bs->unpack_rank[i]) * bs->stride + inrank[i]);
+    }
+    bs->n_pack = int(pk.size());
+    bs->n_unpack = int(upk.size());
+    auto up = [&](auto*& dst, const auto& v) {
+        using T = typename std::decay_t<decltype(v)>::value_type;
+        if (!dst) dst = dalloc<T>(bs, std::max<size_t>(1, bs->units.size()));
+        if (!v.empty()) h2d(dst, v.data(), v.size() * sizeof(T), bs->main);
+    };
+    up(bs->d_pack_refs, pk);
+    up(bs->d_pack_offs, pko);
+    up(bs->d_unpack_refs, upk);
+    up(bs->d_unpack_offs, upko);
+    up(bs->d_gpack_refs, gpk);
+    up(bs->d_gpack_offs, gpko);
+    up(bs->d_gunpack_refs, gupk);
+    up(bs->d_gunpack_offs, gupko);
 }
 
 // (Re)builds the device table of the multi-tensor AdamW launch.
@@ -1660,45 +1725,7 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         bs->d_out1 = dalloc<float>(bs, std::max<size_t>(stage, 1));
         bs->d_ref1 = dalloc<BlockRef>(bs, 1);
         bs->d_apply1 = dalloc<ApplyEntry>(bs, 1);
-        // owner-major all-gather layout
-        std::vector<BlockRef> pk, upk;
-        std::vector<int64_t> pko, upko;
-        bs->shard_elems.assign(size_t(world), 0);
-        for (int r = 0; r < world; ++r) {
-            for (size_t i = 0; i < bs->units.size(); ++i) {
-                const Unit& u = bs->units[i];
-                if (u.owner != r) continue;
-                const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
-                BlockRef br{};
-                br.src = d.theta ? d.theta + u.spec.row_begin * d.ld_theta + u.spec.col_begin : nullptr;
-                br.dst = d.theta ? d.theta + u.spec.row_begin * d.ld_theta + u.spec.col_begin : nullptr;
-                br.ld = d.ld_theta;
-                br.rows = int32_t(u.spec.row_end - u.spec.row_begin);
-                br.cols = int32_t(u.spec.col_end - u.spec.col_begin);
-                if (r == rank) {
-                    pk.push_back(br);
-                    pko.push_back(bs->shard_elems[size_t(r)]);
-                }
-                upk.push_back(br);
-                upko.push_back(bs->shard_elems[size_t(r)]);
-                bs->unpack_rank.push_back(r);
-                bs->shard_elems[size_t(r)] += int64_t(br.rows) * br.cols;
-            }
-        }
-        bs->n_pack = int(pk.size());
-        bs->n_unpack = int(upk.size());
-        bs->d_pack_refs = dalloc<BlockRef>(bs, pk.size());
-        bs->d_pack_offs = dalloc<int64_t>(bs, pko.size());
-        bs->d_unpack_refs = dalloc<BlockRef>(bs, upk.size());
-        bs->d_unpack_offs = dalloc<int64_t>(bs, upko.size());
-        if (!pk.empty()) {
-            h2d(bs->d_pack_refs, pk.data(), pk.size() * sizeof(BlockRef), bs->main);
-            h2d(bs->d_pack_offs, pko.data(), pko.size() * 8, bs->main);
-        }
-        if (!upk.empty()) {
-            h2d(bs->d_unpack_refs, upk.data(), upk.size() * sizeof(BlockRef), bs->main);
-            h2d(bs->d_unpack_offs, upko.data(), upko.size() * 8, bs->main);
-        }
+        build_owner_layout(bs);
         CK(cudaStreamSynchronize(bs->main));
         CK(cudaGetLastError());
         *out = bs;
@@ -1746,6 +1773,7 @@ int asg_blockset_bind_params(asg_blockset* bs, const asg_param_desc* params, int
         bs->params.assign(params, params + n_params);
         for (Group& g : bs->groups) bind_group_tables(bs, g);
         build_adam_table(bs);
+        build_owner_layout(bs);
     });
 }
 
@@ -2255,13 +2283,19 @@ int asg_unpack_gathered(asg_blockset* bs, const float* recvbuf, int64_t stride_e
     return guard([&] {
         CK(cudaSetDevice(bs->device));
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        if (stride_elems == bs->stride) {  // precomputed offsets (asg_gather_stride)
+            launch_unpack_blocks(bs->d_unpack_refs, bs->d_unpack_offs, bs->n_unpack, recvbuf, s);
+            CK(cudaGetLastError());
+            return;
+        }
         // offsets are within each rank's shard; ranks are `stride_elems` apart
         std::vector<int64_t> offs(size_t(bs->n_unpack));
         std::vector<int64_t> host_offs(size_t(bs->n_unpack));
         if (bs->n_unpack > 0)
             CK(cudaMemcpy(host_offs.data(), bs->d_unpack_offs, host_offs.size() * 8, cudaMemcpyDeviceToHost));
-        for (int i = 0; i < bs->n_unpack; ++i)
-            offs[size_t(i)] = int64_t(bs->unpack_rank[size_t(i)]) * stride_elems + host_offs[size_t(i)];
+        for (int i = 0; i < bs->n_unpack; ++i)  // stored offsets use bs->stride: rebase
+            offs[size_t(i)] = int64_t(bs->unpack_rank[size_t(i)]) * stride_elems +
+                              (host_offs[size_t(i)] - int64_t(bs->unpack_rank[size_t(i)]) * bs->stride);
         int64_t* d_offs = nullptr;
         if (bs->n_unpack > 0) {
             CK(cudaMallocAsync(reinterpret_cast<void**>(&d_offs), offs.size() * 8, s));
@@ -2271,6 +2305,56 @@ int asg_unpack_gathered(asg_blockset* bs, const float* recvbuf, int64_t stride_e
             CK(cudaStreamSynchronize(s));
         }
         CK(cudaGetLastError());
+    });
+}
+
+int asg_gather_stride(const asg_blockset* bs, int64_t* stride) {
+    return guard([&] {
+        if (!bs || !stride) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        *stride = bs->stride;
+    });
+}
+
+int asg_pack_grads(asg_blockset* bs, float* sendbuf, void* stream) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        if (bs->world > 1)  // padding between shards stays zero
+            CK(cudaMemsetAsync(sendbuf, 0, size_t(bs->world) * bs->stride * 4, s));
+        launch_pack_blocks(bs->d_gpack_refs, bs->d_gpack_offs, bs->n_unpack, sendbuf, s);
+        CK(cudaGetLastError());
+    });
+}
+
+int asg_unpack_reduced_grads(asg_blockset* bs, const float* recvbuf, float scale, void* stream) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        launch_unpack_scaled(bs->d_gunpack_refs, bs->d_gunpack_offs, bs->n_pack, recvbuf, scale, s);
+        CK(cudaGetLastError());
+    });
+}
+
+int asg_grad_sqnorm_owned(asg_blockset* bs, void* stream, double* sqnorm, int32_t* nonfinite) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        CK(cudaMemsetAsync(bs->d_sqnorm, 0, sizeof(double), s));
+        CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), s));
+        for (const Unit& u : bs->units) {
+            if (u.owner != bs->rank) continue;
+            const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+            launch_sqnorm(d.grad + u.spec.row_begin * d.ld_grad + u.spec.col_begin, u.spec.row_end - u.spec.row_begin,
+                          u.spec.col_end - u.spec.col_begin, d.ld_grad, bs->d_sqnorm, bs->d_flag, s);
+        }
+        double v = 0.0;
+        int f = 0;
+        CK(cudaMemcpyAsync(&v, bs->d_sqnorm, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&f, bs->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), s));
+        if (sqnorm) *sqnorm = v;
+        if (nonfinite) *nonfinite = f;
     });
 }
 

@@ -149,6 +149,56 @@ class AsteriaOptimizer:
         check(lib.asg_shard_elems(self._h, rank, C.byref(e)))
         return e.value
 
+    def gather_stride(self):
+        e = C.c_int64()
+        check(lib.asg_gather_stride(self._h, C.byref(e)))
+        return e.value
+
+    def reduce_scatter_grads(self, group=None):
+        """Data-parallel gradients -> owners: every
+        rank holds full local gradients; each rank receives the average over
+        ranks of the blocks it owns (the reference's allreduce_avg,
+        harness.cpp:425, restricted to what the owner needs) and writes it into
+        its gradient tensors. One reduce-scatter of the owner-major buffer
+        instead of an all-reduce of everything."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        stride = self.gather_stride()
+        if getattr(self, "_rs_send", None) is None:
+            self._rs_send = torch.zeros(stride * self.world, dtype=torch.float32, device=self.device)
+            self._rs_recv = torch.zeros(stride, dtype=torch.float32, device=self.device)
+        cur = torch.cuda.current_stream(self.device)
+        check(lib.asg_pack_grads(self._h, C.c_void_p(self._rs_send.data_ptr()), stream_arg(cur)))
+        if dist.get_backend(group) == "nccl":
+            dist.reduce_scatter_tensor(self._rs_recv, self._rs_send, op=dist.ReduceOp.SUM, group=group)
+        else:  # gloo (CPU test harness): stage through host memory
+            send = self._rs_send.cpu()
+            recv = torch.empty(stride, dtype=torch.float32)
+            dist.reduce_scatter_tensor(recv, send, op=dist.ReduceOp.SUM, group=group)
+            self._rs_recv.copy_(recv)
+        check(lib.asg_unpack_reduced_grads(self._h, C.c_void_p(self._rs_recv.data_ptr()), 1.0 / self.world,
+                                           stream_arg(cur)))
+
+    def global_grad_sqnorm(self, group=None):
+        """Global squared gradient norm after reduce_scatter_grads: the owned
+        partial sums, all-reduced (the clip statistic, harness.cpp:219-223)."""
+        import torch
+        import torch.distributed as dist
+        v, f = C.c_double(), C.c_int32()
+        check(lib.asg_grad_sqnorm_owned(self._h, stream_arg(torch.cuda.current_stream(self.device)), C.byref(v),
+                                        C.byref(f)))
+        if f.value:
+            raise abi.NonFiniteError("non-finite gradient")
+        if self.world == 1:
+            return v.value
+        t = torch.tensor([v.value], dtype=torch.float64)
+        if dist.get_backend(group) == "nccl":
+            t = t.to(self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return float(t.item())
+
     def allgather(self, group=None, stream=None):
         """All-gathers every rank's owned (updated) block slices of theta and
         scatters them back into the parameters (owner-major layout). NCCL
@@ -158,7 +208,7 @@ class AsteriaOptimizer:
         import torch.distributed as dist
         if self.world == 1:
             return
-        stride = max(self.shard_elems(r) for r in range(self.world))
+        stride = self.gather_stride()
         if self._gather_buf is None:
             self._gather_send = torch.zeros(stride, dtype=torch.float32, device=self.device)
             self._gather_buf = torch.zeros(stride * self.world, dtype=torch.float32, device=self.device)

@@ -61,6 +61,10 @@ _SIGS = {
     "asg_block_soap_step_f64": (C.c_int, [_vp, _i64, _P(_f64), _i64, _P(_f64)]),
     "asg_plan_owners": (C.c_int, [_P(abi.OptimizerConfig), _P(_i64), _P(_i64), _i64, _i32, _P(_i32), _i64, _P(_i64)]),
     "asg_shard_elems": (C.c_int, [_vp, _i32, _P(_i64)]),
+    "asg_gather_stride": (C.c_int, [_vp, _P(_i64)]),
+    "asg_pack_grads": (C.c_int, [_vp, _vp, _vp]),
+    "asg_unpack_reduced_grads": (C.c_int, [_vp, _vp, _f32, _vp]),
+    "asg_grad_sqnorm_owned": (C.c_int, [_vp, _vp, _P(_f64), _P(_i32)]),
     "asg_pack_owned": (C.c_int, [_vp, _vp, _vp]),
     "asg_unpack_gathered": (C.c_int, [_vp, _vp, _i64, _vp]),
     "asg_launch_count": (C.c_int, [_P(_u64)]),

@@ -75,3 +75,74 @@ def test_two_ranks_match_single_rank():
     for rank in (0, 1):
         for a, b in zip(results[rank][0], ref):
             assert np.array_equal(a, b), np.abs(a - b).max()
+
+
+# ---- data-parallel gradients -> owners ----------------------
+def _dp_run(rank, world, steps):
+    """Each rank holds DIFFERENT local gradients; reduce_scatter_grads gives
+    every owner the average of its blocks (allreduce_avg, harness.cpp:425);
+    the global clip norm comes from the owned partial sums."""
+    from paper_2605_16184_b200 import abi, runtime
+    from paper_2605_16184_b200.optimizer import AsteriaOptimizer
+    opt = runtime.optimizer_defaults(abi.SOAP)
+    opt.lr, opt.block_dim_limit, opt.precondition_frequency = 1e-2, 128, 2
+    sched = runtime.scheduler_defaults()
+    sched.pf, sched.staleness_S = 2, 1
+    g = torch.Generator().manual_seed(0)
+    params = [(0.1 * torch.randn(*s, generator=g)).cuda() for s in SHAPES]
+    grads = [torch.zeros_like(p) for p in params]
+    o = AsteriaOptimizer(params, grads, opt, sched, rank=rank, world=world)
+    norms = []
+    for step in range(steps):
+        local = [[1e-3 * torch.randn(*gr.shape, generator=g) for gr in grads] for _ in range(2)]
+        if world == 1:  # reference: the averaged gradients directly
+            for gr, a, b in zip(grads, local[0], local[1]):
+                gr.copy_(0.5 * (a + b))
+            norms.append(o.grad_sqnorm())
+        else:
+            for gr, mine in zip(grads, local[rank]):
+                gr.copy_(mine)
+            o.reduce_scatter_grads()
+            norms.append(o.global_grad_sqnorm())
+        o.clock_advance(sched.step_compute_us)
+        o.step(step, clip_scale=1.0)
+        o.allgather()
+    o.synchronize()
+    return [p.cpu().numpy() for p in params], norms
+
+
+def _dp_worker(rank, world, port, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out, norms = _dp_run(rank, world, steps)
+    q.put((rank, out, norms))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_reduce_scatter_grads_matches_averaged_single_rank():
+    import torch.multiprocessing as mp
+    steps = 4
+    ref, ref_norms = _dp_run(0, 1, steps)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(2):
+        rank, out, norms = q.get(timeout=600)
+        results[rank] = (out, norms)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        out, norms = results[rank]
+        # the averaged gradients are formed in a different order (fp32 sum of two
+        # ranks then * 1/2 vs 0.5 * (a + b)): equal to the last bits
+        np.testing.assert_allclose(norms, ref_norms, rtol=1e-5)
+        for a, b in zip(out, ref):
+            np.testing.assert_allclose(a, b, rtol=0, atol=1e-6 * max(1.0, float(np.abs(b).max())))
