@@ -46,6 +46,7 @@ size_t tc_eigh_workspace_floats(int nb, int n);
 // orthonormalize: one Newton-Schulz step on J (callers that re-orthonormalize
 // the product Q J themselves pass false).
 void launch_tc_eigh(const float* B, int D, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
-                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize = true);
+                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize = true,
+                    int* ident = nullptr);  // optional per matrix: 1 if J is exactly the identity
 
 }  // namespace asg

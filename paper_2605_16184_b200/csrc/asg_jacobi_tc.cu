@@ -774,7 +774,7 @@ __global__ void tj_loop_kernel(const int* __restrict__ active, int nb, int* __re
 // eigenvalues come first (padding sits above the spectrum).
 __global__ void tj_rank_kernel(const float* __restrict__ Ah, const float* __restrict__ Al, int n, int D,
                                int* __restrict__ rank, double* __restrict__ values, const int* __restrict__ active,
-                               int* __restrict__ status) {
+                               int* __restrict__ status, const int* __restrict__ sweeps, int* __restrict__ ident) {
     extern __shared__ float dg[];
     const int64_t b = blockIdx.x;
     const int64_t DD = int64_t(D) * D;
@@ -790,6 +790,16 @@ __global__ void tj_rank_kernel(const float* __restrict__ Ah, const float* __rest
         }
         rank[b * D + r] = i;  // inverse permutation: output column r <- V column i
         if (r < n) values[b * n + r] = double(di);
+    }
+    // J = I exactly: no sweep rotated anything and the order is already ascending
+    if (ident) {
+        bool moved = false;
+        for (int i = threadIdx.x; i < D; i += blockDim.x) {
+            const float di = dg[i];
+            for (int j = i + 1; j < D && !moved; ++j) moved |= dg[j] < di;  // a later smaller value reorders
+        }
+        const int any_moved = __syncthreads_or(moved);
+        if (threadIdx.x == 0) ident[b] = (!any_moved && sweeps[b] == 0) ? 1 : 0;
     }
 }
 
@@ -932,7 +942,7 @@ int tc_eigh_dim(int n) { return (n + JP - 1) / JP * JP; }
 
 namespace {
 void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
-                   int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize) {
+                   int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize, int* ident) {
     const int D = (n + JP - 1) / JP * JP;
     (void)D_in;  // B, J, J^T are [nb][D][D] with D = roundup(n, 128) (== the group's padded dim)
     const bool wide = n >= kWidePairN;
@@ -1027,7 +1037,7 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
         check(st, 1);
     };
     auto epilogue = [&](cudaStream_t st) {
-        tj_rank_kernel<<<nb, 512, size_t(D) * 4, st>>>(Ah, Al, n, D, rank, values, active, status);
+        tj_rank_kernel<<<nb, 512, size_t(D) * 4, st>>>(Ah, Al, n, D, rank, values, active, status, sweeps, ident);
         tj_gather_kernel<<<dim3(256, nb), 256, 0, st>>>(Vh, Vl, rank, n, D, Jh, Jl);
         launch_transpose_split(Jh, Jl, nb, D, D, JTh, JTl, false, st);
     };
@@ -1089,9 +1099,9 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
     }
     static std::mutex mu;
     using Key = std::tuple<const void*, const void*, const void*, const void*, const void*, const void*, const void*,
-                           const void*, int, int, float, int>;
+                           const void*, int, int, float, int, const void*>;
     static std::map<Key, cudaGraphExec_t> cache;
-    const Key key{B, values, Jh, Jl, JTh, JTl, ws, status, nb, n, ftol, inner};
+    const Key key{B, values, Jh, Jl, JTh, JTl, ws, status, nb, n, ftol, inner, ident};
     cudaGraphExec_t exec = nullptr;
     {
         std::lock_guard<std::mutex> lk(mu);
@@ -1153,7 +1163,8 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
 }  // namespace
 
 void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* Jl, float* JTh, float* JTl, float* ws,
-                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize) {
+                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize,
+                    int* ident) {
     // the apply kernel keeps every pair flag of a launch in shared memory
     const int D = (n + JP - 1) / JP * JP;
     const int npairs = D / (n >= kWidePairN ? 64 : 32) / 2;
@@ -1163,7 +1174,7 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
         const int cnt = nb - b0 < sub ? nb - b0 : sub;
         tc_eigh_chunk(B + size_t(b0) * DD, D_in, values + size_t(b0) * n, Jh + size_t(b0) * DD,
                       Jl ? Jl + size_t(b0) * DD : nullptr, JTh + size_t(b0) * DD, JTl ? JTl + size_t(b0) * DD : nullptr,
-                      ws, cnt, n, status + b0, num_sms, s, tol, orthonormalize);
+                      ws, cnt, n, status + b0, num_sms, s, tol, orthonormalize, ident ? ident + b0 : nullptr);
     }
 }
 

@@ -193,6 +193,9 @@ struct Group {
     int ntM = 0, ntN = 0;
     int* d_status = nullptr;
     int* h_status = nullptr;  // pinned
+    // F32 refresh: 1 where the eigensolve left the basis exactly unchanged (J = I);
+    // such SOAP installs reduce to the eigenvalue copy
+    int *d_identL = nullptr, *d_identR = nullptr, *h_identL = nullptr, *h_identR = nullptr;
 };
 
 }  // namespace
@@ -235,6 +238,7 @@ struct asg_blockset {
     // F32 refresh: tensor-core Jacobi workspace (side stream)
     float* tc_ws = nullptr;
     int* pair_status = nullptr;  // both-sides eigensolves: per-matrix status before the merge
+    int* pair_ident = nullptr;   // both-sides eigensolves: per-matrix J = I flags
     bool fp64_jacobi = false;  // ASG_F32_FP64_JACOBI=1: F32 refresh with the fp64 block Jacobi (diagnostics)
     // SOAP install workspace (one block)
     double *iw_rotL = nullptr, *iw_rotR = nullptr, *iw_sq = nullptr, *iw_a = nullptr, *iw_b = nullptr;
@@ -523,6 +527,14 @@ void alloc_group(asg_blockset* bs, Group& g) {
     g.d_apply = dalloc<ApplyEntry>(bs, nb);
     g.d_status = dalloc<int>(bs, nb);
     g.h_status = halloc<int>(bs, nb);
+    if (f32_refresh(bs) && is_soap(bs)) {
+        g.d_identL = dalloc<int>(bs, nb);
+        g.d_identR = dalloc<int>(bs, nb);
+        g.h_identL = halloc<int>(bs, nb);
+        g.h_identR = halloc<int>(bs, nb);
+        CK(cudaMemsetAsync(g.d_identL, 0, nb * sizeof(int), s));
+        CK(cudaMemsetAsync(g.d_identR, 0, nb * sizeof(int), s));
+    }
     CK(cudaMemsetAsync(g.d_status, 0, nb * sizeof(int), s));
     const int bnM = gemm_bn_for(g.M), bnN = gemm_bn_for(g.N);
     g.ntM = gemm_sym_tile_list(g.M, bnM, nullptr);
@@ -577,6 +589,7 @@ void alloc_workspace(asg_blockset* bs) {
         for (float*& t : bs->tw) t = dalloc<float>(bs, bs->tw_slab * size_t(2 * bs->ws_chunk));
         bs->tc_ws = dalloc<float>(bs, tc_eigh_workspace_floats(2 * bs->ws_chunk, Dmax));
         bs->pair_status = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
+        bs->pair_ident = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
         if (is_soap(bs))
             for (float*& t : bs->iw32) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
     }
@@ -1051,7 +1064,7 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
         // tensor-core block Jacobi over all sides: J -> (t0, t1), J^T -> (t2, t3)
         // (Q J is re-orthonormalized below / at the SOAP install, so J itself is not)
         launch_tc_eigh(t[4], D, bs->ws_vals, t[0], t1, t[2], t3, bs->tc_ws, nb, d, st, bs->num_sms, s,
-                       f32_refresh_tol(), false);
+                       f32_refresh_tol(), false, g.d_identL ? bs->pair_ident : nullptr);
     } else {
         launch_snapshot_sym(t[4], nb, D, d, bs->ws_snap, s);
         EighOpts eo;
@@ -1059,7 +1072,12 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
         eo.tol = f32_refresh_tol();
         launch_eigh(bs->ws_snap, bs->ws_vals, bs->ws_vecs, bs->ws_work, nb, d, st, s, nullptr, eo);
         launch_f64_to_split(bs->ws_vecs, nb, d, D, false, t[0], t1, t[2], t3, s);
+        if (g.d_identL) CK(cudaMemsetAsync(bs->pair_ident, 0, size_t(nb) * sizeof(int), s));  // unknown: full install
     }
+    if (g.d_identL)
+        for (int j = 0; j < nsides; ++j)
+            CK(cudaMemcpyAsync((sides[size_t(j)].left ? g.d_identL : g.d_identR) + s0, bs->pair_ident + size_t(j) * cnt,
+                               size_t(cnt) * sizeof(int), cudaMemcpyDeviceToDevice, s));
     if (nsides == 2) launch_merge_status(st, cnt, g.d_status + s0, s);
     pt.mark("eigh");
     for (int j = 0; j < nsides; ++j) {
@@ -1175,6 +1193,12 @@ void launch_refreshes(asg_blockset* bs) {
             }
             CK(cudaMemcpyAsync(g.h_status + s0, g.d_status + s0, size_t(cnt) * sizeof(int), cudaMemcpyDeviceToHost,
                                bs->side));
+            if (g.d_identL) {
+                CK(cudaMemcpyAsync(g.h_identL + s0, g.d_identL + s0, size_t(cnt) * sizeof(int), cudaMemcpyDeviceToHost,
+                                   bs->side));
+                CK(cudaMemcpyAsync(g.h_identR + s0, g.d_identR + s0, size_t(cnt) * sizeof(int), cudaMemcpyDeviceToHost,
+                                   bs->side));
+            }
             for (int k = 0; k < cnt; ++k) {
                 Unit& u = bs->units[size_t(g.units[size_t(s0 + k)])];
                 CK(cudaEventRecord(u.done, bs->side));
@@ -1372,9 +1396,28 @@ void run_deferred_installs(asg_blockset* bs) {
     todo.swap(bs->deferred_installs);
     for (int idx : todo) install_wait(bs, bs->units[size_t(idx)]);
     if (f32_refresh(bs) && is_soap(bs)) {
-        // batched: contiguous slot runs of one group, in workspace-sized chunks
-        std::vector<std::pair<int, int>> gs;
-        for (int idx : todo) gs.emplace_back(bs->units[size_t(idx)].group, bs->units[size_t(idx)].slot);
+        // batched: contiguous slot runs of one group, in workspace-sized chunks.
+        // Blocks whose refresh left J = I on both sides (warm, nothing to rotate)
+        // only take the new eigenvalues: basis and moments are unchanged.
+        std::vector<std::pair<int, int>> gs, triv;
+        for (int idx : todo) {
+            const Unit& u = bs->units[size_t(idx)];
+            const Group& g = bs->groups[size_t(u.group)];
+            const bool trivial = g.h_identL && g.h_identL[u.slot] && g.h_identR[u.slot];
+            (trivial ? triv : gs).emplace_back(u.group, u.slot);
+        }
+        std::sort(triv.begin(), triv.end());
+        for (size_t i = 0; i < triv.size();) {
+            size_t j = i + 1;
+            while (j < triv.size() && triv[j].first == triv[i].first && triv[j].second == triv[j - 1].second + 1) ++j;
+            Group& g = bs->groups[size_t(triv[i].first)];
+            const int s0 = triv[i].second, cnt = int(j - i);
+            CK(cudaMemcpyAsync(at(g.valsL, size_t(g.m), s0), at(g.svalsL, size_t(g.m), s0), size_t(cnt) * g.m * 8,
+                               cudaMemcpyDeviceToDevice, bs->main));
+            CK(cudaMemcpyAsync(at(g.valsR, size_t(g.n), s0), at(g.svalsR, size_t(g.n), s0), size_t(cnt) * g.n * 8,
+                               cudaMemcpyDeviceToDevice, bs->main));
+            i = j;
+        }
         std::sort(gs.begin(), gs.end());
         size_t i = 0;
         while (i < gs.size()) {
