@@ -266,6 +266,35 @@ void launch_sqnorm(const float* x, int64_t rows, int64_t cols, int64_t ld, doubl
     count_launch();
 }
 
+// Multi-tensor sum of squares: one CTA per chunk of one tensor.
+__global__ void sqnorm_multi_kernel(const SqChunk* __restrict__ chunks, double* acc, int* flag) {
+    const SqChunk c = chunks[blockIdx.x];
+    double s = 0.0;
+    bool bad = false;
+    for (int64_t e = c.e0 + threadIdx.x; e < c.e1; e += blockDim.x) {
+        const float v = c.x[(e / c.cols) * c.ld + (e % c.cols)];
+        bad |= !isfinite(v);
+        s += double(v) * double(v);
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+    __shared__ double red[32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = s;
+    __syncthreads();
+    if (w == 0) {
+        s = (l < int(blockDim.x >> 5)) ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+        if (l == 0) atomicAdd(acc, s);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, 1);
+}
+
+void launch_sqnorm_multi(const SqChunk* chunks, int count, double* acc, int* flag, cudaStream_t s) {
+    if (count <= 0) return;
+    sqnorm_multi_kernel<<<count, 256, 0, s>>>(chunks, acc, flag);
+    count_launch();
+}
+
 __global__ void clip_scale_kernel(const double* sq, double clip, float* out) {
     const double norm = sqrt(*sq);
     *out = (norm <= clip || norm == 0.0) ? 1.f : float(clip / norm);

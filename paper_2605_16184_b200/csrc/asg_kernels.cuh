@@ -62,6 +62,12 @@ void launch_identity_f32(float* a, int nb, int M, int m, float diag, cudaStream_
 // non-finite flag.
 void launch_sqnorm(const float* x, int64_t rows, int64_t cols, int64_t ld, double* acc, int* flag,
                    cudaStream_t s);
+// Multi-tensor variant: one CTA per chunk [e0, e1) of a strided 2-D tensor.
+struct SqChunk {
+    const float* x;
+    int64_t ld, cols, e0, e1;
+};
+void launch_sqnorm_multi(const SqChunk* chunks, int count, double* acc, int* flag, cudaStream_t s);
 // clip scale from the accumulated squared norm (harness.cpp:219-223).
 void launch_clip_scale(const double* sqnorm, double clip_norm, float* scale_out, cudaStream_t s);
 // AdamW + apply for a 1-D/degenerate parameter (precond.cpp:229-251).

@@ -252,6 +252,9 @@ struct asg_blockset {
     asg::BlockRef* d_ref1 = nullptr;
     asg::ApplyEntry* d_apply1 = nullptr;
     float* d_out1 = nullptr;
+    // multi-tensor gradient-norm chunks (every parameter)
+    asg::SqChunk* d_sq = nullptr;
+    int n_sq = 0;
     // multi-tensor AdamW table (owned 1-D / degenerate parameters)
     asg::AdamEntry* d_adam = nullptr;
     int n_adam = 0;
@@ -701,6 +704,22 @@ void build_owner_layout(asg_blockset* bs) {
     up(bs->d_gpack_offs, gpko);
     up(bs->d_gunpack_refs, gupk);
     up(bs->d_gunpack_offs, gupko);
+}
+
+// (Re)builds the chunk table of the one-launch global gradient norm.
+void build_sq_table(asg_blockset* bs) {
+    constexpr int64_t kChunkElems = 1 << 16;
+    std::vector<SqChunk> t;
+    for (const asg_param_desc& d : bs->params) {
+        if (!d.grad) continue;
+        const int64_t n = d.rows * d.cols;
+        for (int64_t e = 0; e < n; e += kChunkElems) t.push_back({d.grad, d.ld_grad, d.cols, e, std::min(n, e + kChunkElems)});
+    }
+    if (bs->d_sq && int(t.size()) > bs->n_sq) throw Fail{ASG_ERR_SHAPE_MISMATCH, "gradient chunk table grew"};
+    bs->n_sq = int(t.size());
+    if (t.empty()) return;
+    if (!bs->d_sq) bs->d_sq = dalloc<SqChunk>(bs, t.size());
+    h2d(bs->d_sq, t.data(), t.size() * sizeof(SqChunk), bs->main);
 }
 
 // (Re)builds the device table of the multi-tensor AdamW launch.
@@ -1757,6 +1776,7 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
             }
         }
         build_adam_table(bs);
+        build_sq_table(bs);
         bs->d_flag = dalloc<int>(bs, 1);
         bs->d_sqnorm = dalloc<double>(bs, 1);
         bs->d_scale = dalloc<float>(bs, 1);
@@ -1816,6 +1836,7 @@ int asg_blockset_bind_params(asg_blockset* bs, const asg_param_desc* params, int
         bs->params.assign(params, params + n_params);
         for (Group& g : bs->groups) bind_group_tables(bs, g);
         build_adam_table(bs);
+        build_sq_table(bs);
         build_owner_layout(bs);
     });
 }
@@ -1872,7 +1893,7 @@ int asg_grad_sqnorm(asg_blockset* bs, void* stream, double* sqnorm, int32_t* non
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
         CK(cudaMemsetAsync(bs->d_sqnorm, 0, sizeof(double), s));
         CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), s));
-        for (const asg_param_desc& d : bs->params) launch_sqnorm(d.grad, d.rows, d.cols, d.ld_grad, bs->d_sqnorm, bs->d_flag, s);
+        launch_sqnorm_multi(bs->d_sq, bs->n_sq, bs->d_sqnorm, bs->d_flag, s);  // every parameter, one launch
         double v = 0.0;
         int f = 0;
         CK(cudaMemcpyAsync(&v, bs->d_sqnorm, sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -133,3 +133,17 @@ def test_config_json_rules(rt):
     # unknown keys/sections are ignored (read_if, config.cpp:12-15); gpu section is additive
     o, s, prec = rt.config_from_json('{"task": {"kind": "x"}, "gpu": {"precision": "tf32", "install_mode": "event"}}')
     assert prec == abi.PREC_TF32 and s.install_mode == abi.INSTALL_EVENT
+
+
+def test_config_json_gpu_section(rt):
+    """The additive "gpu" section: precision, install mode, refresh mode."""
+    from paper_2605_16184_b200 import abi
+    doc = '{"optimizer": {"method": "SOAP", "precondition_frequency": 4}, "async": {"staleness_S": 2}, ' \
+          '"gpu": {"precision": "tf32", "install_mode": "event", "refresh": "f32"}}'
+    o, s, p = rt.config_from_json(doc)
+    assert o.method == abi.SOAP and o.precondition_frequency == 4 and s.pf == 4 and s.staleness_S == 2
+    assert p == abi.PREC_TF32 and s.install_mode == abi.INSTALL_EVENT and s.refresh_mode == abi.REFRESH_F32
+    o, s, p = rt.config_from_json('{"optimizer": {"method": "Shampoo"}}')
+    assert p == abi.PREC_3XTF32 and s.refresh_mode == abi.REFRESH_F64  # defaults: reference-tight
+    with pytest.raises(abi.ConfigInvalidError):
+        rt.config_from_json('{"optimizer": {"method": "SOAP"}, "gpu": {"refresh": "f16"}}')

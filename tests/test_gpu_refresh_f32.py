@@ -192,3 +192,29 @@ def test_tf32_mode_trajectory_runs_and_tracks_the_oracle(method):
                          refresh_mode=abi.REFRESH_F32, r_scale=(100.0 if method == abi.SOAP else 100.0))
     assert o.stats().installed >= 2 * 7
     assert max(errs) <= 1.0, errs
+
+
+@pytest.mark.parametrize("method", [abi.SOAP, abi.SHAMPOO])
+def test_f32_refresh_rank_deficient_factor(P, method):
+    """A 256 x 96 block: L = sum G G^T has rank <= 96 of 256 (the GPT-2 768 x 256
+    shape class). The F32 refresh must stay finite, return an orthonormal basis,
+    clamp the numerically-zero eigenvalues at the fp32 noise level (no NotPsd,
+    scale_columns_split) and agree with the oracle on the nonzero spectrum."""
+    cfg = P.defaults_for(method)
+    m, n = 256, 96
+    b = P.PrecondBlock(m, n, method, cfg, sched=f32_sched())
+    for s in range(2):
+        P.accumulate_factors(b, orc.random_matrix(m, n, 600 + s), cfg)
+    P.refresh_inverse(b, cfg, 0)
+    P.refresh_inverse(b, cfg, 1)  # warm
+    o = oracle_from(b, method, cfg, 1)
+    if method == abi.SOAP:
+        q = b.basis_l
+        assert np.isfinite(q).all()
+        assert np.abs(q.T @ q - np.eye(m)).max() < 1e-5
+        lam, lam_o = b.get(abi.EIGVALS_L), o.get(abi.EIGVALS_L)
+        top = lam_o > 1e-3 * lam_o.max()
+        assert np.abs(lam[top] - lam_o[top]).max() < 5e-6 * lam_o.max()
+    else:
+        assert np.isfinite(b.inv_l).all() and np.isfinite(b.inv_r).all()
+        assert rel(b.inv_r, o.inv_r) < 2e-5  # R is full rank
