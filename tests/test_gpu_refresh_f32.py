@@ -199,7 +199,8 @@ def test_f32_refresh_rank_deficient_factor(P, method):
     """A 256 x 96 block: L = sum G G^T has rank <= 96 of 256 (the GPT-2 768 x 256
     shape class). The F32 refresh must stay finite, return an orthonormal basis,
     clamp the numerically-zero eigenvalues at the fp32 noise level (no NotPsd,
-    scale_columns_split) and agree with the oracle on the nonzero spectrum."""
+    scale_columns_split) and agree with the oracle / LAPACK on the nonzero
+    spectrum."""
     cfg = P.defaults_for(method)
     m, n = 256, 96
     b = P.PrecondBlock(m, n, method, cfg, sched=f32_sched())
@@ -207,8 +208,8 @@ def test_f32_refresh_rank_deficient_factor(P, method):
         P.accumulate_factors(b, orc.random_matrix(m, n, 600 + s), cfg)
     P.refresh_inverse(b, cfg, 0)
     P.refresh_inverse(b, cfg, 1)  # warm
-    o = oracle_from(b, method, cfg, 1)
     if method == abi.SOAP:
+        o = oracle_from(b, method, cfg, 1)
         q = b.basis_l
         assert np.isfinite(q).all()
         assert np.abs(q.T @ q - np.eye(m)).max() < 1e-5
@@ -216,5 +217,14 @@ def test_f32_refresh_rank_deficient_factor(P, method):
         top = lam_o > 1e-3 * lam_o.max()
         assert np.abs(lam[top] - lam_o[top]).max() < 5e-6 * lam_o.max()
     else:
+        # The fp32 factor's null space carries eigenvalues of either sign at the
+        # rounding level; the reference (densela.hpp:274-278) would throw
+        # NotPsd on it under its 1e-8 relative damping. The GPU clamps that band
+        # to zero (scale_columns_split) and returns finite roots. R is full rank:
+        # compare it with numpy on the same fp32 factor.
         assert np.isfinite(b.inv_l).all() and np.isfinite(b.inv_r).all()
-        assert rel(b.inv_r, o.inv_r) < 2e-5  # R is full rank
+        r = b.factor_r
+        w, v = np.linalg.eigh(r)
+        eps = cfg.damping * np.trace(r) / n
+        ref = (v * (w + eps) ** -0.25) @ v.T
+        assert rel(b.inv_r, ref) < 2e-5
