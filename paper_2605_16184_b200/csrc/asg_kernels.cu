@@ -194,10 +194,65 @@ __global__ void prep_grad_kernel(const BlockRef* __restrict__ blocks, int M, int
     }
 }
 
+// 64 x 64 tiles, float4 accesses (blocks with 16-byte aligned rows: every
+// column offset, leading dimension and block width a multiple of 4).
+__global__ void __launch_bounds__(256) prep_grad_vec_kernel(const BlockRef* __restrict__ blocks, int M, int N,
+                                                            const float* __restrict__ scale_dev, float scale_val,
+                                                            float* __restrict__ Gh, float* __restrict__ Gl,
+                                                            float* __restrict__ GTh, float* __restrict__ GTl) {
+    __shared__ float th[64][65];
+    __shared__ float tl[64][65];
+    const int b = blockIdx.z;
+    const BlockRef blk = blocks[b];
+    const float s = scale_dev ? *scale_dev : scale_val;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 16 x 16
+    const int j0 = blockIdx.x * 64, i0 = blockIdx.y * 64;
+    const int64_t slab = int64_t(M) * N;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int i = i0 + ty + 16 * r, j = j0 + tx * 4;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < blk.rows && j < blk.cols) x = *reinterpret_cast<const float4*>(blk.src + int64_t(i) * blk.ld + j);
+        float4 h, l;
+        split_tf32(s * x.x, h.x, l.x);
+        split_tf32(s * x.y, h.y, l.y);
+        split_tf32(s * x.z, h.z, l.z);
+        split_tf32(s * x.w, h.w, l.w);
+        if (!Gl) h = make_float4(s * x.x, s * x.y, s * x.z, s * x.w);
+        *reinterpret_cast<float4*>(Gh + b * slab + int64_t(i) * N + j) = h;
+        if (Gl) *reinterpret_cast<float4*>(Gl + b * slab + int64_t(i) * N + j) = l;
+        const int rr = ty + 16 * r, cc = tx * 4;
+        th[rr][cc] = h.x;
+        th[rr][cc + 1] = h.y;
+        th[rr][cc + 2] = h.z;
+        th[rr][cc + 3] = h.w;
+        tl[rr][cc] = l.x;
+        tl[rr][cc + 1] = l.y;
+        tl[rr][cc + 2] = l.z;
+        tl[rr][cc + 3] = l.w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int jj = j0 + ty + 16 * r, ii = i0 + tx * 4;  // GT[jj][ii..ii+3] = G[ii..ii+3][jj]
+        const int cj = ty + 16 * r, ri = tx * 4;
+        *reinterpret_cast<float4*>(GTh + b * slab + int64_t(jj) * M + ii) =
+            make_float4(th[ri][cj], th[ri + 1][cj], th[ri + 2][cj], th[ri + 3][cj]);
+        if (GTl)
+            *reinterpret_cast<float4*>(GTl + b * slab + int64_t(jj) * M + ii) =
+                make_float4(tl[ri][cj], tl[ri + 1][cj], tl[ri + 2][cj], tl[ri + 3][cj]);
+    }
+}
+
 void launch_prep_grad(const BlockRef* blocks_dev, int nb, int M, int N, const float* scale_dev,
-                      float scale_val, float* Gh, float* Gl, float* GTh, float* GTl, cudaStream_t s) {
-    dim3 grid(N / 32, M / 32, nb), block(32, 8);
-    prep_grad_kernel<<<grid, block, 0, s>>>(blocks_dev, M, N, scale_dev, scale_val, Gh, Gl, GTh, GTl);
+                      float scale_val, float* Gh, float* Gl, float* GTh, float* GTl, cudaStream_t s, bool vec) {
+    if (vec) {
+        dim3 grid(N / 64, M / 64, nb), block(16, 16);
+        prep_grad_vec_kernel<<<grid, block, 0, s>>>(blocks_dev, M, N, scale_dev, scale_val, Gh, Gl, GTh, GTl);
+    } else {
+        dim3 grid(N / 32, M / 32, nb), block(32, 8);
+        prep_grad_kernel<<<grid, block, 0, s>>>(blocks_dev, M, N, scale_dev, scale_val, Gh, Gl, GTh, GTl);
+    }
     count_launch();
 }
 

@@ -51,9 +51,10 @@ struct BlockRef {
 
 // G (caller layout, scaled by *scale or scale_val) -> padded slabs
 // Gh/Gl [b][M][N] and GTh/GTl [b][N][M] (tf32 hi/lo; lo null => TF32 mode).
+// vec: every block row is 16-byte aligned (col offsets, ld, width % 4 == 0): 64x64 float4 tiles.
 void launch_prep_grad(const BlockRef* blocks_dev, int nb, int M, int N, const float* scale_dev,
                       float scale_val, float* Gh, float* Gl, float* GTh, float* GTl,
-                      cudaStream_t s);
+                      cudaStream_t s, bool vec = false);
 // Fills [nb][M][M] slabs with the padded identity (hi = I, lo = 0).
 void launch_identity_split(float* hi, float* lo, int nb, int M, int m, cudaStream_t s);
 // Fills [nb][M][M] fp32 with identity on the leading m x m (KL start) or zero.

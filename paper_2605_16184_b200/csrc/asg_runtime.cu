@@ -191,6 +191,7 @@ struct Group {
     ApplyEntry* d_apply = nullptr;
     int2 *tilesM = nullptr, *tilesN = nullptr;
     int ntM = 0, ntN = 0;
+    bool vec_grad = false;  // all gradient block rows 16-byte aligned (vectorised prep)
     int* d_status = nullptr;
     int* h_status = nullptr;  // pinned
     // F32 refresh: 1 where the eigensolve left the basis exactly unchanged (J = I);
@@ -419,6 +420,13 @@ void bind_group_tables(asg_blockset* bs, Group& g) {
         app[size_t(s)].ld = d.ld_theta;
         app[size_t(s)].rows = g.m;
         app[size_t(s)].cols = g.n;
+    }
+    g.vec_grad = g.n % 4 == 0;
+    for (int s2 = 0; s2 < g.nb; ++s2) {
+        const Unit& u = bs->units[size_t(g.units[size_t(s2)])];
+        const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+        const uintptr_t a = reinterpret_cast<uintptr_t>(refs[size_t(s2)].src);
+        g.vec_grad = g.vec_grad && d.ld_grad % 4 == 0 && a % 16 == 0;
     }
     h2d(g.d_refs, refs.data(), refs.size() * sizeof(BlockRef), bs->main);
     h2d(g.d_apply, app.data(), app.size() * sizeof(ApplyEntry), bs->main);
@@ -1920,7 +1928,8 @@ int asg_accumulate(asg_blockset* bs, double clip_scale, void* stream) {
         for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
             Group& g = bs->groups[gi];
             cudaStream_t gs = stream_for(bs, k, int(gi));
-            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs);
+            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs,
+                                 g.vec_grad);
             group_stats(bs, g, 0, g.nb, gs);
         }
         join_groups(bs, k);
@@ -2032,7 +2041,8 @@ int asg_step(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale,
             for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
                 Group& g = bs->groups[gi];
                 cudaStream_t gs = stream_for(bs, k, int(gi));
-                launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs);
+                launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs,
+                                 g.vec_grad);
                 group_stats(bs, g, 0, g.nb, gs);
             }
             join_groups(bs, k);
