@@ -42,25 +42,29 @@ def _run(rank, world, steps):
     return [p.cpu().numpy() for p in params], [o.block_info(i).owner_rank for i in range(o.num_blocks)]
 
 
-def _worker(rank, world, port, steps, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
+def _init(rank, world, store):
+    """gloo through a FileStore (no TCP port to race for between tests)."""
     import torch.distributed as dist
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=f"file://{store}", rank=rank, world_size=world)
+
+
+def _worker(rank, world, store, steps, q):
+    import torch.distributed as dist
+    _init(rank, world, store)
     out, owners = _run(rank, world, steps)
     q.put((rank, out, owners))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_ranks_match_single_rank():
+def test_two_ranks_match_single_rank(tmp_path):
     import torch.multiprocessing as mp
     steps = 5
     ref, _ = _run(0, 1, steps)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, steps, q)) for r in range(2)]
+    store = str(tmp_path / "store")
+    procs = [ctx.Process(target=_worker, args=(r, 2, store, steps, q)) for r in range(2)]
     for p in procs:
         p.start()
     results = {}
@@ -111,25 +115,23 @@ def _dp_run(rank, world, steps):
     return [p.cpu().numpy() for p in params], norms
 
 
-def _dp_worker(rank, world, port, steps, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
+def _dp_worker(rank, world, store, steps, q):
     import torch.distributed as dist
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _init(rank, world, store)
     out, norms = _dp_run(rank, world, steps)
     q.put((rank, out, norms))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_reduce_scatter_grads_matches_averaged_single_rank():
+def test_reduce_scatter_grads_matches_averaged_single_rank(tmp_path):
     import torch.multiprocessing as mp
     steps = 4
     ref, ref_norms = _dp_run(0, 1, steps)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, steps, q)) for r in range(2)]
+    store = str(tmp_path / "store")
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, store, steps, q)) for r in range(2)]
     for p in procs:
         p.start()
     results = {}
