@@ -6,14 +6,16 @@
 //
 // Both operands are K-major (row-major with K contiguous), staged by TMA into
 // 128B-swizzled shared memory, multiplied by tcgen05.mma kind::tf32 into an
-// fp32 accumulator in TMEM, and drained by four epilogue warps with
+// fp32 accumulator in TMEM, and drained by eight epilogue warps with
 // tcgen05.ld. Precision: NPASS=1 is plain TF32; NPASS=3 is 3xTF32, where every
 // operand is given as an exact (hi, lo) tf32 pair and the kernel accumulates
 // hi*hi + hi*lo + lo*hi — fp32-faithful products (relative error ~2^-21).
 //
 // Persistent: one CTA per SM loops over output tiles (128 x BN). Warp roles:
 //   warp 0: TMA producer      warp 1: MMA issuer + TMEM owner
-//   warps 2-5: epilogue (TMEM lane quadrant = warp % 4)
+//   warps 2-9: epilogue (TMEM lane quadrant = warp % 4; the two warps of a
+//              quadrant split the tile's 32-column chunks, doubling the
+//              memory parallelism of the fused epilogues)
 // Pipelines: smem stages full/empty (TMA <-> MMA) and a double-buffered TMEM
 // accumulator tfull/tempty (MMA <-> epilogue), so tile t's epilogue overlaps
 // tile t+1's MMAs.
@@ -77,8 +79,10 @@ struct GemmCfg {
     static constexpr uint32_t kBBytes = BN * BK * 4;
     static constexpr uint32_t kStageBytes = (kABytes + kBBytes) * (kSplit ? 2 : 1);
     // per-epilogue-warp 32 x 33 fp32 transpose scratch (coalesced apply)
-    static constexpr uint32_t kScratchBytes = 4 * 32 * 33 * 4;
-    static constexpr int kStagesRaw = (198 * 1024) / kStageBytes;
+    static constexpr int kEpiWarps = 8;
+    static constexpr int kThreads = 32 * (2 + kEpiWarps);
+    static constexpr uint32_t kScratchBytes = kEpiWarps * 32 * 33 * 4;
+    static constexpr int kStagesRaw = (194 * 1024) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
     static constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + 256 + kScratchBytes;
@@ -307,31 +311,34 @@ __device__ __forceinline__ void adam_chunk(const GemmParams& p, int b, int row0,
     const int c = col0 + int(lane);
     float* mm = p.mom_m + int64_t(b) * p.m_bstride + int64_t(row0) * p.ldm + c;
     float* vv = p.mom_v + int64_t(b) * p.m_bstride + int64_t(row0) * p.ldm + c;
-    float mv[32], vvv[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        mv[i] = __ldcs(mm + int64_t(i) * p.ldm);
-        vvv[i] = __ldcs(vv + int64_t(i) * p.ldm);
-    }
     float* dh = p.Dhi + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c;
     float* dl = p.Dlo ? p.Dlo + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c : nullptr;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const float g = scratch[i][lane];
-        const float m = p.b1 * mv[i] + (1.f - p.b1) * g;
-        const float v = p.b2 * vvv[i] + (1.f - p.b2) * (g * g);
-        __stcs(mm + int64_t(i) * p.ldm, m);
-        __stcs(vv + int64_t(i) * p.ldm, v);
-        float h, l;
-        split_tf32((m * p.inv_bc1) / (sqrtf(v * p.inv_bc2) + p.adam_eps), h, l);
-        __stcs(dh + int64_t(i) * p.ldd, h);
-        if (dl) __stcs(dl + int64_t(i) * p.ldd, l);
+    for (int h0 = 0; h0 < 32; h0 += 16) {  // two halves of 16 rows: 32 loads in flight per lane
+        float mv[16], vvv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            mv[i] = __ldcs(mm + int64_t(h0 + i) * p.ldm);
+            vvv[i] = __ldcs(vv + int64_t(h0 + i) * p.ldm);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float g = scratch[h0 + i][lane];
+            const float m = p.b1 * mv[i] + (1.f - p.b1) * g;
+            const float v = p.b2 * vvv[i] + (1.f - p.b2) * (g * g);
+            __stcs(mm + int64_t(h0 + i) * p.ldm, m);
+            __stcs(vv + int64_t(h0 + i) * p.ldm, v);
+            float h, l;
+            split_tf32((m * p.inv_bc1) / (sqrtf(v * p.inv_bc2) + p.adam_eps), h, l);
+            __stcs(dh + int64_t(h0 + i) * p.ldd, h);
+            if (dl) __stcs(dl + int64_t(h0 + i) * p.ldd, l);
+        }
     }
     __syncwarp();
 }
 
 template <int BN, int NPASS, int EPI>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                    const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
                    const __grid_constant__ GemmParams p) {
@@ -350,7 +357,7 @@ __global__ void __launch_bounds__(192, 1)
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
     float (*scratch)[33] = reinterpret_cast<float (*)[33]>(smem + size_t(STAGES) * Cfg::kStageBytes + 256 +
-                                                           size_t(warp & 3) * 32 * 33 * 4);
+                                                           size_t(warp >= 2 ? warp - 2 : 0) * 32 * 33 * 4);
 
     auto a_hi = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes; };
     auto a_lo = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes + Cfg::kABytes; };
@@ -375,7 +382,7 @@ __global__ void __launch_bounds__(192, 1)
             }
             for (int a = 0; a < 2; ++a) {
                 mbar_init(&tfull[a], 1);
-                mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+                mbar_init(&tempty[a], Cfg::kEpiWarps);  // one arrive per epilogue warp
             }
             fence_mbar_init();
         }
@@ -452,7 +459,8 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
     } else {
-        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        const int q = warp & 3;           // TMEM lane quadrant this warp may access
+        const int half = (warp - 2) >> 2;  // which of the quadrant's two warps: even / odd column chunks
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -462,7 +470,7 @@ __global__ void __launch_bounds__(192, 1)
             tc_fence_after();
             const int row = tm * BM + q * 32 + int(lane);
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half; c < BN / 32; c += 2) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32), r);
                 tmem_ld_wait();

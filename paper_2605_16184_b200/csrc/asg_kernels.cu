@@ -81,7 +81,7 @@ cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUte
     }
     const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
     if (grid <= 0) return cudaSuccess;
-    gemm_tn_kernel<BN, NPASS, EPI><<<grid, 192, Cfg::kSmemBytes, s>>>(ah, al, bh, bl, p);
+    gemm_tn_kernel<BN, NPASS, EPI><<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(ah, al, bh, bl, p);
     count_launch();
     return cudaGetLastError();
 }
