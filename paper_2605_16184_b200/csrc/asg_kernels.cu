@@ -122,7 +122,11 @@ int gemm_sym_tile_list(int n, int bn, int2* out) {
 cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStream_t stream) {
     const int M = g.A.rows, N = g.B.rows, K = g.A.K;
     if (M % 128 || N % 128 || K % 32 || g.B.K != K) return cudaErrorInvalidValue;
-    const int bn = gemm_bn_for(N);
+    int bn = gemm_bn_for(N);
+    // Small rectangular problems: 128-wide tiles when 256-wide ones would not
+    // fill two waves of the persistent grid (symmetric schedules keep the tile
+    // width their tile lists were built for).
+    if (!g.sym_tiles && bn == 256 && int64_t(g.batch) * (M / 128) * (N / 256) < 2 * int64_t(num_sms)) bn = 128;
     const bool split = precision == ASG_PREC_3XTF32;
     CUtensorMap ah, al, bh, bl;
     if (!make_map(&ah, g.A.hi, K, M, g.batch, 128)) return cudaErrorInvalidValue;
