@@ -717,6 +717,11 @@ __global__ void __launch_bounds__(192, 1)
     }
 }
 
+__global__ void tj_fill_status_kernel(int* status, int nb, int code) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nb) status[b] = code;
+}
+
 // ---- convergence / loop / finish ------------------------------------------------------
 // Convergence test over the whole matrix (the pair kernels' skip rule applied
 // to every off-diagonal element): big[b] = 1 if some element of matrix b still
@@ -992,7 +997,7 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
               tj_map(&mJl, JPl, JP, JP, nb * ntiles, JP);
     if (!ok) {
         // tensor maps unavailable: report through every matrix's status (no silent fallback)
-        cudaMemsetAsync(status, 0xff, size_t(nb) * sizeof(int), s);
+        tj_fill_status_kernel<<<(nb + 127) / 128, 128, 0, s>>>(status, nb, ASG_ERR_CUDA);
         return;
     }
     const int debug = getenv("ASG_EIGH_DEBUG") != nullptr ? 1 : 0;

@@ -2610,6 +2610,6 @@ int asg_sym_eig_batched_f32(const float* A, double* values, float* vectors, int6
         CK(cudaStreamSynchronize(s));
         CK(cudaGetLastError());
         for (int v : st)
-            if (v != ASG_OK) throw Fail{v == -1 ? ASG_ERR_UNSUPPORTED : v, "sym_eig_batched_f32: a matrix failed"};
+            if (v != ASG_OK) throw Fail{v, "sym_eig_batched_f32: a matrix failed"};
     });
 }
