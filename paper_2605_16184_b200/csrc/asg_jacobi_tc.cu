@@ -950,7 +950,8 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
                    int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize, int* ident) {
     const int D = (n + JP - 1) / JP * JP;
     (void)D_in;  // B, J, J^T are [nb][D][D] with D = roundup(n, 128) (== the group's padded dim)
-    const bool wide = n >= kWidePairN;
+    static const int wide_n = getenv("ASG_TJ_WIDE_N") ? atoi(getenv("ASG_TJ_WIDE_N")) : kWidePairN;  // tuning
+    const bool wide = n >= wide_n;
     const int JW = wide ? 64 : 32;
     const int m = D / JW, npairs = m / 2, ntiles = D / JP;  // 128x128 J tiles per matrix
     const size_t DD = size_t(D) * D;
@@ -1172,7 +1173,8 @@ void launch_tc_eigh(const float* B, int D_in, double* values, float* Jh, float* 
                     int* ident) {
     // the apply kernel keeps every pair flag of a launch in shared memory
     const int D = (n + JP - 1) / JP * JP;
-    const int npairs = D / (n >= kWidePairN ? 64 : 32) / 2;
+    static const int wide_n = getenv("ASG_TJ_WIDE_N") ? atoi(getenv("ASG_TJ_WIDE_N")) : kWidePairN;
+    const int npairs = D / (n >= wide_n ? 64 : 32) / 2;
     const int sub = kMaxFlags / npairs;
     const size_t DD = size_t(D) * D;
     for (int b0 = 0; b0 < nb; b0 += sub) {
