@@ -212,9 +212,11 @@ class AsteriaOptimizer:
         if self._gather_buf is None:
             self._gather_send = torch.zeros(stride, dtype=torch.float32, device=self.device)
             self._gather_buf = torch.zeros(stride * self.world, dtype=torch.float32, device=self.device)
-        main = C.c_void_p(self.stream_handle)
-        check(lib.asg_pack_owned(self._h, C.c_void_p(self._gather_send.data_ptr()), main))
-        torch.cuda.current_stream(self.device).wait_stream(torch.cuda.ExternalStream(self.stream_handle))
+        # pack on the caller's stream once it has waited for the update: the
+        # buffers' zero-fill (and any caller work) is ordered before the pack
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_stream(torch.cuda.ExternalStream(self.stream_handle))
+        check(lib.asg_pack_owned(self._h, C.c_void_p(self._gather_send.data_ptr()), stream_arg(cur)))
         if dist.get_backend(group) == "nccl":
             dist.all_gather_into_tensor(self._gather_buf, self._gather_send, group=group)
         else:
