@@ -452,7 +452,11 @@ def main():
         for _ in range(args.steps):
             one_step(step)
             step += 1
-        e1.record(stream)
+        # the last all-gather runs on the caller's stream: end the region after it
+        cur = torch.cuda.current_stream(dev)
+        cur.wait_stream(stream)
+        e1.record(cur)
+        stream.wait_stream(cur)
         barrier()
         t_wall = time.perf_counter() - t_wall0
     ks = o.kernel_stats(reset=True)
@@ -542,7 +546,7 @@ def main():
         "e2e": e2e,
         "state_bytes": o.state_bytes(),
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         cb = cpu_baseline(wl)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
