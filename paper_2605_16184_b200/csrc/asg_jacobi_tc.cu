@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <tuple>
 
@@ -580,6 +581,8 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* xdone = bars + 8;    // MMA1 complete
     uint64_t* xready = bars + 9;   // X^T staged (4 epilogue warps)
     uint64_t* adone = bars + 10;   // MMA2 complete
+    uint64_t* xfree = bars + 11;   // TMEM cols [0,128) read out (4 epilogue warps)
+    uint64_t* afree = bars + 13;   // TMEM cols [128,256) read out (4 epilogue warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
     const int warp = threadIdx.x >> 5;
@@ -603,6 +606,8 @@ __global__ void __launch_bounds__(192, 1)
             mbar_init(xdone, 1);
             mbar_init(xready, 4);
             mbar_init(adone, 1);
+            mbar_init(xfree, 4);
+            mbar_init(afree, 4);
             fence_mbar_init();
         }
         __syncwarp();
@@ -623,10 +628,18 @@ __global__ void __launch_bounds__(192, 1)
     const int total = p.nb * (p.tilesA + p.tilesV);
     const int npairs = p.m / 2, ntiles = npairs / G;
 
-    // phase bits (per barrier), advanced identically by every role that waits on it
+    // Tiles are pipelined across the roles (no CTA-wide barrier per tile):
+    //   * the producer loads tile u+1's MMA1 operands while tile u's A' drains,
+    //     once region S no longer holds tile u's X^T (adone after an A tile);
+    //   * MMA1(u+1) writes TMEM cols [0,128) once the epilogue has read X(u)
+    //     (xfree); MMA2 writes cols [128,256) once A' of the previous A tile
+    //     has been read (afree).
+    // Every role walks the same tile sequence, so each tracks the phase of
+    // every barrier it waits on by counting.
     uint32_t ph_full1[2] = {0, 0}, ph_empty1[2] = {0, 0}, ph_full2[2] = {0, 0}, ph_empty2[2] = {0, 0};
-    uint32_t ph_x = 0, ph_xr = 0, ph_a = 0;
+    uint32_t ph_x = 0, ph_xr = 0, ph_a = 0, ph_xf = 0, ph_af = 0;
     int use1[2] = {0, 0}, use2[2] = {0, 0};  // producer: number of fills of each stage so far
+    bool prev_a = false, any_prev = false, a_seen = false;  // previous tile was A / exists; an A tile seen
 
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int b, i1, i2;
@@ -653,6 +666,10 @@ __global__ void __launch_bounds__(192, 1)
 
         if (warp == 0) {
             if (lane == 0) {
+                if (prev_a) {  // region S held the previous tile's X^T until its MMA2 completed
+                    mbar_wait(adone, ph_a);
+                    ph_a ^= 1;
+                }
                 // MMA1 operands: 4 K-chunks (pair-k2 columns), ring of 2 stages
                 for (int c = 0; c < 4; ++c) {
                     const int s = c & 1;
@@ -690,6 +707,11 @@ __global__ void __launch_bounds__(192, 1)
             }
         } else if (warp == 1) {
             if (lane == 0) {
+                if (any_prev) {  // the epilogue has read X of the previous tile
+                    mbar_wait(xfree, ph_xf);
+                    ph_xf ^= 1;
+                    tc_fence_after();
+                }
                 // MMA1: X = A_tile * J_k2 into TMEM cols [0, 128)
                 for (int c = 0; c < 4; ++c) {
                     const int s = c & 1;
@@ -712,6 +734,12 @@ __global__ void __launch_bounds__(192, 1)
                 if (isA) {
                     // MMA2: A' = J_k1^T X, B operand = X^T staged in region S
                     mbar_wait(xready, ph_xr);
+                    ph_xr ^= 1;
+                    if (a_seen) {  // A' of the previous A tile has been read out of cols [128, 256)
+                        mbar_wait(afree, ph_af);
+                        ph_af ^= 1;
+                    }
+                    a_seen = true;
                     tc_fence_after();
                     for (int c = 0; c < 4; ++c) {
                         const int s = c & 1;
@@ -738,6 +766,7 @@ __global__ void __launch_bounds__(192, 1)
             const int qd = warp & 3;  // TMEM lane quadrant: rows 32*qd .. 32*qd+31
             const int row = qd * 32 + int(lane);
             mbar_wait(xdone, ph_x);
+            ph_x ^= 1;
             tc_fence_after();
             if (isA) {
                 // X rows [32 qd, 32 qd + 32) = K-chunk qd of MMA2's B operand (X^T)
@@ -760,8 +789,12 @@ __global__ void __launch_bounds__(192, 1)
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(xready);
+                if (lane == 0) {
+                    mbar_arrive(xready);
+                    mbar_arrive(xfree);
+                }
                 mbar_wait(adone, ph_a);
+                ph_a ^= 1;
                 tc_fence_after();
                 // A' rows -> natural positions
                 const int gr = blk1[row / JW] * JW + row % JW;
@@ -785,6 +818,9 @@ __global__ void __launch_bounds__(192, 1)
                         *reinterpret_cast<float4*>(dl + j) = l4;
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(afree);
             } else {
                 const int gr = i1 * JP + row;
                 const int64_t base = int64_t(b) * p.D * p.D + int64_t(gr) * p.D;
@@ -807,18 +843,15 @@ __global__ void __launch_bounds__(192, 1)
                         *reinterpret_cast<float4*>(dl + j) = l4;
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(xfree);
             }
-            tc_fence_before();
         }
-        // every role has finished this tile (TMEM drained, smem operands consumed)
-        ph_x ^= 1;
-        if (isA) {
-            ph_xr ^= 1;
-            ph_a ^= 1;
-        }
-        __syncthreads();
-        tc_fence_after();
+        any_prev = true;
+        prev_a = isA;
     }
+    // the epilogue warps waited for every MMA of their last tile: TMEM is idle
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
@@ -1282,6 +1315,21 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
     }
     count_launch(4 + 2 * uint64_t(m - 1) + 2 + 2);
     cudaGraphLaunch(exec, s);
+    static const bool report = getenv("ASG_TJ_REPORT") != nullptr;  // diagnostics: sweeps per solve
+    if (report) {
+        std::vector<int> sw;
+        sw.resize(size_t(nb));
+        int loops = 0;
+        cudaMemcpyAsync(sw.data(), sweeps, size_t(nb) * sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&loops, loop_count, sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        int mx = 0, mn = 1 << 30;
+        for (int v : sw) {
+            mx = v > mx ? v : mx;
+            mn = v < mn ? v : mn;
+        }
+        fprintf(stderr, "tjreport n=%d nb=%d loops=%d sweeps min=%d max=%d\n", n, nb, loops, mn, mx);
+    }
     rayleigh(s);
 }
 }  // namespace
