@@ -50,10 +50,14 @@ constexpr int JP = 128;  // apply tile: 128/PW pairs of two JW-wide blocks
 // cheap, wide pairs halve the rounds (and the tensor-core work) per sweep.
 constexpr int kWidePairN = 1536;
 constexpr int kFewBig = 8;  // pair solves with at most this many large elements rotate them one by one
-// Pair-solve ordering: the odd-even ordering (one fused conflict-free pass per
-// round, measured 1.75x faster for PW = 128) for wide pairs; narrow pairs keep
-// the round-robin ordering, equally fast there and able to skip empty rounds.
-constexpr int kOddEvenWide = 1, kOddEvenNarrow = 0;
+// Pair-solve ordering: the odd-even ordering (one fused, conflict-free,
+// load-batched pass per round) for both widths -- measured 2.3x (PW = 128) and
+// 1.5x (PW = 64) faster than the round-robin ordering with separate row and
+// column passes, which stays available (ASG_TJ_OE=0) for comparison.
+constexpr int kOddEvenWide = 1, kOddEvenNarrow = 1;
+// fp32 rotation parameters in the odd-even pair solve (the serial part of each
+// round; 6% faster than fp64 at equal residuals): ASG_TJ_ROT32=0 selects fp64.
+constexpr int kRot32 = 1;
 constexpr int kInner = 1;  // inner sweeps of the pair solve (more outer sweeps are cheaper than inner ones)
 
 __device__ __forceinline__ int tourney(int pos, int r, int P) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (P - 1); }
@@ -352,16 +356,54 @@ __global__ void __launch_bounds__(NT) tj_pair_kernel(const float* __restrict__ A
                     swp[kk] = wrap ? 0 : 1;
                 }
                 __syncthreads();
-                // S: 2x2 blocks (ki, kj); a warp covers one ki and 32 consecutive kj
-                for (int e = threadIdx.x; e < (PW / 2) * (PW / 2); e += blockDim.x) {
+                // S: 2x2 blocks (ki, kj); a warp covers one ki and 32 consecutive kj.
+                // Every item of the thread is loaded before any is stored (the
+                // compiler cannot reorder shared loads past shared stores), so
+                // the round is one batch of independent loads, math, stores.
+                constexpr int SI = (PW / 2) * (PW / 2) / NT, ZI = PW * (PW / 2) / NT;
+                static_assert(SI * NT == (PW / 2) * (PW / 2) && ZI * NT == PW * (PW / 2), "thread count");
+                float q[SI][4];
+                int o0[SI], o1[SI];  // offsets of (r0, aj) and (r1, aj)
+                auto bcol = [&](int e) {  // offset of column bj relative to aj
+                    return (odd && e % (PW / 2) == PW / 2 - 1) ? -(PW - 1) : 1;
+                };
+#pragma unroll
+                for (int it = 0; it < SI; ++it) {
+                    const int e = threadIdx.x + it * NT;
                     const int ki = e / (PW / 2), kj = e % (PW / 2);
                     const int ai = 2 * ki + odd, bi = (odd && ki == PW / 2 - 1) ? 0 : ai + 1;
-                    const int aj = 2 * kj + odd, bj = (odd && kj == PW / 2 - 1) ? 0 : aj + 1;
-                    const int r0 = flip ? bi : ai, r1 = flip ? ai : bi;
-                    const float u0 = S[r0 * (PW + 1) + aj], u1 = S[r0 * (PW + 1) + bj];
-                    const float v0 = S[r1 * (PW + 1) + aj], v1 = S[r1 * (PW + 1) + bj];
-                    float s00 = flip ? v0 : u0, s01 = flip ? v1 : u1;
-                    float s10 = flip ? u0 : v0, s11 = flip ? u1 : v1;
+                    const int aj = 2 * kj + odd;
+                    o0[it] = (flip ? bi : ai) * (PW + 1) + aj;
+                    o1[it] = (flip ? ai : bi) * (PW + 1) + aj;
+                    const int bo = bcol(e);
+                    q[it][0] = S[o0[it]];
+                    q[it][1] = S[o0[it] + bo];
+                    q[it][2] = S[o1[it]];
+                    q[it][3] = S[o1[it] + bo];
+                }
+                // Z: column pairs; a warp covers two rows x 16 pairs (row stride PW+1: banks differ)
+                constexpr int ZH = ZI > 8 ? ZI / 2 : ZI;  // Z items per batch
+                auto zoff = [&](int e, int& kk, int& dc) {
+                    const int w = e >> 5, l = e & 31;
+                    const int row = 2 * (w / (PW / 32)) + (l >> 4);
+                    kk = (w % (PW / 32)) * 16 + (l & 15);
+                    dc = (odd && kk == PW / 2 - 1) ? -(PW - 1) : 1;
+                    return row * (PW + 1) + 2 * kk + odd;
+                };
+                float zq[ZH][2];
+#pragma unroll
+                for (int it = 0; it < ZH; ++it) {
+                    int kk, dc;
+                    const int zo = zoff(threadIdx.x + it * NT, kk, dc);
+                    zq[it][0] = Z[zo];
+                    zq[it][1] = Z[zo + dc];
+                }
+#pragma unroll
+                for (int it = 0; it < SI; ++it) {
+                    const int e = threadIdx.x + it * NT;
+                    const int ki = e / (PW / 2), kj = e % (PW / 2);
+                    float s00 = flip ? q[it][2] : q[it][0], s01 = flip ? q[it][3] : q[it][1];
+                    float s10 = flip ? q[it][0] : q[it][2], s11 = flip ? q[it][1] : q[it][3];
                     const float ci = cs[ki], si = sn[ki], cj = cs[kj], sj = sn[kj];
                     const float t00 = ci * s00 - si * s10, t01 = ci * s01 - si * s11;
                     const float t10 = si * s00 + ci * s10, t11 = si * s01 + ci * s11;
@@ -386,23 +428,34 @@ __global__ void __launch_bounds__(NT) tj_pair_kernel(const float* __restrict__ A
                         s10 = s11;
                         s11 = x;
                     }
-                    S[r0 * (PW + 1) + aj] = flip ? s10 : s00;
-                    S[r0 * (PW + 1) + bj] = flip ? s11 : s01;
-                    S[r1 * (PW + 1) + aj] = flip ? s00 : s10;
-                    S[r1 * (PW + 1) + bj] = flip ? s01 : s11;
+                    const int bo = bcol(e);
+                    S[o0[it]] = flip ? s10 : s00;
+                    S[o0[it] + bo] = flip ? s11 : s01;
+                    S[o1[it]] = flip ? s00 : s10;
+                    S[o1[it] + bo] = flip ? s01 : s11;
                 }
-                // Z: column pairs; a warp covers two rows x 16 pairs (row stride PW+1: banks differ)
-                for (int e = threadIdx.x; e < PW * (PW / 2); e += blockDim.x) {
-                    const int w = e >> 5, l = e & 31;
-                    const int row = 2 * (w / (PW / 32)) + (l >> 4);
-                    const int kk = (w % (PW / 32)) * 16 + (l & 15);
-                    const int a = 2 * kk + odd, c = (odd && kk == PW / 2 - 1) ? 0 : a + 1;
-                    const float x = Z[row * (PW + 1) + a], y = Z[row * (PW + 1) + c];
-                    const float cc = cs[kk], ss = sn[kk];
-                    const float na = cc * x - ss * y, nc = ss * x + cc * y;
-                    const bool s2 = swp[kk];
-                    Z[row * (PW + 1) + a] = s2 ? nc : na;
-                    Z[row * (PW + 1) + c] = s2 ? na : nc;
+#pragma unroll
+                for (int h = 0; h < ZI / ZH; ++h) {
+                    if (h > 0) {
+#pragma unroll
+                        for (int it = 0; it < ZH; ++it) {
+                            int kk, dc;
+                            const int zo = zoff(threadIdx.x + (h * ZH + it) * NT, kk, dc);
+                            zq[it][0] = Z[zo];
+                            zq[it][1] = Z[zo + dc];
+                        }
+                    }
+#pragma unroll
+                    for (int it = 0; it < ZH; ++it) {
+                        int kk, dc;
+                        const int zo = zoff(threadIdx.x + (h * ZH + it) * NT, kk, dc);
+                        const float x = zq[it][0], y = zq[it][1];
+                        const float cc = cs[kk], ss = sn[kk];
+                        const float na = cc * x - ss * y, nc = ss * x + cc * y;
+                        const bool s2 = swp[kk];
+                        Z[zo] = s2 ? nc : na;
+                        Z[zo + dc] = s2 ? na : nc;
+                    }
                 }
                 __syncthreads();
             }
@@ -1149,7 +1202,7 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
     const int inner = getenv("ASG_TJ_INNER") ? atoi(getenv("ASG_TJ_INNER")) : kInner;
     static const int oe_env = getenv("ASG_TJ_OE") ? atoi(getenv("ASG_TJ_OE")) : -1;  // tuning override
     const int oe = oe_env >= 0 ? oe_env : (wide ? kOddEvenWide : kOddEvenNarrow);
-    static const int rot32 = getenv("ASG_TJ_ROT32") ? atoi(getenv("ASG_TJ_ROT32")) : 0;     // tuning
+    static const int rot32 = getenv("ASG_TJ_ROT32") ? atoi(getenv("ASG_TJ_ROT32")) : kRot32;  // tuning
     static const int nt_wide = getenv("ASG_TJ_NT") ? atoi(getenv("ASG_TJ_NT")) : 512;      // tuning
     const int total_tiles = nb * (ap.tilesA + ap.tilesV);
     const int apply_grid = total_tiles < num_sms ? total_tiles : num_sms;
