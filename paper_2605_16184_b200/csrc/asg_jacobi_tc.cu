@@ -59,6 +59,10 @@ constexpr int kOddEvenWide = 1, kOddEvenNarrow = 1;
 // equal eigen-residuals, but the non-unit c^2+s^2 it leaves in the accumulated
 // rotations moved the KL-Shampoo F32 trajectory test 1.7x past its tolerance).
 constexpr int kRot32 = 0;
+#ifndef ASG_TJ_NARROW_CTAS
+#define ASG_TJ_NARROW_CTAS 4
+#endif
+constexpr int kNarrowPairCtas = ASG_TJ_NARROW_CTAS;  // resident narrow pair solves per SM (register cap)
 constexpr int kInner = 1;  // inner sweeps of the pair solve (more outer sweeps are cheaper than inner ones)
 
 __device__ __forceinline__ int tourney(int pos, int r, int P) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (P - 1); }
@@ -159,7 +163,7 @@ __global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const 
 // J^T into its diagonal 64x64 block of the quad tile (pairs 2g, 2g+1 share a
 // 128x128 tile; the off-diagonal blocks stay zero).
 template <int PW, int NT>
-__global__ void __launch_bounds__(NT) tj_pair_kernel(const float* __restrict__ Ah, const float* __restrict__ Al,
+__global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_kernel(const float* __restrict__ Ah, const float* __restrict__ Al,
                                                                int D, int m, int round, float* __restrict__ JTh,
                                                                float* __restrict__ JTl, int* __restrict__ pflag,
                                                                int* __restrict__ rotations,
@@ -319,10 +323,27 @@ __global__ void __launch_bounds__(NT) tj_pair_kernel(const float* __restrict__ A
     // access; the end state is a permutation of the eigenpairs, which the
     // ranking below absorbs. Odd rounds leave positions PW-1 and 0 idle; they
     // form the wrap "pair" k = PW/2-1 with the identity and no swap.
-    if (oe_order) {
+    if (oe_order && inner_sweeps > 0) {  // (a classical-path pair has already set inner_sweeps = 0)
         __shared__ unsigned char swp[PW / 2];
         const int lane = threadIdx.x & 31;
         const bool flip = lane & 16;  // half-warps take the two rows in opposite order (banks)
+        // Z lives in registers for the sweep: warp w owns rows [RPW w, RPW w + RPW),
+        // lane l owns columns [CPL l, CPL l + CPL). Even rounds pair columns
+        // inside a lane; odd rounds pair the lane's last column with the next
+        // lane's first (one shuffle each way).
+        // (wide pairs only: for PW = 64 the shuffle-per-odd-round layout measured
+        // 11% slower than the shared-memory Z pass below)
+        constexpr bool ZREG = PW == 128;
+        constexpr int CPL = PW / 32, RPW = ZREG ? PW / (NT / 32) : 1;
+        static_assert(CPL % 2 == 0 && (!ZREG || RPW * (NT / 32) == PW), "Z register layout");
+        const int zrow0 = (threadIdx.x >> 5) * RPW, zcol0 = lane * CPL;
+        float zr[RPW][CPL];
+        if constexpr (ZREG) {
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) zr[i][j] = (zrow0 + i == zcol0 + j) ? 1.f : 0.f;
+        }
         for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
             bool rot_any = false;
             for (int r = 0; r < PW; ++r) {
@@ -361,83 +382,82 @@ __global__ void __launch_bounds__(NT) tj_pair_kernel(const float* __restrict__ A
                 // Every item of the thread is loaded before any is stored (the
                 // compiler cannot reorder shared loads past shared stores), so
                 // the round is one batch of independent loads, math, stores.
-                constexpr int SI = (PW / 2) * (PW / 2) / NT, ZI = PW * (PW / 2) / NT;
-                static_assert(SI * NT == (PW / 2) * (PW / 2) && ZI * NT == PW * (PW / 2), "thread count");
-                float q[SI][4];
-                int o0[SI], o1[SI];  // offsets of (r0, aj) and (r1, aj)
+                constexpr int SI = (PW / 2) * (PW / 2) / NT;
+                constexpr int SB = SI > 4 ? 4 : SI;  // S items per load batch
+                static_assert(SI * NT == (PW / 2) * (PW / 2) && SI % SB == 0, "thread count");
                 auto bcol = [&](int e) {  // offset of column bj relative to aj
                     return (odd && e % (PW / 2) == PW / 2 - 1) ? -(PW - 1) : 1;
                 };
 #pragma unroll
-                for (int it = 0; it < SI; ++it) {
-                    const int e = threadIdx.x + it * NT;
-                    const int ki = e / (PW / 2), kj = e % (PW / 2);
-                    const int ai = 2 * ki + odd, bi = (odd && ki == PW / 2 - 1) ? 0 : ai + 1;
-                    const int aj = 2 * kj + odd;
-                    o0[it] = (flip ? bi : ai) * (PW + 1) + aj;
-                    o1[it] = (flip ? ai : bi) * (PW + 1) + aj;
-                    const int bo = bcol(e);
-                    q[it][0] = S[o0[it]];
-                    q[it][1] = S[o0[it] + bo];
-                    q[it][2] = S[o1[it]];
-                    q[it][3] = S[o1[it] + bo];
-                }
-                // Z: column pairs; a warp covers two rows x 16 pairs (row stride PW+1: banks differ)
-                constexpr int ZH = ZI > 8 ? ZI / 2 : ZI;  // Z items per batch
-                auto zoff = [&](int e, int& kk, int& dc) {
-                    const int w = e >> 5, l = e & 31;
-                    const int row = 2 * (w / (PW / 32)) + (l >> 4);
-                    kk = (w % (PW / 32)) * 16 + (l & 15);
-                    dc = (odd && kk == PW / 2 - 1) ? -(PW - 1) : 1;
-                    return row * (PW + 1) + 2 * kk + odd;
-                };
-                float zq[ZH][2];
+                for (int h = 0; h < SI / SB; ++h) {
+                    float q[SB][4];
+                    int o0[SB], o1[SB];  // offsets of (r0, aj) and (r1, aj)
 #pragma unroll
-                for (int it = 0; it < ZH; ++it) {
-                    int kk, dc;
-                    const int zo = zoff(threadIdx.x + it * NT, kk, dc);
-                    zq[it][0] = Z[zo];
-                    zq[it][1] = Z[zo + dc];
-                }
-#pragma unroll
-                for (int it = 0; it < SI; ++it) {
-                    const int e = threadIdx.x + it * NT;
-                    const int ki = e / (PW / 2), kj = e % (PW / 2);
-                    float s00 = flip ? q[it][2] : q[it][0], s01 = flip ? q[it][3] : q[it][1];
-                    float s10 = flip ? q[it][0] : q[it][2], s11 = flip ? q[it][1] : q[it][3];
-                    const float ci = cs[ki], si = sn[ki], cj = cs[kj], sj = sn[kj];
-                    const float t00 = ci * s00 - si * s10, t01 = ci * s01 - si * s11;
-                    const float t10 = si * s00 + ci * s10, t11 = si * s01 + ci * s11;
-                    s00 = cj * t00 - sj * t01;
-                    s01 = sj * t00 + cj * t01;
-                    s10 = cj * t10 - sj * t11;
-                    s11 = sj * t10 + cj * t11;
-                    if (ki == kj && si != 0.f) s01 = s10 = 0.f;  // the annihilated element
-                    if (swp[ki]) {  // swap the two rows' positions
-                        float x = s00;
-                        s00 = s10;
-                        s10 = x;
-                        x = s01;
-                        s01 = s11;
-                        s11 = x;
+                    for (int it = 0; it < SB; ++it) {
+                        const int e = threadIdx.x + (h * SB + it) * NT;
+                        const int ki = e / (PW / 2), kj = e % (PW / 2);
+                        const int ai = 2 * ki + odd, bi = (odd && ki == PW / 2 - 1) ? 0 : ai + 1;
+                        const int aj = 2 * kj + odd;
+                        o0[it] = (flip ? bi : ai) * (PW + 1) + aj;
+                        o1[it] = (flip ? ai : bi) * (PW + 1) + aj;
+                        const int bo = bcol(e);
+                        q[it][0] = S[o0[it]];
+                        q[it][1] = S[o0[it] + bo];
+                        q[it][2] = S[o1[it]];
+                        q[it][3] = S[o1[it] + bo];
                     }
-                    if (swp[kj]) {  // and the two columns'
-                        float x = s00;
-                        s00 = s01;
-                        s01 = x;
-                        x = s10;
-                        s10 = s11;
-                        s11 = x;
-                    }
-                    const int bo = bcol(e);
-                    S[o0[it]] = flip ? s10 : s00;
-                    S[o0[it] + bo] = flip ? s11 : s01;
-                    S[o1[it]] = flip ? s00 : s10;
-                    S[o1[it] + bo] = flip ? s01 : s11;
-                }
 #pragma unroll
-                for (int h = 0; h < ZI / ZH; ++h) {
-                    if (h > 0) {
+                    for (int it = 0; it < SB; ++it) {
+                        const int e = threadIdx.x + (h * SB + it) * NT;
+                        const int ki = e / (PW / 2), kj = e % (PW / 2);
+                        float s00 = flip ? q[it][2] : q[it][0], s01 = flip ? q[it][3] : q[it][1];
+                        float s10 = flip ? q[it][0] : q[it][2], s11 = flip ? q[it][1] : q[it][3];
+                        const float ci = cs[ki], si = sn[ki], cj = cs[kj], sj = sn[kj];
+                        const float t00 = ci * s00 - si * s10, t01 = ci * s01 - si * s11;
+                        const float t10 = si * s00 + ci * s10, t11 = si * s01 + ci * s11;
+                        s00 = cj * t00 - sj * t01;
+                        s01 = sj * t00 + cj * t01;
+                        s10 = cj * t10 - sj * t11;
+                        s11 = sj * t10 + cj * t11;
+                        if (ki == kj && si != 0.f) s01 = s10 = 0.f;  // the annihilated element
+                        if (swp[ki]) {  // swap the two rows' positions
+                            float x = s00;
+                            s00 = s10;
+                            s10 = x;
+                            x = s01;
+                            s01 = s11;
+                            s11 = x;
+                        }
+                        if (swp[kj]) {  // and the two columns'
+                            float x = s00;
+                            s00 = s01;
+                            s01 = x;
+                            x = s10;
+                            s10 = s11;
+                            s11 = x;
+                        }
+                        const int bo = bcol(e);
+                        S[o0[it]] = flip ? s10 : s00;
+                        S[o0[it] + bo] = flip ? s11 : s01;
+                        S[o1[it]] = flip ? s00 : s10;
+                        S[o1[it] + bo] = flip ? s01 : s11;
+                    }
+                }
+                // Z (registers): rotate + swap column pairs of the lane's rows
+                if constexpr (!ZREG) {
+                    // Z (shared): column pairs; a warp covers two rows x 16 pairs (row
+                    // stride PW+1: banks differ); batches of loads before stores
+                    constexpr int ZI = PW * (PW / 2) / NT, ZH = ZI > 8 ? ZI / 2 : ZI;
+                    auto zoff = [&](int e, int& kk, int& dc) {
+                        const int w = e >> 5, l = e & 31;
+                        const int row = 2 * (w / (PW / 32)) + (l >> 4);
+                        kk = (w % (PW / 32)) * 16 + (l & 15);
+                        dc = (odd && kk == PW / 2 - 1) ? -(PW - 1) : 1;
+                        return row * (PW + 1) + 2 * kk + odd;
+                    };
+#pragma unroll
+                    for (int h = 0; h < ZI / ZH; ++h) {
+                        float zq[ZH][2];
 #pragma unroll
                         for (int it = 0; it < ZH; ++it) {
                             int kk, dc;
@@ -445,22 +465,79 @@ __global__ void __launch_bounds__(NT) tj_pair_kernel(const float* __restrict__ A
                             zq[it][0] = Z[zo];
                             zq[it][1] = Z[zo + dc];
                         }
-                    }
 #pragma unroll
-                    for (int it = 0; it < ZH; ++it) {
-                        int kk, dc;
-                        const int zo = zoff(threadIdx.x + (h * ZH + it) * NT, kk, dc);
-                        const float x = zq[it][0], y = zq[it][1];
+                        for (int it = 0; it < ZH; ++it) {
+                            int kk, dc;
+                            const int zo = zoff(threadIdx.x + (h * ZH + it) * NT, kk, dc);
+                            const float x = zq[it][0], y = zq[it][1];
+                            const float cc = cs[kk], ss = sn[kk];
+                            const float na = cc * x - ss * y, nc = ss * x + cc * y;
+                            const bool s2 = swp[kk];
+                            Z[zo] = s2 ? nc : na;
+                            Z[zo + dc] = s2 ? na : nc;
+                        }
+                    }
+                } else if (!odd) {
+#pragma unroll
+                    for (int j = 0; j < CPL; j += 2) {
+                        const int kk = (zcol0 + j) >> 1;
                         const float cc = cs[kk], ss = sn[kk];
-                        const float na = cc * x - ss * y, nc = ss * x + cc * y;
                         const bool s2 = swp[kk];
-                        Z[zo] = s2 ? nc : na;
-                        Z[zo + dc] = s2 ? na : nc;
+#pragma unroll
+                        for (int i = 0; i < RPW; ++i) {
+                            const float x = zr[i][j], y = zr[i][j + 1];
+                            const float na = cc * x - ss * y, nc = ss * x + cc * y;
+                            zr[i][j] = s2 ? nc : na;
+                            zr[i][j + 1] = s2 ? na : nc;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 1; j + 1 < CPL; j += 2) {  // pairs inside the lane
+                        const int kk = (zcol0 + j - 1) >> 1;
+                        const float cc = cs[kk], ss = sn[kk];
+                        const bool s2 = swp[kk];
+#pragma unroll
+                        for (int i = 0; i < RPW; ++i) {
+                            const float x = zr[i][j], y = zr[i][j + 1];
+                            const float na = cc * x - ss * y, nc = ss * x + cc * y;
+                            zr[i][j] = s2 ? nc : na;
+                            zr[i][j + 1] = s2 ? na : nc;
+                        }
+                    }
+                    // pair (zcol0 + CPL - 1, zcol0 + CPL) spans lanes l, l+1; lane 31's is the
+                    // identity wrap pair (PW-1, 0), as is lane 0's incoming one
+                    const int kl = (zcol0 + CPL - 2) >> 1;        // pair whose first column is mine
+                    const int kr = (zcol0 - 2) >> 1;              // pair whose second column is mine
+                    const float cl = cs[kl], sl = sn[kl];
+                    const bool wl = swp[kl];
+                    const float crr = lane > 0 ? cs[kr] : 1.f, srr = lane > 0 ? sn[kr] : 0.f;
+                    const bool wr = lane > 0 ? swp[kr] : false;
+#pragma unroll
+                    for (int i = 0; i < RPW; ++i) {
+                        const float mine_last = zr[i][CPL - 1], mine_first = zr[i][0];
+                        const float from_right = __shfl_down_sync(0xffffffffu, mine_first, 1);
+                        const float from_left = __shfl_up_sync(0xffffffffu, mine_last, 1);
+                        if (lane < 31) {  // I hold x (first column of pair kl)
+                            const float x = mine_last, y = from_right;
+                            zr[i][CPL - 1] = wl ? (sl * x + cl * y) : (cl * x - sl * y);
+                        }
+                        if (lane > 0) {  // I hold y (second column of pair kr)
+                            const float x = from_left, y = mine_first;
+                            zr[i][0] = wr ? (crr * x - srr * y) : (srr * x + crr * y);
+                        }
                     }
                 }
                 __syncthreads();
             }
             if (!__syncthreads_or(rot_any)) break;
+        }
+        if constexpr (ZREG) {
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) Z[(zrow0 + i) * (PW + 1) + zcol0 + j] = zr[i][j];
+            __syncthreads();
         }
         inner_sweeps = 0;
     }
