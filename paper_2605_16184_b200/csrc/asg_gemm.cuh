@@ -68,7 +68,12 @@ struct GemmParams {
     const ApplyEntry* apply;  // EPI_APPLY: per batch entry
     float lr_eff, wd;
     int* flag;            // set to 1 on a non-finite update (EPI_APPLY)
+    const int* batch_active;  // optional: batches with batch_active[b] == 0 are skipped (no output)
 };
+
+__device__ __forceinline__ bool batch_skipped(const GemmParams& p, int t) {
+    return p.batch_active && p.batch_active[t / p.tiles_per_batch] == 0;
+}
 
 template <int BN, int NPASS>
 struct GemmCfg {
@@ -400,6 +405,7 @@ __global__ void __launch_bounds__(320, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                if (batch_skipped(p, t)) continue;
                 int b, tm, tn;
                 decode_tile(p, t, b, tm, tn);
                 for (int kb = 0; kb < num_k; ++kb) {
@@ -426,6 +432,7 @@ __global__ void __launch_bounds__(320, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                if (batch_skipped(p, t)) continue;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + uint32_t(acc * BN);
@@ -464,6 +471,7 @@ __global__ void __launch_bounds__(320, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            if (batch_skipped(p, t)) continue;
             int b, tm, tn;
             decode_tile(p, t, b, tm, tn);
             mbar_wait(&tfull[acc], acc_phase);

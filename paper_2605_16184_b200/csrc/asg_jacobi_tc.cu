@@ -1106,9 +1106,13 @@ __global__ void tj_gather_kernel(const float* __restrict__ Vh, const float* __re
 // J_i /= |J_i|. This removes the slow drift of |J_i| and diag(A) that the
 // tensor cores' fp32 accumulation leaves over hundreds of rotation products.
 // Grid (D/32 column groups, nb), 256 threads = 32 columns x 8 row phases.
+// Matrices that took no sweep (sweeps[b] == 0) have J = a permutation (the
+// sort) and skipped the W = B J GEMM: their quotient is B's diagonal, read
+// through J (j_i = e_src(i): sum_k J[k][i]^2 B[k][k] = B[src][src]).
 __global__ void tj_rayleigh_kernel(float* __restrict__ Jh, float* __restrict__ Jl, float* __restrict__ JTh,
                                    float* __restrict__ JTl, const float* __restrict__ W, int n, int D,
-                                   double* __restrict__ values) {
+                                   double* __restrict__ values, const float* __restrict__ B, int ldb,
+                                   const int* __restrict__ sweeps) {
     __shared__ double sjw[8][32], sjj[8][32];
     __shared__ float scale[32];
     const int64_t b = blockIdx.y;
@@ -1116,10 +1120,12 @@ __global__ void tj_rayleigh_kernel(float* __restrict__ Jh, float* __restrict__ J
     const int cl = threadIdx.x & 31, ph = threadIdx.x >> 5;
     const int c = blockIdx.x * 32 + cl;
     double jw = 0.0, jj = 0.0;
+    const bool perm = sweeps[b] == 0;
     for (int k = ph; k < n; k += 8) {
         const int64_t o = b * DD + int64_t(k) * D + c;
         const double j = double(Jh[o]) + (Jl ? double(Jl[o]) : 0.0);
-        jw += j * double(W[o]);
+        jw += perm ? (j == 0.0 ? 0.0 : j * j * double(B[b * int64_t(ldb) * ldb + int64_t(k) * ldb + k]))
+                   : j * double(W[o]);
         jj += j * j;
     }
     sjw[ph][cl] = jw;
@@ -1343,8 +1349,9 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
         gl.p.C = Vh;
         gl.p.ldc = D;
         gl.p.c_bstride = int64_t(DD);
+        gl.p.batch_active = sweeps;  // unswept matrices (J a permutation) need no W
         gemm_launch(gl, JTl ? ASG_PREC_3XTF32 : ASG_PREC_TF32, num_sms, st);
-        tj_rayleigh_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(Jh, Jl, JTh, JTl, Vh, n, D, values);
+        tj_rayleigh_kernel<<<dim3(D / 32, nb), 256, 0, st>>>(Jh, Jl, JTh, JTl, Vh, n, D, values, B, D, sweeps);
         tj_sort_values_kernel<<<nb, 512, size_t(n) * 8, st>>>(values, n);
         count_launch(2);  // rayleigh + sort (split / GEMM count themselves)
         if (!orthonormalize) return;
