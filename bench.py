@@ -478,9 +478,18 @@ def main():
         # k+1 streams into a staging buffer on a copy stream while step k
         # computes (double buffering, as a data loader would); step k+1 then
         # moves them into the bound gradient tensors with a device copy.
-        host = [g.cpu().pin_memory() for g in grads]
-        staging = [torch.empty_like(g) for g in grads]
-        h2d = sum(h.numel() * 4 for h in host)
+        # One flat pinned host batch (as a data loader would hand over) and one
+        # flat device staging buffer: a single large DMA per step instead of one
+        # copy per parameter tensor.
+        total = sum(g.numel() for g in grads)
+        host_flat = torch.empty(total, dtype=torch.float32).pin_memory()
+        staging_flat = torch.empty(total, dtype=torch.float32, device=dev)
+        staging, off = [], 0
+        for g in grads:
+            host_flat[off:off + g.numel()].copy_(g.reshape(-1).cpu())
+            staging.append(staging_flat[off:off + g.numel()].view_as(g))
+            off += g.numel()
+        h2d = total * 4
         copy_stream = torch.cuda.Stream(dev)
         ev_copied, ev_consumed = torch.cuda.Event(), torch.cuda.Event()
         cur = torch.cuda.current_stream(dev)
@@ -488,8 +497,7 @@ def main():
         def prefetch():
             with torch.cuda.stream(copy_stream):
                 copy_stream.wait_event(ev_consumed)  # staging free once the previous step took it
-                for st_, h in zip(staging, host):
-                    st_.copy_(h, non_blocking=True)
+                staging_flat.copy_(host_flat, non_blocking=True)
                 ev_copied.record(copy_stream)
 
         n_e2e = max(3, args.steps // 2)
