@@ -330,10 +330,23 @@ __global__ void sqnorm_multi_kernel(const SqChunk* __restrict__ chunks, double* 
     const SqChunk c = chunks[blockIdx.x];
     double s = 0.0;
     bool bad = false;
-    for (int64_t e = c.e0 + threadIdx.x; e < c.e1; e += blockDim.x) {
-        const float v = c.x[(e / c.cols) * c.ld + (e % c.cols)];
-        bad |= !isfinite(v);
-        s += double(v) * double(v);
+    const float* base = c.x + c.e0;
+    const int64_t n = c.e1 - c.e0;
+    if (c.ld == c.cols && (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (n & 3) == 0) {
+        // contiguous chunk: 16-byte loads, no index arithmetic per element
+        const float4* b4 = reinterpret_cast<const float4*>(base);
+        for (int64_t i = threadIdx.x; i < n / 4; i += blockDim.x) {
+            const float4 v = __ldcs(b4 + i);
+            bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+            s += double(v.x) * double(v.x) + double(v.y) * double(v.y) + double(v.z) * double(v.z) +
+                 double(v.w) * double(v.w);
+        }
+    } else {
+        for (int64_t e = c.e0 + threadIdx.x; e < c.e1; e += blockDim.x) {
+            const float v = c.x[(e / c.cols) * c.ld + (e % c.cols)];
+            bad |= !isfinite(v);
+            s += double(v) * double(v);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
     __shared__ double red[32];
