@@ -1011,20 +1011,26 @@ void launch_merge_status(const int* in, int cnt, int* out, cudaStream_t s) {
 // ============================================================================
 // Multi-GPU pack / unpack of block slices (owner-major all-gather layout)
 // ============================================================================
+// Row-wise: CTA x takes rows x, x + gridDim.x, ...; threads run along the row
+// (coalesced on both sides, no per-element index division).
 __global__ void pack_kernel(const BlockRef* blocks, const int64_t* offsets, float* out) {
     const BlockRef blk = blocks[blockIdx.y];
-    const int64_t n = int64_t(blk.rows) * blk.cols;
     float* o = out + offsets[blockIdx.y];
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
-        o[e] = blk.src[(e / blk.cols) * blk.ld + (e % blk.cols)];
+    for (int r = blockIdx.x; r < blk.rows; r += gridDim.x) {
+        const float* src = blk.src + int64_t(r) * blk.ld;
+        float* dst = o + int64_t(r) * blk.cols;
+        for (int c = threadIdx.x; c < blk.cols; c += blockDim.x) dst[c] = src[c];
+    }
 }
 
 __global__ void unpack_kernel(const BlockRef* blocks, const int64_t* offsets, const float* in) {
     const BlockRef blk = blocks[blockIdx.y];
-    const int64_t n = int64_t(blk.rows) * blk.cols;
     const float* i = in + offsets[blockIdx.y];
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
-        blk.dst[(e / blk.cols) * blk.ld + (e % blk.cols)] = i[e];
+    for (int r = blockIdx.x; r < blk.rows; r += gridDim.x) {
+        const float* src = i + int64_t(r) * blk.cols;
+        float* dst = blk.dst + int64_t(r) * blk.ld;
+        for (int c = threadIdx.x; c < blk.cols; c += blockDim.x) dst[c] = src[c];
+    }
 }
 
 void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out, cudaStream_t s) {
@@ -1034,10 +1040,12 @@ void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, 
 
 __global__ void unpack_scaled_kernel(const BlockRef* blocks, const int64_t* offsets, const float* in, float scale) {
     const BlockRef blk = blocks[blockIdx.y];
-    const int64_t n = int64_t(blk.rows) * blk.cols;
     const float* i = in + offsets[blockIdx.y];
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
-        blk.dst[(e / blk.cols) * blk.ld + (e % blk.cols)] = scale * i[e];
+    for (int r = blockIdx.x; r < blk.rows; r += gridDim.x) {
+        const float* src = i + int64_t(r) * blk.cols;
+        float* dst = blk.dst + int64_t(r) * blk.ld;
+        for (int c = threadIdx.x; c < blk.cols; c += blockDim.x) dst[c] = scale * src[c];
+    }
 }
 
 void launch_unpack_scaled(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, const float* in, float scale,
