@@ -264,7 +264,7 @@ __global__ void identity_split_kernel(float* hi, float* lo, int M, int m) {
     const int64_t b = blockIdx.y;
     const int64_t slab = int64_t(M) * M;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < slab; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / M), j = int(e % M);
+        const int i = int(uint32_t(e) / uint32_t(M)), j = int(uint32_t(e) - uint32_t(i) * uint32_t(M));  // per-matrix index < 2^31
         hi[b * slab + e] = (i == j && i < m) ? 1.f : 0.f;
         if (lo) lo[b * slab + e] = 0.f;
     }
@@ -279,7 +279,7 @@ __global__ void identity_f32_kernel(float* a, int M, int m, float diag) {
     const int64_t b = blockIdx.y;
     const int64_t slab = int64_t(M) * M;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < slab; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / M), j = int(e % M);
+        const int i = int(uint32_t(e) / uint32_t(M)), j = int(uint32_t(e) - uint32_t(i) * uint32_t(M));  // per-matrix index < 2^31
         a[b * slab + e] = (i == j && i < m) ? diag : 0.f;
     }
 }
@@ -455,7 +455,7 @@ __global__ void snapshot_kernel(const float* __restrict__ src, int M, int m, dou
     const int64_t b = blockIdx.y;
     const int64_t n = int64_t(m) * m;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / m), j = int(e % m);
+        const int i = int(uint32_t(e) / uint32_t(m)), j = int(uint32_t(e) - uint32_t(i) * uint32_t(m));  // per-matrix index < 2^31
         dst[b * n + e] = double(src[b * int64_t(M) * M + int64_t(i) * M + j]);
     }
 }
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kEigThreads) sym_eig_kernel(const double* __re
     auto off_norm = [&]() {
         double acc = 0.0;
         for (int64_t e = tid; e < nn; e += nt) {
-            const int i = int(e / n), j = int(e % n);
+            const int i = int(uint32_t(e) / uint32_t(n)), j = int(uint32_t(e) - uint32_t(i) * uint32_t(n));  // per-matrix index < 2^31
             if (j > i) acc += A[e] * A[e];
         }
         return sqrt(2.0 * block_reduce_sum(acc, red));
@@ -800,7 +800,7 @@ __global__ void f64_to_f32_kernel(const double* src, int rows, int cols, float* 
     const int64_t b = blockIdx.y;
     const int64_t tot = int64_t(R) * Cc;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / Cc), j = int(e % Cc);
+        const int i = int(uint32_t(e) / uint32_t(Cc)), j = int(uint32_t(e) - uint32_t(i) * uint32_t(Cc));  // per-matrix index < 2^31
         dst[b * tot + e] = (i < rows && j < cols) ? float(src[b * int64_t(rows) * cols + int64_t(i) * cols + j]) : 0.f;
     }
 }
@@ -814,7 +814,7 @@ __global__ void f32_to_f64_kernel(const float* src, int rows, int cols, int R, i
     const int64_t b = blockIdx.y;
     const int64_t tot = int64_t(rows) * cols;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / cols), j = int(e % cols);
+        const int i = int(uint32_t(e) / uint32_t(cols)), j = int(uint32_t(e) - uint32_t(i) * uint32_t(cols));  // per-matrix index < 2^31
         dst[b * tot + e] = double(src[b * int64_t(R) * Cc + int64_t(i) * Cc + j]);
     }
 }
@@ -858,7 +858,7 @@ __global__ void snapshot_sym_kernel(const float* __restrict__ src, int M, int m,
     const int64_t n = int64_t(m) * m;
     const float* sb = src + b * int64_t(M) * M;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / m), j = int(e % m);
+        const int i = int(uint32_t(e) / uint32_t(m)), j = int(uint32_t(e) - uint32_t(i) * uint32_t(m));  // per-matrix index < 2^31
         dst[b * n + e] = 0.5 * (double(sb[int64_t(i) * M + j]) + double(sb[int64_t(j) * M + i]));
     }
 }
@@ -979,7 +979,7 @@ __global__ void ns_x_kernel(const float* S, int d, int D, float* Xh, float* __re
     const int64_t b = blockIdx.y;
     const int64_t DD = int64_t(D) * D;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < DD; e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / D), j = int(e % D);
+        const int i = int(uint32_t(e) / uint32_t(D)), j = int(uint32_t(e) - uint32_t(i) * uint32_t(D));  // per-matrix index < 2^31
         float x = 0.f;
         if (i < d && j < d) x = (i == j ? 1.5f : 0.f) - 0.5f * S[b * DD + e];
         float h, l;
