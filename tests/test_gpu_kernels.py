@@ -98,3 +98,39 @@ def test_sym_eig_batched_f32_matches_lapack(rt, n):
         assert np.abs(v[k] - ref).max() <= 1e-5 * np.abs(ref).max()
         assert np.abs(a @ q[k] - q[k] * v[k]).max() <= 2e-5 * np.abs(ref).max()
         assert np.abs(q[k].T @ q[k] - np.eye(n)).max() <= 2e-5
+
+
+@pytest.mark.gpu
+def test_grad_sqnorm_strided_and_odd_params_through_the_c_abi():
+    """asg_grad_sqnorm (clip statistic, harness.cpp:219-223) over a strided
+    parameter (ld > cols: the per-element path), an odd-sized contiguous one
+    (tail not a multiple of 4) and a large contiguous one (16-byte path),
+    against the fp64 sum of squares; a NaN sets the non-finite flag."""
+    import ctypes as C
+    torch = pytest.importorskip("torch")
+    from paper_2605_16184_b200 import abi, runtime
+    g = torch.Generator(device="cuda").manual_seed(5)
+    big_p = torch.zeros(64, 200, device="cuda")
+    big_g = torch.randn(64, 200, device="cuda", generator=g)
+    p2, g2 = torch.zeros(7, 9, device="cuda"), torch.randn(7, 9, device="cuda", generator=g)
+    p3, g3 = torch.zeros(512, 640, device="cuda"), torch.randn(512, 640, device="cuda", generator=g)
+    descs = (abi.ParamDesc * 3)()
+    descs[0] = abi.ParamDesc(big_p.data_ptr(), big_g.data_ptr(), 64, 150, 200, 200)
+    descs[1] = abi.ParamDesc(p2.data_ptr(), g2.data_ptr(), 7, 9, 9, 9)
+    descs[2] = abi.ParamDesc(p3.data_ptr(), g3.data_ptr(), 512, 640, 640, 640)
+    opt = runtime.optimizer_defaults(abi.SHAMPOO)
+    sched = runtime.scheduler_defaults()
+    h = C.c_void_p()
+    runtime.check(runtime.lib.asg_blockset_create(0, C.byref(opt), C.byref(sched), descs, 3, abi.PREC_3XTF32, 0, 1,
+                                                  1, C.byref(h)))
+    try:
+        v, f = C.c_double(), C.c_int32()
+        runtime.check(runtime.lib.asg_grad_sqnorm(h, C.c_void_p(1), C.byref(v), C.byref(f)))
+        want = sum(float((t.double() ** 2).sum()) for t in (big_g[:, :150], g2, g3))
+        assert f.value == 0
+        assert abs(v.value - want) <= 1e-12 * want
+        g3[100, 7] = float("nan")
+        runtime.check(runtime.lib.asg_grad_sqnorm(h, C.c_void_p(1), C.byref(v), C.byref(f)))
+        assert f.value == 1
+    finally:
+        runtime.lib.asg_blockset_destroy(h)
