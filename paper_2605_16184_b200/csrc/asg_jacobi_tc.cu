@@ -718,6 +718,30 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
+    // per-pair flags and per-matrix activity, read once per launch (most tiles of
+    // a warm refresh are skipped; a global load per tile would serialise them)
+    constexpr int G = JP / (2 * JW), NB = JP / JW;  // pairs and blocks per tile
+    int* sflag = reinterpret_cast<int*>(bars + 16);
+    const int npairs = p.m / 2, ntiles = npairs / G;
+    const int nflags = p.nb * npairs;
+    for (int i = threadIdx.x; i < nflags; i += blockDim.x) sflag[i] = p.pflag[i] | (p.active[i / npairs] << 1);
+    __syncthreads();
+    const int total = p.nb * (p.tilesA + p.tilesV);
+    {
+        // A CTA without a moving tile this round (late sweeps of a warm refresh)
+        // leaves before allocating TMEM or arming barriers.
+        bool work = false;
+        for (int t = blockIdx.x + int(threadIdx.x) * int(gridDim.x); t < total && !work;
+             t += int(blockDim.x) * int(gridDim.x)) {
+            int b, i1, i2;
+            bool isA;
+            tj_decode(p, t, b, isA, i1, i2);
+            if (!(sflag[b * npairs] >> 1)) continue;
+            for (int t2 = 0; t2 < G; ++t2)
+                work |= (sflag[b * npairs + G * i2 + t2] & 1) || (isA && (sflag[b * npairs + G * i1 + t2] & 1));
+        }
+        if (!__syncthreads_or(work)) return;
+    }
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmAh);
         tma_prefetch(&tmAl);
@@ -749,15 +773,6 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t idesc = idesc_tf32(JP, JP);
-    // per-pair flags and per-matrix activity, read once per launch (most tiles of
-    // a warm refresh are skipped; a global load per tile would serialise them)
-    int* sflag = reinterpret_cast<int*>(bars + 16);
-    const int nflags = p.nb * (p.m / 2);
-    for (int i = threadIdx.x; i < nflags; i += blockDim.x) sflag[i] = p.pflag[i] | (p.active[i / (p.m / 2)] << 1);
-    __syncthreads();
-    constexpr int G = JP / (2 * JW), NB = JP / JW;  // pairs and blocks per tile
-    const int total = p.nb * (p.tilesA + p.tilesV);
-    const int npairs = p.m / 2, ntiles = npairs / G;
 
     // Tiles are pipelined across the roles (no CTA-wide barrier per tile):
     //   * the producer loads tile u+1's MMA1 operands while tile u's A' drains,
