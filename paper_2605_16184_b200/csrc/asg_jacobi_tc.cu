@@ -6,20 +6,26 @@
 //
 //   * A (the factor, rotated into the previous eigenbasis) and V (the
 //     accumulated rotation) live in HBM as (hi, lo) tf32 pairs, natural order.
-//   * Columns are split into 64-wide blocks; a round pairs the blocks by a
-//     round-robin tournament (m/2 disjoint pairs, m-1 rounds per sweep).
-//   * tj_pair_kernel: one CTA per (matrix, pair) gathers the 128x128 pair
-//     matrix and diagonalises it exactly in shared memory (parallel cyclic
-//     Jacobi, fp32, ascending order within the pair = sorted block Jacobi);
-//     it writes J^T as a split pair, or flags the pair as converged when no
-//     element exceeds |a_ij| > tol * max(sqrt(a_ii a_jj), ||A||_F / sqrt(n)).
+//   * Columns are split into JW-wide blocks (32 below kWidePairN, 64 from
+//     there); a round pairs the blocks by a round-robin tournament (m/2
+//     disjoint pairs, m-1 rounds per sweep).
+//   * tj_pair_kernel: one CTA per (matrix, pair) gathers the PW x PW pair
+//     matrix (PW = 2 JW) and gives it one inner Jacobi sweep in shared memory
+//     (fp32; odd-even ordering with one fused, conflict-free, load-batched
+//     pass per round; for PW = 128 the pair rotation stays in registers;
+//     ascending order within the pair = sorted block Jacobi); it writes J^T
+//     as a split pair, or flags the pair as converged when no element exceeds
+//     |a_ij| > tol * max(sqrt(a_ii a_jj), noise floor). Pairs with at most
+//     kFewBig large elements rotate them one by one (classical Jacobi).
 //   * tj_apply_kernel (tcgen05): every 128x128 tile (pair k1 rows, pair k2
 //     columns) of A becomes J_k1^T (A_tile J_k2) -- two chained 3xTF32 MMAs
 //     with the intermediate staged TMEM -> registers -> shared memory as the
 //     transposed K-major operand -- and every 128-row panel of V becomes
-//     V_tile J_k2. Tiles whose pairs are both converged are skipped. All
-//     operand tiles are gathered by TMA (64-row / 32-column boxes of the
-//     natural layout), so no data is permuted between rounds.
+//     V_tile J_k2. Tiles whose pairs are both converged are skipped (a CTA
+//     with none left exits before allocating TMEM); tiles are pipelined
+//     across the warp roles. All operand tiles are gathered by TMA (JW-row /
+//     32-column boxes of the natural layout), so no data is permuted between
+//     rounds.
 //   * A sweep that rotated nothing ends the iteration (device flags; the
 //     sweeps run in a CUDA-graph WHILE loop), within the reference's budget of
 //     30 sweeps (densela.hpp:194); eigenvalues diag(A) are sorted ascending
@@ -160,10 +166,10 @@ __global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const 
 }
 
 // ---- pair solve -----------------------------------------------------------------
-// One CTA per (pair k, matrix b): gathers the 64x64 pair matrix (blocks p, q),
-// diagonalises it in shared memory (fp32 parallel cyclic Jacobi) and writes
-// J^T into its diagonal 64x64 block of the quad tile (pairs 2g, 2g+1 share a
-// 128x128 tile; the off-diagonal blocks stay zero).
+// One CTA per (pair k, matrix b): gathers the PW x PW pair matrix (blocks p,
+// q), gives it one inner Jacobi sweep in shared memory and writes J^T into
+// its diagonal PW x PW block of the 128x128 tile (for PW = 64 pairs 2g, 2g+1
+// share a tile; the off-diagonal blocks stay zero).
 template <int PW, int NT>
 __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_kernel(const float* __restrict__ Ah, const float* __restrict__ Al,
                                                                int D, int m, int round, float* __restrict__ JTh,
