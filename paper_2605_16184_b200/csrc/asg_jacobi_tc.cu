@@ -54,9 +54,10 @@ constexpr int JP = 128;  // apply tile: 128/PW pairs of two JW-wide blocks
 // Pair width PW = 2 JW: 64 (tiles of two pairs) below kWidePairN, 128 (one
 // pair per tile) from there on: small pairs make the shared-memory solves
 // cheap, wide pairs halve the rounds (and the tensor-core work) per sweep.
-// 768: measured faster than 1536 for warm refreshes (half the launches per
-// sweep) and for cold solves at n = 1024 once the wide pair solve got faster.
-constexpr int kWidePairN = 768;
+// 512: measured faster than 1536 for warm refreshes (half the launches per
+// sweep) and for cold solves at n = 512 and 1024 once the wide pair solve got
+// faster (tools/gpu_wide.sh, gpu_wide2.sh).
+constexpr int kWidePairN = 512;
 constexpr int kFewBig = 8;  // pair solves with at most this many large elements rotate them one by one
 // Pair-solve ordering: the odd-even ordering (one fused, conflict-free,
 // load-batched pass per round) for both widths -- measured 2.3x (PW = 128) and
