@@ -123,7 +123,13 @@ typedef enum asg_install_mode {
  *        basis Q J, the roots V f(lambda) V^T and the SOAP moment
  *        re-projection J^T M J are 3xTF32 tensor-core GEMMs. Accuracy is that
  *        of the fp32 factor it decomposes. */
-typedef enum asg_refresh_mode { ASG_REFRESH_F64 = 0, ASG_REFRESH_F32 = 1 } asg_refresh_mode;
+/*   NEWTON: as F32, except that the Shampoo (L^-1/4) and KL-Shampoo (L^-1/2,
+ *        L^-1) roots come from a coupled Newton-Schulz iteration on the
+ *        tensor cores (GEMMs only, no eigendecomposition; asg_newton.cu) of
+ *        the damped snapshot (A + eps I), eps = damping * tr/n. Same result
+ *        as inv_root (densela.hpp:267-282) to fp32 level; SOAP, which needs
+ *        the eigenbasis itself, keeps the F32 eigensolve. */
+typedef enum asg_refresh_mode { ASG_REFRESH_F64 = 0, ASG_REFRESH_F32 = 1, ASG_REFRESH_NEWTON = 2 } asg_refresh_mode;
 
 /* SchedulerConfig (asyncsched.hpp:50-59); JSON keys config.cpp:81-86. */
 typedef struct asg_scheduler_config {
@@ -218,7 +224,7 @@ int asg_scheduler_defaults(asg_scheduler_config* out);                      /* S
  * must equal it (config.cpp:42-43). Method strings: "AdamW", "Shampoo",
  * "SOAP", "KL-Shampoo". An optional "gpu" section may set "precision"
  * ("3xtf32"|"tf32"), "install_mode" ("sim_clock"|"event") and "refresh"
- * ("f64"|"f32"). */
+ * ("f64"|"f32"|"newton"). */
 int asg_config_from_json(const char* json, asg_optimizer_config* opt,
                          asg_scheduler_config* sched, int32_t* precision);
 

@@ -18,7 +18,7 @@ PREC_3XTF32, PREC_TF32 = 0, 1
 # asg_install_mode
 INSTALL_SIM_CLOCK, INSTALL_EVENT = 0, 1
 # asg_refresh_mode
-REFRESH_F64, REFRESH_F32 = 0, 1
+REFRESH_F64, REFRESH_F32, REFRESH_NEWTON = 0, 1, 2
 # asg_role (tiers.hpp:35-44 + KL + eigenvalues)
 (FACTOR_L, FACTOR_R, INV_L, INV_R, BASIS_L, BASIS_R, ROTATED_M, ROTATED_V,
  KL_INV_L, KL_INV_R, EIGVALS_L, EIGVALS_R) = range(12)

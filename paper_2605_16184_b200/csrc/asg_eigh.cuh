@@ -49,4 +49,14 @@ void launch_tc_eigh(const float* B, int D, double* values, float* Jh, float* Jl,
                     int nb, int n, int* status, int num_sms, cudaStream_t s, double tol, bool orthonormalize = true,
                     int* ident = nullptr);  // optional per matrix: 1 if J is exactly the identity
 
+// Coupled Newton-Schulz inverse p-th root (asg_newton.cu), p in {2, 4}:
+// out = (A + eps_b I)^(-1/p) for the nb fp32 matrices A [nb][D][D] (leading
+// d x d; out zero-padded, split pair). ws: ns_workspace_floats(nb, D) floats.
+// status: per-matrix asg_status, failures only. sym_tiles: the D x D
+// lower-triangle tile list (gemm_sym_tile_list).
+size_t ns_workspace_floats(int nb, int D);
+void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps, int p, float* outh, float* outl,
+                        float* ws, int* status, const int2* sym_tiles, int nsym, int precision, int num_sms,
+                        cudaStream_t s);
+
 }  // namespace asg

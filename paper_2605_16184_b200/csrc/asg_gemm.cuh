@@ -31,6 +31,11 @@
 //                updates m, v in place, writes S = m^/(sqrt(v^)+eps) as (hi, lo)
 //   EPI_APPLY    theta -= lr*lr_scale*(alpha*acc + wd*theta) on the block's
 //                slice of the caller's parameter (apply_update precond.cpp:244-251)
+//   EPI_SYM_SPLIT  D = alpha*acc as a (hi, lo) pair on the lower triangle,
+//                mirrored (products of commuting symmetric matrices: the
+//                coupled Newton-Schulz inverse root, asg_newton.cu)
+//   EPI_NS       EPI_SYM_SPLIT for M, plus T = ns_a*I - ns_b*M as a second
+//                (hi, lo) pair and max|M - I| per batch into resid[b]
 #pragma once
 
 #include <cuda.h>
@@ -40,7 +45,16 @@
 
 namespace asg {
 
-enum EpiKind { EPI_STORE = 0, EPI_SYM_EMA = 1, EPI_SPLIT = 2, EPI_SPLIT_T = 3, EPI_ADAM = 4, EPI_APPLY = 5 };
+enum EpiKind {
+    EPI_STORE = 0,
+    EPI_SYM_EMA = 1,
+    EPI_SPLIT = 2,
+    EPI_SPLIT_T = 3,
+    EPI_ADAM = 4,
+    EPI_APPLY = 5,
+    EPI_SYM_SPLIT = 6,
+    EPI_NS = 7
+};
 
 struct ApplyEntry {
     float* theta;   // first element of the block inside the parameter
@@ -69,6 +83,10 @@ struct GemmParams {
     float lr_eff, wd;
     int* flag;            // set to 1 on a non-finite update (EPI_APPLY)
     const int* batch_active;  // optional: batches with batch_active[b] == 0 are skipped (no output)
+    float* Thi;           // EPI_NS: T = ns_a I - ns_b M (hi, lo), same layout as D
+    float* Tlo;
+    float ns_a, ns_b;
+    unsigned int* resid;  // EPI_NS: per batch max|M - I| (float bits, atomicMax)
 };
 
 __device__ __forceinline__ bool batch_skipped(const GemmParams& p, int t) {
@@ -342,6 +360,63 @@ __device__ __forceinline__ void adam_chunk(const GemmParams& p, int b, int row0,
     __syncwarp();
 }
 
+// EPI_SYM_SPLIT / EPI_NS, warp-cooperative: the 32 x 32 chunk's lower
+// triangle is written as (hi, lo) rows (coalesced) and mirrored to the upper
+// triangle (lanes = consecutive rows: coalesced), so the output is exactly
+// symmetric. EPI_NS also writes T = ns_a I - ns_b M the same way and folds
+// max|M - I| into resid[b] (a non-finite M reports +inf).
+template <bool NS>
+__device__ __forceinline__ void sym_split_chunk(const GemmParams& p, int b, int row0, int col0,
+                                                const uint32_t (&r)[32], float (*scratch)[33]) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (row0 + 31 < col0) return;  // whole chunk strictly above the diagonal (warp-uniform)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) scratch[lane][j] = p.alpha * __uint_as_float(r[j]);
+    __syncwarp();
+    const int64_t base = int64_t(b) * p.d_bstride;
+    float* mh = p.Dhi + base;
+    float* ml = p.Dlo ? p.Dlo + base : nullptr;
+    float* th = NS ? p.Thi + base : nullptr;
+    float* tl = (NS && p.Tlo) ? p.Tlo + base : nullptr;
+    float res = 0.f;
+    auto put = [&](int64_t off, float v, bool diag) {
+        float h, l;
+        split_tf32(v, h, l);
+        mh[off] = h;
+        if (ml) ml[off] = l;
+        if constexpr (NS) {
+            const float t = (diag ? p.ns_a : 0.f) - p.ns_b * v;
+            split_tf32(t, h, l);
+            th[off] = h;
+            if (tl) tl[off] = l;
+        }
+    };
+    const int c = col0 + int(lane);
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+        const int row = row0 + i;
+        if (row >= c) {
+            const float v = scratch[i][lane];
+            put(int64_t(row) * p.ldd + c, v, row == c);
+            if constexpr (NS) {
+                const float d = fabsf(v - (row == c ? 1.f : 0.f));
+                res = isfinite(v) ? fmaxf(res, d) : __int_as_float(0x7f800000);
+            }
+        }
+    }
+    __syncwarp();
+    const int row = row0 + int(lane);
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j)
+        if (row > col0 + j) put(int64_t(col0 + j) * p.ldd + row, scratch[lane][j], false);
+    if constexpr (NS) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) res = fmaxf(res, __shfl_xor_sync(0xffffffffu, res, o));
+        if (lane == 0) atomicMax(p.resid + b, __float_as_uint(res));
+    }
+    __syncwarp();
+}
+
 template <int BN, int NPASS, int EPI>
 __global__ void __launch_bounds__(320, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
@@ -488,6 +563,8 @@ __global__ void __launch_bounds__(320, 1)
                     adam_chunk(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
                 else if constexpr (EPI == EPI_STORE || EPI == EPI_SPLIT || EPI == EPI_SYM_EMA)
                     rows_chunk<EPI>(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
+                else if constexpr (EPI == EPI_SYM_SPLIT || EPI == EPI_NS)
+                    sym_split_chunk<EPI == EPI_NS>(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
                 else
                     epilogue_chunk<EPI>(p, b, row, tn * BN + c * 32, r);
             }

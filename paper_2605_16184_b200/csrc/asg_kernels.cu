@@ -96,6 +96,8 @@ cudaError_t dispatch_epi(int epi, const CUtensorMap& ah, const CUtensorMap& al, 
         case EPI_SPLIT_T: return launch_inst<BN, NPASS, EPI_SPLIT_T>(ah, al, bh, bl, p, num_sms, s);
         case EPI_ADAM: return launch_inst<BN, NPASS, EPI_ADAM>(ah, al, bh, bl, p, num_sms, s);
         case EPI_APPLY: return launch_inst<BN, NPASS, EPI_APPLY>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SYM_SPLIT: return launch_inst<BN, NPASS, EPI_SYM_SPLIT>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_NS: return launch_inst<BN, NPASS, EPI_NS>(ah, al, bh, bl, p, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }

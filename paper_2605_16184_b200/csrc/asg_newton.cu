@@ -1,0 +1,657 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Coupled Newton-Schulz inverse p-th roots on the tensor cores: the
+// ASG_REFRESH_NEWTON refresh of Shampoo (p = 4) and KL-Shampoo (p = 2),
+// replacing inv_root's eigendecomposition (densela.hpp:267-282) with the same
+// result, (A + eps I)^(-1/p), eps = damping * tr(A) / n (relative_damping
+// precond.cpp:121-125), computed by GEMMs only.
+//
+// Iteration (Guo & Higham's coupled Newton iteration for the inverse p-th
+// root; M_k = X_k^p A is an invariant):
+//     c   = min(||A'||_F, 1.25 * ||A' v||)   (v: 8 power steps; c >= ~lambda_max)
+//     M_0 = A' / c,  X_0 = c^(-1/p) I,  T_k = ((p + 1) I - M_k) / p
+//     X_{k+1} = X_k T_k,   M_{k+1} = T_k^p M_k        (A' = A + eps I)
+// Every matrix in the iteration is a polynomial in A', so every product is
+// symmetric: each GEMM computes the lower-triangle tiles only and mirrors
+// them (EPI_SYM_SPLIT), which halves the tensor-core work. The M-producing
+// GEMM also writes T_{k+1} and max|M_{k+1} - I| (EPI_NS); a power step on
+// I - M_{k+1} tracks the spectral deviation 1 - x_min (all x in (0, 1] after
+// the first iteration, and the slowest eigenvector never changes). Per
+// matrix, once max|M - I| <= 1e-3 and the probe <= 2.5e-4, one more X step
+// (quadratic convergence: error ~1e-6) finishes it; finished matrices are
+// skipped by every later launch
+// (GemmParams::batch_active). The iterations run in a CUDA-graph WHILE loop
+// that ends when no matrix is active. p = 2: 3 GEMMs per iteration
+// (X T, W = T M, M = T W); p = 4: 4 (X T, U = T T, W = U M, M = U W).
+//
+// Failure semantics (inv_root densela.hpp:274-278): a damped eigenvalue <= 0
+// makes the iteration diverge (|1 - x| grows) or stall at x = 0; both report
+// ASG_ERR_NOT_PSD. A non-finite factor reports ASG_ERR_NON_FINITE. The damping
+// is lifted to the products' rounding floor (ns_floor): eigenvalues below
+// ~1e-5 lambda_max are fp32 noise, as in the F32 eigensolve's clamp.
+// After the loop, one symmetric Newton refinement against A' itself,
+// X <- X + (X R + R X)/(2p), R = I - X^(p/2) A' X^(p/2), removes most of the
+// rounding the product chain X_k T_k accumulated.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../../include/asteria_b200.h"
+#include "asg_eigh.cuh"
+#include "asg_kernels.cuh"
+
+namespace asg {
+namespace {
+
+constexpr int kNsMaxIter = 60;
+constexpr float kNsFinal = 1e-3f;   // max|M - I| that (with kNsSpec) triggers the last X step
+constexpr float kNsSpec = 2.5e-4f;  // spectral probe ||(I - M) v|| (a lower bound of 1 - x_min)
+constexpr float kNsDiverged = 3.5f;  // eigenvalues of M outside (0, p + 1): divergence
+constexpr int kPowerSteps = 8;
+// Damping floor relative to lambda_max: the stated error of one 3xTF32
+// product at depth d (gemm_tol, tests/test_gpu_kernels.py). The fp32 factor
+// and every product of the iteration carry noise of that size, so smaller
+// eigenvalues are not resolved by any fp32-level refresh (the F32 eigensolve
+// clamps the same band, scale_columns_split); in the coupled iteration they
+// would turn the damped factor indefinite and diverge. Well-conditioned
+// factors (lambda_min >> floor, every parity test and the bench's KL factors)
+// are unaffected.
+inline float ns_floor(int d) { return 1e-6f + 1.2e-8f * float(d); }
+constexpr int kPowRows = 32;  // rows of A' v per CTA
+
+// y = A' v on the leading d x d (A' = A + eps I); per-CTA partial sums of y^2
+// (and, on the first step, of A'^2 for ||A'||_F) in fixed order.
+__global__ void ns_power_kernel(const float* __restrict__ A, int d, int D, const double* __restrict__ eps,
+                                const float* __restrict__ v, float* __restrict__ y, float* __restrict__ part,
+                                float* __restrict__ partf, int nblk, const int* __restrict__ gate) {
+    extern __shared__ float vs[];
+    const int b = blockIdx.y;
+    if (!gate[b]) return;
+    const float* a = A + size_t(b) * D * D;
+    const float* vb = v + size_t(b) * D;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) vs[j] = vb[j];
+    __syncthreads();
+    const float e = float(eps[b]);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __shared__ float red[2][32];
+    float ysq = 0.f, fsq = 0.f;
+    for (int r = warp; r < kPowRows; r += nw) {
+        const int i = blockIdx.x * kPowRows + r;
+        if (i >= d) break;
+        const float* row = a + size_t(i) * D;
+        float acc = 0.f, f = 0.f;
+        for (int j = lane; j < d; j += 32) {
+            const float x = row[j] + (j == i ? e : 0.f);
+            acc = fmaf(x, vs[j], acc);
+            f = fmaf(x, x, f);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            f += __shfl_xor_sync(0xffffffffu, f, o);
+        }
+        if (lane == 0) y[size_t(b) * D + i] = acc;
+        ysq += acc * acc;
+        fsq += f;
+    }
+    if (lane == 0) {
+        red[0][warp] = ysq;
+        red[1][warp] = fsq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s0 = 0.f, s1 = 0.f;
+        for (int w = 0; w < nw; ++w) {
+            s0 += red[0][w];
+            s1 += red[1][w];
+        }
+        part[size_t(b) * nblk + blockIdx.x] = s0;
+        if (partf) partf[size_t(b) * nblk + blockIdx.x] = s1;
+    }
+}
+
+// v = y / ||y||, est[b] = ||y|| (= ||A' v_prev|| <= lambda_max for a unit
+// v_prev); first call: v = 1/sqrt(d), fro[b] = ||A'||_F.
+__global__ void ns_norm_kernel(const float* __restrict__ y, float* __restrict__ v, const float* __restrict__ part,
+                               const float* __restrict__ partf, int nblk, int d, int D, float* __restrict__ est,
+                               float* __restrict__ fro, int init, const int* __restrict__ gate) {
+    const int b = blockIdx.x;
+    if (!gate[b]) return;
+    __shared__ float s_nrm;
+    if (threadIdx.x == 0) {
+        if (init) {
+            s_nrm = 0.f;
+        } else {
+            float s = 0.f, f = 0.f;
+            for (int k = 0; k < nblk; ++k) {
+                s += part[size_t(b) * nblk + k];
+                if (partf) f += partf[size_t(b) * nblk + k];
+            }
+            s_nrm = sqrtf(s);
+            est[b] = s_nrm;
+            if (partf) fro[b] = sqrtf(f);
+        }
+    }
+    __syncthreads();
+    const float inv = init ? rsqrtf(float(d)) : (s_nrm > 0.f ? 1.f / s_nrm : 0.f);
+    for (int j = threadIdx.x; j < D; j += blockDim.x)
+        v[size_t(b) * D + j] = j < d ? (init ? inv : y[size_t(b) * D + j] * inv) : 0.f;
+}
+
+// M_0 = A'/c, T_0 = ((p+1) I - M_0)/p, X_0 = c^(-1/p) I (padding: identity in
+// all three, so it stays converged); per-matrix iteration state.
+__global__ void ns_init_kernel(const float* __restrict__ A, int d, int D, const double* __restrict__ eps,
+                               const float* __restrict__ est, const float* __restrict__ fro, float p, float floor_rel,
+                               float* __restrict__ Mh, float* __restrict__ Ml, float* __restrict__ Th,
+                               float* __restrict__ Tl, float* __restrict__ Xh, float* __restrict__ Xl,
+                               float* __restrict__ cval, float* __restrict__ eeff, const int* __restrict__ gate) {
+    const int b = blockIdx.y;
+    if (!gate[b]) return;
+    const float f = fro[b], es = est[b];
+    float c = fminf(f, 1.25f * es);
+    if (!(c > 0.f) || !isfinite(c)) c = 1.f;  // reported by ns_state_init
+    // damping lifted to the products' rounding floor (eigenvalues below it are
+    // numerically zero for the iteration; see kNsFloor)
+    const float e0 = float(eps[b]);
+    const float e = fmaxf(e0, floor_rel * c);
+    c += e - e0;
+    const float inv_c = 1.f / c, x0 = powf(c, -1.f / p);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        cval[b] = c;
+        eeff[b] = e;
+    }
+    const size_t DD = size_t(D) * D, base = size_t(b) * DD;
+    for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < DD; k += size_t(gridDim.x) * blockDim.x) {
+        const int i = int(k / D), j = int(k - size_t(i) * D);
+        float m, x;
+        if (i < d && j < d) {
+            m = (A[base + k] + (i == j ? e : 0.f)) * inv_c;
+            x = i == j ? x0 : 0.f;
+        } else {
+            m = x = i == j ? 1.f : 0.f;
+        }
+        const float t = (i == j ? (p + 1.f) / p : 0.f) - m / p;
+        float h, l;
+        split_tf32(m, h, l);
+        Mh[base + k] = h;
+        if (Ml) Ml[base + k] = l;
+        split_tf32(t, h, l);
+        Th[base + k] = h;
+        if (Tl) Tl[base + k] = l;
+        split_tf32(x, h, l);
+        Xh[base + k] = h;
+        if (Xl) Xl[base + k] = l;
+    }
+}
+
+struct NsState {
+    int* actX;   // X step runs
+    int* actM;   // M chain runs
+    int* state;  // 0 running, 1 last X step pending, 2 done
+    int* xbuf;   // buffer holding the finished X
+    unsigned int* resid;  // max|M - I| of the last M product (EPI_NS)
+    int* iter;   // iteration counter (one int)
+    int* any;    // per matrix: still active after the decision
+};
+
+__global__ void ns_state_init_kernel(NsState st, const float* __restrict__ est, const float* __restrict__ fro,
+                                     int nb, int* __restrict__ status, const int* __restrict__ gate) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b == 0) *st.iter = 0;
+    if (b >= nb) return;
+    st.resid[b] = 0u;
+    st.xbuf[b] = 0;
+    if (!gate[b]) {  // not part of this pass
+        st.state[b] = 2;
+        st.actX[b] = st.actM[b] = 0;
+        return;
+    }
+    const float f = fro[b], e = est[b];
+    if (!isfinite(f) || !isfinite(e)) {
+        if (status[b] == 0) status[b] = ASG_ERR_NON_FINITE;
+        st.state[b] = 2;
+        st.actX[b] = st.actM[b] = 0;
+        return;
+    }
+    if (!(f > 0.f)) {  // A' = 0: no positive damped eigenvalue
+        if (status[b] == 0) status[b] = ASG_ERR_NOT_PSD;
+        st.state[b] = 2;
+        st.actX[b] = st.actM[b] = 0;
+        return;
+    }
+    st.state[b] = 0;
+    st.actX[b] = st.actM[b] = 1;
+}
+
+// Spectral residual probe: y = (I - M) v on the leading d x d for matrices
+// whose M chain ran. After the first iteration every eigenvalue x of M lies
+// in (0, 1] (x h(x)^p <= 1 on (0, p + 1)), so ||I - M||_2 = 1 - x_min, and
+// since every M_k is a polynomial in A the slowest eigenvector is the same in
+// every iteration: one power step per iteration tracks it.
+__global__ void ns_spec_kernel(const float* __restrict__ Mh, const float* __restrict__ Ml, int d, int D,
+                               const int* __restrict__ actM, const float* __restrict__ v, float* __restrict__ y,
+                               float* __restrict__ part, int nblk) {
+    const int b = blockIdx.y;
+    if (!actM[b]) return;
+    extern __shared__ float vs[];
+    for (int j = threadIdx.x; j < d; j += blockDim.x) vs[j] = v[size_t(b) * D + j];
+    __syncthreads();
+    const size_t base = size_t(b) * D * D;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __shared__ float red[32];
+    float ysq = 0.f;
+    for (int r = warp; r < kPowRows; r += nw) {
+        const int i = blockIdx.x * kPowRows + r;
+        if (i >= d) break;
+        const float* rh = Mh + base + size_t(i) * D;
+        const float* rl = Ml ? Ml + base + size_t(i) * D : nullptr;
+        float acc = 0.f;
+        for (int j = lane; j < d; j += 32) {
+            const float m = rh[j] + (rl ? rl[j] : 0.f);
+            acc = fmaf((j == i ? 1.f : 0.f) - m, vs[j], acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) y[size_t(b) * D + i] = acc;
+        ysq += acc * acc;
+    }
+    if (lane == 0) red[warp] = ysq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s0 = 0.f;
+        for (int w = 0; w < nw; ++w) s0 += red[w];
+        part[size_t(b) * nblk + blockIdx.x] = s0;
+    }
+}
+
+// After iteration k (X_{k+1}, M_{k+1}, T_{k+1} written), one CTA per matrix:
+// decides its iteration k+1. Stop rule: max|M - I| <= 1e-3 and the spectral
+// probe ||(I - M) v|| <= 2.5e-4, then one last X step (quadratic convergence:
+// X error ~ (p+1)/(2p) e^2 <= 1e-6 for a spectral deviation e <= 1e-3).
+__global__ void ns_decide_kernel(NsState st, int nb, int d, int D, float* __restrict__ v,
+                                 const float* __restrict__ y, const float* __restrict__ part, int nblk,
+                                 int* __restrict__ status, int debug) {
+    const int b = blockIdx.x;
+    const int k = *st.iter;
+    const int s = st.state[b];
+    __shared__ float s_nrm;
+    if (s == 2) {
+        if (threadIdx.x == 0) st.any[b] = 0;
+        return;
+    }
+    if (s == 1) {  // the last X step ran in iteration k
+        if (threadIdx.x == 0) {
+            st.state[b] = 2;
+            st.xbuf[b] = (k + 1) & 1;
+            st.actX[b] = st.actM[b] = 0;
+            st.any[b] = 0;
+        }
+        return;
+    }
+    if (threadIdx.x == 0) {
+        float q = 0.f;
+        for (int i = 0; i < nblk; ++i) q += part[size_t(b) * nblk + i];
+        s_nrm = sqrtf(q);
+    }
+    __syncthreads();
+    const float nrm = s_nrm;
+    const float inv = nrm > 0.f ? 1.f / nrm : 0.f;
+    if (nrm > 0.f && isfinite(nrm))
+        for (int j = threadIdx.x; j < d; j += blockDim.x) v[size_t(b) * D + j] = y[size_t(b) * D + j] * inv;
+    if (threadIdx.x != 0) return;
+    const float r = __uint_as_float(st.resid[b]);
+    st.resid[b] = 0u;
+    if (debug) printf("nsdbg k=%d b=%d d=%d r=%g probe=%g\n", k, b, d, r, nrm);
+    int act = 1;
+    if (!(r <= kNsDiverged) || !(nrm <= kNsDiverged)) {  // diverging or non-finite: a damped eigenvalue <= 0
+        if (status[b] == 0) status[b] = ASG_ERR_NOT_PSD;
+        st.state[b] = 2;
+        st.xbuf[b] = (k + 1) & 1;
+        st.actX[b] = st.actM[b] = 0;
+        act = 0;
+    } else if (r <= kNsFinal && nrm <= kNsSpec) {
+        st.state[b] = 1;
+        st.actX[b] = 1;
+        st.actM[b] = 0;
+    } else if (k + 1 >= kNsMaxIter) {
+        // an eigenvalue stuck at x ~ 0 never leaves |1 - x| ~ 1: not PSD after damping
+        if (status[b] == 0) status[b] = fmaxf(r, nrm) > 0.5f ? ASG_ERR_NOT_PSD : ASG_ERR_NO_CONVERGENCE;
+        st.state[b] = 2;
+        st.xbuf[b] = (k + 1) & 1;
+        st.actX[b] = st.actM[b] = 0;
+        act = 0;
+    }
+    st.any[b] = act;
+}
+
+__global__ void ns_loop_kernel(NsState st, int nb, cudaGraphConditionalHandle handle) {
+    int a = 0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) a |= st.any[b];
+    a = __syncthreads_or(a);
+    if (threadIdx.x == 0) {
+        *st.iter += 1;
+        cudaGraphSetConditional(handle, a ? 1u : 0u);
+    }
+}
+
+// v = a fixed non-constant unit vector on the leading d (the spectral probe's start)
+__global__ void ns_probe_init_kernel(float* __restrict__ v, int d, int D, const int* __restrict__ gate) {
+    const int b = blockIdx.x;
+    if (!gate[b]) return;
+    __shared__ float red[32];
+    float sq = 0.f;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        const float x = 1.f + 0.5f * __sinf(0.7f * float(j));
+        sq += x * x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+        red[0] = rsqrtf(t);
+    }
+    __syncthreads();
+    const float inv = red[0];
+    for (int j = threadIdx.x; j < D; j += blockDim.x)
+        v[size_t(b) * D + j] = j < d ? (1.f + 0.5f * __sinf(0.7f * float(j))) * inv : 0.f;
+}
+
+// out = X[xbuf[b]] on the leading d x d, zero elsewhere (the padding of the
+// root slabs the update GEMMs read).
+__global__ void ns_finish_kernel(const float* __restrict__ X0h, const float* __restrict__ X0l,
+                                 const float* __restrict__ X1h, const float* __restrict__ X1l,
+                                 const int* __restrict__ xbuf, int d, int D, float* __restrict__ outh,
+                                 float* __restrict__ outl, const int* __restrict__ gate) {
+    const int b = blockIdx.y;
+    if (!gate[b]) return;
+    const size_t DD = size_t(D) * D, base = size_t(b) * DD;
+    const bool one = xbuf[b] != 0;
+    const float* sh = one ? X1h : X0h;
+    const float* sl = one ? X1l : X0l;
+    for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < DD; k += size_t(gridDim.x) * blockDim.x) {
+        const int i = int(k / D), j = int(k - size_t(i) * D);
+        const bool in = i < d && j < d;
+        outh[base + k] = in ? sh[base + k] : 0.f;
+        if (outl) outl[base + k] = in && sl ? sl[base + k] : 0.f;
+    }
+}
+
+// A' = A + eps I on the leading d x d (zero padding) as a split pair: the
+// refinement's operand.
+__global__ void ns_damped_split_kernel(const float* __restrict__ A, int d, int D, const float* __restrict__ eeff,
+                                       float* __restrict__ Ah, float* __restrict__ Al, const int* __restrict__ gate) {
+    const int b = blockIdx.y;
+    if (!gate[b]) return;
+    const float e = eeff[b];
+    const size_t DD = size_t(D) * D, base = size_t(b) * DD;
+    for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < DD; k += size_t(gridDim.x) * blockDim.x) {
+        const int i = int(k / D), j = int(k - size_t(i) * D);
+        const float a = (i < d && j < d) ? A[base + k] + (i == j ? e : 0.f) : 0.f;
+        float h, l;
+        split_tf32(a, h, l);
+        Ah[base + k] = h;
+        if (Al) Al[base + k] = l;
+    }
+}
+
+// X <- X + (E + E^T) / (2p) with E = X R, in place on the leading d x d
+// (32 x 32 tiles through shared memory for the transposed read).
+__global__ void ns_refine_kernel(float* __restrict__ Xh, float* __restrict__ Xl, const float* __restrict__ Eh,
+                                 const float* __restrict__ El, int d, int D, float inv2p,
+                                 const int* __restrict__ gate) {
+    __shared__ float tt[32][33];
+    const int b = blockIdx.z;
+    if (!gate[b]) return;
+    const size_t base = size_t(b) * D * D;
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    // E^T tile: tt[c][r] = E[j0 + r][i0 + c]
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const size_t o = base + size_t(j0 + r) * D + i0 + threadIdx.x;
+        tt[threadIdx.x][r] = Eh[o] + (El ? El[o] : 0.f);
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + r, j = j0 + int(threadIdx.x);
+        if (i >= d || j >= d) continue;
+        const size_t o = base + size_t(i) * D + j;
+        const float e = Eh[o] + (El ? El[o] : 0.f);
+        const float x = Xh[o] + (Xl ? Xl[o] : 0.f) + (e + tt[r][threadIdx.x]) * inv2p;
+        float h, l;
+        split_tf32(x, h, l);
+        Xh[o] = h;
+        if (Xl) Xl[o] = l;
+    }
+}
+
+// Pass gates: pass 1 takes every matrix; pass 2 retries, with the damping
+// lifted to the rounding floor, the matrices pass 1 found indefinite.
+// `status` here is the call's own status array (the caller's may already
+// hold another factor side's failure).
+__global__ void ns_gate_kernel(int* __restrict__ gate, int* __restrict__ status, int nb, int retry) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    if (!retry) {
+        gate[b] = 1;
+        status[b] = ASG_OK;
+    } else {
+        const int g = status[b] == ASG_ERR_NOT_PSD;
+        gate[b] = g;
+        if (g) status[b] = ASG_OK;
+    }
+}
+
+// Caller's status <- the call's first failure (never clears one).
+__global__ void ns_merge_status_kernel(const int* __restrict__ local, int* __restrict__ status, int nb) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nb && local[b] != ASG_OK && status[b] == ASG_OK) status[b] = local[b];
+}
+
+}  // namespace
+
+size_t ns_workspace_floats(int nb, int D) {
+    const size_t DD = size_t(D) * D;
+    // 8 split pairs (X0, X1, M0, M1, T0, T1, U, W) + power-iteration vectors/partials + scalars
+    return 16 * size_t(nb) * DD + 2 * size_t(nb) * D + 2 * size_t(nb) * (size_t(D) / kPowRows + 1) + 64 * size_t(nb) +
+           1024;  // (the scalar tail holds 4 float and 10 int arrays of nb)
+}
+
+void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps, int p, float* outh, float* outl,
+                        float* ws, int* caller_status, const int2* sym_tiles, int nsym, int precision, int num_sms,
+                        cudaStream_t s) {
+    const bool split = precision == ASG_PREC_3XTF32;
+    const size_t DD = size_t(D) * D, slab = size_t(nb) * DD;
+    float* w = ws;
+    auto take = [&](size_t n) {
+        float* r = w;
+        w += n;
+        return r;
+    };
+    float *X0h = take(slab), *X0l = take(slab), *X1h = take(slab), *X1l = take(slab);
+    float *M0h = take(slab), *M0l = take(slab), *M1h = take(slab), *M1l = take(slab);
+    float *T0h = take(slab), *T0l = take(slab), *T1h = take(slab), *T1l = take(slab);
+    float *Uh = take(slab), *Ul = take(slab), *Wh = take(slab), *Wl = take(slab);
+    const int nblk = (d + kPowRows - 1) / kPowRows;
+    float* v = take(size_t(nb) * D);
+    float* y = take(size_t(nb) * D);
+    float* part = take(size_t(nb) * nblk);
+    float* partf = take(size_t(nb) * nblk);
+    float* est = take(size_t(nb));
+    float* fro = take(size_t(nb));
+    float* cval = take(size_t(nb));
+    float* eeff = take(size_t(nb));
+    int* ints = reinterpret_cast<int*>(take(9 * size_t(nb) + 32));
+    NsState st{ints, ints + nb, ints + 2 * nb, ints + 3 * nb, reinterpret_cast<unsigned int*>(ints + 4 * nb),
+               ints + 9 * nb, ints + 5 * nb};
+    int* gate = ints + 6 * nb;
+    int* status = ints + 7 * nb;  // this call's status (merged into caller_status at the end)
+    if (!split) X0l = X1l = M0l = M1l = T0l = T1l = Ul = Wl = nullptr;
+    float* outl_ = split ? outl : nullptr;
+    const int pth = 256;
+    const size_t psm = size_t(d) * sizeof(float);
+    const int eblocks = int((DD + 255) / 256 < 1024 ? (DD + 255) / 256 : 1024);
+    const float pf = float(p);
+
+    auto gemm = [&](const float* ah, const float* al, const float* bh, const float* bl, int epi, float* dh, float* dl,
+                    const int* active, float* th, float* tl, bool sym, cudaStream_t st_) {
+        GemmLaunch g{};
+        g.A = Operand{ah, al, D, D};
+        g.B = Operand{bh, bl, D, D};
+        g.batch = nb;
+        g.epi = epi;
+        g.p.alpha = 1.f;
+        g.p.Dhi = dh;
+        g.p.Dlo = dl;
+        g.p.ldd = D;
+        g.p.d_bstride = int64_t(DD);
+        g.p.batch_active = active;
+        g.p.Thi = th;
+        g.p.Tlo = tl;
+        g.p.ns_a = (pf + 1.f) / pf;
+        g.p.ns_b = 1.f / pf;
+        g.p.resid = st.resid;
+        if (sym) {
+            g.sym_tiles = sym_tiles;
+            g.sym_tiles_count = nsym;
+        }
+        gemm_launch(g, precision, num_sms, st_);
+    };
+    // iteration k reads X_k, M_k, T_k from buffers k & 1 and writes buffers (k+1) & 1;
+    // the graph body holds two iterations (even, odd) so the buffer roles are static
+    auto iteration = [&](cudaStream_t st_, bool odd) {
+        const float *xh = odd ? X1h : X0h, *xl = odd ? X1l : X0l;
+        float *xnh = odd ? X0h : X1h, *xnl = odd ? X0l : X1l;
+        const float *mh = odd ? M1h : M0h, *ml = odd ? M1l : M0l;
+        float *mnh = odd ? M0h : M1h, *mnl = odd ? M0l : M1l;
+        const float *th = odd ? T1h : T0h, *tl = odd ? T1l : T0l;
+        float *tnh = odd ? T0h : T1h, *tnl = odd ? T0l : T1l;
+        gemm(xh, xl, th, tl, EPI_SYM_SPLIT, xnh, xnl, st.actX, nullptr, nullptr, true, st_);  // X T
+        if (p == 2) {
+            gemm(th, tl, mh, ml, EPI_SYM_SPLIT, Wh, Wl, st.actM, nullptr, nullptr, true, st_);  // W = T M
+            gemm(th, tl, Wh, Wl, EPI_NS, mnh, mnl, st.actM, tnh, tnl, true, st_);               // M = T W
+        } else {
+            gemm(th, tl, th, tl, EPI_SYM_SPLIT, Uh, Ul, st.actM, nullptr, nullptr, true, st_);  // U = T T
+            gemm(Uh, Ul, mh, ml, EPI_SYM_SPLIT, Wh, Wl, st.actM, nullptr, nullptr, true, st_);  // W = U M
+            gemm(Uh, Ul, Wh, Wl, EPI_NS, mnh, mnl, st.actM, tnh, tnl, true, st_);               // M = U W
+        }
+    };
+    static std::mutex mu;
+    using Key = std::tuple<const void*, const void*, const void*, int, int, int, int, int, const void*>;
+    static std::map<Key, cudaGraphExec_t> cache;
+    const Key key{A, ws, status, nb, d, D, p, precision, sym_tiles};
+    static const int debug = getenv("ASG_NS_DEBUG") != nullptr ? 1 : 0;  // diagnostics: per-iteration residuals
+    cudaGraphExec_t exec = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) exec = it->second;
+    }
+    if (!exec) {
+        cudaStream_t cap;
+        cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+        cudaGraph_t g = nullptr;
+        cudaGraphCreate(&g, 0);
+        cudaGraphConditionalHandle handle;
+        cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault);  // enter the loop
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = handle;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t nloop;
+        cudaGraphAddNode(&nloop, g, nullptr, 0, &cp);
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+        for (int half = 0; half < 2; ++half) {
+            iteration(cap, half == 1);
+            // M_{k+1} sits in buffer (k+1) & 1: M1 after an even iteration, M0 after an odd one
+            ns_spec_kernel<<<dim3(nblk, nb), pth, psm, cap>>>(half ? M0h : M1h, half ? M0l : M1l, d, D, st.actM, v, y,
+                                                           part, nblk);
+            ns_decide_kernel<<<nb, 256, 0, cap>>>(st, nb, d, D, v, y, part, nblk, status, debug);
+            ns_loop_kernel<<<1, 256, 0, cap>>>(st, nb, handle);
+        }
+        cudaStreamEndCapture(cap, &body);
+        cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        cudaStreamDestroy(cap);
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = exec;
+    }
+
+    // Pass 1: damping eps as given. Pass 2: the matrices pass 1 found
+    // indefinite, with the damping lifted to the rounding floor (ns_floor):
+    // a PSD factor whose null space carries fp32 noise of either sign then
+    // gets finite roots, as with the F32 eigensolve's clamp; a genuinely
+    // indefinite one fails again (NotPsd). Pass 2 costs ~20 empty launches
+    // when nothing failed.
+    for (int pass = 0; pass < 2; ++pass) {
+        ns_gate_kernel<<<(nb + 255) / 256, 256, 0, s>>>(gate, status, nb, pass);
+        // ---- scale: c >= ~lambda_max(A') from ||A'||_F and a power estimate ----
+        ns_norm_kernel<<<nb, 256, 0, s>>>(y, v, part, nullptr, nblk, d, D, est, fro, 1, gate);
+        for (int it = 0; it < kPowerSteps; ++it) {
+            ns_power_kernel<<<dim3(nblk, nb), pth, psm, s>>>(A, d, D, eps, v, y, part, it == 0 ? partf : nullptr, nblk,
+                                                             gate);
+            ns_norm_kernel<<<nb, 256, 0, s>>>(y, v, part, it == 0 ? partf : nullptr, nblk, d, D, est, fro, 0, gate);
+        }
+        ns_init_kernel<<<dim3(eblocks, nb), 256, 0, s>>>(A, d, D, eps, est, fro, pf, pass ? ns_floor(d) : 0.f, M0h, M0l,
+                                                         T0h, T0l, X0h, X0l, cval, eeff, gate);
+        ns_state_init_kernel<<<(nb + 255) / 256, 256, 0, s>>>(st, est, fro, nb, status, gate);
+        ns_probe_init_kernel<<<nb, 256, 0, s>>>(v, d, D, gate);
+        cudaGraphLaunch(exec, s);
+        ns_finish_kernel<<<dim3(eblocks, nb), 256, 0, s>>>(X0h, X0l, X1h, X1l, st.xbuf, d, D, outh, outl_, gate);
+
+        // ---- one symmetric Newton refinement against A' itself -------------
+        // R = I - X^(p/2) A' X^(p/2), X <- X + (X R + R X) / (2p). The coupled
+        // iteration never revisits A', so the rounding of the ~3 products per
+        // iteration accumulates in X; this step removes its commuting part
+        // exactly and contracts the rest (tests/test_gpu_newton.py).
+        ns_damped_split_kernel<<<dim3(eblocks, nb), 256, 0, s>>>(A, d, D, eeff, Uh, Ul, gate);
+        const float* xph = outh;  // X^(p/2)
+        const float* xpl = outl_;
+        if (p == 4) {
+            gemm(outh, outl_, outh, outl_, EPI_SYM_SPLIT, T1h, T1l, gate, nullptr, nullptr, true, s);  // X^2
+            xph = T1h;
+            xpl = T1l;
+        }
+        // B = X^(p/2) A' (general product: A' does not commute with the rounded X)
+        gemm(xph, xpl, Uh, Ul, EPI_SPLIT, Wh, Wl, gate, nullptr, nullptr, false, s);
+        // R = I - B X^(p/2) into T0 (EPI_NS with T = 1 I - 1 acc; its M output goes to M0)
+        {
+            GemmLaunch g{};
+            g.A = Operand{Wh, Wl, D, D};
+            g.B = Operand{xph, xpl, D, D};
+            g.batch = nb;
+            g.epi = EPI_NS;
+            g.p.alpha = 1.f;
+            g.p.Dhi = M0h;
+            g.p.Dlo = M0l;
+            g.p.ldd = D;
+            g.p.d_bstride = int64_t(DD);
+            g.p.batch_active = gate;
+            g.p.Thi = T0h;
+            g.p.Tlo = T0l;
+            g.p.ns_a = 1.f;
+            g.p.ns_b = 1.f;
+            g.p.resid = st.resid;
+            g.sym_tiles = sym_tiles;
+            g.sym_tiles_count = nsym;
+            gemm_launch(g, precision, num_sms, s);
+        }
+        gemm(outh, outl_, T0h, T0l, EPI_SPLIT, X1h, X1l, gate, nullptr, nullptr, false, s);  // E = X R
+        ns_refine_kernel<<<dim3(D / 32, D / 32, nb), dim3(32, 8), 0, s>>>(outh, outl_, X1h, X1l, d, D, 0.5f / pf, gate);
+        count_launch(10 + 2 * kPowerSteps + 2 * (p == 2 ? 6 : 7) + (p == 4 ? 4 : 3));
+    }
+    ns_merge_status_kernel<<<(nb + 255) / 256, 256, 0, s>>>(status, caller_status, nb);
+    count_launch(1);
+}
+
+}  // namespace asg

@@ -238,6 +238,8 @@ struct asg_blockset {
     float* iw32[6] = {};
     // F32 refresh: tensor-core Jacobi workspace (side stream)
     float* tc_ws = nullptr;
+    // NEWTON refresh: coupled Newton-Schulz workspace (side stream)
+    float* ns_ws = nullptr;
     int* pair_status = nullptr;  // both-sides eigensolves: per-matrix status before the merge
     int* pair_ident = nullptr;   // both-sides eigensolves: per-matrix J = I flags
     bool fp64_jacobi = false;  // ASG_F32_FP64_JACOBI=1: F32 refresh with the fp64 block Jacobi (diagnostics)
@@ -316,7 +318,11 @@ bool is_precond(const asg_blockset* bs) { return bs->opt.method != ASG_METHOD_AD
 bool is_soap(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_SOAP; }
 bool is_kl(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_KL_SHAMPOO; }
 bool split_mode(const asg_blockset* bs) { return bs->precision == ASG_PREC_3XTF32; }
-bool f32_refresh(const asg_blockset* bs) { return bs->sc.refresh_mode == ASG_REFRESH_F32; }
+// F32 and NEWTON: fp32-level refresh (NEWTON: Newton-Schulz roots for Shampoo / KL)
+bool f32_refresh(const asg_blockset* bs) { return bs->sc.refresh_mode != ASG_REFRESH_F64; }
+bool newton_roots(const asg_blockset* bs) {
+    return bs->sc.refresh_mode == ASG_REFRESH_NEWTON && bs->opt.method != ASG_METHOD_SOAP;
+}
 // Relative threshold of the F32 refresh's Jacobi (asg_eigh.cuh EighOpts).
 constexpr double kF32RefreshTolDefault = 1e-6;
 // ASG_F32_TOL overrides the threshold (diagnostics / tuning).
@@ -503,7 +509,7 @@ void alloc_group(asg_blockset* bs, Group& g) {
         pair_nn(g.sPRh, g.sPRl);
         launch_identity_split(g.PLh, g.PLl, g.nb, g.M, g.m, s);
         launch_identity_split(g.PRh, g.PRl, g.nb, g.N, g.n, s);
-        if (f32_refresh(bs)) {  // basis of the last refresh, identity before the first
+        if (f32_refresh(bs) && !newton_roots(bs)) {  // basis of the last refresh, identity before the first
             pair_mm(g.BLh, g.BLl);
             pair_mm(g.BLTh, g.BLTl);
             pair_nn(g.BRh, g.BRl);
@@ -512,7 +518,7 @@ void alloc_group(asg_blockset* bs, Group& g) {
             launch_identity_split(g.BLTh, g.BLTl, g.nb, g.M, g.m, s);
             launch_identity_split(g.BRh, g.BRl, g.nb, g.N, g.n, s);
             launch_identity_split(g.BRTh, g.BRTl, g.nb, g.N, g.n, s);
-        } else {
+        } else if (!f32_refresh(bs)) {
             g.EL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
             g.ER64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
         }
@@ -592,7 +598,11 @@ void alloc_workspace(asg_blockset* bs) {
     bs->ws_out = dalloc<double>(bs, nn);
     bs->ws_vals = dalloc<double>(bs, size_t(nmax) * bs->ws_chunk * 2);
     bs->ws_eps = dalloc<double>(bs, size_t(bs->ws_chunk) * 2);
-    if (f32_refresh(bs)) {
+    if (newton_roots(bs)) {
+        int Dmax = 0;
+        for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
+        bs->ns_ws = dalloc<float>(bs, ns_workspace_floats(bs->ws_chunk, Dmax));
+    } else if (f32_refresh(bs)) {
         int Dmax = 0;
         for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
         bs->tw_slab = size_t(Dmax) * Dmax;
@@ -1171,6 +1181,40 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
     pt.report(d, nb);
 }
 
+// NEWTON refresh of one chunk (Shampoo / KL-Shampoo): per side, the damped
+// snapshot's inverse root by coupled Newton-Schulz straight into the shadow
+// roots (compute_refresh precond.cpp:136-140: inv_root(F, 4, damping tr/n));
+// KL-Shampoo also forms F^-1 = (F^-1/2)^2 (one symmetric GEMM).
+void refresh_newton(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
+    PhaseTimer pt(s);
+    pt.mark("start");
+    for (int side = 0; side < 2; ++side) {
+        const bool left = side == 0;
+        const int d = left ? g.m : g.n, D = left ? g.M : g.N;
+        const size_t DD = size_t(D) * D;
+        const float* snap = at(left ? g.snapL : g.snapR, DD, s0);
+        launch_relative_damping_f32(snap, cnt, D, d, bs->opt.damping, bs->ws_eps, s);
+        float* ph = at(left ? g.sPLh : g.sPRh, DD, s0);
+        float* pl = at(left ? g.sPLl : g.sPRl, DD, s0);
+        const int2* tiles = left ? g.tilesM : g.tilesN;
+        const int ntiles = left ? g.ntM : g.ntN;
+        launch_ns_inv_root(snap, cnt, d, D, bs->ws_eps, is_kl(bs) ? 2 : 4, ph, pl, bs->ns_ws, g.d_status + s0, tiles,
+                           ntiles, bs->precision, bs->num_sms, s);
+        if (is_kl(bs)) {
+            GemmParams pk{};
+            pk.alpha = 1.f;
+            pk.Dhi = at(left ? g.sKLh : g.sKRh, DD, s0);
+            pk.Dlo = at(left ? g.sKLl : g.sKRl, DD, s0);
+            pk.ldd = D;
+            pk.d_bstride = int64_t(DD);
+            run_gemm(bs, op(ph, pl, D, D), op(ph, pl, D, D), cnt, EPI_SYM_SPLIT, pk, tiles, ntiles, s,
+                     double(cnt) * d * double(d) * d);
+        }
+    }
+    pt.mark("newton roots");
+    pt.report(g.m, cnt);
+}
+
 // Launches the refresh for every unit marked dispatched-but-not-launched.
 void launch_refreshes(asg_blockset* bs) {
     std::vector<std::vector<int>> per_group(bs->groups.size());
@@ -1207,7 +1251,9 @@ void launch_refreshes(asg_blockset* bs) {
             while (j < slots.size() && slots[j] == slots[j - 1] + 1 && int(j - i) < bs->ws_chunk) ++j;
             const int s0 = slots[i], cnt = int(j - i);
             CK(cudaMemsetAsync(g.d_status + s0, 0, size_t(cnt) * sizeof(int), bs->side));
-            if (f32_refresh(bs)) {
+            if (newton_roots(bs)) {
+                refresh_newton(bs, g, s0, cnt, bs->side);
+            } else if (f32_refresh(bs)) {
                 if (g.m == g.n && g.m > kSmallEighN && !bs->fp64_jacobi) {
                     refresh_sides_f32(bs, g, s0, cnt, 2, true, bs->side);
                 } else {
@@ -1688,6 +1734,7 @@ int asg_config_from_json(const char* text, asg_optimizer_config* opt, asg_schedu
                 const std::string r = str(g, "refresh");
                 if (r == "f64") s.refresh_mode = ASG_REFRESH_F64;
                 else if (r == "f32") s.refresh_mode = ASG_REFRESH_F32;
+                else if (r == "newton") s.refresh_mode = ASG_REFRESH_NEWTON;
                 else throw Fail{ASG_ERR_CONFIG_INVALID, "unknown refresh: " + r};
             }
             if (g.has("install_mode")) {
@@ -1732,7 +1779,8 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         validate(*opt);
         if (sched->staleness_S < 0) throw Fail{ASG_ERR_CONFIG_INVALID, "staleness_S must be >= 0"};
         if (sched->pf < 1) throw Fail{ASG_ERR_CONFIG_INVALID, "pf must be >= 1"};
-        if (sched->refresh_mode != ASG_REFRESH_F64 && sched->refresh_mode != ASG_REFRESH_F32)
+        if (sched->refresh_mode != ASG_REFRESH_F64 && sched->refresh_mode != ASG_REFRESH_F32 &&
+            sched->refresh_mode != ASG_REFRESH_NEWTON)
             throw Fail{ASG_ERR_CONFIG_INVALID, "unknown refresh_mode"};
         if (sched->pf != opt->precondition_frequency)
             throw Fail{ASG_ERR_CONFIG_INVALID, "async.pf must equal optimizer.precondition_frequency"};

@@ -113,6 +113,19 @@ class AsteriaOptimizer:
         check(lib.asg_blockset_block_info(self._h, idx, C.byref(i)))
         return i
 
+    def read_block(self, idx, role):
+        """One state tensor of owned block `idx` as fp64 host array (the
+        per-block accessors of precond.hpp:63-75; parity checks)."""
+        import numpy as np
+        i = self.block_info(idx)
+        m, n = i.spec.row_end - i.spec.row_begin, i.spec.col_end - i.spec.col_begin
+        shape = {abi.FACTOR_L: (m, m), abi.FACTOR_R: (n, n), abi.INV_L: (m, m), abi.INV_R: (n, n),
+                 abi.BASIS_L: (m, m), abi.BASIS_R: (n, n), abi.ROTATED_M: (m, n), abi.ROTATED_V: (m, n),
+                 abi.KL_INV_L: (m, m), abi.KL_INV_R: (n, n), abi.EIGVALS_L: (m,), abi.EIGVALS_R: (n,)}[role]
+        out = np.empty(shape)
+        check(lib.asg_block_read(self._h, idx, role, out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
+        return out
+
     def stats(self):
         s = abi.PoolStats()
         check(lib.asg_get_stats(self._h, C.byref(s)))

@@ -1,0 +1,5 @@
+# Full GPU suite + smoke (TAG names the log).
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q --tb=short > gpurun_out/r02_pytest_gpu_${TAG}.log 2>&1
+tail -15 gpurun_out/r02_pytest_gpu_${TAG}.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" 2>&1 | tail -8
