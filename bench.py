@@ -2,29 +2,42 @@
 # SPDX-License-Identifier: Apache-2.0
 """Benchmark of the B200 Asteria optimizer step (SOAP / KL-Shampoo / Shampoo).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl ours|reference]
 
 A step = one full optimizer step over the workload's parameter blocks:
-global-norm clip scale, Kronecker statistics, bounded-staleness refresh
-(dispatched every pf steps on a low-priority side stream), preconditioned
-update + apply; at N > 1 the blocks are ownership-sharded and the updated
-parameters are all-gathered over NCCL. Gradients are synthetic (sigma =
-1/sqrt(cols), fixed per run; every step's inputs, > L2, are read from HBM).
+fresh synthetic gradients, global-norm clip scale, Kronecker statistics,
+bounded-staleness refresh (dispatched every pf steps on a low-priority side
+stream), preconditioned update + apply; at N > 1 the blocks are
+ownership-sharded and the updated parameters are all-gathered over NCCL.
+
+Gradients are regenerated on the device EVERY step: block b at
+step t is N(0, 1/cols) from a Philox generator keyed (1234, t, b), written
+by its owner rank inside the timed region (its cost is included and
+reported as synth_ms_per_step). The factors therefore change every step and
+every refresh does real work (no refresh finds its factor already
+diagonal in the previous basis).
 
 Workloads (BASELINE.json configs):
   C1  Shampoo, one 1024x1024 block, EMA b2=0.95, pf=1, S=0 (reference's quadratic_shampoo.json)
-  C2  SOAP, GPT-2-small layer set (124M params, block 1024, 171 blocks), pf=10, S=5   [default]
-  C3  KL-Shampoo, LLaMA-shaped 1B layer set (256 blocks of 2048^2), pf=10, S=5
+  C2  SOAP, GPT-2-small layer set (124M params, block 1024, 171 blocks), pf=10, S=5
+  C3  KL-Shampoo, LLaMA-shaped 1B layer set (256 blocks of 2048^2), pf=10, S=5   [default:
+      the largest single-GPU config and the north_star target]
   C4  SOAP, the same 256 blocks, ownership-sharded across N GPUs, pf=10, S=5
+  C5  the refresh alone: batched eigensolve (--refresh f32) or Newton-Schulz
+      inverse roots (--refresh newton) of B_n = 2^31/n^2 factors, n = --n
 
 Prints ONE JSON line on rank 0. `value` is algorithmic TFLOP/s of the whole
 job (flop conventions of SURVEY.md 8(d)), `ms_per_step` the step latency.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU).
 """
 import argparse
 import json
 import math
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -170,81 +183,90 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # CPU baseline (oracle port; test infrastructure, used only as the timed CPU leg)
 # ---------------------------------------------------------------------------
-def cpu_baseline(wl, budget_s=20.0):
-    """Times the fp64 oracle (a restatement of the reference's hot path, built
-    -O3 as the reference's Release flags) on a bounded sample and extrapolates
-    to the workload: per-block step work scales as mn(m+n), refresh as n^3
-    (Jacobi); the step runs single-threaded per rank (harness.cpp:448), the
-    refresh on a pool of nproc threads (harness.cpp:312-316)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(wl, native=False, refresh_n=512):
+    """The fp64 oracle (a restatement of the reference's hot path, -O3 as the
+    reference's Release flags; native=True: the same sources -O3
+    -march=native compiled on this host) timed on:
+      * one block step (accumulate_factors + precondition + apply) at the
+        workload's dominant block shape, single thread (the reference runs its
+        per-block loop on one thread per rank, harness.cpp:448);
+      * one refresh (compute_refresh + install, precond.cpp:129-164) of a
+        refresh_n x refresh_n block: the oracle's cyclic Jacobi needs minutes
+        per 2048^2 factor, so the refresh is sampled at n = 512 and scaled by
+        n^3, spread over the host's cores (the reference's refresh pool,
+        harness.cpp:312-316).
+    Extrapolated to the workload by block count and shape (step: mn(m+n);
+    refresh: m^3 + n^3, amortised over pf). Returns the measured sample times,
+    the extrapolation and the resulting per-step time."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
     import orc
     from paper_2605_16184_b200 import abi
+    orc.use_build(native)
     meth = {"SOAP": abi.SOAP, "KL-Shampoo": abi.KL_SHAMPOO, "Shampoo": abi.SHAMPOO}[wl["method"]]
     cfg = orc.defaults_for(meth)
     cfg.precondition_frequency = wl["pf"]
-    ns = 384  # sample block side
-    blk = orc.Block(ns, ns, meth)
-    theta = np.zeros((ns, ns))
-    g = orc.random_matrix(ns, ns, 1) / math.sqrt(ns)
-    # warm factors, then time the per-step path
+    blocks = [b for s in wl["shapes"] for b in blocks_of(s, wl["limit"])]
+    m, n = max(set(blocks), key=blocks.count)  # dominant shape
+    g = orc.random_matrix(m, n, 1) / math.sqrt(n)
+    theta = np.zeros((m, n))
+    blk = orc.Block(m, n, meth)
+    # the update path of a refreshed block (version > 0): identity inverses/bases installed
+    blk.set_counters(1, 0, 0)
+    t0 = time.perf_counter()
     orc.accumulate_factors(blk, g, cfg)
-    orc.refresh_inverse(blk, cfg, 0)
+    theta = orc.apply_update(theta, orc.step_update(blk, g, cfg), cfg)
+    t_step = time.perf_counter() - t0
+    r = refresh_n
+    rb = orc.Block(r, r, meth)
+    for k in range(3):
+        orc.accumulate_factors(rb, orc.random_matrix(r, r, 10 + k) / math.sqrt(r), cfg)
     t0 = time.perf_counter()
-    nstep = 0
-    while time.perf_counter() - t0 < budget_s / 2 or nstep < 1:
-        orc.accumulate_factors(blk, g, cfg)
-        upd = orc.step_update(blk, g, cfg)
-        theta = orc.apply_update(theta, upd, cfg)
-        nstep += 1
-    t_step = (time.perf_counter() - t0) / nstep
+    orc.refresh_inverse(rb, cfg, 0)
+    t_ref = time.perf_counter() - t0
     cores = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    nref = 0
-    while time.perf_counter() - t0 < budget_s / 2 or nref < 1:
-        orc.refresh_inverse(blk, cfg, 1)
-        nref += 1
-    t_ref = (time.perf_counter() - t0) / nref
-    step_units = ns * ns * 2 * ns
-    ref_units = 2 * ns ** 3
-    tot_step = tot_ref = 0.0
-    for s in wl["shapes"]:
-        for (m, n) in blocks_of(s, wl["limit"]):
-            tot_step += t_step * (m * n * (m + n)) / step_units
-            tot_ref += t_ref * (m ** 3 + n ** 3) / ref_units
+    tot_step = sum(t_step * (bm * bn * (bm + bn)) / (m * n * (m + n)) for (bm, bn) in blocks)
+    tot_ref = sum(t_ref * (bm ** 3 + bn ** 3) / (2 * r ** 3) for (bm, bn) in blocks)
     t_per_step = tot_step + tot_ref / wl["pf"] / cores
     _, _, flops = alg_flops(wl)
     return {"value": flops / t_per_step / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-            "ms_per_step": t_per_step * 1e3,
-            "sample": (f"oracle (fp64 restatement, -O3) on one {ns}x{ns} {wl['method']} block: {nstep} steps "
-                       f"single-thread ({t_step*1e3:.1f} ms/step) + {nref} refreshes ({t_ref*1e3:.0f} ms, Jacobi); "
-                       f"extrapolated to the workload by mn(m+n) (step) and n^3 (refresh on {cores} threads, "
-                       f"amortized over pf={wl['pf']})")}
+            "ms_per_step": t_per_step * 1e3, "sample_wall_s": t_step + t_ref,
+            "extrapolation": t_per_step / (t_step + t_ref / wl["pf"]),
+            "sample": (f"oracle (fp64 restatement of the reference path, -O3{' -march=native' if native else ''}, "
+                       f"{cpu_model()}, {cores} cores): one {m}x{n} {wl['method']} block step single-thread "
+                       f"{t_step:.2f} s; one {r}x{r} refresh {t_ref:.2f} s (cyclic Jacobi); extrapolated to "
+                       f"{len(blocks)} blocks by mn(m+n) (step) and n^3 (refresh, {cores}-thread pool, every "
+                       f"pf={wl['pf']} steps)")}
 
 
-# ---------------------------------------------------------------------------
-# C5: batched eigensolve sweep point
-# ---------------------------------------------------------------------------
-def cpu_eigh_baseline(n, batch, budget_s=20.0):
+def cpu_eigh_baseline(n, batch, native=False, ns=384):
     """The oracle's cyclic Jacobi (densela.hpp:182-264 restated, -O3) on one
     384x384 SPD factor, extrapolated by n^3 and spread over nproc threads (the
     reference's refresh pool, harness.cpp:312-316)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import orc
-    ns = 384
+    orc.use_build(native)
     a = orc.random_spd(ns, 7)
     t0 = time.perf_counter()
-    k = 0
-    while time.perf_counter() - t0 < budget_s or k < 1:
-        orc.sym_eig(a)
-        k += 1
-    t1 = (time.perf_counter() - t0) / k
+    orc.sym_eig(a)
+    t1 = time.perf_counter() - t0
     cores = os.cpu_count() or 1
     t_total = t1 * (n / ns) ** 3 * batch / cores
     return {"value": 9.0 * n ** 3 * batch / t_total / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-            "ms_per_step": t_total * 1e3,
-            "sample": f"oracle cyclic Jacobi (fp64, -O3) on one {ns}x{ns} SPD factor: {k} solves, {t1*1e3:.0f} ms "
-                      f"each; extrapolated by n^3 to {batch} factors of n={n} on {cores} threads"}
+            "ms_per_step": t_total * 1e3, "sample_wall_s": t1, "extrapolation": t_total / t1,
+            "sample": f"oracle cyclic Jacobi (fp64, -O3{' -march=native' if native else ''}, {cpu_model()}) on one "
+                      f"{ns}x{ns} SPD factor: {t1*1e3:.0f} ms; extrapolated by n^3 to {batch} factors of n={n} on "
+                      f"{cores} threads"}
 
 
 def run_c5(args, rank, world, local):
@@ -271,8 +293,15 @@ def run_c5(args, rank, world, local):
     v = torch.empty(mine, n, n, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    newton = args.refresh == "newton"
+
     def solve():
-        if mine:
+        if not mine:
+            return
+        if newton:  # KL-Shampoo's L^-1/2 (p = 2) of every factor, relative damping 1e-8
+            rt.check(rt.lib.asg_inv_root_batched_f32(C.c_void_p(a.data_ptr()), C.c_void_p(v.data_ptr()), mine, n, 2,
+                                                     1e-8, 0, C.c_void_p(stream.cuda_stream or 1)))
+        else:
             rt.check(rt.lib.asg_sym_eig_batched_f32(C.c_void_p(a.data_ptr()), C.c_void_p(w.data_ptr()),
                                                     C.c_void_p(v.data_ptr()), mine, n, C.c_void_p(stream.cuda_stream or 1)))
 
@@ -303,20 +332,29 @@ def run_c5(args, rank, world, local):
         ms = t.item()
     k = min(mine, 2)
     ad, vd = a[:k].double(), v[:k].double()
-    resid = ((ad @ vd - vd * w[:k, None, :]).abs().amax() / ad.abs().amax()).item() if k else None
+    if newton:  # ||X A X - I|| of the inverse square root
+        eye = torch.eye(n, dtype=torch.float64, device=dev)
+        eps = 1e-8 * torch.diagonal(ad, dim1=1, dim2=2).sum(-1) / n
+        resid = ((vd @ (ad + eps[:, None, None] * eye) @ vd - eye).abs().amax()).item() if k else None
+    else:
+        resid = ((ad @ vd - vd * w[:k, None, :]).abs().amax() / ad.abs().amax()).item() if k else None
     if rank == 0:
-        flops = 9.0 * n ** 3 * total
+        flops = (10.0 if newton else 9.0) * n ** 3 * total
         peak, _, _, src = measured_peaks()
-        line = {"metric": "batched refresh eigensolve throughput (algorithmic TFLOP/s, 9n^3 per factor)",
+        line = {"metric": ("batched refresh inverse-root throughput (algorithmic TFLOP/s, 9n^3 + n^3 per factor)"
+                           if newton else "batched refresh eigensolve throughput (algorithmic TFLOP/s, 9n^3 per factor)"),
                 "value": flops * args.steps / (ms / 1e3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32 (3xTF32 tcgen05 block Jacobi, fp32 pair solves)",
+                "dtype": ("f32 (3xTF32 tcgen05 coupled Newton-Schulz, L^-1/2)" if newton
+                          else "f32 (3xTF32 tcgen05 block Jacobi, fp32 pair solves)"),
                 "data": "synthetic SPD factors X X^T/2n + 1e-3 I (cold solves)",
                 "config": {"workload": WORKLOADS["C5"]["name"], "n": n, "factors": total,
                            "parallelism": f"factor-sharded x{world}" if world > 1 else "single",
-                           "l2": "inputs > L2 (8 GiB of factors per step)", "max_residual_rel": resid},
-                "roofline": {"kernel": "tj_apply_kernel + tj_pair_kernel (algorithmic 9n^3 vs tensor peak)",
+                           "l2": "inputs > L2 (8 GiB of factors per step)", "refresh": args.refresh,
+                           ("max_abs_XAX_minus_I" if newton else "max_residual_rel"): resid},
+                "roofline": {"kernel": ("gemm_tn_kernel EPI_SYM_SPLIT/EPI_NS chain (algorithmic 10n^3 vs tensor peak)"
+                                        if newton else "tj_apply_kernel + tj_pair_kernel (algorithmic 9n^3 vs tensor peak)"),
                              "bound": "tensor", "achieved": flops * args.steps / (ms / 1e3) / 1e12 / world,
                              "peak": peak, "unit": "TFLOP/s",
                              "frac": flops * args.steps / (ms / 1e3) / 1e12 / world / peak,
@@ -324,7 +362,7 @@ def run_c5(args, rank, world, local):
                 "gpu_launches": lc1.value - lc0.value, "clocks": clk.summary(),
                 "e2e": None}
         if not args.no_cpu_baseline:
-            cb = cpu_eigh_baseline(n, total)
+            cb = cpu_eigh_baseline(n, total)  # the reference refresh is an eigendecomposition either way
             line["cpu_baseline"] = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -335,20 +373,45 @@ def run_c5(args, rank, world, local):
 # ---------------------------------------------------------------------------
 # main
 # ---------------------------------------------------------------------------
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_distributed(n):
+    """`bench.py --gpus N` outside torchrun: one rank per GPU under
+    torch.distributed.run (the launch the driver uses)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def pct(xs, q):
+    if not xs:
+        return None
+    xs = sorted(xs)
+    k = min(len(xs) - 1, max(0, int(math.ceil(q / 100.0 * len(xs))) - 1))
+    return xs[k]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default=os.environ.get("ASG_WORKLOAD", "C2"), choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=os.environ.get("ASG_WORKLOAD", "C3"), choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32"])
-    ap.add_argument("--refresh", default="f32", choices=["f32", "f64"],
-                    help="refresh arithmetic: f32 = fp32-level tensor-core refresh (default), "
-                         "f64 = reference-tight fp64 eigensolve")
+    ap.add_argument("--refresh", default="newton", choices=["newton", "f32", "f64"],
+                    help="refresh arithmetic: newton = Newton-Schulz roots for Shampoo/KL (SOAP: f32 eigensolve), "
+                         "f32 = fp32-level tensor-core eigensolve, f64 = reference-tight fp64 eigensolve")
     ap.add_argument("--n", type=int, default=2048, help="C5: factor dimension of the sweep point")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fixed-grads", action="store_true", help="diagnostics: one gradient draw for the whole run")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -356,6 +419,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args.gpus)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.workload == "C5" and args.impl == "ours":
         run_c5(args, rank, world, local)
         return
@@ -363,7 +430,9 @@ def main():
     cfg_out = {"workload": wl["name"], "method": wl["method"], "blocks": sum(len(blocks_of(s, wl["limit"])) for s in wl["shapes"]),
                "params": sum(math.prod(s) for s in wl["shapes"]), "block_dim_limit": wl["limit"],
                "pf": wl["pf"], "staleness_S": wl["S"], "precision": args.precision, "refresh": args.refresh,
-               "parallelism": f"block-sharded x{args.gpus}" if args.gpus > 1 else "single",
+               "parallelism": f"block-sharded x{world}" if world > 1 else "single",
+               "gradients": ("fixed (diagnostics)" if args.fixed_grads else
+                             "fresh every step: Philox N(0, 1/cols) keyed (1234, step, block), on the owner"),
                "l2": "inputs > L2 (every step streams all state and gradients from HBM)",
                "alg_tflop_per_step": flops / 1e12}
 
@@ -372,27 +441,33 @@ def main():
             return
         if args.workload == "C5":
             total = (1 << 31) // (args.n * args.n)
-            cb = cpu_eigh_baseline(args.n, total, budget_s=max(10.0, 3.0 * args.steps))
+            cb = cpu_eigh_baseline(args.n, total)
             cfg_out = {"workload": wl["name"], "n": args.n, "factors": total}
         else:
-            cb = cpu_baseline(wl, budget_s=max(10.0, 3.0 * args.steps))
+            cb = cpu_baseline(wl)
         metric = ("batched refresh eigensolve throughput (algorithmic TFLOP/s, 9n^3 per factor)" if args.workload == "C5"
                   else "optimizer step throughput (algorithmic TFLOP/s); step latency in ms_per_step")
         line = {"impl": "reference", "metric": metric,
-                "value": cb["value"], "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+                "value": cb["value"], "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": 1,
+                "warmup": 0, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": cfg_out,
                 "cpu_baseline": {"value": cb["value"], "unit": "TFLOP/s", "cores": cb["cores"], "kind": "port",
-                                 "sample": cb["sample"]},
+                                 "sample": cb["sample"], "sample_wall_s": cb["sample_wall_s"],
+                                 "extrapolation": cb["extrapolation"]},
+                "note": ("the reference path (its own sources are unbuildable here: Eigen3 absent, DESIGN.md §4) "
+                         "restated as the fp64 oracle; one sampled block step + one sampled refresh were timed "
+                         f"({cb['sample_wall_s']:.1f} s of CPU work) and extrapolated x{cb['extrapolation']:.0f} "
+                         "to the workload's per-step time (ms_per_step)"),
                 "e2e": {"value": cb["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
 
+    import ctypes as C
     import torch
     import torch.distributed as dist
     from paper_2605_16184_b200 import abi, runtime
-    from paper_2605_16184_b200.optimizer import AsteriaOptimizer
+    from paper_2605_16184_b200.optimizer import AsteriaOptimizer, stream_arg
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -407,22 +482,39 @@ def main():
     sched = runtime.scheduler_defaults()
     sched.pf, sched.staleness_S = wl["pf"], wl["S"]
     sched.install_mode = abi.INSTALL_EVENT if wl["S"] > 0 else abi.INSTALL_SIM_CLOCK
-    sched.refresh_mode = abi.REFRESH_F32 if args.refresh == "f32" else abi.REFRESH_F64
-    # The cold first refresh (dispatched at step 0, no previous basis) must be
-    # installed before timing: its barrier fires at step S+1, so warm up past it.
+    sched.refresh_mode = {"f32": abi.REFRESH_F32, "f64": abi.REFRESH_F64, "newton": abi.REFRESH_NEWTON}[args.refresh]
+    # The cold first refresh (dispatched at step 0) must be installed before
+    # timing: its barrier fires at step S+1, so warm up past it.
     args.warmup = max(args.warmup, wl["S"] + 2)
     prec = abi.PREC_3XTF32 if args.precision == "3xtf32" else abi.PREC_TF32
 
     gen = torch.Generator(device=dev).manual_seed(1234)
     params, grads = [], []
     for s in wl["shapes"]:
-        cols = s[-1]
         params.append((torch.randn(*s, device=dev, generator=gen) * 0.02).contiguous())
-        grads.append((torch.randn(*s, device=dev, generator=gen) / math.sqrt(cols)).contiguous())
+        grads.append(torch.zeros(*s, device=dev))
+    sigma = [1.0 / math.sqrt(s[-1]) for s in wl["shapes"]]
     o = AsteriaOptimizer(params, grads, opt, sched, precision=prec, rank=rank, world=world, seed=1234)
     stream = torch.cuda.ExternalStream(o.stream_handle)
+    # this rank's units (blocks, or whole 1-D AdamW parameters): it writes their gradients
+    owned = []
+    for i in range(o.num_blocks):
+        info = o.block_info(i)
+        if info.owner_rank == rank:
+            sp = info.spec
+            owned.append((i, sp.param_index, sp.row_begin, sp.row_end, sp.col_begin, sp.col_end))
 
-    def one_step(step):
+    def synth(step):
+        """Fresh gradients of this rank's units: N(0, 1/cols), Philox keyed (1234, step, block)."""
+        for (i, p, r0, r1, c0, c1) in owned:
+            gen.manual_seed((1234 << 40) + (step << 20) + i)
+            g = grads[p]
+            view = g[r0:r1, c0:c1] if g.dim() == 2 else g[c0:c1]
+            view.normal_(0.0, sigma[p], generator=gen)
+
+    def one_step(step, fresh=True):
+        if fresh and not args.fixed_grads:
+            synth(step)
         norm = math.sqrt(o.grad_sqnorm())             # D2H of the clip statistic (harness.cpp:435)
         o.step(step, clip_scale=o.clip_scale_from_norm(norm), lr_scale=1.0)
         if world > 1:
@@ -434,94 +526,108 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(x):
+        if world > 1:
+            t = torch.tensor([x], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.item()
+        return x
+
+    if args.fixed_grads:
+        synth(0)
     step = 0
     for _ in range(args.warmup):
         one_step(step)
         step += 1
     barrier()
+    # cost of the gradient synthesis alone (reported; it is inside the timed steps)
+    cur = torch.cuda.current_stream(dev)
+    es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es0.record(cur)
+    for k in range(3):
+        synth(10 ** 6 + k)
+    es1.record(cur)
+    barrier()
+    synth_ms = es0.elapsed_time(es1) / 3 if not args.fixed_grads else 0.0
 
-    # ---- timed region: inputs resident in HBM ----
+    # ---- timed region: inputs resident in HBM (regenerated on the device each step) ----
     o.profile(True)
     o.kernel_stats(reset=True)
+    o.hbm_stats(reset=True)
     st0 = o.stats()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    installs = []
     with ClockSampler(local) as clk:
         barrier()
-        e0.record(stream)
-        t_wall0 = time.perf_counter()
-        for _ in range(args.steps):
+        for k in range(args.steps):
+            evs[k].record(cur)
+            i0 = o.stats().installed
             one_step(step)
+            installs.append(o.stats().installed - i0)
             step += 1
-        # the last all-gather runs on the caller's stream: end the region after it
-        cur = torch.cuda.current_stream(dev)
+        # the step (and the last all-gather) end on the caller's stream
         cur.wait_stream(stream)
-        e1.record(cur)
-        stream.wait_stream(cur)
+        evs[-1].record(cur)
         barrier()
-        t_wall = time.perf_counter() - t_wall0
     ks = o.kernel_stats(reset=True)
+    hb = o.hbm_stats(reset=True)
     o.profile(False)
     st1 = o.stats()
-    ms = e0.elapsed_time(e1)
-    ms = max(ms, t_wall * 1e3 * 0.0)  # device-timed
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+    per_step = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    ms = max_over_ranks(evs[0].elapsed_time(evs[-1]))
     ms_per_step = ms / args.steps
     value = flops * args.steps / (ms / 1e3) / 1e12
+    with_inst = [t for t, n in zip(per_step, installs) if n > 0]
+    without = [t for t, n in zip(per_step, installs) if n == 0]
 
-    # ---- e2e: pinned H2D of each step's gradients + D2H of the clip statistic ----
+    # ---- e2e: each step's gradients from pinned host memory (H2D in the timed
+    # region, double-buffered on a copy stream as a data loader would) + D2H of
+    # the clip statistic ----
     e2e = None
     if not args.no_e2e:
-        # Each step's gradients arrive from pinned host memory. The H2D of step
-        # k+1 streams into a staging buffer on a copy stream while step k
-        # computes (double buffering, as a data loader would); step k+1 then
-        # moves them into the bound gradient tensors with a device copy.
-        # One flat pinned host batch (as a data loader would hand over) and one
-        # flat device staging buffer: a single large DMA per step instead of one
-        # copy per parameter tensor.
-        total = sum(g.numel() for g in grads)
-        host_flat = torch.empty(total, dtype=torch.float32).pin_memory()
-        staging_flat = torch.empty(total, dtype=torch.float32, device=dev)
-        staging, off = [], 0
-        for g in grads:
-            host_flat[off:off + g.numel()].copy_(g.reshape(-1).cpu())
-            staging.append(staging_flat[off:off + g.numel()].view_as(g))
-            off += g.numel()
-        h2d = total * 4
+        stride = o.gather_stride()
+        shard = o.shard_elems(rank)
+        send = torch.zeros(stride * world, dtype=torch.float32, device=dev)
+        ring = []
+        for r in range(3):  # three distinct host batches (fresh Philox draws), cycled
+            synth(2 * 10 ** 6 + r)
+            runtime.check(runtime.lib.asg_pack_grads(o._h, C.c_void_p(send.data_ptr()), stream_arg(cur)))
+            h = torch.empty(shard, dtype=torch.float32).pin_memory()
+            h.copy_(send[rank * stride: rank * stride + shard])
+            ring.append(h)
+        del send
+        staging = [torch.empty(max(1, shard), dtype=torch.float32, device=dev) for _ in range(2)]
         copy_stream = torch.cuda.Stream(dev)
-        ev_copied, ev_consumed = torch.cuda.Event(), torch.cuda.Event()
-        cur = torch.cuda.current_stream(dev)
+        ev_copied = [torch.cuda.Event() for _ in range(2)]
+        ev_consumed = [torch.cuda.Event() for _ in range(2)]
 
-        def prefetch():
+        def prefetch(k):
             with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(ev_consumed)  # staging free once the previous step took it
-                staging_flat.copy_(host_flat, non_blocking=True)
-                ev_copied.record(copy_stream)
+                copy_stream.wait_event(ev_consumed[k % 2])  # staging free once the step two back took it
+                staging[k % 2][:shard].copy_(ring[k % 3], non_blocking=True)
+                ev_copied[k % 2].record(copy_stream)
 
         n_e2e = max(3, args.steps // 2)
-        ev_consumed.record(cur)
+        for e in ev_consumed:
+            e.record(cur)
         barrier()
         t0 = time.perf_counter()
-        prefetch()
+        prefetch(0)
         for k in range(n_e2e):
-            cur.wait_event(ev_copied)
-            for g, st_ in zip(grads, staging):
-                g.copy_(st_, non_blocking=True)
-            ev_consumed.record(cur)
+            cur.wait_event(ev_copied[k % 2])
+            # owner-major segment -> this rank's gradient slices (one kernel)
+            runtime.check(runtime.lib.asg_unpack_reduced_grads(o._h, C.c_void_p(staging[k % 2].data_ptr()), 1.0,
+                                                               stream_arg(cur)))
+            ev_consumed[k % 2].record(cur)
             if k + 1 < n_e2e:
-                prefetch()
-            one_step(step)
+                prefetch(k + 1)
+            one_step(step, fresh=False)
             step += 1
         barrier()
-        t_e2e = (time.perf_counter() - t0) * 1e3
-        if world > 1:
-            t = torch.tensor([t_e2e], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = t.item()
+        t_e2e = max_over_ranks((time.perf_counter() - t0) * 1e3)
         e2e = {"value": flops * n_e2e / (t_e2e / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t_e2e / n_e2e,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 12}
+               "h2d_bytes_per_step": shard * 4, "d2h_bytes_per_step": 12,
+               "note": "host-clock over the e2e steps; three distinct pinned host gradient batches cycled"}
 
     if rank != 0:
         if world > 1:
@@ -530,15 +636,27 @@ def main():
         return
     peak, peak_sus, hbm, peak_src = measured_peaks()
     ach = ks.gemm_alg_flops / (ks.gemm_ms / 1e3) / 1e12 if ks.gemm_ms > 0 else None
+    hbm_kernels = {}
+    for name, (nl, nbytes, kms) in hb.items():
+        if nl:
+            hbm_kernels[name] = {"gbs": nbytes / (kms / 1e3) / 1e9 if kms > 0 else None,
+                                 "ms_per_step": kms / args.steps, "bytes_per_launch": nbytes / nl,
+                                 "frac_of_hbm_peak": (nbytes / (kms / 1e3) / 1e9 / hbm) if kms > 0 else None}
     line = {
         "metric": "optimizer step throughput (algorithmic TFLOP/s); step latency in ms_per_step",
-        "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": ("f32 (3xTF32 tensor-core products; " +
-                  ("fp32-level refresh: tensor-core block Jacobi)" if args.refresh == "f32" else "fp64 refresh)")
-                  if prec == abi.PREC_3XTF32 else "tf32"),
-        "data": "synthetic (N(0, 1/cols) gradients, fixed per run; random-init parameters)",
+                  {"f32": "fp32-level refresh: tensor-core block Jacobi)",
+                   "newton": "fp32-level refresh: Newton-Schulz roots (SOAP: tensor-core block Jacobi))",
+                   "f64": "fp64 refresh)"}[args.refresh] if prec == abi.PREC_3XTF32 else "tf32"),
+        "data": "synthetic (fresh N(0, 1/cols) gradients every step, generated on the device; random-init parameters)",
         "config": cfg_out,
+        "step_ms": {"p50": pct(per_step, 50), "p99": pct(per_step, 99),
+                    "with_install": {"n": len(with_inst), "p50": pct(with_inst, 50), "p99": pct(with_inst, 99)},
+                    "without_install": {"n": len(without), "p50": pct(without, 50), "p99": pct(without, 99)},
+                    "per_step": [round(t, 3) for t in per_step], "installs_per_step": installs},
+        "synth_ms_per_step": synth_ms,
         "roofline": {"kernel": "tcgen05 TN GEMMs of the step, fused epilogues (refresh GEMMs on the side stream excluded)", "bound": "tensor",
                      "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                      "frac": (ach / peak) if ach else None,
@@ -547,16 +665,24 @@ def main():
                      "frac_of_mode_peak": (ach / (peak / 2 / (3 if prec == abi.PREC_3XTF32 else 1))) if ach else None,
                      "gemm_launches": ks.gemm_launches, "gemm_ms_per_step": ks.gemm_ms / args.steps,
                      **traffic_for(args.workload)},
+        "hbm_kernels": hbm_kernels,
         "gpu_launches": ks.launches,
         "clocks": clk.summary(),
         "schedule": {"dispatched": st1.dispatched - st0.dispatched, "installed": st1.installed - st0.installed,
-                     "barrier_waits": st1.barrier_waits - st0.barrier_waits},
+                     "barrier_waits": st1.barrier_waits - st0.barrier_waits,
+                     "barrier_wait_ms": (st1.wait_total_us - st0.wait_total_us) / 1e3},
         "e2e": e2e,
         "state_bytes": o.state_bytes(),
     }
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         cb = cpu_baseline(wl)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "sample_wall_s",
+                                                   "extrapolation")}
+        try:
+            cn = cpu_baseline(wl, native=True)
+            line["cpu_baseline"]["native"] = {k: cn[k] for k in ("value", "sample_wall_s", "sample")}
+        except Exception as e:  # -march=native build unavailable on this host
+            line["cpu_baseline"]["native"] = {"unavailable": str(e)[:200]}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

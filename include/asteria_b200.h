@@ -335,6 +335,36 @@ int asg_pack_owned(asg_blockset* bs, float* sendbuf, void* stream);
  * padded to `stride_elems`) back into every parameter. */
 int asg_unpack_gathered(asg_blockset* bs, const float* recvbuf, int64_t stride_elems, void* stream);
 
+/* ---- bucketed parameter all-gather over NCCL --------
+ * Every shape's units are split into `buckets_per_shape` runs per rank; bucket
+ * (shape, c) holds run c of every rank (1-D AdamW parameters: one bucket). The
+ * plan depends only on the ownership plan, so all ranks hold the same list.
+ * Exchange buffer of a bucket: [world][stride] fp32, rank r's updated slices
+ * at r * stride (asg_bucket_stride). */
+int asg_set_allgather_buckets(asg_blockset* bs, int32_t buckets_per_shape);
+int asg_bucket_count(const asg_blockset* bs, int64_t* count);
+int asg_bucket_stride(const asg_blockset* bs, int64_t bucket, int64_t* stride);
+/* Packs this rank's updated slices of bucket `bucket` into sendbuf [stride]. */
+int asg_bucket_pack(asg_blockset* bs, int64_t bucket, float* sendbuf, void* stream);
+/* Scatters an all-gathered bucket buffer [world][stride] into every parameter. */
+int asg_bucket_unpack(asg_blockset* bs, int64_t bucket, const float* recvbuf, void* stream);
+/* NCCL is loaded at run time (libnccl.so.2). The unique id is 128 bytes
+ * (NCCL_UNIQUE_ID_BYTES); rank 0 creates it, the caller distributes it. The
+ * communicator is a ncclComm_t passed as void*, created on the current
+ * device. */
+int asg_nccl_unique_id(uint8_t* out);
+int asg_nccl_comm_init(int32_t world, int32_t rank, const uint8_t* id, void** comm);
+int asg_nccl_comm_destroy(void* comm);
+/* After asg_step: all-gathers every bucket over `comm` (ncclAllGather) on
+ * `stream` (ordered after the step) and scatters into every parameter. */
+int asg_allgather_params(asg_blockset* bs, void* comm, void* stream);
+/* Fused variant: with a communicator set (NULL unsets), asg_step /
+ * asg_precondition_apply update the blocks bucket by bucket and all-gather
+ * bucket b on a high-priority communication stream while the main stream
+ * updates bucket b+1; the step ends (on the main stream) after the last
+ * bucket's scatter. */
+int asg_set_allgather_comm(asg_blockset* bs, void* comm, int32_t buckets_per_shape);
+
 /* ---- profiling ---------------------------------------------------------- */
 typedef struct asg_kernel_stats {
     uint64_t launches;       /* kernels this library launched (process-wide counter delta) */
@@ -342,6 +372,19 @@ typedef struct asg_kernel_stats {
     double gemm_alg_flops;   /* algorithmic flops of those launches (SYRK: n^2 k, GEMM: 2 m n k) */
     double gemm_ms;          /* sum of their CUDA-event durations on the launching stream */
 } asg_kernel_stats;
+/* HBM-bound kernels of the step, timed while profiling (CUDA events on their
+ * launching stream), with their algorithmic bytes: the gradient prep
+ * (gather + clip scale + tf32 split + transpose; 4 B read + 16 B written per
+ * element), the clip norm (4 B/elt, harness.cpp:219-223) and the multi-tensor
+ * AdamW (28 B/elt, precond.cpp:229-251). */
+typedef enum asg_hbm_kind { ASG_HBM_PREP = 0, ASG_HBM_SQNORM = 1, ASG_HBM_ADAMW = 2, ASG_HBM_KINDS = 3 } asg_hbm_kind;
+typedef struct asg_hbm_stats {
+    uint64_t launches[ASG_HBM_KINDS];
+    double bytes[ASG_HBM_KINDS];
+    double ms[ASG_HBM_KINDS];
+} asg_hbm_stats;
+/* Synchronizes the device, returns the HBM-kernel stats since the last reset. */
+int asg_get_hbm_stats(asg_blockset* bs, asg_hbm_stats* out, int32_t reset);
 /* Process-wide count of kernel launches issued by this library (graph
  * replays count the kernels of one pass through the graph; sweeps repeated by
  * a device-driven WHILE loop are not counted again). */
@@ -367,6 +410,13 @@ int asg_sym_eig_batched(const double* A, double* values, double* vectors, int64_
  * [batch][n] ascending; n > 64. Same stopping rule as ASG_REFRESH_F32. */
 int asg_sym_eig_batched_f32(const float* A, double* values, float* vectors, int64_t batch, int64_t n,
                             void* stream);
+/* The NEWTON refresh's inverse root on its own (inv_root densela.hpp:267-282
+ * with relative_damping precond.cpp:121-125): out[b] = (A[b] + eps_b I)^(-1/p),
+ * eps_b = damping * tr(A[b]) / n, p in {2, 4}, by coupled Newton-Schulz
+ * iterations on the tensor cores. fp32 device buffers [batch][n][n], n <= 4096;
+ * precision: asg_precision of the products. Synchronizes the stream. */
+int asg_inv_root_batched_f32(const float* A, float* out, int64_t batch, int64_t n, int32_t p, double damping,
+                             int32_t precision, void* stream);
 
 #ifdef __cplusplus
 } /* extern "C" */

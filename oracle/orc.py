@@ -27,6 +27,22 @@ def build():
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
 
 
+NATIVE_PATH = os.path.join("/tmp", "asg_oracle_native", "liborc_native.so")
+
+
+def use_build(native=False):
+    """Selects the -O3 build (the reference's Release flags) or an
+    -O3 -march=native one compiled on this machine (make native) for
+    subsequent calls; objects created under one build must not be passed to
+    the other."""
+    global _lib, _LIB_PATH
+    path = NATIVE_PATH if native else os.path.join(_HERE, "build", "liborc.so")
+    if native and not os.path.exists(path):
+        subprocess.run(["make", "-s", "-C", _HERE, "native", f"NATIVE={path}"], check=True)
+    if path != _LIB_PATH:
+        _LIB_PATH, _lib = path, None
+
+
 def lib():
     global _lib
     if _lib is None:

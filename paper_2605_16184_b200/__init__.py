@@ -6,4 +6,4 @@ The product is the in-tree shared library ``csrc/build/libasteria_b200.so``
 immediately if it is missing or no sm_100a device is present; there is no CPU
 fallback.
 """
-__all__ = ["abi", "runtime", "precond", "config"]
+__all__ = ["abi", "runtime", "precond", "optimizer", "trace"]

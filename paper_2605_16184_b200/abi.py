@@ -161,6 +161,15 @@ class Event(C.Structure):
     ]
 
 
+HBM_PREP, HBM_SQNORM, HBM_ADAMW, HBM_KINDS = 0, 1, 2, 3
+HBM_NAMES = {HBM_PREP: "prep", HBM_SQNORM: "sqnorm", HBM_ADAMW: "adamw"}
+
+
+class HbmStats(C.Structure):
+    _fields_ = [("launches", C.c_uint64 * HBM_KINDS), ("bytes", C.c_double * HBM_KINDS),
+                ("ms", C.c_double * HBM_KINDS)]
+
+
 class KernelStats(C.Structure):
     _fields_ = [
         ("launches", C.c_uint64),

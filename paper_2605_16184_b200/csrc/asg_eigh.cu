@@ -461,13 +461,12 @@ void launch_eigh(const double* A, double* values, double* vectors, double* ws, i
     int* pflag = rotations + nb;
     int* loop_count = pflag + size_t(nb) * (m / 2);
     int* ntrue = loop_count + 1;  // n per matrix (uniform here)
-    static bool attr = false;
+    static std::atomic<uint64_t> attr_bits{0};
     const int smem = 2 * kP * (kP + 1) * int(sizeof(double));
-    if (!attr) {
+    if (first_on_device(attr_bits)) {
         cudaFuncSetAttribute(bj_pair_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(bj_apply_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(bj_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
     }
     const int debug = getenv("ASG_EIGH_DEBUG") != nullptr ? 1 : 0;
     const int rel = opts.relative ? 1 : 0;

@@ -259,8 +259,11 @@ __device__ __forceinline__ void apply_chunk(const GemmParams& p, int b, int row0
         for (int i = 0; i < 32; ++i) {
             if (i < rows) {
                 const float u = scratch[i][lane];
-                bad |= !isfinite(u);
-                __stcs(th + int64_t(i) * e.ld, t[i] - p.lr_eff * (u + p.wd * t[i]));
+                const bool ok = isfinite(u);
+                bad |= !ok;
+                // a non-finite update element leaves theta unchanged (the reference
+                // throws before touching theta, precond.cpp:248); the flag surfaces it
+                __stcs(th + int64_t(i) * e.ld, ok ? t[i] - p.lr_eff * (u + p.wd * t[i]) : t[i]);
             }
         }
     }

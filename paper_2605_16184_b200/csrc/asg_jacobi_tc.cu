@@ -1273,8 +1273,8 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
     int* rank = pflag + size_t(nb) * npairs;
     int* loop_count = rank + size_t(nb) * D;
 
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_bits{0};
+    if (first_on_device(attr_bits)) {
         cudaFuncSetAttribute(tj_apply_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kApplySmem));
         cudaFuncSetAttribute(tj_apply_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kApplySmem));
         cudaFuncSetAttribute(tj_pair_kernel<64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 65 * 4);
@@ -1282,7 +1282,6 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
         cudaFuncSetAttribute(tj_pair_kernel<128, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 128 * 129 * 4);
         cudaFuncSetAttribute(tj_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 4);
         cudaFuncSetAttribute(tj_sort_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8);
-        attr = true;
     }
     TJApply ap{};
     ap.Ah = Ah;

@@ -71,13 +71,18 @@ template <int BN, int NPASS, int EPI>
 cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                         const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
     using Cfg = GemmCfg<BN, NPASS>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    // the shared-memory limit is a per-device function attribute
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    cudaError_t de = cudaGetDevice(&dev);
+    if (de != cudaSuccess) return de;
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(attr_set.load() & bit)) {
         cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, NPASS, EPI>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(Cfg::kSmemBytes));
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.fetch_or(bit);
     }
     const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
     if (grid <= 0) return cudaSuccess;
@@ -427,7 +432,10 @@ __global__ void adamw_multi_kernel(const AdamEntry* __restrict__ entries, float 
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / en.cols, c = e % en.cols;
         const float g = scale_val * en.grad[r * en.ld_g + c];
-        bad |= !isfinite(g);
+        if (!isfinite(g)) {  // adamw_step throws NonFinite before touching state (precond.cpp:231)
+            bad = true;
+            continue;
+        }
         const float mm = b1 * en.m[e] + (1.f - b1) * g;
         const float vv = b2 * en.v[e] + (1.f - b2) * g * g;
         en.m[e] = mm;
@@ -637,11 +645,10 @@ __global__ void __launch_bounds__(kEigThreads) sym_eig_kernel(const double* __re
 
 void launch_sym_eig(const double* A, double* values, double* vectors, double* work, int nb, int n, int* status,
                     cudaStream_t s) {
-    static bool attr = false;
+    static std::atomic<uint64_t> attr_bits{0};
     const size_t smem = sizeof(double) * kMaxEigN;
-    if (!attr) {
+    if (first_on_device(attr_bits)) {
         cudaFuncSetAttribute(sym_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
     }
     sym_eig_kernel<<<nb, kEigThreads, smem, s>>>(A, values, vectors, work, n, status);
     count_launch();

@@ -6,11 +6,21 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "asg_gemm.cuh"
 
 namespace asg {
+
+// True the first time it is called for the current device with `bits`:
+// function attributes (dynamic shared-memory limits) are per device.
+inline bool first_on_device(std::atomic<uint64_t>& bits) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t b = uint64_t(1) << (dev & 63);
+    return !(bits.fetch_or(b) & b);
+}
 
 // Process-wide count of kernels launched by this library.
 uint64_t launch_count();

@@ -42,6 +42,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "../../include/asteria_b200.h"
 #include "asg_eigh.cuh"
@@ -544,86 +545,55 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
             gemm(Uh, Ul, Wh, Wl, EPI_NS, mnh, mnl, st.actM, tnh, tnl, true, st_);               // M = U W
         }
     };
-    static std::mutex mu;
-    using Key = std::tuple<const void*, const void*, const void*, int, int, int, int, int, const void*>;
-    static std::map<Key, cudaGraphExec_t> cache;
-    const Key key{A, ws, status, nb, d, D, p, precision, sym_tiles};
     static const int debug = getenv("ASG_NS_DEBUG") != nullptr ? 1 : 0;  // diagnostics: per-iteration residuals
-    cudaGraphExec_t exec = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
-        if (it != cache.end()) exec = it->second;
-    }
-    if (!exec) {
-        cudaStream_t cap;
-        cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
-        cudaGraph_t g = nullptr;
-        cudaGraphCreate(&g, 0);
-        cudaGraphConditionalHandle handle;
-        cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault);  // enter the loop
-        cudaGraphNodeParams cp{};
-        cp.type = cudaGraphNodeTypeConditional;
-        cp.conditional.handle = handle;
-        cp.conditional.type = cudaGraphCondTypeWhile;
-        cp.conditional.size = 1;
-        cudaGraphNode_t nloop;
-        cudaGraphAddNode(&nloop, g, nullptr, 0, &cp);
-        cudaGraph_t body = cp.conditional.phGraph_out[0];
-        cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
-        for (int half = 0; half < 2; ++half) {
-            iteration(cap, half == 1);
-            // M_{k+1} sits in buffer (k+1) & 1: M1 after an even iteration, M0 after an odd one
-            ns_spec_kernel<<<dim3(nblk, nb), pth, psm, cap>>>(half ? M0h : M1h, half ? M0l : M1l, d, D, st.actM, v, y,
-                                                           part, nblk);
-            ns_decide_kernel<<<nb, 256, 0, cap>>>(st, nb, d, D, v, y, part, nblk, status, debug);
-            ns_loop_kernel<<<1, 256, 0, cap>>>(st, nb, handle);
-        }
-        cudaStreamEndCapture(cap, &body);
-        cudaGraphInstantiate(&exec, g, 0);
-        cudaGraphDestroy(g);
-        cudaStreamDestroy(cap);
-        std::lock_guard<std::mutex> lk(mu);
-        cache[key] = exec;
-    }
 
     // Pass 1: damping eps as given. Pass 2: the matrices pass 1 found
     // indefinite, with the damping lifted to the rounding floor (ns_floor):
     // a PSD factor whose null space carries fp32 noise of either sign then
     // gets finite roots, as with the F32 eigensolve's clamp; a genuinely
-    // indefinite one fails again (NotPsd). Pass 2 costs ~20 empty launches
-    // when nothing failed.
-    for (int pass = 0; pass < 2; ++pass) {
-        ns_gate_kernel<<<(nb + 255) / 256, 256, 0, s>>>(gate, status, nb, pass);
+    // indefinite one fails again (NotPsd). Pass 2's launches find no active
+    // matrix and return at once when nothing failed.
+    auto prologue = [&](int pass, cudaStream_t q) {
+        ns_gate_kernel<<<(nb + 255) / 256, 256, 0, q>>>(gate, status, nb, pass);
         // ---- scale: c >= ~lambda_max(A') from ||A'||_F and a power estimate ----
-        ns_norm_kernel<<<nb, 256, 0, s>>>(y, v, part, nullptr, nblk, d, D, est, fro, 1, gate);
+        ns_norm_kernel<<<nb, 256, 0, q>>>(y, v, part, nullptr, nblk, d, D, est, fro, 1, gate);
         for (int it = 0; it < kPowerSteps; ++it) {
-            ns_power_kernel<<<dim3(nblk, nb), pth, psm, s>>>(A, d, D, eps, v, y, part, it == 0 ? partf : nullptr, nblk,
+            ns_power_kernel<<<dim3(nblk, nb), pth, psm, q>>>(A, d, D, eps, v, y, part, it == 0 ? partf : nullptr, nblk,
                                                              gate);
-            ns_norm_kernel<<<nb, 256, 0, s>>>(y, v, part, it == 0 ? partf : nullptr, nblk, d, D, est, fro, 0, gate);
+            ns_norm_kernel<<<nb, 256, 0, q>>>(y, v, part, it == 0 ? partf : nullptr, nblk, d, D, est, fro, 0, gate);
         }
-        ns_init_kernel<<<dim3(eblocks, nb), 256, 0, s>>>(A, d, D, eps, est, fro, pf, pass ? ns_floor(d) : 0.f, M0h, M0l,
+        ns_init_kernel<<<dim3(eblocks, nb), 256, 0, q>>>(A, d, D, eps, est, fro, pf, pass ? ns_floor(d) : 0.f, M0h, M0l,
                                                          T0h, T0l, X0h, X0l, cval, eeff, gate);
-        ns_state_init_kernel<<<(nb + 255) / 256, 256, 0, s>>>(st, est, fro, nb, status, gate);
-        ns_probe_init_kernel<<<nb, 256, 0, s>>>(v, d, D, gate);
-        cudaGraphLaunch(exec, s);
-        ns_finish_kernel<<<dim3(eblocks, nb), 256, 0, s>>>(X0h, X0l, X1h, X1l, st.xbuf, d, D, outh, outl_, gate);
-
+        ns_state_init_kernel<<<(nb + 255) / 256, 256, 0, q>>>(st, est, fro, nb, status, gate);
+        ns_probe_init_kernel<<<nb, 256, 0, q>>>(v, d, D, gate);
+    };
+    auto body = [&](cudaGraphConditionalHandle handle, cudaStream_t q) {
+        for (int half = 0; half < 2; ++half) {
+            iteration(q, half == 1);
+            // M_{k+1} sits in buffer (k+1) & 1: M1 after an even iteration, M0 after an odd one
+            ns_spec_kernel<<<dim3(nblk, nb), pth, psm, q>>>(half ? M0h : M1h, half ? M0l : M1l, d, D, st.actM, v, y,
+                                                         part, nblk);
+            ns_decide_kernel<<<nb, 256, 0, q>>>(st, nb, d, D, v, y, part, nblk, status, debug);
+            ns_loop_kernel<<<1, 256, 0, q>>>(st, nb, handle);
+        }
+    };
+    auto epilogue = [&](cudaStream_t q) {
+        ns_finish_kernel<<<dim3(eblocks, nb), 256, 0, q>>>(X0h, X0l, X1h, X1l, st.xbuf, d, D, outh, outl_, gate);
         // ---- one symmetric Newton refinement against A' itself -------------
         // R = I - X^(p/2) A' X^(p/2), X <- X + (X R + R X) / (2p). The coupled
         // iteration never revisits A', so the rounding of the ~3 products per
         // iteration accumulates in X; this step removes its commuting part
         // exactly and contracts the rest (tests/test_gpu_newton.py).
-        ns_damped_split_kernel<<<dim3(eblocks, nb), 256, 0, s>>>(A, d, D, eeff, Uh, Ul, gate);
+        ns_damped_split_kernel<<<dim3(eblocks, nb), 256, 0, q>>>(A, d, D, eeff, Uh, Ul, gate);
         const float* xph = outh;  // X^(p/2)
         const float* xpl = outl_;
         if (p == 4) {
-            gemm(outh, outl_, outh, outl_, EPI_SYM_SPLIT, T1h, T1l, gate, nullptr, nullptr, true, s);  // X^2
+            gemm(outh, outl_, outh, outl_, EPI_SYM_SPLIT, T1h, T1l, gate, nullptr, nullptr, true, q);  // X^2
             xph = T1h;
             xpl = T1l;
         }
         // B = X^(p/2) A' (general product: A' does not commute with the rounded X)
-        gemm(xph, xpl, Uh, Ul, EPI_SPLIT, Wh, Wl, gate, nullptr, nullptr, false, s);
+        gemm(xph, xpl, Uh, Ul, EPI_SPLIT, Wh, Wl, gate, nullptr, nullptr, false, q);
         // R = I - B X^(p/2) into T0 (EPI_NS with T = 1 I - 1 acc; its M output goes to M0)
         {
             GemmLaunch g{};
@@ -644,14 +614,78 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
             g.p.resid = st.resid;
             g.sym_tiles = sym_tiles;
             g.sym_tiles_count = nsym;
-            gemm_launch(g, precision, num_sms, s);
+            gemm_launch(g, precision, num_sms, q);
         }
-        gemm(outh, outl_, T0h, T0l, EPI_SPLIT, X1h, X1l, gate, nullptr, nullptr, false, s);  // E = X R
-        ns_refine_kernel<<<dim3(D / 32, D / 32, nb), dim3(32, 8), 0, s>>>(outh, outl_, X1h, X1l, d, D, 0.5f / pf, gate);
-        count_launch(10 + 2 * kPowerSteps + 2 * (p == 2 ? 6 : 7) + (p == 4 ? 4 : 3));
+        gemm(outh, outl_, T0h, T0l, EPI_SPLIT, X1h, X1l, gate, nullptr, nullptr, false, q);  // E = X R
+        ns_refine_kernel<<<dim3(D / 32, D / 32, nb), dim3(32, 8), 0, q>>>(outh, outl_, X1h, X1l, d, D, 0.5f / pf, gate);
+    };
+
+    // The whole root (both passes, each a prologue, a device-driven WHILE
+    // loop and an epilogue) is ONE cached graph: one launch per call, so a
+    // refresh of hundreds of factors never fills the stream's launch queue
+    // (which would block the host thread that drives the main stream).
+    static std::mutex mu;
+    using Key = std::tuple<const void*, const void*, const void*, const void*, const void*, const void*, int, int, int,
+                           int, int, const void*>;
+    static std::map<Key, cudaGraphExec_t> cache;
+    const Key key{A, ws, caller_status, eps, outh, outl_, nb, d, D, p, precision, sym_tiles};
+    cudaGraphExec_t exec = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) exec = it->second;
     }
-    ns_merge_status_kernel<<<(nb + 255) / 256, 256, 0, s>>>(status, caller_status, nb);
-    count_launch(1);
+    if (!exec) {
+        cudaStream_t cap;
+        cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+        auto capture = [&](auto&& fn) {
+            cudaGraph_t gph = nullptr;
+            cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+            fn(cap);
+            cudaStreamEndCapture(cap, &gph);
+            return gph;
+        };
+        cudaGraph_t g = nullptr;
+        cudaGraphCreate(&g, 0);
+        cudaGraphNode_t prev = nullptr;
+        std::vector<cudaGraph_t> children;
+        auto add_child = [&](cudaGraph_t child) {
+            cudaGraphNode_t n;
+            cudaGraphAddChildGraphNode(&n, g, prev ? &prev : nullptr, prev ? 1 : 0, child);
+            children.push_back(child);
+            prev = n;
+        };
+        for (int pass = 0; pass < 2; ++pass) {
+            add_child(capture([&](cudaStream_t q) { prologue(pass, q); }));
+            cudaGraphConditionalHandle handle;
+            cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault);  // enter the loop
+            cudaGraphNodeParams cp{};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = handle;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t nloop;
+            cudaGraphAddNode(&nloop, g, &prev, 1, &cp);
+            cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+            cudaStreamBeginCaptureToGraph(cap, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+            body(handle, cap);
+            cudaStreamEndCapture(cap, &bodyg);
+            prev = nloop;
+            add_child(capture([&](cudaStream_t q) { epilogue(q); }));
+        }
+        add_child(capture([&](cudaStream_t q) {
+            ns_merge_status_kernel<<<(nb + 255) / 256, 256, 0, q>>>(status, caller_status, nb);
+        }));
+        cudaGraphInstantiate(&exec, g, 0);
+        for (cudaGraph_t c : children) cudaGraphDestroy(c);
+        cudaGraphDestroy(g);
+        cudaStreamDestroy(cap);
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = exec;
+    }
+    cudaGraphLaunch(exec, s);
+    // one pass through the graph (each loop body counted once)
+    count_launch(2 * (10 + 2 * kPowerSteps + 2 * (p == 2 ? 6 : 7) + (p == 4 ? 4 : 3)) + 1);
 }
 
 }  // namespace asg

@@ -21,6 +21,8 @@
 // (ASG_INSTALL_SIM_CLOCK) or driven by stream events (ASG_INSTALL_EVENT).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -67,8 +69,14 @@ int guard(F&& f) {
     } catch (const Fail& e) {
         g_err = e.msg;
         return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return ASG_ERR_OUT_OF_MEMORY;
     } catch (const std::exception& e) {
         g_err = e.what();
+        return ASG_ERR_INVALID_ARGUMENT;
+    } catch (...) {  // nothing crosses the C-ABI
+        g_err = "unknown exception";
         return ASG_ERR_INVALID_ARGUMENT;
     }
 }
@@ -246,7 +254,17 @@ struct asg_blockset {
     // SOAP install workspace (one block)
     double *iw_rotL = nullptr, *iw_rotR = nullptr, *iw_sq = nullptr, *iw_a = nullptr, *iw_b = nullptr;
     // scalars
-    int* d_flag = nullptr;
+    int* d_flag = nullptr;      // gradient norm: non-finite gradient
+    int* d_upd_flag = nullptr;  // update (EPI_APPLY, AdamW): non-finite update, surfaced at the next host sync
+    int* h_upd_flag = nullptr;  // pinned copy, written on the main stream after every update
+    // EVENT-mode barrier installs that did not block the host: the main stream
+    // waits on the refresh event; the refresh status and the device-side wait
+    // (ev_a -> ev_b on the main stream) are resolved at the next host sync
+    struct DeferredInstall {
+        int unit;
+        cudaEvent_t ev_a, ev_b;
+    };
+    std::vector<DeferredInstall> deferred_status;
     double* d_sqnorm = nullptr;
     float* d_scale = nullptr;
     // parity staging
@@ -274,12 +292,36 @@ struct asg_blockset {
     int64_t stride = 0;  // elements per rank segment of the owner-major buffers
     asg::BlockRef *d_gpack_refs = nullptr, *d_gunpack_refs = nullptr;
     int64_t *d_gpack_offs = nullptr, *d_gunpack_offs = nullptr;
+    // bucketed parameter all-gather: buckets of each shape's
+    // owned units, identical on every rank; with a communicator set, asg_step
+    // all-gathers bucket b on comm_stream while the main stream updates b+1
+    struct Bucket {
+        bool adamw = false;
+        int group = -1, s0 = 0, cnt = 0;  // this rank's slot range in its group for the shape
+        int64_t stride = 0;                // elements per rank segment (the largest over ranks)
+        asg::BlockRef *d_pack_refs = nullptr, *d_unpack_refs = nullptr;
+        int64_t *d_pack_offs = nullptr, *d_unpack_offs = nullptr;
+        int n_pack = 0, n_unpack = 0;
+    };
+    std::vector<Bucket> buckets;
+    int buckets_per_shape = 0;
+    void* ag_comm = nullptr;  // ncclComm_t (fused all-gather in asg_step)
+    cudaStream_t comm_stream = nullptr;
+    float *ag_send = nullptr, *ag_recv = nullptr;
+    std::vector<cudaEvent_t> ag_events;
+    cudaEvent_t ag_done = nullptr;
     // installs decided by the schedule bookkeeping, executed after the
     // step's refreshes are launched as one batch
     std::vector<int> deferred_installs;
     // profiling
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    struct HbmProf {
+        cudaEvent_t e0, e1;
+        int kind;
+        double bytes;
+    };
+    std::vector<HbmProf> prof_hbm;  // HBM-bound kernels of the step (asg_hbm_stats kinds)
     double prof_flops = 0.0;
     uint64_t prof_gemms = 0;
     uint64_t launch_base = 0;
@@ -444,8 +486,11 @@ void alloc_group(asg_blockset* bs, Group& g) {
     const size_t nb = size_t(g.nb);
     g.L = dalloc<float>(bs, nb * slabMM(g));
     g.R = dalloc<float>(bs, nb * slabNN(g));
-    g.snapL = dalloc<float>(bs, nb * slabMM(g));
-    g.snapR = dalloc<float>(bs, nb * slabNN(g));
+    // square blocks: the two sides' snapshots (and, below, roots) are one
+    // allocation, so a refresh can batch both sides (refresh_newton)
+    const bool joint = g.m == g.n;
+    g.snapL = dalloc<float>(bs, (joint ? 2 : 1) * nb * slabMM(g));
+    g.snapR = joint ? g.snapL + nb * slabMM(g) : dalloc<float>(bs, nb * slabNN(g));
     g.Gh = dalloc<float>(bs, nb * slabMN(g));
     g.GTh = dalloc<float>(bs, nb * slabMN(g));
     g.Th = dalloc<float>(bs, nb * slabMN(g));
@@ -503,10 +548,23 @@ void alloc_group(asg_blockset* bs, Group& g) {
         CK(cudaMemsetAsync(g.mom_m, 0, nb * slabMN(g) * 4, s));
         CK(cudaMemsetAsync(g.mom_v, 0, nb * slabMN(g) * 4, s));
     } else {
+        // joint (square) allocation of a left/right pair: R follows L
+        auto pair_lr = [&](float*& lh, float*& ll, float*& rh, float*& rl) {
+            if (!joint) {
+                pair_mm(lh, ll);
+                pair_nn(rh, rl);
+                return;
+            }
+            lh = dalloc<float>(bs, 2 * nb * slabMM(g));
+            rh = lh + nb * slabMM(g);
+            if (sp) {
+                ll = dalloc<float>(bs, 2 * nb * slabMM(g));
+                rl = ll + nb * slabMM(g);
+            }
+        };
         pair_mm(g.PLh, g.PLl);
         pair_nn(g.PRh, g.PRl);
-        pair_mm(g.sPLh, g.sPLl);
-        pair_nn(g.sPRh, g.sPRl);
+        pair_lr(g.sPLh, g.sPLl, g.sPRh, g.sPRl);
         launch_identity_split(g.PLh, g.PLl, g.nb, g.M, g.m, s);
         launch_identity_split(g.PRh, g.PRl, g.nb, g.N, g.n, s);
         if (f32_refresh(bs) && !newton_roots(bs)) {  // basis of the last refresh, identity before the first
@@ -525,8 +583,7 @@ void alloc_group(asg_blockset* bs, Group& g) {
         if (is_kl(bs)) {
             pair_mm(g.KLh, g.KLl);
             pair_nn(g.KRh, g.KRl);
-            pair_mm(g.sKLh, g.sKLl);
-            pair_nn(g.sKRh, g.sKRl);
+            pair_lr(g.sKLh, g.sKLl, g.sKRh, g.sKRl);
             launch_identity_split(g.KLh, g.KLl, g.nb, g.M, g.m, s);
             launch_identity_split(g.KRh, g.KRl, g.nb, g.N, g.n, s);
         }
@@ -601,7 +658,11 @@ void alloc_workspace(asg_blockset* bs) {
     if (newton_roots(bs)) {
         int Dmax = 0;
         for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
-        bs->ns_ws = dalloc<float>(bs, ns_workspace_floats(bs->ws_chunk, Dmax));
+        // both sides of a small square group run as one batch (refresh_newton)
+        bool both = false;
+        for (const Group& g : bs->groups) both |= g.m == g.n && g.nb <= bs->ws_chunk;
+        bs->ns_ws = dalloc<float>(bs, ns_workspace_floats((both ? 2 : 1) * bs->ws_chunk, Dmax));
+        bs->pair_status = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
     } else if (f32_refresh(bs)) {
         int Dmax = 0;
         for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
@@ -654,6 +715,23 @@ void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const 
         bs->prof_events.emplace_back(e0, e1);
         bs->prof_flops += alg_flops;
         bs->prof_gemms += 1;
+    }
+}
+
+// Brackets an HBM-bound launch with CUDA events on its stream while profiling
+// (asg_get_hbm_stats): kind, algorithmic bytes.
+template <class F>
+void hbm_launch(asg_blockset* bs, cudaStream_t s, int kind, double bytes, F&& launch) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (bs->profiling) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, s));
+    }
+    launch();
+    if (e0) {
+        CK(cudaEventRecord(e1, s));
+        bs->prof_hbm.push_back({e0, e1, kind, bytes});
     }
 }
 
@@ -722,6 +800,157 @@ void build_owner_layout(asg_blockset* bs) {
     up(bs->d_gpack_offs, gpko);
     up(bs->d_gunpack_refs, gupk);
     up(bs->d_gunpack_offs, gupko);
+}
+
+// Buckets of the parameter all-gather. For each block shape (in order of
+// first appearance among all units; 1-D AdamW parameters last share one
+// key), every rank's units of that shape in unit order are split into
+// `per_shape` runs of B = ceil(max_r n_r / per_shape) units; bucket (shape, c)
+// holds run c of every rank. The plan is a pure function of the ownership
+// plan, so every rank builds the same bucket list and issues the same
+// collectives. A rank's run c of a shape is slots [cB, cB + cnt) of its group
+// (slots follow unit order, build_groups).
+void build_buckets(asg_blockset* bs, int per_shape) {
+    for (auto& b : bs->buckets)
+        for (void* p : {static_cast<void*>(b.d_pack_refs), static_cast<void*>(b.d_unpack_refs),
+                        static_cast<void*>(b.d_pack_offs), static_cast<void*>(b.d_unpack_offs)})
+            if (p) {
+                cudaFree(p);
+                bs->allocs.erase(std::remove(bs->allocs.begin(), bs->allocs.end(), p), bs->allocs.end());
+            }
+    bs->buckets.clear();
+    bs->buckets_per_shape = per_shape;
+    std::vector<std::pair<int, int>> keys;
+    std::map<std::pair<int, int>, std::vector<std::vector<int>>> lists;  // key -> rank -> units
+    for (size_t i = 0; i < bs->units.size(); ++i) {
+        const Unit& u = bs->units[i];
+        const std::pair<int, int> key =
+            u.adamw ? std::make_pair(-1, -1)
+                    : std::make_pair(int(u.spec.row_end - u.spec.row_begin), int(u.spec.col_end - u.spec.col_begin));
+        auto it = lists.find(key);
+        if (it == lists.end()) {
+            it = lists.emplace(key, std::vector<std::vector<int>>(size_t(bs->world))).first;
+            if (key.first >= 0) keys.push_back(key);
+        }
+        it->second[size_t(u.owner)].push_back(int(i));
+    }
+    if (lists.count({-1, -1})) keys.push_back({-1, -1});
+    auto slice = [&](const Unit& u) {
+        const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+        BlockRef th{};
+        th.src = th.dst = d.theta ? d.theta + u.spec.row_begin * d.ld_theta + u.spec.col_begin : nullptr;
+        th.ld = d.ld_theta;
+        th.rows = int32_t(u.spec.row_end - u.spec.row_begin);
+        th.cols = int32_t(u.spec.col_end - u.spec.col_begin);
+        return th;
+    };
+    for (const auto& key : keys) {
+        const auto& per_rank = lists[key];
+        size_t nmax = 0;
+        for (const auto& l : per_rank) nmax = std::max(nmax, l.size());
+        if (nmax == 0) continue;
+        const size_t B = key.first < 0 ? nmax : (nmax + size_t(per_shape) - 1) / size_t(per_shape);
+        int my_group = -1;
+        for (size_t gi = 0; gi < bs->groups.size(); ++gi)
+            if (bs->groups[gi].m == key.first && bs->groups[gi].n == key.second) my_group = int(gi);
+        for (size_t c0 = 0; c0 < nmax; c0 += B) {
+            asg_blockset::Bucket bk;
+            bk.adamw = key.first < 0;
+            std::vector<int64_t> elems(size_t(bs->world), 0);
+            for (int r = 0; r < bs->world; ++r)
+                for (size_t j = c0; j < std::min(c0 + B, per_rank[size_t(r)].size()); ++j) {
+                    const Unit& u = bs->units[size_t(per_rank[size_t(r)][j])];
+                    elems[size_t(r)] += (u.spec.row_end - u.spec.row_begin) * (u.spec.col_end - u.spec.col_begin);
+                }
+            for (int64_t e : elems) bk.stride = std::max(bk.stride, e);
+            const auto& mine = per_rank[size_t(bs->rank)];
+            bk.group = bk.adamw ? -1 : my_group;
+            bk.s0 = int(c0);
+            bk.cnt = int(std::min(c0 + B, mine.size()) > c0 ? std::min(c0 + B, mine.size()) - c0 : 0);
+            std::vector<BlockRef> pk, upk;
+            std::vector<int64_t> pko, upko;
+            int64_t off = 0;
+            for (size_t j = c0; j < std::min(c0 + B, mine.size()); ++j) {
+                const Unit& u = bs->units[size_t(mine[j])];
+                pk.push_back(slice(u));
+                pko.push_back(off);
+                off += int64_t(pk.back().rows) * pk.back().cols;
+            }
+            for (int r = 0; r < bs->world; ++r) {
+                int64_t o = int64_t(r) * bk.stride;
+                for (size_t j = c0; j < std::min(c0 + B, per_rank[size_t(r)].size()); ++j) {
+                    const Unit& u = bs->units[size_t(per_rank[size_t(r)][j])];
+                    upk.push_back(slice(u));
+                    upko.push_back(o);
+                    o += int64_t(upk.back().rows) * upk.back().cols;
+                }
+            }
+            bk.n_pack = int(pk.size());
+            bk.n_unpack = int(upk.size());
+            if (!pk.empty()) {
+                bk.d_pack_refs = dalloc<BlockRef>(bs, pk.size());
+                bk.d_pack_offs = dalloc<int64_t>(bs, pko.size());
+                h2d(bk.d_pack_refs, pk.data(), pk.size() * sizeof(BlockRef), bs->main);
+                h2d(bk.d_pack_offs, pko.data(), pko.size() * sizeof(int64_t), bs->main);
+            }
+            if (!upk.empty()) {
+                bk.d_unpack_refs = dalloc<BlockRef>(bs, upk.size());
+                bk.d_unpack_offs = dalloc<int64_t>(bs, upko.size());
+                h2d(bk.d_unpack_refs, upk.data(), upk.size() * sizeof(BlockRef), bs->main);
+                h2d(bk.d_unpack_offs, upko.data(), upko.size() * sizeof(int64_t), bs->main);
+            }
+            bs->buckets.push_back(bk);
+        }
+    }
+    int64_t smax = 0;
+    for (const auto& b : bs->buckets) smax = std::max(smax, b.stride);
+    for (float* p : {bs->ag_send, bs->ag_recv})
+        if (p) {
+            cudaFree(p);
+            bs->allocs.erase(std::remove(bs->allocs.begin(), bs->allocs.end(), static_cast<void*>(p)), bs->allocs.end());
+        }
+    bs->ag_send = dalloc<float>(bs, size_t(std::max<int64_t>(1, smax)));
+    bs->ag_recv = dalloc<float>(bs, size_t(std::max<int64_t>(1, smax)) * size_t(bs->world));
+}
+
+// NCCL, loaded at run time (libnccl.so.2: the copy torch already mapped, or
+// the system one), so the library links without it and fails loudly only when
+// a collective is requested.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+        a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.GetErrorString;
+        return a;
+    }();
+    if (!api.ok) throw Fail{ASG_ERR_UNSUPPORTED, "NCCL (libnccl.so.2) not loadable"};
+    return api;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Fail{ASG_ERR_CUDA, std::string(what) + ": " + nccl().GetErrorString(r)};
+}
+
+// Bucket b: pack this rank's updated slices, all-gather, scatter every rank's
+// slices into the parameters (all on stream s).
+void bucket_exchange(asg_blockset* bs, const asg_blockset::Bucket& b, ncclComm_t comm, cudaStream_t s) {
+    launch_pack_blocks(b.d_pack_refs, b.d_pack_offs, b.n_pack, bs->ag_send, s);
+    nccl_check(nccl().AllGather(bs->ag_send, bs->ag_recv, size_t(b.stride), ncclFloat32, comm, s), "ncclAllGather");
+    launch_unpack_blocks(b.d_unpack_refs, b.d_unpack_offs, b.n_unpack, bs->ag_recv, s);
 }
 
 // (Re)builds the chunk table of the one-launch global gradient norm.
@@ -832,6 +1061,25 @@ void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
              cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s, cnt * nf * nf * mf);
 }
 
+// accumulate_factors (precond.cpp:173-189) for every owned block: gradient
+// prep (gather, clip scale, tf32 split, transpose) and the statistics GEMMs,
+// batched per shape group.
+void accumulate_impl(asg_blockset* bs, double clip_scale) {
+    const int k = fork_groups(bs);
+    for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
+        Group& g = bs->groups[gi];
+        cudaStream_t gs = stream_for(bs, k, int(gi));
+        // 4 B read per element, hi/lo of G and G^T written (16 B; 8 B in TF32 mode) per padded element
+        const double bytes = double(g.nb) * (4.0 * g.m * g.n + (g.Gl ? 16.0 : 8.0) * g.M * g.N);
+        hbm_launch(bs, gs, ASG_HBM_PREP, bytes, [&] {
+            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs,
+                             g.vec_grad);
+        });
+        group_stats(bs, g, 0, g.nb, gs);
+    }
+    join_groups(bs, k);
+}
+
 // Preconditioned update for slots [s0, s0+cnt). `final_epi` is EPI_APPLY (step)
 // or EPI_STORE into `store_out` ([cnt][M][N], parity entry points).
 void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, float lr_eff, const ApplyEntry* apply,
@@ -845,7 +1093,7 @@ void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, fl
     pf.apply = apply;
     pf.lr_eff = lr_eff;
     pf.wd = float(o.weight_decay);
-    pf.flag = bs->d_flag;
+    pf.flag = bs->d_upd_flag;
     pf.C = store_out;
     pf.ldc = g.N;
     pf.c_bstride = int64_t(mn);
@@ -1188,18 +1436,26 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
 void refresh_newton(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
     PhaseTimer pt(s);
     pt.mark("start");
-    for (int side = 0; side < 2; ++side) {
+    // square blocks whose whole group is this chunk: both sides in one batch
+    // (the jointly allocated L/R slabs are contiguous), which halves the
+    // iteration's latency when the group is small (C1: one 1024^2 block)
+    const bool both = g.m == g.n && s0 == 0 && cnt == g.nb && g.nb <= bs->ws_chunk;
+    for (int side = 0; side < (both ? 1 : 2); ++side) {
         const bool left = side == 0;
         const int d = left ? g.m : g.n, D = left ? g.M : g.N;
+        const int nmat = both ? 2 * cnt : cnt;
         const size_t DD = size_t(D) * D;
         const float* snap = at(left ? g.snapL : g.snapR, DD, s0);
-        launch_relative_damping_f32(snap, cnt, D, d, bs->opt.damping, bs->ws_eps, s);
+        launch_relative_damping_f32(snap, nmat, D, d, bs->opt.damping, bs->ws_eps, s);
         float* ph = at(left ? g.sPLh : g.sPRh, DD, s0);
         float* pl = at(left ? g.sPLl : g.sPRl, DD, s0);
         const int2* tiles = left ? g.tilesM : g.tilesN;
         const int ntiles = left ? g.ntM : g.ntN;
-        launch_ns_inv_root(snap, cnt, d, D, bs->ws_eps, is_kl(bs) ? 2 : 4, ph, pl, bs->ns_ws, g.d_status + s0, tiles,
-                           ntiles, bs->precision, bs->num_sms, s);
+        int* st = both ? bs->pair_status : g.d_status + s0;
+        if (both) CK(cudaMemsetAsync(st, 0, size_t(nmat) * sizeof(int), s));
+        launch_ns_inv_root(snap, nmat, d, D, bs->ws_eps, is_kl(bs) ? 2 : 4, ph, pl, bs->ns_ws, st, tiles, ntiles,
+                           bs->precision, bs->num_sms, s);
+        if (both) launch_merge_status(st, cnt, g.d_status + s0, s);
         if (is_kl(bs)) {
             GemmParams pk{};
             pk.alpha = 1.f;
@@ -1207,8 +1463,8 @@ void refresh_newton(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s)
             pk.Dlo = at(left ? g.sKLl : g.sKRl, DD, s0);
             pk.ldd = D;
             pk.d_bstride = int64_t(DD);
-            run_gemm(bs, op(ph, pl, D, D), op(ph, pl, D, D), cnt, EPI_SYM_SPLIT, pk, tiles, ntiles, s,
-                     double(cnt) * d * double(d) * d);
+            run_gemm(bs, op(ph, pl, D, D), op(ph, pl, D, D), nmat, EPI_SYM_SPLIT, pk, tiles, ntiles, s,
+                     double(nmat) * d * double(d) * d);
         }
     }
     pt.mark("newton roots");
@@ -1286,11 +1542,29 @@ void launch_refreshes(asg_blockset* bs) {
 
 int status_to_code(int st) { return st; }
 
-// Waits for a unit's refresh (host: its status; main stream: its event).
-void install_wait(asg_blockset* bs, Unit& u) {
+// Orders the install after a unit's refresh. A refresh that has completed is
+// installed at once (its status checked now). Otherwise, in EVENT mode, the
+// main stream waits on the refresh event (no host blocking, SURVEY 8(b)
+// threading row) and the status and device-side wait are resolved at the
+// next host sync (resolve_deferred); in SIM_CLOCK mode (deterministic parity
+// runs) and for the synchronous per-block entry points the host waits and a
+// failed refresh throws here, as future.get() does (asyncsched.cpp:146).
+void install_wait(asg_blockset* bs, Unit& u, bool host_wait) {
     if (u.needs_launch) launch_refreshes(bs);
     Group& g = bs->groups[size_t(u.group)];
-    CK(cudaEventSynchronize(u.done));
+    const cudaError_t q = cudaEventQuery(u.done);
+    if (q != cudaSuccess && q != cudaErrorNotReady) CK(q);
+    if (q == cudaErrorNotReady && !host_wait) {
+        asg_blockset::DeferredInstall d{int(&u - bs->units.data()), nullptr, nullptr};
+        CK(cudaEventCreate(&d.ev_a));
+        CK(cudaEventCreate(&d.ev_b));
+        CK(cudaEventRecord(d.ev_a, bs->main));
+        CK(cudaStreamWaitEvent(bs->main, u.done, 0));
+        CK(cudaEventRecord(d.ev_b, bs->main));
+        bs->deferred_status.push_back(d);
+        return;
+    }
+    if (q == cudaErrorNotReady) CK(cudaEventSynchronize(u.done));
     const int st = g.h_status[u.slot];
     if (st != ASG_OK) {
         const char* what = st == ASG_ERR_NOT_PSD       ? "refresh: damped eigenvalue <= 0"
@@ -1299,7 +1573,6 @@ void install_wait(asg_blockset* bs, Unit& u) {
                                                           : "refresh failed";
         throw Fail{status_to_code(st), what};
     }
-    CK(cudaStreamWaitEvent(bs->main, u.done, 0));
 }
 
 // SOAP install of the F32 refresh for slots [s0, s0+cnt) of a group
@@ -1374,6 +1647,27 @@ void install_soap_f32(asg_blockset* bs, Group& g, int s0, int cnt) {
     (void)flops;
 }
 
+// Shampoo / KL-Shampoo install for slots [s0, s0+cnt) of a group
+// (install_refresh precond.cpp:158-161): shadow roots -> active, one copy per
+// array over the whole slot run.
+void install_roots(asg_blockset* bs, Group& g, int s0, int cnt) {
+    cudaStream_t s = bs->main;
+    const size_t mm = slabMM(g), nn = slabNN(g);
+    auto cp = [&](float* dst, const float* src, size_t n) {
+        if (dst && src) CK(cudaMemcpyAsync(dst, src, n * size_t(cnt) * 4, cudaMemcpyDeviceToDevice, s));
+    };
+    cp(at(g.PLh, mm, s0), at(g.sPLh, mm, s0), mm);
+    cp(at(g.PLl, mm, s0), at(g.sPLl, mm, s0), mm);
+    cp(at(g.PRh, nn, s0), at(g.sPRh, nn, s0), nn);
+    cp(at(g.PRl, nn, s0), at(g.sPRl, nn, s0), nn);
+    if (is_kl(bs)) {
+        cp(at(g.KLh, mm, s0), at(g.sKLh, mm, s0), mm);
+        cp(at(g.KLl, mm, s0), at(g.sKLl, mm, s0), mm);
+        cp(at(g.KRh, nn, s0), at(g.sKRh, nn, s0), nn);
+        cp(at(g.KRl, nn, s0), at(g.sKRl, nn, s0), nn);
+    }
+}
+
 // Device-side install of a finished refresh (install_refresh precond.cpp:144-164).
 void install_apply(asg_blockset* bs, Unit& u) {
     Group& g = bs->groups[size_t(u.group)];
@@ -1383,20 +1677,8 @@ void install_apply(asg_blockset* bs, Unit& u) {
     }
     cudaStream_t s = bs->main;
     const size_t mm = slabMM(g), nn = slabNN(g);
-    auto cp = [&](float* dst, const float* src, size_t n) {
-        if (dst && src) CK(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToDevice, s));
-    };
     if (!is_soap(bs)) {
-        cp(at(g.PLh, mm, u.slot), at(g.sPLh, mm, u.slot), mm);
-        cp(at(g.PLl, mm, u.slot), at(g.sPLl, mm, u.slot), mm);
-        cp(at(g.PRh, nn, u.slot), at(g.sPRh, nn, u.slot), nn);
-        cp(at(g.PRl, nn, u.slot), at(g.sPRl, nn, u.slot), nn);
-        if (is_kl(bs)) {
-            cp(at(g.KLh, mm, u.slot), at(g.sKLh, mm, u.slot), mm);
-            cp(at(g.KLl, mm, u.slot), at(g.sKLl, mm, u.slot), mm);
-            cp(at(g.KRh, nn, u.slot), at(g.sKRh, nn, u.slot), nn);
-            cp(at(g.KRl, nn, u.slot), at(g.sKRl, nn, u.slot), nn);
-        }
+        install_roots(bs, g, u.slot, 1);
         return;
     }
     // SOAP: rot = Q_new^T Q_old per side; M <- rot_L M rot_R^T,
@@ -1467,7 +1749,8 @@ void run_deferred_installs(asg_blockset* bs) {
     launch_refreshes(bs);
     std::vector<int> todo;
     todo.swap(bs->deferred_installs);
-    for (int idx : todo) install_wait(bs, bs->units[size_t(idx)]);
+    const bool host_wait = bs->sc.install_mode != ASG_INSTALL_EVENT;
+    for (int idx : todo) install_wait(bs, bs->units[size_t(idx)], host_wait);
     if (f32_refresh(bs) && is_soap(bs)) {
         // batched: contiguous slot runs of one group, in workspace-sized chunks.
         // Blocks whose refresh left J = I on both sides (warm, nothing to rotate)
@@ -1501,6 +1784,17 @@ void run_deferred_installs(asg_blockset* bs) {
             install_soap_f32(bs, bs->groups[size_t(gs[i].first)], gs[i].second, int(j - i));
             i = j;
         }
+    } else if (!is_soap(bs)) {
+        // roots: contiguous slot runs of one group, one copy per array per run
+        std::vector<std::pair<int, int>> gs;
+        for (int idx : todo) gs.emplace_back(bs->units[size_t(idx)].group, bs->units[size_t(idx)].slot);
+        std::sort(gs.begin(), gs.end());
+        for (size_t i = 0; i < gs.size();) {
+            size_t j = i + 1;
+            while (j < gs.size() && gs[j].first == gs[i].first && gs[j].second == gs[j - 1].second + 1) ++j;
+            install_roots(bs, bs->groups[size_t(gs[i].first)], gs[i].second, int(j - i));
+            i = j;
+        }
     } else {
         for (int idx : todo) install_apply(bs, bs->units[size_t(idx)]);
     }
@@ -1508,7 +1802,7 @@ void run_deferred_installs(asg_blockset* bs) {
 }
 
 void install_device(asg_blockset* bs, Unit& u) {
-    install_wait(bs, u);
+    install_wait(bs, u, true);
     install_apply(bs, u);
 }
 
@@ -1551,7 +1845,10 @@ double sched_barrier(asg_blockset* bs, int idx, int64_t step) {
     double waited;
     const double now = bs->now_us;
     if (bs->sc.install_mode == ASG_INSTALL_EVENT) {
-        waited = 0.0;  // the main stream waits on the refresh event; the host does not block
+        // the main stream waits on the refresh event; the host does not block.
+        // The device-side wait is measured and added to wait_total_us when the
+        // install resolves (resolve_deferred).
+        waited = 0.0;
     } else {
         waited = std::max(0.0, u.completion_sim - now);
     }
@@ -1562,6 +1859,14 @@ double sched_barrier(asg_blockset* bs, int idx, int64_t step) {
     bs->stats.barrier_waits += 1;
     bs->stats.wait_total_us += waited;
     return waited;
+}
+
+// BlockSpec::id (precond.cpp:64-67) with the reference harness's parameter
+// names "w<index>" (harness.cpp:357).
+std::string unit_id(const asg_blockset* bs, int i) {
+    const asg_block_spec& sp = bs->units[size_t(i)].spec;
+    return "w" + std::to_string(sp.param_index) + "[" + std::to_string(sp.row_begin) + ":" +
+           std::to_string(sp.row_end) + "," + std::to_string(sp.col_begin) + ":" + std::to_string(sp.col_end) + "]";
 }
 
 // on_hook(StepEnd) (asyncsched.cpp:268-286).
@@ -1578,6 +1883,10 @@ void sched_step_end(asg_blockset* bs, int64_t step) {
             ok = u.completion_sim <= bs->now_us;
         if (ok) ready.push_back(int(i));
     }
+    // installs in ascending block-id order (asyncsched.cpp:275-276: std::sort
+    // of BlockSpec::id strings, "w<param>[r0:r1,c0:c1]" as the reference
+    // harness names them, harness.cpp:357, precond.cpp:64-67)
+    std::sort(ready.begin(), ready.end(), [&](int a, int b) { return unit_id(bs, a) < unit_id(bs, b); });
     for (int i : ready) sched_install(bs, i, step);
     run_deferred_installs(bs);
 }
@@ -1619,13 +1928,43 @@ void download_block(asg_blockset* bs, Group& g, double* out) {
         for (int j = 0; j < g.n; ++j) out[size_t(i) * g.n + j] = double(buf[size_t(i) * g.N + j]);
 }
 
+// The update's NonFinite flag (apply_update precond.cpp:248; adamw_step
+// precond.cpp:231): set on the device by EPI_APPLY / AdamW (which leave the
+// non-finite elements of theta unchanged), surfaced here once the stream has
+// been synchronized.
 void check_flag(asg_blockset* bs) {
     int f = 0;
-    CK(cudaMemcpy(&f, bs->d_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&f, bs->d_upd_flag, sizeof(int), cudaMemcpyDeviceToHost));
     if (f) {
-        CK(cudaMemset(bs->d_flag, 0, sizeof(int)));
+        CK(cudaMemset(bs->d_upd_flag, 0, sizeof(int)));
         throw Fail{ASG_ERR_NON_FINITE, "apply_update: non-finite update"};
     }
+}
+
+// Resolves EVENT-mode barrier installs whose refresh has completed: the
+// refresh status (a failure surfaces here, at the next host sync after the
+// install) and the main stream's device-side wait (stats.wait_total_us).
+// blocking: wait for every outstanding one.
+void resolve_deferred(asg_blockset* bs, bool blocking) {
+    std::vector<asg_blockset::DeferredInstall> keep;
+    int fail = ASG_OK;
+    for (auto& d : bs->deferred_status) {
+        if (!blocking && cudaEventQuery(d.ev_b) != cudaSuccess) {
+            keep.push_back(d);
+            continue;
+        }
+        CK(cudaEventSynchronize(d.ev_b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, d.ev_a, d.ev_b));
+        bs->stats.wait_total_us += 1e3 * double(ms);
+        const Unit& u = bs->units[size_t(d.unit)];
+        const int st = bs->groups[size_t(u.group)].h_status[u.slot];
+        if (st != ASG_OK && fail == ASG_OK) fail = st;
+        cudaEventDestroy(d.ev_a);
+        cudaEventDestroy(d.ev_b);
+    }
+    bs->deferred_status.swap(keep);
+    if (fail != ASG_OK) throw Fail{fail, "refresh (installed at an earlier barrier) failed"};
 }
 
 }  // namespace
@@ -1834,9 +2173,12 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         build_adam_table(bs);
         build_sq_table(bs);
         bs->d_flag = dalloc<int>(bs, 1);
+        bs->d_upd_flag = dalloc<int>(bs, 1);
+        bs->h_upd_flag = halloc<int>(bs, 1);
         bs->d_sqnorm = dalloc<double>(bs, 1);
         bs->d_scale = dalloc<float>(bs, 1);
         CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), bs->main));
+        CK(cudaMemsetAsync(bs->d_upd_flag, 0, sizeof(int), bs->main));
         size_t stage = 0;
         for (const Group& g : bs->groups) stage = std::max(stage, slabMN(g));
         bs->stage_elems = stage;
@@ -1873,8 +2215,19 @@ int asg_blockset_destroy(asg_blockset* bs) {
     for (auto& u : bs->units)
         if (u.done) cudaEventDestroy(u.done);
     if (bs->ev_snap) cudaEventDestroy(bs->ev_snap);
+    for (auto& e : bs->prof_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    for (auto& h : bs->prof_hbm) {
+        cudaEventDestroy(h.e0);
+        cudaEventDestroy(h.e1);
+    }
     for (void* p : bs->allocs) cudaFree(p);
     for (void* p : bs->host_allocs) cudaFreeHost(p);
+    for (cudaEvent_t e : bs->ag_events) cudaEventDestroy(e);
+    if (bs->ag_done) cudaEventDestroy(bs->ag_done);
+    if (bs->comm_stream) cudaStreamDestroy(bs->comm_stream);
     if (bs->own_main && bs->main) cudaStreamDestroy(bs->main);
     if (bs->side) cudaStreamDestroy(bs->side);
     delete bs;
@@ -1894,6 +2247,7 @@ int asg_blockset_bind_params(asg_blockset* bs, const asg_param_desc* params, int
         build_adam_table(bs);
         build_sq_table(bs);
         build_owner_layout(bs);
+        if (!bs->buckets.empty()) build_buckets(bs, bs->buckets_per_shape);
     });
 }
 
@@ -1949,15 +2303,27 @@ int asg_grad_sqnorm(asg_blockset* bs, void* stream, double* sqnorm, int32_t* non
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
         CK(cudaMemsetAsync(bs->d_sqnorm, 0, sizeof(double), s));
         CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), s));
-        launch_sqnorm_multi(bs->d_sq, bs->n_sq, bs->d_sqnorm, bs->d_flag, s);  // every parameter, one launch
+        double elems = 0.0;
+        for (const asg_param_desc& d : bs->params) elems += d.grad ? double(d.rows) * double(d.cols) : 0.0;
+        hbm_launch(bs, s, ASG_HBM_SQNORM, 4.0 * elems, [&] {
+            launch_sqnorm_multi(bs->d_sq, bs->n_sq, bs->d_sqnorm, bs->d_flag, s);  // every parameter, one launch
+        });
         double v = 0.0;
-        int f = 0;
+        int f = 0, fu = 0;
         CK(cudaMemcpyAsync(&v, bs->d_sqnorm, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(&f, bs->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        // the previous step's update flag (s is ordered after the step that wrote it)
+        CK(cudaMemcpyAsync(&fu, bs->d_upd_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), s));
         if (sqnorm) *sqnorm = v;
         if (nonfinite) *nonfinite = f;
+        resolve_deferred(bs, false);
+        if (fu) {
+            CK(cudaMemsetAsync(bs->d_upd_flag, 0, sizeof(int), s));
+            throw Fail{ASG_ERR_NON_FINITE, "apply_update: the previous step's update was non-finite "
+                                           "(those elements of theta were left unchanged)"};
+        }
     });
 }
 
@@ -1972,15 +2338,7 @@ int asg_accumulate(asg_blockset* bs, double clip_scale, void* stream) {
             CK(cudaStreamWaitEvent(bs->main, e, 0));
             CK(cudaEventDestroy(e));
         }
-        const int k = fork_groups(bs);
-        for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
-            Group& g = bs->groups[gi];
-            cudaStream_t gs = stream_for(bs, k, int(gi));
-            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs,
-                                 g.vec_grad);
-            group_stats(bs, g, 0, g.nb, gs);
-        }
-        join_groups(bs, k);
+        accumulate_impl(bs, clip_scale);
         CK(cudaGetLastError());
     });
 }
@@ -2014,9 +2372,10 @@ int asg_staleness_barrier(asg_blockset* bs, int64_t step, double* waited_us) {
 }
 
 namespace {
+void adamw_impl(asg_blockset* bs, double clip_scale, float lr_eff, cudaStream_t as);
+
 void precondition_apply_impl(asg_blockset* bs, double clip_scale, double lr_scale) {
     const float lr_eff = float(bs->opt.lr * lr_scale);
-    const int k = fork_groups(bs);
     for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
         Group& g = bs->groups[gi];
         if (is_soap(bs)) {
@@ -2028,10 +2387,46 @@ void precondition_apply_impl(asg_blockset* bs, double clip_scale, double lr_scal
                 ms = u.moment_steps;
             }
         }
+    }
+    if (bs->ag_comm) {
+        // fused all-gather: the update runs bucket by bucket on the main stream;
+        // bucket b's all-gather (comm stream) overlaps the update of b+1
+        ncclComm_t comm = static_cast<ncclComm_t>(bs->ag_comm);
+        CK(cudaEventRecord(bs->ag_done, bs->main));  // the comm stream starts after this step's earlier work
+        CK(cudaStreamWaitEvent(bs->comm_stream, bs->ag_done, 0));
+        bool adam_done = false;
+        for (size_t i = 0; i < bs->buckets.size(); ++i) {
+            const auto& b = bs->buckets[i];
+            if (b.adamw) {
+                if (!adam_done) adamw_impl(bs, clip_scale, lr_eff, bs->main);
+                adam_done = true;
+            } else if (b.cnt > 0) {
+                Group& g = bs->groups[size_t(b.group)];
+                group_update(bs, g, b.s0, b.cnt, EPI_APPLY, lr_eff, g.d_apply + b.s0, nullptr, bs->main);
+            }
+            CK(cudaEventRecord(bs->ag_events[i], bs->main));
+            CK(cudaStreamWaitEvent(bs->comm_stream, bs->ag_events[i], 0));
+            bucket_exchange(bs, b, comm, bs->comm_stream);
+        }
+        if (!adam_done) adamw_impl(bs, clip_scale, lr_eff, bs->main);
+        CK(cudaEventRecord(bs->ag_done, bs->comm_stream));
+        CK(cudaStreamWaitEvent(bs->main, bs->ag_done, 0));
+        CK(cudaGetLastError());
+        return;
+    }
+    const int k = fork_groups(bs);
+    for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
+        Group& g = bs->groups[gi];
         group_update(bs, g, 0, g.nb, EPI_APPLY, lr_eff, g.d_apply, nullptr, stream_for(bs, k, int(gi)));
     }
     cudaStream_t as = stream_for(bs, k, int(bs->groups.size()));  // AdamW on the least loaded group stream
-    // AdamW for every owned 1-D / degenerate parameter in one launch (they step together)
+    adamw_impl(bs, clip_scale, lr_eff, as);
+    join_groups(bs, k);
+    CK(cudaGetLastError());
+}
+
+// AdamW for every owned 1-D / degenerate parameter in one launch (they step together)
+void adamw_impl(asg_blockset* bs, double clip_scale, float lr_eff, cudaStream_t as) {
     int64_t t_adam = 0;
     for (Unit& u : bs->units) {
         if (!u.adamw || u.owner != bs->rank) continue;
@@ -2040,13 +2435,17 @@ void precondition_apply_impl(asg_blockset* bs, double clip_scale, double lr_scal
     }
     if (bs->n_adam > 0) {
         const double t = double(t_adam);
-        launch_adamw_multi(bs->d_adam, bs->n_adam, bs->adam_max_elems, float(clip_scale), float(bs->opt.beta1),
-                           float(bs->opt.beta2), float(1.0 / (1.0 - std::pow(bs->opt.beta1, t))),
-                           float(1.0 / (1.0 - std::pow(bs->opt.beta2, t))), float(bs->opt.eps), lr_eff,
-                           float(bs->opt.weight_decay), bs->d_flag, as);
+        double elems = 0.0;
+        for (const Unit& u : bs->units)
+            if (u.adamw && u.owner == bs->rank)
+                elems += double(u.spec.row_end - u.spec.row_begin) * double(u.spec.col_end - u.spec.col_begin);
+        hbm_launch(bs, as, ASG_HBM_ADAMW, 28.0 * elems, [&] {  // theta r/w, g r, m r/w, v r/w
+            launch_adamw_multi(bs->d_adam, bs->n_adam, bs->adam_max_elems, float(clip_scale), float(bs->opt.beta1),
+                               float(bs->opt.beta2), float(1.0 / (1.0 - std::pow(bs->opt.beta1, t))),
+                               float(1.0 / (1.0 - std::pow(bs->opt.beta2, t))), float(bs->opt.eps), lr_eff,
+                               float(bs->opt.weight_decay), bs->d_upd_flag, as);
+        });
     }
-    join_groups(bs, k);
-    CK(cudaGetLastError());
 }
 }  // namespace
 
@@ -2083,18 +2482,11 @@ int asg_step(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale,
             CK(cudaStreamWaitEvent(bs->main, e, 0));
             CK(cudaEventDestroy(e));
         }
-        // accumulate (all owned blocks, batched per shape group, groups concurrent)
-        {
-            const int k = fork_groups(bs);
-            for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
-                Group& g = bs->groups[gi];
-                cudaStream_t gs = stream_for(bs, k, int(gi));
-                launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs,
-                                 g.vec_grad);
-                group_stats(bs, g, 0, g.nb, gs);
-            }
-            join_groups(bs, k);
-        }
+        static const bool host_timing = getenv("ASG_HOST_TIMING") != nullptr;  // diagnostics
+        using clk = std::chrono::steady_clock;
+        const auto t0 = clk::now();
+        accumulate_impl(bs, clip_scale);
+        const auto t1 = clk::now();
         // per-block dispatch -> barrier in the reference's order (harness.cpp:452-454);
         // a barrier install launches any outstanding refresh first.
         for (size_t i = 0; i < bs->units.size(); ++i) {
@@ -2104,8 +2496,16 @@ int asg_step(asg_blockset* bs, int64_t step, double clip_scale, double lr_scale,
             sched_barrier(bs, int(i), step);
         }
         run_deferred_installs(bs);
+        const auto t2 = clk::now();
         precondition_apply_impl(bs, clip_scale, lr_scale);
+        const auto t3 = clk::now();
         sched_step_end(bs, step);
+        const auto t4 = clk::now();
+        if (host_timing) {
+            auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "asg_step %lld host ms: accumulate %.2f dispatch/barrier/install %.2f update %.2f step_end %.2f\n",
+                         (long long)step, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+        }
         if (s != bs->main) {
             cudaEvent_t e;
             CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -2152,6 +2552,7 @@ int asg_synchronize(asg_blockset* bs) {
         CK(cudaSetDevice(bs->device));
         CK(cudaStreamSynchronize(bs->main));
         CK(cudaStreamSynchronize(bs->side));
+        resolve_deferred(bs, true);
         check_flag(bs);
     });
 }
@@ -2470,13 +2871,21 @@ int asg_grad_sqnorm_owned(asg_blockset* bs, void* stream, double* sqnorm, int32_
                           u.spec.col_end - u.spec.col_begin, d.ld_grad, bs->d_sqnorm, bs->d_flag, s);
         }
         double v = 0.0;
-        int f = 0;
+        int f = 0, fu = 0;
         CK(cudaMemcpyAsync(&v, bs->d_sqnorm, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(&f, bs->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        // the previous step's update flag (s is ordered after the step that wrote it)
+        CK(cudaMemcpyAsync(&fu, bs->d_upd_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         CK(cudaMemsetAsync(bs->d_flag, 0, sizeof(int), s));
         if (sqnorm) *sqnorm = v;
         if (nonfinite) *nonfinite = f;
+        resolve_deferred(bs, false);
+        if (fu) {
+            CK(cudaMemsetAsync(bs->d_upd_flag, 0, sizeof(int), s));
+            throw Fail{ASG_ERR_NON_FINITE, "apply_update: the previous step's update was non-finite "
+                                           "(those elements of theta were left unchanged)"};
+        }
     });
 }
 
@@ -2492,6 +2901,31 @@ int asg_profile_enable(asg_blockset* bs, int32_t enable) {
     return guard([&] {
         bs->profiling = enable != 0;
         bs->launch_base = launch_count();
+    });
+}
+
+int asg_get_hbm_stats(asg_blockset* bs, asg_hbm_stats* out, int32_t reset) {
+    return guard([&] {
+        CK(cudaSetDevice(bs->device));
+        CK(cudaStreamSynchronize(bs->main));
+        CK(cudaStreamSynchronize(bs->side));
+        CK(cudaDeviceSynchronize());  // the norm runs on the caller's stream
+        *out = asg_hbm_stats{};
+        for (auto& h : bs->prof_hbm) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, h.e0, h.e1));
+            if (h.kind < 0 || h.kind >= ASG_HBM_KINDS) continue;
+            out->launches[h.kind] += 1;
+            out->bytes[h.kind] += h.bytes;
+            out->ms[h.kind] += t;
+        }
+        if (reset) {
+            for (auto& h : bs->prof_hbm) {
+                cudaEventDestroy(h.e0);
+                cudaEventDestroy(h.e1);
+            }
+            bs->prof_hbm.clear();
+        }
     });
 }
 
@@ -2659,5 +3093,172 @@ int asg_sym_eig_batched_f32(const float* A, double* values, float* vectors, int6
         CK(cudaGetLastError());
         for (int v : st)
             if (v != ASG_OK) throw Fail{v, "sym_eig_batched_f32: a matrix failed"};
+    });
+}
+
+int asg_inv_root_batched_f32(const float* A, float* out, int64_t batch, int64_t n, int32_t p, double damping,
+                             int32_t precision, void* stream) {
+    return guard([&] {
+        if (n < 1 || batch < 1) throw Fail{ASG_ERR_INVALID_ARGUMENT, "inv_root_batched_f32: empty batch"};
+        if (p != 2 && p != 4) throw Fail{ASG_ERR_INVALID_ARGUMENT, "inv_root_batched_f32: p must be 2 or 4"};
+        if (n > 4096) throw Fail{ASG_ERR_UNSUPPORTED, "inv_root_batched_f32: n must be <= 4096"};
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        int sms = 148;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int D = int(round_up(n, 128));
+        const size_t DD = size_t(D) * D, nbDD = size_t(batch) * DD;
+        const int bn = gemm_bn_for(D);
+        std::vector<int2> tl(size_t(gemm_sym_tile_list(D, bn, nullptr)));
+        gemm_sym_tile_list(D, bn, tl.data());
+        float *Ap = nullptr, *R = nullptr, *ws = nullptr;
+        double* eps = nullptr;
+        int* status = nullptr;
+        int2* tiles = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&Ap), nbDD * 4, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&R), 2 * nbDD * 4, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), ns_workspace_floats(int(batch), D) * 4, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&eps), size_t(batch) * 8, s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&status), size_t(batch) * sizeof(int), s));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&tiles), tl.size() * sizeof(int2), s));
+        CK(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(status, 0, size_t(batch) * sizeof(int), s));
+        pad_f32_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(A, int(n), D, Ap);
+        count_launch(1);
+        launch_relative_damping_f32(Ap, int(batch), D, int(n), damping, eps, s);
+        launch_ns_inv_root(Ap, int(batch), int(n), D, eps, p, R, precision == ASG_PREC_3XTF32 ? R + nbDD : nullptr, ws,
+                           status, tiles, int(tl.size()), precision, sms, s);
+        if (precision != ASG_PREC_3XTF32) CK(cudaMemsetAsync(R + nbDD, 0, nbDD * 4, s));
+        unpad_sum_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(R, R + nbDD, int(n), D, out);
+        count_launch(1);
+        std::vector<int> st(static_cast<size_t>(batch));
+        CK(cudaMemcpyAsync(st.data(), status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (void* ptr : {static_cast<void*>(Ap), static_cast<void*>(R), static_cast<void*>(ws), static_cast<void*>(eps),
+                          static_cast<void*>(status), static_cast<void*>(tiles)})
+            CK(cudaFreeAsync(ptr, s));
+        CK(cudaGetLastError());
+        for (int v : st)
+            if (v != ASG_OK) throw Fail{v, "inv_root_batched_f32: a matrix failed"};
+    });
+}
+
+// ---- NCCL and the bucketed parameter all-gather -------
+int asg_nccl_unique_id(uint8_t* out) {
+    return guard([&] {
+        if (!out) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null output"};
+        ncclUniqueId id;
+        nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+    });
+}
+
+int asg_nccl_comm_init(int32_t world, int32_t rank, const uint8_t* id, void** comm) {
+    return guard([&] {
+        if (!id || !comm || world < 1 || rank < 0 || rank >= world) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad arguments"};
+        ncclUniqueId uid;
+        std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+        ncclComm_t c = nullptr;
+        nccl_check(nccl().CommInitRank(&c, world, uid, rank), "ncclCommInitRank");
+        *comm = c;
+    });
+}
+
+int asg_nccl_comm_destroy(void* comm) {
+    return guard([&] {
+        if (comm) nccl_check(nccl().CommDestroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+    });
+}
+
+int asg_set_allgather_buckets(asg_blockset* bs, int32_t buckets_per_shape) {
+    return guard([&] {
+        if (!bs || buckets_per_shape < 1) throw Fail{ASG_ERR_INVALID_ARGUMENT, "buckets_per_shape must be >= 1"};
+        CK(cudaSetDevice(bs->device));
+        CK(cudaStreamSynchronize(bs->main));
+        build_buckets(bs, buckets_per_shape);
+        for (cudaEvent_t e : bs->ag_events) cudaEventDestroy(e);
+        bs->ag_events.assign(bs->buckets.size(), nullptr);
+        for (cudaEvent_t& e : bs->ag_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    });
+}
+
+int asg_bucket_count(const asg_blockset* bs, int64_t* count) {
+    return guard([&] {
+        if (!bs || !count) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        *count = int64_t(bs->buckets.size());
+    });
+}
+
+int asg_bucket_stride(const asg_blockset* bs, int64_t bucket, int64_t* stride) {
+    return guard([&] {
+        if (!bs || !stride || bucket < 0 || bucket >= int64_t(bs->buckets.size()))
+            throw Fail{ASG_ERR_INVALID_ARGUMENT, "bucket index out of range"};
+        *stride = bs->buckets[size_t(bucket)].stride;
+    });
+}
+
+int asg_bucket_pack(asg_blockset* bs, int64_t bucket, float* sendbuf, void* stream) {
+    return guard([&] {
+        if (!bs || bucket < 0 || bucket >= int64_t(bs->buckets.size()))
+            throw Fail{ASG_ERR_INVALID_ARGUMENT, "bucket index out of range"};
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        const auto& b = bs->buckets[size_t(bucket)];
+        launch_pack_blocks(b.d_pack_refs, b.d_pack_offs, b.n_pack, sendbuf, s);
+        CK(cudaGetLastError());
+    });
+}
+
+int asg_bucket_unpack(asg_blockset* bs, int64_t bucket, const float* recvbuf, void* stream) {
+    return guard([&] {
+        if (!bs || bucket < 0 || bucket >= int64_t(bs->buckets.size()))
+            throw Fail{ASG_ERR_INVALID_ARGUMENT, "bucket index out of range"};
+        CK(cudaSetDevice(bs->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        const auto& b = bs->buckets[size_t(bucket)];
+        launch_unpack_blocks(b.d_unpack_refs, b.d_unpack_offs, b.n_unpack, recvbuf, s);
+        CK(cudaGetLastError());
+    });
+}
+
+int asg_set_allgather_comm(asg_blockset* bs, void* comm, int32_t buckets_per_shape) {
+    return guard([&] {
+        if (!bs) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null blockset"};
+        CK(cudaSetDevice(bs->device));
+        if (comm) {
+            nccl();  // fail now if NCCL cannot be loaded
+            if (buckets_per_shape < 1) throw Fail{ASG_ERR_INVALID_ARGUMENT, "buckets_per_shape must be >= 1"};
+            if (int(bs->buckets.size()) == 0 || bs->buckets_per_shape != buckets_per_shape) {
+                if (int rc = asg_set_allgather_buckets(bs, buckets_per_shape)) throw Fail{rc, g_err};
+            }
+            if (!bs->comm_stream) {
+                int lo = 0, hi = 0;
+                CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                CK(cudaStreamCreateWithPriority(&bs->comm_stream, cudaStreamNonBlocking, hi));
+                CK(cudaEventCreateWithFlags(&bs->ag_done, cudaEventDisableTiming));
+            }
+        }
+        bs->ag_comm = comm;
+    });
+}
+
+int asg_allgather_params(asg_blockset* bs, void* comm, void* stream) {
+    return guard([&] {
+        if (!bs || !comm) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null blockset or communicator"};
+        CK(cudaSetDevice(bs->device));
+        if (bs->buckets.empty()) {
+            if (int rc = asg_set_allgather_buckets(bs, 1)) throw Fail{rc, g_err};
+        }
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        if (s != bs->main) {  // after the step's update
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CK(cudaEventRecord(e, bs->main));
+            CK(cudaStreamWaitEvent(s, e, 0));
+            CK(cudaEventDestroy(e));
+        }
+        for (const auto& b : bs->buckets) bucket_exchange(bs, b, static_cast<ncclComm_t>(comm), s);
+        CK(cudaGetLastError());
     });
 }

@@ -61,6 +61,10 @@ class AsteriaOptimizer:
 
     def __del__(self):
         if getattr(self, "_h", None):
+            if getattr(self, "_nccl", None):
+                lib.asg_set_allgather_comm(self._h, None, 1)
+                lib.asg_nccl_comm_destroy(self._nccl)
+                self._nccl = None
             lib.asg_blockset_destroy(self._h)
             self._h = None
 
@@ -156,6 +160,13 @@ class AsteriaOptimizer:
         check(lib.asg_get_kernel_stats(self._h, C.byref(k), 1 if reset else 0))
         return k
 
+    def hbm_stats(self, reset=True):
+        """HBM-bound kernels (prep, clip norm, AdamW) timed while profiling:
+        {name: (launches, algorithmic bytes, ms)}."""
+        h = abi.HbmStats()
+        check(lib.asg_get_hbm_stats(self._h, C.byref(h), 1 if reset else 0))
+        return {abi.HBM_NAMES[k]: (h.launches[k], h.bytes[k], h.ms[k]) for k in range(abi.HBM_KINDS)}
+
     # ---- multi-GPU ------------------------------------------------------------
     def shard_elems(self, rank):
         e = C.c_int64()
@@ -212,14 +223,82 @@ class AsteriaOptimizer:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         return float(t.item())
 
+    def set_allgather_buckets(self, buckets_per_shape):
+        """Bucketed all-gather layout (asg_set_allgather_buckets): allgather()
+        then exchanges bucket by bucket."""
+        check(lib.asg_set_allgather_buckets(self._h, buckets_per_shape))
+        n = C.c_int64()
+        check(lib.asg_bucket_count(self._h, C.byref(n)))
+        self._buckets = []
+        for b in range(n.value):
+            st = C.c_int64()
+            check(lib.asg_bucket_stride(self._h, b, C.byref(st)))
+            self._buckets.append(st.value)
+
+    def use_nccl(self, group=None, buckets_per_shape=4, fused=True):
+        """This library's own NCCL communicator over the ranks (the 128-byte
+        unique id is broadcast through torch.distributed when world > 1).
+        fused: asg_step all-gathers bucket b while it updates bucket b+1
+        (asg_set_allgather_comm); otherwise allgather() calls
+        asg_allgather_params after the step."""
+        import torch
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            check(lib.asg_nccl_unique_id(uid))
+        if self.world > 1:
+            import torch.distributed as dist
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.to(self.device)
+            dist.broadcast(t, src=0, group=group)
+            uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+        comm = C.c_void_p()
+        check(lib.asg_nccl_comm_init(self.world, self.rank, uid, C.byref(comm)))
+        self._nccl = comm
+        self._nccl_fused = fused
+        if fused:
+            check(lib.asg_set_allgather_comm(self._h, comm, buckets_per_shape))
+        else:
+            self.set_allgather_buckets(buckets_per_shape)
+
+    def close_nccl(self):
+        if getattr(self, "_nccl", None):
+            check(lib.asg_set_allgather_comm(self._h, None, 1))
+            check(lib.asg_nccl_comm_destroy(self._nccl))
+            self._nccl = None
+
     def allgather(self, group=None, stream=None):
         """All-gathers every rank's owned (updated) block slices of theta and
-        scatters them back into the parameters (owner-major layout). NCCL
-        groups gather in HBM; gloo groups (CPU test harness) stage through host
-        memory."""
+        scatters them back into the parameters. With use_nccl: the library's
+        own NCCL collective (fused into the step, or asg_allgather_params
+        here). Otherwise through torch.distributed: bucket by bucket after
+        set_allgather_buckets, else one owner-major buffer; NCCL groups gather
+        in HBM, gloo groups (CPU test harness) stage through host memory."""
         import torch
         import torch.distributed as dist
+        if getattr(self, "_nccl", None):
+            if not self._nccl_fused:
+                check(lib.asg_allgather_params(self._h, self._nccl,
+                                               stream_arg(stream or torch.cuda.current_stream(self.device))))
+            return
         if self.world == 1:
+            return
+        if getattr(self, "_buckets", None):
+            cur = torch.cuda.current_stream(self.device)
+            cur.wait_stream(torch.cuda.ExternalStream(self.stream_handle))
+            for b, stride in enumerate(self._buckets):
+                send = torch.zeros(max(1, stride), dtype=torch.float32, device=self.device)
+                check(lib.asg_bucket_pack(self._h, b, C.c_void_p(send.data_ptr()), stream_arg(cur)))
+                if dist.get_backend(group) == "nccl":
+                    recv = torch.empty(max(1, stride) * self.world, dtype=torch.float32, device=self.device)
+                    dist.all_gather_into_tensor(recv, send, group=group)
+                else:
+                    r_cpu = torch.empty(max(1, stride) * self.world, dtype=torch.float32)
+                    dist.all_gather_into_tensor(r_cpu, send.cpu(), group=group)
+                    recv = r_cpu.to(self.device)
+                if stride == 0:
+                    continue
+                check(lib.asg_bucket_unpack(self._h, b, C.c_void_p(recv.data_ptr()), stream_arg(cur)))
             return
         stride = self.gather_stride()
         if self._gather_buf is None:

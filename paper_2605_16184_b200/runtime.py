@@ -73,6 +73,18 @@ _SIGS = {
     "asg_gemm_tn": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _f32, _i32, _vp]),
     "asg_sym_eig_batched": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "asg_sym_eig_batched_f32": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "asg_set_allgather_buckets": (C.c_int, [_vp, _i32]),
+    "asg_bucket_count": (C.c_int, [_vp, _P(_i64)]),
+    "asg_bucket_stride": (C.c_int, [_vp, _i64, _P(_i64)]),
+    "asg_bucket_pack": (C.c_int, [_vp, _i64, _vp, _vp]),
+    "asg_bucket_unpack": (C.c_int, [_vp, _i64, _vp, _vp]),
+    "asg_nccl_unique_id": (C.c_int, [_vp]),
+    "asg_nccl_comm_init": (C.c_int, [_i32, _i32, _vp, _P(_vp)]),
+    "asg_nccl_comm_destroy": (C.c_int, [_vp]),
+    "asg_allgather_params": (C.c_int, [_vp, _vp, _vp]),
+    "asg_set_allgather_comm": (C.c_int, [_vp, _vp, _i32]),
+    "asg_get_hbm_stats": (C.c_int, [_vp, _P(abi.HbmStats), _i32]),
+    "asg_inv_root_batched_f32": (C.c_int, [_vp, _vp, _i64, _i64, _i32, C.c_double, _i32, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

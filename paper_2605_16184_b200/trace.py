@@ -12,6 +12,7 @@ audit_staleness (proj/src/metrics.cpp:131-210), so a GPU run can be audited
 with the reference's own rule set and file format.
 """
 import json
+import math
 
 from . import abi
 
@@ -35,7 +36,7 @@ def events_from_optimizer(opt, worker=0, param_names=None):
         if e.block not in ids:
             ids[e.block] = block_id(opt.block_info(e.block).spec, param_names)
         rows.append({"step": int(e.step), "worker": int(worker), "event": EVENT_NAMES[e.kind],
-                     "block_id": ids[e.block], "version": int(e.version), "t_micros": int(e.t_us), "seq": seq})
+                     "block_id": ids[e.block], "version": int(e.version), "t_micros": int(math.floor(e.t_us + 0.5)), "seq": seq})
     return rows
 
 

@@ -148,3 +148,91 @@ def test_reduce_scatter_grads_matches_averaged_single_rank(tmp_path):
         np.testing.assert_allclose(norms, ref_norms, rtol=1e-5)
         for a, b in zip(out, ref):
             np.testing.assert_allclose(a, b, rtol=0, atol=1e-6 * max(1.0, float(np.abs(b).max())))
+
+
+# ---- bucketed all-gather (asg_bucket_pack / asg_bucket_unpack) -------------------
+def _bucket_worker(rank, world, store, steps, q):
+    import torch.distributed as dist
+    _init(rank, world, store)
+    out = _run_buckets(rank, world, steps)
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run_buckets(rank, world, steps, buckets=2):
+    """As _run, exchanging bucket by bucket (the layout the fused NCCL path
+    uses: every shape's units split into runs, 1-D parameters last)."""
+    from paper_2605_16184_b200 import abi, runtime
+    from paper_2605_16184_b200.optimizer import AsteriaOptimizer
+    opt = runtime.optimizer_defaults(abi.SOAP)
+    opt.lr, opt.block_dim_limit, opt.precondition_frequency = 1e-2, 128, 2
+    sched = runtime.scheduler_defaults()
+    sched.pf, sched.staleness_S = 2, 1
+    g = torch.Generator().manual_seed(0)
+    params = [(0.1 * torch.randn(*s, generator=g)).cuda() for s in SHAPES]
+    grads = [torch.zeros_like(p) for p in params]
+    o = AsteriaOptimizer(params, grads, opt, sched, rank=rank, world=world)
+    o.set_allgather_buckets(buckets)
+    assert len(o._buckets) >= 4  # (128,128) x2 runs, (128,...) ..., AdamW
+    for step in range(steps):
+        for gr in grads:
+            gr.copy_(1e-3 * torch.randn(*gr.shape, generator=g))
+        o.clock_advance(sched.step_compute_us)
+        o.step(step)
+        o.allgather()
+    o.synchronize()
+    return [p.cpu().numpy() for p in params]
+
+
+def test_two_ranks_bucketed_allgather_match_single_rank(tmp_path):
+    import torch.multiprocessing as mp
+    steps = 4
+    ref, _ = _run(0, 1, steps)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    store = str(tmp_path / "store")
+    procs = [ctx.Process(target=_bucket_worker, args=(r, 2, store, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(2):
+        rank, out = q.get(timeout=600)
+        results[rank] = out
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        for a, b in zip(results[rank], ref):
+            assert np.array_equal(a, b), np.abs(a - b).max()
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_nccl_allgather_through_the_c_abi_single_rank(fused):
+    """The library's own NCCL path (asg_nccl_comm_init, asg_set_allgather_comm /
+    asg_allgather_params) at world 1: every bucket's pack -> ncclAllGather ->
+    scatter runs (fused: on the communication stream, bucket b overlapping the
+    update of b+1) and must leave the parameters bit-identical to a run
+    without any collective."""
+    ref, _ = _run(0, 1, 4)
+    from paper_2605_16184_b200 import abi, runtime
+    from paper_2605_16184_b200.optimizer import AsteriaOptimizer
+    opt = runtime.optimizer_defaults(abi.SOAP)
+    opt.lr, opt.block_dim_limit, opt.precondition_frequency = 1e-2, 128, 2
+    sched = runtime.scheduler_defaults()
+    sched.pf, sched.staleness_S = 2, 1
+    g = torch.Generator().manual_seed(0)
+    params = [(0.1 * torch.randn(*s, generator=g)).cuda() for s in SHAPES]
+    grads = [torch.zeros_like(p) for p in params]
+    o = AsteriaOptimizer(params, grads, opt, sched)
+    o.use_nccl(buckets_per_shape=3, fused=fused)
+    for step in range(4):
+        for gr in grads:
+            gr.copy_(1e-3 * torch.randn(*gr.shape, generator=g))
+        o.clock_advance(sched.step_compute_us)
+        o.step(step)
+        o.allgather()
+    o.synchronize()
+    o.close_nccl()
+    for a, b in zip([p.cpu().numpy() for p in params], ref):
+        assert np.array_equal(a, b), np.abs(a - b).max()

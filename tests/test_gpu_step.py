@@ -230,3 +230,55 @@ def test_event_mode_bounded_staleness(O):
     assert st.installed >= 10 and st.dispatched == st.installed + st.pending
     assert worst <= (sched.staleness_S + 1) * sched.pf
     assert torch.isfinite(W).all()
+
+
+def test_event_barrier_does_not_block_and_books_the_device_wait(O):
+    """EVENT install mode, S = 0: every step's refresh is installed at the same
+    step's barrier (asyncsched.cpp:191-221). The install makes the main stream
+    wait on the refresh event instead of blocking the host; the device-side
+    wait is measured and booked into wait_total_us at the next host sync."""
+    from paper_2605_16184_b200 import runtime
+    opt = runtime.optimizer_defaults(abi.SOAP)
+    opt.precondition_frequency = 1
+    sched = runtime.scheduler_defaults()
+    sched.pf, sched.staleness_S, sched.install_mode, sched.refresh_mode = 1, 0, abi.INSTALL_EVENT, abi.REFRESH_F32
+    W = (0.1 * torch.randn(512, 512, device="cuda")).contiguous()
+    G = torch.randn(512, 512, device="cuda") * 1e-3
+    o = O.AsteriaOptimizer([W], [G], opt, sched)
+    for step in range(4):
+        G.normal_(0.0, 1e-3)
+        o.step(step)
+    o.synchronize()
+    st = o.stats()
+    assert st.installed == 4 and st.barrier_waits == 4
+    assert st.wait_total_us > 0.0
+    assert torch.isfinite(W).all()
+
+
+def test_non_finite_update_leaves_theta_and_surfaces_at_sync(O):
+    """apply_update (precond.cpp:244-251) throws NonFinite without touching
+    theta. The fused apply epilogue leaves every non-finite update element's
+    theta unchanged, sets the update flag, and the next host sync raises
+    NonFiniteError (the gradient-norm flag is separate)."""
+    from paper_2605_16184_b200 import runtime
+    opt = runtime.optimizer_defaults(abi.SHAMPOO)
+    opt.precondition_frequency = 100
+    sched = runtime.scheduler_defaults()
+    sched.pf, sched.staleness_S = 100, 0
+    W = (0.1 * torch.randn(128, 128, device="cuda")).contiguous()
+    G = (1e-3 * torch.randn(128, 128, device="cuda")).contiguous()
+    o = O.AsteriaOptimizer([W], [G], opt, sched)
+    o.step(0)  # refresh dispatched and installed at step 0 (S = 0)
+    o.synchronize()
+    inv = o.read_block(0, abi.INV_L)
+    inv[3, 5] = float("nan")
+    import ctypes as C
+    runtime.check(runtime.lib.asg_block_write(o._h, 0, abi.INV_L, inv.ctypes.data_as(C.POINTER(C.c_double)), inv.size))
+    before = W.clone()
+    o.step(1)  # no refresh at step 1: the update uses the poisoned root -> row 3 of U is NaN
+    with pytest.raises(abi.NonFiniteError):
+        o.synchronize()
+    assert torch.equal(W[3], before[3])
+    assert torch.isfinite(W).all()
+    assert not torch.equal(W[4], before[4])
+    o.synchronize()  # flag cleared once reported
