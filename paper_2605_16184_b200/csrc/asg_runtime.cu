@@ -2147,7 +2147,8 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         int lo = 0, hi = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CK(cudaStreamCreateWithPriority(&bs->main, cudaStreamNonBlocking, hi));
-        CK(cudaStreamCreateWithPriority(&bs->side, cudaStreamNonBlocking, lo));
+        static const bool same_prio = getenv("ASG_SIDE_SAME_PRIORITY") != nullptr;  // diagnostics
+        CK(cudaStreamCreateWithPriority(&bs->side, cudaStreamNonBlocking, same_prio ? hi : lo));
         bs->own_main = true;
         for (int k = 0; k < asg_blockset::kGroupStreams; ++k) {
             CK(cudaStreamCreateWithPriority(&bs->gstream[k], cudaStreamNonBlocking, hi));
