@@ -193,21 +193,32 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_baseline(wl, native=False, refresh_n=512):
-    """The fp64 oracle (a restatement of the reference's hot path, -O3 as the
-    reference's Release flags; native=True: the same sources -O3
-    -march=native compiled on this host) timed on:
-      * one block step (accumulate_factors + precondition + apply) at the
-        workload's dominant block shape, single thread (the reference runs its
-        per-block loop on one thread per rank, harness.cpp:448);
-      * one refresh (compute_refresh + install, precond.cpp:129-164) of a
-        refresh_n x refresh_n block: the oracle's cyclic Jacobi needs minutes
-        per 2048^2 factor, so the refresh is sampled at n = 512 and scaled by
-        n^3, spread over the host's cores (the reference's refresh pool,
-        harness.cpp:312-316).
-    Extrapolated to the workload by block count and shape (step: mn(m+n);
-    refresh: m^3 + n^3, amortised over pf). Returns the measured sample times,
-    the extrapolation and the resulting per-step time."""
+def cpu_sample_shape(wl):
+    """The workload's dominant block shape scaled so that one sampled step
+    (plus 1/pf of a refresh) is about a second of CPU work: the oracle's
+    cyclic Jacobi needs ~20 s per 512^2 factor pair and minutes per 2048^2
+    factor."""
+    blocks = [b for s in wl["shapes"] for b in blocks_of(s, wl["limit"])]
+    m, n = max(set(blocks), key=blocks.count)
+    side = 512 if wl["pf"] >= 10 else 256
+    f = min(1.0, side / max(m, n))
+    return (m, n), (max(8, int(round(m * f))), max(8, int(round(n * f))))
+
+
+def cpu_baseline(wl, steps, warmup, native=False):
+    """The reference path on the host CPU: the fp64 oracle (a restatement of
+    the reference's per-block loop, harness.cpp:448-471 with the synchronous
+    refresh of reference_opt.cpp:96-99: accumulate_factors, refresh every pf
+    steps, precondition, apply_update), built -O3 as the reference's Release
+    flags (native=True: the same sources -O3 -march=native, compiled on this
+    host), on ONE block of the workload's dominant shape scaled to a bounded
+    sample (cpu_sample_shape), with fresh N(0, 1/cols) gradients every step,
+    single thread. Each step is one such block step; value is the algorithmic
+    flop rate of the timed steps (SURVEY 8(d) conventions for the sampled
+    shape), the same metric as the GPU arm; workload_ms_per_step scales the
+    measured time to the workload by its block count and shapes (mn(m+n) for
+    the step, n^3 for the refresh, refreshes on an nproc-thread pool,
+    harness.cpp:312-316)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
     import orc
@@ -216,37 +227,45 @@ def cpu_baseline(wl, native=False, refresh_n=512):
     meth = {"SOAP": abi.SOAP, "KL-Shampoo": abi.KL_SHAMPOO, "Shampoo": abi.SHAMPOO}[wl["method"]]
     cfg = orc.defaults_for(meth)
     cfg.precondition_frequency = wl["pf"]
-    blocks = [b for s in wl["shapes"] for b in blocks_of(s, wl["limit"])]
-    m, n = max(set(blocks), key=blocks.count)  # dominant shape
-    g = orc.random_matrix(m, n, 1) / math.sqrt(n)
-    theta = np.zeros((m, n))
+    cfg.accumulation = abi.EMA if wl["accumulation"] == "EMA" else abi.SUM
+    cfg.lr = wl["lr"]
+    (M, N), (m, n) = cpu_sample_shape(wl)
     blk = orc.Block(m, n, meth)
-    # the update path of a refreshed block (version > 0): identity inverses/bases installed
-    blk.set_counters(1, 0, 0)
-    t0 = time.perf_counter()
-    orc.accumulate_factors(blk, g, cfg)
-    theta = orc.apply_update(theta, orc.step_update(blk, g, cfg), cfg)
-    t_step = time.perf_counter() - t0
-    r = refresh_n
-    rb = orc.Block(r, r, meth)
-    for k in range(3):
-        orc.accumulate_factors(rb, orc.random_matrix(r, r, 10 + k) / math.sqrt(r), cfg)
-    t0 = time.perf_counter()
-    orc.refresh_inverse(rb, cfg, 0)
-    t_ref = time.perf_counter() - t0
+    theta = np.zeros((m, n))
+    rng = np.random.default_rng(1234)
+    t_step, t_ref, n_ref = 0.0, 0.0, 0
+    for k in range(warmup + steps):
+        g = rng.standard_normal((m, n)) / math.sqrt(n)
+        t0 = time.perf_counter()
+        orc.accumulate_factors(blk, g, cfg)
+        t1 = time.perf_counter()
+        if k % wl["pf"] == 0:
+            orc.refresh_inverse(blk, cfg, k)
+        t2 = time.perf_counter()
+        theta = orc.apply_update(theta, orc.step_update(blk, g, cfg), cfg)
+        t3 = time.perf_counter()
+        if k >= warmup:
+            t_step += (t1 - t0) + (t3 - t2)
+            t_ref += t2 - t1
+            n_ref += (k % wl["pf"] == 0)
+    sample_wl = dict(wl, shapes=[(m, n)], limit=max(m, n))
+    st_f, ref_f, _ = alg_flops(sample_wl)
+    flops = st_f * steps + ref_f * n_ref
+    wall = t_step + t_ref
     cores = os.cpu_count() or 1
-    tot_step = sum(t_step * (bm * bn * (bm + bn)) / (m * n * (m + n)) for (bm, bn) in blocks)
-    tot_ref = sum(t_ref * (bm ** 3 + bn ** 3) / (2 * r ** 3) for (bm, bn) in blocks)
-    t_per_step = tot_step + tot_ref / wl["pf"] / cores
-    _, _, flops = alg_flops(wl)
-    return {"value": flops / t_per_step / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-            "ms_per_step": t_per_step * 1e3, "sample_wall_s": t_step + t_ref,
-            "extrapolation": t_per_step / (t_step + t_ref / wl["pf"]),
+    blocks = [b for s in wl["shapes"] for b in blocks_of(s, wl["limit"])]
+    step_ps = t_step / steps
+    ref_each = t_ref / n_ref if n_ref else 0.0
+    w_step = sum(step_ps * (bm * bn * (bm + bn)) / (m * n * (m + n)) for (bm, bn) in blocks)
+    w_ref = sum(ref_each * (bm ** 3 + bn ** 3) / (m ** 3 + n ** 3) for (bm, bn) in blocks)
+    return {"value": flops / wall / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "port",
+            "ms_per_step": wall * 1e3 / steps, "wall_s": wall,
+            "workload_ms_per_step": (w_step + w_ref / wl["pf"] / cores) * 1e3,
             "sample": (f"oracle (fp64 restatement of the reference path, -O3{' -march=native' if native else ''}, "
-                       f"{cpu_model()}, {cores} cores): one {m}x{n} {wl['method']} block step single-thread "
-                       f"{t_step:.2f} s; one {r}x{r} refresh {t_ref:.2f} s (cyclic Jacobi); extrapolated to "
-                       f"{len(blocks)} blocks by mn(m+n) (step) and n^3 (refresh, {cores}-thread pool, every "
-                       f"pf={wl['pf']} steps)")}
+                       f"{cpu_model()}): {steps} timed steps of one {m}x{n} {wl['method']} block (the workload's "
+                       f"dominant {M}x{N} shape scaled to a bounded sample), fresh gradients, {n_ref} synchronous "
+                       f"refreshes (cyclic Jacobi) every pf={wl['pf']} steps, single thread; "
+                       f"{step_ps*1e3:.1f} ms per block step, {ref_each:.1f} s per refresh")}
 
 
 def cpu_eigh_baseline(n, batch, native=False, ns=384):
@@ -443,23 +462,27 @@ def main():
             total = (1 << 31) // (args.n * args.n)
             cb = cpu_eigh_baseline(args.n, total)
             cfg_out = {"workload": wl["name"], "n": args.n, "factors": total}
+            cb["wall_s"] = cb["sample_wall_s"]
+            steps_run = 1
         else:
-            cb = cpu_baseline(wl)
+            cb = cpu_baseline(wl, args.steps, args.warmup)
+            steps_run = args.steps
         metric = ("batched refresh eigensolve throughput (algorithmic TFLOP/s, 9n^3 per factor)" if args.workload == "C5"
                   else "optimizer step throughput (algorithmic TFLOP/s); step latency in ms_per_step")
         line = {"impl": "reference", "metric": metric,
-                "value": cb["value"], "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": 1,
-                "warmup": 0, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+                "value": cb["value"], "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": steps_run,
+                "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": cfg_out,
                 "cpu_baseline": {"value": cb["value"], "unit": "TFLOP/s", "cores": cb["cores"], "kind": "port",
-                                 "sample": cb["sample"], "sample_wall_s": cb["sample_wall_s"],
-                                 "extrapolation": cb["extrapolation"]},
-                "note": ("the reference path (its own sources are unbuildable here: Eigen3 absent, DESIGN.md §4) "
-                         "restated as the fp64 oracle; one sampled block step + one sampled refresh were timed "
-                         f"({cb['sample_wall_s']:.1f} s of CPU work) and extrapolated x{cb['extrapolation']:.0f} "
-                         "to the workload's per-step time (ms_per_step)"),
+                                 "sample": cb["sample"], "wall_s": cb["wall_s"]},
+                "note": ("the reference path restated as the fp64 oracle (the reference's own sources are "
+                         "unbuildable here: Eigen3 absent, DESIGN.md §4); each step is a bounded sample of the "
+                         "workload (see cpu_baseline.sample), value is its algorithmic flop rate and ms_per_step "
+                         "its measured time"),
                 "e2e": {"value": cb["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        if "workload_ms_per_step" in cb:
+            line["workload_ms_per_step_extrapolated"] = cb["workload_ms_per_step"]
         print(json.dumps(line), flush=True)
         return
 
@@ -675,12 +698,12 @@ def main():
         "state_bytes": o.state_bytes(),
     }
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
-        cb = cpu_baseline(wl)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "sample_wall_s",
-                                                   "extrapolation")}
+        cb = cpu_baseline(wl, steps=10, warmup=1)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "wall_s",
+                                                   "workload_ms_per_step")}
         try:
-            cn = cpu_baseline(wl, native=True)
-            line["cpu_baseline"]["native"] = {k: cn[k] for k in ("value", "sample_wall_s", "sample")}
+            cn = cpu_baseline(wl, steps=10, warmup=1, native=True)
+            line["cpu_baseline"]["native"] = {k: cn[k] for k in ("value", "wall_s", "sample")}
         except Exception as e:  # -march=native build unavailable on this host
             line["cpu_baseline"]["native"] = {"unavailable": str(e)[:200]}
     print(json.dumps(line), flush=True)
