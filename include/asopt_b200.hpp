@@ -14,14 +14,22 @@
 //   precondition_shampoo    precond.hpp:109    precondition_shampoo (also KL-Shampoo)
 //   precondition_soap       precond.hpp:113    precondition_soap
 //   soap_scaled_step        precond.hpp:119    soap_scaled_step
+//   FactorSnapshot / snapshot_factors / compute_refresh / install_refresh
+//                           precond.hpp:77-98  same names (state in HBM; compute is pure)
+//   AdamState / adamw_step / apply_update
+//                           precond.hpp:122-134 same names (the step fuses them on the device)
+//   replicated_state / load_replicated_state
+//                           precond.hpp:138-139 same names (flat std::vector<double>)
+//   pack_spd / unpack_spd   densela.hpp:124-142 same names on host vectors (index shuffle only)
 //   asopt::*Error           errors.hpp:10-47   asopt::b200::*Error, thrown from status codes
 //
 // Matrices cross the boundary as host row-major double (`Matd`, the
 // reference's Eigen `Matd` is row-major double too, densela.hpp:29); inside,
 // state is fp32 on the GPU (3xTF32 tensor-core products, see DESIGN.md §4 for
-// the stated tolerances). `apply_update` / `adamw_step` are not re-exposed for
-// host matrices: on the device they are fused into the update GEMM's epilogue
-// (asg_precondition_apply / asg_step), and the shim adds no CPU arithmetic.
+// the stated tolerances). In the optimizer step, `apply_update` / `adamw_step`
+// are fused into the update GEMM's epilogue (asg_precondition_apply /
+// asg_step); the per-call versions here run their own device kernels. The
+// shim adds no CPU arithmetic.
 //
 // Link with -lasteria_b200 (paper_2605_16184_b200/csrc/build/).
 #pragma once
@@ -332,6 +340,134 @@ inline Matd soap_scaled_step(PrecondBlock& b, const Matd& g, const OptimizerConf
 inline Matd precondition_soap(PrecondBlock& b, const Matd& g, const OptimizerConfig& cfg) {
     if (b.version() == 0) throw StaleUninitializedError("precondition_soap: no refreshed basis installed");
     return soap_scaled_step(b, g, cfg);
+}
+
+// ---- the split refresh (precond.hpp:77-98) ---------------------------------------
+/// FactorSnapshot: device copies of a block's L and R (snapshot_factors precond.cpp:112-117).
+class FactorSnapshot {
+public:
+    FactorSnapshot(asg_blockset* bs, asg_snapshot* h) : bs_(bs), h_(h) {}
+    FactorSnapshot(FactorSnapshot&& o) noexcept : bs_(o.bs_), h_(o.h_) { o.h_ = nullptr; }
+    FactorSnapshot(const FactorSnapshot&) = delete;
+    FactorSnapshot& operator=(const FactorSnapshot&) = delete;
+    ~FactorSnapshot() {
+        if (h_) asg_snapshot_destroy(h_);
+    }
+    /// snapshot_checksum (precond.cpp:114-115) over the fp32 factor bytes.
+    uint64_t checksum() const {
+        uint64_t c = 0;
+        check(asg_snapshot_checksum(h_, &c));
+        return c;
+    }
+    asg_blockset* blockset() const { return bs_; }
+    const asg_snapshot* handle() const { return h_; }
+
+private:
+    asg_blockset* bs_;
+    asg_snapshot* h_;
+};
+
+/// RefreshResult (precond.hpp:83-87), held in HBM until installed.
+class RefreshResult {
+public:
+    explicit RefreshResult(asg_refresh_result* h) : h_(h) {}
+    RefreshResult(RefreshResult&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+    RefreshResult(const RefreshResult&) = delete;
+    RefreshResult& operator=(const RefreshResult&) = delete;
+    ~RefreshResult() {
+        if (h_) asg_refresh_result_destroy(h_);
+    }
+    asg_refresh_result* release() {
+        asg_refresh_result* h = h_;
+        h_ = nullptr;
+        return h;
+    }
+
+private:
+    asg_refresh_result* h_;
+};
+
+inline FactorSnapshot snapshot_factors(const PrecondBlock& b) {
+    asg_snapshot* h = nullptr;
+    check(asg_snapshot_factors(b.handle(), 0, &h));
+    return FactorSnapshot(b.handle(), h);
+}
+
+/// compute_refresh (precond.cpp:129-142): pure over the snapshot.
+inline RefreshResult compute_refresh(const FactorSnapshot& snap, const OptimizerConfig& cfg) {
+    (void)cfg;  // the snapshot's block carries the configuration its GPU state was created with
+    asg_refresh_result* h = nullptr;
+    check(asg_compute_refresh(snap.blockset(), snap.handle(), &h));
+    return RefreshResult(h);
+}
+
+/// install_refresh (precond.cpp:144-164): consumes the result.
+inline void install_refresh(PrecondBlock& b, RefreshResult&& r, int64_t step) {
+    check(asg_install_refresh(b.handle(), 0, r.release(), step));
+}
+
+// ---- AdamW and apply (precond.hpp:122-134) ------------------------------------------
+class AdamState {
+public:
+    AdamState(int64_t rows, int64_t cols) : rows_(rows), cols_(cols) { check(asg_adam_state_create(rows, cols, &h_)); }
+    AdamState(AdamState&& o) noexcept : rows_(o.rows_), cols_(o.cols_), h_(o.h_) { o.h_ = nullptr; }
+    AdamState(const AdamState&) = delete;
+    AdamState& operator=(const AdamState&) = delete;
+    ~AdamState() {
+        if (h_) asg_adam_state_destroy(h_);
+    }
+    static AdamState zeros(int64_t rows, int64_t cols) { return AdamState(rows, cols); }
+    int64_t rows() const { return rows_; }
+    int64_t cols() const { return cols_; }
+    asg_adam_state* handle() { return h_; }
+
+private:
+    int64_t rows_, cols_;
+    asg_adam_state* h_ = nullptr;
+};
+
+/// adamw_step (precond.cpp:229-242): the bias-corrected Adam direction.
+inline Matd adamw_step(AdamState& st, const Matd& g, const OptimizerConfig& cfg) {
+    if (g.rows != st.rows() || g.cols != st.cols()) throw ShapeMismatchError("adamw_step: gradient shape mismatch");
+    Matd out(g.rows, g.cols);
+    const asg_optimizer_config c = cfg.to_c();
+    check(asg_adamw_step_f64(st.handle(), g.ptr(), &c, out.ptr()));
+    return out;
+}
+
+/// apply_update (precond.cpp:244-251): theta -= lr * lr_scale * (update + wd * theta).
+inline void apply_update(Matd& theta, const Matd& update, const OptimizerConfig& cfg, double lr_scale = 1.0) {
+    if (theta.rows != update.rows || theta.cols != update.cols) throw ShapeMismatchError("apply_update: shape mismatch");
+    const asg_optimizer_config c = cfg.to_c();
+    check(asg_apply_update_f64(theta.ptr(), update.ptr(), theta.rows, theta.cols, &c, lr_scale));
+}
+
+// ---- replicated state (precond.hpp:138-139) -----------------------------------------
+inline std::vector<double> replicated_state(const PrecondBlock& b, Method /*method: the block's*/) {
+    std::vector<double> flat(size_t(b.rows() * b.rows() + b.cols() * b.cols()));
+    check(asg_block_replicated_state(b.handle(), 0, flat.data(), int64_t(flat.size())));
+    return flat;
+}
+inline void load_replicated_state(PrecondBlock& b, Method /*method: the block's*/, const std::vector<double>& flat) {
+    check(asg_block_load_replicated_state(b.handle(), 0, flat.data(), int64_t(flat.size())));
+}
+
+// ---- packed symmetric storage (densela.hpp:124-142) ---------------------------------
+/// Lower triangle packed row-major: (0,0), (1,0), (1,1), (2,0), ...
+inline std::vector<double> pack_spd(const Matd& m) {
+    if (m.rows != m.cols) throw LayoutMismatchError("pack_spd: expected a square Full matrix");
+    std::vector<double> p;
+    p.reserve(size_t(m.rows * (m.rows + 1) / 2));
+    for (int64_t i = 0; i < m.rows; ++i)
+        for (int64_t j = 0; j <= i; ++j) p.push_back(m(i, j));
+    return p;
+}
+inline Matd unpack_spd(const std::vector<double>& p, int64_t n) {
+    if (int64_t(p.size()) != n * (n + 1) / 2) throw LayoutMismatchError("unpack_spd: expected PackedLower of size n(n+1)/2");
+    Matd m(n, n);
+    for (int64_t i = 0, k = 0; i < n; ++i)
+        for (int64_t j = 0; j <= i; ++j, ++k) m(i, j) = m(j, i) = p[size_t(k)];
+    return m;
 }
 
 }  // namespace b200

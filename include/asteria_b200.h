@@ -305,6 +305,48 @@ int asg_block_precondition_f64(asg_blockset* bs, int64_t idx, const double* g, i
 int asg_block_soap_step_f64(asg_blockset* bs, int64_t idx, const double* g, int64_t ld,
                             double* out);
 
+/* ---- the split refresh (precond.hpp:77-98) ------------------------------
+ * snapshot_factors (precond.cpp:112-117): device copies of a block's L and R;
+ * its checksum is the reference's snapshot_checksum (precond.cpp:114-115,
+ * FNV-1a bytes.hpp:14-22) over the fp32 factor bytes, for isolation audits.
+ * compute_refresh (precond.cpp:129-142) is pure over the snapshot (the block's
+ * own factors and installed state are untouched; synchronous). install_refresh
+ * (precond.cpp:144-164) consumes the result: roots swapped in (Shampoo /
+ * KL-Shampoo) or, for SOAP, rot = Q_new^T Q_old applied to the moments and
+ * the bases swapped; version += 1, last_refresh_step = step. The block must
+ * have no scheduled (maybe_dispatch) refresh in flight. */
+typedef struct asg_snapshot asg_snapshot;
+typedef struct asg_refresh_result asg_refresh_result;
+int asg_snapshot_factors(asg_blockset* bs, int64_t idx, asg_snapshot** out);
+int asg_snapshot_checksum(const asg_snapshot* snap, uint64_t* checksum);
+int asg_snapshot_destroy(asg_snapshot* snap);
+int asg_compute_refresh(asg_blockset* bs, const asg_snapshot* snap, asg_refresh_result** out);
+int asg_install_refresh(asg_blockset* bs, int64_t idx, asg_refresh_result* result, int64_t step);
+int asg_refresh_result_destroy(asg_refresh_result* result);
+/* replicated_state / load_replicated_state (precond.cpp:253-279): flat
+ * [L side m*m | R side n*n] of the inverse roots (Shampoo, KL-Shampoo) or the
+ * eigenbases (SOAP), host fp64. */
+int asg_block_replicated_state(asg_blockset* bs, int64_t idx, double* out, int64_t count);
+int asg_block_load_replicated_state(asg_blockset* bs, int64_t idx, const double* in, int64_t count);
+/* pack_spd / unpack_spd (densela.hpp:124-142): lower triangle packed row-major
+ * ((0,0), (1,0), (1,1), (2,0), ...), n(n+1)/2 entries per matrix; fp32 device
+ * buffers, batched. */
+int asg_pack_spd_f32(const float* A, int64_t batch, int64_t n, float* packed, void* stream);
+int asg_unpack_spd_f32(const float* packed, int64_t batch, int64_t n, float* A, void* stream);
+
+/* adamw_step (precond.cpp:229-242) and apply_update (precond.cpp:244-251) with
+ * host matrices (the step fuses both into its kernels; these are the
+ * per-call entry points). AdamState: fp32 moments in HBM. adamw_step returns
+ * the bias-corrected direction and throws NonFinite on a non-finite gradient
+ * before touching the state; apply_update: theta -= lr*lr_scale*(u + wd*theta)
+ * (fp64), NonFinite on a non-finite update before touching theta. */
+typedef struct asg_adam_state asg_adam_state;
+int asg_adam_state_create(int64_t rows, int64_t cols, asg_adam_state** out);
+int asg_adam_state_destroy(asg_adam_state* st);
+int asg_adamw_step_f64(asg_adam_state* st, const double* g, const asg_optimizer_config* cfg, double* out);
+int asg_apply_update_f64(double* theta, const double* update, int64_t rows, int64_t cols,
+                         const asg_optimizer_config* cfg, double lr_scale);
+
 /* ---- multi-GPU: ownership sharding + parameter all-gather ---------------- */
 /* Host-only ownership plan (no device needed): partitions every parameter with
  * opt->block_dim_limit (precond.cpp:69-82) and assigns each unit (block, or a

@@ -161,6 +161,7 @@ struct Unit {
     double dispatch_sim = 0.0, completion_sim = 0.0;
     bool launched = false;  // refresh enqueued on the side stream
     bool needs_launch = false;  // dispatched, refresh not yet enqueued
+    bool snap_preloaded = false;  // compute_refresh: the snapshot slot already holds the caller's snapshot
     bool warm_start = false;    // a previous eigenbasis exists (decided at dispatch)
     cudaEvent_t done = nullptr;
     bool has_fresh = false;
@@ -1485,13 +1486,22 @@ void launch_refreshes(asg_blockset* bs) {
     // side stream works from the snapshot (snapshot isolation, asyncsched.cpp:129-136)
     for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
         Group& g = bs->groups[gi];
-        for (int ui : per_group[gi]) {
-            const Unit& u = bs->units[size_t(ui)];
-            CK(cudaMemcpyAsync(at(g.snapL, slabMM(g), u.slot), at(g.L, slabMM(g), u.slot), slabMM(g) * 4,
+        // one copy per contiguous slot run (a dispatch step snapshots hundreds of blocks)
+        std::vector<int> sl;
+        for (int ui : per_group[gi])
+            if (!bs->units[size_t(ui)].snap_preloaded) sl.push_back(bs->units[size_t(ui)].slot);
+        std::sort(sl.begin(), sl.end());
+        for (size_t a = 0; a < sl.size();) {
+            size_t b = a + 1;
+            while (b < sl.size() && sl[b] == sl[b - 1] + 1) ++b;
+            const size_t cnt = b - a;
+            CK(cudaMemcpyAsync(at(g.snapL, slabMM(g), sl[a]), at(g.L, slabMM(g), sl[a]), cnt * slabMM(g) * 4,
                                cudaMemcpyDeviceToDevice, bs->main));
-            CK(cudaMemcpyAsync(at(g.snapR, slabNN(g), u.slot), at(g.R, slabNN(g), u.slot), slabNN(g) * 4,
+            CK(cudaMemcpyAsync(at(g.snapR, slabNN(g), sl[a]), at(g.R, slabNN(g), sl[a]), cnt * slabNN(g) * 4,
                                cudaMemcpyDeviceToDevice, bs->main));
+            a = b;
         }
+        for (int ui : per_group[gi]) bs->units[size_t(ui)].snap_preloaded = false;
     }
     CK(cudaEventRecord(bs->ev_snap, bs->main));
     CK(cudaStreamWaitEvent(bs->side, bs->ev_snap, 0));
@@ -3261,5 +3271,436 @@ int asg_allgather_params(asg_blockset* bs, void* comm, void* stream) {
         }
         for (const auto& b : bs->buckets) bucket_exchange(bs, b, static_cast<ncclComm_t>(comm), s);
         CK(cudaGetLastError());
+    });
+}
+
+// ---- split refresh API: snapshot_factors / compute_refresh / install_refresh
+// (precond.hpp:90-98, precond.cpp:112-164) ------------------------------------
+struct asg_snapshot {
+    int64_t idx = 0;
+    int M = 0, N = 0, m = 0, n = 0;
+    float *L = nullptr, *R = nullptr;  // device copies of the padded factor slabs
+};
+
+struct asg_refresh_result {
+    int64_t idx = 0;
+    int method = 0;
+    bool f64_soap = false;
+    std::vector<void*> bufs;  // device
+    // roots (Shampoo / KL-Shampoo): P (+K) per side, split pairs
+    float *PLh = nullptr, *PLl = nullptr, *PRh = nullptr, *PRl = nullptr;
+    float *KLh = nullptr, *KLl = nullptr, *KRh = nullptr, *KRl = nullptr;
+    // SOAP, F32 refresh: the new bases transposed (split); F64 refresh: the new bases (fp64)
+    float *QLTh = nullptr, *QLTl = nullptr, *QRTh = nullptr, *QRTl = nullptr;
+    double *QL64 = nullptr, *QR64 = nullptr, *valsL = nullptr, *valsR = nullptr;
+};
+
+namespace {
+template <class T>
+T* ralloc(asg_refresh_result* r, size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+    r->bufs.push_back(p);
+    return static_cast<T*>(p);
+}
+void free_result(asg_refresh_result* r) {
+    if (!r) return;
+    for (void* p : r->bufs) cudaFree(p);
+    delete r;
+}
+void d2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (dst && src && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+}
+uint64_t fnv1a64(const void* data, size_t n, uint64_t h = 0xcbf29ce484222325ull) {  // bytes.hpp:14-22
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+}  // namespace
+
+int asg_snapshot_factors(asg_blockset* bs, int64_t idx, asg_snapshot** out) {
+    return guard([&] {
+        if (!bs || !out) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        Group& g = owned_group(bs, u);
+        auto* sn = new asg_snapshot();
+        sn->idx = idx;
+        sn->M = g.M;
+        sn->N = g.N;
+        sn->m = g.m;
+        sn->n = g.n;
+        cudaError_t e1 = cudaMalloc(reinterpret_cast<void**>(&sn->L), slabMM(g) * 4);
+        cudaError_t e2 = cudaMalloc(reinterpret_cast<void**>(&sn->R), slabNN(g) * 4);
+        if (e1 != cudaSuccess || e2 != cudaSuccess) {
+            cudaFree(sn->L);
+            cudaFree(sn->R);
+            delete sn;
+            throw Fail{ASG_ERR_OUT_OF_MEMORY, "snapshot_factors: device allocation failed"};
+        }
+        d2d(sn->L, at(g.L, slabMM(g), u.slot), slabMM(g) * 4, bs->main);
+        d2d(sn->R, at(g.R, slabNN(g), u.slot), slabNN(g) * 4, bs->main);
+        CK(cudaStreamSynchronize(bs->main));
+        *out = sn;
+    });
+}
+
+int asg_snapshot_checksum(const asg_snapshot* sn, uint64_t* out) {
+    return guard([&] {
+        if (!sn || !out) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        auto side = [&](const float* d, int D, int k) {
+            std::vector<float> h(size_t(D) * D);
+            CK(cudaMemcpy(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost));
+            uint64_t x = 0xcbf29ce484222325ull;
+            for (int i = 0; i < k; ++i) x = fnv1a64(h.data() + size_t(i) * D, size_t(k) * 4, x);
+            return x;
+        };
+        const uint64_t hl = side(sn->L, sn->M, sn->m), hr = side(sn->R, sn->N, sn->n);
+        *out = hr ^ (hl * 0x9e3779b97f4a7c15ull);  // snapshot_checksum precond.cpp:114-115
+    });
+}
+
+int asg_snapshot_destroy(asg_snapshot* sn) {
+    if (!sn) return ASG_OK;
+    cudaFree(sn->L);
+    cudaFree(sn->R);
+    delete sn;
+    return ASG_OK;
+}
+
+int asg_compute_refresh(asg_blockset* bs, const asg_snapshot* sn, asg_refresh_result** out) {
+    asg_refresh_result* r = nullptr;
+    const int rc = guard([&] {
+        if (!bs || !sn || !out) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, sn->idx);
+        Unit& u = bs->units[size_t(sn->idx)];
+        Group& g = owned_group(bs, u);
+        if (g.M != sn->M || g.N != sn->N) throw Fail{ASG_ERR_SHAPE_MISMATCH, "compute_refresh: snapshot shape"};
+        if (u.pending || u.needs_launch || u.launched)
+            throw Fail{ASG_ERR_INVALID_ARGUMENT, "compute_refresh: block has a scheduled refresh in flight"};
+        CK(cudaStreamSynchronize(bs->main));
+        CK(cudaStreamSynchronize(bs->side));
+        const size_t mm = slabMM(g), nn = slabNN(g);
+        d2d(at(g.snapL, mm, u.slot), sn->L, mm * 4, bs->main);
+        d2d(at(g.snapR, nn, u.slot), sn->R, nn * 4, bs->main);
+        u.snap_preloaded = true;
+        u.needs_launch = true;
+        u.warm_start = u.version > 0;
+        launch_refreshes(bs);
+        CK(cudaEventSynchronize(u.done));
+        u.launched = false;
+        const int st = g.h_status[u.slot];
+        if (st != ASG_OK) throw Fail{st, "compute_refresh: refresh failed"};
+        r = new asg_refresh_result();
+        r->idx = sn->idx;
+        r->method = bs->opt.method;
+        cudaStream_t s = bs->side;
+        const bool sp = split_mode(bs);
+        if (!is_soap(bs)) {
+            r->PLh = ralloc<float>(r, mm);
+            r->PRh = ralloc<float>(r, nn);
+            d2d(r->PLh, at(g.sPLh, mm, u.slot), mm * 4, s);
+            d2d(r->PRh, at(g.sPRh, nn, u.slot), nn * 4, s);
+            if (sp) {
+                r->PLl = ralloc<float>(r, mm);
+                r->PRl = ralloc<float>(r, nn);
+                d2d(r->PLl, at(g.sPLl, mm, u.slot), mm * 4, s);
+                d2d(r->PRl, at(g.sPRl, nn, u.slot), nn * 4, s);
+            }
+            if (is_kl(bs)) {
+                r->KLh = ralloc<float>(r, mm);
+                r->KRh = ralloc<float>(r, nn);
+                d2d(r->KLh, at(g.sKLh, mm, u.slot), mm * 4, s);
+                d2d(r->KRh, at(g.sKRh, nn, u.slot), nn * 4, s);
+                if (sp) {
+                    r->KLl = ralloc<float>(r, mm);
+                    r->KRl = ralloc<float>(r, nn);
+                    d2d(r->KLl, at(g.sKLl, mm, u.slot), mm * 4, s);
+                    d2d(r->KRl, at(g.sKRl, nn, u.slot), nn * 4, s);
+                }
+            }
+        } else if (f32_refresh(bs)) {
+            // absolute new bases, transposed: Q_new^T = J^T Q_cur^T (A = J^T, B = Q_cur)
+            r->valsL = ralloc<double>(r, size_t(g.m));
+            r->valsR = ralloc<double>(r, size_t(g.n));
+            d2d(r->valsL, at(g.svalsL, size_t(g.m), u.slot), size_t(g.m) * 8, s);
+            d2d(r->valsR, at(g.svalsR, size_t(g.n), u.slot), size_t(g.n) * 8, s);
+            for (int side = 0; side < 2; ++side) {
+                const bool left = side == 0;
+                const int D = left ? g.M : g.N, d = left ? g.m : g.n;
+                const size_t DD = size_t(D) * D;
+                float* th = ralloc<float>(r, DD);
+                float* tl = sp ? ralloc<float>(r, DD) : nullptr;
+                (left ? r->QLTh : r->QRTh) = th;
+                (left ? r->QLTl : r->QRTl) = tl;
+                GemmParams p{};
+                p.alpha = 1.f;
+                p.Dhi = th;
+                p.Dlo = tl;
+                p.ldd = D;
+                p.d_bstride = int64_t(DD);
+                run_gemm(bs, op(at(left ? g.sJLTh : g.sJRTh, DD, u.slot), at(left ? g.sJLTl : g.sJRTl, DD, u.slot), D, D),
+                         op(at(left ? g.QLh : g.QRh, DD, u.slot), at(left ? g.QLl : g.QRl, DD, u.slot), D, D), 1,
+                         EPI_SPLIT, p, nullptr, 0, s, 2.0 * double(d) * d * d);
+            }
+        } else {
+            r->f64_soap = true;
+            const size_t dm = size_t(g.m) * g.m, dn = size_t(g.n) * g.n;
+            r->QL64 = ralloc<double>(r, dm);
+            r->QR64 = ralloc<double>(r, dn);
+            r->valsL = ralloc<double>(r, size_t(g.m));
+            r->valsR = ralloc<double>(r, size_t(g.n));
+            d2d(r->QL64, at(g.sQL64, dm, u.slot), dm * 8, s);
+            d2d(r->QR64, at(g.sQR64, dn, u.slot), dn * 8, s);
+            d2d(r->valsL, at(g.svalsL, size_t(g.m), u.slot), size_t(g.m) * 8, s);
+            d2d(r->valsR, at(g.svalsR, size_t(g.n), u.slot), size_t(g.n) * 8, s);
+        }
+        CK(cudaStreamSynchronize(s));
+        *out = r;
+        r = nullptr;
+    });
+    free_result(r);
+    return rc;
+}
+
+int asg_install_refresh(asg_blockset* bs, int64_t idx, asg_refresh_result* r, int64_t step) {
+    return guard([&] {
+        if (!bs || !r) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        CK(cudaSetDevice(bs->device));
+        check_owned_index(bs, idx);
+        Unit& u = bs->units[size_t(idx)];
+        Group& g = owned_group(bs, u);
+        if (r->idx != idx || r->method != bs->opt.method)
+            throw Fail{ASG_ERR_SHAPE_MISMATCH, "install_refresh: result of another block or method"};
+        if (u.pending || u.launched) throw Fail{ASG_ERR_INVALID_ARGUMENT, "install_refresh: a scheduled refresh is in flight"};
+        CK(cudaStreamSynchronize(bs->side));
+        cudaStream_t s = bs->main;
+        const size_t mm = slabMM(g), nn = slabNN(g);
+        u.version += 1;  // install_refresh precond.cpp:162-163 (SOAP installs read the bumped version)
+        u.last_refresh_step = step;
+        if (!is_soap(bs)) {
+            d2d(at(g.sPLh, mm, u.slot), r->PLh, mm * 4, s);
+            d2d(at(g.sPRh, nn, u.slot), r->PRh, nn * 4, s);
+            d2d(at(g.sPLl, mm, u.slot), r->PLl, mm * 4, s);
+            d2d(at(g.sPRl, nn, u.slot), r->PRl, nn * 4, s);
+            d2d(at(g.sKLh, mm, u.slot), r->KLh, mm * 4, s);
+            d2d(at(g.sKRh, nn, u.slot), r->KRh, nn * 4, s);
+            d2d(at(g.sKLl, mm, u.slot), r->KLl, mm * 4, s);
+            d2d(at(g.sKRl, nn, u.slot), r->KRl, nn * 4, s);
+            install_roots(bs, g, u.slot, 1);
+        } else if (!r->f64_soap) {
+            // rot = Q_new^T Q_old (precond.cpp:146-147) as the shadow rotation J^T:
+            // A = Q_new^T (result), B = Q_old^T (the block's transposed basis)
+            for (int side = 0; side < 2; ++side) {
+                const bool left = side == 0;
+                const int D = left ? g.M : g.N, d = left ? g.m : g.n;
+                const size_t DD = size_t(D) * D;
+                GemmParams p{};
+                p.alpha = 1.f;
+                p.Dhi = at(left ? g.sJLTh : g.sJRTh, DD, u.slot);
+                p.Dlo = at(left ? g.sJLTl : g.sJRTl, DD, u.slot);
+                p.ldd = D;
+                p.d_bstride = int64_t(DD);
+                run_gemm(bs, op(left ? r->QLTh : r->QRTh, left ? r->QLTl : r->QRTl, D, D),
+                         op(at(left ? g.QLTh : g.QRTh, DD, u.slot), at(left ? g.QLTl : g.QRTl, DD, u.slot), D, D), 1,
+                         EPI_SPLIT, p, nullptr, 0, s, 2.0 * double(d) * d * d);
+            }
+            d2d(at(g.svalsL, size_t(g.m), u.slot), r->valsL, size_t(g.m) * 8, s);
+            d2d(at(g.svalsR, size_t(g.n), u.slot), r->valsR, size_t(g.n) * 8, s);
+            install_soap_f32(bs, g, u.slot, 1);
+        } else {
+            const size_t dm = size_t(g.m) * g.m, dn = size_t(g.n) * g.n;
+            d2d(at(g.sQL64, dm, u.slot), r->QL64, dm * 8, s);
+            d2d(at(g.sQR64, dn, u.slot), r->QR64, dn * 8, s);
+            d2d(at(g.svalsL, size_t(g.m), u.slot), r->valsL, size_t(g.m) * 8, s);
+            d2d(at(g.svalsR, size_t(g.n), u.slot), r->valsR, size_t(g.n) * 8, s);
+            install_apply(bs, u);
+        }
+        CK(cudaStreamSynchronize(s));
+        free_result(r);  // consumed (RefreshResult&&)
+    });
+}
+
+int asg_refresh_result_destroy(asg_refresh_result* r) {
+    free_result(r);
+    return ASG_OK;
+}
+
+// ---- replicated_state / load_replicated_state (precond.cpp:253-279) --------
+int asg_block_replicated_state(asg_blockset* bs, int64_t idx, double* out, int64_t count) {
+    return guard([&] {
+        if (!bs || !out) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        owned_group(bs, u);
+        const int64_t nr = u.spec.row_end - u.spec.row_begin, nc = u.spec.col_end - u.spec.col_begin;
+        if (count < nr * nr + nc * nc) throw Fail{ASG_ERR_SHAPE_MISMATCH, "replicated_state: output too small"};
+        const bool soap = is_soap(bs);
+        if (int rc = asg_block_read(bs, idx, soap ? ASG_ROLE_BASIS_L : ASG_ROLE_INV_L, out, nr * nr)) throw Fail{rc, g_err};
+        if (int rc = asg_block_read(bs, idx, soap ? ASG_ROLE_BASIS_R : ASG_ROLE_INV_R, out + nr * nr, nc * nc))
+            throw Fail{rc, g_err};
+    });
+}
+
+int asg_block_load_replicated_state(asg_blockset* bs, int64_t idx, const double* in, int64_t count) {
+    return guard([&] {
+        if (!bs || !in) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        check_owned_index(bs, idx);
+        const Unit& u = bs->units[size_t(idx)];
+        owned_group(bs, u);
+        const int64_t nr = u.spec.row_end - u.spec.row_begin, nc = u.spec.col_end - u.spec.col_begin;
+        if (count != nr * nr + nc * nc) throw Fail{ASG_ERR_SHAPE_MISMATCH, "load_replicated_state: size mismatch"};
+        const bool soap = is_soap(bs);
+        if (int rc = asg_block_write(bs, idx, soap ? ASG_ROLE_BASIS_L : ASG_ROLE_INV_L, in, nr * nr)) throw Fail{rc, g_err};
+        if (int rc = asg_block_write(bs, idx, soap ? ASG_ROLE_BASIS_R : ASG_ROLE_INV_R, in + nr * nr, nc * nc))
+            throw Fail{rc, g_err};
+    });
+}
+
+// ---- packed symmetric storage (pack_spd / unpack_spd densela.hpp:124-142) ----
+namespace asg {
+namespace {
+// packed lower triangle, row-major: (0,0), (1,0), (1,1), (2,0), ...
+__global__ void pack_spd_kernel(const float* __restrict__ A, int n, float* __restrict__ P) {
+    const int i = blockIdx.x;
+    const int64_t b = blockIdx.y;
+    const float* row = A + (b * n + i) * int64_t(n);
+    float* dst = P + b * (int64_t(n) * (n + 1) / 2) + int64_t(i) * (i + 1) / 2;
+    for (int j = threadIdx.x; j <= i; j += blockDim.x) dst[j] = row[j];
+}
+__global__ void unpack_spd_kernel(const float* __restrict__ P, int n, float* __restrict__ A) {
+    const int i = blockIdx.x;
+    const int64_t b = blockIdx.y;
+    const float* pk = P + b * (int64_t(n) * (n + 1) / 2);
+    float* row = A + (b * n + i) * int64_t(n);
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+        row[j] = j <= i ? pk[int64_t(i) * (i + 1) / 2 + j] : pk[int64_t(j) * (j + 1) / 2 + i];
+}
+}  // namespace
+}  // namespace asg
+
+int asg_pack_spd_f32(const float* A, int64_t batch, int64_t n, float* packed, void* stream) {
+    return guard([&] {
+        if (!A || !packed || n < 1 || batch < 1 || n > 65535) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad arguments"};
+        pack_spd_kernel<<<dim3(unsigned(n), unsigned(batch)), 256, 0, static_cast<cudaStream_t>(stream)>>>(A, int(n),
+                                                                                                        packed);
+        count_launch();
+        CK(cudaGetLastError());
+    });
+}
+
+int asg_unpack_spd_f32(const float* packed, int64_t batch, int64_t n, float* A, void* stream) {
+    return guard([&] {
+        if (!A || !packed || n < 1 || batch < 1 || n > 65535) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad arguments"};
+        unpack_spd_kernel<<<dim3(unsigned(n), unsigned(batch)), 256, 0, static_cast<cudaStream_t>(stream)>>>(packed,
+                                                                                                          int(n), A);
+        count_launch();
+        CK(cudaGetLastError());
+    });
+}
+
+// ---- adamw_step / apply_update with host matrices (precond.cpp:229-251) ----
+struct asg_adam_state {
+    int64_t rows = 0, cols = 0, t = 0;
+    float *m = nullptr, *v = nullptr;
+};
+
+namespace asg {
+namespace {
+__global__ void adamw_dir_kernel(const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                 float b1, float b2, float inv_bc1, float inv_bc2, float eps, float* __restrict__ out) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const float mm = b1 * m[e] + (1.f - b1) * g[e];
+        const float vv = b2 * v[e] + (1.f - b2) * g[e] * g[e];
+        m[e] = mm;
+        v[e] = vv;
+        out[e] = (mm * inv_bc1) / (sqrtf(vv * inv_bc2) + eps);
+    }
+}
+__global__ void apply_update_kernel(double* __restrict__ theta, const double* __restrict__ u, int64_t n, double lr,
+                                    double wd) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+        theta[e] -= lr * (u[e] + wd * theta[e]);
+}
+}  // namespace
+}  // namespace asg
+
+int asg_adam_state_create(int64_t rows, int64_t cols, asg_adam_state** out) {
+    return guard([&] {
+        if (!out || rows < 1 || cols < 1) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad arguments"};
+        auto* st = new asg_adam_state();
+        st->rows = rows;
+        st->cols = cols;
+        const size_t n = size_t(rows * cols);
+        if (cudaMalloc(reinterpret_cast<void**>(&st->m), n * 4) != cudaSuccess ||
+            cudaMalloc(reinterpret_cast<void**>(&st->v), n * 4) != cudaSuccess) {
+            cudaFree(st->m);
+            cudaFree(st->v);
+            delete st;
+            throw Fail{ASG_ERR_OUT_OF_MEMORY, "adam state allocation failed"};
+        }
+        CK(cudaMemset(st->m, 0, n * 4));
+        CK(cudaMemset(st->v, 0, n * 4));
+        *out = st;
+    });
+}
+
+int asg_adam_state_destroy(asg_adam_state* st) {
+    if (!st) return ASG_OK;
+    cudaFree(st->m);
+    cudaFree(st->v);
+    delete st;
+    return ASG_OK;
+}
+
+int asg_adamw_step_f64(asg_adam_state* st, const double* g, const asg_optimizer_config* cfg, double* out) {
+    return guard([&] {
+        if (!st || !g || !cfg || !out) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null argument"};
+        const size_t n = size_t(st->rows * st->cols);
+        std::vector<float> gf(n);
+        for (size_t i = 0; i < n; ++i) {
+            if (!std::isfinite(g[i])) throw Fail{ASG_ERR_NON_FINITE, "adamw_step: non-finite gradient"};
+            gf[i] = float(g[i]);
+        }
+        float *dg = nullptr, *dout = nullptr;
+        CK(cudaMalloc(reinterpret_cast<void**>(&dg), n * 4));
+        CK(cudaMalloc(reinterpret_cast<void**>(&dout), n * 4));
+        CK(cudaMemcpy(dg, gf.data(), n * 4, cudaMemcpyHostToDevice));
+        st->t += 1;
+        const double t = double(st->t);
+        adamw_dir_kernel<<<256, 256>>>(dg, st->m, st->v, int64_t(n), float(cfg->beta1), float(cfg->beta2),
+                                       float(1.0 / (1.0 - std::pow(cfg->beta1, t))),
+                                       float(1.0 / (1.0 - std::pow(cfg->beta2, t))), float(cfg->eps), dout);
+        count_launch();
+        CK(cudaMemcpy(gf.data(), dout, n * 4, cudaMemcpyDeviceToHost));
+        cudaFree(dg);
+        cudaFree(dout);
+        for (size_t i = 0; i < n; ++i) out[i] = double(gf[i]);
+    });
+}
+
+int asg_apply_update_f64(double* theta, const double* update, int64_t rows, int64_t cols,
+                         const asg_optimizer_config* cfg, double lr_scale) {
+    return guard([&] {
+        if (!theta || !update || !cfg || rows < 0 || cols < 0) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad arguments"};
+        const size_t n = size_t(rows * cols);
+        for (size_t i = 0; i < n; ++i)
+            if (!std::isfinite(update[i])) throw Fail{ASG_ERR_NON_FINITE, "apply_update: non-finite update"};
+        if (n == 0) return;
+        double *dt = nullptr, *du = nullptr;
+        CK(cudaMalloc(reinterpret_cast<void**>(&dt), n * 8));
+        CK(cudaMalloc(reinterpret_cast<void**>(&du), n * 8));
+        CK(cudaMemcpy(dt, theta, n * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(du, update, n * 8, cudaMemcpyHostToDevice));
+        apply_update_kernel<<<256, 256>>>(dt, du, int64_t(n), cfg->lr * lr_scale, cfg->weight_decay);
+        count_launch();
+        CK(cudaMemcpy(theta, dt, n * 8, cudaMemcpyDeviceToHost));
+        cudaFree(dt);
+        cudaFree(du);
     });
 }

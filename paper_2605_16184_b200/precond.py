@@ -160,3 +160,105 @@ def precondition_soap(b, g, cfg=None):
     if b.version == 0:
         raise abi.StaleUninitializedError("precondition_soap: no basis installed")
     return soap_scaled_step(b, g, cfg)
+
+
+# ---- the split refresh (precond.hpp:77-98) --------------------------------------
+class FactorSnapshot:
+    """snapshot_factors (precond.cpp:112-117): device copies of L and R."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @property
+    def checksum(self):
+        """snapshot_checksum (precond.cpp:114-115) over the fp32 factor bytes."""
+        v = C.c_uint64()
+        check(lib.asg_snapshot_checksum(self._h, C.byref(v)))
+        return v.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.asg_snapshot_destroy(self._h)
+            self._h = None
+
+
+class RefreshResult:
+    """compute_refresh's result (precond.hpp:83-87), held in HBM until installed."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.asg_refresh_result_destroy(self._h)
+            self._h = None
+
+
+def snapshot_factors(b):
+    h = C.c_void_p()
+    check(lib.asg_snapshot_factors(b._h, 0, C.byref(h)))
+    return FactorSnapshot(h)
+
+
+def compute_refresh(b, snap, cfg=None):
+    """Pure over the snapshot (precond.cpp:129-142); computed with the
+    block's refresh arithmetic."""
+    _check_cfg(b, cfg)
+    h = C.c_void_p()
+    check(lib.asg_compute_refresh(b._h, snap._h, C.byref(h)))
+    return RefreshResult(h)
+
+
+def install_refresh(b, result, step):
+    """install_refresh (precond.cpp:144-164); consumes the result."""
+    h, result._h = result._h, None
+    check(lib.asg_install_refresh(b._h, 0, h, step))
+
+
+def replicated_state(b):
+    """replicated_state (precond.cpp:253-265): [L side | R side] of the inverse
+    roots (Shampoo / KL-Shampoo) or the eigenbases (SOAP)."""
+    out = np.empty(b.rows * b.rows + b.cols * b.cols)
+    check(lib.asg_block_replicated_state(b._h, 0, _p(out), out.size))
+    return out
+
+
+def load_replicated_state(b, flat):
+    """load_replicated_state (precond.cpp:267-279)."""
+    flat = _f64(flat).ravel()
+    check(lib.asg_block_load_replicated_state(b._h, 0, _p(flat), flat.size))
+
+
+class AdamState:
+    """AdamState (precond.hpp:122-126) with its moments in HBM."""
+
+    def __init__(self, rows, cols):
+        self.shape = (rows, cols)
+        h = C.c_void_p()
+        check(lib.asg_adam_state_create(rows, cols, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.asg_adam_state_destroy(self._h)
+            self._h = None
+
+
+def adamw_step(state, g, cfg):
+    """adamw_step (precond.cpp:229-242): the bias-corrected Adam direction."""
+    g = _f64(g)
+    if g.shape != state.shape:
+        raise abi.ShapeMismatchError("adamw_step: gradient shape mismatch")
+    out = np.empty_like(g)
+    check(lib.asg_adamw_step_f64(state._h, _p(g), C.byref(cfg), _p(out)))
+    return out
+
+
+def apply_update(theta, update, cfg, lr_scale=1.0):
+    """apply_update (precond.cpp:244-251); returns the updated copy of theta."""
+    t = _f64(theta).copy()
+    u = _f64(update)
+    if t.shape != u.shape:
+        raise abi.ShapeMismatchError("apply_update: shape mismatch")
+    check(lib.asg_apply_update_f64(_p(t), _p(u), t.shape[0], t.shape[1] if t.ndim > 1 else 1, C.byref(cfg), lr_scale))
+    return t

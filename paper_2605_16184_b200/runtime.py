@@ -83,6 +83,20 @@ _SIGS = {
     "asg_nccl_comm_destroy": (C.c_int, [_vp]),
     "asg_allgather_params": (C.c_int, [_vp, _vp, _vp]),
     "asg_set_allgather_comm": (C.c_int, [_vp, _vp, _i32]),
+    "asg_snapshot_factors": (C.c_int, [_vp, _i64, _P(_vp)]),
+    "asg_snapshot_checksum": (C.c_int, [_vp, _P(_u64)]),
+    "asg_snapshot_destroy": (C.c_int, [_vp]),
+    "asg_compute_refresh": (C.c_int, [_vp, _vp, _P(_vp)]),
+    "asg_install_refresh": (C.c_int, [_vp, _i64, _vp, _i64]),
+    "asg_refresh_result_destroy": (C.c_int, [_vp]),
+    "asg_block_replicated_state": (C.c_int, [_vp, _i64, _P(_f64), _i64]),
+    "asg_block_load_replicated_state": (C.c_int, [_vp, _i64, _P(_f64), _i64]),
+    "asg_pack_spd_f32": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
+    "asg_unpack_spd_f32": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
+    "asg_adam_state_create": (C.c_int, [_i64, _i64, _P(_vp)]),
+    "asg_adam_state_destroy": (C.c_int, [_vp]),
+    "asg_adamw_step_f64": (C.c_int, [_vp, _P(_f64), _P(abi.OptimizerConfig), _P(_f64)]),
+    "asg_apply_update_f64": (C.c_int, [_P(_f64), _P(_f64), _i64, _i64, _P(abi.OptimizerConfig), _f64]),
     "asg_get_hbm_stats": (C.c_int, [_vp, _P(abi.HbmStats), _i32]),
     "asg_inv_root_batched_f32": (C.c_int, [_vp, _vp, _i64, _i64, _i32, C.c_double, _i32, _vp]),
 }

@@ -192,6 +192,61 @@ int main() {
         cfg.precondition_frequency = 0;
         CHECK_THROWS_AS(cfg.validate(), ConfigInvalidError);
     }
+    // precond.hpp:90-98 split refresh: install(compute(snapshot)) == refresh_inverse,
+    // compute is pure, the snapshot is isolated from later accumulation
+    {
+        auto cfg = OptimizerConfig::defaults_for(Method::Shampoo);
+        PrecondBlock a(24, 16, cfg), b(24, 16, cfg);
+        for (uint64_t s = 0; s < 3; ++s) {
+            const Matd g = random_matrix(24, 16, 40 + s);
+            accumulate_factors(a, g, cfg);
+            accumulate_factors(b, g, cfg);
+        }
+        refresh_inverse_inplace(a, cfg, 3);
+        FactorSnapshot snap = snapshot_factors(b);
+        const uint64_t c0 = snap.checksum();
+        accumulate_factors(b, random_matrix(24, 16, 50), cfg);  // after the snapshot
+        CHECK(snap.checksum() == c0);
+        RefreshResult r = compute_refresh(snap, cfg);
+        CHECK(b.version() == 0);
+        install_refresh(b, std::move(r), 3);
+        CHECK(b.version() == 1 && b.last_refresh_step() == 3);
+        CHECK(maxabs_diff(a.inv_l(), b.inv_l()) < 1e-6);
+        CHECK(maxabs_diff(a.inv_r(), b.inv_r()) < 1e-6);
+        // replicated_state round trip (precond.cpp:253-279)
+        std::vector<double> flat = replicated_state(b, Method::Shampoo);
+        CHECK(flat.size() == size_t(24 * 24 + 16 * 16));
+        PrecondBlock c(24, 16, cfg);
+        load_replicated_state(c, Method::Shampoo, flat);
+        CHECK(maxabs_diff(c.inv_l(), b.inv_l()) == 0.0);
+        flat.pop_back();
+        CHECK_THROWS_AS(load_replicated_state(c, Method::Shampoo, flat), ShapeMismatchError);
+    }
+    // precond_test.cpp:283-342: AdamW direction and apply_update KATs
+    {
+        auto cfg = OptimizerConfig::defaults_for(Method::AdamW);
+        AdamState st = AdamState::zeros(2, 2);
+        Matd g(2, 2, 0.5);
+        Matd d = adamw_step(st, g, cfg);  // first step: m^/sqrt(v^) = sign(g)
+        for (double x : d.data) CHECK(std::fabs(x - 1.0) < 2e-5);  // fp32 moments; 1/(1-beta2) = 1000 scales their rounding
+        Matd theta(2, 2, 1.0);
+        cfg.weight_decay = 0.5;
+        apply_update(theta, Matd(2, 2, 1.0), cfg, 2.0);  // 1 - lr*2*(1 + 0.5)
+        for (double x : theta.data) CHECK(std::fabs(x - (1.0 - cfg.lr * 2.0 * 1.5)) < 1e-15);
+        Matd bad(2, 2, 0.0);
+        bad(1, 0) = std::nan("");
+        CHECK_THROWS_AS(apply_update(theta, bad, cfg), NonFiniteError);
+    }
+    // densela_test.cpp:117-153: pack / unpack round trip
+    {
+        Matd m = random_matrix(5, 5, 60);
+        for (int64_t i = 0; i < 5; ++i)
+            for (int64_t j = 0; j < i; ++j) m(j, i) = m(i, j);
+        std::vector<double> p = pack_spd(m);
+        CHECK(p.size() == 15 && p[1] == m(1, 0) && p[2] == m(1, 1));
+        CHECK(maxabs_diff(unpack_spd(p, 5), m) == 0.0);
+        CHECK_THROWS_AS(unpack_spd(p, 4), LayoutMismatchError);
+    }
     std::printf("shim_precond_test: %d checks, %d failed\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
