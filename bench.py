@@ -109,6 +109,17 @@ def alg_flops(wl):
     return step, refresh, step + refresh / wl["pf"]
 
 
+def executed_step_flops(wl):
+    """Flops the step's GEMMs execute (the 8(d) products as this library
+    forms them). Equal to the convention except KL-Shampoo, whose statistics
+    reuse the root P = F^-1/2 (F^-1 = P^2): W = G P_R (2mn^2), L from W W^T
+    (m^2 n), V^T = G^T P_L (2m^2 n), R from V^T V (mn^2), update V P_R (2mn^2)
+    = 5mn^2 + 3m^2 n instead of 5mn(m+n)."""
+    if wl["method"] != "KL-Shampoo":
+        return alg_flops(wl)[0]
+    return sum(5 * m * n * n + 3 * m * m * n for s in wl["shapes"] for (m, n) in blocks_of(s, wl["limit"]))
+
+
 # ---------------------------------------------------------------------------
 # clocks (sampled during the timed region)
 # ---------------------------------------------------------------------------
@@ -453,7 +464,12 @@ def main():
                "gradients": ("fixed (diagnostics)" if args.fixed_grads else
                              "fresh every step: Philox N(0, 1/cols) keyed (1234, step, block), on the owner"),
                "l2": "inputs > L2 (every step streams all state and gradients from HBM)",
-               "alg_tflop_per_step": flops / 1e12}
+               "alg_tflop_per_step": flops / 1e12,
+               "executed_step_tflop": executed_step_flops(wl) / 1e12,
+               "flops_note": ("value counts the SURVEY 8(d) convention flops (stats + update + refresh/pf); "
+                              "executed_step_tflop is what the step's GEMMs execute (KL-Shampoo forms "
+                              "G F^-1 G^T as (G P)(G P)^T with P = F^-1/2, 20% fewer); roofline.achieved "
+                              "uses executed flops")}
 
     if args.impl == "reference":
         if rank != 0:
@@ -696,6 +712,7 @@ def main():
                      "barrier_wait_ms": (st1.wait_total_us - st0.wait_total_us) / 1e3},
         "e2e": e2e,
         "state_bytes": o.state_bytes(),
+        "workspace_bytes": o.workspace_bytes(),
     }
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         cb = cpu_baseline(wl, steps=10, warmup=1)

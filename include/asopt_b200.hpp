@@ -268,13 +268,11 @@ private:
                                               ASG_ROLE_BASIS_R, ASG_ROLE_ROTATED_M, ASG_ROLE_ROTATED_V,
                                               ASG_ROLE_EIGVALS_L, ASG_ROLE_EIGVALS_R};
         static const asg_role root_roles[] = {ASG_ROLE_FACTOR_L, ASG_ROLE_FACTOR_R, ASG_ROLE_INV_L, ASG_ROLE_INV_R};
-        static const asg_role kl_roles[] = {ASG_ROLE_KL_INV_L, ASG_ROLE_KL_INV_R};
+        // (KL-Shampoo's inverses F^-1 = INV^2 are derived from the roots, not stored)
         if (cfg_.method == Method::Soap) {
             for (asg_role r : soap_roles) set(r, o.get(r));
         } else if (cfg_.method != Method::AdamW) {
             for (asg_role r : root_roles) set(r, o.get(r));
-            if (cfg_.method == Method::KlShampoo)
-                for (asg_role r : kl_roles) set(r, o.get(r));
         }
         const asg_block_info i = o.info();
         set_counters(i.version, i.last_refresh_step, i.moment_steps);

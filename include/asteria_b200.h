@@ -80,7 +80,7 @@ typedef enum asg_role {
     ASG_ROLE_BASIS_R = 5,
     ASG_ROLE_ROTATED_M = 6,
     ASG_ROLE_ROTATED_V = 7,
-    ASG_ROLE_KL_INV_L = 8,  /* KL-Shampoo: L^-1 */
+    ASG_ROLE_KL_INV_L = 8,  /* KL-Shampoo: L^-1 = INV_L^2 (read-only: derived from the installed root) */
     ASG_ROLE_KL_INV_R = 9,
     ASG_ROLE_EIGVALS_L = 10, /* SOAP installed eigenvalues (ascending) */
     ASG_ROLE_EIGVALS_R = 11
@@ -249,8 +249,12 @@ int asg_blockset_destroy(asg_blockset* bs);
 int asg_blockset_bind_params(asg_blockset* bs, const asg_param_desc* params, int64_t n_params);
 int asg_blockset_num_blocks(const asg_blockset* bs, int64_t* n);
 int asg_blockset_block_info(const asg_blockset* bs, int64_t idx, asg_block_info* out);
-/* Bytes of optimizer state resident in HBM. */
+/* Bytes of optimizer state resident in HBM (every device allocation of the
+ * blockset except the refresh workspace). */
 int asg_blockset_state_bytes(const asg_blockset* bs, uint64_t* bytes);
+/* Bytes of the refresh / install workspace (chunked; independent of the
+ * block count above one chunk). */
+int asg_blockset_workspace_bytes(const asg_blockset* bs, uint64_t* bytes);
 /* The blockset's main stream (cudaStream_t) for callers that want to order
  * their own work with it. */
 int asg_blockset_stream(const asg_blockset* bs, void** stream);

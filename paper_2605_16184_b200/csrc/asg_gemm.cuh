@@ -36,6 +36,9 @@
 //                coupled Newton-Schulz inverse root, asg_newton.cu)
 //   EPI_NS       EPI_SYM_SPLIT for M, plus T = ns_a*I - ns_b*M as a second
 //                (hi, lo) pair and max|M - I| per batch into resid[b]
+//   EPI_SPLIT2   EPI_SPLIT, plus the transpose as a second (hi, lo) pair in
+//                Thi/Tlo (leading dimension ldt): both operand layouts of one
+//                product (KL-Shampoo's V^T = G^T P_L, asg_runtime.cu group_stats)
 #pragma once
 
 #include <cuda.h>
@@ -53,7 +56,8 @@ enum EpiKind {
     EPI_ADAM = 4,
     EPI_APPLY = 5,
     EPI_SYM_SPLIT = 6,
-    EPI_NS = 7
+    EPI_NS = 7,
+    EPI_SPLIT2 = 8
 };
 
 struct ApplyEntry {
@@ -83,23 +87,32 @@ struct GemmParams {
     float lr_eff, wd;
     int* flag;            // set to 1 on a non-finite update (EPI_APPLY)
     const int* batch_active;  // optional: batches with batch_active[b] == 0 are skipped (no output)
-    float* Thi;           // EPI_NS: T = ns_a I - ns_b M (hi, lo), same layout as D
+    float* Thi;           // EPI_NS: T = ns_a I - ns_b M (hi, lo), same layout as D; EPI_SPLIT2: D^T
     float* Tlo;
+    int64_t ldt;          // EPI_SPLIT2: leading dimension of D^T (batch stride d_bstride)
     float ns_a, ns_b;
     unsigned int* resid;  // EPI_NS: per batch max|M - I| (float bits, atomicMax)
+    int sym_T;            // CTA-pair symmetric schedules: T x T tile grid, lower triangle decoded
+                          // arithmetically (tile_list unused)
 };
 
 __device__ __forceinline__ bool batch_skipped(const GemmParams& p, int t) {
     return p.batch_active && p.batch_active[t / p.tiles_per_batch] == 0;
 }
 
-template <int BN, int NPASS>
+// CG = 1: one CTA per 128 x BN tile. CG = 2: a CTA pair (cluster (2,1,1),
+// tcgen05 cta_group::2) per 256 x BN tile; each CTA stages 128 rows of A and
+// BN/2 rows of B, so the per-SM operand bytes (shared-memory reads of the
+// MMA, TMA writes) drop by a third at BN = 256 and the ring gets deeper.
+template <int BN, int NPASS, int CG = 1>
 struct GemmCfg {
-    static constexpr int BM = 128;
+    static constexpr int BM = 128;       // accumulator rows per CTA
+    static constexpr int TM = 128 * CG;  // output tile rows
     static constexpr int BK = 32;  // 32 fp32 = one 128-byte swizzle row
     static constexpr bool kSplit = NPASS > 1;
+    static constexpr int kBRows = BN / CG;  // B rows staged by each CTA
     static constexpr uint32_t kABytes = BM * BK * 4;
-    static constexpr uint32_t kBBytes = BN * BK * 4;
+    static constexpr uint32_t kBBytes = kBRows * BK * 4;
     static constexpr uint32_t kStageBytes = (kABytes + kBBytes) * (kSplit ? 2 : 1);
     // per-epilogue-warp 32 x 33 fp32 transpose scratch (coalesced apply)
     static constexpr int kEpiWarps = 8;
@@ -116,7 +129,13 @@ struct GemmCfg {
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& b, int& tm, int& tn) {
     b = t / p.tiles_per_batch;
     const int l = t - b * p.tiles_per_batch;
-    if (p.tile_list) {
+    if (p.sym_T) {  // lower triangle of a T x T grid, row by row: l = tm (tm + 1) / 2 + tn
+        int r = int((sqrtf(8.f * float(l) + 1.f) - 1.f) * 0.5f);
+        while (r * (r + 1) / 2 > l) --r;
+        while ((r + 1) * (r + 2) / 2 <= l) ++r;
+        tm = r;
+        tn = l - r * (r + 1) / 2;
+    } else if (p.tile_list) {
         const int2 c = p.tile_list[l];
         tm = c.x;
         tn = c.y;
@@ -286,7 +305,7 @@ __device__ __forceinline__ void rows_chunk(const GemmParams& p, int b, int row0,
     for (int j = 0; j < 32; ++j) scratch[lane][j] = p.alpha * __uint_as_float(r[j]);
     __syncwarp();
     const int c = col0 + int(lane);
-    if constexpr (EPI == EPI_SPLIT) {
+    if constexpr (EPI == EPI_SPLIT || EPI == EPI_SPLIT2) {
         float* dh = p.Dhi + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c;
         float* dl = p.Dlo ? p.Dlo + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c : nullptr;
 #pragma unroll 8
@@ -295,6 +314,18 @@ __device__ __forceinline__ void rows_chunk(const GemmParams& p, int b, int row0,
             split_tf32(scratch[i][lane], h, l);
             dh[int64_t(i) * p.ldd] = h;
             if (dl) dl[int64_t(i) * p.ldd] = l;
+        }
+        if constexpr (EPI == EPI_SPLIT2) {
+            // D^T[col][row]: lanes = consecutive rows of one column (coalesced)
+            float* th = p.Thi + int64_t(b) * p.d_bstride + int64_t(col0) * p.ldt + row0 + int(lane);
+            float* tl = p.Tlo ? p.Tlo + int64_t(b) * p.d_bstride + int64_t(col0) * p.ldt + row0 + int(lane) : nullptr;
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                float h, l;
+                split_tf32(scratch[lane][j], h, l);
+                th[int64_t(j) * p.ldt] = h;
+                if (tl) tl[int64_t(j) * p.ldt] = l;
+            }
         }
     } else {
         float* cc = p.C + int64_t(b) * p.c_bstride + int64_t(row0) * p.ldc + c;
@@ -420,14 +451,15 @@ __device__ __forceinline__ void sym_split_chunk(const GemmParams& p, int b, int 
     __syncwarp();
 }
 
-template <int BN, int NPASS, int EPI>
+template <int BN, int NPASS, int EPI, int CG = 1>
 __global__ void __launch_bounds__(320, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                    const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
                    const __grid_constant__ GemmParams p) {
-    using Cfg = GemmCfg<BN, NPASS>;
+    using Cfg = GemmCfg<BN, NPASS, CG>;
     constexpr int BM = Cfg::BM, BK = Cfg::BK, STAGES = Cfg::kStages;
     constexpr bool SPLIT = Cfg::kSplit;
+    constexpr bool PAIR = CG == 2;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -441,6 +473,11 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane = threadIdx.x & 31;
     float (*scratch)[33] = reinterpret_cast<float (*)[33]>(smem + size_t(STAGES) * Cfg::kStageBytes + 256 +
                                                            size_t(warp >= 2 ? warp - 2 : 0) * 32 * 33 * 4);
+    // CTA pair: rank within the pair, the pair's index and count (tiles are
+    // walked per pair; both CTAs decode the same tile sequence)
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+    const int nunits = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
 
     auto a_hi = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes; };
     auto a_lo = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes + Cfg::kABytes; };
@@ -465,15 +502,22 @@ __global__ void __launch_bounds__(320, 1)
             }
             for (int a = 0; a < 2; ++a) {
                 mbar_init(&tfull[a], 1);
-                mbar_init(&tempty[a], Cfg::kEpiWarps);  // one arrive per epilogue warp
+                // one arrive per epilogue warp (of both CTAs of a pair: the leader's barrier)
+                mbar_init(&tempty[a], Cfg::kEpiWarps * CG);
             }
             fence_mbar_init();
         }
         __syncwarp();
-        tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+        if constexpr (PAIR)
+            tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+        else
+            tmem_alloc<Cfg::kTmemCols>(tmem_slot);
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR)
+        cluster_sync();  // the peer's TMA and epilogue signal the leader's barriers: all initialised first
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int num_k = p.K / BK;
@@ -482,18 +526,33 @@ __global__ void __launch_bounds__(320, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            const uint32_t full0 = PAIR ? mapa_shared(&full[0], 0) : 0u;
+            for (int t = unit; t < p.num_tiles; t += nunits) {
                 if (batch_skipped(p, t)) continue;
                 int b, tm, tn;
                 decode_tile(p, t, b, tm, tn);
+                const int arow = tm * Cfg::TM + int(rank) * BM;
+                const int brow = tn * BN + int(rank) * Cfg::kBRows;
                 for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-                    tma_load_3d(a_hi(stage), &tmAh, &full[stage], kb * BK, tm * BM, b);
-                    tma_load_3d(b_hi(stage), &tmBh, &full[stage], kb * BK, tn * BN, b);
-                    if (SPLIT) {
-                        tma_load_3d(a_lo(stage), &tmAl, &full[stage], kb * BK, tm * BM, b);
-                        tma_load_3d(b_lo(stage), &tmBl, &full[stage], kb * BK, tn * BN, b);
+                    if constexpr (PAIR) {
+                        // the leader's barrier expects both CTAs' bytes
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes * 2);
+                        const uint32_t fb = full0 + uint32_t(stage) * 8u;
+                        tma_load_3d_pair(a_hi(stage), &tmAh, fb, kb * BK, arow, b);
+                        tma_load_3d_pair(b_hi(stage), &tmBh, fb, kb * BK, brow, b);
+                        if (SPLIT) {
+                            tma_load_3d_pair(a_lo(stage), &tmAl, fb, kb * BK, arow, b);
+                            tma_load_3d_pair(b_lo(stage), &tmBl, fb, kb * BK, brow, b);
+                        }
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+                        tma_load_3d(a_hi(stage), &tmAh, &full[stage], kb * BK, arow, b);
+                        tma_load_3d(b_hi(stage), &tmBh, &full[stage], kb * BK, brow, b);
+                        if (SPLIT) {
+                            tma_load_3d(a_lo(stage), &tmAl, &full[stage], kb * BK, arow, b);
+                            tma_load_3d(b_lo(stage), &tmBl, &full[stage], kb * BK, brow, b);
+                        }
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -503,13 +562,13 @@ __global__ void __launch_bounds__(320, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_tf32(BM, BN);
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = idesc_tf32(Cfg::TM, BN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (int t = unit; t < p.num_tiles; t += nunits) {
                 if (batch_skipped(p, t)) continue;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -524,19 +583,33 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 8; ++k) {
                         const uint64_t adv = uint64_t(k * 32) >> 4;  // 8 tf32 = 32 bytes along K
-                        mma_tf32(d, ah + adv, bh + adv, idesc, (kb | k) != 0 ? 1u : 0u);
-                        if (SPLIT) {
-                            mma_tf32(d, ah + adv, bl + adv, idesc, 1u);
-                            mma_tf32(d, al + adv, bh + adv, idesc, 1u);
+                        if constexpr (PAIR) {
+                            mma_tf32_pair(d, ah + adv, bh + adv, idesc, (kb | k) != 0 ? 1u : 0u);
+                            if (SPLIT) {
+                                mma_tf32_pair(d, ah + adv, bl + adv, idesc, 1u);
+                                mma_tf32_pair(d, al + adv, bh + adv, idesc, 1u);
+                            }
+                        } else {
+                            mma_tf32(d, ah + adv, bh + adv, idesc, (kb | k) != 0 ? 1u : 0u);
+                            if (SPLIT) {
+                                mma_tf32(d, ah + adv, bl + adv, idesc, 1u);
+                                mma_tf32(d, al + adv, bh + adv, idesc, 1u);
+                            }
                         }
                     }
-                    mma_commit(&empty[stage]);
+                    if constexpr (PAIR)
+                        mma_commit_pair(&empty[stage], 0x3);  // both CTAs' stage is free
+                    else
+                        mma_commit(&empty[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                mma_commit(&tfull[acc]);
+                if constexpr (PAIR)
+                    mma_commit_pair(&tfull[acc], 0x3);  // both CTAs' accumulator halves are ready
+                else
+                    mma_commit(&tfull[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -548,42 +621,59 @@ __global__ void __launch_bounds__(320, 1)
         const int half = (warp - 2) >> 2;  // which of the quadrant's two warps: even / odd column chunks
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const uint32_t tempty0 = PAIR ? mapa_shared(&tempty[0], 0) : 0u;
+        for (int t = unit; t < p.num_tiles; t += nunits) {
             if (batch_skipped(p, t)) continue;
             int b, tm, tn;
             decode_tile(p, t, b, tm, tn);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int row = tm * BM + q * 32 + int(lane);
+            const int row0 = tm * Cfg::TM + int(rank) * BM + q * 32;
+            const int row = row0 + int(lane);
 #pragma unroll 1
             for (int c = half; c < BN / 32; c += 2) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32), r);
                 tmem_ld_wait();
                 if constexpr (EPI == EPI_APPLY)
-                    apply_chunk(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
+                    apply_chunk(p, b, row0, tn * BN + c * 32, r, scratch);
                 else if constexpr (EPI == EPI_ADAM)
-                    adam_chunk(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
-                else if constexpr (EPI == EPI_STORE || EPI == EPI_SPLIT || EPI == EPI_SYM_EMA)
-                    rows_chunk<EPI>(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
+                    adam_chunk(p, b, row0, tn * BN + c * 32, r, scratch);
+                else if constexpr (EPI == EPI_STORE || EPI == EPI_SPLIT || EPI == EPI_SPLIT2 || EPI == EPI_SYM_EMA)
+                    rows_chunk<EPI>(p, b, row0, tn * BN + c * 32, r, scratch);
                 else if constexpr (EPI == EPI_SYM_SPLIT || EPI == EPI_NS)
-                    sym_split_chunk<EPI == EPI_NS>(p, b, tm * BM + q * 32, tn * BN + c * 32, r, scratch);
+                    sym_split_chunk<EPI == EPI_NS>(p, b, row0, tn * BN + c * 32, r, scratch);
                 else
                     epilogue_chunk<EPI>(p, b, row, tn * BN + c * 32, r);
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (PAIR)
+                    mbar_arrive_remote(tempty0 + uint32_t(acc) * 8u);
+                else
+                    mbar_arrive(&tempty[acc]);
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
         }
     }
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    if constexpr (PAIR) {
+        // no CTA leaves while its peer may still signal its barriers or read its TMEM
+        tc_fence_before();
+        cluster_sync();
+        if (warp == 1) {
+            tc_fence_after();
+            tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+        }
+    } else {
+        __syncthreads();
+        if (warp == 1) {
+            tc_fence_after();
+            tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+        }
     }
 }
 

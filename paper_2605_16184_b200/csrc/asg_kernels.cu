@@ -67,42 +67,82 @@ bool make_map(CUtensorMap* map, const float* base, int K, int rows, int batch, i
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int NPASS, int EPI>
+template <int BN, int NPASS, int EPI, int CG>
 cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                         const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
-    using Cfg = GemmCfg<BN, NPASS>;
-    // the shared-memory limit is a per-device function attribute
+    using Cfg = GemmCfg<BN, NPASS, CG>;
+    auto kern = gemm_tn_kernel<BN, NPASS, EPI, CG>;
+    // the shared-memory limit is a per-device function attribute; so is the
+    // number of CTA pairs that can be co-resident (GPCs with an odd SM count)
     static std::atomic<uint64_t> attr_set{0};
+    static int max_pairs[64] = {};
     int dev = 0;
     cudaError_t de = cudaGetDevice(&dev);
     if (de != cudaSuccess) return de;
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_set.load() & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, NPASS, EPI>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(Cfg::kSmemBytes));
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmemBytes));
         if (e != cudaSuccess) return e;
+        if (CG == 2) {
+            cudaLaunchConfig_t qc = {};
+            qc.gridDim = dim3(2 * 74, 1, 1);
+            qc.blockDim = dim3(Cfg::kThreads, 1, 1);
+            qc.dynamicSmemBytes = Cfg::kSmemBytes;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = 2;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            qc.attrs = qa;
+            qc.numAttrs = 1;
+            int n = 0;
+            e = cudaOccupancyMaxActiveClusters(&n, kern, &qc);
+            if (e != cudaSuccess) return e;
+            max_pairs[dev & 63] = n;
+        }
         attr_set.fetch_or(bit);
     }
-    const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
-    if (grid <= 0) return cudaSuccess;
-    gemm_tn_kernel<BN, NPASS, EPI><<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(ah, al, bh, bl, p);
+    if (p.num_tiles <= 0) return cudaSuccess;
+    if (CG == 1) {
+        const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+        kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(ah, al, bh, bl, p);
+    } else {
+        int pairs = max_pairs[dev & 63];
+        if (pairs > num_sms / 2) pairs = num_sms / 2;
+        if (pairs > p.num_tiles) pairs = p.num_tiles;
+        if (pairs <= 0) return cudaErrorInvalidConfiguration;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * pairs, 1, 1);
+        cfg.blockDim = dim3(Cfg::kThreads, 1, 1);
+        cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+        cfg.stream = s;
+        cudaLaunchAttribute a[1];
+        a[0].id = cudaLaunchAttributeClusterDimension;
+        a[0].val.clusterDim.x = 2;
+        a[0].val.clusterDim.y = 1;
+        a[0].val.clusterDim.z = 1;
+        cfg.attrs = a;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, p);
+        if (e != cudaSuccess) return e;
+    }
     count_launch();
     return cudaGetLastError();
 }
 
-template <int BN, int NPASS>
+template <int BN, int NPASS, int CG>
 cudaError_t dispatch_epi(int epi, const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                          const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
     switch (epi) {
-        case EPI_STORE: return launch_inst<BN, NPASS, EPI_STORE>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SYM_EMA: return launch_inst<BN, NPASS, EPI_SYM_EMA>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SPLIT: return launch_inst<BN, NPASS, EPI_SPLIT>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SPLIT_T: return launch_inst<BN, NPASS, EPI_SPLIT_T>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_ADAM: return launch_inst<BN, NPASS, EPI_ADAM>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_APPLY: return launch_inst<BN, NPASS, EPI_APPLY>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SYM_SPLIT: return launch_inst<BN, NPASS, EPI_SYM_SPLIT>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_NS: return launch_inst<BN, NPASS, EPI_NS>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_STORE: return launch_inst<BN, NPASS, EPI_STORE, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SYM_EMA: return launch_inst<BN, NPASS, EPI_SYM_EMA, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT: return launch_inst<BN, NPASS, EPI_SPLIT, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT_T: return launch_inst<BN, NPASS, EPI_SPLIT_T, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_ADAM: return launch_inst<BN, NPASS, EPI_ADAM, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_APPLY: return launch_inst<BN, NPASS, EPI_APPLY, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SYM_SPLIT: return launch_inst<BN, NPASS, EPI_SYM_SPLIT, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_NS: return launch_inst<BN, NPASS, EPI_NS, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT2: return launch_inst<BN, NPASS, EPI_SPLIT2, CG>(ah, al, bh, bl, p, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -126,6 +166,12 @@ int gemm_sym_tile_list(int n, int bn, int2* out) {
     return count;
 }
 
+// CTA-pair (cta_group::2, 256-row tiles) schedules: on unless ASG_GEMM_PAIR=0.
+static bool pair_enabled() {
+    static const bool on = !(getenv("ASG_GEMM_PAIR") && atoi(getenv("ASG_GEMM_PAIR")) == 0);
+    return on;
+}
+
 cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStream_t stream) {
     const int M = g.A.rows, N = g.B.rows, K = g.A.K;
     if (M % 128 || N % 128 || K % 32 || g.B.K != K) return cudaErrorInvalidValue;
@@ -134,14 +180,22 @@ cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStr
     // fill two waves of the persistent grid (symmetric schedules keep the tile
     // width their tile lists were built for).
     if (!g.sym_tiles && bn == 256 && int64_t(g.batch) * (M / 128) * (N / 256) < 2 * int64_t(num_sms)) bn = 128;
+    // CTA pairs: 256 x BN tiles, when M splits into 256-row tiles, the pair grid
+    // still gets two waves, and (symmetric outputs) the 256 x 256 lower-triangle
+    // grid covers the output (N % 256 == 0, M == N)
+    bool pair = pair_enabled() && M % 256 == 0;
+    if (pair && g.sym_tiles) pair = (bn == 256 && M == N);
+    if (pair && !g.sym_tiles && int64_t(g.batch) * (M / 256) * (N / bn) < int64_t(num_sms)) pair = false;
+    const int tm_rows = pair ? 256 : 128;
+    const int brows = pair ? bn / 2 : bn;
     const bool split = precision == ASG_PREC_3XTF32;
     CUtensorMap ah, al, bh, bl;
     if (!make_map(&ah, g.A.hi, K, M, g.batch, 128)) return cudaErrorInvalidValue;
-    if (!make_map(&bh, g.B.hi, K, N, g.batch, bn)) return cudaErrorInvalidValue;
+    if (!make_map(&bh, g.B.hi, K, N, g.batch, brows)) return cudaErrorInvalidValue;
     if (split) {
         if (!g.A.lo || !g.B.lo) return cudaErrorInvalidValue;
         if (!make_map(&al, g.A.lo, K, M, g.batch, 128)) return cudaErrorInvalidValue;
-        if (!make_map(&bl, g.B.lo, K, N, g.batch, bn)) return cudaErrorInvalidValue;
+        if (!make_map(&bl, g.B.lo, K, N, g.batch, brows)) return cudaErrorInvalidValue;
     } else {
         al = ah;
         bl = bh;
@@ -152,19 +206,32 @@ cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStr
     p.K = K;
     p.batch = g.batch;
     p.tiles_n = N / bn;
-    if (g.sym_tiles) {
+    p.sym_T = 0;
+    if (g.sym_tiles && pair) {
+        const int T = N / 256;
+        p.tile_list = nullptr;
+        p.sym_T = T;
+        p.tiles_per_batch = T * (T + 1) / 2;
+    } else if (g.sym_tiles) {
         p.tile_list = g.sym_tiles;
         p.tiles_per_batch = g.sym_tiles_count;
     } else {
         p.tile_list = nullptr;
-        p.tiles_per_batch = (M / 128) * (N / bn);
+        p.tiles_per_batch = (M / tm_rows) * (N / bn);
     }
     p.num_tiles = p.tiles_per_batch * g.batch;
+    if (pair) {
+        if (bn == 256)
+            return split ? dispatch_epi<256, 3, 2>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                         : dispatch_epi<256, 1, 2>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+        return split ? dispatch_epi<128, 3, 2>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                     : dispatch_epi<128, 1, 2>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+    }
     if (bn == 256)
-        return split ? dispatch_epi<256, 3>(g.epi, ah, al, bh, bl, p, num_sms, stream)
-                     : dispatch_epi<256, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream);
-    return split ? dispatch_epi<128, 3>(g.epi, ah, al, bh, bl, p, num_sms, stream)
-                 : dispatch_epi<128, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+        return split ? dispatch_epi<256, 3, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                     : dispatch_epi<256, 1, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+    return split ? dispatch_epi<128, 3, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                 : dispatch_epi<128, 1, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream);
 }
 
 // ============================================================================

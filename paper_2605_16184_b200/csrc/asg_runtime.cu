@@ -178,11 +178,15 @@ struct Group {
     float *L = nullptr, *R = nullptr, *snapL = nullptr, *snapR = nullptr;
     float *Gh = nullptr, *Gl = nullptr, *GTh = nullptr, *GTl = nullptr;
     float *Th = nullptr, *Tl = nullptr, *Sh = nullptr, *Sl = nullptr;
-    // Shampoo: P = F^-1/4 ; KL: P = F^-1/2 and K = F^-1 (active + shadow)
+    // Shampoo: P = F^-1/4 ; KL: P = F^-1/2 (active + shadow). KL-Shampoo's
+    // F^-1 is never stored: it enters the statistics only as G F_R^-1 G^T =
+    // (G P_R)(G P_R)^T and G^T F_L^-1 G = (P_L G)^T (P_L G) (group_stats)
     float *PLh = nullptr, *PLl = nullptr, *PRh = nullptr, *PRl = nullptr;
     float *sPLh = nullptr, *sPLl = nullptr, *sPRh = nullptr, *sPRl = nullptr;
-    float *KLh = nullptr, *KLl = nullptr, *KRh = nullptr, *KRl = nullptr;
-    float *sKLh = nullptr, *sKLl = nullptr, *sKRh = nullptr, *sKRl = nullptr;
+    // KL-Shampoo: slot k of T holds V = P_L G for the block's current G and
+    // roots (left there by group_stats); the update reuses it unless an
+    // install or a new gradient intervened
+    std::vector<uint8_t> v_ok;
     // SOAP
     float *QLh = nullptr, *QLl = nullptr, *QLTh = nullptr, *QLTl = nullptr;
     float *QRh = nullptr, *QRl = nullptr, *QRTh = nullptr, *QRTl = nullptr;
@@ -222,6 +226,8 @@ struct asg_blockset {
     std::vector<asg::Unit> units;
     std::vector<asg::Group> groups;
     std::vector<void*> allocs;
+    size_t alloc_bytes = 0;      // every device allocation of the blockset
+    size_t workspace_bytes = 0;  // of which: refresh / install workspace (alloc_workspace)
     std::vector<void*> host_allocs;
     cudaStream_t main = nullptr, side = nullptr;
     bool own_main = false;
@@ -337,6 +343,7 @@ T* dalloc(asg_blockset* bs, size_t count) {
     void* p = nullptr;
     CK(cudaMalloc(&p, count * sizeof(T)));
     bs->allocs.push_back(p);
+    bs->alloc_bytes += count * sizeof(T);
     return static_cast<T*>(p);
 }
 
@@ -581,13 +588,7 @@ void alloc_group(asg_blockset* bs, Group& g) {
             g.EL64 = dalloc<double>(bs, nb * size_t(g.m) * g.m);
             g.ER64 = dalloc<double>(bs, nb * size_t(g.n) * g.n);
         }
-        if (is_kl(bs)) {
-            pair_mm(g.KLh, g.KLl);
-            pair_nn(g.KRh, g.KRl);
-            pair_lr(g.sKLh, g.sKLl, g.sKRh, g.sKRl);
-            launch_identity_split(g.KLh, g.KLl, g.nb, g.M, g.m, s);
-            launch_identity_split(g.KRh, g.KRl, g.nb, g.N, g.n, s);
-        }
+        g.v_ok.assign(nb, 0);
     }
     // statistics: zero (precond.cpp:89-90); KL-Shampoo starts from identity
     launch_identity_f32(g.L, g.nb, g.M, g.m, is_kl(bs) ? 1.f : 0.f, s);
@@ -1031,35 +1032,46 @@ void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
                  cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s, cnt * nf * nf * mf);
         return;
     }
-    // KL-Shampoo: X = G R^-1 (T) ; L = b L + a/n X G^T
+    // KL-Shampoo with K = F^-1 = P^2 (P = F^-1/2 is symmetric; both come from
+    // one refresh with one damping, compute_refresh in oracle/): G K_R G^T =
+    // W W^T with W = G P_R, and G^T K_L G = V^T V with V = P_L G. V is also
+    // the update's first product (group_update), so a step costs 8 instead of
+    // 10 block-GEMM units (n^3 each at m = n), and F^-1 is never stored.
+    // W = G P_R -> T
     GemmParams px{};
     px.alpha = 1.f;
     px.Dhi = at(g.Th, mn, s0);
     px.Dlo = at(g.Tl, mn, s0);
     px.ldd = g.N;
     px.d_bstride = int64_t(mn);
-    run_gemm(bs, op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N), op(at(g.KRh, nn, s0), at(g.KRl, nn, s0), g.N, g.N),
+    run_gemm(bs, op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N), op(at(g.PRh, nn, s0), at(g.PRl, nn, s0), g.N, g.N),
              cnt, EPI_SPLIT, px, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
+    // L = b L + a/n W W^T
     const double a = ema ? (1.0 - o.beta2) : 1.0;
     p.beta = ema ? float(o.beta2) : 1.f;
     p.alpha = float(a / double(g.n));
     p.C = at(g.L, mm, s0);
     p.ldc = g.M;
     p.c_bstride = int64_t(mm);
-    run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.Gh, mn, s0), at(g.Gl, mn, s0), g.M, g.N),
+    run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N),
              cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s, cnt * mf * mf * nf);
-    // Z^T = G^T L^-1 (S, [N][M]) ; R = b R + a/m G^T Z
+    // V^T = G^T P_L -> S ([N][M]) and V -> T ([M][N], the update's operand)
     px.Dhi = at(g.Sh, mn, s0);
     px.Dlo = at(g.Sl, mn, s0);
     px.ldd = g.M;
-    run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.KLh, mm, s0), at(g.KLl, mm, s0), g.M, g.M),
-             cnt, EPI_SPLIT, px, nullptr, 0, s, cnt * 2.0 * nf * mf * mf);
+    px.Thi = at(g.Th, mn, s0);
+    px.Tlo = at(g.Tl, mn, s0);
+    px.ldt = g.N;
+    run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.PLh, mm, s0), at(g.PLl, mm, s0), g.M, g.M),
+             cnt, EPI_SPLIT2, px, nullptr, 0, s, cnt * 2.0 * nf * mf * mf);
+    // R = b R + a/m V^T V
     p.alpha = float(a / double(g.m));
     p.C = at(g.R, nn, s0);
     p.ldc = g.N;
     p.c_bstride = int64_t(nn);
-    run_gemm(bs, op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M), op(at(g.Sh, mn, s0), at(g.Sl, mn, s0), g.N, g.M),
+    run_gemm(bs, op(at(g.Sh, mn, s0), at(g.Sl, mn, s0), g.N, g.M), op(at(g.Sh, mn, s0), at(g.Sl, mn, s0), g.N, g.M),
              cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s, cnt * nf * nf * mf);
+    std::fill(g.v_ok.begin() + s0, g.v_ok.begin() + s0 + cnt, uint8_t(1));
 }
 
 // accumulate_factors (precond.cpp:173-189) for every owned block: gradient
@@ -1103,11 +1115,22 @@ void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, fl
     ps.ldd = g.N;
     ps.d_bstride = int64_t(mn);
     if (!is_soap(bs)) {
-        // Y = P_L G -> T ; U = Y P_R
-        ps.Dhi = at(g.Th, mn, s0);
-        ps.Dlo = at(g.Tl, mn, s0);
-        run_gemm(bs, op(at(g.PLh, mm, s0), at(g.PLl, mm, s0), g.M, g.M), op(at(g.GTh, mn, s0), at(g.GTl, mn, s0), g.N, g.M),
-                 cnt, EPI_SPLIT, ps, nullptr, 0, s, cnt * 2.0 * mf * mf * nf);
+        // Y = P_L G -> T ; U = Y P_R. KL-Shampoo: T already holds V = P_L G
+        // from the statistics (group_stats) for the slots whose roots and
+        // gradient are unchanged since; only the others are recomputed.
+        int r0 = s0, r1 = s0 + cnt;
+        if (is_kl(bs)) {
+            while (r0 < r1 && g.v_ok[size_t(r0)]) ++r0;
+            while (r1 > r0 && g.v_ok[size_t(r1 - 1)]) --r1;
+        }
+        if (r1 > r0) {
+            ps.Dhi = at(g.Th, mn, r0);
+            ps.Dlo = at(g.Tl, mn, r0);
+            run_gemm(bs, op(at(g.PLh, mm, r0), at(g.PLl, mm, r0), g.M, g.M),
+                     op(at(g.GTh, mn, r0), at(g.GTl, mn, r0), g.N, g.M), r1 - r0, EPI_SPLIT, ps, nullptr, 0, s,
+                     (r1 - r0) * 2.0 * mf * mf * nf);
+            if (is_kl(bs)) std::fill(g.v_ok.begin() + r0, g.v_ok.begin() + r1, uint8_t(1));
+        }
         run_gemm(bs, op(at(g.Th, mn, s0), at(g.Tl, mn, s0), g.M, g.N), op(at(g.PRh, nn, s0), at(g.PRl, nn, s0), g.N, g.N),
                  cnt, final_epi, pf, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
         return;
@@ -1184,13 +1207,9 @@ void refresh_side(asg_blockset* bs, Group& g, int s0, int cnt, bool left, cudaSt
         double power;
         float *hi, *lo;
     };
-    std::vector<Out> outs;
-    if (is_kl(bs)) {
-        outs.push_back({-0.5, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
-        outs.push_back({-1.0, at(left ? g.sKLh : g.sKRh, DD, s0), at(left ? g.sKLl : g.sKRl, DD, s0)});
-    } else {
-        outs.push_back({-0.25, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
-    }
+    // Shampoo F^-1/4, KL-Shampoo F^-1/2 (its F^-1 = (F^-1/2)^2 is not stored)
+    const Out outs[1] = {{is_kl(bs) ? -0.5 : -0.25, at(left ? g.sPLh : g.sPRh, DD, s0),
+                          at(left ? g.sPLl : g.sPRl, DD, s0)}};
     for (const Out& o : outs) {
         launch_scale_columns(bs->ws_vecs, bs->ws_vals, bs->ws_eps, o.power, cnt, d, bs->ws_W, g.d_status + s0, s);
         // V diag(w) V^T  (densela.hpp:280), symmetrized on conversion
@@ -1406,13 +1425,8 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
             double power;
             float *hi, *lo;
         };
-        std::vector<Out> outs;
-        if (is_kl(bs)) {
-            outs.push_back({-0.5, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
-            outs.push_back({-1.0, at(left ? g.sKLh : g.sKRh, DD, s0), at(left ? g.sKLl : g.sKRl, DD, s0)});
-        } else {
-            outs.push_back({-0.25, at(left ? g.sPLh : g.sPRh, DD, s0), at(left ? g.sPLl : g.sPRl, DD, s0)});
-        }
+        const Out outs[1] = {{is_kl(bs) ? -0.5 : -0.25, at(left ? g.sPLh : g.sPRh, DD, s0),
+                              at(left ? g.sPLl : g.sPRl, DD, s0)}};
         for (const Out& o : outs) {
             launch_scale_columns_split(V, Vl, vals, bs->ws_eps + size_t(j) * cnt, o.power, cnt, d, D, off(t[6], j),
                                        sp ? off(t[7], j) : nullptr, g.d_status + s0, s);
@@ -1433,7 +1447,7 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
 // NEWTON refresh of one chunk (Shampoo / KL-Shampoo): per side, the damped
 // snapshot's inverse root by coupled Newton-Schulz straight into the shadow
 // roots (compute_refresh precond.cpp:136-140: inv_root(F, 4, damping tr/n));
-// KL-Shampoo also forms F^-1 = (F^-1/2)^2 (one symmetric GEMM).
+// KL-Shampoo's F^-1 is (F^-1/2)^2 and is never formed (group_stats).
 void refresh_newton(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
     PhaseTimer pt(s);
     pt.mark("start");
@@ -1457,16 +1471,6 @@ void refresh_newton(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s)
         launch_ns_inv_root(snap, nmat, d, D, bs->ws_eps, is_kl(bs) ? 2 : 4, ph, pl, bs->ns_ws, st, tiles, ntiles,
                            bs->precision, bs->num_sms, s);
         if (both) launch_merge_status(st, cnt, g.d_status + s0, s);
-        if (is_kl(bs)) {
-            GemmParams pk{};
-            pk.alpha = 1.f;
-            pk.Dhi = at(left ? g.sKLh : g.sKRh, DD, s0);
-            pk.Dlo = at(left ? g.sKLl : g.sKRl, DD, s0);
-            pk.ldd = D;
-            pk.d_bstride = int64_t(DD);
-            run_gemm(bs, op(ph, pl, D, D), op(ph, pl, D, D), nmat, EPI_SYM_SPLIT, pk, tiles, ntiles, s,
-                     double(nmat) * d * double(d) * d);
-        }
     }
     pt.mark("newton roots");
     pt.report(g.m, cnt);
@@ -1670,12 +1674,7 @@ void install_roots(asg_blockset* bs, Group& g, int s0, int cnt) {
     cp(at(g.PLl, mm, s0), at(g.sPLl, mm, s0), mm);
     cp(at(g.PRh, nn, s0), at(g.sPRh, nn, s0), nn);
     cp(at(g.PRl, nn, s0), at(g.sPRl, nn, s0), nn);
-    if (is_kl(bs)) {
-        cp(at(g.KLh, mm, s0), at(g.sKLh, mm, s0), mm);
-        cp(at(g.KLl, mm, s0), at(g.sKLl, mm, s0), mm);
-        cp(at(g.KRh, nn, s0), at(g.sKRh, nn, s0), nn);
-        cp(at(g.KRl, nn, s0), at(g.sKRl, nn, s0), nn);
-    }
+    if (is_kl(bs)) std::fill(g.v_ok.begin() + s0, g.v_ok.begin() + s0 + cnt, uint8_t(0));
 }
 
 // Device-side install of a finished refresh (install_refresh precond.cpp:144-164).
@@ -1926,6 +1925,7 @@ Group& owned_group(asg_blockset* bs, const Unit& u) {
 
 void prep_single(asg_blockset* bs, Group& g, const Unit& u) {
     const size_t mn = slabMN(g);
+    if (!g.v_ok.empty()) g.v_ok[size_t(u.slot)] = 0;
     launch_prep_grad(bs->d_ref1, 1, g.M, g.N, nullptr, 1.f, at(g.Gh, mn, u.slot), at(g.Gl, mn, u.slot),
                      at(g.GTh, mn, u.slot), at(g.GTl, mn, u.slot), bs->main);
 }
@@ -2170,7 +2170,9 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         build_units(bs);
         build_groups(bs);
         for (Group& g : bs->groups) alloc_group(bs, g);
+        const size_t before_ws = bs->alloc_bytes;
         alloc_workspace(bs);
+        bs->workspace_bytes = bs->alloc_bytes - before_ws;
         for (Unit& u : bs->units) {
             CK(cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming));
             if (u.adamw && u.owner == rank) {
@@ -2284,24 +2286,11 @@ int asg_blockset_block_info(const asg_blockset* bs, int64_t idx, asg_block_info*
 }
 
 int asg_blockset_state_bytes(const asg_blockset* bs, uint64_t* bytes) {
-    return guard([&] {
-        size_t total = 0;
-        for (void* p : bs->allocs) {
-            (void)p;
-        }
-        // recompute from group sizes (allocation sizes are not tracked per pointer)
-        for (const Group& g : bs->groups) {
-            const size_t nb = size_t(g.nb);
-            size_t f = nb * (2 * slabMM(g) + 2 * slabNN(g) + 4 * slabMN(g) * (split_mode(bs) ? 2 : 1));
-            if (is_soap(bs))
-                f += nb * ((slabMM(g) * 2 + slabNN(g) * 2) * (split_mode(bs) ? 2 : 1) + 2 * slabMN(g)) +
-                     nb * 2 * (size_t(g.m) * g.m + size_t(g.n) * g.n) * 2;
-            else
-                f += nb * (slabMM(g) + slabNN(g)) * 2 * (split_mode(bs) ? 2 : 1) * (is_kl(bs) ? 2 : 1);
-            total += f * 4;
-        }
-        *bytes = total;
-    });
+    return guard([&] { *bytes = bs->alloc_bytes - bs->workspace_bytes; });
+}
+
+int asg_blockset_workspace_bytes(const asg_blockset* bs, uint64_t* bytes) {
+    return guard([&] { *bytes = bs->workspace_bytes; });
 }
 
 int asg_blockset_stream(const asg_blockset* bs, void** stream) {
@@ -2601,8 +2590,25 @@ int asg_block_read(asg_blockset* bs, int64_t idx, int32_t role, double* out, int
             case ASG_ROLE_FACTOR_R: rd32(g.R, slabNN(g), g.N, g.N, n, n, nullptr); break;
             case ASG_ROLE_INV_L: rd32(g.PLh, slabMM(g), g.M, g.M, m, m, g.PLl); break;
             case ASG_ROLE_INV_R: rd32(g.PRh, slabNN(g), g.N, g.N, n, n, g.PRl); break;
-            case ASG_ROLE_KL_INV_L: rd32(g.KLh, slabMM(g), g.M, g.M, m, m, g.KLl); break;
-            case ASG_ROLE_KL_INV_R: rd32(g.KRh, slabNN(g), g.N, g.N, n, n, g.KRl); break;
+            case ASG_ROLE_KL_INV_L:
+            case ASG_ROLE_KL_INV_R: {
+                // F^-1 = (F^-1/2)^2 (not stored, group_stats): the installed root squared in fp64
+                if (!is_kl(bs)) throw Fail{ASG_ERR_INVALID_ARGUMENT, "role not held by this method"};
+                const bool left = role == ASG_ROLE_KL_INV_L;
+                const int d = left ? m : n;
+                if (count < int64_t(d) * d) throw Fail{ASG_ERR_SHAPE_MISMATCH, "output too small"};
+                if (left)
+                    rd32(g.PLh, slabMM(g), g.M, g.M, m, m, g.PLl);
+                else
+                    rd32(g.PRh, slabNN(g), g.N, g.N, n, n, g.PRl);
+                const size_t dd = size_t(d) * d;
+                h2d(bs->ws_out, out, dd * 8, bs->main);
+                launch_dgemm(false, false, d, d, d, 1.0, bs->ws_out, d, 0, bs->ws_out, d, 0, 0.0, bs->ws_W, d, 0, 1,
+                             bs->main);
+                CK(cudaStreamSynchronize(bs->main));
+                CK(cudaMemcpy(out, bs->ws_W, dd * 8, cudaMemcpyDeviceToHost));
+                break;
+            }
             case ASG_ROLE_BASIS_L:
                 if (g.QL64) rd64(g.QL64, size_t(m) * m, size_t(m) * m);
                 else rd32(g.QLh, slabMM(g), g.M, g.M, m, m, g.QLl);  // F32 refresh: split basis
@@ -2626,6 +2632,7 @@ int asg_block_write(asg_blockset* bs, int64_t idx, int32_t role, const double* i
         check_owned_index(bs, idx);
         const Unit& u = bs->units[size_t(idx)];
         Group& g = owned_group(bs, u);
+        if (!g.v_ok.empty()) g.v_ok[size_t(u.slot)] = 0;  // roots may change: KL's cached V = P_L G is stale
         CK(cudaStreamSynchronize(bs->main));
         CK(cudaStreamSynchronize(bs->side));
         const int m = g.m, n = g.n;
@@ -2659,8 +2666,10 @@ int asg_block_write(asg_blockset* bs, int64_t idx, int32_t role, const double* i
             case ASG_ROLE_FACTOR_R: wr32(g.R, slabNN(g), g.N, g.N, n, n, nullptr, nullptr, nullptr); break;
             case ASG_ROLE_INV_L: wr32(g.PLh, slabMM(g), g.M, g.M, m, m, sp ? g.PLl : nullptr, nullptr, nullptr); break;
             case ASG_ROLE_INV_R: wr32(g.PRh, slabNN(g), g.N, g.N, n, n, sp ? g.PRl : nullptr, nullptr, nullptr); break;
-            case ASG_ROLE_KL_INV_L: wr32(g.KLh, slabMM(g), g.M, g.M, m, m, sp ? g.KLl : nullptr, nullptr, nullptr); break;
-            case ASG_ROLE_KL_INV_R: wr32(g.KRh, slabNN(g), g.N, g.N, n, n, sp ? g.KRl : nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_KL_INV_L:
+            case ASG_ROLE_KL_INV_R:
+                throw Fail{ASG_ERR_INVALID_ARGUMENT,
+                           "KL-Shampoo's F^-1 is derived from the installed root (INV^2); write ASG_ROLE_INV_*"};
             case ASG_ROLE_BASIS_L:
             case ASG_ROLE_BASIS_R: {
                 const bool left = role == ASG_ROLE_BASIS_L;
@@ -3287,9 +3296,8 @@ struct asg_refresh_result {
     int method = 0;
     bool f64_soap = false;
     std::vector<void*> bufs;  // device
-    // roots (Shampoo / KL-Shampoo): P (+K) per side, split pairs
+    // roots (Shampoo / KL-Shampoo): P per side, split pairs (KL: F^-1 = P^2)
     float *PLh = nullptr, *PLl = nullptr, *PRh = nullptr, *PRl = nullptr;
-    float *KLh = nullptr, *KLl = nullptr, *KRh = nullptr, *KRl = nullptr;
     // SOAP, F32 refresh: the new bases transposed (split); F64 refresh: the new bases (fp64)
     float *QLTh = nullptr, *QLTl = nullptr, *QRTh = nullptr, *QRTl = nullptr;
     double *QL64 = nullptr, *QR64 = nullptr, *valsL = nullptr, *valsR = nullptr;
@@ -3412,18 +3420,6 @@ int asg_compute_refresh(asg_blockset* bs, const asg_snapshot* sn, asg_refresh_re
                 d2d(r->PLl, at(g.sPLl, mm, u.slot), mm * 4, s);
                 d2d(r->PRl, at(g.sPRl, nn, u.slot), nn * 4, s);
             }
-            if (is_kl(bs)) {
-                r->KLh = ralloc<float>(r, mm);
-                r->KRh = ralloc<float>(r, nn);
-                d2d(r->KLh, at(g.sKLh, mm, u.slot), mm * 4, s);
-                d2d(r->KRh, at(g.sKRh, nn, u.slot), nn * 4, s);
-                if (sp) {
-                    r->KLl = ralloc<float>(r, mm);
-                    r->KRl = ralloc<float>(r, nn);
-                    d2d(r->KLl, at(g.sKLl, mm, u.slot), mm * 4, s);
-                    d2d(r->KRl, at(g.sKRl, nn, u.slot), nn * 4, s);
-                }
-            }
         } else if (f32_refresh(bs)) {
             // absolute new bases, transposed: Q_new^T = J^T Q_cur^T (A = J^T, B = Q_cur)
             r->valsL = ralloc<double>(r, size_t(g.m));
@@ -3488,10 +3484,6 @@ int asg_install_refresh(asg_blockset* bs, int64_t idx, asg_refresh_result* r, in
             d2d(at(g.sPRh, nn, u.slot), r->PRh, nn * 4, s);
             d2d(at(g.sPLl, mm, u.slot), r->PLl, mm * 4, s);
             d2d(at(g.sPRl, nn, u.slot), r->PRl, nn * 4, s);
-            d2d(at(g.sKLh, mm, u.slot), r->KLh, mm * 4, s);
-            d2d(at(g.sKRh, nn, u.slot), r->KRh, nn * 4, s);
-            d2d(at(g.sKLl, mm, u.slot), r->KLl, mm * 4, s);
-            d2d(at(g.sKRl, nn, u.slot), r->KRl, nn * 4, s);
             install_roots(bs, g, u.slot, 1);
         } else if (!r->f64_soap) {
             // rot = Q_new^T Q_old (precond.cpp:146-147) as the shadow rotation J^T:

@@ -152,6 +152,11 @@ class AsteriaOptimizer:
         check(lib.asg_blockset_state_bytes(self._h, C.byref(b)))
         return b.value
 
+    def workspace_bytes(self):
+        b = C.c_uint64()
+        check(lib.asg_blockset_workspace_bytes(self._h, C.byref(b)))
+        return b.value
+
     def profile(self, enable=True):
         check(lib.asg_profile_enable(self._h, 1 if enable else 0))
 

@@ -39,6 +39,7 @@ _SIGS = {
     "asg_blockset_num_blocks": (C.c_int, [_vp, _P(_i64)]),
     "asg_blockset_block_info": (C.c_int, [_vp, _i64, _P(abi.BlockInfo)]),
     "asg_blockset_state_bytes": (C.c_int, [_vp, _P(_u64)]),
+    "asg_blockset_workspace_bytes": (C.c_int, [_vp, _P(_u64)]),
     "asg_blockset_stream": (C.c_int, [_vp, _P(_vp)]),
     "asg_grad_sqnorm": (C.c_int, [_vp, _vp, _P(_f64), _P(_i32)]),
     "asg_accumulate": (C.c_int, [_vp, _f64, _vp]),

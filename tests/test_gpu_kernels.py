@@ -30,7 +30,10 @@ def _ptr(t):
 
 
 @pytest.mark.parametrize("prec,tol", [(0, 3e-6), (1, 3e-3)])
-@pytest.mark.parametrize("batch,M,N,K", [(1, 128, 128, 32), (2, 256, 384, 96), (3, 384, 256, 512), (1, 1024, 1024, 1024)])
+# the last three take the CTA-pair (cta_group::2, 256-row tile) schedule:
+# BN = 256, BN = 128, and a deep K on the bench's block size
+@pytest.mark.parametrize("batch,M,N,K", [(1, 128, 128, 32), (2, 256, 384, 96), (3, 384, 256, 512), (1, 1024, 1024, 1024),
+                                         (40, 512, 512, 256), (40, 512, 384, 128), (2, 2048, 2048, 512)])
 def test_gemm_tn_matches_fp64(rt, prec, tol, batch, M, N, K):
     g = torch.Generator().manual_seed(M * 7 + N + K)
     A = torch.randn(batch, M, K, generator=g, dtype=torch.float64)

@@ -183,10 +183,15 @@ def test_f32_refresh_roots_at_bench_sizes(P, method, n, mode):
         P.refresh_inverse(b, cfg, step)
         r = orc_np.compute_refresh(b.factor_l, b.factor_r, cfg)
         errs = [rel(b.inv_l, r["inv_l"]), rel(b.inv_r, r["inv_r"])]
+        kerrs = []
         if method == abi.KL_SHAMPOO:
-            errs += [rel(b.get(abi.KL_INV_L), r["kl_inv_l"]), rel(b.get(abi.KL_INV_R), r["kl_inv_r"])]
-        print(f"n={n} {abi.METHOD_NAMES[method]} mode {mode} step {step}: root errors {['%.2e' % e for e in errs]}")
+            # F^-1 is derived as (F^-1/2)^2 (never stored): to first order its
+            # relative error is twice the root's, hence the stated 2x bound
+            kerrs = [rel(b.get(abi.KL_INV_L), r["kl_inv_l"]), rel(b.get(abi.KL_INV_R), r["kl_inv_r"])]
+        print(f"n={n} {abi.METHOD_NAMES[method]} mode {mode} step {step}: root errors "
+              f"{['%.2e' % e for e in errs + kerrs]}")
         assert max(errs) <= root_tol(n), errs
+        assert not kerrs or max(kerrs) <= 2 * root_tol(n), kerrs
 
 
 @pytest.mark.parametrize("m,n", [(1024, 1024), (768, 1024), (2048, 2048)])
