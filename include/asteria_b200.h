@@ -50,7 +50,11 @@ typedef enum asg_status {
     ASG_ERR_CUDA = 11,               /* CUDA runtime/driver failure            */
     ASG_ERR_OUT_OF_MEMORY = 12,      /* device allocation failed               */
     ASG_ERR_INVALID_ARGUMENT = 13,   /* bad handle / pointer / index           */
-    ASG_ERR_UNSUPPORTED = 14         /* no sm_100a device, or feature absent   */
+    ASG_ERR_UNSUPPORTED = 14,        /* no sm_100a device, or feature absent   */
+    ASG_ERR_CAPACITY_EXHAUSTED = 15, /* CapacityExhaustedError    errors.hpp:26 */
+    ASG_ERR_IO = 16,                 /* IoError                   errors.hpp:28 */
+    ASG_ERR_PINNED_ENTRY = 17,       /* PinnedEntryError          errors.hpp:29 */
+    ASG_ERR_DIRTY_NOT_PERSISTED = 18 /* DirtyNotPersistedError    errors.hpp:30 */
 } asg_status;
 
 /* Method (precond.hpp:19) extended with KL-Shampoo, which the reference only
@@ -136,7 +140,7 @@ typedef struct asg_scheduler_config {
     int64_t staleness_S;
     int64_t pf;
     int32_t pool_size;     /* accepted for schema compatibility; refresh runs on a side stream */
-    int32_t drain_budget;  /* accepted for schema compatibility (tier staging is out of scope) */
+    int32_t drain_budget;  /* staged tier-store transfers installed per ForwardPost (asg_on_hook) */
     double inject_job_delay_steps;
     double inject_job_delay_jitter_steps;
     double step_compute_us;
@@ -193,7 +197,9 @@ typedef enum asg_event_kind {
     ASG_EV_JOB_DONE = 2,
     ASG_EV_INSTALL = 3,
     ASG_EV_BARRIER_WAIT_BEGIN = 4,
-    ASG_EV_BARRIER_WAIT_END = 5
+    ASG_EV_BARRIER_WAIT_END = 5,
+    ASG_EV_PREFETCH = 6, /* tier-store staging of inverse state (trace.hpp:25, asyncsched.cpp:183,261) */
+    ASG_EV_DRAIN = 7     /* a staged transfer installed at ForwardPost (asyncsched.cpp:240) */
 } asg_event_kind;
 
 typedef struct asg_event {
@@ -439,6 +445,99 @@ int asg_launch_count(uint64_t* count);
 int asg_profile_enable(asg_blockset* bs, int32_t enable);
 /* Synchronizes, returns the stats accumulated since the last reset. */
 int asg_get_kernel_stats(asg_blockset* bs, asg_kernel_stats* out, int32_t reset);
+
+
+/* ---- tiered store of optimizer state (F3; tierstore.hpp, tierstore.cpp) ---
+ * Keyed tensors ("block_id/role") across three tiers, with the reference's
+ * semantics: byte-accurate residency gauges, least-recently-touched eviction
+ * one tier down, pinning, explicit flush/reclaim, an append-only cold file in
+ * the reference's bit-exact ASTRCOLD format (tierstore.hpp:8-13), and
+ * asynchronous prefetch by a transfer worker whose completed copies are
+ * installed only by drain_ready (never blocking on incomplete ones).
+ * B200 mapping: Hot = device memory (HBM) of `hot_device`, Host = pinned host
+ * memory, Cold = the file. Host<->Hot moves are DMA copies on the store's own
+ * copy stream; a prefetch to Hot is staged by the worker thread (file read ->
+ * pinned -> cudaMemcpyAsync into a stream-ordered device allocation) so the
+ * training thread never waits for the link. hot_device = -1 keeps the Hot
+ * tier in host memory (bookkeeping-only hosts without a GPU). */
+typedef enum asg_tier { ASG_TIER_HOT = 0, ASG_TIER_HOST = 1, ASG_TIER_COLD = 2 } asg_tier;
+
+typedef struct asg_store_config {           /* StoreConfig tierstore.hpp:33-39 */
+    uint64_t hot_capacity_bytes;            /* default 1 GiB */
+    uint64_t host_capacity_bytes;           /* default 1 GiB */
+    const char* cold_path;                  /* required */
+    double transfer_bandwidth_bytes_per_sec; /* injected link model; 0 = unthrottled */
+    uint64_t transfer_latency_us;
+    int32_t hot_device;                     /* CUDA device of the Hot tier; -1: host memory */
+} asg_store_config;
+
+typedef struct asg_entry_view {             /* EntryView tierstore.hpp:61-69 */
+    int32_t tier;
+    uint64_t bytes;
+    int32_t dirty, pinned;
+    int64_t last_touch_step;
+    int32_t staged_pending, staged_ready;
+} asg_entry_view;
+
+typedef struct asg_residency {              /* ResidencyGauges tierstore.hpp:41-45 */
+    uint64_t hot_bytes, host_bytes, cold_bytes;
+} asg_residency;
+
+typedef struct asg_io_counters {            /* IoCounters tierstore.hpp:47-59 */
+    uint64_t file_writes, file_reads, write_skips, page_ins, evictions, prefetch_requests, transfers_started,
+        transfers_coalesced, transfers_completed, transfers_dropped, drains_installed;
+} asg_io_counters;
+
+typedef struct asg_tierstore asg_tierstore;
+
+/* Fills the reference's defaults (tierstore.hpp:33-39; cold_path NULL, hot_device -1). */
+int asg_store_config_defaults(asg_store_config* out);
+/* TierStore::TierStore tierstore.cpp:24-43: truncates/creates the cold file and writes its header. */
+int asg_tierstore_create(const asg_store_config* cfg, asg_tierstore** out);
+int asg_tierstore_destroy(asg_tierstore* st);
+/* Keys are (block_id, role): role is an asg_role (TensorRole tiers.hpp:35-44). */
+/* put tierstore.cpp:169-211 (bytes: host memory) */
+int asg_tier_put(asg_tierstore* st, const char* block_id, int32_t role, const void* bytes, uint64_t size, int32_t tier,
+                 asg_entry_view* out);
+/* put from device memory (the Hot-tier source of a blockset's state: no host round trip for Hot puts) */
+int asg_tier_put_device(asg_tierstore* st, const char* block_id, int32_t role, const void* dev_bytes, uint64_t size,
+                        int32_t tier, asg_entry_view* out);
+/* get tierstore.cpp:213-229: copies the payload to host `out` (capacity `cap`;
+ * *size receives the payload size even when cap is too small -> ShapeMismatch);
+ * a Cold entry is paged in to Host. */
+int asg_tier_get(asg_tierstore* st, const char* block_id, int32_t role, void* out, uint64_t cap, uint64_t* size,
+                 int32_t* tier);
+/* Device address of a Hot entry's payload (valid until the entry moves). */
+int asg_tier_device_ptr(asg_tierstore* st, const char* block_id, int32_t role, void** dev_ptr);
+int asg_tier_demote(asg_tierstore* st, const char* block_id, int32_t role, int32_t to);   /* :231-234 */
+int asg_tier_promote(asg_tierstore* st, const char* block_id, int32_t role, int32_t to);  /* :236-257 */
+int asg_tier_reclaim(asg_tierstore* st, const char* block_id, int32_t role, uint64_t* freed); /* :259-273 */
+int asg_tier_flush(asg_tierstore* st, const char* block_id, int32_t role);                 /* :275-282 */
+int asg_tier_pin(asg_tierstore* st, const char* block_id, int32_t role);
+int asg_tier_unpin(asg_tierstore* st, const char* block_id, int32_t role);
+/* prefetch tierstore.cpp:294-308: returns at once; duplicates coalesce onto one ticket */
+int asg_tier_prefetch(asg_tierstore* st, const char* block_id, int32_t role, int32_t to, uint64_t* ticket);
+/* drain_ready tierstore.cpp:404-420 */
+int asg_tier_drain_ready(asg_tierstore* st, int32_t max_items, int32_t* installed);
+int asg_tier_advance_step(asg_tierstore* st, int64_t step);
+int asg_tier_contains(asg_tierstore* st, const char* block_id, int32_t role, int32_t* out);
+int asg_tier_inspect(asg_tierstore* st, const char* block_id, int32_t role, asg_entry_view* out);
+int asg_tier_gauges(asg_tierstore* st, asg_residency* out);
+int asg_tier_counters(asg_tierstore* st, asg_io_counters* out);
+/* audit tierstore.cpp:437-456: ASG_ERR_AUDIT on any mismatch */
+int asg_tier_audit(asg_tierstore* st);
+
+/* The scheduler side of the store (ShadowScheduler with a TierStore,
+ * asyncsched.hpp:117-119): once attached, every scheduler install writes the
+ * block's refreshed inverse state (INV_L/R; SOAP: BASIS_L/R) to the Host tier
+ * and prefetches it toward Hot (asyncsched.cpp:164-184); the store is not
+ * owned. NULL detaches. */
+int asg_blockset_attach_store(asg_blockset* bs, asg_tierstore* store);
+/* HookEvent kinds (asyncsched.hpp): ForwardPost drains at most drain_budget staged
+ * transfers enqueued before `step`; BackwardPre prefetches Cold inverse state
+ * to Host; StepEnd is asg_step_end (asyncsched.cpp:223-286). */
+typedef enum asg_hook { ASG_HOOK_FORWARD_POST = 0, ASG_HOOK_BACKWARD_PRE = 1, ASG_HOOK_STEP_END = 2 } asg_hook;
+int asg_on_hook(asg_blockset* bs, int32_t kind, int64_t step);
 
 /* ---- diagnostics: the tensor-core GEMM on its own ----------------------- */
 /* C[b] = alpha * A[b] * B[b]^T + beta * C[b] for b < batch, fp32 device

@@ -23,7 +23,10 @@ REFRESH_F64, REFRESH_F32, REFRESH_NEWTON = 0, 1, 2
 (FACTOR_L, FACTOR_R, INV_L, INV_R, BASIS_L, BASIS_R, ROTATED_M, ROTATED_V,
  KL_INV_L, KL_INV_R, EIGVALS_L, EIGVALS_R) = range(12)
 # asg_event_kind
-EV_DISPATCH, EV_JOB_START, EV_JOB_DONE, EV_INSTALL, EV_BARRIER_WAIT_BEGIN, EV_BARRIER_WAIT_END = range(6)
+(EV_DISPATCH, EV_JOB_START, EV_JOB_DONE, EV_INSTALL, EV_BARRIER_WAIT_BEGIN, EV_BARRIER_WAIT_END,
+ EV_PREFETCH, EV_DRAIN) = range(8)
+# asg_hook (HookEvent::Kind asyncsched.hpp)
+HOOK_FORWARD_POST, HOOK_BACKWARD_PRE, HOOK_STEP_END = range(3)
 
 
 class OptimizerConfig(C.Structure):
@@ -240,10 +243,54 @@ class UnsupportedError(Error):
     code = 14
 
 
+class CapacityExhaustedError(Error):
+    code = 15
+
+
+class IoError(Error):
+    code = 16
+
+
+class PinnedEntryError(Error):
+    code = 17
+
+
+class DirtyNotPersistedError(Error):
+    code = 18
+
+
 _BY_CODE = {cls.code: cls for cls in (
     NonFiniteError, NoConvergenceError, NotPsdError, LayoutMismatchError, ShapeMismatchError,
     StaleUninitializedError, WorkerPoolDownError, ConfigInvalidError, AuditError,
-    MissingKeyError, CudaError, OutOfMemoryError, InvalidArgumentError, UnsupportedError)}
+    MissingKeyError, CudaError, OutOfMemoryError, InvalidArgumentError, UnsupportedError,
+    CapacityExhaustedError, IoError, PinnedEntryError, DirtyNotPersistedError)}
+
+
+# ---- tiered store (F3; tierstore.hpp) ----------------------------------------
+TIER_HOT, TIER_HOST, TIER_COLD = 0, 1, 2
+TIER_NAMES = {TIER_HOT: "Hot", TIER_HOST: "Host", TIER_COLD: "Cold"}
+
+
+class StoreConfig(C.Structure):
+    _fields_ = [("hot_capacity_bytes", C.c_uint64), ("host_capacity_bytes", C.c_uint64),
+                ("cold_path", C.c_char_p), ("transfer_bandwidth_bytes_per_sec", C.c_double),
+                ("transfer_latency_us", C.c_uint64), ("hot_device", C.c_int32)]
+
+
+class EntryView(C.Structure):
+    _fields_ = [("tier", C.c_int32), ("bytes", C.c_uint64), ("dirty", C.c_int32), ("pinned", C.c_int32),
+                ("last_touch_step", C.c_int64), ("staged_pending", C.c_int32), ("staged_ready", C.c_int32)]
+
+
+class Residency(C.Structure):
+    _fields_ = [("hot_bytes", C.c_uint64), ("host_bytes", C.c_uint64), ("cold_bytes", C.c_uint64)]
+
+
+class IoCounters(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "file_writes", "file_reads", "write_skips", "page_ins", "evictions", "prefetch_requests",
+        "transfers_started", "transfers_coalesced", "transfers_completed", "transfers_dropped",
+        "drains_installed")]
 
 
 def raise_for(code, message):

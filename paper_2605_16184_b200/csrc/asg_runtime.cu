@@ -30,11 +30,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -226,6 +228,17 @@ struct asg_blockset {
     std::vector<asg::Unit> units;
     std::vector<asg::Group> groups;
     std::vector<void*> allocs;
+    // F3: optional tiered store of the installed inverse state (asyncsched.cpp:164-184,223-267)
+    asg_tierstore* store = nullptr;
+    float* store_stage = nullptr;  // contiguous (hi | lo) staging of one installed root / basis
+    size_t store_stage_floats = 0;
+    struct QueuedPrefetch {
+        std::string block_id;
+        int32_t role;
+        int unit;
+        int64_t enqueue_step;
+    };
+    std::deque<QueuedPrefetch> queued_prefetches;
     size_t alloc_bytes = 0;      // every device allocation of the blockset
     size_t workspace_bytes = 0;  // of which: refresh / install workspace (alloc_workspace)
     std::vector<void*> host_allocs;
@@ -1748,8 +1761,52 @@ void sched_install(asg_blockset* bs, int idx, int64_t step) {
     u.fresh.installed_snapshot_step = u.dispatch_step;
     u.fresh.dispatch_step_of_pending = -1;
     u.pending = false;
+    if (bs->store) emit(bs, step, ASG_EV_PREFETCH, idx, u.version, bs->now_us);  // asyncsched.cpp:183
     emit(bs, step, ASG_EV_INSTALL, idx, u.version, bs->now_us);
     bs->stats.installed += 1;
+}
+
+// F3 write-back (ShadowScheduler::install asyncsched.cpp:164-184): the
+// refreshed inverse state (Shampoo / KL roots, SOAP bases) of each installed
+// block goes to the store's Host tier (pinned) as it lives in HBM -- the
+// padded fp32 (hi | lo) slabs, or the fp64 basis of the F64 refresh -- and is
+// prefetched back toward Hot; ForwardPost drains it (asg_on_hook).
+std::string unit_id(const asg_blockset* bs, int i);
+void store_write_back(asg_blockset* bs, const std::vector<int>& todo) {
+    CK(cudaStreamSynchronize(bs->main));  // the installs above are complete
+    for (int idx : todo) {
+        const Unit& u = bs->units[size_t(idx)];
+        Group& g = bs->groups[size_t(u.group)];
+        const std::string id = unit_id(bs, idx);
+        for (int side = 0; side < 2; ++side) {
+            const bool left = side == 0;
+            const int32_t role = is_soap(bs) ? (left ? ASG_ROLE_BASIS_L : ASG_ROLE_BASIS_R)
+                                             : (left ? ASG_ROLE_INV_L : ASG_ROLE_INV_R);
+            const int d = left ? g.m : g.n, D = left ? g.M : g.N;
+            const size_t DD = size_t(D) * D;
+            const void* src = nullptr;
+            uint64_t bytes = 0;
+            if (is_soap(bs) && g.QL64) {  // F64 refresh: the fp64 basis itself
+                src = at(left ? g.QL64 : g.QR64, size_t(d) * d, u.slot);
+                bytes = uint64_t(d) * d * 8;
+            } else {
+                const float* hi = is_soap(bs) ? at(left ? g.QLh : g.QRh, DD, u.slot) : at(left ? g.PLh : g.PRh, DD, u.slot);
+                const float* lo = is_soap(bs) ? at(left ? g.QLl : g.QRl, DD, u.slot) : at(left ? g.PLl : g.PRl, DD, u.slot);
+                CK(cudaMemcpyAsync(bs->store_stage, hi, DD * 4, cudaMemcpyDeviceToDevice, bs->main));
+                bytes = DD * 4;
+                if (lo) {
+                    CK(cudaMemcpyAsync(bs->store_stage + DD, lo, DD * 4, cudaMemcpyDeviceToDevice, bs->main));
+                    bytes += DD * 4;
+                }
+                CK(cudaStreamSynchronize(bs->main));
+                src = bs->store_stage;
+            }
+            int rc = asg_tier_put_device(bs->store, id.c_str(), role, src, bytes, ASG_TIER_HOST, nullptr);
+            if (rc == ASG_OK) rc = asg_tier_prefetch(bs->store, id.c_str(), role, ASG_TIER_HOT, nullptr);
+            if (rc != ASG_OK) throw Fail{rc, asg_last_error()};
+            bs->queued_prefetches.push_back({id, role, idx, u.last_refresh_step});
+        }
+    }
 }
 
 // Launches every outstanding refresh as one batch, then performs the deferred
@@ -1808,6 +1865,7 @@ void run_deferred_installs(asg_blockset* bs) {
         for (int idx : todo) install_apply(bs, bs->units[size_t(idx)]);
     }
     for (int idx : todo) bs->units[size_t(idx)].launched = false;
+    if (bs->store && !todo.empty()) store_write_back(bs, todo);
 }
 
 void install_device(asg_blockset* bs, Unit& u) {
@@ -1984,6 +2042,11 @@ void resolve_deferred(asg_blockset* bs, bool blocking) {
 // C-ABI
 // ============================================================================
 using namespace asg;
+
+namespace asg {
+// the message of asg_last_error() for entry points defined in other files (asg_tierstore.cu)
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace asg
 
 extern "C" {
 
@@ -2468,6 +2531,83 @@ int asg_step_end(asg_blockset* bs, int64_t step) {
     return guard([&] {
         CK(cudaSetDevice(bs->device));
         sched_step_end(bs, step);
+        if (bs->store) {  // asyncsched.cpp:284
+            const int rc = asg_tier_advance_step(bs->store, step);
+            if (rc != ASG_OK) throw Fail{rc, asg_last_error()};
+        }
+    });
+}
+
+int asg_blockset_attach_store(asg_blockset* bs, asg_tierstore* store) {
+    return guard([&] {
+        if (!bs) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null blockset"};
+        CK(cudaSetDevice(bs->device));
+        bs->store = store;
+        bs->queued_prefetches.clear();
+        if (store && !bs->store_stage) {
+            size_t mx = 0;
+            for (const Group& g : bs->groups) mx = std::max({mx, size_t(g.M) * g.M, size_t(g.N) * g.N});
+            bs->store_stage_floats = 2 * mx;
+            if (mx) bs->store_stage = dalloc<float>(bs, bs->store_stage_floats);
+        }
+    });
+}
+
+// on_hook(ForwardPost / BackwardPre) asyncsched.cpp:223-267 (StepEnd is asg_step_end)
+int asg_on_hook(asg_blockset* bs, int32_t kind, int64_t step) {
+    return guard([&] {
+        if (!bs) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null blockset"};
+        if (kind == ASG_HOOK_STEP_END) {
+            const int rc = asg_step_end(bs, step);
+            if (rc != ASG_OK) throw Fail{rc, asg_last_error()};
+            return;
+        }
+        if (!bs->store) return;
+        auto ok = [](int rc) {
+            if (rc != ASG_OK) throw Fail{rc, asg_last_error()};
+        };
+        if (kind == ASG_HOOK_FORWARD_POST) {
+            // deterministic drain: only transfers enqueued before this step count,
+            // and the (real) link time is waited out for them
+            int budget = bs->sc.drain_budget;
+            while (budget > 0 && !bs->queued_prefetches.empty() && bs->queued_prefetches.front().enqueue_step < step) {
+                const asg_blockset::QueuedPrefetch q = bs->queued_prefetches.front();
+                bs->queued_prefetches.pop_front();
+                for (int spins = 0; spins < 200000; ++spins) {
+                    int32_t n = 0;
+                    ok(asg_tier_drain_ready(bs->store, bs->sc.drain_budget, &n));
+                    asg_entry_view v{};
+                    ok(asg_tier_inspect(bs->store, q.block_id.c_str(), q.role, &v));
+                    if (!v.staged_pending && !v.staged_ready) break;
+                    std::this_thread::sleep_for(std::chrono::microseconds(50));
+                }
+                const Unit& u = bs->units[size_t(q.unit)];
+                emit(bs, step, ASG_EV_DRAIN, q.unit, u.fresh.installed_version, bs->now_us);
+                budget -= 1;
+            }
+        } else if (kind == ASG_HOOK_BACKWARD_PRE) {
+            for (size_t i = 0; i < bs->units.size(); ++i) {
+                const Unit& u = bs->units[i];
+                if (u.adamw || u.group < 0) continue;
+                const std::string id = unit_id(bs, int(i));
+                for (int side = 0; side < 2; ++side) {
+                    const int32_t role = is_soap(bs) ? (side == 0 ? ASG_ROLE_BASIS_L : ASG_ROLE_BASIS_R)
+                                                     : (side == 0 ? ASG_ROLE_INV_L : ASG_ROLE_INV_R);
+                    int32_t has = 0;
+                    ok(asg_tier_contains(bs->store, id.c_str(), role, &has));
+                    if (!has) continue;
+                    asg_entry_view v{};
+                    ok(asg_tier_inspect(bs->store, id.c_str(), role, &v));
+                    if (v.tier == ASG_TIER_COLD) {
+                        ok(asg_tier_prefetch(bs->store, id.c_str(), role, ASG_TIER_HOST, nullptr));
+                        bs->queued_prefetches.push_back({id, role, int(i), step});
+                        emit(bs, step, ASG_EV_PREFETCH, int64_t(i), u.version, bs->now_us);
+                    }
+                }
+            }
+        } else {
+            throw Fail{ASG_ERR_INVALID_ARGUMENT, "unknown hook kind"};
+        }
     });
 }
 

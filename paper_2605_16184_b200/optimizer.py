@@ -152,6 +152,20 @@ class AsteriaOptimizer:
         check(lib.asg_blockset_state_bytes(self._h, C.byref(b)))
         return b.value
 
+    def attach_store(self, store):
+        """F3: mirror every scheduler install's refreshed inverse state into a
+        ``tierstore.TierStore`` (Host tier, prefetched toward Hot), as the
+        reference's ShadowScheduler does with its store (asyncsched.cpp:164-184).
+        The store must outlive the optimizer or be detached with ``None``."""
+        self._store = store
+        check(lib.asg_blockset_attach_store(self._h, store._h if store is not None else None))
+
+    def on_hook(self, kind, step):
+        """on_hook(ForwardPost / BackwardPre / StepEnd) asyncsched.cpp:223-286:
+        ``abi.HOOK_FORWARD_POST`` drains staged transfers, ``abi.HOOK_BACKWARD_PRE``
+        prefetches Cold inverse state to Host."""
+        check(lib.asg_on_hook(self._h, kind, step))
+
     def workspace_bytes(self):
         b = C.c_uint64()
         check(lib.asg_blockset_workspace_bytes(self._h, C.byref(b)))

@@ -40,6 +40,29 @@ _SIGS = {
     "asg_blockset_block_info": (C.c_int, [_vp, _i64, _P(abi.BlockInfo)]),
     "asg_blockset_state_bytes": (C.c_int, [_vp, _P(_u64)]),
     "asg_blockset_workspace_bytes": (C.c_int, [_vp, _P(_u64)]),
+    "asg_store_config_defaults": (C.c_int, [_P(abi.StoreConfig)]),
+    "asg_tierstore_create": (C.c_int, [_P(abi.StoreConfig), _P(_vp)]),
+    "asg_tierstore_destroy": (C.c_int, [_vp]),
+    "asg_tier_put": (C.c_int, [_vp, C.c_char_p, _i32, _vp, _u64, _i32, _P(abi.EntryView)]),
+    "asg_tier_put_device": (C.c_int, [_vp, C.c_char_p, _i32, _vp, _u64, _i32, _P(abi.EntryView)]),
+    "asg_tier_get": (C.c_int, [_vp, C.c_char_p, _i32, _vp, _u64, _P(_u64), _P(_i32)]),
+    "asg_tier_device_ptr": (C.c_int, [_vp, C.c_char_p, _i32, _P(_vp)]),
+    "asg_tier_demote": (C.c_int, [_vp, C.c_char_p, _i32, _i32]),
+    "asg_tier_promote": (C.c_int, [_vp, C.c_char_p, _i32, _i32]),
+    "asg_tier_reclaim": (C.c_int, [_vp, C.c_char_p, _i32, _P(_u64)]),
+    "asg_tier_flush": (C.c_int, [_vp, C.c_char_p, _i32]),
+    "asg_tier_pin": (C.c_int, [_vp, C.c_char_p, _i32]),
+    "asg_tier_unpin": (C.c_int, [_vp, C.c_char_p, _i32]),
+    "asg_tier_prefetch": (C.c_int, [_vp, C.c_char_p, _i32, _i32, _P(_u64)]),
+    "asg_tier_drain_ready": (C.c_int, [_vp, _i32, _P(_i32)]),
+    "asg_tier_advance_step": (C.c_int, [_vp, _i64]),
+    "asg_tier_contains": (C.c_int, [_vp, C.c_char_p, _i32, _P(_i32)]),
+    "asg_tier_inspect": (C.c_int, [_vp, C.c_char_p, _i32, _P(abi.EntryView)]),
+    "asg_tier_gauges": (C.c_int, [_vp, _P(abi.Residency)]),
+    "asg_tier_counters": (C.c_int, [_vp, _P(abi.IoCounters)]),
+    "asg_tier_audit": (C.c_int, [_vp]),
+    "asg_blockset_attach_store": (C.c_int, [_vp, _vp]),
+    "asg_on_hook": (C.c_int, [_vp, _i32, _i64]),
     "asg_blockset_stream": (C.c_int, [_vp, _P(_vp)]),
     "asg_grad_sqnorm": (C.c_int, [_vp, _vp, _P(_f64), _P(_i32)]),
     "asg_accumulate": (C.c_int, [_vp, _f64, _vp]),

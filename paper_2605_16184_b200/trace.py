@@ -18,7 +18,7 @@ from . import abi
 
 EVENT_NAMES = {abi.EV_DISPATCH: "dispatch", abi.EV_JOB_START: "job_start", abi.EV_JOB_DONE: "job_done",
                abi.EV_INSTALL: "install", abi.EV_BARRIER_WAIT_BEGIN: "barrier_wait_begin",
-               abi.EV_BARRIER_WAIT_END: "barrier_wait_end"}
+               abi.EV_BARRIER_WAIT_END: "barrier_wait_end", abi.EV_PREFETCH: "prefetch", abi.EV_DRAIN: "drain"}
 
 
 def block_id(spec, param_names=None):
