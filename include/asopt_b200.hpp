@@ -34,6 +34,7 @@
 // Link with -lasteria_b200 (paper_2605_16184_b200/csrc/build/).
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -59,6 +60,10 @@ struct MissingKeyError : Error { using Error::Error; };
 struct WorkerPoolDownError : Error { using Error::Error; };
 struct ConfigInvalidError : Error { using Error::Error; };
 struct AuditError : Error { using Error::Error; };
+struct CapacityExhaustedError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
+struct PinnedEntryError : Error { using Error::Error; };
+struct DirtyNotPersistedError : Error { using Error::Error; };
 // GPU-layer failures (no reference counterpart)
 struct DeviceError : Error { using Error::Error; };
 
@@ -76,6 +81,10 @@ inline void check(int rc) {
         case ASG_ERR_CONFIG_INVALID: throw ConfigInvalidError(msg);
         case ASG_ERR_AUDIT: throw AuditError(msg);
         case ASG_ERR_MISSING_KEY: throw MissingKeyError(msg);
+        case ASG_ERR_CAPACITY_EXHAUSTED: throw CapacityExhaustedError(msg);
+        case ASG_ERR_IO: throw IoError(msg);
+        case ASG_ERR_PINNED_ENTRY: throw PinnedEntryError(msg);
+        case ASG_ERR_DIRTY_NOT_PERSISTED: throw DirtyNotPersistedError(msg);
         default: throw DeviceError(msg);
     }
 }
@@ -467,6 +476,120 @@ inline Matd unpack_spd(const std::vector<double>& p, int64_t n) {
         for (int64_t j = 0; j <= i; ++j, ++k) m(i, j) = m(j, i) = p[size_t(k)];
     return m;
 }
+
+// ---- tiered store (tierstore.hpp:71-114, tiers.hpp) ------------------------
+enum class TierTag { Hot = ASG_TIER_HOT, Host = ASG_TIER_HOST, Cold = ASG_TIER_COLD };
+enum class TensorRole : int32_t {
+    FactorL = ASG_ROLE_FACTOR_L, FactorR = ASG_ROLE_FACTOR_R, InvFactorL = ASG_ROLE_INV_L,
+    InvFactorR = ASG_ROLE_INV_R, BasisL = ASG_ROLE_BASIS_L, BasisR = ASG_ROLE_BASIS_R,
+    RotatedM = ASG_ROLE_ROTATED_M, RotatedV = ASG_ROLE_ROTATED_V
+};
+struct TierKey {
+    std::string block_id;
+    TensorRole role;
+};
+struct StoreConfig {
+    uint64_t hot_capacity_bytes = 1ull << 30;
+    uint64_t host_capacity_bytes = 1ull << 30;
+    std::string cold_path;
+    double transfer_bandwidth_bytes_per_sec = 0.0;
+    uint64_t transfer_latency_us = 0;
+    int hot_device = -1;  // B200: the Hot tier's CUDA device (-1: host memory)
+};
+struct EntryView {
+    TierTag tier = TierTag::Cold;
+    uint64_t bytes = 0;
+    bool dirty = false, pinned = false;
+    int64_t last_touch_step = 0;
+    bool staged_pending = false, staged_ready = false;
+};
+
+class TierStore {
+  public:
+    explicit TierStore(StoreConfig cfg) : cfg_(std::move(cfg)) {
+        asg_store_config c;
+        check(asg_store_config_defaults(&c));
+        c.hot_capacity_bytes = cfg_.hot_capacity_bytes;
+        c.host_capacity_bytes = cfg_.host_capacity_bytes;
+        c.cold_path = cfg_.cold_path.c_str();
+        c.transfer_bandwidth_bytes_per_sec = cfg_.transfer_bandwidth_bytes_per_sec;
+        c.transfer_latency_us = cfg_.transfer_latency_us;
+        c.hot_device = cfg_.hot_device;
+        check(asg_tierstore_create(&c, &h_));
+    }
+    ~TierStore() {
+        if (h_) asg_tierstore_destroy(h_);
+    }
+    TierStore(const TierStore&) = delete;
+    TierStore& operator=(const TierStore&) = delete;
+
+    EntryView put(const TierKey& k, const std::vector<std::byte>& bytes, TierTag tier) {
+        asg_entry_view v;
+        check(asg_tier_put(h_, k.block_id.c_str(), int32_t(k.role), bytes.data(), bytes.size(), int32_t(tier), &v));
+        return view(v);
+    }
+    std::pair<std::vector<std::byte>, TierTag> get(const TierKey& k) {
+        asg_entry_view v;
+        check(asg_tier_inspect(h_, k.block_id.c_str(), int32_t(k.role), &v));
+        std::vector<std::byte> out(v.bytes);
+        uint64_t n = 0;
+        int32_t t = 0;
+        check(asg_tier_get(h_, k.block_id.c_str(), int32_t(k.role), out.data(), out.size(), &n, &t));
+        return {std::move(out), TierTag(t)};
+    }
+    void demote(const TierKey& k, TierTag to) { check(asg_tier_demote(h_, k.block_id.c_str(), int32_t(k.role), int32_t(to))); }
+    void promote(const TierKey& k, TierTag to) { check(asg_tier_promote(h_, k.block_id.c_str(), int32_t(k.role), int32_t(to))); }
+    uint64_t reclaim(const TierKey& k) {
+        uint64_t f = 0;
+        check(asg_tier_reclaim(h_, k.block_id.c_str(), int32_t(k.role), &f));
+        return f;
+    }
+    void flush(const TierKey& k) { check(asg_tier_flush(h_, k.block_id.c_str(), int32_t(k.role))); }
+    void pin(const TierKey& k) { check(asg_tier_pin(h_, k.block_id.c_str(), int32_t(k.role))); }
+    void unpin(const TierKey& k) { check(asg_tier_unpin(h_, k.block_id.c_str(), int32_t(k.role))); }
+    uint64_t prefetch(const TierKey& k, TierTag to) {
+        uint64_t t = 0;
+        check(asg_tier_prefetch(h_, k.block_id.c_str(), int32_t(k.role), int32_t(to), &t));
+        return t;
+    }
+    int drain_ready(int max_items) {
+        int32_t n = 0;
+        check(asg_tier_drain_ready(h_, max_items, &n));
+        return n;
+    }
+    void advance_step(int64_t step) { check(asg_tier_advance_step(h_, step)); }
+    bool contains(const TierKey& k) const {
+        int32_t o = 0;
+        check(asg_tier_contains(h_, k.block_id.c_str(), int32_t(k.role), &o));
+        return o != 0;
+    }
+    EntryView inspect(const TierKey& k) const {
+        asg_entry_view v;
+        check(asg_tier_inspect(h_, k.block_id.c_str(), int32_t(k.role), &v));
+        return view(v);
+    }
+    asg_residency gauges() const {
+        asg_residency g;
+        check(asg_tier_gauges(h_, &g));
+        return g;
+    }
+    asg_io_counters counters() const {
+        asg_io_counters c;
+        check(asg_tier_counters(h_, &c));
+        return c;
+    }
+    const StoreConfig& config() const { return cfg_; }
+    void audit() const { check(asg_tier_audit(h_)); }
+    asg_tierstore* handle() const { return h_; }
+
+  private:
+    static EntryView view(const asg_entry_view& v) {
+        return EntryView{TierTag(v.tier), v.bytes, v.dirty != 0, v.pinned != 0, v.last_touch_step,
+                         v.staged_pending != 0, v.staged_ready != 0};
+    }
+    StoreConfig cfg_;
+    asg_tierstore* h_ = nullptr;
+};
 
 }  // namespace b200
 }  // namespace asopt

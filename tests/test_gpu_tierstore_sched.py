@@ -47,7 +47,7 @@ def test_installs_write_back_to_the_store_and_drain_to_hbm(tmp_path, method, ref
     kinds = [e.kind for e in o.events()]
     assert abi.EV_PREFETCH in kinds and abi.EV_DRAIN in kinds
     # the store holds each block's installed inverse state, byte-exact: (hi | lo) padded fp32 slabs
-    nb = o.num_blocks()
+    nb = o.num_blocks
     for i in range(nb):
         bid = _bid(o, i)
         for side, role in enumerate(roles):
@@ -59,14 +59,20 @@ def test_installs_write_back_to_the_store_and_drain_to_hbm(tmp_path, method, ref
             D = int(np.sqrt(len(payload) // 8))  # hi and lo slabs of D x D fp32
             a = np.frombuffer(payload, dtype=np.float32).reshape(2, D, D).astype(np.float64)
             np.testing.assert_array_equal((a[0] + a[1])[:d, :d], ref)
-    # demote everything to Cold: BackwardPre re-prefetches, ForwardPost drains to Host
+    # a Cold entry: BackwardPre re-prefetches it to Host, ForwardPost drains it
+    # (first let the install-time Hot prefetches land: a new prefetch of a key
+    # with a transfer in flight coalesces onto it, tierstore.cpp:298-302)
     bid = _bid(o, 0)
+    for k in range(1, 6):
+        o.on_hook(abi.HOOK_FORWARD_POST, steps + k)
+    v = store.inspect((bid, roles[0]))
+    assert v.tier == abi.TIER_HOT and not v.staged_pending and not v.staged_ready
     store.demote((bid, roles[0]), abi.TIER_COLD)
     n_ev = len(o.events())
-    o.on_hook(abi.HOOK_BACKWARD_PRE, steps)
+    o.on_hook(abi.HOOK_BACKWARD_PRE, steps + 6)
     new = [e.kind for e in o.events()[n_ev:]]
     assert new.count(abi.EV_PREFETCH) == 1
-    o.on_hook(abi.HOOK_FORWARD_POST, steps + 1)
+    o.on_hook(abi.HOOK_FORWARD_POST, steps + 7)
     assert store.inspect((bid, roles[0])).tier == abi.TIER_HOST
     store.audit()
     o.attach_store(None)
