@@ -532,24 +532,12 @@ def main():
     for s in wl["shapes"]:
         params.append((torch.randn(*s, device=dev, generator=gen) * 0.02).contiguous())
         grads.append(torch.zeros(*s, device=dev))
-    sigma = [1.0 / math.sqrt(s[-1]) for s in wl["shapes"]]
     o = AsteriaOptimizer(params, grads, opt, sched, precision=prec, rank=rank, world=world, seed=1234)
     stream = torch.cuda.ExternalStream(o.stream_handle)
-    # this rank's units (blocks, or whole 1-D AdamW parameters): it writes their gradients
-    owned = []
-    for i in range(o.num_blocks):
-        info = o.block_info(i)
-        if info.owner_rank == rank:
-            sp = info.spec
-            owned.append((i, sp.param_index, sp.row_begin, sp.row_end, sp.col_begin, sp.col_end))
-
     def synth(step):
-        """Fresh gradients of this rank's units: N(0, 1/cols), Philox keyed (1234, step, block)."""
-        for (i, p, r0, r1, c0, c1) in owned:
-            gen.manual_seed((1234 << 40) + (step << 20) + i)
-            g = grads[p]
-            view = g[r0:r1, c0:c1] if g.dim() == 2 else g[c0:c1]
-            view.normal_(0.0, sigma[p], generator=gen)
+        """Fresh gradients of this rank's units: N(0, 1/cols), Philox4x32-10 keyed
+        (1234, step, block): one fused launch over every owned block (asg_synth_gradients)."""
+        o.synth_gradients(1234, step)
 
     def one_step(step, fresh=True):
         if fresh and not args.fixed_grads:

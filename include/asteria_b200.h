@@ -539,6 +539,12 @@ int asg_blockset_attach_store(asg_blockset* bs, asg_tierstore* store);
 typedef enum asg_hook { ASG_HOOK_FORWARD_POST = 0, ASG_HOOK_BACKWARD_PRE = 1, ASG_HOOK_STEP_END = 2 } asg_hook;
 int asg_on_hook(asg_blockset* bs, int32_t kind, int64_t step);
 
+/* Benchmark input: overwrites the gradient slice of every unit
+ * this rank owns with N(0, 1/cols(param)) i.i.d. values from Philox4x32-10
+ * keyed (seed, step, unit) -- one launch on `stream` (NULL: the main stream).
+ * Not part of the optimizer step; the caller's gradient buffers are written. */
+int asg_synth_gradients(asg_blockset* bs, uint64_t seed, int64_t step, void* stream);
+
 /* ---- diagnostics: the tensor-core GEMM on its own ----------------------- */
 /* C[b] = alpha * A[b] * B[b]^T + beta * C[b] for b < batch, fp32 device
  * slabs: A is [batch][M][K], B is [batch][N][K], C is [batch][M][N]

@@ -92,6 +92,7 @@ struct GemmParams {
     int64_t ldt;          // EPI_SPLIT2: leading dimension of D^T (batch stride d_bstride)
     float ns_a, ns_b;
     unsigned int* resid;  // EPI_NS: per batch max|M - I| (float bits, atomicMax)
+    int raster;           // rectangular schedules: 0 row-major tiles, 1 column-major
     int sym_T;            // CTA-pair symmetric schedules: T x T tile grid, lower triangle decoded
                           // arithmetically (tile_list unused)
 };
@@ -140,8 +141,14 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& b, 
         tm = c.x;
         tn = c.y;
     } else {
-        tm = l / p.tiles_n;
-        tn = l - tm * p.tiles_n;
+        if (p.raster == 1) {  // column-major: consecutive tiles share the B panel
+            const int tiles_m = p.tiles_per_batch / p.tiles_n;
+            tn = l / tiles_m;
+            tm = l - tn * tiles_m;
+        } else {
+            tm = l / p.tiles_n;
+            tn = l - tm * p.tiles_n;
+        }
     }
 }
 

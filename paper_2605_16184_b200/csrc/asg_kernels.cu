@@ -207,6 +207,8 @@ cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStr
     p.batch = g.batch;
     p.tiles_n = N / bn;
     p.sym_T = 0;
+    static const int raster = getenv("ASG_GEMM_RASTER") ? atoi(getenv("ASG_GEMM_RASTER")) : 0;  // tuning
+    p.raster = raster;
     if (g.sym_tiles && pair) {
         const int T = N / 256;
         p.tile_list = nullptr;
@@ -1133,6 +1135,61 @@ void launch_unpack_scaled(const BlockRef* blocks_dev, const int64_t* offsets_dev
 void launch_unpack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, const float* in,
                           cudaStream_t s) {
     if (nb > 0) unpack_kernel<<<dim3(64, nb), 256, 0, s>>>(blocks_dev, offsets_dev, in);
+    count_launch();
+}
+
+
+// ============================================================================
+// Synthetic gradients: block b at step t is N(0, sigma_b^2)
+// i.i.d. from Philox4x32-10 keyed (seed, t, b), one launch for every block.
+// Benchmark input generation, not part of the optimizer step.
+// ============================================================================
+namespace {
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = c.x * 0xD2511F53u, hi0 = __umulhi(c.x, 0xD2511F53u);
+        const uint32_t lo1 = c.z * 0xCD9E8D57u, hi1 = __umulhi(c.z, 0xCD9E8D57u);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+__device__ __forceinline__ float u01(uint32_t x) { return (float(x >> 8) + 0.5f) * (1.0f / 16777216.0f); }  // (0, 1)
+
+// grid (chunks of 1024 elements, blocks); each thread 4 consecutive elements of a row-major block view
+__global__ void synth_normal_kernel(const SynthBlock* __restrict__ blocks, uint64_t seed, uint64_t step) {
+    const SynthBlock b = blocks[blockIdx.y];
+    const int64_t n = int64_t(b.rows) * b.cols;
+    const uint2 key = make_uint2(uint32_t(seed) ^ uint32_t(step * 0x9E3779B97F4A7C15ull),
+                                 uint32_t(seed >> 32) ^ uint32_t((step * 0x9E3779B97F4A7C15ull) >> 32));
+    for (int64_t e0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4; e0 < n;
+         e0 += int64_t(gridDim.x) * blockDim.x * 4) {
+        const uint4 r = philox4x32_10(make_uint4(uint32_t(e0 >> 2), uint32_t(e0 >> 34), uint32_t(b.key), 0u), key);
+        const float r1 = sqrtf(-2.f * __logf(u01(r.x))), r2 = sqrtf(-2.f * __logf(u01(r.z)));
+        float s1, c1, s2, c2;
+        __sincosf(6.2831853f * u01(r.y), &s1, &c1);
+        __sincosf(6.2831853f * u01(r.w), &s2, &c2);
+        const float z[4] = {r1 * c1, r1 * s1, r2 * c2, r2 * s2};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t e = e0 + j;
+            if (e < n) {
+                const int64_t i = e / b.cols, c = e - i * b.cols;
+                b.dst[i * b.ld + c] = b.sigma * z[j];
+            }
+        }
+    }
+}
+}  // namespace
+
+void launch_synth_normal(const SynthBlock* blocks_dev, int nb, int64_t max_elems, uint64_t seed, uint64_t step,
+                         cudaStream_t s) {
+    if (nb <= 0 || max_elems <= 0) return;
+    const int64_t chunks = (max_elems + 1023) / 1024;
+    const int gx = int(chunks < 4096 ? chunks : 4096);
+    synth_normal_kernel<<<dim3(gx, nb), 256, 0, s>>>(blocks_dev, seed, step);
     count_launch();
 }
 

@@ -162,4 +162,15 @@ void launch_unpack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev
 void launch_unpack_scaled(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, const float* in,
                           float scale, cudaStream_t s);
 
+// Synthetic N(0, sigma^2) gradients into block views, Philox4x32-10 keyed (seed, step, key).
+struct SynthBlock {
+    float* dst;
+    int64_t ld;
+    int32_t rows, cols;
+    float sigma;
+    uint32_t key;
+};
+void launch_synth_normal(const SynthBlock* blocks_dev, int nb, int64_t max_elems, uint64_t seed, uint64_t step,
+                         cudaStream_t s);
+
 }  // namespace asg

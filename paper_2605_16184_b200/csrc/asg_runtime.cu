@@ -239,6 +239,10 @@ struct asg_blockset {
         int64_t enqueue_step;
     };
     std::deque<QueuedPrefetch> queued_prefetches;
+    // asg_synth_gradients: this rank's unit gradient views (bench input generation)
+    asg::SynthBlock* d_synth = nullptr;
+    int n_synth = 0;
+    int64_t synth_max = 0;
     size_t alloc_bytes = 0;      // every device allocation of the blockset
     size_t workspace_bytes = 0;  // of which: refresh / install workspace (alloc_workspace)
     std::vector<void*> host_allocs;
@@ -515,12 +519,20 @@ void alloc_group(asg_blockset* bs, Group& g) {
     g.Gh = dalloc<float>(bs, nb * slabMN(g));
     g.GTh = dalloc<float>(bs, nb * slabMN(g));
     g.Th = dalloc<float>(bs, nb * slabMN(g));
-    g.Sh = dalloc<float>(bs, nb * slabMN(g));
     if (sp) {
         g.Gl = dalloc<float>(bs, nb * slabMN(g));
         g.GTl = dalloc<float>(bs, nb * slabMN(g));
         g.Tl = dalloc<float>(bs, nb * slabMN(g));
-        g.Sl = dalloc<float>(bs, nb * slabMN(g));
+    }
+    // S: SOAP's Adam output; KL-Shampoo's V^T, which aliases G (G is dead once
+    // W = G P_R is formed; the update recomputes V from G^T, group_update);
+    // Shampoo has no use for it
+    if (is_soap(bs)) {
+        g.Sh = dalloc<float>(bs, nb * slabMN(g));
+        if (sp) g.Sl = dalloc<float>(bs, nb * slabMN(g));
+    } else if (is_kl(bs)) {
+        g.Sh = g.Gh;
+        g.Sl = g.Gl;
     }
     auto pair_mm = [&](float*& h, float*& l) {
         h = dalloc<float>(bs, nb * slabMM(g));
@@ -653,17 +665,21 @@ void alloc_workspace(asg_blockset* bs) {
     for (const Group& g : bs->groups) maxnb = std::max(maxnb, g.nb);
     bs->ws_chunk = std::min(chunk, std::max(1, maxnb));
     bs->ws_n = nmax;
-    const size_t nn = size_t(nmax) * nmax * size_t(bs->ws_chunk);
+    // NEWTON refresh: the fp64 buffers only stage single-block parity I/O
+    // (asg_block_read / asg_block_write), so they hold one block, not a chunk
+    const size_t nn = size_t(nmax) * nmax * size_t(newton_roots(bs) ? 1 : bs->ws_chunk);
     bs->ws_snap = dalloc<double>(bs, nn);
     bs->ws_vecs = dalloc<double>(bs, nn);
     size_t ew = nn;
-    for (const Group& g : bs->groups) {
-        ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.m));
-        ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.n));
-    }
-    for (const Group& g : bs->groups) {
-        ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.m));
-        ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.n));
+    if (!newton_roots(bs)) {
+        for (const Group& g : bs->groups) {
+            ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.m));
+            ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.n));
+        }
+        for (const Group& g : bs->groups) {
+            ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.m));
+            ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.n));
+        }
     }
     bs->ws_work = dalloc<double>(bs, ew);
     bs->ws_W = dalloc<double>(bs, nn);
@@ -2535,6 +2551,38 @@ int asg_step_end(asg_blockset* bs, int64_t step) {
             const int rc = asg_tier_advance_step(bs->store, step);
             if (rc != ASG_OK) throw Fail{rc, asg_last_error()};
         }
+    });
+}
+
+// Synthetic gradients of this rank's units (benchmark input):
+// unit u's gradient slice <- N(0, 1/cols(param)) i.i.d., Philox keyed (seed, step, u).
+int asg_synth_gradients(asg_blockset* bs, uint64_t seed, int64_t step, void* stream) {
+    return guard([&] {
+        if (!bs) throw Fail{ASG_ERR_INVALID_ARGUMENT, "null blockset"};
+        CK(cudaSetDevice(bs->device));
+        if (!bs->d_synth) {
+            std::vector<SynthBlock> v;
+            for (size_t i = 0; i < bs->units.size(); ++i) {
+                const Unit& u = bs->units[i];
+                if (u.owner != bs->rank) continue;
+                const asg_param_desc& d = bs->params[size_t(u.spec.param_index)];
+                if (!d.grad) continue;
+                const int64_t r0 = u.spec.row_begin, r1 = u.spec.row_end, c0 = u.spec.col_begin, c1 = u.spec.col_end;
+                SynthBlock b{const_cast<float*>(d.grad) + r0 * d.ld_grad + c0, d.ld_grad, int32_t(r1 - r0),
+                             int32_t(c1 - c0), float(1.0 / std::sqrt(double(d.cols))), uint32_t(i)};
+                bs->synth_max = std::max<int64_t>(bs->synth_max, int64_t(b.rows) * b.cols);
+                v.push_back(b);
+            }
+            bs->n_synth = int(v.size());
+            if (!v.empty()) {
+                bs->d_synth = dalloc<SynthBlock>(bs, v.size());
+                h2d(bs->d_synth, v.data(), v.size() * sizeof(SynthBlock), bs->main);
+                CK(cudaStreamSynchronize(bs->main));
+            }
+        }
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
+        launch_synth_normal(bs->d_synth, bs->n_synth, bs->synth_max, seed, uint64_t(step), s);
+        CK(cudaGetLastError());
     });
 }
 

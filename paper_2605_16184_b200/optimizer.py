@@ -166,6 +166,11 @@ class AsteriaOptimizer:
         prefetches Cold inverse state to Host."""
         check(lib.asg_on_hook(self._h, kind, step))
 
+    def synth_gradients(self, seed, step, stream=None):
+        """Benchmark input: this rank's gradient slices <- N(0, 1/cols) from Philox keyed
+        (seed, step, unit), one launch (asg_synth_gradients)."""
+        check(lib.asg_synth_gradients(self._h, seed, step, stream_arg(stream)))
+
     def workspace_bytes(self):
         b = C.c_uint64()
         check(lib.asg_blockset_workspace_bytes(self._h, C.byref(b)))

@@ -63,6 +63,7 @@ _SIGS = {
     "asg_tier_audit": (C.c_int, [_vp]),
     "asg_blockset_attach_store": (C.c_int, [_vp, _vp]),
     "asg_on_hook": (C.c_int, [_vp, _i32, _i64]),
+    "asg_synth_gradients": (C.c_int, [_vp, _u64, _i64, _vp]),
     "asg_blockset_stream": (C.c_int, [_vp, _P(_vp)]),
     "asg_grad_sqnorm": (C.c_int, [_vp, _vp, _P(_f64), _P(_i32)]),
     "asg_accumulate": (C.c_int, [_vp, _f64, _vp]),

@@ -282,3 +282,33 @@ def test_non_finite_update_leaves_theta_and_surfaces_at_sync(O):
     assert torch.isfinite(W).all()
     assert not torch.equal(W[4], before[4])
     o.synchronize()  # flag cleared once reported
+
+
+def test_synth_gradients_philox_statistics_and_determinism():
+    """asg_synth_gradients (the bench's input): every owned block
+    slice gets N(0, 1/cols) values, deterministic in (seed, step), fresh per
+    step, independent across blocks."""
+    import torch
+    from paper_2605_16184_b200 import abi, runtime
+    from paper_2605_16184_b200.optimizer import AsteriaOptimizer
+    opt = runtime.optimizer_defaults(abi.SHAMPOO)
+    opt.block_dim_limit = 256
+    W = [torch.zeros(512, 768, device="cuda"), torch.zeros(300, device="cuda")]
+    G = [torch.zeros_like(w) for w in W]
+    o = AsteriaOptimizer(W, G, opt, runtime.scheduler_defaults())
+    o.synth_gradients(1234, 7)
+    torch.cuda.synchronize()
+    a = G[0].clone()
+    assert abs(a.mean().item()) < 5e-3 and abs(a.std().item() * 768 ** 0.5 - 1.0) < 1e-2
+    b1 = G[1].clone()
+    assert abs(b1.std().item() * 300 ** 0.5 - 1.0) < 0.15
+    o.synth_gradients(1234, 7)
+    torch.cuda.synchronize()
+    assert torch.equal(G[0], a)                      # deterministic in (seed, step)
+    o.synth_gradients(1234, 8)
+    torch.cuda.synchronize()
+    assert (G[0] - a).abs().max().item() > 0.1      # fresh every step
+    blk = G[0][:256, :256], G[0][:256, 256:512]      # distinct blocks draw distinct streams
+    assert not torch.equal(blk[0], blk[1])
+    c = torch.corrcoef(torch.stack([blk[0].flatten(), blk[1].flatten()]))[0, 1].item()
+    assert abs(c) < 0.02
