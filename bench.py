@@ -169,14 +169,18 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
-def traffic_for(workload):
+def traffic_for(workload, precision="3xtf32"):
     """DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) per launch of
-    the dominant kernel, from the committed `ncu --set full` capture summary
-    (profiles/r01_traffic.json, written by profiles/ncu_traffic.py)."""
-    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if not os.path.exists(p):
-        return {"traffic": None}
-    d = json.load(open(p)).get(workload)
+    the dominant kernel, from the newest committed `ncu --set full` capture
+    summary (profiles/r02_traffic.json, else r01; written by profiles/ncu_traffic.py)."""
+    key = workload + ("_smem" if precision == "3xtf32_smem" else "")
+    d = None
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            d = json.load(open(p)).get(key)
+            if d:
+                break
     if not d:
         return {"traffic": None}
     return {"traffic": d["dram_bytes_per_launch"], "traffic_kernel": d["kernel"],
@@ -434,7 +438,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default=os.environ.get("ASG_WORKLOAD", "C3"), choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "3xtf32_smem", "tf32"],
+                    help="3xtf32: operands stored as (hi, lo) tf32 pairs; 3xtf32_smem: the same products, operands "
+                         "stored as plain fp32 and split in shared memory; tf32: one product")
     ap.add_argument("--refresh", default="newton", choices=["newton", "f32", "f64"],
                     help="refresh arithmetic: newton = Newton-Schulz roots for Shampoo/KL (SOAP: f32 eigensolve), "
                          "f32 = fp32-level tensor-core eigensolve, f64 = reference-tight fp64 eigensolve")
@@ -525,7 +531,7 @@ def main():
     # The cold first refresh (dispatched at step 0) must be installed before
     # timing: its barrier fires at step S+1, so warm up past it.
     args.warmup = max(args.warmup, wl["S"] + 2)
-    prec = abi.PREC_3XTF32 if args.precision == "3xtf32" else abi.PREC_TF32
+    prec = {"3xtf32": abi.PREC_3XTF32, "3xtf32_smem": abi.PREC_3XTF32_SMEM, "tf32": abi.PREC_TF32}[args.precision]
 
     gen = torch.Generator(device=dev).manual_seed(1234)
     params, grads = [], []
@@ -676,7 +682,7 @@ def main():
         "dtype": ("f32 (3xTF32 tensor-core products; " +
                   {"f32": "fp32-level refresh: tensor-core block Jacobi)",
                    "newton": "fp32-level refresh: Newton-Schulz roots (SOAP: tensor-core block Jacobi))",
-                   "f64": "fp64 refresh)"}[args.refresh] if prec == abi.PREC_3XTF32 else "tf32"),
+                   "f64": "fp64 refresh)"}[args.refresh] if prec != abi.PREC_TF32 else "tf32"),
         "data": "synthetic (fresh N(0, 1/cols) gradients every step, generated on the device; random-init parameters)",
         "config": cfg_out,
         "step_ms": {"p50": pct(per_step, 50), "p99": pct(per_step, 99),
@@ -689,9 +695,9 @@ def main():
                      "frac": (ach / peak) if ach else None,
                      "peak_note": f"{peak_src} dense bf16 (MEASURED_PEAKS.json bf16_tflops); tf32 kind = bf16/2, "
                                   f"3xTF32 issues 3 tf32 MMAs per algorithmic product",
-                     "frac_of_mode_peak": (ach / (peak / 2 / (3 if prec == abi.PREC_3XTF32 else 1))) if ach else None,
+                     "frac_of_mode_peak": (ach / (peak / 2 / (3 if prec != abi.PREC_TF32 else 1))) if ach else None,
                      "gemm_launches": ks.gemm_launches, "gemm_ms_per_step": ks.gemm_ms / args.steps,
-                     **traffic_for(args.workload)},
+                     **traffic_for(args.workload, args.precision)},
         "hbm_kernels": hbm_kernels,
         "gpu_launches": ks.launches,
         "clocks": clk.summary(),

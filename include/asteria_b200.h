@@ -71,7 +71,12 @@ typedef enum asg_accumulation { ASG_ACCUM_SUM = 0, ASG_ACCUM_EMA = 1 } asg_accum
 
 /* Arithmetic of the tensor-core GEMMs. 3xTF32 (hi/lo split, three tcgen05
  * kind::tf32 products) is fp32-faithful and is the parity mode. */
-typedef enum asg_precision { ASG_PREC_3XTF32 = 0, ASG_PREC_TF32 = 1 } asg_precision;
+typedef enum asg_precision {
+    ASG_PREC_3XTF32 = 0,     /* operands stored in HBM as (hi, lo) tf32 pairs */
+    ASG_PREC_TF32 = 1,
+    ASG_PREC_3XTF32_SMEM = 2 /* the same 3xTF32 products; operands stored as plain fp32 (half the
+                                bytes) and split into (hi, lo) in shared memory after the TMA load */
+} asg_precision;
 
 /* Tensor roles (tiers.hpp:35-44) plus the KL-Shampoo inverses and the
  * installed eigenvalues. */

@@ -93,6 +93,8 @@ struct GemmParams {
     float ns_a, ns_b;
     unsigned int* resid;  // EPI_NS: per batch max|M - I| (float bits, atomicMax)
     int raster;           // rectangular schedules: 0 row-major tiles, 1 column-major
+    int raw_out;          // 3xTF32: an output without a lo array stores the full fp32 value
+    int a_raw, b_raw;     // SPL kernels: operand given as plain fp32 (split in shared memory)
     int sym_T;            // CTA-pair symmetric schedules: T x T tile grid, lower triangle decoded
                           // arithmetically (tile_list unused)
 };
@@ -101,11 +103,27 @@ __device__ __forceinline__ bool batch_skipped(const GemmParams& p, int t) {
     return p.batch_active && p.batch_active[t / p.tiles_per_batch] == 0;
 }
 
+// An output operand value: a (hi, lo) tf32 pair when the lo array exists;
+// otherwise the full fp32 value in 3xTF32 mode (its consumer splits it in
+// shared memory, gemm_tn_kernel<..., SPL>) or its tf32 rounding in TF32 mode.
+__device__ __forceinline__ void out_split(const GemmParams& p, float x, float& hi, float& lo, bool has_lo) {
+    if (has_lo)
+        split_tf32(x, hi, lo);
+    else
+        hi = p.raw_out ? x : tf32_round(x);
+}
+
 // CG = 1: one CTA per 128 x BN tile. CG = 2: a CTA pair (cluster (2,1,1),
 // tcgen05 cta_group::2) per 256 x BN tile; each CTA stages 128 rows of A and
 // BN/2 rows of B, so the per-SM operand bytes (shared-memory reads of the
 // MMA, TMA writes) drop by a third at BN = 256 and the ring gets deeper.
-template <int BN, int NPASS, int CG = 1>
+// SPL (3xTF32 only): operands flagged raw (GemmParams::a_raw / b_raw) arrive
+// as plain fp32; four converter warps write each staged tile's lo part in
+// shared memory (the stage keeps its (hi, lo) layout; either operand may be
+// raw), so HBM holds and streams one fp32 per element. (A variant with a
+// deeper hi-only TMA ring and a separate 2-slot lo ring measured 1.4x slower
+// per launch: the conversion, not the load latency, sets the pace.)
+template <int BN, int NPASS, int CG = 1, bool SPL = false>
 struct GemmCfg {
     static constexpr int BM = 128;       // accumulator rows per CTA
     static constexpr int TM = 128 * CG;  // output tile rows
@@ -117,12 +135,16 @@ struct GemmCfg {
     static constexpr uint32_t kStageBytes = (kABytes + kBBytes) * (kSplit ? 2 : 1);
     // per-epilogue-warp 32 x 33 fp32 transpose scratch (coalesced apply)
     static constexpr int kEpiWarps = 8;
-    static constexpr int kThreads = 32 * (2 + kEpiWarps);
+    static constexpr int kConvWarps = SPL ? 4 : 0;  // warps 2 + kEpiWarps ...
+    static_assert(SPL == 0 || ((kABytes / 16) % 512 == 0 && (kBBytes / 16) % 512 == 0),
+                  "converter: whole 4 x 128-thread batches of 16-byte words");
+    static constexpr int kThreads = 32 * (2 + kEpiWarps + kConvWarps);
     static constexpr uint32_t kScratchBytes = kEpiWarps * 32 * 33 * 4;
-    static constexpr int kStagesRaw = (194 * 1024) / kStageBytes;
+    static constexpr int kStagesRaw = int((194 * 1024) / kStageBytes);
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr size_t kRingBytes = size_t(kStages) * kStageBytes;
     static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
-    static constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + 256 + kScratchBytes;
+    static constexpr size_t kSmemBytes = 1024 /*align slack*/ + kRingBytes + 256 + kScratchBytes;
     static_assert(kStages >= 2, "need at least two pipeline stages");
     static_assert(kTmemCols == 256 || kTmemCols == 512, "TMEM allocation must be a power of two");
 };
@@ -212,10 +234,10 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int r
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
             float4 h, l;
-            split_tf32(p.alpha * __uint_as_float(r[j + 0]), h.x, l.x);
-            split_tf32(p.alpha * __uint_as_float(r[j + 1]), h.y, l.y);
-            split_tf32(p.alpha * __uint_as_float(r[j + 2]), h.z, l.z);
-            split_tf32(p.alpha * __uint_as_float(r[j + 3]), h.w, l.w);
+            out_split(p, p.alpha * __uint_as_float(r[j + 0]), h.x, l.x, p.Dlo != nullptr);
+            out_split(p, p.alpha * __uint_as_float(r[j + 1]), h.y, l.y, p.Dlo != nullptr);
+            out_split(p, p.alpha * __uint_as_float(r[j + 2]), h.z, l.z, p.Dlo != nullptr);
+            out_split(p, p.alpha * __uint_as_float(r[j + 3]), h.w, l.w, p.Dlo != nullptr);
             *reinterpret_cast<float4*>(dh + j) = h;
             if (p.Dlo) *reinterpret_cast<float4*>(dl + j) = l;
         }
@@ -225,7 +247,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int r
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             float h, l;
-            split_tf32(p.alpha * __uint_as_float(r[j]), h, l);
+            out_split(p, p.alpha * __uint_as_float(r[j]), h, l, p.Dlo != nullptr);
             dh[int64_t(col0 + j) * p.ldd] = h;
             if (p.Dlo) dl[int64_t(col0 + j) * p.ldd] = l;
         }
@@ -251,7 +273,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int r
                 mp[e] = m;
                 vp[e] = v;
                 const float s = (m * p.inv_bc1) / (sqrtf(v * p.inv_bc2) + p.adam_eps);
-                split_tf32(s, hp[e], lp[e]);
+                out_split(p, s, hp[e], lp[e], p.Dlo != nullptr);
             }
             *reinterpret_cast<float4*>(mm + j) = m4;
             *reinterpret_cast<float4*>(vv + j) = v4;
@@ -318,7 +340,7 @@ __device__ __forceinline__ void rows_chunk(const GemmParams& p, int b, int row0,
 #pragma unroll 8
         for (int i = 0; i < 32; ++i) {
             float h, l;
-            split_tf32(scratch[i][lane], h, l);
+            out_split(p, scratch[i][lane], h, l, dl != nullptr);
             dh[int64_t(i) * p.ldd] = h;
             if (dl) dl[int64_t(i) * p.ldd] = l;
         }
@@ -329,7 +351,7 @@ __device__ __forceinline__ void rows_chunk(const GemmParams& p, int b, int row0,
 #pragma unroll 8
             for (int j = 0; j < 32; ++j) {
                 float h, l;
-                split_tf32(scratch[lane][j], h, l);
+                out_split(p, scratch[lane][j], h, l, tl != nullptr);
                 th[int64_t(j) * p.ldt] = h;
                 if (tl) tl[int64_t(j) * p.ldt] = l;
             }
@@ -393,7 +415,7 @@ __device__ __forceinline__ void adam_chunk(const GemmParams& p, int b, int row0,
             __stcs(mm + int64_t(h0 + i) * p.ldm, m);
             __stcs(vv + int64_t(h0 + i) * p.ldm, v);
             float h, l;
-            split_tf32((m * p.inv_bc1) / (sqrtf(v * p.inv_bc2) + p.adam_eps), h, l);
+            out_split(p, (m * p.inv_bc1) / (sqrtf(v * p.inv_bc2) + p.adam_eps), h, l, dl != nullptr);
             __stcs(dh + int64_t(h0 + i) * p.ldd, h);
             if (dl) __stcs(dl + int64_t(h0 + i) * p.ldd, l);
         }
@@ -422,12 +444,12 @@ __device__ __forceinline__ void sym_split_chunk(const GemmParams& p, int b, int 
     float res = 0.f;
     auto put = [&](int64_t off, float v, bool diag) {
         float h, l;
-        split_tf32(v, h, l);
+        out_split(p, v, h, l, ml != nullptr);
         mh[off] = h;
         if (ml) ml[off] = l;
         if constexpr (NS) {
             const float t = (diag ? p.ns_a : 0.f) - p.ns_b * v;
-            split_tf32(t, h, l);
+            out_split(p, t, h, l, tl != nullptr);
             th[off] = h;
             if (tl) tl[off] = l;
         }
@@ -458,27 +480,29 @@ __device__ __forceinline__ void sym_split_chunk(const GemmParams& p, int b, int 
     __syncwarp();
 }
 
-template <int BN, int NPASS, int EPI, int CG = 1>
-__global__ void __launch_bounds__(320, 1)
+template <int BN, int NPASS, int EPI, int CG = 1, bool SPL = false>
+__global__ void __launch_bounds__(SPL ? 448 : 320, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                    const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
                    const __grid_constant__ GemmParams p) {
-    using Cfg = GemmCfg<BN, NPASS, CG>;
+    using Cfg = GemmCfg<BN, NPASS, CG, SPL>;
+    static_assert(!SPL || NPASS == 3, "the shared-memory split serves 3xTF32 only");
     constexpr int BM = Cfg::BM, BK = Cfg::BK, STAGES = Cfg::kStages;
     constexpr bool SPLIT = Cfg::kSplit;
     constexpr bool PAIR = CG == 2;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * Cfg::kStageBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* conv = tempty + 2;  // SPL: stage converted (the leader's: one arrive per CTA)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + STAGES);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    float (*scratch)[33] = reinterpret_cast<float (*)[33]>(smem + size_t(STAGES) * Cfg::kStageBytes + 256 +
+    float (*scratch)[33] = reinterpret_cast<float (*)[33]>(smem + Cfg::kRingBytes + 256 +
                                                            size_t(warp >= 2 ? warp - 2 : 0) * 32 * 33 * 4);
     // CTA pair: rank within the pair, the pair's index and count (tiles are
     // walked per pair; both CTAs decode the same tile sequence)
@@ -486,6 +510,7 @@ __global__ void __launch_bounds__(320, 1)
     const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
     const int nunits = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
 
+    // stage s: (A hi, A lo, B hi, B lo)
     auto a_hi = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes; };
     auto a_lo = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes + Cfg::kABytes; };
     auto b_hi = [&](int s) { return smem + size_t(s) * Cfg::kStageBytes + (SPLIT ? 2 : 1) * Cfg::kABytes; };
@@ -512,6 +537,8 @@ __global__ void __launch_bounds__(320, 1)
                 // one arrive per epilogue warp (of both CTAs of a pair: the leader's barrier)
                 mbar_init(&tempty[a], Cfg::kEpiWarps * CG);
             }
+            if (SPL)
+                for (int s = 0; s < STAGES; ++s) mbar_init(&conv[s], CG);
             fence_mbar_init();
         }
         __syncwarp();
@@ -542,7 +569,15 @@ __global__ void __launch_bounds__(320, 1)
                 const int brow = tn * BN + int(rank) * Cfg::kBRows;
                 for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if constexpr (PAIR) {
+                    if constexpr (SPL) {
+                        // local barrier: this CTA's converter warps split the raw operands
+                        const uint32_t bytes = Cfg::kABytes * (p.a_raw ? 1 : 2) + Cfg::kBBytes * (p.b_raw ? 1 : 2);
+                        mbar_arrive_expect_tx(&full[stage], bytes);
+                        tma_load_3d(a_hi(stage), &tmAh, &full[stage], kb * BK, arow, b);
+                        tma_load_3d(b_hi(stage), &tmBh, &full[stage], kb * BK, brow, b);
+                        if (!p.a_raw) tma_load_3d(a_lo(stage), &tmAl, &full[stage], kb * BK, arow, b);
+                        if (!p.b_raw) tma_load_3d(b_lo(stage), &tmBl, &full[stage], kb * BK, brow, b);
+                    } else if constexpr (PAIR) {
                         // the leader's barrier expects both CTAs' bytes
                         if (rank == 0) mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes * 2);
                         const uint32_t fb = full0 + uint32_t(stage) * 8u;
@@ -581,7 +616,7 @@ __global__ void __launch_bounds__(320, 1)
                 tc_fence_after();
                 const uint32_t d = tmem_base + uint32_t(acc * BN);
                 for (int kb = 0; kb < num_k; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    mbar_wait(SPL ? &conv[stage] : &full[stage], phase);
                     tc_fence_after();
                     const uint64_t ah = umma_desc_k_sw128(a_hi(stage));
                     const uint64_t bh = umma_desc_k_sw128(b_hi(stage));
@@ -620,6 +655,61 @@ __global__ void __launch_bounds__(320, 1)
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (SPL && warp >= 2 + Cfg::kEpiWarps) {
+        // converters: x -> (hi, lo) in place for the raw operands of each stage
+        const int ct = threadIdx.x - 32 * (2 + Cfg::kEpiWarps);  // 0 .. 127
+        const uint32_t conv0 = PAIR ? mapa_shared(&conv[0], 0) : 0u;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = unit; t < p.num_tiles; t += nunits) {
+            if (batch_skipped(p, t)) continue;
+            for (int kb = 0; kb < num_k; ++kb) {
+                mbar_wait(&full[stage], phase);
+                // kind::tf32 reads the leading 19 bits of each operand word and drops
+                // the low 13 (measured: tools/tf32_probe.py), so the raw fp32 word
+                // already is the operand hi = trunc_tf32(x); only lo = rn_tf32(x - hi)
+                // is written (|lo| < ulp_tf32(x): x = hi + lo to 2^-22 relative)
+                auto split_region = [&](const uint8_t* hi, uint8_t* lo, uint32_t bytes) {
+                    const uint32_t h0 = smem_u32(hi), l0 = smem_u32(lo);
+                    // lo = rn_tf32(x - trunc_tf32(x)): integer round-half-away on the
+                    // magnitude bits (cvt.rna.tf32.f32 without its special-value checks)
+                    auto lo_of = [](uint32_t xb) {
+                        const float r = __uint_as_float(xb) - __uint_as_float(xb & 0xffffe000u);
+                        return (__float_as_uint(r) + 0x1000u) & 0xffffe000u;
+                    };
+                    // bytes / 16 is a multiple of 512: four 16-byte loads in flight per thread
+                    for (uint32_t i0 = ct; i0 < bytes / 16; i0 += 512) {
+                        uint32_t x[4][4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(x[u][0]), "=r"(x[u][1]), "=r"(x[u][2]), "=r"(x[u][3])
+                                         : "r"(h0 + (i0 + 128u * u) * 16u));
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(l0 + (i0 + 128u * u) * 16u),
+                                         "r"(lo_of(x[u][0])), "r"(lo_of(x[u][1])), "r"(lo_of(x[u][2])),
+                                         "r"(lo_of(x[u][3]))
+                                         : "memory");
+                    }
+                };
+                if (p.a_raw) split_region(a_hi(stage), a_lo(stage), Cfg::kABytes);
+                if (p.b_raw) split_region(b_hi(stage), b_lo(stage), Cfg::kBBytes);
+                // generic-proxy smem writes -> visible to the tensor core's async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (ct == 0) {
+                    if constexpr (PAIR)
+                        mbar_arrive_remote(conv0 + uint32_t(stage) * 8u);
+                    else
+                        mbar_arrive(&conv[stage]);
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }

@@ -67,11 +67,11 @@ bool make_map(CUtensorMap* map, const float* base, int K, int rows, int batch, i
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int NPASS, int EPI, int CG>
+template <int BN, int NPASS, int EPI, int CG, bool SPL>
 cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                         const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
-    using Cfg = GemmCfg<BN, NPASS, CG>;
-    auto kern = gemm_tn_kernel<BN, NPASS, EPI, CG>;
+    using Cfg = GemmCfg<BN, NPASS, CG, SPL>;
+    auto kern = gemm_tn_kernel<BN, NPASS, EPI, CG, SPL>;
     // the shared-memory limit is a per-device function attribute; so is the
     // number of CTA pairs that can be co-resident (GPCs with an odd SM count)
     static std::atomic<uint64_t> attr_set{0};
@@ -130,19 +130,19 @@ cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUte
     return cudaGetLastError();
 }
 
-template <int BN, int NPASS, int CG>
+template <int BN, int NPASS, int CG, bool SPL>
 cudaError_t dispatch_epi(int epi, const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                          const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
     switch (epi) {
-        case EPI_STORE: return launch_inst<BN, NPASS, EPI_STORE, CG>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SYM_EMA: return launch_inst<BN, NPASS, EPI_SYM_EMA, CG>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SPLIT: return launch_inst<BN, NPASS, EPI_SPLIT, CG>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SPLIT_T: return launch_inst<BN, NPASS, EPI_SPLIT_T, CG>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_ADAM: return launch_inst<BN, NPASS, EPI_ADAM, CG>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_APPLY: return launch_inst<BN, NPASS, EPI_APPLY, CG>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SYM_SPLIT: return launch_inst<BN, NPASS, EPI_SYM_SPLIT, CG>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_NS: return launch_inst<BN, NPASS, EPI_NS, CG>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SPLIT2: return launch_inst<BN, NPASS, EPI_SPLIT2, CG>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_STORE: return launch_inst<BN, NPASS, EPI_STORE, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SYM_EMA: return launch_inst<BN, NPASS, EPI_SYM_EMA, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT: return launch_inst<BN, NPASS, EPI_SPLIT, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT_T: return launch_inst<BN, NPASS, EPI_SPLIT_T, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_ADAM: return launch_inst<BN, NPASS, EPI_ADAM, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_APPLY: return launch_inst<BN, NPASS, EPI_APPLY, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SYM_SPLIT: return launch_inst<BN, NPASS, EPI_SYM_SPLIT, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_NS: return launch_inst<BN, NPASS, EPI_NS, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT2: return launch_inst<BN, NPASS, EPI_SPLIT2, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -188,19 +188,21 @@ cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStr
     if (pair && !g.sym_tiles && int64_t(g.batch) * (M / 256) * (N / bn) < int64_t(num_sms)) pair = false;
     const int tm_rows = pair ? 256 : 128;
     const int brows = pair ? bn / 2 : bn;
-    const bool split = precision == ASG_PREC_3XTF32;
+    const bool split = precision != ASG_PREC_TF32;  // 3XTF32 and 3XTF32_SMEM
+    // 3xTF32 operands without a lo array hold plain fp32: split in shared memory (SPL)
+    const bool a_raw = split && !g.A.lo, b_raw = split && !g.B.lo;
+    const bool spl = a_raw || b_raw;
     CUtensorMap ah, al, bh, bl;
     if (!make_map(&ah, g.A.hi, K, M, g.batch, 128)) return cudaErrorInvalidValue;
     if (!make_map(&bh, g.B.hi, K, N, g.batch, brows)) return cudaErrorInvalidValue;
-    if (split) {
-        if (!g.A.lo || !g.B.lo) return cudaErrorInvalidValue;
-        if (!make_map(&al, g.A.lo, K, M, g.batch, 128)) return cudaErrorInvalidValue;
-        if (!make_map(&bl, g.B.lo, K, N, g.batch, brows)) return cudaErrorInvalidValue;
-    } else {
-        al = ah;
-        bl = bh;
-    }
+    al = ah;
+    bl = bh;
+    if (split && !a_raw && !make_map(&al, g.A.lo, K, M, g.batch, 128)) return cudaErrorInvalidValue;
+    if (split && !b_raw && !make_map(&bl, g.B.lo, K, N, g.batch, brows)) return cudaErrorInvalidValue;
     GemmParams p = g.p;
+    p.raw_out = split ? 1 : 0;
+    p.a_raw = a_raw ? 1 : 0;
+    p.b_raw = b_raw ? 1 : 0;
     p.M = M;
     p.N = N;
     p.K = K;
@@ -222,18 +224,25 @@ cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStr
         p.tiles_per_batch = (M / tm_rows) * (N / bn);
     }
     p.num_tiles = p.tiles_per_batch * g.batch;
+    if (spl) {
+        if (pair)
+            return bn == 256 ? dispatch_epi<256, 3, 2, true>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                             : dispatch_epi<128, 3, 2, true>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+        return bn == 256 ? dispatch_epi<256, 3, 1, true>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                         : dispatch_epi<128, 3, 1, true>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+    }
     if (pair) {
         if (bn == 256)
-            return split ? dispatch_epi<256, 3, 2>(g.epi, ah, al, bh, bl, p, num_sms, stream)
-                         : dispatch_epi<256, 1, 2>(g.epi, ah, al, bh, bl, p, num_sms, stream);
-        return split ? dispatch_epi<128, 3, 2>(g.epi, ah, al, bh, bl, p, num_sms, stream)
-                     : dispatch_epi<128, 1, 2>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+            return split ? dispatch_epi<256, 3, 2, false>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                         : dispatch_epi<256, 1, 2, false>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+        return split ? dispatch_epi<128, 3, 2, false>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                     : dispatch_epi<128, 1, 2, false>(g.epi, ah, al, bh, bl, p, num_sms, stream);
     }
     if (bn == 256)
-        return split ? dispatch_epi<256, 3, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream)
-                     : dispatch_epi<256, 1, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream);
-    return split ? dispatch_epi<128, 3, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream)
-                 : dispatch_epi<128, 1, 1>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+        return split ? dispatch_epi<256, 3, 1, false>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                     : dispatch_epi<256, 1, 1, false>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+    return split ? dispatch_epi<128, 3, 1, false>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                 : dispatch_epi<128, 1, 1, false>(g.epi, ah, al, bh, bl, p, num_sms, stream);
 }
 
 // ============================================================================
@@ -915,6 +924,18 @@ void launch_square_f64(const double* a, double* out, int64_t n, cudaStream_t s) 
 // ============================================================================
 // fp32-level refresh (tensor-core transforms): split / transpose / scale
 // ============================================================================
+__global__ void merge_pair_kernel(const float* __restrict__ hi, const float* __restrict__ lo, float* __restrict__ dst,
+                                  int64_t count) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x)
+        dst[e] = hi[e] + lo[e];
+}
+
+void launch_merge_pair(const float* hi, const float* lo, float* dst, int64_t count, cudaStream_t s) {
+    const int64_t blocks = (count + 255) / 256;
+    merge_pair_kernel<<<int(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(hi, lo, dst, count);
+    count_launch();
+}
+
 __global__ void split_slab_kernel(const float* __restrict__ src, float* __restrict__ hi, float* __restrict__ lo,
                                   int64_t count) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x) {
@@ -963,7 +984,7 @@ __global__ void transpose_split_kernel(const float* __restrict__ src_hi, const f
     for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
         const int64_t off = b * slab + int64_t(c0 + dy) * R + r0 + threadIdx.x;
         float h, l;
-        split_tf32(t[threadIdx.x][dy], h, l);
+        pair_or_raw(t[threadIdx.x][dy], h, l, dst_lo != nullptr);
         dst_hi[off] = h;
         if (dst_lo) dst_lo[off] = l;
     }
@@ -982,7 +1003,7 @@ __global__ void square_split_kernel(const float* __restrict__ hi, const float* _
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x) {
         const float x = hi[e] + (lo ? lo[e] : 0.f);
         float h, l;
-        split_tf32(x * x, h, l);
+        pair_or_raw(x * x, h, l, ol != nullptr);
         oh[e] = h;
         if (ol) ol[e] = l;
     }
@@ -1021,7 +1042,7 @@ __global__ void scale_columns_split_kernel(const float* __restrict__ Vh, const f
             }
         }
         float h, l;
-        split_tf32(out, h, l);
+        pair_or_raw(out, h, l, Wl != nullptr);
         Wh[b * DD + idx] = h;
         if (Wl) Wl[b * DD + idx] = l;
     }
@@ -1061,7 +1082,7 @@ __global__ void ns_x_kernel(const float* S, int d, int D, float* Xh, float* __re
         float x = 0.f;
         if (i < d && j < d) x = (i == j ? 1.5f : 0.f) - 0.5f * S[b * DD + e];
         float h, l;
-        split_tf32(x, h, l);
+        pair_or_raw(x, h, l, Xl != nullptr);
         Xh[b * DD + e] = h;
         if (Xl) Xl[b * DD + e] = l;
     }
@@ -1158,38 +1179,37 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 }
 __device__ __forceinline__ float u01(uint32_t x) { return (float(x >> 8) + 0.5f) * (1.0f / 16777216.0f); }  // (0, 1)
 
-// grid (chunks of 1024 elements, blocks); each thread 4 consecutive elements of a row-major block view
+// grid (column quads / 256, rows, blocks): thread = 4 consecutive columns of
+// one row, Philox counter (quad, row, block key); one 16-byte store when the
+// row segment is aligned (no per-element index division)
 __global__ void synth_normal_kernel(const SynthBlock* __restrict__ blocks, uint64_t seed, uint64_t step) {
-    const SynthBlock b = blocks[blockIdx.y];
-    const int64_t n = int64_t(b.rows) * b.cols;
+    const SynthBlock b = blocks[blockIdx.z];
+    const int row = blockIdx.y;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;  // column quad
+    if (row >= b.rows || 4 * q >= b.cols) return;
     const uint2 key = make_uint2(uint32_t(seed) ^ uint32_t(step * 0x9E3779B97F4A7C15ull),
                                  uint32_t(seed >> 32) ^ uint32_t((step * 0x9E3779B97F4A7C15ull) >> 32));
-    for (int64_t e0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4; e0 < n;
-         e0 += int64_t(gridDim.x) * blockDim.x * 4) {
-        const uint4 r = philox4x32_10(make_uint4(uint32_t(e0 >> 2), uint32_t(e0 >> 34), uint32_t(b.key), 0u), key);
-        const float r1 = sqrtf(-2.f * __logf(u01(r.x))), r2 = sqrtf(-2.f * __logf(u01(r.z)));
-        float s1, c1, s2, c2;
-        __sincosf(6.2831853f * u01(r.y), &s1, &c1);
-        __sincosf(6.2831853f * u01(r.w), &s2, &c2);
-        const float z[4] = {r1 * c1, r1 * s1, r2 * c2, r2 * s2};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t e = e0 + j;
-            if (e < n) {
-                const int64_t i = e / b.cols, c = e - i * b.cols;
-                b.dst[i * b.ld + c] = b.sigma * z[j];
-            }
-        }
+    const uint4 r = philox4x32_10(make_uint4(uint32_t(q), uint32_t(row), b.key, 0u), key);
+    const float r1 = sqrtf(-2.f * __logf(u01(r.x))), r2 = sqrtf(-2.f * __logf(u01(r.z)));
+    float s1, c1, s2, c2;
+    __sincosf(6.2831853f * u01(r.y), &s1, &c1);
+    __sincosf(6.2831853f * u01(r.w), &s2, &c2);
+    const float4 z = make_float4(b.sigma * r1 * c1, b.sigma * r1 * s1, b.sigma * r2 * c2, b.sigma * r2 * s2);
+    float* d = b.dst + int64_t(row) * b.ld + 4 * q;
+    if (4 * q + 3 < b.cols && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+        *reinterpret_cast<float4*>(d) = z;
+    } else {
+        const float zz[4] = {z.x, z.y, z.z, z.w};
+        for (int j = 0; j < 4 && 4 * q + j < b.cols; ++j) d[j] = zz[j];
     }
 }
 }  // namespace
 
-void launch_synth_normal(const SynthBlock* blocks_dev, int nb, int64_t max_elems, uint64_t seed, uint64_t step,
-                         cudaStream_t s) {
-    if (nb <= 0 || max_elems <= 0) return;
-    const int64_t chunks = (max_elems + 1023) / 1024;
-    const int gx = int(chunks < 4096 ? chunks : 4096);
-    synth_normal_kernel<<<dim3(gx, nb), 256, 0, s>>>(blocks_dev, seed, step);
+void launch_synth_normal(const SynthBlock* blocks_dev, int nb, int max_rows, int max_cols, uint64_t seed,
+                         uint64_t step, cudaStream_t s) {
+    if (nb <= 0 || max_rows <= 0 || max_cols <= 0) return;
+    const int quads = (max_cols + 3) / 4;
+    synth_normal_kernel<<<dim3((quads + 255) / 256, max_rows, nb), 256, 0, s>>>(blocks_dev, seed, step);
     count_launch();
 }
 

@@ -131,6 +131,8 @@ void launch_square_f64(const double* a, double* out, int64_t n, cudaStream_t s);
 // fp32-level refresh helpers (tensor-core transforms of the refresh).
 // Elementwise hi/lo tf32 split of an fp32 array.
 void launch_split_slab(const float* src, float* hi, float* lo, int64_t count, cudaStream_t s);
+// dst = hi + lo (a pair stored as plain fp32, ASG_PREC_3XTF32_SMEM state).
+void launch_merge_pair(const float* hi, const float* lo, float* dst, int64_t count, cudaStream_t s);
 // [b][M][M] fp32 slab (leading m x m) -> [b][m][m] fp64, symmetrized (A + A^T)/2.
 void launch_snapshot_sym(const float* src, int nb, int M, int m, double* dst, cudaStream_t s);
 // dst[b] = split(op(src[b])^T) for [b][R][C] -> [b][C][R]; op = identity or
@@ -170,7 +172,7 @@ struct SynthBlock {
     float sigma;
     uint32_t key;
 };
-void launch_synth_normal(const SynthBlock* blocks_dev, int nb, int64_t max_elems, uint64_t seed, uint64_t step,
-                         cudaStream_t s);
+void launch_synth_normal(const SynthBlock* blocks_dev, int nb, int max_rows, int max_cols, uint64_t seed,
+                         uint64_t step, cudaStream_t s);
 
 }  // namespace asg

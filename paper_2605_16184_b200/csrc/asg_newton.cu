@@ -179,13 +179,13 @@ __global__ void ns_init_kernel(const float* __restrict__ A, int d, int D, const 
         // first X product is a scaling, written here instead of computed
         const float x = (in ? x0 : 1.f) * t;
         float h, l;
-        split_tf32(m, h, l);
+        pair_or_raw(m, h, l, Ml != nullptr);
         Mh[base + k] = h;
         if (Ml) Ml[base + k] = l;
-        split_tf32(t, h, l);
+        pair_or_raw(t, h, l, Tl != nullptr);
         Th[base + k] = h;
         if (Tl) Tl[base + k] = l;
-        split_tf32(x, h, l);
+        pair_or_raw(x, h, l, Xl != nullptr);
         Xh[base + k] = h;
         if (Xl) Xl[base + k] = l;
     }
@@ -386,8 +386,9 @@ __global__ void ns_finish_kernel(const float* __restrict__ X0h, const float* __r
     for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < DD; k += size_t(gridDim.x) * blockDim.x) {
         const int i = int(k / D), j = int(k - size_t(i) * D);
         const bool in = i < d && j < d;
-        outh[base + k] = in ? sh[base + k] : 0.f;
-        if (outl) outl[base + k] = in && sl ? sl[base + k] : 0.f;
+        const float h = in ? sh[base + k] : 0.f, l = in && sl ? sl[base + k] : 0.f;
+        outh[base + k] = outl ? h : h + l;  // no lo array: the full fp32 value (pair_or_raw)
+        if (outl) outl[base + k] = l;
     }
 }
 
@@ -403,7 +404,7 @@ __global__ void ns_damped_split_kernel(const float* __restrict__ A, int d, int D
         const int i = int(k / D), j = int(k - size_t(i) * D);
         const float a = (i < d && j < d) ? A[base + k] + (i == j ? e : 0.f) : 0.f;
         float h, l;
-        split_tf32(a, h, l);
+        pair_or_raw(a, h, l, Al != nullptr);
         Ah[base + k] = h;
         if (Al) Al[base + k] = l;
     }
@@ -432,7 +433,7 @@ __global__ void ns_refine_kernel(float* __restrict__ Xh, float* __restrict__ Xl,
         const float e = Eh[o] + (El ? El[o] : 0.f);
         const float x = Xh[o] + (Xl ? Xl[o] : 0.f) + (e + tt[r][threadIdx.x]) * inv2p;
         float h, l;
-        split_tf32(x, h, l);
+        pair_or_raw(x, h, l, Xl != nullptr);
         Xh[o] = h;
         if (Xl) Xl[o] = l;
     }
@@ -473,7 +474,7 @@ size_t ns_workspace_floats(int nb, int D) {
 void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps, int p, float* outh, float* outl,
                         float* ws, int* caller_status, const int2* sym_tiles, int nsym, int precision, int num_sms,
                         cudaStream_t s) {
-    const bool split = precision == ASG_PREC_3XTF32;
+    const bool split = precision != ASG_PREC_TF32;  // internal iterates: (hi, lo) pairs
     const size_t DD = size_t(D) * D, slab = size_t(nb) * DD;
     float* w = ws;
     auto take = [&](size_t n) {

@@ -221,5 +221,16 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
     hi = tf32_round(x);
     lo = tf32_round(x - hi);
 }
+// What an operand array stores: an exact (hi, lo) tf32 pair when its lo array
+// exists, otherwise the full fp32 value (3xTF32 consumers split it in shared
+// memory; TF32 consumers use its leading bits).
+__device__ __forceinline__ void pair_or_raw(float x, float& hi, float& lo, bool has_lo) {
+    if (has_lo) {
+        split_tf32(x, hi, lo);
+    } else {
+        hi = x;
+        lo = 0.f;
+    }
+}
 
 }  // namespace asg

@@ -242,7 +242,7 @@ struct asg_blockset {
     // asg_synth_gradients: this rank's unit gradient views (bench input generation)
     asg::SynthBlock* d_synth = nullptr;
     int n_synth = 0;
-    int64_t synth_max = 0;
+    int synth_rows = 0, synth_cols = 0;
     size_t alloc_bytes = 0;      // every device allocation of the blockset
     size_t workspace_bytes = 0;  // of which: refresh / install workspace (alloc_workspace)
     std::vector<void*> host_allocs;
@@ -384,7 +384,11 @@ void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 bool is_precond(const asg_blockset* bs) { return bs->opt.method != ASG_METHOD_ADAMW; }
 bool is_soap(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_SOAP; }
 bool is_kl(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_KL_SHAMPOO; }
+// operand slabs of the state hold (hi, lo) pairs (3XTF32); 3XTF32_SMEM keeps
+// them as plain fp32, split in shared memory by the GEMM (asg_gemm.cuh SPL)
 bool split_mode(const asg_blockset* bs) { return bs->precision == ASG_PREC_3XTF32; }
+// the refresh's internal tensor-core Jacobi works on (hi, lo) pairs in both 3xTF32 modes
+bool work_split(const asg_blockset* bs) { return bs->precision != ASG_PREC_TF32; }
 // F32 and NEWTON: fp32-level refresh (NEWTON: Newton-Schulz roots for Shampoo / KL)
 bool f32_refresh(const asg_blockset* bs) { return bs->sc.refresh_mode != ASG_REFRESH_F64; }
 bool newton_roots(const asg_blockset* bs) {
@@ -1392,8 +1396,8 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
     launch_relative_damping_f32(t[4], nb, D, d, bs->opt.damping, bs->ws_eps, s);
     int* st = nsides == 2 ? bs->pair_status : g.d_status + s0;
     if (nsides == 2) CK(cudaMemsetAsync(st, 0, size_t(nb) * sizeof(int), s));
-    float* t1 = sp ? t[1] : nullptr;
-    float* t3 = sp ? t[3] : nullptr;
+    float* t1 = work_split(bs) ? t[1] : nullptr;
+    float* t3 = work_split(bs) ? t[3] : nullptr;
     if (d > kSmallEighN && !bs->fp64_jacobi) {
         // tensor-core block Jacobi over all sides: J -> (t0, t1), J^T -> (t2, t3)
         // (Q J is re-orthonormalized below / at the SOAP install, so J itself is not)
@@ -1419,10 +1423,15 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
         const bool left = sd.left;
         const double* vals = bs->ws_vals + size_t(j) * cnt * d;
         if (is_soap(bs)) {
-            CK(cudaMemcpyAsync(at(left ? g.sJLTh : g.sJRTh, DD, s0), off(t[2], j), cntDD * 4, cudaMemcpyDeviceToDevice, s));
-            if (sp)
-                CK(cudaMemcpyAsync(at(left ? g.sJLTl : g.sJRTl, DD, s0), off(t[3], j), cntDD * 4,
+            if (sp || !t3) {
+                CK(cudaMemcpyAsync(at(left ? g.sJLTh : g.sJRTh, DD, s0), off(t[2], j), cntDD * 4,
                                    cudaMemcpyDeviceToDevice, s));
+                if (sp)
+                    CK(cudaMemcpyAsync(at(left ? g.sJLTl : g.sJRTl, DD, s0), off(t[3], j), cntDD * 4,
+                                       cudaMemcpyDeviceToDevice, s));
+            } else {  // 3XTF32_SMEM: the shadow rotation is stored as plain fp32 (hi + lo)
+                launch_merge_pair(off(t[2], j), off(t[3], j), at(left ? g.sJLTh : g.sJRTh, DD, s0), int64_t(cntDD), s);
+            }
             CK(cudaMemcpyAsync(at(left ? g.svalsL : g.svalsR, size_t(d), s0), vals, size_t(cnt) * d * 8,
                                cudaMemcpyDeviceToDevice, s));
             continue;
@@ -1436,7 +1445,7 @@ void refresh_sides_f32(asg_blockset* bs, Group& g, int s0, int cnt, int nsides, 
         p3.Dlo = Vl;
         p3.ldd = D;
         p3.d_bstride = int64_t(DD);
-        run_gemm(bs, op(sd.Qh, sd.Ql, D, D), op(off(t[2], j), sp ? off(t[3], j) : nullptr, D, D), cnt, EPI_SPLIT, p3,
+        run_gemm(bs, op(sd.Qh, sd.Ql, D, D), op(off(t[2], j), t3 ? off(t[3], j) : nullptr, D, D), cnt, EPI_SPLIT, p3,
                  nullptr, 0, s, 2.0 * dd3);
         // re-orthonormalize (the products drift at the fp32 level), straight into the basis
         if (needs_ns(bs, g, s0, cnt, false)) {
@@ -2155,6 +2164,7 @@ int asg_config_from_json(const char* text, asg_optimizer_config* opt, asg_schedu
             if (g.has("precision")) {
                 const std::string p = str(g, "precision");
                 if (p == "3xtf32") prec = ASG_PREC_3XTF32;
+                else if (p == "3xtf32_smem") prec = ASG_PREC_3XTF32_SMEM;
                 else if (p == "tf32") prec = ASG_PREC_TF32;
                 else throw Fail{ASG_ERR_CONFIG_INVALID, "unknown precision: " + p};
             }
@@ -2213,7 +2223,7 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         if (sched->pf != opt->precondition_frequency)
             throw Fail{ASG_ERR_CONFIG_INVALID, "async.pf must equal optimizer.precondition_frequency"};
         if (world < 1 || rank < 0 || rank >= world) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad rank/world"};
-        if (precision != ASG_PREC_3XTF32 && precision != ASG_PREC_TF32)
+        if (precision != ASG_PREC_3XTF32 && precision != ASG_PREC_TF32 && precision != ASG_PREC_3XTF32_SMEM)
             throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad precision"};
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
@@ -2570,7 +2580,8 @@ int asg_synth_gradients(asg_blockset* bs, uint64_t seed, int64_t step, void* str
                 const int64_t r0 = u.spec.row_begin, r1 = u.spec.row_end, c0 = u.spec.col_begin, c1 = u.spec.col_end;
                 SynthBlock b{const_cast<float*>(d.grad) + r0 * d.ld_grad + c0, d.ld_grad, int32_t(r1 - r0),
                              int32_t(c1 - c0), float(1.0 / std::sqrt(double(d.cols))), uint32_t(i)};
-                bs->synth_max = std::max<int64_t>(bs->synth_max, int64_t(b.rows) * b.cols);
+                bs->synth_rows = std::max(bs->synth_rows, int(b.rows));
+                bs->synth_cols = std::max(bs->synth_cols, int(b.cols));
                 v.push_back(b);
             }
             bs->n_synth = int(v.size());
@@ -2581,7 +2592,7 @@ int asg_synth_gradients(asg_blockset* bs, uint64_t seed, int64_t step, void* str
             }
         }
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : bs->main;
-        launch_synth_normal(bs->d_synth, bs->n_synth, bs->synth_max, seed, uint64_t(step), s);
+        launch_synth_normal(bs->d_synth, bs->n_synth, bs->synth_rows, bs->synth_cols, seed, uint64_t(step), s);
         CK(cudaGetLastError());
     });
 }
@@ -3212,7 +3223,9 @@ int asg_gemm_tn(const float* A, const float* B, float* C, int64_t batch, int64_t
         g.p.C = C;
         g.p.ldc = N;
         g.p.c_bstride = M * N;
-        CK(gemm_launch(g, precision, prop.multiProcessorCount, s));
+        // diagnostics: ASG_GEMM_REPEAT = k times the same product (kernel timing by difference)
+        static const int reps = getenv("ASG_GEMM_REPEAT") ? std::max(1, atoi(getenv("ASG_GEMM_REPEAT"))) : 1;
+        for (int r = 0; r < reps; ++r) CK(gemm_launch(g, precision, prop.multiProcessorCount, s));
         CK(cudaStreamSynchronize(s));
         for (void* p : {static_cast<void*>(Ah), static_cast<void*>(Al), static_cast<void*>(Bh), static_cast<void*>(Bl),
                         static_cast<void*>(scrA), static_cast<void*>(scrB), static_cast<void*>(dra), static_cast<void*>(drb)})

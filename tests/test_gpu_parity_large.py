@@ -224,7 +224,7 @@ def well_grad(rng, m, n, scale=1e-3):
 
 
 def big_trajectory(method, m, n, steps, pf, S, lr, accumulation, r, first_step=0, mode=abi.REFRESH_F32,
-                   adopt_basis=False):
+                   adopt_basis=False, precision=abi.PREC_3XTF32):
     """One block through AsteriaOptimizer (asg_step: the per-block call order
     of harness.cpp:448-475, S = 0: the refresh dispatched at step % pf == 0
     is installed by the same step's barrier) against orc_np's per-block
@@ -240,7 +240,7 @@ def big_trajectory(method, m, n, steps, pf, S, lr, accumulation, r, first_step=0
     th0 = 0.02 * rng.standard_normal((m, n))
     W = torch.tensor(th0, dtype=torch.float32, device="cuda")
     G = torch.zeros_like(W)
-    o = optimizer.AsteriaOptimizer([W], [G], opt, sched)
+    o = optimizer.AsteriaOptimizer([W], [G], opt, sched, precision=precision)
     nb = orc_np.Block(m, n, method)
     th = th0.copy()
     for step in range(first_step, first_step + steps):
@@ -264,23 +264,29 @@ def big_trajectory(method, m, n, steps, pf, S, lr, accumulation, r, first_step=0
     return err
 
 
+PRECS = [abi.PREC_3XTF32, abi.PREC_3XTF32_SMEM]
+
+
+@pytest.mark.parametrize("precision", PRECS)
 @pytest.mark.parametrize("mode", [abi.REFRESH_F32, abi.REFRESH_NEWTON])
-def test_c1_trajectory_shampoo_1024_pf1(rt, mode):
+def test_c1_trajectory_shampoo_1024_pf1(rt, mode, precision):
     """BASELINE C1: Shampoo on one 1024^2 block with the reference's
     quadratic_shampoo.json hyper-parameters (EMA b2 = 0.95, pf = 1, S = 0,
     lr 3e-3): a synchronous refresh every step."""
     assert big_trajectory(abi.SHAMPOO, 1024, 1024, steps=6, pf=1, S=0, lr=3e-3, accumulation=abi.EMA, r=5e-4,
-                          mode=mode) <= 1.0
+                          mode=mode, precision=precision) <= 1.0
 
 
+@pytest.mark.parametrize("precision", PRECS)
 @pytest.mark.parametrize("mode", [abi.REFRESH_F32, abi.REFRESH_NEWTON])
-def test_c3_block_trajectory_kl_shampoo_2048(rt, mode):
+def test_c3_block_trajectory_kl_shampoo_2048(rt, mode, precision):
     """One C3 block: KL-Shampoo on a 2048^2 block, pf = 2, S = 0."""
     assert big_trajectory(abi.KL_SHAMPOO, 2048, 2048, steps=5, pf=2, S=0, lr=1e-3, accumulation=abi.EMA,
-                          r=5e-4, mode=mode) <= 1.0
+                          r=5e-4, mode=mode, precision=precision) <= 1.0
 
 
-def test_c2_block_trajectory_soap_768x1024(rt):
+@pytest.mark.parametrize("precision", PRECS)
+def test_c2_block_trajectory_soap_768x1024(rt, precision):
     """One C2 block shape (768 x 1024, the c_attn / c_fc slices): SOAP,
     pf = 4, S = 0, steps 1-8 (the caller numbers the steps, harness.cpp:382):
     steps 1-3 are the identity-basis cold start (harness.cpp:458-461) and the
@@ -304,7 +310,7 @@ def test_c2_block_trajectory_soap_768x1024(rt):
     docstring); that case is covered for finiteness and orthonormality by
     test_f32_refresh_rank_deficient_factor."""
     assert big_trajectory(abi.SOAP, 768, 1024, steps=8, pf=4, S=0, lr=1e-3, accumulation=abi.EMA, r=5e-4,
-                          first_step=1, adopt_basis=True) <= 1.0
+                          first_step=1, adopt_basis=True, precision=precision) <= 1.0
 
 
 def test_c2_block_trajectory_soap_768x1024_own_basis(rt):
