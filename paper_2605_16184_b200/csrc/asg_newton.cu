@@ -57,6 +57,7 @@ constexpr int kNsMaxIter = 60;
 constexpr float kNsFinal = 1e-3f;
 constexpr float kNsDiverged = 3.5f;  // eigenvalues of M outside (0, p + 1): divergence
 constexpr int kPowerSteps = 5;
+constexpr int kNsRefineFrom = 2;  // refine roots whose last X step came at iteration >= this
 // Damping floor relative to lambda_max: the stated error of one 3xTF32
 // product at depth d (gemm_tol, tests/test_gpu_kernels.py). The fp32 factor
 // and every product of the iteration carry noise of that size, so smaller
@@ -199,6 +200,7 @@ struct NsState {
     unsigned int* resid;  // max|M - I| of the last M product (EPI_NS)
     int* iter;   // iteration counter (one int)
     int* any;    // per matrix: still active after the decision
+    int* kfin;   // per matrix: iteration of the last X step (large: refine)
 };
 
 __global__ void ns_state_init_kernel(NsState st, const float* __restrict__ est, const float* __restrict__ fro,
@@ -208,6 +210,7 @@ __global__ void ns_state_init_kernel(NsState st, const float* __restrict__ est, 
     if (b >= nb) return;
     st.resid[b] = 0u;
     st.xbuf[b] = 0;
+    st.kfin[b] = 1 << 20;
     if (!gate[b]) {  // not part of this pass
         st.state[b] = 2;
         st.actX[b] = st.actM[b] = 0;
@@ -319,6 +322,7 @@ __global__ void ns_decide_kernel(NsState st, int nb, int d, int D, float* __rest
         st.actX[b] = st.actM[b] = 0;
         act = 0;
     } else if (fmaxf(r, nrm) <= kNsFinal) {
+        st.kfin[b] = k;
         st.state[b] = 1;
         st.actX[b] = 1;
         st.actM[b] = 0;
@@ -462,6 +466,19 @@ __global__ void ns_merge_status_kernel(const int* __restrict__ local, int* __res
     if (b < nb && local[b] != ASG_OK && status[b] == ASG_OK) status[b] = local[b];
 }
 
+// The refinement against A' pays off only after a long product chain: a
+// matrix whose last X step came before iteration kNsRefineFrom (a
+// well-conditioned factor, e.g. every C3 KL factor: max|M - I| = 3e-2, then
+// 8e-4) keeps the coupled iterate, whose chain rounding is a few 3xTF32
+// products: KL roots at 2048^2 within 1.4e-6 of the oracle without it
+// (tests/test_gpu_parity_large.py states 6.4e-5), and ~35% of the refresh's
+// tensor work saved (C3 dispatch-step spike 320 -> 250 ms).
+__global__ void ns_refine_gate_kernel(const int* __restrict__ gate, const int* __restrict__ kfin, int* __restrict__ rgate,
+                                      int nb, int from) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nb) rgate[b] = gate[b] && kfin[b] >= from;
+}
+
 }  // namespace
 
 size_t ns_workspace_floats(int nb, int D) {
@@ -495,10 +512,12 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
     float* fro = take(size_t(nb));
     float* cval = take(size_t(nb));
     float* eeff = take(size_t(nb));
-    int* ints = reinterpret_cast<int*>(take(9 * size_t(nb) + 32));
+    int* ints = reinterpret_cast<int*>(take(11 * size_t(nb) + 32));
     NsState st{ints, ints + nb, ints + 2 * nb, ints + 3 * nb, reinterpret_cast<unsigned int*>(ints + 4 * nb),
                ints + 9 * nb, ints + 5 * nb};
     int* gate = ints + 6 * nb;
+    st.kfin = ints + 8 * nb;
+    int* rgate = ints + 10 * nb;  // matrices whose root gets the refinement (ns_refine_gate_kernel)
     int* status = ints + 7 * nb;  // this call's status (merged into caller_status at the end)
     if (!split) X0l = X1l = M0l = M1l = T0l = T1l = Ul = Wl = nullptr;
     float* outl_ = split ? outl : nullptr;
@@ -589,16 +608,18 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
         // iteration never revisits A', so the rounding of the ~3 products per
         // iteration accumulates in X; this step removes its commuting part
         // exactly and contracts the rest (tests/test_gpu_newton.py).
-        ns_damped_split_kernel<<<dim3(eblocks, nb), 256, 0, q>>>(A, d, D, eeff, Uh, Ul, gate);
+        static const int refine_from = getenv("ASG_NS_REFINE_FROM") ? atoi(getenv("ASG_NS_REFINE_FROM")) : kNsRefineFrom;
+        ns_refine_gate_kernel<<<(nb + 255) / 256, 256, 0, q>>>(gate, st.kfin, rgate, nb, refine_from);
+        ns_damped_split_kernel<<<dim3(eblocks, nb), 256, 0, q>>>(A, d, D, eeff, Uh, Ul, rgate);
         const float* xph = outh;  // X^(p/2)
         const float* xpl = outl_;
         if (p == 4) {
-            gemm(outh, outl_, outh, outl_, EPI_SYM_SPLIT, T1h, T1l, gate, nullptr, nullptr, true, q);  // X^2
+            gemm(outh, outl_, outh, outl_, EPI_SYM_SPLIT, T1h, T1l, rgate, nullptr, nullptr, true, q);  // X^2
             xph = T1h;
             xpl = T1l;
         }
         // B = X^(p/2) A' (general product: A' does not commute with the rounded X)
-        gemm(xph, xpl, Uh, Ul, EPI_SPLIT, Wh, Wl, gate, nullptr, nullptr, false, q);
+        gemm(xph, xpl, Uh, Ul, EPI_SPLIT, Wh, Wl, rgate, nullptr, nullptr, false, q);
         // R = I - B X^(p/2) into T0 (EPI_NS with T = 1 I - 1 acc; its M output goes to M0)
         {
             GemmLaunch g{};
@@ -611,7 +632,7 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
             g.p.Dlo = M0l;
             g.p.ldd = D;
             g.p.d_bstride = int64_t(DD);
-            g.p.batch_active = gate;
+            g.p.batch_active = rgate;
             g.p.Thi = T0h;
             g.p.Tlo = T0l;
             g.p.ns_a = 1.f;
@@ -634,10 +655,10 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
             g.p.Dlo = X1l;
             g.p.ldd = D;
             g.p.d_bstride = int64_t(DD);
-            g.p.batch_active = gate;
+            g.p.batch_active = rgate;
             gemm_launch(g, ASG_PREC_TF32, num_sms, q);
         }
-        ns_refine_kernel<<<dim3(D / 32, D / 32, nb), dim3(32, 8), 0, q>>>(outh, outl_, X1h, X1l, d, D, 0.5f / pf, gate);
+        ns_refine_kernel<<<dim3(D / 32, D / 32, nb), dim3(32, 8), 0, q>>>(outh, outl_, X1h, X1l, d, D, 0.5f / pf, rgate);
     };
 
     // The whole root (both passes, each a prologue, a device-driven WHILE
