@@ -1,7 +1,7 @@
 # Kernel-only timing of the 3xTF32 GEMM modes on a C3-shaped batched product:
 # asg_gemm_tn with ASG_GEMM_REPEAT = 1 and 11 (same operands); the difference
 # / 10 is one GEMM launch. Environment knobs select kernel variants.
-import ctypes as C, os, subprocess, sys, time
+import ctypes as C, os, subprocess, sys, time  # run from the repo root: python tools/r02/gemm_diag.py PREC
 sys.path.insert(0, os.getcwd())
 if len(sys.argv) > 2:  # child: time one configuration
     import torch
