@@ -109,6 +109,8 @@ cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUte
     } else {
         int pairs = max_pairs[dev & 63];
         if (pairs > num_sms / 2) pairs = num_sms / 2;
+        static const int cap = getenv("ASG_GEMM_MAX_PAIRS") ? atoi(getenv("ASG_GEMM_MAX_PAIRS")) : 0;  // tuning
+        if (cap > 0 && pairs > cap) pairs = cap;
         if (pairs > p.num_tiles) pairs = p.num_tiles;
         if (pairs <= 0) return cudaErrorInvalidConfiguration;
         cudaLaunchConfig_t cfg = {};
