@@ -438,9 +438,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default=os.environ.get("ASG_WORKLOAD", "C3"), choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "3xtf32_smem", "tf32"],
+    ap.add_argument("--precision", default="auto", choices=["auto", "3xtf32", "3xtf32_smem", "3xf16", "tf32"],
                     help="3xtf32: operands stored as (hi, lo) tf32 pairs; 3xtf32_smem: the same products, operands "
-                         "stored as plain fp32 and split in shared memory; tf32: one product")
+                         "stored as plain fp32 and split in shared memory; 3xf16: the step's operands as scaled "
+                         "(hi, lo) fp16 pairs (kind::f16, twice the tf32 rate); tf32: one product; auto (default): "
+                         "3xf16 for Shampoo / KL-Shampoo, 3xtf32 for SOAP (whose chain 3xf16 does not cover)")
     ap.add_argument("--refresh", default="newton", choices=["newton", "f32", "f64"],
                     help="refresh arithmetic: newton = Newton-Schulz roots for Shampoo/KL (SOAP: f32 eigensolve), "
                          "f32 = fp32-level tensor-core eigensolve, f64 = reference-tight fp64 eigensolve")
@@ -462,6 +464,8 @@ def main():
     if args.workload == "C5" and args.impl == "ours":
         run_c5(args, rank, world, local)
         return
+    if args.precision == "auto":
+        args.precision = "3xtf32" if wl["method"] == "SOAP" else "3xf16"
     step_flops, refresh_flops, flops = alg_flops(wl)
     cfg_out = {"workload": wl["name"], "method": wl["method"], "blocks": sum(len(blocks_of(s, wl["limit"])) for s in wl["shapes"]),
                "params": sum(math.prod(s) for s in wl["shapes"]), "block_dim_limit": wl["limit"],
@@ -531,7 +535,8 @@ def main():
     # The cold first refresh (dispatched at step 0) must be installed before
     # timing: its barrier fires at step S+1, so warm up past it.
     args.warmup = max(args.warmup, wl["S"] + 2)
-    prec = {"3xtf32": abi.PREC_3XTF32, "3xtf32_smem": abi.PREC_3XTF32_SMEM, "tf32": abi.PREC_TF32}[args.precision]
+    prec = {"3xtf32": abi.PREC_3XTF32, "3xtf32_smem": abi.PREC_3XTF32_SMEM, "3xf16": abi.PREC_3XF16,
+            "tf32": abi.PREC_TF32}[args.precision]
 
     gen = torch.Generator(device=dev).manual_seed(1234)
     params, grads = [], []
@@ -679,7 +684,8 @@ def main():
         "metric": "optimizer step throughput (algorithmic TFLOP/s); step latency in ms_per_step",
         "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": ("f32 (3xTF32 tensor-core products; " +
+        "dtype": (("f32 (3xFP16 tensor-core products: scaled fp16 (hi, lo) pairs, fp32-faithful; "
+                   if prec == abi.PREC_3XF16 else "f32 (3xTF32 tensor-core products; ") +
                   {"f32": "fp32-level refresh: tensor-core block Jacobi)",
                    "newton": "fp32-level refresh: Newton-Schulz roots (SOAP: tensor-core block Jacobi))",
                    "f64": "fp64 refresh)"}[args.refresh] if prec != abi.PREC_TF32 else "tf32"),
@@ -694,8 +700,10 @@ def main():
                      "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                      "frac": (ach / peak) if ach else None,
                      "peak_note": f"{peak_src} dense bf16 (MEASURED_PEAKS.json bf16_tflops); tf32 kind = bf16/2, "
-                                  f"3xTF32 issues 3 tf32 MMAs per algorithmic product",
-                     "frac_of_mode_peak": (ach / (peak / 2 / (3 if prec != abi.PREC_TF32 else 1))) if ach else None,
+                                  f"fp16 kind = bf16; 3xTF32 / 3xFP16 issue 3 MMAs per algorithmic product "
+                                  f"(mode peak = bf16/6 / bf16/3)",
+                     "frac_of_mode_peak": (ach / (peak / {abi.PREC_TF32: 2, abi.PREC_3XF16: 3}.get(prec, 6)))
+                                          if ach else None,
                      "gemm_launches": ks.gemm_launches, "gemm_ms_per_step": ks.gemm_ms / args.steps,
                      **traffic_for(args.workload, args.precision)},
         "hbm_kernels": hbm_kernels,

@@ -74,8 +74,11 @@ typedef enum asg_accumulation { ASG_ACCUM_SUM = 0, ASG_ACCUM_EMA = 1 } asg_accum
 typedef enum asg_precision {
     ASG_PREC_3XTF32 = 0,     /* operands stored in HBM as (hi, lo) tf32 pairs */
     ASG_PREC_TF32 = 1,
-    ASG_PREC_3XTF32_SMEM = 2 /* the same 3xTF32 products; operands stored as plain fp32 (half the
-                                bytes) and split into (hi, lo) in shared memory after the TMA load */
+    ASG_PREC_3XTF32_SMEM = 2, /* the same 3xTF32 products; operands stored as plain fp32 (half the
+                                 bytes) and split into (hi, lo) in shared memory after the TMA load */
+    ASG_PREC_3XF16 = 3        /* 3xFP16: the step's operands as exact (hi, lo) fp16 pairs with a
+                                 per-matrix power-of-two scale (x s = hi + lo to ~2^-22), multiplied by
+                                 tcgen05 kind::f16 at twice the tf32 rate; other products as 3XTF32_SMEM */
 } asg_precision;
 
 /* Tensor roles (tiers.hpp:35-44) plus the KL-Shampoo inverses and the

@@ -14,7 +14,7 @@ METHOD_NAMES = {ADAMW: "AdamW", SHAMPOO: "Shampoo", SOAP: "SOAP", KL_SHAMPOO: "K
 # asg_accumulation (precond.hpp:20)
 SUM, EMA = 0, 1
 # asg_precision
-PREC_3XTF32, PREC_TF32, PREC_3XTF32_SMEM = 0, 1, 2
+PREC_3XTF32, PREC_TF32, PREC_3XTF32_SMEM, PREC_3XF16 = 0, 1, 2, 3
 # asg_install_mode
 INSTALL_SIM_CLOCK, INSTALL_EVENT = 0, 1
 # asg_refresh_mode

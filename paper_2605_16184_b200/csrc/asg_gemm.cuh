@@ -95,6 +95,9 @@ struct GemmParams {
     int raster;           // rectangular schedules: 0 row-major tiles, 1 column-major
     int raw_out;          // 3xTF32: an output without a lo array stores the full fp32 value
     int a_raw, b_raw;     // SPL kernels: operand given as plain fp32 (split in shared memory)
+    const float* ascale;  // F16 kernels: per-batch power-of-two scales the fp16 operands carry
+    const float* bscale;  //   (the accumulator is divided by ascale[b] * bscale[b])
+    unsigned int* omax;   // optional: per-batch max |output| (float bits, atomicMax) of SPLIT / SPLIT2
     int sym_T;            // CTA-pair symmetric schedules: T x T tile grid, lower triangle decoded
                           // arithmetically (tile_list unused)
 };
@@ -123,15 +126,19 @@ __device__ __forceinline__ void out_split(const GemmParams& p, float x, float& h
 // raw), so HBM holds and streams one fp32 per element. (A variant with a
 // deeper hi-only TMA ring and a separate 2-slot lo ring measured 1.4x slower
 // per launch: the conversion, not the load latency, sets the pace.)
-template <int BN, int NPASS, int CG = 1, bool SPL = false>
+// F16: 3xFP16 -- every operand is an exact (hi, lo) pair of fp16 values
+// carrying a per-matrix power-of-two scale (x * s = hi + lo to ~2^-22;
+// max |x| s in [2^14, 2^15)), multiplied by tcgen05.mma kind::f16 at twice the
+// tf32 rate per staged byte; a 128-byte smem row then holds 64 K elements.
+template <int BN, int NPASS, int CG = 1, bool SPL = false, bool F16 = false>
 struct GemmCfg {
     static constexpr int BM = 128;       // accumulator rows per CTA
     static constexpr int TM = 128 * CG;  // output tile rows
-    static constexpr int BK = 32;  // 32 fp32 = one 128-byte swizzle row
+    static constexpr int BK = F16 ? 64 : 32;  // K elements per 128-byte swizzle row
     static constexpr bool kSplit = NPASS > 1;
     static constexpr int kBRows = BN / CG;  // B rows staged by each CTA
-    static constexpr uint32_t kABytes = BM * BK * 4;
-    static constexpr uint32_t kBBytes = kBRows * BK * 4;
+    static constexpr uint32_t kABytes = BM * 128;
+    static constexpr uint32_t kBBytes = kBRows * 128;
     static constexpr uint32_t kStageBytes = (kABytes + kBBytes) * (kSplit ? 2 : 1);
     // per-epilogue-warp 32 x 33 fp32 transpose scratch (coalesced apply)
     static constexpr int kEpiWarps = 8;
@@ -335,6 +342,14 @@ __device__ __forceinline__ void rows_chunk(const GemmParams& p, int b, int row0,
     __syncwarp();
     const int c = col0 + int(lane);
     if constexpr (EPI == EPI_SPLIT || EPI == EPI_SPLIT2) {
+        if (p.omax) {  // per-batch max |D| for the next product's fp16 scale
+            float mx = 0.f;
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) mx = fmaxf(mx, fabsf(scratch[lane][j]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane == 0) atomicMax(p.omax + b, __float_as_uint(mx));
+        }
         float* dh = p.Dhi + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c;
         float* dl = p.Dlo ? p.Dlo + int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c : nullptr;
 #pragma unroll 8
@@ -480,12 +495,13 @@ __device__ __forceinline__ void sym_split_chunk(const GemmParams& p, int b, int 
     __syncwarp();
 }
 
-template <int BN, int NPASS, int EPI, int CG = 1, bool SPL = false>
+template <int BN, int NPASS, int EPI, int CG = 1, bool SPL = false, bool F16 = false>
 __global__ void __launch_bounds__(SPL ? 448 : 320, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                    const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
                    const __grid_constant__ GemmParams p) {
-    using Cfg = GemmCfg<BN, NPASS, CG, SPL>;
+    using Cfg = GemmCfg<BN, NPASS, CG, SPL, F16>;
+    static_assert(!F16 || (NPASS == 3 && !SPL), "3xFP16 takes (hi, lo) fp16 pairs from HBM");
     static_assert(!SPL || NPASS == 3, "the shared-memory split serves 3xTF32 only");
     constexpr int BM = Cfg::BM, BK = Cfg::BK, STAGES = Cfg::kStages;
     constexpr bool SPLIT = Cfg::kSplit;
@@ -554,7 +570,7 @@ __global__ void __launch_bounds__(SPL ? 448 : 320, 1)
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int num_k = p.K / BK;
+    const int num_k = (p.K + BK - 1) / BK;  // F16: a K tail short of 64 is zero-filled by the TMA
 
     if (warp == 0) {
         if (lane == 0) {
@@ -605,7 +621,7 @@ __global__ void __launch_bounds__(SPL ? 448 : 320, 1)
         }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = idesc_tf32(Cfg::TM, BN);
+            constexpr uint32_t idesc = F16 ? idesc_f16(Cfg::TM, BN) : idesc_tf32(Cfg::TM, BN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -623,8 +639,20 @@ __global__ void __launch_bounds__(SPL ? 448 : 320, 1)
                     const uint64_t al = SPLIT ? umma_desc_k_sw128(a_lo(stage)) : 0;
                     const uint64_t bl = SPLIT ? umma_desc_k_sw128(b_lo(stage)) : 0;
 #pragma unroll
-                    for (int k = 0; k < BK / 8; ++k) {
-                        const uint64_t adv = uint64_t(k * 32) >> 4;  // 8 tf32 = 32 bytes along K
+                    for (int k = 0; k < 4; ++k) {  // four 32-byte K steps per 128-byte row
+                        const uint64_t adv = uint64_t(k * 32) >> 4;  // 8 tf32 / 16 fp16 = 32 bytes along K
+                        if constexpr (F16) {  // hi*hi + hi*lo + lo*hi, kind::f16
+                            if constexpr (PAIR) {
+                                mma_f16_pair(d, ah + adv, bh + adv, idesc, (kb | k) != 0 ? 1u : 0u);
+                                mma_f16_pair(d, ah + adv, bl + adv, idesc, 1u);
+                                mma_f16_pair(d, al + adv, bh + adv, idesc, 1u);
+                            } else {
+                                mma_f16(d, ah + adv, bh + adv, idesc, (kb | k) != 0 ? 1u : 0u);
+                                mma_f16(d, ah + adv, bl + adv, idesc, 1u);
+                                mma_f16(d, al + adv, bh + adv, idesc, 1u);
+                            }
+                            continue;
+                        }
                         if constexpr (PAIR) {
                             mma_tf32_pair(d, ah + adv, bh + adv, idesc, (kb | k) != 0 ? 1u : 0u);
                             if (SPLIT) {
@@ -727,11 +755,16 @@ __global__ void __launch_bounds__(SPL ? 448 : 320, 1)
             tc_fence_after();
             const int row0 = tm * Cfg::TM + int(rank) * BM + q * 32;
             const int row = row0 + int(lane);
+            const float unscale = F16 ? 1.f / (p.ascale[b] * p.bscale[b]) : 1.f;  // exact (powers of two)
 #pragma unroll 1
             for (int c = half; c < BN / 32; c += 2) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32), r);
                 tmem_ld_wait();
+                if constexpr (F16) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * unscale);
+                }
                 if constexpr (EPI == EPI_APPLY)
                     apply_chunk(p, b, row0, tn * BN + c * 32, r, scratch);
                 else if constexpr (EPI == EPI_ADAM)

@@ -10,8 +10,10 @@
 //   K9 adamw      AdamW + apply for 1-D parameters (precond.cpp:229-251)
 //   K10 sqnorm    global gradient norm + non-finite flag (harness.cpp:219-223)
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -54,24 +56,26 @@ PFN_encodeTiled encode_fn() {
 
 // 3-D map over a [batch][rows][K] fp32 slab with a (32 x box_rows x 1) box,
 // 128-byte swizzle (matches the UMMA K-major SWIZZLE_128B descriptor).
-bool make_map(CUtensorMap* map, const float* base, int K, int rows, int batch, int box_rows) {
+bool make_map(CUtensorMap* map, const float* base, int K, int rows, int batch, int box_rows, bool f16 = false) {
     PFN_encodeTiled enc = encode_fn();
     if (!enc) return false;
+    const cuuint64_t es = f16 ? 2 : 4;  // element bytes; a box row is 128 bytes either way
     cuuint64_t dims[3] = {cuuint64_t(K), cuuint64_t(rows), cuuint64_t(batch)};
-    cuuint64_t strides[2] = {cuuint64_t(K) * 4, cuuint64_t(K) * cuuint64_t(rows) * 4};
-    cuuint32_t box[3] = {32, cuuint32_t(box_rows), 1};
+    cuuint64_t strides[2] = {cuuint64_t(K) * es, cuuint64_t(K) * cuuint64_t(rows) * es};
+    cuuint32_t box[3] = {cuuint32_t(128 / es), cuuint32_t(box_rows), 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+    CUresult r = enc(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                     const_cast<float*>(base), dims, strides,
                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int NPASS, int EPI, int CG, bool SPL>
+template <int BN, int NPASS, int EPI, int CG, bool SPL, bool F16>
 cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                         const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
-    using Cfg = GemmCfg<BN, NPASS, CG, SPL>;
-    auto kern = gemm_tn_kernel<BN, NPASS, EPI, CG, SPL>;
+    using Cfg = GemmCfg<BN, NPASS, CG, SPL, F16>;
+    auto kern = gemm_tn_kernel<BN, NPASS, EPI, CG, SPL, F16>;
     // the shared-memory limit is a per-device function attribute; so is the
     // number of CTA pairs that can be co-resident (GPCs with an odd SM count)
     static std::atomic<uint64_t> attr_set{0};
@@ -132,19 +136,19 @@ cudaError_t launch_inst(const CUtensorMap& ah, const CUtensorMap& al, const CUte
     return cudaGetLastError();
 }
 
-template <int BN, int NPASS, int CG, bool SPL>
+template <int BN, int NPASS, int CG, bool SPL, bool F16 = false>
 cudaError_t dispatch_epi(int epi, const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                          const CUtensorMap& bl, const GemmParams& p, int num_sms, cudaStream_t s) {
     switch (epi) {
-        case EPI_STORE: return launch_inst<BN, NPASS, EPI_STORE, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SYM_EMA: return launch_inst<BN, NPASS, EPI_SYM_EMA, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SPLIT: return launch_inst<BN, NPASS, EPI_SPLIT, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SPLIT_T: return launch_inst<BN, NPASS, EPI_SPLIT_T, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_ADAM: return launch_inst<BN, NPASS, EPI_ADAM, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_APPLY: return launch_inst<BN, NPASS, EPI_APPLY, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SYM_SPLIT: return launch_inst<BN, NPASS, EPI_SYM_SPLIT, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_NS: return launch_inst<BN, NPASS, EPI_NS, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
-        case EPI_SPLIT2: return launch_inst<BN, NPASS, EPI_SPLIT2, CG, SPL>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_STORE: return launch_inst<BN, NPASS, EPI_STORE, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SYM_EMA: return launch_inst<BN, NPASS, EPI_SYM_EMA, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT: return launch_inst<BN, NPASS, EPI_SPLIT, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT_T: return launch_inst<BN, NPASS, EPI_SPLIT_T, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_ADAM: return launch_inst<BN, NPASS, EPI_ADAM, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_APPLY: return launch_inst<BN, NPASS, EPI_APPLY, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SYM_SPLIT: return launch_inst<BN, NPASS, EPI_SYM_SPLIT, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_NS: return launch_inst<BN, NPASS, EPI_NS, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
+        case EPI_SPLIT2: return launch_inst<BN, NPASS, EPI_SPLIT2, CG, SPL, F16>(ah, al, bh, bl, p, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -190,21 +194,27 @@ cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStr
     if (pair && !g.sym_tiles && int64_t(g.batch) * (M / 256) * (N / bn) < int64_t(num_sms)) pair = false;
     const int tm_rows = pair ? 256 : 128;
     const int brows = pair ? bn / 2 : bn;
-    const bool split = precision != ASG_PREC_TF32;  // 3XTF32 and 3XTF32_SMEM
+    const bool split = precision != ASG_PREC_TF32;  // 3XTF32, 3XTF32_SMEM, 3XF16
+    // 3xFP16: both operands fp16 (hi, lo) pairs with per-batch scales
+    const bool f16 = g.A.scale != nullptr;
+    if (f16 != (g.B.scale != nullptr) || (f16 && (!g.A.lo || !g.B.lo || !split)))
+        return cudaErrorInvalidValue;
     // 3xTF32 operands without a lo array hold plain fp32: split in shared memory (SPL)
-    const bool a_raw = split && !g.A.lo, b_raw = split && !g.B.lo;
+    const bool a_raw = split && !f16 && !g.A.lo, b_raw = split && !f16 && !g.B.lo;
     const bool spl = a_raw || b_raw;
     CUtensorMap ah, al, bh, bl;
-    if (!make_map(&ah, g.A.hi, K, M, g.batch, 128)) return cudaErrorInvalidValue;
-    if (!make_map(&bh, g.B.hi, K, N, g.batch, brows)) return cudaErrorInvalidValue;
+    if (!make_map(&ah, g.A.hi, K, M, g.batch, 128, f16)) return cudaErrorInvalidValue;
+    if (!make_map(&bh, g.B.hi, K, N, g.batch, brows, f16)) return cudaErrorInvalidValue;
     al = ah;
     bl = bh;
-    if (split && !a_raw && !make_map(&al, g.A.lo, K, M, g.batch, 128)) return cudaErrorInvalidValue;
-    if (split && !b_raw && !make_map(&bl, g.B.lo, K, N, g.batch, brows)) return cudaErrorInvalidValue;
+    if (split && !a_raw && !make_map(&al, g.A.lo, K, M, g.batch, 128, f16)) return cudaErrorInvalidValue;
+    if (split && !b_raw && !make_map(&bl, g.B.lo, K, N, g.batch, brows, f16)) return cudaErrorInvalidValue;
     GemmParams p = g.p;
     p.raw_out = split ? 1 : 0;
     p.a_raw = a_raw ? 1 : 0;
     p.b_raw = b_raw ? 1 : 0;
+    p.ascale = g.A.scale;
+    p.bscale = g.B.scale;
     p.M = M;
     p.N = N;
     p.K = K;
@@ -226,6 +236,13 @@ cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStr
         p.tiles_per_batch = (M / tm_rows) * (N / bn);
     }
     p.num_tiles = p.tiles_per_batch * g.batch;
+    if (f16) {
+        if (pair)
+            return bn == 256 ? dispatch_epi<256, 3, 2, false, true>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                             : dispatch_epi<128, 3, 2, false, true>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+        return bn == 256 ? dispatch_epi<256, 3, 1, false, true>(g.epi, ah, al, bh, bl, p, num_sms, stream)
+                         : dispatch_epi<128, 3, 1, false, true>(g.epi, ah, al, bh, bl, p, num_sms, stream);
+    }
     if (spl) {
         if (pair)
             return bn == 256 ? dispatch_epi<256, 3, 2, true>(g.epi, ah, al, bh, bl, p, num_sms, stream)
@@ -1213,6 +1230,129 @@ void launch_synth_normal(const SynthBlock* blocks_dev, int nb, int max_rows, int
     const int quads = (max_cols + 3) / 4;
     synth_normal_kernel<<<dim3((quads + 255) / 256, max_rows, nb), 256, 0, s>>>(blocks_dev, seed, step);
     count_launch();
+}
+
+
+// ============================================================================
+// 3xFP16 operands: power-of-two scales and (hi, lo) fp16 pairs
+// ============================================================================
+namespace {
+// s = 2^(14 - floor(log2 m)): m s in [2^14, 2^15) (max fp16 65504); 1 for m == 0 / non-finite
+__device__ __forceinline__ float f16_scale(unsigned int mbits) {
+    const int e = int((mbits >> 23) & 0xff);
+    if (e == 0 || e == 0xff) return 1.f;
+    const int ex = 268 - e;  // biased exponent of 2^(14 - (e - 127))
+    return __uint_as_float(uint32_t(ex > 254 ? 254 : ex) << 23);
+}
+__device__ __forceinline__ void f16_split(float y, __half& h, __half& l) {
+    h = __float2half_rn(y);
+    l = __float2half_rn(y - __half2float(h));
+}
+
+__global__ void absmax_kernel(const float* __restrict__ src, int64_t per, unsigned int* __restrict__ amax) {
+    const int64_t b = blockIdx.y;
+    const float4* p4 = reinterpret_cast<const float4*>(src + b * per);
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per / 4; i += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = p4[i];
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        if (!isfinite(v.x + v.y + v.z + v.w)) m = __int_as_float(0x7f800000);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(amax + b, __float_as_uint(m));
+}
+
+__global__ void to_f16pair_kernel(const float* __restrict__ src, const unsigned int* __restrict__ amax, int64_t per,
+                                  __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ scale) {
+    const int64_t b = blockIdx.y;
+    const float s = f16_scale(amax[b]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) scale[b] = s;
+    const float4* p4 = reinterpret_cast<const float4*>(src + b * per);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per / 4; i += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = p4[i];
+        __half h[4], l[4];
+        f16_split(v.x * s, h[0], l[0]);
+        f16_split(v.y * s, h[1], l[1]);
+        f16_split(v.z * s, h[2], l[2]);
+        f16_split(v.w * s, h[3], l[3]);
+        *reinterpret_cast<uint2*>(hi + b * per + 4 * i) = *reinterpret_cast<const uint2*>(h);
+        *reinterpret_cast<uint2*>(lo + b * per + 4 * i) = *reinterpret_cast<const uint2*>(l);
+    }
+}
+
+// max |x| over each gradient block's view (rows x cols of the caller's tensor)
+__global__ void block_absmax_kernel(const BlockRef* __restrict__ blocks, unsigned int* __restrict__ amax) {
+    const BlockRef blk = blocks[blockIdx.y];
+    float m = 0.f;
+    for (int i = blockIdx.x; i < blk.rows; i += gridDim.x)
+        for (int j = threadIdx.x; j < blk.cols; j += blockDim.x) {
+            const float x = blk.src[int64_t(i) * blk.ld + j];
+            m = isfinite(x) ? fmaxf(m, fabsf(x)) : __int_as_float(0x7f800000);
+        }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(amax + blockIdx.y, __float_as_uint(m));
+}
+
+// G (x scale_val, x the block's fp16 scale) -> fp16 pairs of G [b][M][N] and G^T [b][N][M]
+__global__ void prep_grad_f16_kernel(const BlockRef* __restrict__ blocks, int M, int N, float scale_val,
+                                     const unsigned int* __restrict__ amax, __half* __restrict__ Gh,
+                                     __half* __restrict__ Gl, __half* __restrict__ GTh, __half* __restrict__ GTl,
+                                     float* __restrict__ gscale) {
+    __shared__ float t[32][33];
+    const int b = blockIdx.z;
+    const BlockRef blk = blocks[b];
+    // the scale covers the clip-scaled values: max |scale_val x| = scale_val max |x|
+    const float s = f16_scale(__float_as_uint(__uint_as_float(amax[b]) * scale_val));
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) gscale[b] = s;
+    const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    const int64_t slab = int64_t(M) * N;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int i = i0 + dy, j = j0 + threadIdx.x;
+        float x = 0.f;
+        if (i < blk.rows && j < blk.cols) x = scale_val * blk.src[int64_t(i) * blk.ld + j] * s;
+        __half h, l;
+        f16_split(x, h, l);
+        Gh[b * slab + int64_t(i) * N + j] = h;
+        Gl[b * slab + int64_t(i) * N + j] = l;
+        t[dy][threadIdx.x] = x;
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int jj = j0 + dy, ii = i0 + threadIdx.x;
+        __half h, l;
+        f16_split(t[threadIdx.x][dy], h, l);
+        GTh[b * slab + int64_t(jj) * M + ii] = h;
+        GTl[b * slab + int64_t(jj) * M + ii] = l;
+    }
+}
+}  // namespace
+
+void launch_absmax(const float* src, int nb, int64_t per, unsigned int* amax, cudaStream_t s) {
+    if (nb <= 0) return;
+    cudaMemsetAsync(amax, 0, size_t(nb) * sizeof(unsigned int), s);
+    const int64_t blocks = std::min<int64_t>(1024, (per / 4 + 255) / 256);
+    absmax_kernel<<<dim3(unsigned(blocks > 0 ? blocks : 1), nb), 256, 0, s>>>(src, per, amax);
+    count_launch();
+}
+
+void launch_to_f16pair(const float* src, const unsigned int* amax, int nb, int64_t per, void* hi16, void* lo16,
+                       float* scale, cudaStream_t s) {
+    if (nb <= 0) return;
+    const int64_t blocks = std::min<int64_t>(1024, (per / 4 + 255) / 256);
+    to_f16pair_kernel<<<dim3(unsigned(blocks > 0 ? blocks : 1), nb), 256, 0, s>>>(
+        src, amax, per, static_cast<__half*>(hi16), static_cast<__half*>(lo16), scale);
+    count_launch();
+}
+
+void launch_prep_grad_f16(const BlockRef* blocks_dev, int nb, int M, int N, float scale_val, unsigned int* amax,
+                          void* Gh16, void* Gl16, void* GTh16, void* GTl16, float* gscale, cudaStream_t s) {
+    if (nb <= 0) return;
+    cudaMemsetAsync(amax, 0, size_t(nb) * sizeof(unsigned int), s);
+    block_absmax_kernel<<<dim3(std::min(M, 256), nb), 256, 0, s>>>(blocks_dev, amax);
+    prep_grad_f16_kernel<<<dim3(N / 32, M / 32, nb), dim3(32, 8), 0, s>>>(
+        blocks_dev, M, N, scale_val, amax, static_cast<__half*>(Gh16), static_cast<__half*>(Gl16),
+        static_cast<__half*>(GTh16), static_cast<__half*>(GTl16), gscale);
+    count_launch(2);
 }
 
 }  // namespace asg

@@ -33,6 +33,9 @@ struct Operand {
     const float* lo;
     int rows;
     int K;
+    // 3xFP16 operand: hi / lo point at [batch][rows][K] fp16 arrays (cast), scaled
+    // by the per-batch power of two `scale` (GemmCfg F16, f16_scale)
+    const float* scale = nullptr;
 };
 
 struct GemmLaunch {
@@ -154,6 +157,18 @@ void launch_ns_x(const float* S, int nb, int d, int D, float* Xh, float* Xl, cud
 
 // Per-block status from a both-sides eigensolve: out[k] <- first failure of in[k], in[cnt+k].
 void launch_merge_status(const int* in, int cnt, int* out, cudaStream_t s);
+
+// 3xFP16 operands (GemmCfg F16): the power of two s with max|x| s in [2^14, 2^15)
+// (1 for an all-zero or non-finite max), hi = rn_f16(x s), lo = rn_f16(x s - hi).
+// Per-batch max |x| of [nb][per] fp32 slabs into amax (float bits; zeroed first).
+void launch_absmax(const float* src, int nb, int64_t per, unsigned int* amax, cudaStream_t s);
+// [nb][per] fp32 -> fp16 pairs hi16 / lo16 ([nb][per] each) and the scales.
+void launch_to_f16pair(const float* src, const unsigned int* amax, int nb, int64_t per, void* hi16, void* lo16,
+                       float* scale, cudaStream_t s);
+// Gradient blocks (caller layout, times scale_val) -> fp16 pairs of G [b][M][N] and
+// G^T [b][N][M] with per-block scales (a max pass over the blocks first).
+void launch_prep_grad_f16(const BlockRef* blocks_dev, int nb, int M, int N, float scale_val, unsigned int* amax,
+                          void* Gh16, void* Gl16, void* GTh16, void* GTl16, float* gscale, cudaStream_t s);
 
 // Multi-GPU: pack owned block slices into a contiguous buffer and back.
 void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out,

@@ -189,6 +189,13 @@ struct Group {
     // roots (left there by group_stats); the update reuses it unless an
     // install or a new gradient intervened
     std::vector<uint8_t> v_ok;
+    // 3XF16 (Shampoo / KL-Shampoo): the step's operands as fp16 (hi, lo) pairs
+    // ([nb][rows][K] hi, then lo; 4 B per element) with per-block power-of-two
+    // scales. G16 / GT16 reuse the G / G^T slabs; T16 (W or V), S16 (V^T), P16
+    // (installed roots, converted at install; the fp32 roots stay for readers).
+    uint16_t *G16 = nullptr, *GT16 = nullptr, *T16 = nullptr, *S16 = nullptr, *PL16 = nullptr, *PR16 = nullptr;
+    float *gscale = nullptr, *tscale = nullptr, *sscale = nullptr, *plscale = nullptr, *prscale = nullptr;
+    unsigned int *amax = nullptr, *amax2 = nullptr;  // per-block max |x| scratch
     // SOAP
     float *QLh = nullptr, *QLl = nullptr, *QLTh = nullptr, *QLTl = nullptr;
     float *QRh = nullptr, *QRl = nullptr, *QRTh = nullptr, *QRTl = nullptr;
@@ -389,6 +396,12 @@ bool is_kl(const asg_blockset* bs) { return bs->opt.method == ASG_METHOD_KL_SHAM
 bool split_mode(const asg_blockset* bs) { return bs->precision == ASG_PREC_3XTF32; }
 // the refresh's internal tensor-core Jacobi works on (hi, lo) pairs in both 3xTF32 modes
 bool work_split(const asg_blockset* bs) { return bs->precision != ASG_PREC_TF32; }
+void to_f16(const float* src, int nb, int s0, int cnt, int64_t per, uint16_t* dst, float* scale, unsigned int* amax,
+            cudaStream_t s);
+// 3XF16: the Shampoo / KL-Shampoo step chains on fp16 pairs (SOAP runs as 3XTF32_SMEM)
+bool f16_mode(const asg_blockset* bs) {
+    return bs->precision == ASG_PREC_3XF16 && bs->opt.method != ASG_METHOD_SOAP;
+}
 // F32 and NEWTON: fp32-level refresh (NEWTON: Newton-Schulz roots for Shampoo / KL)
 bool f32_refresh(const asg_blockset* bs) { return bs->sc.refresh_mode != ASG_REFRESH_F64; }
 bool newton_roots(const asg_blockset* bs) {
@@ -538,6 +551,17 @@ void alloc_group(asg_blockset* bs, Group& g) {
         g.Sh = g.Gh;
         g.Sl = g.Gl;
     }
+    if (f16_mode(bs)) {
+        g.G16 = reinterpret_cast<uint16_t*>(g.Gh);  // prep writes fp16 pairs; no fp32 G in this mode
+        g.GT16 = reinterpret_cast<uint16_t*>(g.GTh);
+        g.T16 = reinterpret_cast<uint16_t*>(dalloc<float>(bs, nb * slabMN(g)));
+        if (is_kl(bs)) g.S16 = reinterpret_cast<uint16_t*>(dalloc<float>(bs, nb * slabMN(g)));
+        g.PL16 = reinterpret_cast<uint16_t*>(dalloc<float>(bs, nb * slabMM(g)));
+        g.PR16 = reinterpret_cast<uint16_t*>(dalloc<float>(bs, nb * slabNN(g)));
+        for (float** sc : {&g.gscale, &g.tscale, &g.sscale, &g.plscale, &g.prscale}) *sc = dalloc<float>(bs, nb);
+        g.amax = dalloc<unsigned int>(bs, nb);
+        g.amax2 = dalloc<unsigned int>(bs, nb);
+    }
     auto pair_mm = [&](float*& h, float*& l) {
         h = dalloc<float>(bs, nb * slabMM(g));
         if (sp) l = dalloc<float>(bs, nb * slabMM(g));
@@ -604,6 +628,10 @@ void alloc_group(asg_blockset* bs, Group& g) {
         pair_lr(g.sPLh, g.sPLl, g.sPRh, g.sPRl);
         launch_identity_split(g.PLh, g.PLl, g.nb, g.M, g.m, s);
         launch_identity_split(g.PRh, g.PRl, g.nb, g.N, g.n, s);
+        if (f16_mode(bs)) {
+            to_f16(g.PLh, g.nb, 0, g.nb, int64_t(slabMM(g)), g.PL16, g.plscale, g.amax, s);
+            to_f16(g.PRh, g.nb, 0, g.nb, int64_t(slabNN(g)), g.PR16, g.prscale, g.amax, s);
+        }
         if (f32_refresh(bs) && !newton_roots(bs)) {  // basis of the last refresh, identity before the first
             pair_mm(g.BLh, g.BLl);
             pair_mm(g.BLTh, g.BLTl);
@@ -725,6 +753,19 @@ void alloc_workspace(asg_blockset* bs) {
 // GEMM helpers
 // ---------------------------------------------------------------------------
 Operand op(const float* h, const float* l, int rows, int K) { return Operand{h, l, rows, K}; }
+// slots [s0, ...) of an fp16-pair slab of nb blocks of rows x K, with their scales
+Operand op16(const uint16_t* base, int nb, int s0, int rows, int K, const float* scale) {
+    const size_t per = size_t(rows) * K;
+    return Operand{reinterpret_cast<const float*>(base + size_t(s0) * per),
+                   reinterpret_cast<const float*>(base + size_t(nb) * per + size_t(s0) * per), rows, K, scale + s0};
+}
+// fp32 slots [s0, s0+cnt) (rows x K each) -> fp16 pairs + scales of the same slots
+void to_f16(const float* src, int nb, int s0, int cnt, int64_t per, uint16_t* dst, float* scale, unsigned int* amax,
+            cudaStream_t s) {
+    launch_absmax(src + size_t(s0) * per, cnt, per, amax + s0, s);
+    launch_to_f16pair(src + size_t(s0) * per, amax + s0, cnt, per, dst + size_t(s0) * per,
+                      dst + size_t(nb) * per + size_t(s0) * per, scale + s0, s);
+}
 
 void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const GemmParams& p,
               const int2* sym_tiles, int nsym, cudaStream_t s, double alg_flops) {
@@ -1044,11 +1085,81 @@ void join_groups(asg_blockset* bs, int k) {
 }
 
 // Statistics for slots [s0, s0+cnt) of a group (G slabs already staged).
+// 3XF16 statistics (same products as group_stats; operands fp16 pairs with
+// per-block scales; every fp32 intermediate is converted once, to_f16).
+void group_stats_f16(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
+    const asg_optimizer_config& o = bs->opt;
+    const double mf = g.m, nf = g.n;
+    const bool ema = o.accumulation == ASG_ACCUM_EMA;
+    const size_t mn = slabMN(g), mm = slabMM(g), nn = slabNN(g);
+    const int nb = g.nb;
+    GemmParams p{};
+    p.beta = ema ? float(o.beta2) : 1.f;
+    if (!is_kl(bs)) {
+        p.alpha = ema ? float(1.0 - o.beta2) : 1.f;
+        p.C = at(g.L, mm, s0);
+        p.ldc = g.M;
+        p.c_bstride = int64_t(mm);
+        const Operand gop = op16(g.G16, nb, s0, g.M, g.N, g.gscale);
+        run_gemm(bs, gop, gop, cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s, cnt * mf * mf * nf);
+        p.C = at(g.R, nn, s0);
+        p.ldc = g.N;
+        p.c_bstride = int64_t(nn);
+        const Operand gtop = op16(g.GT16, nb, s0, g.N, g.M, g.gscale);
+        run_gemm(bs, gtop, gtop, cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s, cnt * nf * nf * mf);
+        return;
+    }
+    // W = G P_R (fp32, max) -> T16 ; L = b L + a/n W W^T
+    CK(cudaMemsetAsync(g.amax + s0, 0, size_t(cnt) * sizeof(unsigned int), s));
+    GemmParams px{};
+    px.alpha = 1.f;
+    px.Dhi = at(g.Th, mn, s0);
+    px.ldd = g.N;
+    px.d_bstride = int64_t(mn);
+    px.omax = g.amax + s0;
+    run_gemm(bs, op16(g.G16, nb, s0, g.M, g.N, g.gscale), op16(g.PR16, nb, s0, g.N, g.N, g.prscale), cnt, EPI_SPLIT,
+             px, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
+    launch_to_f16pair(at(g.Th, mn, s0), g.amax + s0, cnt, int64_t(mn), g.T16 + size_t(s0) * mn,
+                      g.T16 + size_t(nb) * mn + size_t(s0) * mn, g.tscale + s0, s);
+    const double a = ema ? (1.0 - o.beta2) : 1.0;
+    p.alpha = float(a / double(g.n));
+    p.C = at(g.L, mm, s0);
+    p.ldc = g.M;
+    p.c_bstride = int64_t(mm);
+    const Operand wop = op16(g.T16, nb, s0, g.M, g.N, g.tscale);
+    run_gemm(bs, wop, wop, cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s, cnt * mf * mf * nf);
+    // V^T = G^T P_L (fp32 into S, which aliases G: dead once W is formed) and V (fp32 into T), one max
+    CK(cudaMemsetAsync(g.amax + s0, 0, size_t(cnt) * sizeof(unsigned int), s));
+    px.Dhi = at(g.Sh, mn, s0);
+    px.ldd = g.M;
+    px.Thi = at(g.Th, mn, s0);
+    px.Tlo = nullptr;
+    px.ldt = g.N;
+    run_gemm(bs, op16(g.GT16, nb, s0, g.N, g.M, g.gscale), op16(g.PL16, nb, s0, g.M, g.M, g.plscale), cnt, EPI_SPLIT2,
+             px, nullptr, 0, s, cnt * 2.0 * nf * mf * mf);
+    launch_to_f16pair(at(g.Sh, mn, s0), g.amax + s0, cnt, int64_t(mn), g.S16 + size_t(s0) * mn,
+                      g.S16 + size_t(nb) * mn + size_t(s0) * mn, g.sscale + s0, s);
+    launch_to_f16pair(at(g.Th, mn, s0), g.amax + s0, cnt, int64_t(mn), g.T16 + size_t(s0) * mn,
+                      g.T16 + size_t(nb) * mn + size_t(s0) * mn, g.tscale + s0, s);
+    // R = b R + a/m V^T V
+    p.alpha = float(a / double(g.m));
+    p.C = at(g.R, nn, s0);
+    p.ldc = g.N;
+    p.c_bstride = int64_t(nn);
+    const Operand vtop = op16(g.S16, nb, s0, g.N, g.M, g.sscale);
+    run_gemm(bs, vtop, vtop, cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s, cnt * nf * nf * mf);
+    std::fill(g.v_ok.begin() + s0, g.v_ok.begin() + s0 + cnt, uint8_t(1));
+}
+
 void group_stats(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s) {
     const asg_optimizer_config& o = bs->opt;
     const double mf = g.m, nf = g.n;  // algorithmic flops use the unpadded block
     const bool ema = o.accumulation == ASG_ACCUM_EMA;
     const size_t mn = slabMN(g), mm = slabMM(g), nn = slabNN(g);
+    if (f16_mode(bs)) {
+        group_stats_f16(bs, g, s0, cnt, s);
+        return;
+    }
     GemmParams p{};
     if (!is_kl(bs)) {
         p.alpha = ema ? float(1.0 - o.beta2) : 1.f;
@@ -1118,8 +1229,13 @@ void accumulate_impl(asg_blockset* bs, double clip_scale) {
         // 4 B read per element, hi/lo of G and G^T written (16 B; 8 B in TF32 mode) per padded element
         const double bytes = double(g.nb) * (4.0 * g.m * g.n + (g.Gl ? 16.0 : 8.0) * g.M * g.N);
         hbm_launch(bs, gs, ASG_HBM_PREP, bytes, [&] {
-            launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs,
-                             g.vec_grad);
+            if (f16_mode(bs))  // (+ a 4 B/elt max pass; G, G^T as fp16 pairs: 8 B/elt written)
+                launch_prep_grad_f16(g.d_refs, g.nb, g.M, g.N, float(clip_scale), g.amax2, g.G16,
+                                     g.G16 + size_t(g.nb) * slabMN(g), g.GT16, g.GT16 + size_t(g.nb) * slabMN(g),
+                                     g.gscale, gs);
+            else
+                launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs,
+                                 g.vec_grad);
         });
         group_stats(bs, g, 0, g.nb, gs);
     }
@@ -1155,6 +1271,23 @@ void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, fl
         if (is_kl(bs)) {
             while (r0 < r1 && g.v_ok[size_t(r0)]) ++r0;
             while (r1 > r0 && g.v_ok[size_t(r1 - 1)]) --r1;
+        }
+        if (f16_mode(bs)) {
+            const int nb = g.nb;
+            if (r1 > r0) {
+                CK(cudaMemsetAsync(g.amax + r0, 0, size_t(r1 - r0) * sizeof(unsigned int), s));
+                ps.Dhi = at(g.Th, mn, r0);
+                ps.Dlo = nullptr;
+                ps.omax = g.amax + r0;
+                run_gemm(bs, op16(g.PL16, nb, r0, g.M, g.M, g.plscale), op16(g.GT16, nb, r0, g.N, g.M, g.gscale),
+                         r1 - r0, EPI_SPLIT, ps, nullptr, 0, s, (r1 - r0) * 2.0 * mf * mf * nf);
+                launch_to_f16pair(at(g.Th, mn, r0), g.amax + r0, r1 - r0, int64_t(mn), g.T16 + size_t(r0) * mn,
+                                  g.T16 + size_t(nb) * mn + size_t(r0) * mn, g.tscale + r0, s);
+                if (is_kl(bs)) std::fill(g.v_ok.begin() + r0, g.v_ok.begin() + r1, uint8_t(1));
+            }
+            run_gemm(bs, op16(g.T16, nb, s0, g.M, g.N, g.tscale), op16(g.PR16, nb, s0, g.N, g.N, g.prscale), cnt,
+                     final_epi, pf, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
+            return;
         }
         if (r1 > r0) {
             ps.Dhi = at(g.Th, mn, r0);
@@ -1712,6 +1845,10 @@ void install_roots(asg_blockset* bs, Group& g, int s0, int cnt) {
     cp(at(g.PLl, mm, s0), at(g.sPLl, mm, s0), mm);
     cp(at(g.PRh, nn, s0), at(g.sPRh, nn, s0), nn);
     cp(at(g.PRl, nn, s0), at(g.sPRl, nn, s0), nn);
+    if (f16_mode(bs)) {  // the step's fp16 copies of the installed roots
+        to_f16(g.PLh, g.nb, s0, cnt, int64_t(mm), g.PL16, g.plscale, g.amax2, s);
+        to_f16(g.PRh, g.nb, s0, cnt, int64_t(nn), g.PR16, g.prscale, g.amax2, s);
+    }
     if (is_kl(bs)) std::fill(g.v_ok.begin() + s0, g.v_ok.begin() + s0 + cnt, uint8_t(0));
 }
 
@@ -2009,6 +2146,12 @@ Group& owned_group(asg_blockset* bs, const Unit& u) {
 void prep_single(asg_blockset* bs, Group& g, const Unit& u) {
     const size_t mn = slabMN(g);
     if (!g.v_ok.empty()) g.v_ok[size_t(u.slot)] = 0;
+    if (f16_mode(bs)) {
+        const size_t o = size_t(u.slot) * mn, lo = size_t(g.nb) * mn;
+        launch_prep_grad_f16(bs->d_ref1, 1, g.M, g.N, 1.f, g.amax2 + u.slot, g.G16 + o, g.G16 + lo + o, g.GT16 + o,
+                             g.GT16 + lo + o, g.gscale + u.slot, bs->main);
+        return;
+    }
     launch_prep_grad(bs->d_ref1, 1, g.M, g.N, nullptr, 1.f, at(g.Gh, mn, u.slot), at(g.Gl, mn, u.slot),
                      at(g.GTh, mn, u.slot), at(g.GTl, mn, u.slot), bs->main);
 }
@@ -2165,6 +2308,7 @@ int asg_config_from_json(const char* text, asg_optimizer_config* opt, asg_schedu
                 const std::string p = str(g, "precision");
                 if (p == "3xtf32") prec = ASG_PREC_3XTF32;
                 else if (p == "3xtf32_smem") prec = ASG_PREC_3XTF32_SMEM;
+                else if (p == "3xf16") prec = ASG_PREC_3XF16;
                 else if (p == "tf32") prec = ASG_PREC_TF32;
                 else throw Fail{ASG_ERR_CONFIG_INVALID, "unknown precision: " + p};
             }
@@ -2223,7 +2367,8 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         if (sched->pf != opt->precondition_frequency)
             throw Fail{ASG_ERR_CONFIG_INVALID, "async.pf must equal optimizer.precondition_frequency"};
         if (world < 1 || rank < 0 || rank >= world) throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad rank/world"};
-        if (precision != ASG_PREC_3XTF32 && precision != ASG_PREC_TF32 && precision != ASG_PREC_3XTF32_SMEM)
+        if (precision != ASG_PREC_3XTF32 && precision != ASG_PREC_TF32 && precision != ASG_PREC_3XTF32_SMEM &&
+            precision != ASG_PREC_3XF16)
             throw Fail{ASG_ERR_INVALID_ARGUMENT, "bad precision"};
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
@@ -2863,8 +3008,14 @@ int asg_block_write(asg_blockset* bs, int64_t idx, int32_t role, const double* i
         switch (role) {
             case ASG_ROLE_FACTOR_L: wr32(g.L, slabMM(g), g.M, g.M, m, m, nullptr, nullptr, nullptr); break;
             case ASG_ROLE_FACTOR_R: wr32(g.R, slabNN(g), g.N, g.N, n, n, nullptr, nullptr, nullptr); break;
-            case ASG_ROLE_INV_L: wr32(g.PLh, slabMM(g), g.M, g.M, m, m, sp ? g.PLl : nullptr, nullptr, nullptr); break;
-            case ASG_ROLE_INV_R: wr32(g.PRh, slabNN(g), g.N, g.N, n, n, sp ? g.PRl : nullptr, nullptr, nullptr); break;
+            case ASG_ROLE_INV_L:
+                wr32(g.PLh, slabMM(g), g.M, g.M, m, m, sp ? g.PLl : nullptr, nullptr, nullptr);
+                if (f16_mode(bs)) to_f16(g.PLh, g.nb, u.slot, 1, int64_t(slabMM(g)), g.PL16, g.plscale, g.amax2, bs->main);
+                break;
+            case ASG_ROLE_INV_R:
+                wr32(g.PRh, slabNN(g), g.N, g.N, n, n, sp ? g.PRl : nullptr, nullptr, nullptr);
+                if (f16_mode(bs)) to_f16(g.PRh, g.nb, u.slot, 1, int64_t(slabNN(g)), g.PR16, g.prscale, g.amax2, bs->main);
+                break;
             case ASG_ROLE_KL_INV_L:
             case ASG_ROLE_KL_INV_R:
                 throw Fail{ASG_ERR_INVALID_ARGUMENT,
@@ -3216,6 +3367,21 @@ int asg_gemm_tn(const float* A, const float* B, float* C, int64_t batch, int64_t
         GemmLaunch g{};
         g.A = Operand{Ah, Al, int(M), int(K)};
         g.B = Operand{Bh, Bl, int(N), int(K)};
+        float* scales = nullptr;
+        unsigned int* amax = nullptr;
+        if (precision == ASG_PREC_3XF16) {  // operands as fp16 pairs with per-matrix scales (in the scratch)
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&scales), size_t(batch) * 2 * sizeof(float), s));
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&amax), size_t(batch) * 2 * sizeof(unsigned int), s));
+            launch_absmax(Ah, int(batch), M * K, amax, s);
+            launch_absmax(Bh, int(batch), N * K, amax + batch, s);
+            launch_to_f16pair(Ah, amax, int(batch), M * K, scrA, reinterpret_cast<uint16_t*>(scrA) + na, scales, s);
+            launch_to_f16pair(Bh, amax + batch, int(batch), N * K, scrB, reinterpret_cast<uint16_t*>(scrB) + nbb,
+                              scales + batch, s);
+            g.A = Operand{scrA, reinterpret_cast<const float*>(reinterpret_cast<uint16_t*>(scrA) + na), int(M), int(K),
+                          scales};
+            g.B = Operand{scrB, reinterpret_cast<const float*>(reinterpret_cast<uint16_t*>(scrB) + nbb), int(N),
+                          int(K), scales + batch};
+        }
         g.batch = int(batch);
         g.epi = EPI_STORE;
         g.p.alpha = alpha;
@@ -3223,12 +3389,29 @@ int asg_gemm_tn(const float* A, const float* B, float* C, int64_t batch, int64_t
         g.p.C = C;
         g.p.ldc = N;
         g.p.c_bstride = M * N;
-        // diagnostics: ASG_GEMM_REPEAT = k times the same product (kernel timing by difference)
-        static const int reps = getenv("ASG_GEMM_REPEAT") ? std::max(1, atoi(getenv("ASG_GEMM_REPEAT"))) : 1;
-        for (int r = 0; r < reps; ++r) CK(gemm_launch(g, precision, prop.multiProcessorCount, s));
+        // diagnostics: ASG_GEMM_BENCH_REPS = k > 0 times the product, timed by CUDA events after one
+        // warm-up launch; the mean kernel time goes to stderr (kernel-only, on prepared operands)
+        static const int reps = getenv("ASG_GEMM_BENCH_REPS") ? std::max(0, atoi(getenv("ASG_GEMM_BENCH_REPS"))) : 0;
+        CK(gemm_launch(g, precision, prop.multiProcessorCount, s));
+        if (reps > 0) {
+            cudaEvent_t e0, e1;
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            CK(cudaEventRecord(e0, s));
+            for (int r = 0; r < reps; ++r) CK(gemm_launch(g, precision, prop.multiProcessorCount, s));
+            CK(cudaEventRecord(e1, s));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            std::fprintf(stderr, "asg_gemm_tn bench: %d x (%lld x %lld x %lld x %lld) %.4f ms per launch\n", reps,
+                         (long long)batch, (long long)M, (long long)N, (long long)K, ms / reps);
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
         CK(cudaStreamSynchronize(s));
         for (void* p : {static_cast<void*>(Ah), static_cast<void*>(Al), static_cast<void*>(Bh), static_cast<void*>(Bl),
-                        static_cast<void*>(scrA), static_cast<void*>(scrB), static_cast<void*>(dra), static_cast<void*>(drb)})
+                        static_cast<void*>(scrA), static_cast<void*>(scrB), static_cast<void*>(dra), static_cast<void*>(drb),
+                        static_cast<void*>(scales), static_cast<void*>(amax)})
             if (p) CK(cudaFreeAsync(p, s));
         CK(cudaStreamSynchronize(s));
     });

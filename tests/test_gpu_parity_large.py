@@ -264,7 +264,7 @@ def big_trajectory(method, m, n, steps, pf, S, lr, accumulation, r, first_step=0
     return err
 
 
-PRECS = [abi.PREC_3XTF32, abi.PREC_3XTF32_SMEM]
+PRECS = [abi.PREC_3XTF32, abi.PREC_3XTF32_SMEM, abi.PREC_3XF16]
 
 
 @pytest.mark.parametrize("precision", PRECS)
