@@ -43,7 +43,7 @@ def O():
 
 
 def run_pair(O, method, shapes, limit, pf, steps, seed=0, S=0, lr=1e-2, wd=0.0, clip=1.0, well=True, delay=0.0,
-             refresh_mode=abi.REFRESH_F64, r_scale=1.0):
+             refresh_mode=abi.REFRESH_F64, r_scale=1.0, precision=abi.PREC_3XTF32):
     """GPU step vs the oracle's per-block harness loop (harness.cpp:439-475) with
     the oracle's ShadowScheduler on the same simulated clock."""
     from paper_2605_16184_b200 import runtime
@@ -56,7 +56,7 @@ def run_pair(O, method, shapes, limit, pf, steps, seed=0, S=0, lr=1e-2, wd=0.0, 
     thetas0 = [0.1 * rng.standard_normal(s) for s in shapes]
     params = [torch.tensor(t, dtype=torch.float32, device="cuda") for t in thetas0]
     grads = [torch.zeros_like(p) for p in params]
-    o = O.AsteriaOptimizer(params, grads, opt, sched)
+    o = O.AsteriaOptimizer(params, grads, opt, sched, precision=precision)
     osched = orc.Scheduler(opt, sched, seed=1)
     ref, all_blocks = [], []
     for t in thetas0:
@@ -128,6 +128,18 @@ def test_trajectory_matches_oracle_bounded_staleness(O, method):
     errs, o = run_pair(O, method, shapes, limit=128, pf=4, steps=10, S=3, delay=2.0)
     assert o.num_blocks == 6 + 1 + 1 + 1
     assert o.stats().installed >= 2 * 8
+    assert max(errs) <= 1.0, errs
+
+
+@pytest.mark.parametrize("precision", [abi.PREC_3XF16, abi.PREC_3XTF32_SMEM])
+@pytest.mark.parametrize("method", [abi.SHAMPOO, abi.SOAP, abi.KL_SHAMPOO])
+def test_trajectory_operand_storage_modes(O, method, precision):
+    """The same bounded-staleness trajectories with the step's operands stored
+    as scaled fp16 (hi, lo) pairs multiplied by kind::f16 (3XF16; SOAP runs its
+    chain as 3XTF32_SMEM there) and as plain fp32 split in shared memory
+    (3XTF32_SMEM): the 3xTF32 tolerances hold unchanged."""
+    shapes = [(256, 384), (300,), (96, 96), (72, 72)]
+    errs, o = run_pair(O, method, shapes, limit=128, pf=4, steps=10, S=3, delay=2.0, precision=precision)
     assert max(errs) <= 1.0, errs
 
 

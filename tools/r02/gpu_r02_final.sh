@@ -15,3 +15,8 @@ print(sys.argv[1], round(d["value"], 2), round(d["ms_per_step"], 2), d["step_ms"
 PY
 done
 timeout 900 python bench.py --workload C3 --impl reference --steps 3 --warmup 1 > gpurun_out/r02_${TAG}_C3_reference.jsonl 2>&1; tail -c 300 gpurun_out/r02_${TAG}_C3_reference.jsonl
+bash tools/r02/gpu_r02_ncu_traffic.sh 2>&1 | grep -E "gemm_tn|wrote" | cut -c1-200
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --csv --log-file /tmp/ncu/c3final.csv \
+  python bench.py --steps 2 --warmup 8 --no-e2e --no-cpu-baseline > /tmp/ncu/c3final.log 2>&1
+python profiles/launch_summary.py /tmp/ncu/c3final.csv > gpurun_out/r02_bench_C3_ncu_launches_${TAG}.txt 2>&1
+head -14 gpurun_out/r02_bench_C3_ncu_launches_${TAG}.txt
