@@ -42,6 +42,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "asg_ptx.cuh"
@@ -100,6 +101,8 @@ struct GemmParams {
     unsigned int* omax;   // optional: per-batch max |output| (float bits, atomicMax) of SPLIT / SPLIT2
     int sym_T;            // CTA-pair symmetric schedules: T x T tile grid, lower triangle decoded
                           // arithmetically (tile_list unused)
+    const float* oscale;  // SPLIT / SPLIT2 fp16-pair output: D (and D^T) are written as scaled fp16
+                          // (hi, lo) pairs, __half arrays at Dhi/Dlo (Thi/Tlo), value * oscale[b]
 };
 
 __device__ __forceinline__ bool batch_skipped(const GemmParams& p, int t) {
@@ -342,6 +345,32 @@ __device__ __forceinline__ void rows_chunk(const GemmParams& p, int b, int row0,
     __syncwarp();
     const int c = col0 + int(lane);
     if constexpr (EPI == EPI_SPLIT || EPI == EPI_SPLIT2) {
+        if (p.oscale) {  // fp16 (hi, lo) pairs at a scale fixed before the product (a bound on |D|)
+            const float os = p.oscale[b];
+            const int64_t o = int64_t(b) * p.d_bstride + int64_t(row0) * p.ldd + c;
+            __half* dh = reinterpret_cast<__half*>(p.Dhi) + o;
+            __half* dl = reinterpret_cast<__half*>(p.Dlo) + o;
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i) {
+                const float y = scratch[i][lane] * os;
+                const __half h = __float2half_rn(y);
+                dh[int64_t(i) * p.ldd] = h;
+                dl[int64_t(i) * p.ldd] = __float2half_rn(y - __half2float(h));
+            }
+            if constexpr (EPI == EPI_SPLIT2) {
+                const int64_t ot = int64_t(b) * p.d_bstride + int64_t(col0) * p.ldt + row0 + int(lane);
+                __half* th = reinterpret_cast<__half*>(p.Thi) + ot;
+                __half* tl = reinterpret_cast<__half*>(p.Tlo) + ot;
+#pragma unroll 8
+                for (int j = 0; j < 32; ++j) {
+                    const float y = scratch[lane][j] * os;
+                    const __half h = __float2half_rn(y);
+                    th[int64_t(j) * p.ldt] = h;
+                    tl[int64_t(j) * p.ldt] = __float2half_rn(y - __half2float(h));
+                }
+            }
+            return;
+        }
         if (p.omax) {  // per-batch max |D| for the next product's fp16 scale
             float mx = 0.f;
 #pragma unroll 8

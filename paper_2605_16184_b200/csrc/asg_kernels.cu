@@ -1249,17 +1249,35 @@ __device__ __forceinline__ void f16_split(float y, __half& h, __half& l) {
     l = __float2half_rn(y - __half2float(h));
 }
 
-__global__ void absmax_kernel(const float* __restrict__ src, int64_t per, unsigned int* __restrict__ amax) {
+__device__ __forceinline__ float absmax4(const float4 v) {
+    const float m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+    return isfinite(v.x + v.y + v.z + v.w) ? m : __int_as_float(0x7f800000);
+}
+// one atomic per CTA (256 threads)
+__device__ __forceinline__ void block_max_atomic(float m, unsigned int* dst) {
+    __shared__ float red[8];
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+        atomicMax(dst, __float_as_uint(m));
+    }
+}
+
+__global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ src, int64_t per,
+                                                     unsigned int* __restrict__ amax) {
     const int64_t b = blockIdx.y;
     const float4* p4 = reinterpret_cast<const float4*>(src + b * per);
+    const int64_t n4 = per / 4, stride = int64_t(gridDim.x) * blockDim.x;
     float m = 0.f;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per / 4; i += int64_t(gridDim.x) * blockDim.x) {
-        const float4 v = p4[i];
-        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-        if (!isfinite(v.x + v.y + v.z + v.w)) m = __int_as_float(0x7f800000);
+    int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < n4; i += 4 * stride) {  // four loads in flight per thread
+        const float4 v0 = p4[i], v1 = p4[i + stride], v2 = p4[i + 2 * stride], v3 = p4[i + 3 * stride];
+        m = fmaxf(m, fmaxf(fmaxf(absmax4(v0), absmax4(v1)), fmaxf(absmax4(v2), absmax4(v3))));
     }
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(amax + b, __float_as_uint(m));
+    for (; i < n4; i += stride) m = fmaxf(m, absmax4(p4[i]));
+    block_max_atomic(m, amax + b);
 }
 
 __global__ void to_f16pair_kernel(const float* __restrict__ src, const unsigned int* __restrict__ amax, int64_t per,
@@ -1278,6 +1296,46 @@ __global__ void to_f16pair_kernel(const float* __restrict__ src, const unsigned 
         *reinterpret_cast<uint2*>(hi + b * per + 4 * i) = *reinterpret_cast<const uint2*>(h);
         *reinterpret_cast<uint2*>(lo + b * per + 4 * i) = *reinterpret_cast<const uint2*>(l);
     }
+}
+
+// max over columns of sum_i |P_ij| (the 1-norm) of each n x n slot, as float bits.
+// 32 x 32 threads per 32-column strip: warp y sums rows y, y+32, ... (one 128-byte row
+// segment per load), the 32 partial sums of a column are combined in shared memory.
+__global__ void __launch_bounds__(1024) colabs_max_kernel(const float* __restrict__ src, int n, int64_t per,
+                                                          unsigned int* __restrict__ out) {
+    __shared__ float part[32][33];
+    const int j = blockIdx.x * 32 + threadIdx.x;
+    const float* p = src + int64_t(blockIdx.y) * per;
+    float a0 = 0.f, a1 = 0.f;
+    if (j < n) {
+        int i = threadIdx.y;
+        for (; i + 32 < n; i += 64) {
+            a0 += fabsf(p[int64_t(i) * n + j]);
+            a1 += fabsf(p[int64_t(i + 32) * n + j]);
+        }
+        if (i < n) a0 += fabsf(p[int64_t(i) * n + j]);
+    }
+    part[threadIdx.y][threadIdx.x] = a0 + a1;
+    __syncthreads();
+    if (threadIdx.y == 0) {
+        float c = 0.f;
+        for (int y = 0; y < 32; ++y) c += part[y][threadIdx.x];
+        if (!isfinite(c)) c = __int_as_float(0x7f800000);
+        for (int o = 16; o > 0; o >>= 1) c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, o));
+        if (threadIdx.x == 0) atomicMax(out + blockIdx.y, __float_as_uint(c));
+    }
+}
+
+// the fp16 output scale of D = A B with |D_ij| <= max|A| ||B||_1: max|A| < 2^15 / ascale (the
+// fp16 scale of A puts max|A| ascale in [2^14, 2^15)), so D's bound is 2^15 ||B||_1 / ascale
+__global__ void bound_scale_kernel(int nb, const float* __restrict__ ascale, const unsigned int* __restrict__ n1,
+                                   float* __restrict__ out0, float* __restrict__ out1) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const float bound = 32768.f / ascale[b] * __uint_as_float(n1[b]);
+    const float s = f16_scale(__float_as_uint(bound));
+    out0[b] = s;
+    if (out1) out1[b] = s;
 }
 
 // max |x| over each gradient block's view (rows x cols of the caller's tensor)
@@ -1325,12 +1383,95 @@ __global__ void prep_grad_f16_kernel(const BlockRef* __restrict__ blocks, int M,
         GTl[b * slab + int64_t(jj) * M + ii] = l;
     }
 }
+// float4 variants for blocks whose rows are 16-byte aligned (BlockRef src, ld, cols % 4 == 0)
+// (rows x cols/4) float4 cells of the block flattened, four loads in flight per thread
+__global__ void __launch_bounds__(256) block_absmax_vec_kernel(const BlockRef* __restrict__ blocks,
+                                                               unsigned int* __restrict__ amax) {
+    const BlockRef blk = blocks[blockIdx.y];
+    const int c4 = blk.cols / 4;
+    const int64_t n4 = int64_t(blk.rows) * c4, stride = int64_t(gridDim.x) * blockDim.x;
+    auto at = [&](int64_t q) {
+        const int64_t r = q / c4;
+        return *reinterpret_cast<const float4*>(blk.src + r * blk.ld + 4 * (q - r * c4));
+    };
+    float m = 0.f;
+    int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    for (; q + 3 * stride < n4; q += 4 * stride) {
+        const float4 v0 = at(q), v1 = at(q + stride), v2 = at(q + 2 * stride), v3 = at(q + 3 * stride);
+        m = fmaxf(m, fmaxf(fmaxf(absmax4(v0), absmax4(v1)), fmaxf(absmax4(v2), absmax4(v3))));
+    }
+    for (; q < n4; q += stride) m = fmaxf(m, absmax4(at(q)));
+    block_max_atomic(m, amax + blockIdx.y);
+}
+
+// 64 x 64 tiles, 16 x 16 threads: float4 loads, 8-byte fp16 stores of 4 (hi, lo) values per row segment
+__global__ void __launch_bounds__(256) prep_grad_f16_vec_kernel(const BlockRef* __restrict__ blocks, int M, int N,
+                                                                float scale_val, const unsigned int* __restrict__ amax,
+                                                                __half* __restrict__ Gh, __half* __restrict__ Gl,
+                                                                __half* __restrict__ GTh, __half* __restrict__ GTl,
+                                                                float* __restrict__ gscale) {
+    __shared__ float t[64][65];
+    const int b = blockIdx.z;
+    const BlockRef blk = blocks[b];
+    const float s = f16_scale(__float_as_uint(__uint_as_float(amax[b]) * scale_val));
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) gscale[b] = s;
+    const float f = scale_val * s;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int j0 = blockIdx.x * 64, i0 = blockIdx.y * 64;
+    const int64_t slab = int64_t(M) * N;
+    auto put4 = [](__half* hp, __half* lp, float a, float bb, float c, float d) {
+        __half h[4], l[4];
+        f16_split(a, h[0], l[0]);
+        f16_split(bb, h[1], l[1]);
+        f16_split(c, h[2], l[2]);
+        f16_split(d, h[3], l[3]);
+        *reinterpret_cast<uint2*>(hp) = *reinterpret_cast<const uint2*>(h);
+        *reinterpret_cast<uint2*>(lp) = *reinterpret_cast<const uint2*>(l);
+    };
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int i = i0 + ty + 16 * r, j = j0 + tx * 4;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < blk.rows && j < blk.cols) x = *reinterpret_cast<const float4*>(blk.src + int64_t(i) * blk.ld + j);
+        x = make_float4(f * x.x, f * x.y, f * x.z, f * x.w);
+        const int64_t o = b * slab + int64_t(i) * N + j;
+        put4(Gh + o, Gl + o, x.x, x.y, x.z, x.w);
+        const int rr = ty + 16 * r, cc = tx * 4;
+        t[rr][cc] = x.x;
+        t[rr][cc + 1] = x.y;
+        t[rr][cc + 2] = x.z;
+        t[rr][cc + 3] = x.w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int jj = j0 + ty + 16 * r, ii = i0 + tx * 4;  // GT[jj][ii..ii+3] = G[ii..ii+3][jj]
+        const int cc = ty + 16 * r, rr = tx * 4;
+        const int64_t o = b * slab + int64_t(jj) * M + ii;
+        put4(GTh + o, GTl + o, t[rr][cc], t[rr + 1][cc], t[rr + 2][cc], t[rr + 3][cc]);
+    }
+}
 }  // namespace
+
+void launch_colabs_max(const float* src, int nb, int n, int64_t per, unsigned int* out, cudaStream_t s) {
+    if (nb <= 0) return;
+    cudaMemsetAsync(out, 0, size_t(nb) * sizeof(unsigned int), s);
+    colabs_max_kernel<<<dim3((n + 31) / 32, nb), dim3(32, 32), 0, s>>>(src, n, per, out);
+    count_launch(1);
+}
+
+void launch_bound_scale(int nb, const float* ascale, const unsigned int* n1, float* out0, float* out1, cudaStream_t s) {
+    if (nb <= 0) return;
+    bound_scale_kernel<<<(nb + 127) / 128, 128, 0, s>>>(nb, ascale, n1, out0, out1);
+    count_launch(1);
+}
 
 void launch_absmax(const float* src, int nb, int64_t per, unsigned int* amax, cudaStream_t s) {
     if (nb <= 0) return;
     cudaMemsetAsync(amax, 0, size_t(nb) * sizeof(unsigned int), s);
-    const int64_t blocks = std::min<int64_t>(1024, (per / 4 + 255) / 256);
+    // about 8 CTAs per SM over the whole batch, each thread with >= 16 float4 of work
+    const int64_t want = (8 * 148 + nb - 1) / nb;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(want, (per / 4 + 4095) / 4096));
     absmax_kernel<<<dim3(unsigned(blocks > 0 ? blocks : 1), nb), 256, 0, s>>>(src, per, amax);
     count_launch();
 }
@@ -1345,13 +1486,22 @@ void launch_to_f16pair(const float* src, const unsigned int* amax, int nb, int64
 }
 
 void launch_prep_grad_f16(const BlockRef* blocks_dev, int nb, int M, int N, float scale_val, unsigned int* amax,
-                          void* Gh16, void* Gl16, void* GTh16, void* GTl16, float* gscale, cudaStream_t s) {
+                          void* Gh16, void* Gl16, void* GTh16, void* GTl16, float* gscale, cudaStream_t s, bool vec) {
     if (nb <= 0) return;
     cudaMemsetAsync(amax, 0, size_t(nb) * sizeof(unsigned int), s);
-    block_absmax_kernel<<<dim3(std::min(M, 256), nb), 256, 0, s>>>(blocks_dev, amax);
-    prep_grad_f16_kernel<<<dim3(N / 32, M / 32, nb), dim3(32, 8), 0, s>>>(
-        blocks_dev, M, N, scale_val, amax, static_cast<__half*>(Gh16), static_cast<__half*>(Gl16),
-        static_cast<__half*>(GTh16), static_cast<__half*>(GTl16), gscale);
+    if (vec && M % 64 == 0 && N % 64 == 0) {
+        const int want = (8 * 148 + nb - 1) / nb;
+        const int gx = std::max(1, std::min(want, int((int64_t(M) * N / 4 + 4095) / 4096)));
+        block_absmax_vec_kernel<<<dim3(gx, nb), 256, 0, s>>>(blocks_dev, amax);
+        prep_grad_f16_vec_kernel<<<dim3(N / 64, M / 64, nb), dim3(16, 16), 0, s>>>(
+            blocks_dev, M, N, scale_val, amax, static_cast<__half*>(Gh16), static_cast<__half*>(Gl16),
+            static_cast<__half*>(GTh16), static_cast<__half*>(GTl16), gscale);
+    } else {
+        block_absmax_kernel<<<dim3(std::min(M, 256), nb), 256, 0, s>>>(blocks_dev, amax);
+        prep_grad_f16_kernel<<<dim3(N / 32, M / 32, nb), dim3(32, 8), 0, s>>>(
+            blocks_dev, M, N, scale_val, amax, static_cast<__half*>(Gh16), static_cast<__half*>(Gl16),
+            static_cast<__half*>(GTh16), static_cast<__half*>(GTl16), gscale);
+    }
     count_launch(2);
 }
 

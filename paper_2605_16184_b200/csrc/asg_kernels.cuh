@@ -162,13 +162,18 @@ void launch_merge_status(const int* in, int cnt, int* out, cudaStream_t s);
 // (1 for an all-zero or non-finite max), hi = rn_f16(x s), lo = rn_f16(x s - hi).
 // Per-batch max |x| of [nb][per] fp32 slabs into amax (float bits; zeroed first).
 void launch_absmax(const float* src, int nb, int64_t per, unsigned int* amax, cudaStream_t s);
+// per-slot max column abs-sum (1-norm) of n x n fp32 slots, float bits
+void launch_colabs_max(const float* src, int nb, int n, int64_t per, unsigned int* out, cudaStream_t s);
+// out0[b] (= out1[b] when given) = fp16 scale of a product bounded by 2^15 n1[b] / ascale[b]
+void launch_bound_scale(int nb, const float* ascale, const unsigned int* n1, float* out0, float* out1, cudaStream_t s);
 // [nb][per] fp32 -> fp16 pairs hi16 / lo16 ([nb][per] each) and the scales.
 void launch_to_f16pair(const float* src, const unsigned int* amax, int nb, int64_t per, void* hi16, void* lo16,
                        float* scale, cudaStream_t s);
 // Gradient blocks (caller layout, times scale_val) -> fp16 pairs of G [b][M][N] and
 // G^T [b][N][M] with per-block scales (a max pass over the blocks first).
 void launch_prep_grad_f16(const BlockRef* blocks_dev, int nb, int M, int N, float scale_val, unsigned int* amax,
-                          void* Gh16, void* Gl16, void* GTh16, void* GTl16, float* gscale, cudaStream_t s);
+                          void* Gh16, void* Gl16, void* GTh16, void* GTl16, float* gscale, cudaStream_t s,
+                          bool vec = false);
 
 // Multi-GPU: pack owned block slices into a contiguous buffer and back.
 void launch_pack_blocks(const BlockRef* blocks_dev, const int64_t* offsets_dev, int nb, float* out,

@@ -196,6 +196,7 @@ struct Group {
     uint16_t *G16 = nullptr, *GT16 = nullptr, *T16 = nullptr, *S16 = nullptr, *PL16 = nullptr, *PR16 = nullptr;
     float *gscale = nullptr, *tscale = nullptr, *sscale = nullptr, *plscale = nullptr, *prscale = nullptr;
     unsigned int *amax = nullptr, *amax2 = nullptr;  // per-block max |x| scratch
+    unsigned int *pln1 = nullptr, *prn1 = nullptr;   // per-block 1-norm of the fp16 roots (float bits)
     // SOAP
     float *QLh = nullptr, *QLl = nullptr, *QLTh = nullptr, *QLTl = nullptr;
     float *QRh = nullptr, *QRl = nullptr, *QRTh = nullptr, *QRTl = nullptr;
@@ -397,7 +398,7 @@ bool split_mode(const asg_blockset* bs) { return bs->precision == ASG_PREC_3XTF3
 // the refresh's internal tensor-core Jacobi works on (hi, lo) pairs in both 3xTF32 modes
 bool work_split(const asg_blockset* bs) { return bs->precision != ASG_PREC_TF32; }
 void to_f16(const float* src, int nb, int s0, int cnt, int64_t per, uint16_t* dst, float* scale, unsigned int* amax,
-            cudaStream_t s);
+            cudaStream_t s, unsigned int* n1 = nullptr, int n = 0);
 // 3XF16: the Shampoo / KL-Shampoo step chains on fp16 pairs (SOAP runs as 3XTF32_SMEM)
 bool f16_mode(const asg_blockset* bs) {
     return bs->precision == ASG_PREC_3XF16 && bs->opt.method != ASG_METHOD_SOAP;
@@ -554,13 +555,17 @@ void alloc_group(asg_blockset* bs, Group& g) {
     if (f16_mode(bs)) {
         g.G16 = reinterpret_cast<uint16_t*>(g.Gh);  // prep writes fp16 pairs; no fp32 G in this mode
         g.GT16 = reinterpret_cast<uint16_t*>(g.GTh);
-        g.T16 = reinterpret_cast<uint16_t*>(dalloc<float>(bs, nb * slabMN(g)));
-        if (is_kl(bs)) g.S16 = reinterpret_cast<uint16_t*>(dalloc<float>(bs, nb * slabMN(g)));
+        // the step's products are written as fp16 pairs straight from the GEMM epilogue, so
+        // the fp32 T slab holds T16; KL's V^T pairs (S16) alias G16, dead once W = G P_R is formed
+        g.T16 = reinterpret_cast<uint16_t*>(g.Th);
+        if (is_kl(bs)) g.S16 = g.G16;
         g.PL16 = reinterpret_cast<uint16_t*>(dalloc<float>(bs, nb * slabMM(g)));
         g.PR16 = reinterpret_cast<uint16_t*>(dalloc<float>(bs, nb * slabNN(g)));
         for (float** sc : {&g.gscale, &g.tscale, &g.sscale, &g.plscale, &g.prscale}) *sc = dalloc<float>(bs, nb);
         g.amax = dalloc<unsigned int>(bs, nb);
         g.amax2 = dalloc<unsigned int>(bs, nb);
+        g.pln1 = dalloc<unsigned int>(bs, nb);
+        g.prn1 = dalloc<unsigned int>(bs, nb);
     }
     auto pair_mm = [&](float*& h, float*& l) {
         h = dalloc<float>(bs, nb * slabMM(g));
@@ -629,8 +634,8 @@ void alloc_group(asg_blockset* bs, Group& g) {
         launch_identity_split(g.PLh, g.PLl, g.nb, g.M, g.m, s);
         launch_identity_split(g.PRh, g.PRl, g.nb, g.N, g.n, s);
         if (f16_mode(bs)) {
-            to_f16(g.PLh, g.nb, 0, g.nb, int64_t(slabMM(g)), g.PL16, g.plscale, g.amax, s);
-            to_f16(g.PRh, g.nb, 0, g.nb, int64_t(slabNN(g)), g.PR16, g.prscale, g.amax, s);
+            to_f16(g.PLh, g.nb, 0, g.nb, int64_t(slabMM(g)), g.PL16, g.plscale, g.amax, s, g.pln1, g.M);
+            to_f16(g.PRh, g.nb, 0, g.nb, int64_t(slabNN(g)), g.PR16, g.prscale, g.amax, s, g.prn1, g.N);
         }
         if (f32_refresh(bs) && !newton_roots(bs)) {  // basis of the last refresh, identity before the first
             pair_mm(g.BLh, g.BLl);
@@ -761,8 +766,11 @@ Operand op16(const uint16_t* base, int nb, int s0, int rows, int K, const float*
 }
 // fp32 slots [s0, s0+cnt) (rows x K each) -> fp16 pairs + scales of the same slots
 void to_f16(const float* src, int nb, int s0, int cnt, int64_t per, uint16_t* dst, float* scale, unsigned int* amax,
-            cudaStream_t s) {
+            cudaStream_t s, unsigned int* n1, int n) {
     launch_absmax(src + size_t(s0) * per, cnt, per, amax + s0, s);
+    // a root's 1-norm bounds the products it enters (|G P|_ij <= max|G| |P|_1): the fp16
+    // scale of those products is fixed before them, so they write fp16 pairs directly
+    if (n1) launch_colabs_max(src + size_t(s0) * per, cnt, n, per, n1 + s0, s);
     launch_to_f16pair(src + size_t(s0) * per, amax + s0, cnt, per, dst + size_t(s0) * per,
                       dst + size_t(nb) * per + size_t(s0) * per, scale + s0, s);
 }
@@ -1109,18 +1117,17 @@ void group_stats_f16(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s
         run_gemm(bs, gtop, gtop, cnt, EPI_SYM_EMA, p, g.tilesN, g.ntN, s, cnt * nf * nf * mf);
         return;
     }
-    // W = G P_R (fp32, max) -> T16 ; L = b L + a/n W W^T
-    CK(cudaMemsetAsync(g.amax + s0, 0, size_t(cnt) * sizeof(unsigned int), s));
+    // W = G P_R -> T16 (fp16 pairs at the scale of the bound max|G| |P_R|_1) ; L = b L + a/n W W^T
     GemmParams px{};
     px.alpha = 1.f;
-    px.Dhi = at(g.Th, mn, s0);
     px.ldd = g.N;
     px.d_bstride = int64_t(mn);
-    px.omax = g.amax + s0;
+    launch_bound_scale(cnt, g.gscale + s0, g.prn1 + s0, g.tscale + s0, nullptr, s);
+    px.Dhi = reinterpret_cast<float*>(g.T16 + size_t(s0) * mn);
+    px.Dlo = reinterpret_cast<float*>(g.T16 + size_t(nb) * mn + size_t(s0) * mn);
+    px.oscale = g.tscale + s0;
     run_gemm(bs, op16(g.G16, nb, s0, g.M, g.N, g.gscale), op16(g.PR16, nb, s0, g.N, g.N, g.prscale), cnt, EPI_SPLIT,
              px, nullptr, 0, s, cnt * 2.0 * mf * nf * nf);
-    launch_to_f16pair(at(g.Th, mn, s0), g.amax + s0, cnt, int64_t(mn), g.T16 + size_t(s0) * mn,
-                      g.T16 + size_t(nb) * mn + size_t(s0) * mn, g.tscale + s0, s);
     const double a = ema ? (1.0 - o.beta2) : 1.0;
     p.alpha = float(a / double(g.n));
     p.C = at(g.L, mm, s0);
@@ -1128,19 +1135,17 @@ void group_stats_f16(asg_blockset* bs, Group& g, int s0, int cnt, cudaStream_t s
     p.c_bstride = int64_t(mm);
     const Operand wop = op16(g.T16, nb, s0, g.M, g.N, g.tscale);
     run_gemm(bs, wop, wop, cnt, EPI_SYM_EMA, p, g.tilesM, g.ntM, s, cnt * mf * mf * nf);
-    // V^T = G^T P_L (fp32 into S, which aliases G: dead once W is formed) and V (fp32 into T), one max
-    CK(cudaMemsetAsync(g.amax + s0, 0, size_t(cnt) * sizeof(unsigned int), s));
-    px.Dhi = at(g.Sh, mn, s0);
+    // V^T = G^T P_L -> S16 and V -> T16, fp16 pairs at the scale of the bound max|G| |P_L|_1
+    launch_bound_scale(cnt, g.gscale + s0, g.pln1 + s0, g.sscale + s0, g.tscale + s0, s);
+    px.Dhi = reinterpret_cast<float*>(g.S16 + size_t(s0) * mn);
+    px.Dlo = reinterpret_cast<float*>(g.S16 + size_t(nb) * mn + size_t(s0) * mn);
     px.ldd = g.M;
-    px.Thi = at(g.Th, mn, s0);
-    px.Tlo = nullptr;
+    px.Thi = reinterpret_cast<float*>(g.T16 + size_t(s0) * mn);
+    px.Tlo = reinterpret_cast<float*>(g.T16 + size_t(nb) * mn + size_t(s0) * mn);
     px.ldt = g.N;
+    px.oscale = g.sscale + s0;
     run_gemm(bs, op16(g.GT16, nb, s0, g.N, g.M, g.gscale), op16(g.PL16, nb, s0, g.M, g.M, g.plscale), cnt, EPI_SPLIT2,
              px, nullptr, 0, s, cnt * 2.0 * nf * mf * mf);
-    launch_to_f16pair(at(g.Sh, mn, s0), g.amax + s0, cnt, int64_t(mn), g.S16 + size_t(s0) * mn,
-                      g.S16 + size_t(nb) * mn + size_t(s0) * mn, g.sscale + s0, s);
-    launch_to_f16pair(at(g.Th, mn, s0), g.amax + s0, cnt, int64_t(mn), g.T16 + size_t(s0) * mn,
-                      g.T16 + size_t(nb) * mn + size_t(s0) * mn, g.tscale + s0, s);
     // R = b R + a/m V^T V
     p.alpha = float(a / double(g.m));
     p.C = at(g.R, nn, s0);
@@ -1232,7 +1237,7 @@ void accumulate_impl(asg_blockset* bs, double clip_scale) {
             if (f16_mode(bs))  // (+ a 4 B/elt max pass; G, G^T as fp16 pairs: 8 B/elt written)
                 launch_prep_grad_f16(g.d_refs, g.nb, g.M, g.N, float(clip_scale), g.amax2, g.G16,
                                      g.G16 + size_t(g.nb) * slabMN(g), g.GT16, g.GT16 + size_t(g.nb) * slabMN(g),
-                                     g.gscale, gs);
+                                     g.gscale, gs, g.vec_grad);
             else
                 launch_prep_grad(g.d_refs, g.nb, g.M, g.N, nullptr, float(clip_scale), g.Gh, g.Gl, g.GTh, g.GTl, gs,
                                  g.vec_grad);
@@ -1275,14 +1280,12 @@ void group_update(asg_blockset* bs, Group& g, int s0, int cnt, int final_epi, fl
         if (f16_mode(bs)) {
             const int nb = g.nb;
             if (r1 > r0) {
-                CK(cudaMemsetAsync(g.amax + r0, 0, size_t(r1 - r0) * sizeof(unsigned int), s));
-                ps.Dhi = at(g.Th, mn, r0);
-                ps.Dlo = nullptr;
-                ps.omax = g.amax + r0;
+                launch_bound_scale(r1 - r0, g.gscale + r0, g.pln1 + r0, g.tscale + r0, nullptr, s);
+                ps.Dhi = reinterpret_cast<float*>(g.T16 + size_t(r0) * mn);
+                ps.Dlo = reinterpret_cast<float*>(g.T16 + size_t(nb) * mn + size_t(r0) * mn);
+                ps.oscale = g.tscale + r0;
                 run_gemm(bs, op16(g.PL16, nb, r0, g.M, g.M, g.plscale), op16(g.GT16, nb, r0, g.N, g.M, g.gscale),
                          r1 - r0, EPI_SPLIT, ps, nullptr, 0, s, (r1 - r0) * 2.0 * mf * mf * nf);
-                launch_to_f16pair(at(g.Th, mn, r0), g.amax + r0, r1 - r0, int64_t(mn), g.T16 + size_t(r0) * mn,
-                                  g.T16 + size_t(nb) * mn + size_t(r0) * mn, g.tscale + r0, s);
                 if (is_kl(bs)) std::fill(g.v_ok.begin() + r0, g.v_ok.begin() + r1, uint8_t(1));
             }
             run_gemm(bs, op16(g.T16, nb, s0, g.M, g.N, g.tscale), op16(g.PR16, nb, s0, g.N, g.N, g.prscale), cnt,
@@ -1846,8 +1849,8 @@ void install_roots(asg_blockset* bs, Group& g, int s0, int cnt) {
     cp(at(g.PRh, nn, s0), at(g.sPRh, nn, s0), nn);
     cp(at(g.PRl, nn, s0), at(g.sPRl, nn, s0), nn);
     if (f16_mode(bs)) {  // the step's fp16 copies of the installed roots
-        to_f16(g.PLh, g.nb, s0, cnt, int64_t(mm), g.PL16, g.plscale, g.amax2, s);
-        to_f16(g.PRh, g.nb, s0, cnt, int64_t(nn), g.PR16, g.prscale, g.amax2, s);
+        to_f16(g.PLh, g.nb, s0, cnt, int64_t(mm), g.PL16, g.plscale, g.amax2, s, g.pln1, g.M);
+        to_f16(g.PRh, g.nb, s0, cnt, int64_t(nn), g.PR16, g.prscale, g.amax2, s, g.prn1, g.N);
     }
     if (is_kl(bs)) std::fill(g.v_ok.begin() + s0, g.v_ok.begin() + s0 + cnt, uint8_t(0));
 }
@@ -3010,11 +3013,13 @@ int asg_block_write(asg_blockset* bs, int64_t idx, int32_t role, const double* i
             case ASG_ROLE_FACTOR_R: wr32(g.R, slabNN(g), g.N, g.N, n, n, nullptr, nullptr, nullptr); break;
             case ASG_ROLE_INV_L:
                 wr32(g.PLh, slabMM(g), g.M, g.M, m, m, sp ? g.PLl : nullptr, nullptr, nullptr);
-                if (f16_mode(bs)) to_f16(g.PLh, g.nb, u.slot, 1, int64_t(slabMM(g)), g.PL16, g.plscale, g.amax2, bs->main);
+                if (f16_mode(bs)) to_f16(g.PLh, g.nb, u.slot, 1, int64_t(slabMM(g)), g.PL16, g.plscale, g.amax2, bs->main,
+                                          g.pln1, g.M);
                 break;
             case ASG_ROLE_INV_R:
                 wr32(g.PRh, slabNN(g), g.N, g.N, n, n, sp ? g.PRl : nullptr, nullptr, nullptr);
-                if (f16_mode(bs)) to_f16(g.PRh, g.nb, u.slot, 1, int64_t(slabNN(g)), g.PR16, g.prscale, g.amax2, bs->main);
+                if (f16_mode(bs)) to_f16(g.PRh, g.nb, u.slot, 1, int64_t(slabNN(g)), g.PR16, g.prscale, g.amax2, bs->main,
+                                          g.prn1, g.N);
                 break;
             case ASG_ROLE_KL_INV_L:
             case ASG_ROLE_KL_INV_R:
