@@ -173,7 +173,7 @@ def traffic_for(workload, precision="3xtf32"):
     """DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) per launch of
     the dominant kernel, from the newest committed `ncu --set full` capture
     summary (profiles/r02_traffic.json, else r01; written by profiles/ncu_traffic.py)."""
-    key = workload + ("_smem" if precision == "3xtf32_smem" else "")
+    key = workload + {"3xtf32_smem": "_smem", "3xf16": "_f16"}.get(precision, "")
     d = None
     for name in ("r02_traffic.json", "r01_traffic.json"):
         p = os.path.join(ROOT, "profiles", name)
@@ -307,6 +307,7 @@ def run_c5(args, rank, world, local):
     import ctypes as C
     import torch
     import torch.distributed as dist
+    from paper_2605_16184_b200 import abi
     from paper_2605_16184_b200 import runtime as rt
     n = args.n
     total = (1 << 31) // (n * n)
@@ -328,13 +329,15 @@ def run_c5(args, rank, world, local):
     stream = torch.cuda.current_stream(dev)
 
     newton = args.refresh == "newton"
+    # NEWTON iterates: 3xFP16 (auto) or 3xTF32 pairs
+    nprec = abi.PREC_3XTF32 if args.precision in ("3xtf32", "3xtf32_smem") else abi.PREC_3XF16
 
     def solve():
         if not mine:
             return
         if newton:  # KL-Shampoo's L^-1/2 (p = 2) of every factor, relative damping 1e-8
             rt.check(rt.lib.asg_inv_root_batched_f32(C.c_void_p(a.data_ptr()), C.c_void_p(v.data_ptr()), mine, n, 2,
-                                                     1e-8, 0, C.c_void_p(stream.cuda_stream or 1)))
+                                                     1e-8, nprec, C.c_void_p(stream.cuda_stream or 1)))
         else:
             rt.check(rt.lib.asg_sym_eig_batched_f32(C.c_void_p(a.data_ptr()), C.c_void_p(w.data_ptr()),
                                                     C.c_void_p(v.data_ptr()), mine, n, C.c_void_p(stream.cuda_stream or 1)))
@@ -380,7 +383,8 @@ def run_c5(args, rank, world, local):
                 "value": flops * args.steps / (ms / 1e3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": ("f32 (3xTF32 tcgen05 coupled Newton-Schulz, L^-1/2)" if newton
+                "dtype": (f"f32 ({'3xFP16' if nprec == abi.PREC_3XF16 else '3xTF32'} tcgen05 coupled Newton-Schulz, L^-1/2)"
+                          if newton
                           else "f32 (3xTF32 tcgen05 block Jacobi, fp32 pair solves)"),
                 "data": "synthetic SPD factors X X^T/2n + 1e-3 I (cold solves)",
                 "config": {"workload": WORKLOADS["C5"]["name"], "n": n, "factors": total,

@@ -101,8 +101,8 @@ struct GemmParams {
     unsigned int* omax;   // optional: per-batch max |output| (float bits, atomicMax) of SPLIT / SPLIT2
     int sym_T;            // CTA-pair symmetric schedules: T x T tile grid, lower triangle decoded
                           // arithmetically (tile_list unused)
-    const float* oscale;  // SPLIT / SPLIT2 fp16-pair output: D (and D^T) are written as scaled fp16
-                          // (hi, lo) pairs, __half arrays at Dhi/Dlo (Thi/Tlo), value * oscale[b]
+    const float* oscale;  // SPLIT / SPLIT2 / SYM_SPLIT / NS fp16-pair output: D (and D^T, T) are written
+                          // as scaled fp16 (hi, lo) pairs, __half arrays at Dhi/Dlo (Thi/Tlo), value * oscale[b]
 };
 
 __device__ __forceinline__ bool batch_skipped(const GemmParams& p, int t) {
@@ -485,8 +485,27 @@ __device__ __forceinline__ void sym_split_chunk(const GemmParams& p, int b, int 
     float* ml = p.Dlo ? p.Dlo + base : nullptr;
     float* th = NS ? p.Thi + base : nullptr;
     float* tl = (NS && p.Tlo) ? p.Tlo + base : nullptr;
+    // fp16-pair outputs (oscale): M (and T) as scaled fp16 (hi, lo) __half arrays at the same offsets
+    const float os = p.oscale ? p.oscale[b] : 0.f;
+    __half* mh16 = reinterpret_cast<__half*>(p.Dhi) + base;
+    __half* ml16 = reinterpret_cast<__half*>(p.Dlo) + base;
+    __half* th16 = NS ? reinterpret_cast<__half*>(p.Thi) + base : nullptr;
+    __half* tl16 = NS ? reinterpret_cast<__half*>(p.Tlo) + base : nullptr;
     float res = 0.f;
     auto put = [&](int64_t off, float v, bool diag) {
+        if (p.oscale) {
+            const float y = v * os;
+            __half h = __float2half_rn(y);
+            mh16[off] = h;
+            ml16[off] = __float2half_rn(y - __half2float(h));
+            if constexpr (NS) {
+                const float t = ((diag ? p.ns_a : 0.f) - p.ns_b * v) * os;
+                h = __float2half_rn(t);
+                th16[off] = h;
+                tl16[off] = __float2half_rn(t - __half2float(h));
+            }
+            return;
+        }
         float h, l;
         out_split(p, v, h, l, ml != nullptr);
         mh[off] = h;

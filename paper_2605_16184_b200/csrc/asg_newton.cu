@@ -32,7 +32,21 @@
 // After the loop, one symmetric Newton refinement against A' itself,
 // X <- X + (X R + R X)/(2p), R = I - X^(p/2) A' X^(p/2), removes most of the
 // rounding the product chain X_k T_k accumulated.
+//
+// 3XF16 (precision ASG_PREC_3XF16): the iterates are scaled fp16 (hi, lo) pairs
+// and every product of the loop runs as 3xFP16 (kind::f16, twice the tf32
+// rate). Their scales are fixed before each product, from spectral bounds:
+// M, T, U, W have ||.||_2 <= (p+1)/p once M's eigenvalues lie in [0, p+1] (a
+// damped PSD factor; |entry| <= ||.||_2), so they share one scale (kNsF16Scale,
+// entries up to 16). The X chain runs normalised, X~_k = c^(1/p) X_k with
+// X~_0 = I, so ||X~_k||_2 <= ((p+1)/p)^k: iteration k's X product writes at
+// the scale of that bound (ns_x_scale), and ns_finish applies c^(-1/p). An
+// indefinite factor breaks the bounds, overflows to inf and is reported
+// exactly as the fp32 iteration reports divergence (NotPsd, then the pass-2
+// retry at the damping floor). The refinement keeps 3xTF32 products on plain
+// fp32 buffers (split in shared memory).
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -68,6 +82,19 @@ constexpr int kNsRefineFrom = 2;  // refine roots whose last X step came at iter
 // are unaffected.
 inline float ns_floor(int d) { return 1e-6f + 1.2e-8f * float(d); }
 constexpr int kPowRows = 32;  // rows of A' v per CTA
+constexpr float kNsF16Scale = 4096.f;  // M, T, U, W as fp16 pairs: entries up to 16
+
+// scale of the normalised iterate X~_k: 2^(14 - ceil(k log2(1.002 (p+1)/p))), so the bound
+// ||X~_k||_2 <= ((p+1)/p)^k maps to at most 2^14 (fp16 max 65504)
+__device__ __forceinline__ float ns_x_scale(int k, float p) {
+    const float lg = float(k) * log2f(1.002f * (p + 1.f) / p);
+    return exp2f(14.f - ceilf(lg));
+}
+__device__ __forceinline__ void put16(__half* h, __half* l, size_t off, float y) {
+    const __half a = __float2half_rn(y);
+    h[off] = a;
+    l[off] = __float2half_rn(y - __half2float(a));
+}
 
 // y = A' v on the leading d x d (A' = A + eps I); per-CTA partial sums of y^2
 // (and, on the first step, of A'^2 for ||A'||_F) in fixed order.
@@ -150,11 +177,14 @@ __global__ void ns_norm_kernel(const float* __restrict__ y, float* __restrict__ 
 
 // M_0 = A'/c, T_0 = ((p+1) I - M_0)/p and X_1 = X_0 T_0 with X_0 = c^(-1/p) I
 // (padding: identity, so it stays converged); iteration 0 skips its X product.
+// f16 (sx0 != nullptr): M_0, T_0 and X~_1 = T_0 as fp16 pairs (hi at *h, lo at *l of each
+// buffer), scales kNsF16Scale / ns_x_scale(1); sx0 = ns_x_scale(2) (iteration 1's X product)
 __global__ void ns_init_kernel(const float* __restrict__ A, int d, int D, const double* __restrict__ eps,
                                const float* __restrict__ est, const float* __restrict__ fro, float p, float floor_rel,
                                float* __restrict__ Mh, float* __restrict__ Ml, float* __restrict__ Th,
                                float* __restrict__ Tl, float* __restrict__ Xh, float* __restrict__ Xl,
-                               float* __restrict__ cval, float* __restrict__ eeff, const int* __restrict__ gate) {
+                               float* __restrict__ cval, float* __restrict__ eeff, const int* __restrict__ gate,
+                               float* __restrict__ sx0, float* __restrict__ sx1, float* __restrict__ sc) {
     const int b = blockIdx.y;
     if (!gate[b]) return;
     const float f = fro[b], es = est[b];
@@ -166,11 +196,32 @@ __global__ void ns_init_kernel(const float* __restrict__ A, int d, int D, const 
     const float e = fmaxf(e0, floor_rel * c);
     c += e - e0;
     const float inv_c = 1.f / c, x0 = powf(c, -1.f / p);
+    const bool f16 = sx0 != nullptr;
+    const float s1 = f16 ? ns_x_scale(1, p) : 0.f;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         cval[b] = c;
         eeff[b] = e;
+        if (f16) {
+            sx1[b] = s1;
+            sx0[b] = ns_x_scale(2, p);
+            sc[b] = kNsF16Scale;
+        }
     }
     const size_t DD = size_t(D) * D, base = size_t(b) * DD;
+    if (f16) {  // normalised X~_1 = T_0 (identity on the padding)
+        const size_t slab = size_t(gridDim.y) * DD;
+        __half *mh = reinterpret_cast<__half*>(Mh), *th = reinterpret_cast<__half*>(Th), *xh = reinterpret_cast<__half*>(Xh);
+        for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < DD; k += size_t(gridDim.x) * blockDim.x) {
+            const int i = int(k / D), j = int(k - size_t(i) * D);
+            const bool in = i < d && j < d;
+            const float m = in ? (A[base + k] + (i == j ? e : 0.f)) * inv_c : (i == j ? 1.f : 0.f);
+            const float t = (i == j ? (p + 1.f) / p : 0.f) - m / p;
+            put16(mh, mh + slab, base + k, m * kNsF16Scale);
+            put16(th, th + slab, base + k, t * kNsF16Scale);
+            put16(xh, xh + slab, base + k, (in ? t : (i == j ? 1.f : 0.f)) * s1);
+        }
+        return;
+    }
     for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < DD; k += size_t(gridDim.x) * blockDim.x) {
         const int i = int(k / D), j = int(k - size_t(i) * D);
         const bool in = i < d && j < d;
@@ -201,6 +252,9 @@ struct NsState {
     int* iter;   // iteration counter (one int)
     int* any;    // per matrix: still active after the decision
     int* kfin;   // per matrix: iteration of the last X step (large: refine)
+    float* sx0;  // 3XF16: per-matrix scales of the X~ iterates in buffers 0 / 1 (null otherwise)
+    float* sx1;
+    float p;
 };
 
 __global__ void ns_state_init_kernel(NsState st, const float* __restrict__ est, const float* __restrict__ fro,
@@ -241,7 +295,7 @@ __global__ void ns_state_init_kernel(NsState st, const float* __restrict__ est, 
 // every iteration: one power step per iteration tracks it.
 __global__ void ns_spec_kernel(const float* __restrict__ Mh, const float* __restrict__ Ml, int d, int D,
                                const int* __restrict__ actM, const float* __restrict__ v, float* __restrict__ y,
-                               float* __restrict__ part, int nblk) {
+                               float* __restrict__ part, int nblk, int f16) {
     const int b = blockIdx.y;
     if (!actM[b]) return;
     extern __shared__ float vs[];
@@ -254,12 +308,21 @@ __global__ void ns_spec_kernel(const float* __restrict__ Mh, const float* __rest
     for (int r = warp; r < kPowRows; r += nw) {
         const int i = blockIdx.x * kPowRows + r;
         if (i >= d) break;
-        const float* rh = Mh + base + size_t(i) * D;
-        const float* rl = Ml ? Ml + base + size_t(i) * D : nullptr;
         float acc = 0.f;
-        for (int j = lane; j < d; j += 32) {
-            const float m = rh[j] + (rl ? rl[j] : 0.f);
-            acc = fmaf((j == i ? 1.f : 0.f) - m, vs[j], acc);
+        if (f16) {  // fp16 pair at kNsF16Scale: hi at Mh, lo one slab (gridDim.y matrices) further
+            const __half* rh = reinterpret_cast<const __half*>(Mh) + base + size_t(i) * D;
+            const __half* rl = rh + size_t(gridDim.y) * D * D;
+            for (int j = lane; j < d; j += 32) {
+                const float m = (__half2float(rh[j]) + __half2float(rl[j])) * (1.f / kNsF16Scale);
+                acc = fmaf((j == i ? 1.f : 0.f) - m, vs[j], acc);
+            }
+        } else {
+            const float* rh = Mh + base + size_t(i) * D;
+            const float* rl = Ml ? Ml + base + size_t(i) * D : nullptr;
+            for (int j = lane; j < d; j += 32) {
+                const float m = rh[j] + (rl ? rl[j] : 0.f);
+                acc = fmaf((j == i ? 1.f : 0.f) - m, vs[j], acc);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -335,6 +398,8 @@ __global__ void ns_decide_kernel(NsState st, int nb, int d, int D, float* __rest
         act = 0;
     }
     if (act && st.state[b] == 0) st.actX[b] = 1;
+    // iteration k+1's X product writes X~_{k+2} into buffer k & 1 (X~_k there is dead)
+    if (act && st.sx0) (k & 1 ? st.sx1 : st.sx0)[b] = ns_x_scale(k + 2, st.p);
     st.any[b] = act;
 }
 
@@ -377,14 +442,30 @@ __global__ void ns_probe_init_kernel(float* __restrict__ v, int d, int D, const 
 
 // out = X[xbuf[b]] on the leading d x d, zero elsewhere (the padding of the
 // root slabs the update GEMMs read).
+// 3XF16 (sx0 != nullptr): X = c^(-1/p) X~ from the fp16 pair at its scale
 __global__ void ns_finish_kernel(const float* __restrict__ X0h, const float* __restrict__ X0l,
                                  const float* __restrict__ X1h, const float* __restrict__ X1l,
                                  const int* __restrict__ xbuf, int d, int D, float* __restrict__ outh,
-                                 float* __restrict__ outl, const int* __restrict__ gate) {
+                                 float* __restrict__ outl, const int* __restrict__ gate, const float* __restrict__ sx0,
+                                 const float* __restrict__ sx1, const float* __restrict__ cval, float p) {
     const int b = blockIdx.y;
     if (!gate[b]) return;
     const size_t DD = size_t(D) * D, base = size_t(b) * DD;
     const bool one = xbuf[b] != 0;
+    if (sx0) {
+        const float f = powf(cval[b], -1.f / p) / (one ? sx1[b] : sx0[b]);
+        const __half* sh = reinterpret_cast<const __half*>(one ? X1h : X0h);
+        const __half* sl = sh + size_t(gridDim.y) * DD;
+        for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < DD; k += size_t(gridDim.x) * blockDim.x) {
+            const int i = int(k / D), j = int(k - size_t(i) * D);
+            const float x = (i < d && j < d) ? (__half2float(sh[base + k]) + __half2float(sl[base + k])) * f : 0.f;
+            float h, l;
+            pair_or_raw(x, h, l, outl != nullptr);
+            outh[base + k] = h;
+            if (outl) outl[base + k] = l;
+        }
+        return;
+    }
     const float* sh = one ? X1h : X0h;
     const float* sl = one ? X1l : X0l;
     for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < DD; k += size_t(gridDim.x) * blockDim.x) {
@@ -492,6 +573,7 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
                         float* ws, int* caller_status, const int2* sym_tiles, int nsym, int precision, int num_sms,
                         cudaStream_t s) {
     const bool split = precision != ASG_PREC_TF32;  // internal iterates: (hi, lo) pairs
+    const bool f16 = precision == ASG_PREC_3XF16;    // ... as scaled fp16 pairs (one slab: hi | lo)
     const size_t DD = size_t(D) * D, slab = size_t(nb) * DD;
     float* w = ws;
     auto take = [&](size_t n) {
@@ -512,14 +594,22 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
     float* fro = take(size_t(nb));
     float* cval = take(size_t(nb));
     float* eeff = take(size_t(nb));
+    float* sx0 = take(size_t(nb));  // 3XF16 scales: X~ buffers 0 / 1, the shared M/T/U/W scale
+    float* sx1 = take(size_t(nb));
+    float* sc = take(size_t(nb));
     int* ints = reinterpret_cast<int*>(take(11 * size_t(nb) + 32));
     NsState st{ints, ints + nb, ints + 2 * nb, ints + 3 * nb, reinterpret_cast<unsigned int*>(ints + 4 * nb),
                ints + 9 * nb, ints + 5 * nb};
+    st.sx0 = f16 ? sx0 : nullptr;
+    st.sx1 = f16 ? sx1 : nullptr;
+    st.p = float(p);
     int* gate = ints + 6 * nb;
     st.kfin = ints + 8 * nb;
     int* rgate = ints + 10 * nb;  // matrices whose root gets the refinement (ns_refine_gate_kernel)
     int* status = ints + 7 * nb;  // this call's status (merged into caller_status at the end)
-    if (!split) X0l = X1l = M0l = M1l = T0l = T1l = Ul = Wl = nullptr;
+    // f16: each iterate's (hi, lo) fp16 pair fills its own fp32 slab; the refinement's
+    // buffers hold plain fp32 (its 3xTF32 products split them in shared memory)
+    if (!split || f16) X0l = X1l = M0l = M1l = T0l = T1l = Ul = Wl = nullptr;
     float* outl_ = split ? outl : nullptr;
     const int pth = 256;
     const size_t psm = size_t(d) * sizeof(float);
@@ -527,10 +617,12 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
     const float pf = float(p);
 
     auto gemm = [&](const float* ah, const float* al, const float* bh, const float* bl, int epi, float* dh, float* dl,
-                    const int* active, float* th, float* tl, bool sym, cudaStream_t st_) {
+                    const int* active, float* th, float* tl, bool sym, cudaStream_t st_, const float* as = nullptr,
+                    const float* bsc = nullptr, const float* os = nullptr) {
         GemmLaunch g{};
-        g.A = Operand{ah, al, D, D};
-        g.B = Operand{bh, bl, D, D};
+        g.A = Operand{ah, al, D, D, as};
+        g.B = Operand{bh, bl, D, D, bsc};
+        g.p.oscale = os;
         g.batch = nb;
         g.epi = epi;
         g.p.alpha = 1.f;
@@ -559,6 +651,27 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
         float *mnh = odd ? M0h : M1h, *mnl = odd ? M0l : M1l;
         const float *th = odd ? T1h : T0h, *tl = odd ? T1l : T0l;
         float *tnh = odd ? T0h : T1h, *tnl = odd ? T0l : T1l;
+        if (f16) {  // fp16 pairs: lo half a slab past hi; scales sx (X~ chain) and sc (the rest)
+            auto lo = [&](const float* h) { return h + slab / 2; };
+            auto lom = [&](float* h) { return h + slab / 2; };
+            const float *sxi = odd ? sx1 : sx0, *sxo = odd ? sx0 : sx1;
+            gemm(xh, lo(xh), th, lo(th), EPI_SYM_SPLIT, xnh, lom(xnh), st.actX, nullptr, nullptr, true, st_, sxi, sc,
+                 sxo);  // X~ T
+            if (p == 2) {
+                gemm(th, lo(th), mh, lo(mh), EPI_SYM_SPLIT, Wh, lom(Wh), st.actM, nullptr, nullptr, true, st_, sc, sc,
+                     sc);  // W = T M
+                gemm(th, lo(th), Wh, lo(Wh), EPI_NS, mnh, lom(mnh), st.actM, tnh, lom(tnh), true, st_, sc, sc,
+                     sc);  // M = T W
+            } else {
+                gemm(th, lo(th), th, lo(th), EPI_SYM_SPLIT, Uh, lom(Uh), st.actM, nullptr, nullptr, true, st_, sc, sc,
+                     sc);  // U = T T
+                gemm(Uh, lo(Uh), mh, lo(mh), EPI_SYM_SPLIT, Wh, lom(Wh), st.actM, nullptr, nullptr, true, st_, sc, sc,
+                     sc);  // W = U M
+                gemm(Uh, lo(Uh), Wh, lo(Wh), EPI_NS, mnh, lom(mnh), st.actM, tnh, lom(tnh), true, st_, sc, sc,
+                     sc);  // M = U W
+            }
+            return;
+        }
         gemm(xh, xl, th, tl, EPI_SYM_SPLIT, xnh, xnl, st.actX, nullptr, nullptr, true, st_);  // X T
         if (p == 2) {
             gemm(th, tl, mh, ml, EPI_SYM_SPLIT, Wh, Wl, st.actM, nullptr, nullptr, true, st_);  // W = T M
@@ -587,7 +700,7 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
             ns_norm_kernel<<<nb, 256, 0, q>>>(y, v, part, it == 0 ? partf : nullptr, nblk, d, D, est, fro, 0, gate);
         }
         ns_init_kernel<<<dim3(eblocks, nb), 256, 0, q>>>(A, d, D, eps, est, fro, pf, pass ? ns_floor(d) : 0.f, M0h, M0l,
-                                                         T0h, T0l, X1h, X1l, cval, eeff, gate);
+                                                         T0h, T0l, X1h, X1l, cval, eeff, gate, st.sx0, st.sx1, sc);
         ns_state_init_kernel<<<(nb + 255) / 256, 256, 0, q>>>(st, est, fro, nb, status, gate);
         ns_probe_init_kernel<<<nb, 256, 0, q>>>(v, d, D, gate);
     };
@@ -596,13 +709,14 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
             iteration(q, half == 1);
             // M_{k+1} sits in buffer (k+1) & 1: M1 after an even iteration, M0 after an odd one
             ns_spec_kernel<<<dim3(nblk, nb), pth, psm, q>>>(half ? M0h : M1h, half ? M0l : M1l, d, D, st.actM, v, y,
-                                                         part, nblk);
+                                                         part, nblk, f16 ? 1 : 0);
             ns_decide_kernel<<<nb, 256, 0, q>>>(st, nb, d, D, v, y, part, nblk, status, debug);
             ns_loop_kernel<<<1, 256, 0, q>>>(st, nb, handle);
         }
     };
     auto epilogue = [&](cudaStream_t q) {
-        ns_finish_kernel<<<dim3(eblocks, nb), 256, 0, q>>>(X0h, X0l, X1h, X1l, st.xbuf, d, D, outh, outl_, gate);
+        ns_finish_kernel<<<dim3(eblocks, nb), 256, 0, q>>>(X0h, X0l, X1h, X1l, st.xbuf, d, D, outh, outl_, gate, st.sx0,
+                                                           st.sx1, cval, pf);
         // ---- one symmetric Newton refinement against A' itself -------------
         // R = I - X^(p/2) A' X^(p/2), X <- X + (X R + R X) / (2p). The coupled
         // iteration never revisits A', so the rounding of the ~3 products per
@@ -731,7 +845,7 @@ void launch_ns_inv_root(const float* A, int nb, int d, int D, const double* eps,
             for (int k = 0; k < unroll; ++k) {
                 iteration(s, (k & 1) == 1);
                 ns_spec_kernel<<<dim3(nblk, nb), pth, psm, s>>>((k & 1) ? M0h : M1h, (k & 1) ? M0l : M1l, d, D, st.actM,
-                                                             v, y, part, nblk);
+                                                             v, y, part, nblk, f16 ? 1 : 0);
                 ns_decide_kernel<<<nb, 256, 0, s>>>(st, nb, d, D, v, y, part, nblk, status, debug);
                 ns_iter_kernel<<<1, 1, 0, s>>>(st.iter);
             }

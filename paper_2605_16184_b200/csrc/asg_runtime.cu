@@ -33,6 +33,7 @@
 #include <deque>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -3466,6 +3467,45 @@ __global__ void unpad_sum_kernel(const float* __restrict__ hi, const float* __re
         dst[b * nn + e] = hi[o] + lo[o];
     }
 }
+
+// Scratch of the batched C-ABI solvers (asg_sym_eig_batched_f32 / asg_inv_root_batched_f32):
+// one grow-only device buffer per device, held for the whole call (calls serialise on it), so
+// a call neither maps fresh memory (a 100+ GB cudaMallocAsync per call dominated C5) nor
+// re-captures the solvers' cached graphs (their keys hold the buffer pointers). Batches are
+// processed in chunks that fit batched_scratch_bytes() (24 GiB).
+size_t batched_scratch_bytes() {  // ASG_BATCHED_SCRATCH_BYTES: tests force small chunks
+    static const size_t b = getenv("ASG_BATCHED_SCRATCH_BYTES") ? size_t(atoll(getenv("ASG_BATCHED_SCRATCH_BYTES")))
+                                                               : (size_t(24) << 30);
+    return b;
+}
+struct Arena {
+    std::mutex mu;
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+Arena& batched_arena(int dev) {
+    static std::mutex m;
+    static std::map<int, std::unique_ptr<Arena>> arenas;
+    std::lock_guard<std::mutex> lk(m);
+    auto& a = arenas[dev];
+    if (!a) a = std::make_unique<Arena>();
+    return *a;
+}
+// caller holds a.mu
+char* arena_reserve(Arena& a, size_t bytes) {
+    if (a.bytes < bytes) {
+        if (a.p) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaFree(a.p));
+            a.p = nullptr;
+            a.bytes = 0;
+        }
+        CK(cudaMalloc(&a.p, bytes));
+        a.bytes = bytes;
+    }
+    return static_cast<char*>(a.p);
+}
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 }  // namespace
 }  // namespace asg
 
@@ -3478,26 +3518,36 @@ int asg_sym_eig_batched_f32(const float* A, double* values, float* vectors, int6
         int sms = 148;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         const int D = tc_eigh_dim(int(n));
-        const size_t DD = size_t(D) * D, nbDD = size_t(batch) * DD;
-        float *Bp = nullptr, *J = nullptr, *ws = nullptr;
-        int* status = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&Bp), nbDD * 4, s));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&J), 4 * nbDD * 4, s));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), tc_eigh_workspace_floats(int(batch), int(n)) * 4, s));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&status), size_t(batch) * sizeof(int), s));
-        CK(cudaMemsetAsync(status, 0, size_t(batch) * sizeof(int), s));
-        pad_f32_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(A, int(n), D, Bp);
-        launch_tc_eigh(Bp, D, values, J, J + nbDD, J + 2 * nbDD, J + 3 * nbDD, ws, int(batch), int(n), status, sms, s,
-                       f32_refresh_tol());
-        unpad_sum_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(J, J + nbDD, int(n), D, vectors);
-        count_launch(2);
+        const size_t DD = size_t(D) * D;
+        auto need = [&](int64_t c) {
+            return align256(size_t(c) * DD * 4) + align256(4 * size_t(c) * DD * 4) +
+                   align256(tc_eigh_workspace_floats(int(c), int(n)) * 4) + align256(size_t(c) * sizeof(int));
+        };
+        int64_t cb = batch;
+        while (cb > 1 && need(cb) > batched_scratch_bytes()) cb = (cb + 1) / 2;
+        Arena& ar = batched_arena(dev);
+        std::lock_guard<std::mutex> lk(ar.mu);
+        char* base = arena_reserve(ar, need(cb));
         std::vector<int> st(static_cast<size_t>(batch));
-        CK(cudaMemcpyAsync(st.data(), status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        CK(cudaFreeAsync(Bp, s));
-        CK(cudaFreeAsync(J, s));
-        CK(cudaFreeAsync(ws, s));
-        CK(cudaFreeAsync(status, s));
+        for (int64_t b0 = 0; b0 < batch; b0 += cb) {
+            const int64_t c = std::min(cb, batch - b0);
+            const size_t nbDD = size_t(c) * DD;
+            char* q = base;
+            float* Bp = reinterpret_cast<float*>(q);
+            q += align256(nbDD * 4);
+            float* J = reinterpret_cast<float*>(q);
+            q += align256(4 * nbDD * 4);
+            float* ws = reinterpret_cast<float*>(q);
+            q += align256(tc_eigh_workspace_floats(int(c), int(n)) * 4);
+            int* status = reinterpret_cast<int*>(q);
+            CK(cudaMemsetAsync(status, 0, size_t(c) * sizeof(int), s));
+            pad_f32_kernel<<<dim3(256, unsigned(c)), 256, 0, s>>>(A + b0 * n * n, int(n), D, Bp);
+            launch_tc_eigh(Bp, D, values + b0 * n, J, J + nbDD, J + 2 * nbDD, J + 3 * nbDD, ws, int(c), int(n), status,
+                           sms, s, f32_refresh_tol());
+            unpad_sum_kernel<<<dim3(256, unsigned(c)), 256, 0, s>>>(J, J + nbDD, int(n), D, vectors + b0 * n * n);
+            count_launch(2);
+            CK(cudaMemcpyAsync(st.data() + b0, status, size_t(c) * sizeof(int), cudaMemcpyDeviceToHost, s));
+        }
         CK(cudaStreamSynchronize(s));
         CK(cudaGetLastError());
         for (int v : st)
@@ -3517,36 +3567,49 @@ int asg_inv_root_batched_f32(const float* A, float* out, int64_t batch, int64_t 
         int sms = 148;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         const int D = int(round_up(n, 128));
-        const size_t DD = size_t(D) * D, nbDD = size_t(batch) * DD;
+        const size_t DD = size_t(D) * D;
         const int bn = gemm_bn_for(D);
         std::vector<int2> tl(size_t(gemm_sym_tile_list(D, bn, nullptr)));
         gemm_sym_tile_list(D, bn, tl.data());
-        float *Ap = nullptr, *R = nullptr, *ws = nullptr;
-        double* eps = nullptr;
-        int* status = nullptr;
-        int2* tiles = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&Ap), nbDD * 4, s));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&R), 2 * nbDD * 4, s));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), ns_workspace_floats(int(batch), D) * 4, s));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&eps), size_t(batch) * 8, s));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&status), size_t(batch) * sizeof(int), s));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&tiles), tl.size() * sizeof(int2), s));
-        CK(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
-        CK(cudaMemsetAsync(status, 0, size_t(batch) * sizeof(int), s));
-        pad_f32_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(A, int(n), D, Ap);
-        count_launch(1);
-        launch_relative_damping_f32(Ap, int(batch), D, int(n), damping, eps, s);
-        launch_ns_inv_root(Ap, int(batch), int(n), D, eps, p, R, precision == ASG_PREC_3XTF32 ? R + nbDD : nullptr, ws,
-                           status, tiles, int(tl.size()), precision, sms, s);
-        if (precision != ASG_PREC_3XTF32) CK(cudaMemsetAsync(R + nbDD, 0, nbDD * 4, s));
-        unpad_sum_kernel<<<dim3(256, unsigned(batch)), 256, 0, s>>>(R, R + nbDD, int(n), D, out);
-        count_launch(1);
+        auto need = [&](int64_t c) {
+            return align256(size_t(c) * DD * 4) + align256(2 * size_t(c) * DD * 4) +
+                   align256(ns_workspace_floats(int(c), D) * 4) + align256(size_t(c) * 8) +
+                   align256(size_t(c) * sizeof(int)) + align256(tl.size() * sizeof(int2));
+        };
+        int64_t cb = batch;
+        while (cb > 1 && need(cb) > batched_scratch_bytes()) cb = (cb + 1) / 2;
+        Arena& ar = batched_arena(dev);
+        std::lock_guard<std::mutex> lk(ar.mu);
+        char* base = arena_reserve(ar, need(cb));
         std::vector<int> st(static_cast<size_t>(batch));
-        CK(cudaMemcpyAsync(st.data(), status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+        for (int64_t b0 = 0; b0 < batch; b0 += cb) {
+            const int64_t c = std::min(cb, batch - b0);
+            const size_t nbDD = size_t(c) * DD;
+            char* q = base;
+            auto take = [&](size_t b) {
+                char* r = q;
+                q += align256(b);
+                return r;
+            };
+            float* Ap = reinterpret_cast<float*>(take(nbDD * 4));
+            float* R = reinterpret_cast<float*>(take(2 * nbDD * 4));
+            float* ws = reinterpret_cast<float*>(take(ns_workspace_floats(int(c), D) * 4));
+            double* eps = reinterpret_cast<double*>(take(size_t(c) * 8));
+            int* status = reinterpret_cast<int*>(take(size_t(c) * sizeof(int)));
+            int2* tiles = reinterpret_cast<int2*>(take(tl.size() * sizeof(int2)));
+            CK(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+            CK(cudaMemsetAsync(status, 0, size_t(c) * sizeof(int), s));
+            pad_f32_kernel<<<dim3(256, unsigned(c)), 256, 0, s>>>(A + b0 * n * n, int(n), D, Ap);
+            count_launch(1);
+            launch_relative_damping_f32(Ap, int(c), D, int(n), damping, eps, s);
+            launch_ns_inv_root(Ap, int(c), int(n), D, eps, p, R, precision == ASG_PREC_3XTF32 ? R + nbDD : nullptr, ws,
+                               status, tiles, int(tl.size()), precision, sms, s);
+            if (precision != ASG_PREC_3XTF32) CK(cudaMemsetAsync(R + nbDD, 0, nbDD * 4, s));
+            unpad_sum_kernel<<<dim3(256, unsigned(c)), 256, 0, s>>>(R, R + nbDD, int(n), D, out + b0 * n * n);
+            count_launch(1);
+            CK(cudaMemcpyAsync(st.data() + b0, status, size_t(c) * sizeof(int), cudaMemcpyDeviceToHost, s));
+        }
         CK(cudaStreamSynchronize(s));
-        for (void* ptr : {static_cast<void*>(Ap), static_cast<void*>(R), static_cast<void*>(ws), static_cast<void*>(eps),
-                          static_cast<void*>(status), static_cast<void*>(tiles)})
-            CK(cudaFreeAsync(ptr, s));
         CK(cudaGetLastError());
         for (int v : st)
             if (v != ASG_OK) throw Fail{v, "inv_root_batched_f32: a matrix failed"};

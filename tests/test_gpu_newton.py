@@ -39,11 +39,16 @@ def newton_sched():
     return s
 
 
+PRECS = [pytest.param(abi.PREC_3XTF32, id="3xtf32"), pytest.param(abi.PREC_3XF16, id="3xf16")]
+
+
+@pytest.mark.parametrize("precision", PRECS)
 @pytest.mark.parametrize("method", [abi.SHAMPOO, abi.KL_SHAMPOO])
 @pytest.mark.parametrize("m,n", [(8, 8), (33, 64), (130, 96), (256, 200)])
-def test_newton_roots_match_oracle(P, method, m, n):
+def test_newton_roots_match_oracle(P, method, m, n, precision):
+    """3XF16: the iterates as scaled fp16 pairs (asg_newton.cu header); same bound."""
     cfg = P.defaults_for(method)
-    b = P.PrecondBlock(m, n, method, cfg, sched=newton_sched())
+    b = P.PrecondBlock(m, n, method, cfg, precision=precision, sched=newton_sched())
     for s in range(4):
         P.accumulate_factors(b, orc.random_matrix(m, n, 70 + s), cfg)
     for step, extra in ((3, 0), (6, 3)):
@@ -62,13 +67,14 @@ def test_newton_roots_match_oracle(P, method, m, n):
     assert b.version == 2
 
 
+@pytest.mark.parametrize("precision", PRECS)
 @pytest.mark.parametrize("method", [abi.SHAMPOO, abi.KL_SHAMPOO])
-def test_newton_refresh_kat(P, method):
+def test_newton_refresh_kat(P, method, precision):
     """precond_test.cpp:107-121: the refresh of I is I; of 16 I is 0.5 I for
     L^-1/4 (Shampoo) and 0.25 I for L^-1/2 (KL-Shampoo); damping 0."""
     cfg = P.defaults_for(method)
     cfg.damping = 0.0
-    b = P.PrecondBlock(4, 4, method, cfg, sched=newton_sched())
+    b = P.PrecondBlock(4, 4, method, cfg, precision=precision, sched=newton_sched())
     b.set(abi.FACTOR_L, np.eye(4))
     b.set(abi.FACTOR_R, 16.0 * np.eye(4))
     P.refresh_inverse(b, cfg, 0)
@@ -77,22 +83,25 @@ def test_newton_refresh_kat(P, method):
     assert np.abs(b.inv_r - want * np.eye(4)).max() < 1e-6
 
 
+@pytest.mark.parametrize("precision", PRECS)
 @pytest.mark.parametrize("method", [abi.SHAMPOO, abi.KL_SHAMPOO])
-def test_newton_rejects_indefinite(P, method):
+def test_newton_rejects_indefinite(P, method, precision):
     """densela_test.cpp:110-115 (inv_root of an indefinite matrix -> NotPsd):
     a negative damped eigenvalue makes the iteration diverge, reported as
-    NotPsdError at install."""
+    NotPsdError at install (3XF16: the broken bounds overflow to inf, reported
+    the same way)."""
     cfg = P.defaults_for(method)
     cfg.damping = 0.0
-    b = P.PrecondBlock(2, 2, method, cfg, sched=newton_sched())
+    b = P.PrecondBlock(2, 2, method, cfg, precision=precision, sched=newton_sched())
     b.set(abi.FACTOR_L, np.diag([1.0, -2.0]))
     b.set(abi.FACTOR_R, np.eye(2))
     with pytest.raises(abi.NotPsdError):
         P.refresh_inverse(b, cfg, 0)
 
 
+@pytest.mark.parametrize("precision", PRECS)
 @pytest.mark.parametrize("method", [abi.SHAMPOO, abi.KL_SHAMPOO])
-def test_newton_trajectory_matches_oracle_bounded_staleness(method):
+def test_newton_trajectory_matches_oracle_bounded_staleness(method, precision):
     """The trajectory case of test_gpu_step.py (three shape groups incl. a
     padded one, a 1-D AdamW parameter, pf=4, S=3, 2-step jobs) with the
     NEWTON refresh."""
@@ -100,6 +109,6 @@ def test_newton_trajectory_matches_oracle_bounded_staleness(method):
     from paper_2605_16184_b200 import optimizer
     shapes = [(256, 384), (300,), (96, 96), (72, 72)]
     errs, o = T.run_pair(optimizer, method, shapes, limit=128, pf=4, steps=10, S=3, delay=2.0,
-                         refresh_mode=abi.REFRESH_NEWTON, r_scale=2.5)
+                         refresh_mode=abi.REFRESH_NEWTON, r_scale=2.5, precision=precision)
     assert o.stats().installed >= 2 * 8
     assert max(errs) <= 1.0, errs

@@ -145,12 +145,12 @@ def f32_sched(mode=abi.REFRESH_F32):
     return s
 
 
-def big_block(P, method, m, n, steps, seed, mode=abi.REFRESH_F32):
+def big_block(P, method, m, n, steps, seed, mode=abi.REFRESH_F32, precision=abi.PREC_3XTF32):
     """A PrecondBlock after `steps` i.i.d. N(0, 1/n) gradients (the bench's
     distribution), and the orc_np block fed the identical fp32
     gradients."""
     cfg = P.defaults_for(method)
-    b = P.PrecondBlock(m, n, method, cfg, sched=f32_sched(mode))
+    b = P.PrecondBlock(m, n, method, cfg, precision=precision, sched=f32_sched(mode))
     nb = orc_np.Block(m, n, method)
     rng = np.random.default_rng(seed)
     for _ in range(steps):
@@ -166,16 +166,18 @@ def P(rt):
     return precond
 
 
-@pytest.mark.parametrize("mode", [abi.REFRESH_F32, abi.REFRESH_NEWTON])
+@pytest.mark.parametrize("mode,precision", [(abi.REFRESH_F32, abi.PREC_3XTF32), (abi.REFRESH_NEWTON, abi.PREC_3XTF32),
+                                            (abi.REFRESH_NEWTON, abi.PREC_3XF16)])
 @pytest.mark.parametrize("method", [abi.SHAMPOO, abi.KL_SHAMPOO])
 @pytest.mark.parametrize("n", [1024, 2048])
-def test_f32_refresh_roots_at_bench_sizes(P, method, n, mode):
+def test_f32_refresh_roots_at_bench_sizes(P, method, n, mode, precision):
     """compute_refresh (precond.cpp:129-142) at C1 / C3 block sizes: cold
     refresh, then a warm one after more statistics, each against the
     LAPACK-backed oracle on the GPU's own fp32 factor. Both fp32-level
     refreshes: the tensor-core Jacobi (F32) and the coupled Newton-Schulz
-    roots (NEWTON)."""
-    cfg, b, _ = big_block(P, method, n, n, 4, 11, mode)
+    roots (NEWTON; 3xTF32 iterates, or 3xFP16 iterates at bound-derived
+    scales)."""
+    cfg, b, _ = big_block(P, method, n, n, 4, 11, mode, precision)
     for step, extra in ((3, 0), (6, 3)):
         rng = np.random.default_rng(100 + step)
         for _ in range(extra):
@@ -188,7 +190,7 @@ def test_f32_refresh_roots_at_bench_sizes(P, method, n, mode):
             # F^-1 is derived as (F^-1/2)^2 (never stored): to first order its
             # relative error is twice the root's, hence the stated 2x bound
             kerrs = [rel(b.get(abi.KL_INV_L), r["kl_inv_l"]), rel(b.get(abi.KL_INV_R), r["kl_inv_r"])]
-        print(f"n={n} {abi.METHOD_NAMES[method]} mode {mode} step {step}: root errors "
+        print(f"n={n} {abi.METHOD_NAMES[method]} mode {mode} prec {precision} step {step}: root errors "
               f"{['%.2e' % e for e in errs + kerrs]}")
         assert max(errs) <= root_tol(n), errs
         assert not kerrs or max(kerrs) <= 2 * root_tol(n), kerrs
