@@ -155,10 +155,14 @@ cudaError_t dispatch_epi(int epi, const CUtensorMap& ah, const CUtensorMap& al, 
 
 }  // namespace
 
-int gemm_bn_for(int n) {
+int gemm_bn_for(int n, int batch) {
     static const int force = getenv("ASG_GEMM_BN") ? atoi(getenv("ASG_GEMM_BN")) : 0;  // tuning experiments
     if (force == 128) return 128;
-    return (n % 256 == 0) ? 256 : 128;
+    if (n % 256 != 0) return 128;
+    // symmetric outputs of a few matrices (C1: one 1024^2 block): the 256-wide CTA-pair
+    // triangle (10 tiles at 1024) would leave most SMs idle; 128-wide tiles give 36
+    const int t = n / 256;
+    return int64_t(batch) * t * (t + 1) / 2 < 74 ? 128 : 256;
 }
 
 int gemm_sym_tile_list(int n, int bn, int2* out) {
@@ -181,7 +185,10 @@ static bool pair_enabled() {
 cudaError_t gemm_launch(const GemmLaunch& g, int precision, int num_sms, cudaStream_t stream) {
     const int M = g.A.rows, N = g.B.rows, K = g.A.K;
     if (M % 128 || N % 128 || K % 32 || g.B.K != K) return cudaErrorInvalidValue;
-    int bn = gemm_bn_for(N);
+    // symmetric schedules: the tile width their list was built for (gemm_bn_for(N, batch) of
+    // the owner; the 128-wide lower triangle has more tiles than the 256-wide one)
+    int bn = (N % 256 == 0) ? 256 : 128;
+    if (g.sym_tiles && bn == 256 && g.sym_tiles_count == gemm_sym_tile_list(N, 128, nullptr)) bn = 128;
     // Small rectangular problems: 128-wide tiles when 256-wide ones would not
     // fill two waves of the persistent grid (symmetric schedules keep the tile
     // width their tile lists were built for).

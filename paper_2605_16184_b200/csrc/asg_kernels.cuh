@@ -48,7 +48,8 @@ struct GemmLaunch {
 };
 
 // Picks the output tile width for an output with `n` columns (multiple of 128).
-int gemm_bn_for(int n);
+// tile width of an n x n symmetric output over `batch` matrices (its lower-triangle tile list)
+int gemm_bn_for(int n, int batch);
 // Builds the lower-triangle tile list for an n x n symmetric output with
 // 128 x BN tiles. Returns the count; `out` may be null to query.
 int gemm_sym_tile_list(int n, int bn, int2* out);

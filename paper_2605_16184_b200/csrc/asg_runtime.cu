@@ -675,7 +675,7 @@ void alloc_group(asg_blockset* bs, Group& g) {
         CK(cudaMemsetAsync(g.d_identR, 0, nb * sizeof(int), s));
     }
     CK(cudaMemsetAsync(g.d_status, 0, nb * sizeof(int), s));
-    const int bnM = gemm_bn_for(g.M), bnN = gemm_bn_for(g.N);
+    const int bnM = gemm_bn_for(g.M, nb), bnN = gemm_bn_for(g.N, nb);
     g.ntM = gemm_sym_tile_list(g.M, bnM, nullptr);
     g.ntN = gemm_sym_tile_list(g.N, bnN, nullptr);
     std::vector<int2> tl(size_t(std::max(g.ntM, g.ntN)));
@@ -3568,7 +3568,7 @@ int asg_inv_root_batched_f32(const float* A, float* out, int64_t batch, int64_t 
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         const int D = int(round_up(n, 128));
         const size_t DD = size_t(D) * D;
-        const int bn = gemm_bn_for(D);
+        const int bn = gemm_bn_for(D, int(std::min<int64_t>(batch, 1 << 20)));
         std::vector<int2> tl(size_t(gemm_sym_tile_list(D, bn, nullptr)));
         gemm_sym_tile_list(D, bn, tl.data());
         auto need = [&](int64_t c) {
