@@ -1205,16 +1205,19 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 }
 __device__ __forceinline__ float u01(uint32_t x) { return (float(x >> 8) + 0.5f) * (1.0f / 16777216.0f); }  // (0, 1)
 
-// grid (column quads / 256, rows, blocks): thread = 4 consecutive columns of
-// one row, Philox counter (quad, row, block key); one 16-byte store when the
-// row segment is aligned (no per-element index division)
+// grid (column quads / 256, row groups of kSynthRows, blocks): thread = 4 consecutive
+// columns of kSynthRows rows, Philox counter (quad, row, block key) per 4 values; one
+// 16-byte store when the row segment is aligned (no per-element index division)
+constexpr int kSynthRows = 8;
 __global__ void synth_normal_kernel(const SynthBlock* __restrict__ blocks, uint64_t seed, uint64_t step) {
     const SynthBlock b = blocks[blockIdx.z];
-    const int row = blockIdx.y;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;  // column quad
-    if (row >= b.rows || 4 * q >= b.cols) return;
+    if (4 * q >= b.cols) return;
     const uint2 key = make_uint2(uint32_t(seed) ^ uint32_t(step * 0x9E3779B97F4A7C15ull),
                                  uint32_t(seed >> 32) ^ uint32_t((step * 0x9E3779B97F4A7C15ull) >> 32));
+    const int row1 = min(b.rows, int(blockIdx.y + 1) * kSynthRows);
+#pragma unroll 2
+    for (int row = blockIdx.y * kSynthRows; row < row1; ++row) {
     const uint4 r = philox4x32_10(make_uint4(uint32_t(q), uint32_t(row), b.key, 0u), key);
     const float r1 = sqrtf(-2.f * __logf(u01(r.x))), r2 = sqrtf(-2.f * __logf(u01(r.z)));
     float s1, c1, s2, c2;
@@ -1228,6 +1231,7 @@ __global__ void synth_normal_kernel(const SynthBlock* __restrict__ blocks, uint6
         const float zz[4] = {z.x, z.y, z.z, z.w};
         for (int j = 0; j < 4 && 4 * q + j < b.cols; ++j) d[j] = zz[j];
     }
+    }
 }
 }  // namespace
 
@@ -1235,7 +1239,8 @@ void launch_synth_normal(const SynthBlock* blocks_dev, int nb, int max_rows, int
                          uint64_t step, cudaStream_t s) {
     if (nb <= 0 || max_rows <= 0 || max_cols <= 0) return;
     const int quads = (max_cols + 3) / 4;
-    synth_normal_kernel<<<dim3((quads + 255) / 256, max_rows, nb), 256, 0, s>>>(blocks_dev, seed, step);
+    synth_normal_kernel<<<dim3((quads + 255) / 256, (max_rows + kSynthRows - 1) / kSynthRows, nb), 256, 0, s>>>(
+        blocks_dev, seed, step);
     count_launch();
 }
 
@@ -1458,7 +1463,115 @@ __global__ void __launch_bounds__(256) prep_grad_f16_vec_kernel(const BlockRef* 
         put4(GTh + o, GTl + o, t[rr][cc], t[rr + 1][cc], t[rr + 2][cc], t[rr + 3][cc]);
     }
 }
+
+// 3xFP16 gradient prep without a separate max pass: G and G^T are written at the scale
+// predicted from the previous step's max of the same block (pred, raw |G| bits; two binades
+// of headroom), while this step's max is accumulated into `now`. prep_f16_check_kernel then
+// flags the blocks whose prediction was unsafe (overflow risk) or too loose (< 2^2 of fp16's
+// top binade used) -- and every block on the first step (pred = 0) -- and the same kernel in
+// FIX mode (fix != nullptr) rewrites just those blocks at the exact scale of `now`. Grid-stride
+// over (block, 64 x 64 tile), so the FIX launch costs ~nothing when no block is flagged.
+__global__ void __launch_bounds__(256) prep_grad_f16_pred_kernel(const BlockRef* __restrict__ blocks, int nb, int M,
+                                                                 int N, float scale_val,
+                                                                 const unsigned int* __restrict__ pred,
+                                                                 unsigned int* __restrict__ now,
+                                                                 const int* __restrict__ fix, __half* __restrict__ Gh,
+                                                                 __half* __restrict__ Gl, __half* __restrict__ GTh,
+                                                                 __half* __restrict__ GTl, float* __restrict__ gscale) {
+    __shared__ float t[64][65];
+    __shared__ float red[8];
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 16 + tx;
+    const int tj = N / 64, ti = M / 64, per = ti * tj;
+    const int64_t slab = int64_t(M) * N;
+    auto put4 = [](__half* hp, __half* lp, float a, float bb, float c, float d) {
+        __half h[4], l[4];
+        f16_split(a, h[0], l[0]);
+        f16_split(bb, h[1], l[1]);
+        f16_split(c, h[2], l[2]);
+        f16_split(d, h[3], l[3]);
+        *reinterpret_cast<uint2*>(hp) = *reinterpret_cast<const uint2*>(h);
+        *reinterpret_cast<uint2*>(lp) = *reinterpret_cast<const uint2*>(l);
+    };
+    for (int64_t w = blockIdx.x; w < int64_t(nb) * per; w += gridDim.x) {
+        const int b = int(w / per), tile = int(w - int64_t(b) * per);
+        if (fix && !fix[b]) continue;  // block-uniform
+        const BlockRef blk = blocks[b];
+        const float s = fix ? f16_scale(__float_as_uint(__uint_as_float(now[b]) * scale_val))
+                            : (pred[b] ? f16_scale(__float_as_uint(__uint_as_float(pred[b]) * scale_val * 4.f)) : 1.f);
+        if (tile == 0 && tid == 0) gscale[b] = s;
+        const float f = scale_val * s;
+        const int j0 = (tile % tj) * 64, i0 = (tile / tj) * 64;
+        float mx = 0.f;
+        float4 xs[4];  // all four loads in flight before the first store
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = i0 + ty + 16 * r, j = j0 + tx * 4;
+            xs[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (i < blk.rows && j < blk.cols) xs[r] = __ldcs(reinterpret_cast<const float4*>(blk.src + int64_t(i) * blk.ld + j));
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = i0 + ty + 16 * r, j = j0 + tx * 4;
+            float4 x = xs[r];
+            mx = fmaxf(mx, absmax4(x));
+            x = make_float4(f * x.x, f * x.y, f * x.z, f * x.w);
+            const int64_t o = b * slab + int64_t(i) * N + j;
+            put4(Gh + o, Gl + o, x.x, x.y, x.z, x.w);
+            const int rr = ty + 16 * r, cc = tx * 4;
+            t[rr][cc] = x.x;
+            t[rr][cc + 1] = x.y;
+            t[rr][cc + 2] = x.z;
+            t[rr][cc + 3] = x.w;
+        }
+        if (!fix) {  // this step's max |G| of the block (raw)
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if ((tid & 31) == 0) red[tid >> 5] = mx;
+        }
+        __syncthreads();
+        if (!fix && tid == 0) {
+            for (int k = 1; k < 8; ++k) mx = fmaxf(mx, red[k]);
+            atomicMax(now + b, __float_as_uint(mx));
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int jj = j0 + ty + 16 * r, ii = i0 + tx * 4;  // GT[jj][ii..ii+3] = G[ii..ii+3][jj]
+            const int cc = ty + 16 * r, rr = tx * 4;
+            const int64_t o = b * slab + int64_t(jj) * M + ii;
+            put4(GTh + o, GTl + o, t[rr][cc], t[rr + 1][cc], t[rr + 2][cc], t[rr + 3][cc]);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void prep_f16_check_kernel(int nb, float scale_val, unsigned int* __restrict__ pred,
+                                      const unsigned int* __restrict__ now, const float* __restrict__ gscale,
+                                      int* __restrict__ fix) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const float m = __uint_as_float(now[b]) * scale_val, y = m * gscale[b];
+    fix[b] = (m == 0.f || (y >= 4.f && y < 32768.f)) ? 0 : 1;  // (non-finite: fixed, then reported downstream)
+    pred[b] = now[b];
+}
 }  // namespace
+
+void launch_prep_grad_f16_pred(const BlockRef* blocks_dev, int nb, int M, int N, float scale_val, unsigned int* pred,
+                               unsigned int* now, int* fix, void* Gh16, void* Gl16, void* GTh16, void* GTl16,
+                               float* gscale, cudaStream_t s) {
+    if (nb <= 0) return;
+    cudaMemsetAsync(now, 0, size_t(nb) * sizeof(unsigned int), s);
+    const int64_t work = int64_t(nb) * (M / 64) * (N / 64);
+    const int grid = int(std::min<int64_t>(work, 148 * 8));
+    auto* gh = static_cast<__half*>(Gh16);
+    auto* gl = static_cast<__half*>(Gl16);
+    auto* th = static_cast<__half*>(GTh16);
+    auto* tl = static_cast<__half*>(GTl16);
+    prep_grad_f16_pred_kernel<<<grid, dim3(16, 16), 0, s>>>(blocks_dev, nb, M, N, scale_val, pred, now, nullptr, gh, gl,
+                                                            th, tl, gscale);
+    prep_f16_check_kernel<<<(nb + 127) / 128, 128, 0, s>>>(nb, scale_val, pred, now, gscale, fix);
+    prep_grad_f16_pred_kernel<<<grid, dim3(16, 16), 0, s>>>(blocks_dev, nb, M, N, scale_val, pred, now, fix, gh, gl, th,
+                                                            tl, gscale);
+    count_launch(3);
+}
 
 void launch_colabs_max(const float* src, int nb, int n, int64_t per, unsigned int* out, cudaStream_t s) {
     if (nb <= 0) return;

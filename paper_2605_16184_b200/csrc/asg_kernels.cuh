@@ -172,6 +172,13 @@ void launch_to_f16pair(const float* src, const unsigned int* amax, int nb, int64
                        float* scale, cudaStream_t s);
 // Gradient blocks (caller layout, times scale_val) -> fp16 pairs of G [b][M][N] and
 // G^T [b][N][M] with per-block scales (a max pass over the blocks first).
+// the same with the scale predicted from the previous step's max (pred, persistent per block;
+// zero before the first step), this step's max fused into the pass (now), and the blocks whose
+// prediction failed rewritten at the exact scale (fix: per-block flags); needs M, N % 64 == 0
+// and 16-byte aligned gradient rows
+void launch_prep_grad_f16_pred(const BlockRef* blocks_dev, int nb, int M, int N, float scale_val, unsigned int* pred,
+                               unsigned int* now, int* fix, void* Gh16, void* Gl16, void* GTh16, void* GTl16,
+                               float* gscale, cudaStream_t s);
 void launch_prep_grad_f16(const BlockRef* blocks_dev, int nb, int M, int N, float scale_val, unsigned int* amax,
                           void* Gh16, void* Gl16, void* GTh16, void* GTl16, float* gscale, cudaStream_t s,
                           bool vec = false);

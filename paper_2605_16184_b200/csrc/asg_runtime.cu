@@ -198,6 +198,8 @@ struct Group {
     float *gscale = nullptr, *tscale = nullptr, *sscale = nullptr, *plscale = nullptr, *prscale = nullptr;
     unsigned int *amax = nullptr, *amax2 = nullptr;  // per-block max |x| scratch
     unsigned int *pln1 = nullptr, *prn1 = nullptr;   // per-block 1-norm of the fp16 roots (float bits)
+    unsigned int* amaxp = nullptr;  // previous step's max |G| per block (the predicted fp16 scale)
+    int* gfix = nullptr;            // blocks whose predicted scale failed this step
     // SOAP
     float *QLh = nullptr, *QLl = nullptr, *QLTh = nullptr, *QLTl = nullptr;
     float *QRh = nullptr, *QRl = nullptr, *QRTh = nullptr, *QRTl = nullptr;
@@ -567,6 +569,9 @@ void alloc_group(asg_blockset* bs, Group& g) {
         g.amax2 = dalloc<unsigned int>(bs, nb);
         g.pln1 = dalloc<unsigned int>(bs, nb);
         g.prn1 = dalloc<unsigned int>(bs, nb);
+        g.amaxp = dalloc<unsigned int>(bs, nb);
+        g.gfix = dalloc<int>(bs, nb);
+        CK(cudaMemsetAsync(g.amaxp, 0, nb * sizeof(unsigned int), bs->main));
     }
     auto pair_mm = [&](float*& h, float*& l) {
         h = dalloc<float>(bs, nb * slabMM(g));
@@ -1235,7 +1240,13 @@ void accumulate_impl(asg_blockset* bs, double clip_scale) {
         // 4 B read per element, hi/lo of G and G^T written (16 B; 8 B in TF32 mode) per padded element
         const double bytes = double(g.nb) * (4.0 * g.m * g.n + (g.Gl ? 16.0 : 8.0) * g.M * g.N);
         hbm_launch(bs, gs, ASG_HBM_PREP, bytes, [&] {
-            if (f16_mode(bs))  // (+ a 4 B/elt max pass; G, G^T as fp16 pairs: 8 B/elt written)
+            if (f16_mode(bs) && g.vec_grad && g.M % 64 == 0 && g.N % 64 == 0)
+                // G, G^T as fp16 pairs (8 B/elt written) at the scale predicted from the last
+                // step's max, the max fused in; mispredicted blocks rewritten
+                launch_prep_grad_f16_pred(g.d_refs, g.nb, g.M, g.N, float(clip_scale), g.amaxp, g.amax2, g.gfix, g.G16,
+                                          g.G16 + size_t(g.nb) * slabMN(g), g.GT16,
+                                          g.GT16 + size_t(g.nb) * slabMN(g), g.gscale, gs);
+            else if (f16_mode(bs))  // (+ a 4 B/elt max pass)
                 launch_prep_grad_f16(g.d_refs, g.nb, g.M, g.N, float(clip_scale), g.amax2, g.G16,
                                      g.G16 + size_t(g.nb) * slabMN(g), g.GT16, g.GT16 + size_t(g.nb) * slabMN(g),
                                      g.gscale, gs, g.vec_grad);

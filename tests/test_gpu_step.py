@@ -43,7 +43,7 @@ def O():
 
 
 def run_pair(O, method, shapes, limit, pf, steps, seed=0, S=0, lr=1e-2, wd=0.0, clip=1.0, well=True, delay=0.0,
-             refresh_mode=abi.REFRESH_F64, r_scale=1.0, precision=abi.PREC_3XTF32):
+             refresh_mode=abi.REFRESH_F64, r_scale=1.0, precision=abi.PREC_3XTF32, grad_scale=None):
     """GPU step vs the oracle's per-block harness loop (harness.cpp:439-475) with
     the oracle's ShadowScheduler on the same simulated clock."""
     from paper_2605_16184_b200 import runtime
@@ -88,6 +88,8 @@ def run_pair(O, method, shapes, limit, pf, steps, seed=0, S=0, lr=1e-2, wd=0.0, 
 
     for step in range(steps):
         gs = [grad_for(s) for s in shapes]
+        if grad_scale is not None:
+            gs = [g * grad_scale(step) for g in gs]
         for g, gt in zip(grads, gs):
             g.copy_(torch.tensor(gt, dtype=torch.float32))
         o.clock_advance(sched.step_compute_us)
@@ -140,6 +142,19 @@ def test_trajectory_operand_storage_modes(O, method, precision):
     (3XTF32_SMEM): the 3xTF32 tolerances hold unchanged."""
     shapes = [(256, 384), (300,), (96, 96), (72, 72)]
     errs, o = run_pair(O, method, shapes, limit=128, pf=4, steps=10, S=3, delay=2.0, precision=precision)
+    assert max(errs) <= 1.0, errs
+
+
+@pytest.mark.parametrize("method", [abi.SHAMPOO, abi.KL_SHAMPOO])
+def test_f16_gradient_scale_prediction_survives_magnitude_jumps(O, method):
+    """3XF16 writes each step's G at the scale predicted from the block's previous
+    max and rewrites the blocks whose prediction fails (launch_prep_grad_f16_pred):
+    gradients jumping 1e3x up (overflow side) and 1e-4x down (precision side)
+    between steps keep the 3xTF32 tolerances against the oracle."""
+    seq = [1.0, 1e3, 1e-1, 1e-4, 1.0, 30.0, 1e-2, 1.0]
+    shapes = [(256, 256), (96, 96)]
+    errs, _ = run_pair(O, method, shapes, limit=128, pf=2, steps=len(seq), S=1, delay=1.0,
+                       precision=abi.PREC_3XF16, grad_scale=lambda s: seq[s])
     assert max(errs) <= 1.0, errs
 
 
