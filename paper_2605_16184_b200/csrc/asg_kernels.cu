@@ -1469,8 +1469,9 @@ __global__ void __launch_bounds__(256) prep_grad_f16_vec_kernel(const BlockRef* 
 // of headroom), while this step's max is accumulated into `now`. prep_f16_check_kernel then
 // flags the blocks whose prediction was unsafe (overflow risk) or too loose (< 2^2 of fp16's
 // top binade used) -- and every block on the first step (pred = 0) -- and the same kernel in
-// FIX mode (fix != nullptr) rewrites just those blocks at the exact scale of `now`. Grid-stride
-// over (block, 64 x 64 tile), so the FIX launch costs ~nothing when no block is flagged.
+// FIX mode (fix != nullptr) rewrites just those blocks at the exact scale of `now`. The main
+// pass runs one 64 x 64 tile per CTA; the FIX pass is grid-stride over (block, tile) and
+// returns at once when no block is flagged (one load per thread).
 __global__ void __launch_bounds__(256) prep_grad_f16_pred_kernel(const BlockRef* __restrict__ blocks, int nb, int M,
                                                                  int N, float scale_val,
                                                                  const unsigned int* __restrict__ pred,
@@ -1492,7 +1493,14 @@ __global__ void __launch_bounds__(256) prep_grad_f16_pred_kernel(const BlockRef*
         *reinterpret_cast<uint2*>(hp) = *reinterpret_cast<const uint2*>(h);
         *reinterpret_cast<uint2*>(lp) = *reinterpret_cast<const uint2*>(l);
     };
-    for (int64_t w = blockIdx.x; w < int64_t(nb) * per; w += gridDim.x) {
+    if (fix) {
+        int any = 0;
+        for (int b = tid; b < nb; b += 256) any |= fix[b];
+        if (!__syncthreads_or(any)) return;
+    }
+    const int64_t w0 = fix ? blockIdx.x : (int64_t(blockIdx.z) * ti + blockIdx.y) * tj + blockIdx.x;
+    const int64_t wstep = fix ? gridDim.x : int64_t(nb) * per;
+    for (int64_t w = w0; w < int64_t(nb) * per; w += wstep) {
         const int b = int(w / per), tile = int(w - int64_t(b) * per);
         if (fix && !fix[b]) continue;  // block-uniform
         const BlockRef blk = blocks[b];
@@ -1565,8 +1573,8 @@ void launch_prep_grad_f16_pred(const BlockRef* blocks_dev, int nb, int M, int N,
     auto* gl = static_cast<__half*>(Gl16);
     auto* th = static_cast<__half*>(GTh16);
     auto* tl = static_cast<__half*>(GTl16);
-    prep_grad_f16_pred_kernel<<<grid, dim3(16, 16), 0, s>>>(blocks_dev, nb, M, N, scale_val, pred, now, nullptr, gh, gl,
-                                                            th, tl, gscale);
+    prep_grad_f16_pred_kernel<<<dim3(N / 64, M / 64, nb), dim3(16, 16), 0, s>>>(blocks_dev, nb, M, N, scale_val, pred,
+                                                                                now, nullptr, gh, gl, th, tl, gscale);
     prep_f16_check_kernel<<<(nb + 127) / 128, 128, 0, s>>>(nb, scale_val, pred, now, gscale, fix);
     prep_grad_f16_pred_kernel<<<grid, dim3(16, 16), 0, s>>>(blocks_dev, nb, M, N, scale_val, pred, now, fix, gh, gl, th,
                                                             tl, gscale);

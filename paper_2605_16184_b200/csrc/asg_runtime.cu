@@ -1240,7 +1240,8 @@ void accumulate_impl(asg_blockset* bs, double clip_scale) {
         // 4 B read per element, hi/lo of G and G^T written (16 B; 8 B in TF32 mode) per padded element
         const double bytes = double(g.nb) * (4.0 * g.m * g.n + (g.Gl ? 16.0 : 8.0) * g.M * g.N);
         hbm_launch(bs, gs, ASG_HBM_PREP, bytes, [&] {
-            if (f16_mode(bs) && g.vec_grad && g.M % 64 == 0 && g.N % 64 == 0)
+            static const bool pred_on = !(getenv("ASG_F16_PRED") && atoi(getenv("ASG_F16_PRED")) == 0);  // A/B knob
+            if (f16_mode(bs) && pred_on && g.vec_grad && g.M % 64 == 0 && g.N % 64 == 0)
                 // G, G^T as fp16 pairs (8 B/elt written) at the scale predicted from the last
                 // step's max, the max fused in; mispredicted blocks rewritten
                 launch_prep_grad_f16_pred(g.d_refs, g.nb, g.M, g.N, float(clip_scale), g.amaxp, g.amax2, g.gfix, g.G16,
