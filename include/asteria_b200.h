@@ -566,14 +566,19 @@ int asg_sym_eig_batched(const double* A, double* values, double* vectors, int64_
                         void* stream);
 /* The F32 refresh's tensor-core block Jacobi on its own: fp32 device buffers
  * A [batch][n][n] (symmetric), vectors [batch][n][n] (columns), fp64 values
- * [batch][n] ascending; n > 64. Same stopping rule as ASG_REFRESH_F32. */
+ * [batch][n] ascending; n > 64. Same stopping rule as ASG_REFRESH_F32.
+ * Works in chunks on a per-device scratch arena that persists between calls
+ * (calls on one device serialise on it); synchronizes the stream. */
 int asg_sym_eig_batched_f32(const float* A, double* values, float* vectors, int64_t batch, int64_t n,
                             void* stream);
 /* The NEWTON refresh's inverse root on its own (inv_root densela.hpp:267-282
  * with relative_damping precond.cpp:121-125): out[b] = (A[b] + eps_b I)^(-1/p),
  * eps_b = damping * tr(A[b]) / n, p in {2, 4}, by coupled Newton-Schulz
  * iterations on the tensor cores. fp32 device buffers [batch][n][n], n <= 4096;
- * precision: asg_precision of the products. Synchronizes the stream. */
+ * precision: asg_precision of the iterates and products (ASG_PREC_3XF16: scaled
+ * fp16 pairs at spectral-bound scales; 3XTF32 / 3XTF32_SMEM: tf32 pairs; TF32).
+ * Chunked on the same scratch arena as asg_sym_eig_batched_f32; synchronizes
+ * the stream. */
 int asg_inv_root_batched_f32(const float* A, float* out, int64_t batch, int64_t n, int32_t p, double damping,
                              int32_t precision, void* stream);
 
