@@ -38,14 +38,16 @@ def sched(mode):
 MODES = [abi.REFRESH_F64, abi.REFRESH_F32, abi.REFRESH_NEWTON]
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode,precision", [(m, abi.PREC_3XTF32) for m in MODES] +
+                         [(abi.REFRESH_NEWTON, abi.PREC_3XF16), (abi.REFRESH_F32, abi.PREC_3XF16)])
 @pytest.mark.parametrize("method", [abi.SHAMPOO, abi.SOAP, abi.KL_SHAMPOO])
-def test_split_refresh_equals_refresh_inverse(P, method, mode):
-    """install(compute(snapshot)) is refresh_inverse (precond.cpp:166-171)."""
+def test_split_refresh_equals_refresh_inverse(P, method, mode, precision):
+    """install(compute(snapshot)) is refresh_inverse (precond.cpp:166-171), also
+    with 3XF16 step arithmetic (the install converts the roots to fp16 pairs)."""
     m, n = 96, 80
     cfg = P.defaults_for(method)
-    a = P.PrecondBlock(m, n, method, cfg, sched=sched(mode))
-    b = P.PrecondBlock(m, n, method, cfg, sched=sched(mode))
+    a = P.PrecondBlock(m, n, method, cfg, precision=precision, sched=sched(mode))
+    b = P.PrecondBlock(m, n, method, cfg, precision=precision, sched=sched(mode))
     for s in range(3):
         g = orc.random_matrix(m, n, 10 + s)
         P.accumulate_factors(a, g, cfg)
