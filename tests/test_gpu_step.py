@@ -150,8 +150,9 @@ def test_f16_gradient_scale_prediction_survives_magnitude_jumps(O, method):
     """3XF16 writes each step's G at the scale predicted from the block's previous
     max and rewrites the blocks whose prediction fails (launch_prep_grad_f16_pred):
     gradients jumping 1e3x up (overflow side) and 1e-4x down (precision side)
-    between steps keep the 3xTF32 tolerances against the oracle."""
-    seq = [1.0, 1e3, 1e-1, 1e-4, 1.0, 30.0, 1e-2, 1.0]
+    between steps, and an all-zero gradient step, keep the 3xTF32 tolerances
+    against the oracle."""
+    seq = [1.0, 1e3, 1e-1, 0.0, 1e-4, 1.0, 30.0, 1e-2, 1.0]  # (0: an all-zero gradient step)
     shapes = [(256, 256), (96, 96)]
     errs, _ = run_pair(O, method, shapes, limit=128, pf=2, steps=len(seq), S=1, delay=1.0,
                        precision=abi.PREC_3XF16, grad_scale=lambda s: seq[s])
