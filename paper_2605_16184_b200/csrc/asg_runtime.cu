@@ -285,6 +285,18 @@ struct asg_blockset {
     float* ns_ws = nullptr;
     int* pair_status = nullptr;  // both-sides eigensolves: per-matrix status before the merge
     int* pair_ident = nullptr;   // both-sides eigensolves: per-matrix J = I flags
+    // Refresh chunks alternate between two side streams, each with its own copy of the
+    // side-stream workspace above (ws_* .. pair_ident): the active set is loaded into those
+    // fields while a chunk's work is launched (kernels capture the pointers), set 0 otherwise.
+    struct SideWs {
+        double *snap, *vecs, *work, *W, *out, *vals, *eps;
+        float* tw[8];
+        float *tc_ws, *ns_ws;
+        int *pair_status, *pair_ident;
+    };
+    SideWs side_ws[2] = {};
+    int nside = 1;
+    cudaStream_t side2 = nullptr;
     bool fp64_jacobi = false;  // ASG_F32_FP64_JACOBI=1: F32 refresh with the fp64 block Jacobi (diagnostics)
     // SOAP install workspace (one block)
     double *iw_rotL = nullptr, *iw_rotR = nullptr, *iw_sq = nullptr, *iw_a = nullptr, *iw_b = nullptr;
@@ -693,6 +705,41 @@ void alloc_group(asg_blockset* bs, Group& g) {
     bind_group_tables(bs, g);
 }
 
+asg_blockset::SideWs save_side_ws(const asg_blockset* bs) {
+    asg_blockset::SideWs w{};
+    w.snap = bs->ws_snap;
+    w.vecs = bs->ws_vecs;
+    w.work = bs->ws_work;
+    w.W = bs->ws_W;
+    w.out = bs->ws_out;
+    w.vals = bs->ws_vals;
+    w.eps = bs->ws_eps;
+    for (int k = 0; k < 8; ++k) w.tw[k] = bs->tw[k];
+    w.tc_ws = bs->tc_ws;
+    w.ns_ws = bs->ns_ws;
+    w.pair_status = bs->pair_status;
+    w.pair_ident = bs->pair_ident;
+    return w;
+}
+void load_side_ws(asg_blockset* bs, const asg_blockset::SideWs& w) {
+    bs->ws_snap = w.snap;
+    bs->ws_vecs = w.vecs;
+    bs->ws_work = w.work;
+    bs->ws_W = w.W;
+    bs->ws_out = w.out;
+    bs->ws_vals = w.vals;
+    bs->ws_eps = w.eps;
+    for (int k = 0; k < 8; ++k) bs->tw[k] = w.tw[k];
+    bs->tc_ws = w.tc_ws;
+    bs->ns_ws = w.ns_ws;
+    bs->pair_status = w.pair_status;
+    bs->pair_ident = w.pair_ident;
+}
+void sync_side(asg_blockset* bs) {
+    if (bs->side) CK(cudaStreamSynchronize(bs->side));
+    if (bs->side2) CK(cudaStreamSynchronize(bs->side2));
+}
+
 void alloc_workspace(asg_blockset* bs) {
     int nmax = 0;
     size_t state_per_block = 0;
@@ -710,45 +757,60 @@ void alloc_workspace(asg_blockset* bs) {
     bs->ws_n = nmax;
     // NEWTON refresh: the fp64 buffers only stage single-block parity I/O
     // (asg_block_read / asg_block_write), so they hold one block, not a chunk
-    const size_t nn = size_t(nmax) * nmax * size_t(newton_roots(bs) ? 1 : bs->ws_chunk);
-    bs->ws_snap = dalloc<double>(bs, nn);
-    bs->ws_vecs = dalloc<double>(bs, nn);
-    size_t ew = nn;
-    if (!newton_roots(bs)) {
-        for (const Group& g : bs->groups) {
-            ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.m));
-            ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.n));
+    auto alloc_side = [&]() {
+        const size_t nn = size_t(nmax) * nmax * size_t(newton_roots(bs) ? 1 : bs->ws_chunk);
+        bs->ws_snap = dalloc<double>(bs, nn);
+        bs->ws_vecs = dalloc<double>(bs, nn);
+        size_t ew = nn;
+        if (!newton_roots(bs)) {
+            for (const Group& g : bs->groups) {
+                ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.m));
+                ew = std::max(ew, eigh_workspace_doubles(bs->ws_chunk, g.n));
+            }
+            for (const Group& g : bs->groups) {
+                ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.m));
+                ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.n));
+            }
         }
-        for (const Group& g : bs->groups) {
-            ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.m));
-            ew = std::max(ew, eigh_workspace_doubles_warm(bs->ws_chunk, g.n));
+        bs->ws_work = dalloc<double>(bs, ew);
+        bs->ws_W = dalloc<double>(bs, nn);
+        bs->ws_out = dalloc<double>(bs, nn);
+        bs->ws_vals = dalloc<double>(bs, size_t(nmax) * bs->ws_chunk * 2);
+        bs->ws_eps = dalloc<double>(bs, size_t(bs->ws_chunk) * 2);
+        if (newton_roots(bs)) {
+            int Dmax = 0;
+            for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
+            // both sides of a small square group run as one batch (refresh_newton)
+            bool both = false;
+            for (const Group& g : bs->groups) both |= g.m == g.n && g.nb <= bs->ws_chunk;
+            bs->ns_ws = dalloc<float>(bs, ns_workspace_floats((both ? 2 : 1) * bs->ws_chunk, Dmax));
+            bs->pair_status = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
+        } else if (f32_refresh(bs)) {
+            int Dmax = 0;
+            for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
+            bs->tw_slab = size_t(Dmax) * Dmax;
+            // two factor sides per chunk (square blocks share one eigensolve)
+            for (float*& t : bs->tw) t = dalloc<float>(bs, bs->tw_slab * size_t(2 * bs->ws_chunk));
+            bs->tc_ws = dalloc<float>(bs, tc_eigh_workspace_floats(2 * bs->ws_chunk, Dmax));
+            bs->pair_status = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
+            bs->pair_ident = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
         }
+    };
+    alloc_side();
+    bs->side_ws[0] = save_side_ws(bs);
+    // a second set for the second refresh stream when a dispatch can launch more than one
+    // chunk (several shape groups, or a group larger than a chunk); ASG_REFRESH_STREAMS=1: one
+    int maxnb2 = 0;
+    for (const Group& g : bs->groups) maxnb2 = std::max(maxnb2, g.nb);
+    static const int want = getenv("ASG_REFRESH_STREAMS") ? atoi(getenv("ASG_REFRESH_STREAMS")) : 2;
+    if (want >= 2 && (bs->groups.size() > 1 || maxnb2 > bs->ws_chunk)) {
+        alloc_side();
+        bs->side_ws[1] = save_side_ws(bs);
+        bs->nside = 2;
+        load_side_ws(bs, bs->side_ws[0]);
     }
-    bs->ws_work = dalloc<double>(bs, ew);
-    bs->ws_W = dalloc<double>(bs, nn);
-    bs->ws_out = dalloc<double>(bs, nn);
-    bs->ws_vals = dalloc<double>(bs, size_t(nmax) * bs->ws_chunk * 2);
-    bs->ws_eps = dalloc<double>(bs, size_t(bs->ws_chunk) * 2);
-    if (newton_roots(bs)) {
-        int Dmax = 0;
-        for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
-        // both sides of a small square group run as one batch (refresh_newton)
-        bool both = false;
-        for (const Group& g : bs->groups) both |= g.m == g.n && g.nb <= bs->ws_chunk;
-        bs->ns_ws = dalloc<float>(bs, ns_workspace_floats((both ? 2 : 1) * bs->ws_chunk, Dmax));
-        bs->pair_status = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
-    } else if (f32_refresh(bs)) {
-        int Dmax = 0;
-        for (const Group& g : bs->groups) Dmax = std::max({Dmax, g.M, g.N});
-        bs->tw_slab = size_t(Dmax) * Dmax;
-        // two factor sides per chunk (square blocks share one eigensolve)
-        for (float*& t : bs->tw) t = dalloc<float>(bs, bs->tw_slab * size_t(2 * bs->ws_chunk));
-        bs->tc_ws = dalloc<float>(bs, tc_eigh_workspace_floats(2 * bs->ws_chunk, Dmax));
-        bs->pair_status = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
-        bs->pair_ident = dalloc<int>(bs, size_t(2 * bs->ws_chunk));
-        if (is_soap(bs))
-            for (float*& t : bs->iw32) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
-    }
+    if (f32_refresh(bs) && !newton_roots(bs) && is_soap(bs))
+        for (float*& t : bs->iw32) t = dalloc<float>(bs, bs->tw_slab * size_t(bs->ws_chunk));
     if (is_soap(bs)) {
         int maxmn = 0;
         for (const Group& g : bs->groups) maxmn = std::max(maxmn, g.m * g.n);
@@ -786,7 +848,7 @@ void run_gemm(asg_blockset* bs, Operand A, Operand B, int batch, int epi, const 
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     // profile the step's GEMMs (main and group streams); refresh GEMMs on the
     // side stream overlap them and are not part of the step's roofline
-    if (bs->profiling && s != bs->side) {
+    if (bs->profiling && s != bs->side && s != bs->side2) {
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, s));
@@ -1696,6 +1758,8 @@ void launch_refreshes(asg_blockset* bs) {
     }
     CK(cudaEventRecord(bs->ev_snap, bs->main));
     CK(cudaStreamWaitEvent(bs->side, bs->ev_snap, 0));
+    if (bs->nside == 2) CK(cudaStreamWaitEvent(bs->side2, bs->ev_snap, 0));
+    int chunk_no = 0;  // chunks alternate between the side streams (own workspace sets)
     for (size_t gi = 0; gi < bs->groups.size(); ++gi) {
         Group& g = bs->groups[gi];
         std::vector<int> slots;
@@ -1707,37 +1771,41 @@ void launch_refreshes(asg_blockset* bs) {
             size_t j = i + 1;
             while (j < slots.size() && slots[j] == slots[j - 1] + 1 && int(j - i) < bs->ws_chunk) ++j;
             const int s0 = slots[i], cnt = int(j - i);
-            CK(cudaMemsetAsync(g.d_status + s0, 0, size_t(cnt) * sizeof(int), bs->side));
+            const int lane = bs->nside == 2 ? (chunk_no++ & 1) : 0;
+            cudaStream_t sst = lane ? bs->side2 : bs->side;
+            load_side_ws(bs, bs->side_ws[lane]);
+            CK(cudaMemsetAsync(g.d_status + s0, 0, size_t(cnt) * sizeof(int), sst));
             if (newton_roots(bs)) {
-                refresh_newton(bs, g, s0, cnt, bs->side);
+                refresh_newton(bs, g, s0, cnt, sst);
             } else if (f32_refresh(bs)) {
                 if (g.m == g.n && g.m > kSmallEighN && !bs->fp64_jacobi) {
-                    refresh_sides_f32(bs, g, s0, cnt, 2, true, bs->side);
+                    refresh_sides_f32(bs, g, s0, cnt, 2, true, sst);
                 } else {
-                    refresh_sides_f32(bs, g, s0, cnt, 1, true, bs->side);
-                    refresh_sides_f32(bs, g, s0, cnt, 1, false, bs->side);
+                    refresh_sides_f32(bs, g, s0, cnt, 1, true, sst);
+                    refresh_sides_f32(bs, g, s0, cnt, 1, false, sst);
                 }
             } else {
-                refresh_side(bs, g, s0, cnt, true, bs->side);
-                refresh_side(bs, g, s0, cnt, false, bs->side);
+                refresh_side(bs, g, s0, cnt, true, sst);
+                refresh_side(bs, g, s0, cnt, false, sst);
             }
             CK(cudaMemcpyAsync(g.h_status + s0, g.d_status + s0, size_t(cnt) * sizeof(int), cudaMemcpyDeviceToHost,
-                               bs->side));
+                               sst));
             if (g.d_identL) {
                 CK(cudaMemcpyAsync(g.h_identL + s0, g.d_identL + s0, size_t(cnt) * sizeof(int), cudaMemcpyDeviceToHost,
-                                   bs->side));
+                                   sst));
                 CK(cudaMemcpyAsync(g.h_identR + s0, g.d_identR + s0, size_t(cnt) * sizeof(int), cudaMemcpyDeviceToHost,
-                                   bs->side));
+                                   sst));
             }
             for (int k = 0; k < cnt; ++k) {
                 Unit& u = bs->units[size_t(g.units[size_t(s0 + k)])];
-                CK(cudaEventRecord(u.done, bs->side));
+                CK(cudaEventRecord(u.done, sst));
                 u.launched = true;
                 u.needs_launch = false;
             }
             i = j;
         }
     }
+    load_side_ws(bs, bs->side_ws[0]);
     CK(cudaGetLastError());
 }
 
@@ -2409,6 +2477,7 @@ int asg_blockset_create(int device, const asg_optimizer_config* opt, const asg_s
         CK(cudaStreamCreateWithPriority(&bs->main, cudaStreamNonBlocking, hi));
         static const bool same_prio = getenv("ASG_SIDE_SAME_PRIORITY") != nullptr;  // diagnostics
         CK(cudaStreamCreateWithPriority(&bs->side, cudaStreamNonBlocking, same_prio ? hi : lo));
+        CK(cudaStreamCreateWithPriority(&bs->side2, cudaStreamNonBlocking, same_prio ? hi : lo));
         bs->own_main = true;
         for (int k = 0; k < asg_blockset::kGroupStreams; ++k) {
             CK(cudaStreamCreateWithPriority(&bs->gstream[k], cudaStreamNonBlocking, hi));
@@ -2467,6 +2536,7 @@ int asg_blockset_destroy(asg_blockset* bs) {
     cudaSetDevice(bs->device);
     if (bs->main) cudaStreamSynchronize(bs->main);
     if (bs->side) cudaStreamSynchronize(bs->side);
+    if (bs->side2) cudaStreamSynchronize(bs->side2);
     for (int k = 0; k < asg_blockset::kGroupStreams; ++k) {
         if (bs->gstream[k]) {
             cudaStreamSynchronize(bs->gstream[k]);
@@ -2493,6 +2563,7 @@ int asg_blockset_destroy(asg_blockset* bs) {
     if (bs->comm_stream) cudaStreamDestroy(bs->comm_stream);
     if (bs->own_main && bs->main) cudaStreamDestroy(bs->main);
     if (bs->side) cudaStreamDestroy(bs->side);
+    if (bs->side2) cudaStreamDestroy(bs->side2);
     delete bs;
     return ASG_OK;
 }
@@ -2911,7 +2982,7 @@ int asg_synchronize(asg_blockset* bs) {
     return guard([&] {
         CK(cudaSetDevice(bs->device));
         CK(cudaStreamSynchronize(bs->main));
-        CK(cudaStreamSynchronize(bs->side));
+        sync_side(bs);
         resolve_deferred(bs, true);
         check_flag(bs);
     });
@@ -2925,7 +2996,7 @@ int asg_block_read(asg_blockset* bs, int64_t idx, int32_t role, double* out, int
         const Unit& u = bs->units[size_t(idx)];
         Group& g = owned_group(bs, u);
         CK(cudaStreamSynchronize(bs->main));
-        CK(cudaStreamSynchronize(bs->side));
+        sync_side(bs);
         const int m = g.m, n = g.n;
         auto rd32 = [&](const float* base, size_t stride, int R, int Cc, int rows, int cols, const float* lo) {
             if (count < int64_t(rows) * cols) throw Fail{ASG_ERR_SHAPE_MISMATCH, "output too small"};
@@ -2994,7 +3065,7 @@ int asg_block_write(asg_blockset* bs, int64_t idx, int32_t role, const double* i
         Group& g = owned_group(bs, u);
         if (!g.v_ok.empty()) g.v_ok[size_t(u.slot)] = 0;  // roots may change: KL's cached V = P_L G is stale
         CK(cudaStreamSynchronize(bs->main));
-        CK(cudaStreamSynchronize(bs->side));
+        sync_side(bs);
         const int m = g.m, n = g.n;
         auto wr32 = [&](float* base, size_t stride, int R, int Cc, int rows, int cols, float* lo, float* hi_t, float* lo_t) {
             if (count < int64_t(rows) * cols) throw Fail{ASG_ERR_SHAPE_MISMATCH, "input too small"};
@@ -3296,7 +3367,7 @@ int asg_get_hbm_stats(asg_blockset* bs, asg_hbm_stats* out, int32_t reset) {
     return guard([&] {
         CK(cudaSetDevice(bs->device));
         CK(cudaStreamSynchronize(bs->main));
-        CK(cudaStreamSynchronize(bs->side));
+        sync_side(bs);
         CK(cudaDeviceSynchronize());  // the norm runs on the caller's stream
         *out = asg_hbm_stats{};
         for (auto& h : bs->prof_hbm) {
@@ -3321,7 +3392,7 @@ int asg_get_kernel_stats(asg_blockset* bs, asg_kernel_stats* out, int32_t reset)
     return guard([&] {
         CK(cudaSetDevice(bs->device));
         CK(cudaStreamSynchronize(bs->main));
-        CK(cudaStreamSynchronize(bs->side));
+        sync_side(bs);
         double ms = 0.0;
         for (auto& e : bs->prof_events) {
             float t = 0.f;
@@ -3856,7 +3927,7 @@ int asg_compute_refresh(asg_blockset* bs, const asg_snapshot* sn, asg_refresh_re
         if (u.pending || u.needs_launch || u.launched)
             throw Fail{ASG_ERR_INVALID_ARGUMENT, "compute_refresh: block has a scheduled refresh in flight"};
         CK(cudaStreamSynchronize(bs->main));
-        CK(cudaStreamSynchronize(bs->side));
+        sync_side(bs);
         const size_t mm = slabMM(g), nn = slabNN(g);
         d2d(at(g.snapL, mm, u.slot), sn->L, mm * 4, bs->main);
         d2d(at(g.snapR, nn, u.slot), sn->R, nn * 4, bs->main);
@@ -3938,7 +4009,7 @@ int asg_install_refresh(asg_blockset* bs, int64_t idx, asg_refresh_result* r, in
         if (r->idx != idx || r->method != bs->opt.method)
             throw Fail{ASG_ERR_SHAPE_MISMATCH, "install_refresh: result of another block or method"};
         if (u.pending || u.launched) throw Fail{ASG_ERR_INVALID_ARGUMENT, "install_refresh: a scheduled refresh is in flight"};
-        CK(cudaStreamSynchronize(bs->side));
+        sync_side(bs);
         cudaStream_t s = bs->main;
         const size_t mm = slabMM(g), nn = slabNN(g);
         u.version += 1;  // install_refresh precond.cpp:162-163 (SOAP installs read the bumped version)
