@@ -18,7 +18,9 @@
 //     |a_ij| > tol * max(sqrt(a_ii a_jj), noise floor). Pairs with at most
 //     kFewBig large elements rotate them one by one (classical Jacobi).
 //   * tj_apply_kernel (tcgen05): every 128x128 tile (pair k1 rows, pair k2
-//     columns) of A becomes J_k1^T (A_tile J_k2) -- two chained 3xTF32 MMAs
+//     columns, k1 <= k2: A stays exactly symmetric, so the epilogue writes the
+//     transpose of an off-diagonal result into tile (k2, k1)) of A becomes
+//     J_k1^T (A_tile J_k2) -- two chained 3xTF32 MMAs
 //     with the intermediate staged TMEM -> registers -> shared memory as the
 //     transposed K-major operand -- and every 128-row panel of V becomes
 //     V_tile J_k2. Tiles whose pairs are both converged are skipped (a CTA
@@ -670,7 +672,7 @@ struct TJApply {
     const int* pflag;           // [nb][m/2] per pair
     const int* active;          // [nb]
     int D, m, round, nb;
-    int tilesA, tilesV;         // per matrix: (m/4)^2 and (D/128)*(m/4)
+    int tilesA, tilesV;         // per matrix: T(T+1)/2 (upper triangle) and T^2, T = D/128
 };
 
 constexpr uint32_t kChunk = JP * 32 * 4;      // 128 rows x 32 fp32 = 16 KB
@@ -687,9 +689,15 @@ __device__ __forceinline__ void tj_decode(const TJApply& p, int t, int& b, bool&
     int l = t - b * per;
     const int np2 = p.D / JP;  // 128x128 tiles per matrix row
     if (l < p.tilesA) {
+        // A is symmetric: only tiles i1 <= i2 are computed (row-major upper
+        // triangle); the epilogue writes each off-diagonal result to both halves.
         isA = true;
-        i1 = l / np2;
-        i2 = l - i1 * np2;
+        i1 = 0;
+        while (l >= np2 - i1) {
+            l -= np2 - i1;
+            ++i1;
+        }
+        i2 = i1 + l;
     } else {
         isA = false;
         l -= p.tilesA;
@@ -971,6 +979,18 @@ __global__ void __launch_bounds__(192, 1)
                         split_tf32(__uint_as_float(r[j + 3]), h4.w, l4.w);
                         *reinterpret_cast<float4*>(dh + j) = h4;
                         *reinterpret_cast<float4*>(dl + j) = l4;
+                    }
+                    if (i1 != i2) {
+                        // mirror tile (i2, i1): column gc + j of these rows becomes row gc + j;
+                        // a warp's 32 rows are consecutive (one JW block), so each store is 128 B
+                        const int64_t tb = int64_t(b) * p.D * p.D + int64_t(gc) * p.D + gr;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            float h, l;
+                            split_tf32(__uint_as_float(r[j]), h, l);
+                            p.Ah[tb + int64_t(j) * p.D] = h;
+                            p.Al[tb + int64_t(j) * p.D] = l;
+                        }
                     }
                 }
                 tc_fence_before();
@@ -1293,7 +1313,7 @@ void tc_eigh_chunk(const float* B, int D_in, double* values, float* Jh, float* J
     ap.D = D;
     ap.m = m;
     ap.nb = nb;
-    ap.tilesA = ntiles * ntiles;
+    ap.tilesA = ntiles * (ntiles + 1) / 2;
     ap.tilesV = ntiles * ntiles;
     CUtensorMap mAh, mAl, mVh, mVl, mJh, mJl;
     bool ok = tj_map(&mAh, Ah, D, D, nb, JW) && tj_map(&mAl, Al, D, D, nb, JW) && tj_map(&mVh, Vh, D, D, nb, JW) &&
