@@ -335,7 +335,6 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
     // ranking below absorbs. Odd rounds leave positions PW-1 and 0 idle; they
     // form the wrap "pair" k = PW/2-1 with the identity and no swap.
     if (oe_order && inner_sweeps > 0) {  // (a classical-path pair has already set inner_sweeps = 0)
-        __shared__ unsigned char swp[PW / 2];
         const int lane = threadIdx.x & 31;
         const bool flip = lane & 16;  // half-warps take the two rows in opposite order (banks)
         // Z lives in registers for the sweep: warp w owns rows [RPW w, RPW w + RPW),
@@ -363,7 +362,10 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                     const int kk = threadIdx.x;
                     const bool wrap = odd && kk == PW / 2 - 1;
                     const int a = 2 * kk + odd, c = wrap ? 0 : a + 1;
-                    float cc = 1.f, ss = 0.f;
+                    // Every pair's two positions swap after its rotation, so the
+                    // idle wrap pair gets (c, s) = (0, 1): rotation + swap = diag(1, -1),
+                    // an exact sign flip of position 0 -- the swaps stay unconditional.
+                    float cc = wrap ? 0.f : 1.f, ss = wrap ? 1.f : 0.f;
                     if (!wrap && big(a, c, itol)) {
                         if (rot32) {  // fp32 rotation (the serial part of the round)
                             const float apq = S[a * (PW + 1) + c];
@@ -386,7 +388,6 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                     }
                     cs[kk] = cc;
                     sn[kk] = ss;
-                    swp[kk] = wrap ? 0 : 1;
                 }
                 __syncthreads();
                 // S: 2x2 blocks (ki, kj); a warp covers one ki and 32 consecutive kj.
@@ -421,37 +422,27 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                     for (int it = 0; it < SB; ++it) {
                         const int e = threadIdx.x + (h * SB + it) * NT;
                         const int ki = e / (PW / 2), kj = e % (PW / 2);
-                        float s00 = flip ? q[it][2] : q[it][0], s01 = flip ? q[it][3] : q[it][1];
-                        float s10 = flip ? q[it][0] : q[it][2], s11 = flip ? q[it][1] : q[it][3];
-                        const float ci = cs[ki], si = sn[ki], cj = cs[kj], sj = sn[kj];
-                        const float t00 = ci * s00 - si * s10, t01 = ci * s01 - si * s11;
-                        const float t10 = si * s00 + ci * s10, t11 = si * s01 + ci * s11;
-                        s00 = cj * t00 - sj * t01;
-                        s01 = sj * t00 + cj * t01;
-                        s10 = cj * t10 - sj * t11;
-                        s11 = sj * t10 + cj * t11;
-                        if (ki == kj && si != 0.f) s01 = s10 = 0.f;  // the annihilated element
-                        if (swp[ki]) {  // swap the two rows' positions
-                            float x = s00;
-                            s00 = s10;
-                            s10 = x;
-                            x = s01;
-                            s01 = s11;
-                            s11 = x;
-                        }
-                        if (swp[kj]) {  // and the two columns'
-                            float x = s00;
-                            s00 = s01;
-                            s01 = x;
-                            x = s10;
-                            s10 = s11;
-                            s11 = x;
+                        // slots: f = the row loaded first (ai, or bi on flip lanes), g = the
+                        // other; negating s on flip lanes makes the row rotation
+                        // order-agnostic: F = c f - s' g, G = s' f + c g. The
+                        // unconditional swaps are slot exchanges: the first row's
+                        // address takes G, columns aj <- X1 and bj <- X0.
+                        const float f0 = q[it][0], f1 = q[it][1], g0 = q[it][2], g1 = q[it][3];
+                        const float ci = cs[ki], cj = cs[kj], sj = sn[kj];
+                        const float si = flip ? -sn[ki] : sn[ki];
+                        const float F0 = ci * f0 - si * g0, F1 = ci * f1 - si * g1;
+                        const float G0 = si * f0 + ci * g0, G1 = si * f1 + ci * g1;
+                        float r00 = sj * G0 + cj * G1, r01 = cj * G0 - sj * G1;  // first row's address
+                        float r10 = sj * F0 + cj * F1, r11 = cj * F0 - sj * F1;  // second row's
+                        if (ki == kj && si != 0.f && ci != 0.f) {  // the annihilated element (not the wrap pair)
+                            if (flip) r00 = r11 = 0.f;
+                            else r01 = r10 = 0.f;
                         }
                         const int bo = bcol(e);
-                        S[o0[it]] = flip ? s10 : s00;
-                        S[o0[it] + bo] = flip ? s11 : s01;
-                        S[o1[it]] = flip ? s00 : s10;
-                        S[o1[it] + bo] = flip ? s01 : s11;
+                        S[o0[it]] = r00;
+                        S[o0[it] + bo] = r01;
+                        S[o1[it]] = r10;
+                        S[o1[it] + bo] = r11;
                     }
                 }
                 // Z (registers): rotate + swap column pairs of the lane's rows
@@ -482,10 +473,8 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                             const int zo = zoff(threadIdx.x + (h * ZH + it) * NT, kk, dc);
                             const float x = zq[it][0], y = zq[it][1];
                             const float cc = cs[kk], ss = sn[kk];
-                            const float na = cc * x - ss * y, nc = ss * x + cc * y;
-                            const bool s2 = swp[kk];
-                            Z[zo] = s2 ? nc : na;
-                            Z[zo + dc] = s2 ? na : nc;
+                            Z[zo] = ss * x + cc * y;  // rotate, then swap the two positions
+                            Z[zo + dc] = cc * x - ss * y;
                         }
                     }
                 } else if (!odd) {
@@ -493,13 +482,11 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                     for (int j = 0; j < CPL; j += 2) {
                         const int kk = (zcol0 + j) >> 1;
                         const float cc = cs[kk], ss = sn[kk];
-                        const bool s2 = swp[kk];
 #pragma unroll
                         for (int i = 0; i < RPW; ++i) {
                             const float x = zr[i][j], y = zr[i][j + 1];
-                            const float na = cc * x - ss * y, nc = ss * x + cc * y;
-                            zr[i][j] = s2 ? nc : na;
-                            zr[i][j + 1] = s2 ? na : nc;
+                            zr[i][j] = ss * x + cc * y;  // rotate, then swap the two positions
+                            zr[i][j + 1] = cc * x - ss * y;
                         }
                     }
                 } else {
@@ -507,35 +494,32 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                     for (int j = 1; j + 1 < CPL; j += 2) {  // pairs inside the lane
                         const int kk = (zcol0 + j - 1) >> 1;
                         const float cc = cs[kk], ss = sn[kk];
-                        const bool s2 = swp[kk];
 #pragma unroll
                         for (int i = 0; i < RPW; ++i) {
                             const float x = zr[i][j], y = zr[i][j + 1];
-                            const float na = cc * x - ss * y, nc = ss * x + cc * y;
-                            zr[i][j] = s2 ? nc : na;
-                            zr[i][j + 1] = s2 ? na : nc;
+                            zr[i][j] = ss * x + cc * y;  // rotate, then swap the two positions
+                            zr[i][j + 1] = cc * x - ss * y;
                         }
                     }
                     // pair (zcol0 + CPL - 1, zcol0 + CPL) spans lanes l, l+1; lane 31's is the
                     // identity wrap pair (PW-1, 0), as is lane 0's incoming one
                     const int kl = (zcol0 + CPL - 2) >> 1;        // pair whose first column is mine
                     const int kr = (zcol0 - 2) >> 1;              // pair whose second column is mine
+                    // (lane 0's incoming pair is the wrap pair: c = 0, s = 1 negates its column)
                     const float cl = cs[kl], sl = sn[kl];
-                    const bool wl = swp[kl];
-                    const float crr = lane > 0 ? cs[kr] : 1.f, srr = lane > 0 ? sn[kr] : 0.f;
-                    const bool wr = lane > 0 ? swp[kr] : false;
+                    const float crr = cs[lane > 0 ? kr : PW / 2 - 1], srr = sn[lane > 0 ? kr : PW / 2 - 1];
 #pragma unroll
                     for (int i = 0; i < RPW; ++i) {
                         const float mine_last = zr[i][CPL - 1], mine_first = zr[i][0];
                         const float from_right = __shfl_down_sync(0xffffffffu, mine_first, 1);
                         const float from_left = __shfl_up_sync(0xffffffffu, mine_last, 1);
-                        if (lane < 31) {  // I hold x (first column of pair kl)
+                        if (lane < 31) {  // I hold x (first column of pair kl); lane 31's is the wrap's x (kept)
                             const float x = mine_last, y = from_right;
-                            zr[i][CPL - 1] = wl ? (sl * x + cl * y) : (cl * x - sl * y);
+                            zr[i][CPL - 1] = sl * x + cl * y;
                         }
-                        if (lane > 0) {  // I hold y (second column of pair kr)
+                        {  // I hold y (second column of pair kr)
                             const float x = from_left, y = mine_first;
-                            zr[i][0] = wr ? (crr * x - srr * y) : (srr * x + crr * y);
+                            zr[i][0] = crr * x - srr * y;
                         }
                     }
                 }
