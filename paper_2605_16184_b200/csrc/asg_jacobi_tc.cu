@@ -396,23 +396,32 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                 // the round is one batch of independent loads, math, stores.
                 constexpr int SI = (PW / 2) * (PW / 2) / NT;
                 constexpr int SB = SI > 4 ? 4 : SI;  // S items per load batch
-                static_assert(SI * NT == (PW / 2) * (PW / 2) && SI % SB == 0, "thread count");
-                auto bcol = [&](int e) {  // offset of column bj relative to aj
-                    return (odd && e % (PW / 2) == PW / 2 - 1) ? -(PW - 1) : 1;
-                };
+                static_assert(SI * NT == (PW / 2) * (PW / 2) && SI % SB == 0 && NT % (PW / 2) == 0, "thread count");
+                // a thread's items share one column pair kj (item it: ki = ki0 + it NT/(PW/2)),
+                // so the column rotation and offsets are per round, not per item
+                const int ki0 = threadIdx.x / (PW / 2), kj = threadIdx.x % (PW / 2);
+                const int aj = 2 * kj + odd;
+                const int bo = (odd && kj == PW / 2 - 1) ? -(PW - 1) : 1;  // column bj relative to aj
+                const float cj = cs[kj], sj = sn[kj];
+                // item 0's row offsets (first = the row this lane loads first); item it
+                // adds it * ISTEP; only the last item of the last ki0 holds the odd
+                // rounds' wrap pair, whose second row is position 0, not PW
+                constexpr int ISTEP = 2 * (NT / (PW / 2)) * (PW + 1);
+                const int ra = 2 * ki0 + odd;
+                const int base0 = (flip ? ra + 1 : ra) * (PW + 1) + aj, base1 = (flip ? ra : ra + 1) * (PW + 1) + aj;
+                const bool wrap_item = odd && ki0 == NT / (PW / 2) - 1;  // (for it = SI - 1)
 #pragma unroll
                 for (int h = 0; h < SI / SB; ++h) {
                     float q[SB][4];
                     int o0[SB], o1[SB];  // offsets of (r0, aj) and (r1, aj)
 #pragma unroll
                     for (int it = 0; it < SB; ++it) {
-                        const int e = threadIdx.x + (h * SB + it) * NT;
-                        const int ki = e / (PW / 2), kj = e % (PW / 2);
-                        const int ai = 2 * ki + odd, bi = (odd && ki == PW / 2 - 1) ? 0 : ai + 1;
-                        const int aj = 2 * kj + odd;
-                        o0[it] = (flip ? bi : ai) * (PW + 1) + aj;
-                        o1[it] = (flip ? ai : bi) * (PW + 1) + aj;
-                        const int bo = bcol(e);
+                        o0[it] = base0 + (h * SB + it) * ISTEP;
+                        o1[it] = base1 + (h * SB + it) * ISTEP;
+                        if (h * SB + it == SI - 1 && wrap_item) {
+                            if (flip) o0[it] -= PW * (PW + 1);
+                            else o1[it] -= PW * (PW + 1);
+                        }
                         q[it][0] = S[o0[it]];
                         q[it][1] = S[o0[it] + bo];
                         q[it][2] = S[o1[it]];
@@ -420,29 +429,35 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                     }
 #pragma unroll
                     for (int it = 0; it < SB; ++it) {
-                        const int e = threadIdx.x + (h * SB + it) * NT;
-                        const int ki = e / (PW / 2), kj = e % (PW / 2);
+                        const int ki = ki0 + (h * SB + it) * (NT / (PW / 2));
                         // slots: f = the row loaded first (ai, or bi on flip lanes), g = the
                         // other; negating s on flip lanes makes the row rotation
                         // order-agnostic: F = c f - s' g, G = s' f + c g. The
                         // unconditional swaps are slot exchanges: the first row's
                         // address takes G, columns aj <- X1 and bj <- X0.
                         const float f0 = q[it][0], f1 = q[it][1], g0 = q[it][2], g1 = q[it][3];
-                        const float ci = cs[ki], cj = cs[kj], sj = sn[kj];
+                        const float ci = cs[ki];
                         const float si = flip ? -sn[ki] : sn[ki];
                         const float F0 = ci * f0 - si * g0, F1 = ci * f1 - si * g1;
                         const float G0 = si * f0 + ci * g0, G1 = si * f1 + ci * g1;
-                        float r00 = sj * G0 + cj * G1, r01 = cj * G0 - sj * G1;  // first row's address
-                        float r10 = sj * F0 + cj * F1, r11 = cj * F0 - sj * F1;  // second row's
-                        if (ki == kj && si != 0.f && ci != 0.f) {  // the annihilated element (not the wrap pair)
-                            if (flip) r00 = r11 = 0.f;
-                            else r01 = r10 = 0.f;
-                        }
-                        const int bo = bcol(e);
+                        const float r00 = sj * G0 + cj * G1, r01 = cj * G0 - sj * G1;  // first row's address
+                        const float r10 = sj * F0 + cj * F1, r11 = cj * F0 - sj * F1;  // second row's
                         S[o0[it]] = r00;
                         S[o0[it] + bo] = r01;
                         S[o1[it]] = r10;
                         S[o1[it] + bo] = r11;
+                    }
+                }
+                {
+                    // the annihilated element of a rotated pair (not the wrap pair): the
+                    // thread whose item is the diagonal block ki == kj zeroes its two
+                    // off-diagonal slots after the item's own stores
+                    constexpr int KS = NT / (PW / 2);
+                    const int d = kj - ki0;
+                    if (d >= 0 && d % KS == 0 && sn[kj] != 0.f && cs[kj] != 0.f) {
+                        const int a0 = base0 + (d / KS) * ISTEP, a1 = base1 + (d / KS) * ISTEP;
+                        S[flip ? a0 : a0 + 1] = 0.f;
+                        S[flip ? a1 + 1 : a1] = 0.f;
                     }
                 }
                 // Z (registers): rotate + swap column pairs of the lane's rows
