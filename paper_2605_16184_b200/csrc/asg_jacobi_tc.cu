@@ -375,12 +375,15 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                             cc = 1.f / sqrtf(fmaf(t, t, 1.f));
                             ss = t * cc;
                         } else {
-                            const double apq = S[a * (PW + 1) + c];
-                            const double app = S[a * (PW + 1) + a], aqq = S[c * (PW + 1) + c];
-                            const double tau = (aqq - app) / (2.0 * apq);
-                            const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau))
-                                                          : -1.0 / (-tau + sqrt(1.0 + tau * tau));
-                            const double c1 = 1.0 / sqrt(1.0 + t * t);
+                            // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = u / v, written as
+                            // sign(tau) |v| / (|u| + sqrt(u^2 + v^2)) so the round's serial chain
+                            // is one sqrt, one division and one rsqrt (was three divisions and
+                            // two square roots); sign(tau) >= 0 for u == 0 as before
+                            const double v = 2.0 * double(S[a * (PW + 1) + c]);
+                            const double u = double(S[c * (PW + 1) + c]) - double(S[a * (PW + 1) + a]);
+                            const double r = sqrt(fma(u, u, v * v));
+                            const double t = copysign(fabs(v) / (fabs(u) + r), (u == 0.0 || (u > 0.0) == (v > 0.0)) ? 1.0 : -1.0);
+                            const double c1 = rsqrt(fma(t, t, 1.0));
                             cc = float(c1);
                             ss = float(t * c1);
                         }
