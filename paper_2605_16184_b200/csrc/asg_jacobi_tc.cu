@@ -728,6 +728,9 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* empty1 = bars + 2;   // [2]
     uint64_t* full2 = bars + 4;    // [2]
     uint64_t* empty2 = bars + 6;   // [2]
+    // TMEM holds two tile buffers of 256 columns (X at +0, A' at +128), used by
+    // alternating tiles: MMA1 of tile u+1 runs while the epilogue drains tile u.
+    // xdone / xfree are per buffer (bars 8 / 14 and 11 / 15).
     uint64_t* xdone = bars + 8;    // MMA1 complete
     uint64_t* xready = bars + 9;   // X^T staged (4 epilogue warps)
     uint64_t* adone = bars + 10;   // MMA2 complete
@@ -778,6 +781,8 @@ __global__ void __launch_bounds__(192, 1)
                 mbar_init(&empty2[s], 1);
             }
             mbar_init(xdone, 1);
+            mbar_init(bars + 14, 1);
+            mbar_init(bars + 15, 4);
             mbar_init(xready, 4);
             mbar_init(adone, 1);
             mbar_init(xfree, 4);
@@ -785,7 +790,7 @@ __global__ void __launch_bounds__(192, 1)
             fence_mbar_init();
         }
         __syncwarp();
-        tmem_alloc<256>(tmem_slot);
+        tmem_alloc<512>(tmem_slot);
     }
     tc_fence_before();
     __syncthreads();
@@ -802,9 +807,10 @@ __global__ void __launch_bounds__(192, 1)
     // Every role walks the same tile sequence, so each tracks the phase of
     // every barrier it waits on by counting.
     uint32_t ph_full1[2] = {0, 0}, ph_empty1[2] = {0, 0}, ph_full2[2] = {0, 0}, ph_empty2[2] = {0, 0};
-    uint32_t ph_x = 0, ph_xr = 0, ph_a = 0, ph_xf = 0, ph_af = 0;
+    uint32_t ph_x = 0, ph_xr = 0, ph_a = 0, ph_xf = 0, ph_af = 0;  // ph_x / ph_xf: bit b = buffer b
+    int nt = 0;  // tiles processed so far (the TMEM buffer of this tile is nt & 1)
     int use1[2] = {0, 0}, use2[2] = {0, 0};  // producer: number of fills of each stage so far
-    bool prev_a = false, any_prev = false, a_seen = false;  // previous tile was A / exists; an A tile seen
+    bool prev_a = false, a_seen = false;  // previous tile was A; an A tile seen
 
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int b, i1, i2;
@@ -828,6 +834,10 @@ __global__ void __launch_bounds__(192, 1)
             else blk1[2 * t2] = blk1[2 * t2 + 1] = 0;
         }
         const int jb2 = b * ntiles + i2, jb1 = b * ntiles + i1;
+        const int tb = nt & 1;
+        const uint32_t tbuf = tmem + uint32_t(tb * 256);
+        uint64_t* xdone_b = tb ? bars + 14 : xdone;
+        uint64_t* xfree_b = tb ? bars + 15 : xfree;
 
         if (warp == 0) {
             if (lane == 0) {
@@ -872,12 +882,12 @@ __global__ void __launch_bounds__(192, 1)
             }
         } else if (warp == 1) {
             if (lane == 0) {
-                if (any_prev) {  // the epilogue has read X of the previous tile
-                    mbar_wait(xfree, ph_xf);
-                    ph_xf ^= 1;
+                if (nt >= 2) {  // the epilogue has read X of the tile that last used this buffer
+                    mbar_wait(xfree_b, (ph_xf >> tb) & 1u);
+                    ph_xf ^= 1u << tb;
                     tc_fence_after();
                 }
-                // MMA1: X = A_tile * J_k2 into TMEM cols [0, 128)
+                // MMA1: X = A_tile * J_k2 into the buffer's cols [0, 128)
                 for (int c = 0; c < 4; ++c) {
                     const int s = c & 1;
                     mbar_wait(&full1[s], ph_full1[s]);
@@ -889,13 +899,13 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t adv = uint64_t(kk * 32) >> 4;
-                        mma_tf32(tmem, ah + adv, bh + adv, idesc, (c | kk) != 0 ? 1u : 0u);
-                        mma_tf32(tmem, ah + adv, bl + adv, idesc, 1u);
-                        mma_tf32(tmem, al + adv, bh + adv, idesc, 1u);
+                        mma_tf32(tbuf, ah + adv, bh + adv, idesc, (c | kk) != 0 ? 1u : 0u);
+                        mma_tf32(tbuf, ah + adv, bl + adv, idesc, 1u);
+                        mma_tf32(tbuf, al + adv, bh + adv, idesc, 1u);
                     }
                     mma_commit(&empty1[s]);
                 }
-                mma_commit(xdone);
+                mma_commit(xdone_b);
                 if (isA) {
                     // MMA2: A' = J_k1^T X, B operand = X^T staged in region S
                     mbar_wait(xready, ph_xr);
@@ -918,9 +928,9 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint64_t adv = uint64_t(kk * 32) >> 4;
-                            mma_tf32(tmem + JP, ah + adv, bh + adv, idesc, (c | kk) != 0 ? 1u : 0u);
-                            mma_tf32(tmem + JP, ah + adv, bl + adv, idesc, 1u);
-                            mma_tf32(tmem + JP, al + adv, bh + adv, idesc, 1u);
+                            mma_tf32(tbuf + JP, ah + adv, bh + adv, idesc, (c | kk) != 0 ? 1u : 0u);
+                            mma_tf32(tbuf + JP, ah + adv, bl + adv, idesc, 1u);
+                            mma_tf32(tbuf + JP, al + adv, bh + adv, idesc, 1u);
                         }
                         mma_commit(&empty2[s]);
                     }
@@ -930,8 +940,8 @@ __global__ void __launch_bounds__(192, 1)
         } else {
             const int qd = warp & 3;  // TMEM lane quadrant: rows 32*qd .. 32*qd+31
             const int row = qd * 32 + int(lane);
-            mbar_wait(xdone, ph_x);
-            ph_x ^= 1;
+            mbar_wait(xdone_b, (ph_x >> tb) & 1u);
+            ph_x ^= 1u << tb;
             tc_fence_after();
             if (isA) {
                 // X rows [32 qd, 32 qd + 32) = K-chunk qd of MMA2's B operand (X^T)
@@ -940,7 +950,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t r[32];
-                    tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
+                    tmem_ld_32x32b_x32(tbuf + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
                     tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -956,7 +966,7 @@ __global__ void __launch_bounds__(192, 1)
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(xready);
-                    mbar_arrive(xfree);
+                    mbar_arrive(xfree_b);
                 }
                 mbar_wait(adone, ph_a);
                 ph_a ^= 1;
@@ -967,7 +977,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t r[32];
-                    tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(JP + cc * 32), r);
+                    tmem_ld_32x32b_x32(tbuf + (uint32_t(qd * 32) << 16) + uint32_t(JP + cc * 32), r);
                     tmem_ld_wait();
                     const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
                     float* dh = p.Ah + base + gc;
@@ -1004,7 +1014,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t r[32];
-                    tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
+                    tmem_ld_32x32b_x32(tbuf + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
                     tmem_ld_wait();
                     const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
                     float* dh = p.Vh + base + gc;
@@ -1022,17 +1032,17 @@ __global__ void __launch_bounds__(192, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(xfree);
+                if (lane == 0) mbar_arrive(xfree_b);
             }
         }
-        any_prev = true;
+        ++nt;
         prev_a = isA;
     }
     // the epilogue warps waited for every MMA of their last tile: TMEM is idle
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<256>(tmem);
+        tmem_dealloc<512>(tmem);
     }
 }
 
