@@ -376,13 +376,22 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                             ss = t * cc;
                         } else {
                             // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = u / v, written as
-                            // sign(tau) |v| / (|u| + sqrt(u^2 + v^2)) so the round's serial chain
-                            // is one sqrt, one division and one rsqrt (was three divisions and
-                            // two square roots); sign(tau) >= 0 for u == 0 as before
-                            const double v = 2.0 * double(S[a * (PW + 1) + c]);
-                            const double u = double(S[c * (PW + 1) + c]) - double(S[a * (PW + 1) + a]);
-                            const double r = sqrt(fma(u, u, v * v));
-                            const double t = copysign(fabs(v) / (fabs(u) + r), (u == 0.0 || (u > 0.0) == (v > 0.0)) ? 1.0 : -1.0);
+                            // sign(tau) |v| / (|u| + sqrt(u^2 + v^2)) (sign(tau) >= 0 for u == 0
+                            // as before) in fp32: t only sets how well a_pq is annihilated (the
+                            // pass zeroes it exactly); c = rsqrt(1 + t^2), s = t c in fp64 keep
+                            // c^2 + s^2 = 1 to fp64 before the fp32 rounding. The round's
+                            // serial chain: fp32 sqrt and division, one fp64 rsqrt (was three
+                            // fp64 divisions and two fp64 square roots).
+                            float v = 2.f * S[a * (PW + 1) + c];
+                            float u = S[c * (PW + 1) + c] - S[a * (PW + 1) + a];
+                            const float m = fmaxf(fabsf(u), fabsf(v));
+                            if (m > 1e18f || m < 1e-18f) {  // t is scale-free: keep u^2 + v^2 finite
+                                const int e = ilogbf(m);
+                                u = ldexpf(u, -e);
+                                v = ldexpf(v, -e);
+                            }
+                            const float r = sqrtf(fmaf(u, u, v * v));
+                            const double t = double(copysignf(fabsf(v) / (fabsf(u) + r), (u == 0.f || (u > 0.f) == (v > 0.f)) ? 1.f : -1.f));
                             const double c1 = rsqrt(fma(t, t, 1.0));
                             cc = float(c1);
                             ss = float(t * c1);
