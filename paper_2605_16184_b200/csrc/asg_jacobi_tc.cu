@@ -70,6 +70,9 @@ constexpr int kOddEvenWide = 1, kOddEvenNarrow = 1;
 // equal eigen-residuals, but the non-unit c^2+s^2 it leaves in the accumulated
 // rotations moved the KL-Shampoo F32 trajectory test 1.7x past its tolerance).
 constexpr int kRot32 = 0;
+#ifndef ASG_TJ_SB
+#define ASG_TJ_SB 4  // S items per load batch of the odd-even pass (2: same time, 8: 3-5% slower)
+#endif
 #ifndef ASG_TJ_NARROW_CTAS
 #define ASG_TJ_NARROW_CTAS 4
 #endif
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
                 // compiler cannot reorder shared loads past shared stores), so
                 // the round is one batch of independent loads, math, stores.
                 constexpr int SI = (PW / 2) * (PW / 2) / NT;
-                constexpr int SB = SI > 4 ? 4 : SI;  // S items per load batch
+                constexpr int SB = SI > ASG_TJ_SB ? ASG_TJ_SB : SI;  // S items per load batch
                 static_assert(SI * NT == (PW / 2) * (PW / 2) && SI % SB == 0 && NT % (PW / 2) == 0, "thread count");
                 // a thread's items share one column pair kj (item it: ki = ki0 + it NT/(PW/2)),
                 // so the column rotation and offsets are per round, not per item
