@@ -161,11 +161,11 @@ __global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const 
         float x;
         if (i < n && j < n) x = 0.5f * (t1[dy][threadIdx.x] + t2[threadIdx.x][dy]);
         else x = (i == j) ? float(pad[b] * (1.0 + double(i - n + 1) * 1e-3)) : 0.f;
-        float h, l;
-        split_tf32(x, h, l);
+        // A and V are stored as plain fp32 (the apply splits them in shared
+        // memory); the lo slabs stay zero, so readers of Ah + Al see A
         const int64_t o = b * DD + int64_t(i) * D + j;
-        Ah[o] = h;
-        Al[o] = l;
+        Ah[o] = x;
+        Al[o] = 0.f;
         Vh[o] = (i == j) ? 1.f : 0.f;
         Vl[o] = 0.f;
     }
@@ -720,6 +720,30 @@ __device__ __forceinline__ void tj_decode(const TJApply& p, int t, int& b, bool&
     }
 }
 
+// lo = rn_tf32(x - trunc_tf32(x)) of a 16 KB operand chunk (elementwise, so the
+// swizzle does not matter), by one warp: kind::tf32 reads each raw fp32 word
+// as hi = trunc_tf32(x) (asg_gemm.cuh's in-smem split), so x = hi + lo to 2^-22.
+__device__ __forceinline__ void tj_split_lo(const uint8_t* hi, uint8_t* lo, uint32_t lane) {
+    const uint32_t h0 = smem_u32(hi), l0 = smem_u32(lo);
+    auto lo_of = [](uint32_t xb) {
+        const float r = __uint_as_float(xb) - __uint_as_float(xb & 0xffffe000u);
+        return (__float_as_uint(r) + 0x1000u) & 0xffffe000u;
+    };
+    for (uint32_t i0 = lane; i0 < kChunk / 16; i0 += 128) {  // 4 16-byte loads in flight per lane
+        uint32_t x[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x[u][0]), "=r"(x[u][1]), "=r"(x[u][2]), "=r"(x[u][3])
+                         : "r"(h0 + (i0 + 32u * u) * 16u));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(l0 + (i0 + 32u * u) * 16u),
+                         "r"(lo_of(x[u][0])), "r"(lo_of(x[u][1])), "r"(lo_of(x[u][2])), "r"(lo_of(x[u][3]))
+                         : "memory");
+    }
+}
+
 // Swizzled (SWIZZLE_128B, K-major, 128 B rows) address of element (row, k) in a chunk buffer.
 __device__ __forceinline__ uint32_t sw128(int row, int k) {
     return uint32_t(row) * 128u + ((uint32_t(k >> 2) ^ uint32_t(row & 7)) << 4) + uint32_t(k & 3) * 4u;
@@ -866,13 +890,12 @@ __global__ void __launch_bounds__(192, 1)
                     }
                     ++use1[s];
                     uint8_t* st = S + s * kStage1;
-                    mbar_arrive_expect_tx(&full1[s], kStage1);
+                    mbar_arrive_expect_tx(&full1[s], kStage1 - kChunk);  // A / V lo: split by the MMA warp
                     const int col = blk2[(c * 32) / JW] * JW + (c * 32) % JW;  // K-chunk c: 32 columns
 #pragma unroll
                     for (int rb = 0; rb < NB; ++rb) {  // JW-row boxes
                         const int row0 = isA ? blk1[rb] * JW : i1 * JP + rb * JW;
                         tma_load_3d(st + rb * (kChunk / NB), isA ? &tmAh : &tmVh, &full1[s], col, row0, b);
-                        tma_load_3d(st + kChunk + rb * (kChunk / NB), isA ? &tmAl : &tmVl, &full1[s], col, row0, b);
                     }
                     tma_load_3d(st + 2 * kChunk, &tmJh, &full1[s], c * 32, 0, jb2);
                     tma_load_3d(st + 3 * kChunk, &tmJl, &full1[s], c * 32, 0, jb2);
@@ -893,19 +916,23 @@ __global__ void __launch_bounds__(192, 1)
                 }
             }
         } else if (warp == 1) {
-            if (lane == 0) {
-                if (nt >= 2) {  // the epilogue has read X of the tile that last used this buffer
-                    mbar_wait(xfree_b, (ph_xf >> tb) & 1u);
-                    ph_xf ^= 1u << tb;
+            if (lane == 0 && nt >= 2) {  // the epilogue has read X of the tile that last used this buffer
+                mbar_wait(xfree_b, (ph_xf >> tb) & 1u);
+                ph_xf ^= 1u << tb;
+            }
+            // MMA1: X = A_tile * J_k2 into the buffer's cols [0, 128). The A / V chunk
+            // arrives as plain fp32; the warp writes its lo part next to it while the
+            // previous chunk's MMAs run (kind::tf32 reads the raw word as trunc_tf32(x)).
+            for (int c = 0; c < 4; ++c) {
+                const int s = c & 1;
+                mbar_wait(&full1[s], ph_full1[s]);
+                ph_full1[s] ^= 1;
+                uint8_t* st = S + s * kStage1;
+                tj_split_lo(st, st + kChunk, lane);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
                     tc_fence_after();
-                }
-                // MMA1: X = A_tile * J_k2 into the buffer's cols [0, 128)
-                for (int c = 0; c < 4; ++c) {
-                    const int s = c & 1;
-                    mbar_wait(&full1[s], ph_full1[s]);
-                    ph_full1[s] ^= 1;
-                    tc_fence_after();
-                    uint8_t* st = S + s * kStage1;
                     const uint64_t ah = umma_desc_k_sw128(st), al = umma_desc_k_sw128(st + kChunk);
                     const uint64_t bh = umma_desc_k_sw128(st + 2 * kChunk), bl = umma_desc_k_sw128(st + 3 * kChunk);
 #pragma unroll
@@ -917,6 +944,9 @@ __global__ void __launch_bounds__(192, 1)
                     }
                     mma_commit(&empty1[s]);
                 }
+                __syncwarp();
+            }
+            if (lane == 0) {
                 mma_commit(xdone_b);
                 if (isA) {
                     // MMA2: A' = J_k1^T X, B operand = X^T staged in region S
@@ -992,29 +1022,17 @@ __global__ void __launch_bounds__(192, 1)
                     tmem_ld_32x32b_x32(tbuf + (uint32_t(qd * 32) << 16) + uint32_t(JP + cc * 32), r);
                     tmem_ld_wait();
                     const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
-                    float* dh = p.Ah + base + gc;
-                    float* dl = p.Al + base + gc;
+                    float* dh = p.Ah + base + gc;  // A is plain fp32 (Al stays zero)
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 h4, l4;
-                        split_tf32(__uint_as_float(r[j + 0]), h4.x, l4.x);
-                        split_tf32(__uint_as_float(r[j + 1]), h4.y, l4.y);
-                        split_tf32(__uint_as_float(r[j + 2]), h4.z, l4.z);
-                        split_tf32(__uint_as_float(r[j + 3]), h4.w, l4.w);
-                        *reinterpret_cast<float4*>(dh + j) = h4;
-                        *reinterpret_cast<float4*>(dl + j) = l4;
-                    }
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(dh + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                                         __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
                     if (i1 != i2) {
                         // mirror tile (i2, i1): column gc + j of these rows becomes row gc + j;
                         // a warp's 32 rows are consecutive (one JW block), so each store is 128 B
                         const int64_t tb = int64_t(b) * p.D * p.D + int64_t(gc) * p.D + gr;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            float h, l;
-                            split_tf32(__uint_as_float(r[j]), h, l);
-                            p.Ah[tb + int64_t(j) * p.D] = h;
-                            p.Al[tb + int64_t(j) * p.D] = l;
-                        }
+                        for (int j = 0; j < 32; ++j) p.Ah[tb + int64_t(j) * p.D] = __uint_as_float(r[j]);
                     }
                 }
                 tc_fence_before();
@@ -1029,18 +1047,11 @@ __global__ void __launch_bounds__(192, 1)
                     tmem_ld_32x32b_x32(tbuf + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
                     tmem_ld_wait();
                     const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
-                    float* dh = p.Vh + base + gc;
-                    float* dl = p.Vl + base + gc;
+                    float* dh = p.Vh + base + gc;  // V is plain fp32 (Vl stays zero)
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 h4, l4;
-                        split_tf32(__uint_as_float(r[j + 0]), h4.x, l4.x);
-                        split_tf32(__uint_as_float(r[j + 1]), h4.y, l4.y);
-                        split_tf32(__uint_as_float(r[j + 2]), h4.z, l4.z);
-                        split_tf32(__uint_as_float(r[j + 3]), h4.w, l4.w);
-                        *reinterpret_cast<float4*>(dh + j) = h4;
-                        *reinterpret_cast<float4*>(dl + j) = l4;
-                    }
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(dh + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                                         __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -1161,8 +1172,7 @@ __global__ void tj_gather_kernel(const float* __restrict__ Vh, const float* __re
         float h = 0.f, l = 0.f;
         if (i < n && r < n) {
             const int64_t o = b * DD + int64_t(i) * D + src[b * D + r];
-            h = Vh[o];
-            l = Vl[o];
+            split_tf32(Vh[o] + Vl[o], h, l);  // V is plain fp32 (Vl = 0)
         }
         Jh[b * DD + e] = h;
         if (Jl) Jl[b * DD + e] = l;
