@@ -5,7 +5,8 @@
 // factors above kSmallEighN. fp32-level arithmetic:
 //
 //   * A (the factor, rotated into the previous eigenbasis) and V (the
-//     accumulated rotation) live in HBM as (hi, lo) tf32 pairs, natural order.
+//     accumulated rotation) live in HBM as plain fp32, natural order; the
+//     apply splits each operand chunk into (hi, lo) in shared memory.
 //   * Columns are split into JW-wide blocks (32 below kWidePairN, 64 from
 //     there); a round pairs the blocks by a round-robin tournament (m/2
 //     disjoint pairs, m-1 rounds per sweep).
@@ -20,9 +21,10 @@
 //   * tj_apply_kernel (tcgen05): every 128x128 tile (pair k1 rows, pair k2
 //     columns, k1 <= k2: A stays exactly symmetric, so the epilogue writes the
 //     transpose of an off-diagonal result into tile (k2, k1)) of A becomes
-//     J_k1^T (A_tile J_k2) -- two chained 3xTF32 MMAs
-//     with the intermediate staged TMEM -> registers -> shared memory as the
-//     transposed K-major operand -- and every 128-row panel of V becomes
+//     (J_k1^T A_tile) J_k2 -- two chained 3xTF32 MMAs: the first takes the
+//     mirror tile A(k2, k1) as its K-major B operand, the intermediate Y stays
+//     in TMEM (split in place into (Y_hi, Y_lo)) as the A operand of the
+//     second -- and every 128-row panel of V becomes
 //     V_tile J_k2. Tiles whose pairs are both converged are skipped (a CTA
 //     with none left exits before allocating TMEM); tiles are pipelined
 //     across the warp roles. All operand tiles are gathered by TMA (JW-row /
@@ -744,11 +746,6 @@ __device__ __forceinline__ void tj_split_lo(const uint8_t* hi, uint8_t* lo, uint
     }
 }
 
-// Swizzled (SWIZZLE_128B, K-major, 128 B rows) address of element (row, k) in a chunk buffer.
-__device__ __forceinline__ uint32_t sw128(int row, int k) {
-    return uint32_t(row) * 128u + ((uint32_t(k >> 2) ^ uint32_t(row & 7)) << 4) + uint32_t(k & 3) * 4u;
-}
-
 template <int JW>
 __global__ void __launch_bounds__(192, 1)
     tj_apply_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
@@ -764,14 +761,15 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* empty1 = bars + 2;   // [2]
     uint64_t* full2 = bars + 4;    // [2]
     uint64_t* empty2 = bars + 6;   // [2]
-    // TMEM holds two tile buffers of 256 columns (X at +0, A' at +128), used by
-    // alternating tiles: MMA1 of tile u+1 runs while the epilogue drains tile u.
-    // xdone / xfree are per buffer (bars 8 / 14 and 11 / 15).
+    // TMEM (512 columns): MMA1 outputs in two 128-column buffers used by
+    // alternating tiles (MMA1 of tile u+1 runs while the epilogue drains tile u),
+    // Y_lo at 256 and A' at 384 for A tiles. xdone / xfree are per buffer
+    // (bars 8 / 14 and 11 / 15).
     uint64_t* xdone = bars + 8;    // MMA1 complete
-    uint64_t* xready = bars + 9;   // X^T staged (4 epilogue warps)
+    uint64_t* xready = bars + 9;   // Y split into (Y_hi, Y_lo) in TMEM (4 epilogue warps)
     uint64_t* adone = bars + 10;   // MMA2 complete
-    uint64_t* xfree = bars + 11;   // TMEM cols [0,128) read out (4 epilogue warps)
-    uint64_t* afree = bars + 13;   // TMEM cols [128,256) read out (4 epilogue warps)
+    uint64_t* xfree = bars + 11;   // buffer 0 done with (4 epilogue warps)
+    uint64_t* afree = bars + 13;   // A' read out (4 epilogue warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
     const int warp = threadIdx.x >> 5;
@@ -835,18 +833,18 @@ __global__ void __launch_bounds__(192, 1)
     constexpr uint32_t idesc = idesc_tf32(JP, JP);
 
     // Tiles are pipelined across the roles (no CTA-wide barrier per tile):
-    //   * the producer loads tile u+1's MMA1 operands while tile u's A' drains,
-    //     once region S no longer holds tile u's X^T (adone after an A tile);
-    //   * MMA1(u+1) writes TMEM cols [0,128) once the epilogue has read X(u)
-    //     (xfree); MMA2 writes cols [128,256) once A' of the previous A tile
-    //     has been read (afree).
+    //   * the producer runs ahead through the operand rings (shared memory only
+    //     holds operands: the A-tile intermediate stays in TMEM);
+    //   * MMA1(u+2) reuses tile u's buffer once the epilogue is done with it
+    //     (xfree: after X(u) is stored, or after MMA2(u) read Y(u)); MMA2 writes
+    //     A' once the previous A tile's A' has been read (afree).
     // Every role walks the same tile sequence, so each tracks the phase of
     // every barrier it waits on by counting.
     uint32_t ph_full1[2] = {0, 0}, ph_empty1[2] = {0, 0}, ph_full2[2] = {0, 0}, ph_empty2[2] = {0, 0};
     uint32_t ph_x = 0, ph_xr = 0, ph_a = 0, ph_xf = 0, ph_af = 0;  // ph_x / ph_xf: bit b = buffer b
     int nt = 0;  // tiles processed so far (the TMEM buffer of this tile is nt & 1)
     int use1[2] = {0, 0}, use2[2] = {0, 0};  // producer: number of fills of each stage so far
-    bool prev_a = false, a_seen = false;  // previous tile was A; an A tile seen
+    bool a_seen = false;  // an A tile seen
 
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int b, i1, i2;
@@ -871,17 +869,18 @@ __global__ void __launch_bounds__(192, 1)
         }
         const int jb2 = b * ntiles + i2, jb1 = b * ntiles + i1;
         const int tb = nt & 1;
-        const uint32_t tbuf = tmem + uint32_t(tb * 256);
+        const uint32_t tbuf = tmem + uint32_t(tb * 128);  // MMA1 output (X or Y), double-buffered
+        const uint32_t tylo = tmem + 256u, tap = tmem + 384u;  // Y_lo and A' (A tiles, single)
         uint64_t* xdone_b = tb ? bars + 14 : xdone;
         uint64_t* xfree_b = tb ? bars + 15 : xfree;
 
         if (warp == 0) {
             if (lane == 0) {
-                if (prev_a) {  // region S held the previous tile's X^T until its MMA2 completed
-                    mbar_wait(adone, ph_a);
-                    ph_a ^= 1;
-                }
-                // MMA1 operands: 4 K-chunks (pair-k2 columns), ring of 2 stages
+                // MMA1 operands, 4 K-chunks, ring of 2 stages. Slots: M-side hi, lo;
+                // B-side hi, lo. A plain-fp32 operand leaves its lo slot to the MMA warp.
+                //   V tile: V panel (M, fp32) x J_k2 (B, hi/lo)  -> X = V J_k2
+                //   A tile: J_k1^T (M, hi/lo) x mirror tile A(k2, k1) (B = A_tile in
+                //           K-major form, fp32)                   -> Y = J_k1^T A_tile
                 for (int c = 0; c < 4; ++c) {
                     const int s = c & 1;
                     if (use1[s] > 0) {
@@ -890,17 +889,24 @@ __global__ void __launch_bounds__(192, 1)
                     }
                     ++use1[s];
                     uint8_t* st = S + s * kStage1;
-                    mbar_arrive_expect_tx(&full1[s], kStage1 - kChunk);  // A / V lo: split by the MMA warp
-                    const int col = blk2[(c * 32) / JW] * JW + (c * 32) % JW;  // K-chunk c: 32 columns
+                    mbar_arrive_expect_tx(&full1[s], kStage1 - kChunk);
+                    if (isA) {
+                        tma_load_3d(st, &tmJh, &full1[s], c * 32, 0, jb1);
+                        tma_load_3d(st + kChunk, &tmJl, &full1[s], c * 32, 0, jb1);
+                        const int col = blk1[(c * 32) / JW] * JW + (c * 32) % JW;  // K-chunk c: 32 k1 columns
 #pragma unroll
-                    for (int rb = 0; rb < NB; ++rb) {  // JW-row boxes
-                        const int row0 = isA ? blk1[rb] * JW : i1 * JP + rb * JW;
-                        tma_load_3d(st + rb * (kChunk / NB), isA ? &tmAh : &tmVh, &full1[s], col, row0, b);
+                        for (int rb = 0; rb < NB; ++rb)  // JW-row boxes: the k2 rows
+                            tma_load_3d(st + 2 * kChunk + rb * (kChunk / NB), &tmAh, &full1[s], col, blk2[rb] * JW, b);
+                    } else {
+                        const int col = blk2[(c * 32) / JW] * JW + (c * 32) % JW;  // K-chunk c: 32 k2 columns
+#pragma unroll
+                        for (int rb = 0; rb < NB; ++rb)
+                            tma_load_3d(st + rb * (kChunk / NB), &tmVh, &full1[s], col, i1 * JP + rb * JW, b);
+                        tma_load_3d(st + 2 * kChunk, &tmJh, &full1[s], c * 32, 0, jb2);
+                        tma_load_3d(st + 3 * kChunk, &tmJl, &full1[s], c * 32, 0, jb2);
                     }
-                    tma_load_3d(st + 2 * kChunk, &tmJh, &full1[s], c * 32, 0, jb2);
-                    tma_load_3d(st + 3 * kChunk, &tmJl, &full1[s], c * 32, 0, jb2);
                 }
-                if (isA) {  // MMA2 A-operand: J_k1^T chunks
+                if (isA) {  // MMA2 B operand: J_k2 chunks (hi, lo)
                     for (int c = 0; c < 4; ++c) {
                         const int s = c & 1;
                         if (use2[s] > 0) {
@@ -910,25 +916,26 @@ __global__ void __launch_bounds__(192, 1)
                         ++use2[s];
                         uint8_t* st = T + s * kStage2;
                         mbar_arrive_expect_tx(&full2[s], kStage2);
-                        tma_load_3d(st, &tmJh, &full2[s], c * 32, 0, jb1);
-                        tma_load_3d(st + kChunk, &tmJl, &full2[s], c * 32, 0, jb1);
+                        tma_load_3d(st, &tmJh, &full2[s], c * 32, 0, jb2);
+                        tma_load_3d(st + kChunk, &tmJl, &full2[s], c * 32, 0, jb2);
                     }
                 }
             }
         } else if (warp == 1) {
-            if (lane == 0 && nt >= 2) {  // the epilogue has read X of the tile that last used this buffer
+            if (lane == 0 && nt >= 2) {  // the epilogue is done with the tile that last used this buffer
                 mbar_wait(xfree_b, (ph_xf >> tb) & 1u);
                 ph_xf ^= 1u << tb;
             }
-            // MMA1: X = A_tile * J_k2 into the buffer's cols [0, 128). The A / V chunk
-            // arrives as plain fp32; the warp writes its lo part next to it while the
-            // previous chunk's MMAs run (kind::tf32 reads the raw word as trunc_tf32(x)).
+            // MMA1 into the buffer (128 columns). The plain-fp32 operand's lo part is
+            // written next to it by the warp while the previous chunk's MMAs run
+            // (kind::tf32 reads the raw word as trunc_tf32(x)).
             for (int c = 0; c < 4; ++c) {
                 const int s = c & 1;
                 mbar_wait(&full1[s], ph_full1[s]);
                 ph_full1[s] ^= 1;
                 uint8_t* st = S + s * kStage1;
-                tj_split_lo(st, st + kChunk, lane);
+                if (isA) tj_split_lo(st + 2 * kChunk, st + 3 * kChunk, lane);
+                else tj_split_lo(st, st + kChunk, lane);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
@@ -949,10 +956,11 @@ __global__ void __launch_bounds__(192, 1)
             if (lane == 0) {
                 mma_commit(xdone_b);
                 if (isA) {
-                    // MMA2: A' = J_k1^T X, B operand = X^T staged in region S
+                    // MMA2: A' = Y J_k2 with A = (Y_hi, Y_lo) read from TMEM (the epilogue
+                    // split Y in place), B = J_k2 chunks from ring T
                     mbar_wait(xready, ph_xr);
                     ph_xr ^= 1;
-                    if (a_seen) {  // A' of the previous A tile has been read out of cols [128, 256)
+                    if (a_seen) {  // A' of the previous A tile has been read out
                         mbar_wait(afree, ph_af);
                         ph_af ^= 1;
                     }
@@ -964,15 +972,14 @@ __global__ void __launch_bounds__(192, 1)
                         ph_full2[s] ^= 1;
                         tc_fence_after();
                         uint8_t* st = T + s * kStage2;
-                        const uint64_t ah = umma_desc_k_sw128(st), al = umma_desc_k_sw128(st + kChunk);
-                        uint8_t* xb = S + c * 2 * kChunk;
-                        const uint64_t bh = umma_desc_k_sw128(xb), bl = umma_desc_k_sw128(xb + kChunk);
+                        const uint64_t bh = umma_desc_k_sw128(st), bl = umma_desc_k_sw128(st + kChunk);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint64_t adv = uint64_t(kk * 32) >> 4;
-                            mma_tf32(tbuf + JP, ah + adv, bh + adv, idesc, (c | kk) != 0 ? 1u : 0u);
-                            mma_tf32(tbuf + JP, ah + adv, bl + adv, idesc, 1u);
-                            mma_tf32(tbuf + JP, al + adv, bh + adv, idesc, 1u);
+                            const uint32_t k0 = uint32_t(c * 32 + kk * 8);
+                            mma_tf32_ts(tap, tbuf + k0, bh + adv, idesc, (c | kk) != 0 ? 1u : 0u);
+                            mma_tf32_ts(tap, tbuf + k0, bl + adv, idesc, 1u);
+                            mma_tf32_ts(tap, tylo + k0, bh + adv, idesc, 1u);
                         }
                         mma_commit(&empty2[s]);
                     }
@@ -982,34 +989,31 @@ __global__ void __launch_bounds__(192, 1)
         } else {
             const int qd = warp & 3;  // TMEM lane quadrant: rows 32*qd .. 32*qd+31
             const int row = qd * 32 + int(lane);
+            const uint32_t lq = uint32_t(qd * 32) << 16;
             mbar_wait(xdone_b, (ph_x >> tb) & 1u);
             ph_x ^= 1u << tb;
             tc_fence_after();
             if (isA) {
-                // X rows [32 qd, 32 qd + 32) = K-chunk qd of MMA2's B operand (X^T)
-                uint8_t* xh = S + qd * 2 * kChunk;
-                uint8_t* xl = xh + kChunk;
+                // Y -> (Y_hi in place, Y_lo), the A operand pair of MMA2
 #pragma unroll 1
                 for (int cc = 0; cc < 4; ++cc) {
-                    uint32_t r[32];
-                    tmem_ld_32x32b_x32(tbuf + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
+                    uint32_t r[32], lo[32];
+                    tmem_ld_32x32b_x32(tbuf + lq + uint32_t(cc * 32), r);
                     tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         float h, l;
                         split_tf32(__uint_as_float(r[j]), h, l);
-                        const uint32_t off = sw128(cc * 32 + j, int(lane));
-                        *reinterpret_cast<float*>(xh + off) = h;
-                        *reinterpret_cast<float*>(xl + off) = l;
+                        r[j] = __float_as_uint(h);
+                        lo[j] = __float_as_uint(l);
                     }
+                    tmem_st_32x32b_x32(tbuf + lq + uint32_t(cc * 32), r);
+                    tmem_st_32x32b_x32(tylo + lq + uint32_t(cc * 32), lo);
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(xready);
-                    mbar_arrive(xfree_b);
-                }
+                if (lane == 0) mbar_arrive(xready);
                 mbar_wait(adone, ph_a);
                 ph_a ^= 1;
                 tc_fence_after();
@@ -1019,7 +1023,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t r[32];
-                    tmem_ld_32x32b_x32(tbuf + (uint32_t(qd * 32) << 16) + uint32_t(JP + cc * 32), r);
+                    tmem_ld_32x32b_x32(tap + lq + uint32_t(cc * 32), r);
                     tmem_ld_wait();
                     const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
                     float* dh = p.Ah + base + gc;  // A is plain fp32 (Al stays zero)
@@ -1030,21 +1034,24 @@ __global__ void __launch_bounds__(192, 1)
                     if (i1 != i2) {
                         // mirror tile (i2, i1): column gc + j of these rows becomes row gc + j;
                         // a warp's 32 rows are consecutive (one JW block), so each store is 128 B
-                        const int64_t tb = int64_t(b) * p.D * p.D + int64_t(gc) * p.D + gr;
+                        const int64_t tb2 = int64_t(b) * p.D * p.D + int64_t(gc) * p.D + gr;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) p.Ah[tb + int64_t(j) * p.D] = __uint_as_float(r[j]);
+                        for (int j = 0; j < 32; ++j) p.Ah[tb2 + int64_t(j) * p.D] = __uint_as_float(r[j]);
                     }
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(afree);
+                if (lane == 0) {
+                    mbar_arrive(afree);
+                    mbar_arrive(xfree_b);  // MMA2 (complete: adone) was the last reader of Y
+                }
             } else {
                 const int gr = i1 * JP + row;
                 const int64_t base = int64_t(b) * p.D * p.D + int64_t(gr) * p.D;
 #pragma unroll 1
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t r[32];
-                    tmem_ld_32x32b_x32(tbuf + (uint32_t(qd * 32) << 16) + uint32_t(cc * 32), r);
+                    tmem_ld_32x32b_x32(tbuf + lq + uint32_t(cc * 32), r);
                     tmem_ld_wait();
                     const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
                     float* dh = p.Vh + base + gc;  // V is plain fp32 (Vl stays zero)
@@ -1059,7 +1066,6 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
         ++nt;
-        prev_a = isA;
     }
     // the epilogue warps waited for every MMA of their last tile: TMEM is idle
     __syncthreads();
