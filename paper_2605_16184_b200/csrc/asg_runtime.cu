@@ -1107,7 +1107,14 @@ void bucket_exchange(asg_blockset* bs, const asg_blockset::Bucket& b, ncclComm_t
 
 // (Re)builds the chunk table of the one-launch global gradient norm.
 void build_sq_table(asg_blockset* bs) {
-    constexpr int64_t kChunkElems = 1 << 16;
+    // chunks of 2^12..2^16 elements (multiples of 1024, so every chunk of a
+    // contiguous gradient keeps 16-byte loads), at least ~4 CTAs per SM when the
+    // gradients are small (one 1024^2 block: 16 chunks of 2^16 took 23 us)
+    int64_t total = 0;
+    for (const asg_param_desc& d : bs->params)
+        if (d.grad) total += d.rows * d.cols;
+    const int64_t want = (total / (4 * int64_t(bs->num_sms)) + 1023) / 1024 * 1024;
+    const int64_t kChunkElems = std::max<int64_t>(4096, std::min<int64_t>(int64_t(1) << 16, want));
     std::vector<SqChunk> t;
     for (const asg_param_desc& d : bs->params) {
         if (!d.grad) continue;
