@@ -163,13 +163,11 @@ __global__ void tj_init_kernel(const float* __restrict__ B, int n, int D, const 
         float x;
         if (i < n && j < n) x = 0.5f * (t1[dy][threadIdx.x] + t2[threadIdx.x][dy]);
         else x = (i == j) ? float(pad[b] * (1.0 + double(i - n + 1) * 1e-3)) : 0.f;
-        // A and V are stored as plain fp32 (the apply splits them in shared
-        // memory); the lo slabs stay zero, so readers of Ah + Al see A
+        // A and V are stored as plain fp32 in the Ah / Vh slabs (the apply splits
+        // them in shared memory); the Al / Vl slabs are not used by the solve
         const int64_t o = b * DD + int64_t(i) * D + j;
         Ah[o] = x;
-        Al[o] = 0.f;
         Vh[o] = (i == j) ? 1.f : 0.f;
-        Vl[o] = 0.f;
     }
 }
 
@@ -207,7 +205,7 @@ __global__ void __launch_bounds__(NT, PW == 64 ? kNarrowPairCtas : 1) tj_pair_ke
     for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) {
         const int i = e / PW, j = e % PW;
         const int64_t off = b * DD + int64_t(nat<JW>(i, p, q)) * D + nat<JW>(j, p, q);
-        S[i * (PW + 1) + j] = Ah[off] + Al[off];
+        S[i * (PW + 1) + j] = Ah[off];
         Z[i * (PW + 1) + j] = (i == j) ? 1.f : 0.f;
     }
     __syncthreads();
@@ -1026,7 +1024,7 @@ __global__ void __launch_bounds__(192, 1)
                     tmem_ld_32x32b_x32(tap + lq + uint32_t(cc * 32), r);
                     tmem_ld_wait();
                     const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
-                    float* dh = p.Ah + base + gc;  // A is plain fp32 (Al stays zero)
+                    float* dh = p.Ah + base + gc;  // A is plain fp32 (the Al slab is not used by the solve)
 #pragma unroll
                     for (int j = 0; j < 32; j += 4)
                         *reinterpret_cast<float4*>(dh + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
@@ -1054,7 +1052,7 @@ __global__ void __launch_bounds__(192, 1)
                     tmem_ld_32x32b_x32(tbuf + lq + uint32_t(cc * 32), r);
                     tmem_ld_wait();
                     const int gc = blk2[(cc * 32) / JW] * JW + (cc * 32) % JW;
-                    float* dh = p.Vh + base + gc;  // V is plain fp32 (Vl stays zero)
+                    float* dh = p.Vh + base + gc;  // V is plain fp32 (the Vl slab is not used by the solve)
 #pragma unroll
                     for (int j = 0; j < 32; j += 4)
                         *reinterpret_cast<float4*>(dh + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
@@ -1092,7 +1090,7 @@ __global__ void tj_check_kernel(const float* __restrict__ Ah, const float* __res
     if (!active[b]) return;
     const int64_t DD = int64_t(D) * D;
     for (int i = threadIdx.x; i < D; i += blockDim.x)
-        dgs[i] = fabsf(Ah[b * DD + int64_t(i) * D + i] + Al[b * DD + int64_t(i) * D + i]);
+        dgs[i] = fabsf(Ah[b * DD + int64_t(i) * D + i]);
     __syncthreads();
     const float floor_s = noise_floor(fro[b], n, tol);
     bool any = false;
@@ -1102,7 +1100,7 @@ __global__ void tj_check_kernel(const float* __restrict__ Ah, const float* __res
         // triangles differ in their last bits after independent tile products)
         for (int c = r + 1 + (threadIdx.x & 31); c < D; c += 32) {
             const int64_t o = b * DD + int64_t(r) * D + c;
-            const float x = fabsf(Ah[o] + Al[o]);
+            const float x = fabsf(Ah[o]);
             if (x == 0.f) continue;
             const float dc = dgs[c];
             any |= x > tol * fmaxf(sqrtf(dr * dc), floor_s);
@@ -1141,7 +1139,7 @@ __global__ void tj_rank_kernel(const float* __restrict__ Ah, const float* __rest
     extern __shared__ float dg[];
     const int64_t b = blockIdx.x;
     const int64_t DD = int64_t(D) * D;
-    for (int i = threadIdx.x; i < D; i += blockDim.x) dg[i] = Ah[b * DD + int64_t(i) * D + i] + Al[b * DD + int64_t(i) * D + i];
+    for (int i = threadIdx.x; i < D; i += blockDim.x) dg[i] = Ah[b * DD + int64_t(i) * D + i];
     __syncthreads();
     if (threadIdx.x == 0 && active[b]) atomicCAS(&status[b], ASG_OK, ASG_ERR_NO_CONVERGENCE);
     for (int i = threadIdx.x; i < D; i += blockDim.x) {
@@ -1178,7 +1176,7 @@ __global__ void tj_gather_kernel(const float* __restrict__ Vh, const float* __re
         float h = 0.f, l = 0.f;
         if (i < n && r < n) {
             const int64_t o = b * DD + int64_t(i) * D + src[b * D + r];
-            split_tf32(Vh[o] + Vl[o], h, l);  // V is plain fp32 (Vl = 0)
+            split_tf32(Vh[o], h, l);  // V is plain fp32
         }
         Jh[b * DD + e] = h;
         if (Jl) Jl[b * DD + e] = l;
