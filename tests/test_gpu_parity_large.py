@@ -117,6 +117,34 @@ def test_sym_eig_batched_f32_wide_pairs_match_lapack(rt, n):
     check_eigh(n, mats, vals.cpu().numpy(), vecs.cpu().numpy(), tol, tol)
 
 
+@pytest.mark.parametrize("n", [768, 1024, 2048])
+def test_sym_eig_batched_f32_warm_refresh_matches_lapack(rt, n):
+    """The matrix a warm SOAP refresh hands the eigensolver with fresh gradients
+    (pf 10, beta 0.95): B = Q^T (0.6 A1 + 0.4 A_fresh) Q, Q the eigenbasis of A1,
+    so B is diagonally dominant with 40% fresh off-diagonal mass. This exercises
+    the classical few-element pair path, skipped tiles and the symmetric apply
+    at the bench's block sizes. Same tolerances as the cold test."""
+    rng = np.random.default_rng(n)
+
+    def gram():
+        x = rng.standard_normal((n, 2 * n)) / np.sqrt(2 * n)
+        return x @ x.T + 1e-3 * np.eye(n)
+
+    a1 = gram()
+    _, q = np.linalg.eigh(a1)
+    mats = []
+    for _ in range(2):
+        b = q.T @ (0.6 * a1 + 0.4 * gram()) @ q
+        mats.append(0.5 * (b + b.T))
+    batch = len(mats)
+    A = torch.from_numpy(np.stack(mats).astype(np.float32)).cuda()
+    vals = torch.empty(batch, n, dtype=torch.float64, device="cuda")
+    vecs = torch.empty(batch, n, n, dtype=torch.float32, device="cuda")
+    rt.check(rt.lib.asg_sym_eig_batched_f32(_ptr(A), _ptr(vals), _ptr(vecs), batch, n, None))
+    tol = 2e-5 * s_n(n)
+    check_eigh(n, mats, vals.cpu().numpy(), vecs.cpu().numpy(), tol, tol, label="warm")
+
+
 def test_wide_pair_path_forced_at_small_n():
     """ASG_TJ_WIDE_N=128 forces the 128 x 128 pair solves from n = 129 (read
     once per process, so in a subprocess): same bounds as the narrow path's
